@@ -1,0 +1,381 @@
+#!/usr/bin/env python3
+"""Generate the golden vectors that pin the oracle and the GPU path.
+
+Runs the UNMODIFIED reference package (read from /root/reference/pkg/src in
+the build container only -- it does not exist on the GPU box) and writes:
+
+  wire/                 the reference's own wire fixtures, regenerated with
+                        pkg/scripts/make_golden_packets.py (the .bin files are
+                        absent from the reference mount; the regenerated
+                        manifest.json is byte-identical to the shipped one)
+  codec_cases.npz/json  encode_delta / encode_snapshot inputs and payloads
+  raster_cases.npz/json prepare_splats / render / backward inputs and outputs
+  step_cases.npz/json   optim.step trajectories (model + OptimizerState)
+  dyn_cases.npz/json    update_light_visibility / ObjectRegistry transforms
+
+Usage:  python tests/golden/make_golden.py [--ref /root/reference/pkg]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import pathlib
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default="/root/reference/pkg")
+    args = ap.parse_args()
+    ref = pathlib.Path(args.ref)
+    sys.path.insert(0, str(ref / "src"))
+    import splatstream  # noqa: F401  (the reference)
+
+    wire = HERE / "wire"
+    if wire.exists():
+        shutil.rmtree(wire)
+    subprocess.run([sys.executable, str(ref / "scripts" / "make_golden_packets.py"), str(wire)], check=True)
+    shipped = (ref / "tests" / "golden" / "manifest.json").read_bytes()
+    assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
+
+    codec_cases()
+    raster_cases()
+    step_cases()
+    dyn_cases()
+    print("golden vectors written to", HERE)
+
+
+class Store:
+    def __init__(self):
+        self.arrays = {}
+        self.cases = []
+
+    def add(self, meta: dict, **arrays):
+        i = len(self.cases)
+        meta = dict(meta, id=i, arrays=sorted(arrays))
+        for k, v in arrays.items():
+            self.arrays[f"c{i}_{k}"] = np.asarray(v)
+        self.cases.append(meta)
+
+    def save(self, stem):
+        np.savez_compressed(HERE / f"{stem}.npz", **self.arrays)
+        (HERE / f"{stem}.json").write_text(json.dumps(self.cases, indent=1) + "\n")
+
+
+def b2a(b: bytes):
+    return np.frombuffer(b, np.uint8).copy()
+
+
+def random_model(rng, n, degree, frozen=0, spread=3.0):
+    from splatstream.geometry import quat_normalize
+    from splatstream.model import GaussianModel
+    B = (degree + 1) ** 2
+    sh = np.concatenate([rng.uniform(-0.5, 0.5, (n, 3, 1)), rng.uniform(-0.1, 0.1, (n, 3, B - 1))], axis=2)
+    return GaussianModel(
+        means=rng.uniform(-spread, spread, (n, 3)).astype(np.float32),
+        log_scales=rng.uniform(-3.5, -1.5, (n, 3)).astype(np.float32),
+        quaternions=quat_normalize(rng.normal(size=(n, 4))).astype(np.float32),
+        logit_opacities=rng.uniform(-2, 3, n).astype(np.float32),
+        sh_coeffs=sh.astype(np.float32),
+        light_visibility=(rng.random(n) > 0.4).astype(np.float32),
+        object_ids=rng.integers(0, 4, n).astype(np.int32),
+        active_count=n - frozen, sh_degree=degree)
+
+
+def model_arrays(m):
+    return dict(means=m.means, log_scales=m.log_scales, quaternions=m.quaternions,
+                logit_opacities=m.logit_opacities, sh_coeffs=m.sh_coeffs,
+                light_visibility=m.light_visibility, object_ids=m.object_ids)
+
+
+# ------------------------------------------------------------------ codec
+def codec_cases():
+    from splatstream.protocol import (PROFILE_DEFAULT, PROFILE_LOSSLESS, AttributeId,
+                                      QuantizationProfile, encode_delta, encode_snapshot, decode_snapshot)
+    from splatstream.model import GaussianModel
+    st = Store()
+    rng = np.random.default_rng(1234)
+
+    def delta(name, attr, cur, base=None, gate=None):
+        arrays = dict(cur=cur)
+        for comp in (0, 1):
+            payload, nb = encode_delta(attr, cur, base, gating_threshold=gate, compression_id=comp)
+            arrays[f"payload{comp}"] = b2a(payload)
+        if base is not None:
+            arrays["base"] = base
+            arrays["new_base"] = nb
+        st.add(dict(kind="delta", name=name, attr=int(attr), gate=gate,
+                    dtype=str(np.asarray(cur).dtype)), **arrays)
+
+    A = AttributeId
+    for n in (1, 7, 40, 333, 2000):
+        base = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+        # dense: every row moves
+        cur = (base + rng.uniform(-0.02, 0.02, base.shape)).astype(np.float32)
+        delta(f"means_dense_{n}", A.MEANS, cur, base)
+        delta(f"ls_dense_{n}", A.LOG_SCALES, (cur * 3 - 4).astype(np.float32), (base * 3 - 4).astype(np.float32))
+        # sparse: a few rows move, some just under/over the gate
+        cur = base.copy()
+        mv = rng.random(n) < 0.15
+        cur[mv] += rng.normal(0, 0.01, (int(mv.sum()), 3)).astype(np.float32)
+        if n > 5:
+            cur[3, 1] = np.float32(np.float64(base[3, 1]) + 1e-3)
+            cur[4, 2] = np.float32(np.float64(base[4, 2]) + 0.99e-3)
+        delta(f"means_sparse_{n}", A.MEANS, cur, base)
+        delta(f"ls_sparse_{n}", A.LOG_SCALES, cur, base, gate=5e-4)
+        delta(f"means_nochange_{n}", A.MEANS, base.copy(), base)
+        delta(f"means_gate0_{n}", A.MEANS, cur, base, gate=0.0)
+        # absolute attributes
+        delta(f"quat_{n}", A.QUATERNIONS, rng.normal(0, 0.6, (n, 4)).astype(np.float32))
+        delta(f"opac_{n}", A.LOGIT_OPACITIES, rng.uniform(-10, 10, n).astype(np.float32))
+        delta(f"dc_{n}", A.SH_DC, rng.uniform(-5, 5, (n, 3)).astype(np.float32))
+        delta(f"rest1_{n}", A.SH_REST, rng.uniform(-1.2, 1.2, (n, 3, 3)).astype(np.float32))
+        delta(f"rest3_{n}", A.SH_REST, rng.uniform(-1.2, 1.2, (n, 3, 15)).astype(np.float32))
+        delta(f"vis_{n}", A.LIGHT_VISIBILITY, rng.random(n).astype(np.float32))
+    # large-survivor-gap varints, huge residuals, float64 input
+    n = 20000
+    base = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    cur = base.copy()
+    cur[[0, 5, 200, 19000, 19999]] += np.float32(0.5)
+    delta("means_sparse_gaps", A.MEANS, cur, base)
+    cur = base.copy()
+    cur[::2] += np.float32(40.0)
+    delta("means_dense_huge", A.MEANS, cur, base)
+    delta("means_f64_input", A.MEANS, (base[:50] + 0.01).astype(np.float64), base[:50].astype(np.float64))
+    delta("opac_f64_input", A.LOGIT_OPACITIES, rng.uniform(-9, 9, 77))
+    delta("means_empty", A.MEANS, np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32))
+    delta("opac_empty", A.LOGIT_OPACITIES, np.zeros(0, np.float32))
+
+    # snapshots
+    for (n, deg, frozen) in ((1, 0, 0), (8, 1, 2), (64, 2, 0), (513, 3, 100), (3000, 3, 0)):
+        m = random_model(rng, n, deg, frozen)
+        if n == 64:
+            m.means[:, 1] = np.float32(0.25)  # degenerate AABB axis
+        arrays = {}
+        for prof in (PROFILE_DEFAULT, PROFILE_LOSSLESS,
+                     QuantizationProfile(0, 0), QuantizationProfile(1, 0)):
+            payload = encode_snapshot(m, prof)
+            arrays[f"payload_p{prof.profile_id}c{prof.compression_id}"] = b2a(payload)
+            if prof.profile_id == 0:
+                dec, _ = decode_snapshot(payload)
+        st.add(dict(kind="snapshot", name=f"snap_{n}_{deg}", n=n, degree=deg, active=int(m.active_count)),
+               dec_means=dec.means, dec_log_scales=dec.log_scales, **arrays, **model_arrays(m))
+    m = GaussianModel.empty(2)
+    payload = encode_snapshot(m, QuantizationProfile(0, 0))
+    st.add(dict(kind="snapshot", name="snap_empty", n=0, degree=2, active=0),
+           payload_p0c0=b2a(payload), payload_p1c0=b2a(encode_snapshot(m, QuantizationProfile(1, 0))),
+           payload_p0c1=b2a(encode_snapshot(m)), payload_p1c1=b2a(encode_snapshot(m, PROFILE_LOSSLESS)),
+           **model_arrays(m))
+    st.save("codec_cases")
+
+
+# ------------------------------------------------------------------ raster
+def _pose_arrays(pose):
+    return np.concatenate([pose.position, pose.quaternion])
+
+
+def raster_cases():
+    from splatstream.geometry import CameraIntrinsics, Pose, look_at, quat_normalize
+    from splatstream.model import GaussianModel
+    from splatstream.optim import ReferenceView, backward
+    from splatstream.render import LightState, flat_ambient_sh, prepare_splats, render, splat_window
+    st = Store()
+
+    def light_for(rng, mode):
+        direction = np.array([0.3, -1.0, 0.2]) + rng.normal(0, 0.2, 3)
+        intensity = rng.uniform(0.4, 0.9, 3)
+        if mode == "none":
+            amb = None
+        elif mode == "flat":
+            amb = flat_ambient_sh(rng.uniform(0.25, 0.5, 3))
+        else:
+            amb = np.concatenate([flat_ambient_sh(rng.uniform(0.25, 0.5, 3)), rng.uniform(-0.1, 0.1, (3, 3))], 1)
+        return LightState(direction=direction, intensity=intensity, ambient_sh=amb)
+
+    def scene_model(rng, n, degree, W, H, fov, frozen=0, zr=(2.5, 6.0), sig=(1.2, 0.5)):
+        z = rng.uniform(*zr, n)
+        f = (H / 2) / np.tan(fov / 2)
+        hx = z * (W / 2) / f
+        hy = z * (H / 2) / f
+        means = np.stack([rng.uniform(-1, 1, n) * hx * 1.1, rng.uniform(-1, 1, n) * hy * 1.1, z], -1)
+        spx = np.exp(rng.normal(np.log(sig[0]), sig[1], n))
+        ls = np.log(spx * z / f)[:, None] + rng.normal(0, 0.3, (n, 3))
+        B = (degree + 1) ** 2
+        sh = np.concatenate([rng.uniform(-0.6, 0.6, (n, 3, 1)), rng.uniform(-0.08, 0.08, (n, 3, B - 1))], 2)
+        return GaussianModel(
+            means=means.astype(np.float32), log_scales=ls.astype(np.float32),
+            quaternions=quat_normalize(rng.normal(size=(n, 4))).astype(np.float32),
+            logit_opacities=rng.uniform(-1, 2.5, n).astype(np.float32), sh_coeffs=sh.astype(np.float32),
+            light_visibility=(rng.random(n) > 0.3).astype(np.float32),
+            object_ids=np.zeros(n, np.int32), active_count=n - frozen, sh_degree=degree)
+
+    def add(name, model, pose, intr, light, bg, gt_model=None, subset=None, cutoff=True, rng=None):
+        prep = prepare_splats(model, pose, intr, light, subset, cutoff)
+        img, T = render(model, pose, intr, light, subset, bg, return_transmittance=True, extent_cutoff=cutoff)
+        if gt_model is None:
+            gt = np.clip(img + rng.uniform(-0.2, 0.2, img.shape), 0, 1)
+        else:
+            gt = render(gt_model, pose, intr, light, None, bg, extent_cutoff=cutoff)
+        view = ReferenceView(pose=pose, intrinsics=intr, image=gt.astype(np.float32), light_state=light,
+                             background=np.asarray(bg, np.float64))
+        L, g, img2 = backward(model, view, subset, cutoff)
+        assert np.array_equal(img, img2)
+        M = prep.rows.size
+        wins = np.array([splat_window(prep.mu2d[i], prep.radius[i], intr.width, intr.height) for i in range(M)],
+                        np.int64).reshape(M, 4)
+        meta = dict(kind="raster", name=name, W=intr.width, H=intr.height, fov=float(intr.fov_y),
+                    near=float(intr.near), degree=int(model.sh_degree), active=int(model.active_count),
+                    cutoff=bool(cutoff), ambient=light.ambient_sh is not None, loss=L,
+                    subset=subset is not None)
+        arrays = dict(pose=_pose_arrays(pose), light_dir=light.direction, light_int=light.intensity,
+                      bg=np.asarray(bg, np.float64), gt=view.image, image=img, T=T,
+                      rows=prep.rows, order=prep.order, depth=prep.depth, mu2d=prep.mu2d,
+                      Sigma2d=prep.Sigma2d, radius=prep.radius, windows=wins, color=prep.color,
+                      color_pre=prep.color_pre, opacity=prep.opacity, s=prep.shade_inter["s"],
+                      Sigma3d=prep.Sigma3d,
+                      g_means=g.means, g_log_scales=g.log_scales, g_quaternions=g.quaternions,
+                      g_logit_opacities=g.logit_opacities, g_sh_coeffs=g.sh_coeffs,
+                      **model_arrays(model))
+        if light.ambient_sh is not None:
+            arrays["ambient"] = light.ambient_sh
+        if subset is not None:
+            arrays["subset"] = np.asarray(subset, np.int64)
+        st.add(meta, **arrays)
+
+    rng = np.random.default_rng(99)
+    case = 0
+    for degree in (0, 1, 2, 3):
+        for mode in ("none", "flat", "sh1"):
+            W, H, fov = (32, 24, 1.1) if case % 2 else (40, 33, 0.9)
+            m = scene_model(rng, 48, degree, W, H, fov)
+            tgt = m.copy()
+            tgt.sh_coeffs = (tgt.sh_coeffs + rng.uniform(-0.3, 0.3, tgt.sh_coeffs.shape)).astype(np.float32)
+            eye = rng.normal(0, 0.15, 3)
+            pose = look_at(eye, [0.05, -0.03, 4.0])
+            intr = CameraIntrinsics(width=W, height=H, fov_y=fov, near=0.05, far=100.0)
+            add(f"deg{degree}_{mode}", m, pose, intr, light_for(rng, mode), (0.05, 0.05, 0.08), gt_model=tgt)
+            case += 1
+    # finite-difference style configuration: 16x16, cutoff disabled
+    for seed in range(3):
+        r2 = np.random.default_rng(500 + seed)
+        m = scene_model(r2, 5, 1, 16, 16, np.pi / 2, zr=(2.5, 5.0), sig=(2.0, 0.3))
+        add(f"nocutoff_{seed}", m, Pose(np.zeros(3), np.array([1.0, 0, 0, 0])),
+            CameraIntrinsics(width=16, height=16, fov_y=np.pi / 2, near=0.1, far=100.0),
+            light_for(r2, ("flat", "none", "sh1")[seed]), (0.0, 0.0, 0.0), cutoff=False, rng=r2)
+    # frozen tail + subset + a row behind the camera
+    m = scene_model(rng, 60, 2, 48, 32, 1.0, frozen=17)
+    m.means[5] = [0.0, 0.0, -3.0]
+    pose = look_at([0.1, 0.0, 0.0], [0.0, 0.0, 4.0])
+    intr = CameraIntrinsics(width=48, height=32, fov_y=1.0, near=0.05, far=100.0)
+    add("frozen_tail", m, pose, intr, light_for(rng, "flat"), (0.1, 0.2, 0.3), rng=rng)
+    subset = np.sort(rng.choice(60, 35, replace=False))
+    add("subset", m, pose, intr, light_for(rng, "flat"), (0.1, 0.2, 0.3), subset=subset, rng=rng)
+    # capped alpha: one huge near-opaque splat plus small ones in front
+    m = scene_model(rng, 6, 0, 16, 16, np.pi / 2)
+    m.means[0] = [0.0, 0.0, 8.0]
+    m.log_scales[0] = 6.0
+    m.logit_opacities[0] = 14.0
+    add("capped", m, Pose(np.zeros(3), np.array([1.0, 0, 0, 0])),
+        CameraIntrinsics(width=16, height=16, fov_y=np.pi / 2, near=0.1, far=100.0),
+        light_for(rng, "flat"), (0.0, 0.0, 0.0), rng=rng)
+    # exact depth ties, broken by row
+    m = scene_model(rng, 12, 1, 24, 24, 1.2)
+    m.means[:, 2] = np.float32(4.0)
+    add("depth_ties", m, Pose(np.zeros(3), np.array([1.0, 0, 0, 0])),
+        CameraIntrinsics(width=24, height=24, fov_y=1.2, near=0.05, far=100.0),
+        light_for(rng, "none"), (0.0, 0.0, 0.0), rng=rng)
+    # dense saturated medium scene (exercises the T cutoff and many tiles)
+    m = scene_model(rng, 2500, 3, 96, 64, 1.2, sig=(2.5, 0.5))
+    tgt = m.copy()
+    tgt.sh_coeffs = (tgt.sh_coeffs + rng.uniform(-0.3, 0.3, tgt.sh_coeffs.shape)).astype(np.float32)
+    tgt.means = (tgt.means + rng.normal(0, 0.01, tgt.means.shape)).astype(np.float32)
+    add("medium", m, look_at([0.2, 0.1, -0.3], [0.0, 0.0, 4.5]),
+        CameraIntrinsics(width=96, height=64, fov_y=1.2, near=0.05, far=100.0),
+        light_for(rng, "flat"), (0.05, 0.05, 0.08), gt_model=tgt)
+    # empty model
+    m = GaussianModel.empty(1)
+    add("empty", m, Pose(np.zeros(3), np.array([1.0, 0, 0, 0])),
+        CameraIntrinsics(width=8, height=8, fov_y=1.0), light_for(rng, "flat"), (0.2, 0.4, 0.6), rng=rng)
+    st.save("raster_cases")
+
+
+# ------------------------------------------------------------------ step
+def step_cases():
+    from splatstream.geometry import CameraIntrinsics, look_at
+    from splatstream.optim import OptimizerState, ReferenceView, step
+    from splatstream.render import LightState, flat_ambient_sh, render
+    st = Store()
+    rng = np.random.default_rng(7)
+    for degree, frozen in ((1, 0), (3, 9)):
+        m = random_model(rng, 40, degree, frozen, spread=1.0)
+        m.means[:, 2] += np.float32(4.0)
+        m.log_scales[:] = rng.uniform(-2.8, -1.8, m.log_scales.shape).astype(np.float32)
+        light = LightState([0.3, -1.0, 0.2], [0.6, 0.6, 0.6], flat_ambient_sh([0.35, 0.35, 0.35]))
+        intr = CameraIntrinsics(width=32, height=32, fov_y=1.2)
+        poses = [look_at([0.3 * np.cos(a), 0.3 * np.sin(a), 0.0], [0, 0, 4.5]) for a in (0.0, 2.1, 4.2)]
+        tgt = m.copy()
+        tgt.sh_coeffs = (tgt.sh_coeffs + rng.uniform(-0.3, 0.3, tgt.sh_coeffs.shape)).astype(np.float32)
+        bg = np.array([0.05, 0.05, 0.08])
+        views = [ReferenceView(p, intr, render(tgt, p, intr, light, background=bg).astype(np.float32), light, bg)
+                 for p in poses]
+        init = model_arrays(m)
+        init = {k: v.copy() for k, v in init.items()}
+        state = OptimizerState(m, scene_extent=2.5)
+        losses, snaps = [], {}
+        for it in range(3):
+            losses.append(step(m, state, views))
+            for k in ("means", "log_scales", "quaternions", "logit_opacities", "sh_coeffs"):
+                snaps[f"after{it}_{k}"] = m.attribute(k).copy()
+        arrays = {f"init_{k}": v for k, v in init.items()}
+        arrays.update(snaps)
+        arrays.update({f"m_{k}": v for k, v in state.m.items()})
+        arrays.update({f"v_{k}": v for k, v in state.v.items()})
+        arrays.update(age=state.age, grad_ema=state.grad_ema, losses=np.array(losses),
+                      poses=np.stack([_pose_arrays(p) for p in poses]),
+                      gts=np.stack([v.image for v in views]), bg=bg,
+                      light_dir=light.direction, light_int=light.intensity, ambient=light.ambient_sh)
+        st.add(dict(kind="step", degree=degree, active=int(m.active_count), n=40, W=32, H=32, fov=1.2,
+                    near=0.05, scene_extent=2.5, steps=3), **arrays)
+    st.save("step_cases")
+
+
+# ------------------------------------------------------------------ dynamics
+def dyn_cases():
+    from splatstream.geometry import OrthoCamera, look_at, quat_from_axis_angle
+    from splatstream.model import ObjectRegistry
+    from splatstream.render import update_light_visibility
+    st = Store()
+    rng = np.random.default_rng(3)
+    for n in (5, 1000):
+        m = random_model(rng, n, 1)
+        pose = look_at([0.5, 6.0, 0.3], [0.0, 0.0, 0.0])
+        cam = OrthoCamera(pose=pose, half_width=3.5, half_height=3.0, width=64, height=48, far=20.0)
+        depth = rng.uniform(4.0, 9.0, (48, 64))
+        mm = m.copy()
+        update_light_visibility(mm, depth, cam, bias=0.02)
+        st.add(dict(kind="lightvis", n=n, half_width=3.5, half_height=3.0, width=64, height=48, bias=0.02),
+               means=m.means, depth=depth, cam_pos=pose.position, cam_quat=pose.quaternion,
+               vis=mm.light_visibility)
+        reg = ObjectRegistry()
+        for oid in (1, 2, 3):
+            reg.set_transform(oid, quat_from_axis_angle(rng.normal(size=3), rng.uniform(0, 3)), rng.normal(size=3))
+        reg.refresh_locals(m)
+        q = quat_from_axis_angle(rng.normal(size=3), 0.4)
+        t = rng.normal(size=3)
+        mm = m.copy()
+        rows = reg.apply_transform(mm, 2, q, t)
+        st.add(dict(kind="transform", n=n, oid=2), means=m.means, quats=m.quaternions, object_ids=m.object_ids,
+               local_means=reg.local_means, local_rots=reg.local_rotations, q=q, t=t, rows=rows,
+               out_means=mm.means, out_quats=mm.quaternions)
+    st.save("dyn_cases")
+
+
+if __name__ == "__main__":
+    main()
