@@ -1,0 +1,234 @@
+/*
+ * splatstream_b200.h -- C ABI of the B200 hot path of splatstream
+ * (arXiv 2604.02851, reference package /root/reference/pkg).
+ *
+ * The reference has no FFI: its boundary is the Python API that
+ * pkg/src/splatstream/server.py and client.py call.  These entry points are
+ * what a ctypes/cffi binding of that API binds to; every function names the
+ * reference interface it replaces.  Plain C types only: device pointers,
+ * sizes, and POD parameter blocks.  No torch types cross this boundary.
+ *
+ * Ownership: the caller owns every device buffer passed in; the library owns
+ * only the opaque ss_ctx (stream binding + a grow-only scratch arena).
+ * Threading: one ss_ctx per host thread / stream; no global state.
+ * Errors: every function returns SS_OK (0) or a negative code; the message
+ * is in ss_last_error(ctx).  SS_ERR_INVALID maps to Python ValueError,
+ * SS_ERR_PROTOCOL to splatstream.protocol.ProtocolError, SS_ERR_CUDA to
+ * RuntimeError (ref optim.py:46-47, optim.py:357-361, protocol/delta.py:90-94).
+ */
+#ifndef SPLATSTREAM_B200_H
+#define SPLATSTREAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_OK 0
+#define SS_ERR_INVALID (-1)
+#define SS_ERR_PROTOCOL (-2)
+#define SS_ERR_CUDA (-3)
+#define SS_ERR_CAPACITY (-4)
+
+#define SS_ABI_VERSION 1
+
+typedef struct ss_ctx ss_ctx;
+
+/* Columnar Gaussian store on the device: the layout of ref model.py:233-245
+ * (GaussianModel).  Rows [0, active_count) are trainable. */
+typedef struct {
+    float* means;            /* (count, 3)            */
+    float* log_scales;       /* (count, 3)            */
+    float* quaternions;      /* (count, 4)  w x y z   */
+    float* logit_opacities;  /* (count,)              */
+    float* sh_coeffs;        /* (count, 3, B), B = (sh_degree+1)^2, [:, :, 0] = DC */
+    float* light_visibility; /* (count,)  in {0, 1}   */
+    int32_t* object_ids;     /* (count,)              */
+    int32_t count;
+    int32_t active_count;
+    int32_t sh_degree;       /* 0..3 */
+} ss_model;
+
+/* Pinhole camera: ref geometry.py:111-181 (CameraIntrinsics, Pose). */
+typedef struct {
+    double position[3];
+    double rot_cw[9];        /* camera->world rotation, row-major (Pose.rotation()) */
+    double fx, fy, cx, cy;
+    double near_plane;
+    int32_t width, height;
+} ss_camera;
+
+/* ref render.py:34-48 (LightState). */
+typedef struct {
+    double direction[3];     /* unit, from the light into the scene */
+    double intensity[3];
+    int32_t ambient_bands;   /* 0 = no ambient SH */
+    int32_t _pad;
+    double ambient[3 * 16];  /* (3, ambient_bands) row-major */
+} ss_light;
+
+/* Per-call render options: ref render.py:339-341 arguments. */
+typedef struct {
+    double background[3];
+    const int64_t* subset;   /* device, ascending rows, or NULL = all rows */
+    int32_t subset_count;
+    int32_t extent_cutoff;   /* 1 = 3-sigma windows, 0 = every splat covers the image */
+    int32_t precision;       /* 0 = fp32 blend (throughput); 1 = fp64 blend (verbatim parity) */
+    int32_t deterministic;   /* backward: 1 = fixed-order per-(tile,splat) partials, 0 = atomics */
+} ss_render_opts;
+
+/* Host-readable summary of the last render/backward call. */
+typedef struct {
+    int64_t visible;         /* splats passing the near test */
+    int64_t pairs;           /* (tile, splat) overlaps emitted */
+    int64_t tiles;
+} ss_render_stats;
+
+/* Optimizer hyper-parameters: ref optim.py:271-293 (LearningRates, OptimizerState). */
+typedef struct {
+    double lr_means;         /* already multiplied by scene_extent (optim.py:345-347) */
+    double lr_log_scales, lr_quaternions, lr_logit_opacities, lr_sh_dc, lr_sh_rest;
+    double beta1, beta2, eps, ema_beta;
+} ss_adam_hparams;
+
+/* Device optimizer state, flat in the gradient layout (see ss_grad_layout). */
+typedef struct {
+    double* m;               /* a * (11 + 3B) */
+    double* v;               /* a * (11 + 3B) */
+    double* grad_ema;        /* (a,) */
+    int64_t* age;            /* (a,) */
+    int32_t step_count;      /* t before this step; the call uses t+1 */
+} ss_adam_state;
+
+/* ---- context ------------------------------------------------------------ */
+int ss_ctx_create(int device, ss_ctx** out);
+void ss_ctx_destroy(ss_ctx* ctx);
+const char* ss_last_error(const ss_ctx* ctx);
+int ss_set_stream(ss_ctx* ctx, void* cuda_stream);   /* cudaStream_t */
+int ss_abi_version(void);
+/* Flat gradient buffer layout for `a` active rows at SH degree d:
+ * [means a*3 | log_scales a*3 | quaternions a*4 | logit_opacities a | sh_coeffs a*3*B]
+ * (the Gradients dataclass of ref optim.py:50-77, flattened). Returns floats. */
+int64_t ss_grad_layout(int64_t active_rows, int32_t sh_degree, int64_t offsets_out[5]);
+
+/* ---- measurement --------------------------------------------------------- */
+/* Per-kernel-class device time, measured with CUDA events on the ctx stream
+ * around each launch group.  Classes: 0 preprocess, 1 depth sort, 2 binning
+ * (count/scan/emit/ranges), 3 tile sort, 4 forward blend, 5 backward blend,
+ * 6 chain rule, 7 Adam, 8 encoders.  While enabled, the forward blend also
+ * counts T-gated (pixel, splat) evaluations (counters[0]); counters[1] is the
+ * number of kernels this context launched. */
+#define SS_KC_COUNT 9
+int ss_set_timing(ss_ctx* ctx, int enable);
+/* Synchronises; returns accumulated ms and launch-group counts per class
+ * and the counters, then (reset != 0) clears them. */
+int ss_get_timing(ss_ctx* ctx, double ms_out[SS_KC_COUNT], int64_t groups_out[SS_KC_COUNT],
+                  uint64_t counters_out[4], int reset);
+/* Measured FP32 FMA throughput of this device in TFLOP/s (roofline denominator). */
+int ss_measure_fp32_peak(ss_ctx* ctx, double* tflops_out);
+
+/* ---- renderer (ref render.py:226-347) ------------------------------------ */
+/* render(): ref render.py:339.  image_out (H,W,3) and T_out (H,W) are float
+ * for precision 0 and double for precision 1; T_out may be NULL. */
+int ss_render(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, const ss_light* light,
+              const ss_render_opts* opts, void* image_out, void* T_out, ss_render_stats* stats_out);
+
+/* prepare_splats(): ref render.py:226 -- host-inspectable per-splat view.
+ * All outputs are device arrays sized by `capacity` rows (>= visible), in
+ * model-row order; `order_out` holds the composite order (ref render.py:283).
+ * Any output pointer may be NULL. */
+typedef struct {
+    int64_t* rows;           /* (M,) model row index           */
+    double* depth;           /* (M,) camera-space z            */
+    double* mu2d;            /* (M,2)                          */
+    double* sigma2d;         /* (M,3) = [s00, s01, s11]        */
+    double* radius;          /* (M,) inf when cutoff disabled  */
+    int32_t* window;         /* (M,4) = [x0, x1, y0, y1)       */
+    double* opacity;         /* (M,)                           */
+    double* color;           /* (M,3) clamped                  */
+    double* color_pre;       /* (M,3)                          */
+    double* shade_s;         /* (M,) signed cosine             */
+    int64_t* order;          /* (M,) composite order           */
+    int64_t capacity;
+} ss_prepared;
+int ss_prepare_splats(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, const ss_light* light,
+                      const ss_render_opts* opts, ss_prepared* out, int64_t* visible_out);
+
+/* Tile-binning products for parity tests (sort keys / tile ranges,
+ * SURVEY §8c): depth-ordered rows, per-tile [start, end) and the depth rank
+ * of every sorted (tile, splat) pair. */
+int ss_debug_bins(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, const ss_render_opts* opts,
+                  int64_t* order_rows_out, int64_t rows_cap, int64_t* tile_ranges_out, int64_t tiles_cap,
+                  int64_t* pair_rank_out, int64_t pairs_cap, ss_render_stats* stats_out);
+
+/* backward(): ref optim.py:113.  Accumulates (+=) this view's gradients of
+ * the L1 loss over active rows into grad_accum (flat layout above, float32)
+ * and the loss into *loss_accum (device double).  gt is (H,W,3) float32.
+ * image_out (may be NULL) receives the forward image as in ss_render. */
+int ss_backward(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, const ss_light* light,
+                const ss_render_opts* opts, const float* gt, float* grad_accum, double* loss_accum,
+                void* image_out, ss_render_stats* stats_out);
+
+/* The Adam part of step(): ref optim.py:374-406.  grad_sum holds the SUM of
+ * per-view gradients; it is scaled by 1/n_views here.  Updates model rows
+ * [0, active) in place, renormalises quaternions, advances EMA and age. */
+int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* state, const float* grad_sum,
+                 int32_t n_views, const ss_adam_hparams* hp);
+
+/* ---- encoders (ref protocol/) -------------------------------------------- */
+/* encode_delta(): ref protocol/delta.py:72 with compression_id 0 (raw).
+ * cur/base are (rows, dims) of float32 (in_dtype 0) or float64 (1); base is
+ * required for MEANS/LOG_SCALES and new_base_out (float32) receives the
+ * advanced baseline.  The payload is written to out (device) and its length
+ * to *out_len (device uint64) -- no host synchronisation.  Use
+ * ss_delta_bound() for the capacity. */
+int ss_encode_delta(ss_ctx* ctx, int32_t attribute_id, const void* cur, int32_t in_dtype,
+                    const void* base, float* new_base_out, int64_t rows, int32_t dims,
+                    double gating_threshold, uint8_t* out, uint64_t out_cap, uint64_t* out_len);
+uint64_t ss_delta_bound(int32_t attribute_id, int64_t rows, int32_t dims);
+
+/* encode_snapshot(): ref protocol/snapshot.py:47 with compression_id 0.
+ * profile 0 = quantized, 1 = lossless.  base_means_out / base_log_scales_out
+ * (float32, may be NULL) receive the decoded means / log scales -- the
+ * server's baseline reset of ref server.py:481-484 without a re-decode. */
+int ss_encode_snapshot(ss_ctx* ctx, const ss_model* model, int32_t profile_id, uint8_t* out,
+                       uint64_t out_cap, uint64_t* out_len, float* base_means_out,
+                       float* base_log_scales_out);
+uint64_t ss_snapshot_bound(int64_t count, int32_t sh_degree, int32_t profile_id);
+
+/* encode_light_visibility(): ref protocol/packets.py:73-76 ('<I' count + 1-bit pack). */
+int ss_encode_light_visibility(ss_ctx* ctx, const float* vis, int64_t n, uint8_t* out, uint64_t out_cap,
+                               uint64_t* out_len);
+
+/* The compression stage (compression_id 1): host zlib level 6, byte-identical
+ * to ref protocol/profiles.py:41-46.  Host buffers. */
+int ss_host_zlib_compress(const uint8_t* src, uint64_t n, uint8_t* dst, uint64_t cap, uint64_t* out_len);
+uint64_t ss_host_zlib_bound(uint64_t n);
+
+/* ---- dynamics ------------------------------------------------------------ */
+/* update_light_visibility(): ref render.py:350-368 with the orthographic
+ * projection of ref geometry.py:267-271.  Writes model->light_visibility. */
+typedef struct {
+    double position[3];
+    double rot_cw[9];
+    double half_width, half_height;
+    int32_t width, height;
+} ss_ortho_camera;
+int ss_update_light_visibility(ss_ctx* ctx, ss_model* model, const double* depth_map,
+                               const ss_ortho_camera* cam, double bias);
+
+/* ObjectRegistry.apply_transform(): ref model.py:557-572.  Rewrites the rows
+ * with object_ids == object_id from their local poses (device f64 arrays
+ * (count,3) / (count,4)); q (wxyz, normalised by the call) and t are host. */
+int ss_apply_object_transform(ss_ctx* ctx, ss_model* model, int32_t object_id, const double* local_means,
+                              const double* local_rots, const double q[4], const double t[3]);
+/* ObjectRegistry.refresh_locals(): ref model.py:539-555, for rows of one object. */
+int ss_refresh_object_locals(ss_ctx* ctx, const ss_model* model, int32_t object_id, int32_t active_only,
+                             double* local_means, double* local_rots, const double q[4], const double t[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLATSTREAM_B200_H */

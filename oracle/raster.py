@@ -57,12 +57,18 @@ def det_exp(x):
 
 
 # ---------------------------------------------------------------- geometry
-def quat_rotmat(q):
-    """(..., 4) wxyz -> (..., 3, 3), normalising first (ref geometry.py:53-60)."""
+def quat_rotmat(q, norm_like_numpy=False):
+    """(..., 4) wxyz -> (..., 3, 3), normalising first (ref geometry.py:53-60).
+    Gaussians: explicit ((w^2+x^2)+y^2)+z^2 norm (mirrored by the kernel);
+    cameras (norm_like_numpy): np.linalg.norm as the host code computes it."""
     q = np.asarray(q, np.float64)
-    w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
-    n = np.sqrt(((w * w + x * x) + y * y) + z * z)
-    w, x, y, z = w / n, x / n, y / n, z / n
+    if norm_like_numpy:
+        q = q / np.linalg.norm(q, axis=-1, keepdims=True)
+        w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
+    else:
+        w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
+        n = np.sqrt(((w * w + x * x) + y * y) + z * z)
+        w, x, y, z = w / n, x / n, y / n, z / n
     R = np.empty(q.shape[:-1] + (3, 3))
     R[..., 0, 0] = 1.0 - 2.0 * (y * y + z * z)
     R[..., 0, 1] = 2.0 * (x * y - w * z)
@@ -100,7 +106,7 @@ def drot_dquat(q):
 
 def camera(pose, intr):
     """Flatten a pose/intrinsics pair into the numbers the kernels use."""
-    R = quat_rotmat(np.asarray(pose.quaternion, np.float64))
+    R = quat_rotmat(np.asarray(pose.quaternion, np.float64), norm_like_numpy=True)
     fy = (intr.height / 2.0) / np.tan(intr.fov_y / 2.0)
     return dict(pos=np.asarray(pose.position, np.float64), R=R, W=intr.width, H=intr.height,
                 fx=fy, fy=fy, cx=intr.width / 2.0, cy=intr.height / 2.0, near=intr.near)

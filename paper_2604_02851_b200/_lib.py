@@ -1,0 +1,208 @@
+"""ctypes binding of include/splatstream_b200.h (the C ABI).
+
+The product has exactly one compute path: libsplat_b200.so on a CUDA device.
+If the library is missing or no GPU is present, `lib()` raises -- there is no
+CPU fallback.  Device buffers are torch CUDA tensors; only their data
+pointers and sizes cross the boundary.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import pathlib
+import threading
+
+import numpy as np
+
+from .errors import ProtocolError
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libsplat_b200.so"
+
+SS_OK, SS_ERR_INVALID, SS_ERR_PROTOCOL, SS_ERR_CUDA, SS_ERR_CAPACITY = 0, -1, -2, -3, -4
+
+vp = C.c_void_p
+i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+
+
+class SSModel(C.Structure):
+    _fields_ = [("means", vp), ("log_scales", vp), ("quaternions", vp), ("logit_opacities", vp),
+                ("sh_coeffs", vp), ("light_visibility", vp), ("object_ids", vp),
+                ("count", i32), ("active_count", i32), ("sh_degree", i32)]
+
+
+class SSCamera(C.Structure):
+    _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("fx", f64), ("fy", f64), ("cx", f64),
+                ("cy", f64), ("near_plane", f64), ("width", i32), ("height", i32)]
+
+
+class SSLight(C.Structure):
+    _fields_ = [("direction", f64 * 3), ("intensity", f64 * 3), ("ambient_bands", i32), ("_pad", i32),
+                ("ambient", f64 * 48)]
+
+
+class SSRenderOpts(C.Structure):
+    _fields_ = [("background", f64 * 3), ("subset", vp), ("subset_count", i32), ("extent_cutoff", i32),
+                ("precision", i32), ("deterministic", i32)]
+
+
+class SSRenderStats(C.Structure):
+    _fields_ = [("visible", i64), ("pairs", i64), ("tiles", i64)]
+
+
+class SSAdamHparams(C.Structure):
+    _fields_ = [("lr_means", f64), ("lr_log_scales", f64), ("lr_quaternions", f64),
+                ("lr_logit_opacities", f64), ("lr_sh_dc", f64), ("lr_sh_rest", f64),
+                ("beta1", f64), ("beta2", f64), ("eps", f64), ("ema_beta", f64)]
+
+
+class SSAdamState(C.Structure):
+    _fields_ = [("m", vp), ("v", vp), ("grad_ema", vp), ("age", vp), ("step_count", i32)]
+
+
+class SSPrepared(C.Structure):
+    _fields_ = [("rows", vp), ("depth", vp), ("mu2d", vp), ("sigma2d", vp), ("radius", vp), ("window", vp),
+                ("opacity", vp), ("color", vp), ("color_pre", vp), ("shade_s", vp), ("order", vp),
+                ("capacity", i64)]
+
+
+class SSOrthoCamera(C.Structure):
+    _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("half_width", f64), ("half_height", f64),
+                ("width", i32), ("height", i32)]
+
+
+_SIGS = {
+    "ss_abi_version": (i32, []),
+    "ss_ctx_create": (i32, [i32, C.POINTER(vp)]),
+    "ss_ctx_destroy": (None, [vp]),
+    "ss_last_error": (C.c_char_p, [vp]),
+    "ss_set_stream": (i32, [vp, vp]),
+    "ss_grad_layout": (i64, [i64, i32, C.POINTER(i64)]),
+    "ss_set_timing": (i32, [vp, i32]),
+    "ss_get_timing": (i32, [vp, C.POINTER(f64), C.POINTER(i64), C.POINTER(u64), i32]),
+    "ss_measure_fp32_peak": (i32, [vp, C.POINTER(f64)]),
+    "ss_render": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSCamera), C.POINTER(SSLight),
+                        C.POINTER(SSRenderOpts), vp, vp, C.POINTER(SSRenderStats)]),
+    "ss_prepare_splats": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSCamera), C.POINTER(SSLight),
+                                C.POINTER(SSRenderOpts), C.POINTER(SSPrepared), C.POINTER(i64)]),
+    "ss_debug_bins": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSCamera), C.POINTER(SSRenderOpts), vp, i64, vp,
+                            i64, vp, i64, C.POINTER(SSRenderStats)]),
+    "ss_backward": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSCamera), C.POINTER(SSLight),
+                          C.POINTER(SSRenderOpts), vp, vp, vp, vp, C.POINTER(SSRenderStats)]),
+    "ss_adam_step": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSAdamState), vp, i32, C.POINTER(SSAdamHparams)]),
+    "ss_encode_delta": (i32, [vp, i32, vp, i32, vp, vp, i64, i32, f64, vp, u64, vp]),
+    "ss_delta_bound": (u64, [i32, i64, i32]),
+    "ss_encode_snapshot": (i32, [vp, C.POINTER(SSModel), i32, vp, u64, vp, vp, vp]),
+    "ss_snapshot_bound": (u64, [i64, i32, i32]),
+    "ss_encode_light_visibility": (i32, [vp, vp, i64, vp, u64, vp]),
+    "ss_host_zlib_compress": (i32, [vp, u64, vp, u64, C.POINTER(u64)]),
+    "ss_host_zlib_bound": (u64, [u64]),
+    "ss_update_light_visibility": (i32, [vp, C.POINTER(SSModel), vp, C.POINTER(SSOrthoCamera), f64]),
+    "ss_apply_object_transform": (i32, [vp, C.POINTER(SSModel), i32, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
+    "ss_refresh_object_locals": (i32, [vp, C.POINTER(SSModel), i32, i32, vp, vp, C.POINTER(f64),
+                                       C.POINTER(f64)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path=LIB_PATH):
+    """Load and type the shared library (works without a GPU)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not pathlib.Path(path).exists():
+                raise RuntimeError(
+                    f"{path} is missing: build it with `python -m paper_2604_02851_b200._build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(str(path))
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+class Context:
+    """One ss_ctx per (device, thread); binds the current torch stream per call."""
+
+    def __init__(self, device: int):
+        self.lib = load_library()
+        h = vp()
+        rc = self.lib.ss_ctx_create(device, C.byref(h))
+        if rc != SS_OK:
+            raise RuntimeError(f"ss_ctx_create failed ({rc}) on cuda:{device}")
+        self.handle = h
+        self.device = device
+
+    def check(self, rc: int):
+        if rc == SS_OK:
+            return
+        msg = self.lib.ss_last_error(self.handle).decode(errors="replace")
+        if rc == SS_ERR_INVALID:
+            raise ValueError(msg)
+        if rc == SS_ERR_PROTOCOL:
+            raise ProtocolError(msg)
+        raise RuntimeError(f"splatstream_b200 error {rc}: {msg}")
+
+    def bind_stream(self):
+        import torch
+        s = torch.cuda.current_stream(self.device)
+        self.check(self.lib.ss_set_stream(self.handle, vp(s.cuda_stream)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.lib.ss_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_ctx = threading.local()
+
+
+def ctx(device=None) -> Context:
+    """The calling thread's context for `device` (default: current CUDA device)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("splatstream_b200 needs a CUDA device (there is no CPU fallback)")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    cache = getattr(_ctx, "by_dev", None)
+    if cache is None:
+        cache = _ctx.by_dev = {}
+    if dev not in cache:
+        cache[dev] = Context(dev)
+    c = cache[dev]
+    c.bind_stream()
+    return c
+
+
+KERNEL_CLASSES = ("preprocess", "depth_sort", "binning", "tile_sort", "blend_forward", "blend_backward",
+                  "chain_rule", "adam", "encoders")
+
+
+def set_timing(c: "Context", on: bool):
+    c.check(c.lib.ss_set_timing(c.handle, 1 if on else 0))
+
+
+def get_timing(c: "Context", reset=True):
+    """{class: (ms, launch groups)}, counters (evaluated pairs, kernel launches)."""
+    ms = (f64 * 9)()
+    groups = (i64 * 9)()
+    cnt = (u64 * 4)()
+    c.check(c.lib.ss_get_timing(c.handle, ms, groups, cnt, 1 if reset else 0))
+    return {k: (ms[i], groups[i]) for i, k in enumerate(KERNEL_CLASSES)}, list(cnt)
+
+
+def ptr(t) -> vp:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return vp(0) if t is None else vp(t.data_ptr())
+
+
+def f64arr(values, n):
+    a = (f64 * n)()
+    v = np.asarray(values, np.float64).ravel()
+    for i in range(min(n, v.size)):
+        a[i] = float(v[i])
+    return a

@@ -1,0 +1,118 @@
+// Fused Adam over the active prefix (ref pkg/src/splatstream/optim.py:374-406).
+//
+// One pass over the flat gradient buffer (layout of ss_grad_layout): scale by
+// 1/n_views, fp64 moments, bias correction, per-group learning rate (DC vs
+// the rest of SH), f32(f64(p) - update).  A second per-row pass renormalises
+// quaternions and advances the grad-norm EMA and the age.  Every double op
+// is explicitly rounded in numpy's order so the trajectory follows the
+// reference's float64 arithmetic.
+#include <math.h>
+
+#include "ss_internal.cuh"
+
+namespace {
+
+struct AdamConst {
+    double scale, b1, b2, omb1, omb2, bc1, bc2, eps, ema_beta, omema;
+    double lr[6];  // means, log_scales, quaternions, logit_opacities, sh_dc, sh_rest
+    int64_t a;
+    int B;
+};
+
+__global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float* __restrict__ quats,
+                       float* __restrict__ logits, float* __restrict__ sh, double* __restrict__ m,
+                       double* __restrict__ v, const float* __restrict__ g, AdamConst c) {
+    const int64_t a = c.a, total = a * (11 + 3 * (int64_t)c.B);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        float* p;
+        double lr;
+        if (e < 3 * a) {
+            p = means + e;
+            lr = c.lr[0];
+        } else if (e < 6 * a) {
+            p = ls + (e - 3 * a);
+            lr = c.lr[1];
+        } else if (e < 10 * a) {
+            p = quats + (e - 6 * a);
+            lr = c.lr[2];
+        } else if (e < 11 * a) {
+            p = logits + (e - 10 * a);
+            lr = c.lr[3];
+        } else {
+            const int64_t k = e - 11 * a;
+            p = sh + k;
+            lr = (k % c.B) == 0 ? c.lr[4] : c.lr[5];
+        }
+        const double gg = dm((double)g[e], c.scale);
+        const double mm = da(dm(c.b1, m[e]), dm(c.omb1, gg));
+        const double vv = da(dm(c.b2, v[e]), dm(dm(c.omb2, gg), gg));
+        m[e] = mm;
+        v[e] = vv;
+        const double mh = dd(mm, c.bc1);
+        const double vh = dd(vv, c.bc2);
+        const double upd = dm(dd(mh, da(dsq(vh), c.eps)), lr);
+        *p = __double2float_rn(ds((double)*p, upd));
+    }
+}
+
+__global__ void k_adam_rows(float* __restrict__ quats, const float* __restrict__ g, double* __restrict__ ema,
+                            int64_t* __restrict__ age, AdamConst c) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.a; i += (int64_t)gridDim.x * blockDim.x) {
+        float* q = quats + 4 * i;
+        const double w = q[0], x = q[1], y = q[2], z = q[3];
+        const double n = dsq(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
+        q[0] = __double2float_rn(dd(w, n));
+        q[1] = __double2float_rn(dd(x, n));
+        q[2] = __double2float_rn(dd(y, n));
+        q[3] = __double2float_rn(dd(z, n));
+        const double g0 = dm((double)g[3 * i], c.scale), g1 = dm((double)g[3 * i + 1], c.scale),
+                     g2 = dm((double)g[3 * i + 2], c.scale);
+        const double norm = dsq(da(da(dm(g0, g0), dm(g1, g1)), dm(g2, g2)));
+        ema[i] = age[i] == 0 ? norm : da(dm(c.ema_beta, ema[i]), dm(c.omema, norm));
+        age[i] += 1;
+    }
+}
+
+}  // namespace
+
+extern "C" int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int32_t n_views,
+                            const ss_adam_hparams* hp) {
+    if (!ctx || !model || !st || !grad || !hp) return SS_ERR_INVALID;
+    if (n_views < 1) return ss_fail(ctx, SS_ERR_INVALID, "no ready views");
+    const int64_t a = model->active_count;
+    if (a == 0) return SS_OK;  // frozen-only model: no state change (optim.py:374)
+    const int t = st->step_count + 1;
+    AdamConst c;
+    c.scale = 1.0 / (double)n_views;
+    c.b1 = hp->beta1;
+    c.b2 = hp->beta2;
+    c.omb1 = 1.0 - hp->beta1;
+    c.omb2 = 1.0 - hp->beta2;
+    c.bc1 = 1.0 - pow(hp->beta1, (double)t);  // host libm pow, as Python's float **
+    c.bc2 = 1.0 - pow(hp->beta2, (double)t);
+    c.eps = hp->eps;
+    c.ema_beta = hp->ema_beta;
+    c.omema = 1.0 - hp->ema_beta;
+    c.lr[0] = hp->lr_means;
+    c.lr[1] = hp->lr_log_scales;
+    c.lr[2] = hp->lr_quaternions;
+    c.lr[3] = hp->lr_logit_opacities;
+    c.lr[4] = hp->lr_sh_dc;
+    c.lr[5] = hp->lr_sh_rest;
+    c.a = a;
+    c.B = (model->sh_degree + 1) * (model->sh_degree + 1);
+    const int64_t total = a * (11 + 3 * (int64_t)c.B);
+    int64_t grid = (total + 255) / 256;
+    if (grid > (int64_t)ctx->num_sms * 32) grid = (int64_t)ctx->num_sms * 32;
+    ss_tic(ctx, KC_ADAM);
+    k_adam<<<(int)grid, 256, 0, ctx->stream>>>(model->means, model->log_scales, model->quaternions,
+                                                model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c);
+    SS_CHECK_LAUNCH(ctx);
+    int64_t rg = (a + 255) / 256;
+    if (rg > (int64_t)ctx->num_sms * 32) rg = (int64_t)ctx->num_sms * 32;
+    k_adam_rows<<<(int)rg, 256, 0, ctx->stream>>>(model->quaternions, grad, st->grad_ema, st->age, c);
+    SS_CHECK_LAUNCH(ctx);
+    ss_toc(ctx, KC_ADAM);
+    st->step_count = t;
+    return SS_OK;
+}

@@ -1,0 +1,616 @@
+// Bit-exact wire encoders (compression_id 0) for the splatstream protocol.
+//
+//   ss_encode_delta     ref pkg/src/splatstream/protocol/delta.py:72-137
+//   ss_encode_snapshot  ref protocol/snapshot.py:47-82 (+ server baseline
+//                       reset, server.py:481-484, computed from the codes)
+//   ss_encode_light_visibility  ref protocol/packets.py:73-76
+//
+// Arithmetic: float64 with explicitly rounded ops (no FMA contraction) in the
+// reference's order, rint() = round-half-even, float32 stores via
+// __double2float_rn -- identical to numpy.  The kernels never synchronise
+// with the host: the residual mode decision, the survivor count and every
+// byte offset live in device memory, and the payload length is written to a
+// device word.
+#include "ss_internal.cuh"
+
+namespace {
+
+enum { A_MEANS = 0, A_LS, A_QUAT, A_OPAC, A_DC, A_REST, A_VIS };
+
+struct QSpec {
+    int bits;
+    double lo, hi;
+};
+
+__host__ __device__ inline QSpec qspec(int attr) {
+    switch (attr) {
+        case A_MEANS: return {16, 0.0, 0.0};
+        case A_LS: return {8, -10.0, 2.0};
+        case A_QUAT: return {10, -1.0, 1.0};
+        case A_OPAC: return {8, -8.0, 8.0};
+        case A_DC: return {8, -4.0, 4.0};
+        case A_REST: return {8, -1.0, 1.0};
+        default: return {1, 0.0, 1.0};
+    }
+}
+
+// ref quantize.py:8-17
+__device__ __forceinline__ uint32_t quantize(double v, double lo, double hi, int bits) {
+    const double levels = (double)((1u << bits) - 1u);
+    const double span = hi > lo ? ds(hi, lo) : 1.0;
+    double c = fmin(fmax(v, lo), hi);
+    double t = dd(ds(c, lo), span);
+    t = fmin(fmax(t, 0.0), 1.0);
+    return (uint32_t)rint(dm(t, levels));
+}
+
+// ref quantize.py:20-24
+__device__ __forceinline__ double dequantize(uint32_t code, double lo, double hi, int bits) {
+    const double levels = (double)((1u << bits) - 1u);
+    return da(lo, dm(dd((double)code, levels), ds(hi, lo)));
+}
+
+__device__ __forceinline__ int varint_len(uint64_t v) {
+    int n = 1;
+    while (v >= 0x80) {
+        v >>= 7;
+        ++n;
+    }
+    return n;
+}
+
+__device__ __forceinline__ void varint_put(uint8_t* p, uint64_t v) {
+    while (v >= 0x80) {
+        *p++ = (uint8_t)(v & 0x7F) | 0x80;
+        v >>= 7;
+    }
+    *p = (uint8_t)v;
+}
+
+__device__ __forceinline__ void put_u32(uint8_t* p, uint32_t v) {
+    p[0] = v & 0xff;
+    p[1] = (v >> 8) & 0xff;
+    p[2] = (v >> 16) & 0xff;
+    p[3] = v >> 24;
+}
+__device__ __forceinline__ void put_f32(uint8_t* p, float f) { put_u32(p, __float_as_uint(f)); }
+
+__device__ __forceinline__ void put_code(uint8_t* p, uint32_t code, int bits) {
+    if (bits == 16) {
+        p[0] = code & 0xff;
+        p[1] = code >> 8;
+    } else {
+        p[0] = (uint8_t)code;
+    }
+}
+
+// order-preserving maps for float min/max with integer atomics
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+template <typename T>
+__device__ __forceinline__ double ld(const T* p, int64_t i) { return (double)p[i]; }
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------- residual
+struct ResidState {
+    unsigned long long count;    // rows with max|r| >= gate
+    unsigned long long max_all;  // bits of max |r| over all rows (>= 0 doubles order as ints)
+    unsigned long long max_keep; // bits of max |r| over gated rows
+    unsigned long long varint_bytes;
+    int mode;                    // 0 dense, 1 sparse
+    int bits;
+    double m;                    // f32-rounded symmetric range
+};
+
+template <typename T>
+__global__ void k_resid_stats(const T* __restrict__ cur, const T* __restrict__ base, int64_t rows, int dims,
+                              double gate, uint8_t* __restrict__ keep, ResidState* st) {
+    unsigned long long cnt = 0, mall = 0, mkeep = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+        double rmax = 0.0;
+        for (int d = 0; d < dims; ++d) {
+            double r = ds(ld(cur, i * dims + d), ld(base, i * dims + d));
+            rmax = fmax(rmax, fabs(r));
+        }
+        bool k = rmax >= gate;
+        keep[i] = k;
+        unsigned long long b = (unsigned long long)__double_as_longlong(rmax);
+        cnt += k;
+        mall = b > mall ? b : mall;
+        if (k) mkeep = b > mkeep ? b : mkeep;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    mall = warp_max_u64(mall);
+    mkeep = warp_max_u64(mkeep);
+    if ((threadIdx.x & 31) == 0) {
+        if (cnt) atomicAdd(&st->count, cnt);
+        atomicMax(&st->max_all, mall);
+        atomicMax(&st->max_keep, mkeep);
+    }
+}
+
+__global__ void k_resid_decide(ResidState* st, int64_t rows, int bits) {
+    const unsigned long long k = st->count;
+    const bool sparse = 2 * (int64_t)k < rows;  // k < rows * 0.5 (delta.py:101)
+    double m;
+    if (sparse) m = k ? (double)__double2float_rn(__longlong_as_double((long long)st->max_keep)) : 0.0;
+    else m = rows ? (double)__double2float_rn(__longlong_as_double((long long)st->max_all)) : 0.0;
+    st->mode = sparse ? 1 : 0;
+    st->m = m;
+    st->bits = bits;
+}
+
+template <typename T>
+__global__ void k_resid_dense(const T* __restrict__ cur, const T* __restrict__ base, int64_t n, int bits,
+                              const ResidState* st, uint8_t* __restrict__ block, float* __restrict__ new_base) {
+    if (st->mode != 0) return;
+    const double m = st->m, lo = -m;
+    const int cb = bits / 8;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        double b = ld(base, e);
+        double r = ds(ld(cur, e), b);
+        uint32_t code = quantize(r, lo, m, bits);
+        put_code(block + e * cb, code, bits);
+        if (new_base) new_base[e] = __double2float_rn(da(b, dequantize(code, lo, m, bits)));
+    }
+}
+
+template <typename T>
+__global__ void k_copy_base(const T* __restrict__ base, int64_t n, const ResidState* st, float* __restrict__ out) {
+    if (st->mode != 1) return;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = (float)base[e];
+}
+
+__global__ void k_sparse_compact(const uint8_t* __restrict__ keep, const uint64_t* __restrict__ pos, int64_t rows,
+                                 const ResidState* st, uint32_t* __restrict__ idx) {
+    if (st->mode != 1) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+        if (keep[i]) idx[pos[i]] = (uint32_t)i;
+}
+
+__global__ void k_sparse_lens(const uint32_t* __restrict__ idx, int64_t rows, const ResidState* st,
+                              uint32_t* __restrict__ lens) {
+    const int64_t k = st->mode == 1 ? (int64_t)st->count : 0;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < rows; s += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t L = 0;
+        if (s < k) {
+            int64_t prev = s ? (int64_t)idx[s - 1] : -1;
+            L = varint_len((uint64_t)((int64_t)idx[s] - prev - 1));
+        }
+        lens[s] = L;
+    }
+}
+
+template <typename T>
+__global__ void k_sparse_write(const T* __restrict__ cur, const T* __restrict__ base, int dims, int bits,
+                               const uint32_t* __restrict__ idx, const uint64_t* __restrict__ voff, int64_t rows,
+                               const ResidState* st, uint8_t* __restrict__ block, float* __restrict__ new_base) {
+    if (st->mode != 1) return;
+    const int64_t k = (int64_t)st->count;
+    const uint64_t V = st->varint_bytes;
+    const double m = st->m, lo = -m;
+    const int cb = bits / 8;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < k; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx[s];
+        const int64_t prev = s ? (int64_t)idx[s - 1] : -1;
+        varint_put(block + voff[s], (uint64_t)(i - prev - 1));
+        uint8_t* cp = block + V + (uint64_t)s * dims * cb;
+        for (int d = 0; d < dims; ++d) {
+            double b = ld(base, i * dims + d);
+            double r = ds(ld(cur, i * dims + d), b);
+            uint32_t code = quantize(r, lo, m, bits);
+            put_code(cp + d * cb, code, bits);
+            if (new_base) new_base[i * dims + d] = __double2float_rn(da(b, dequantize(code, lo, m, bits)));
+        }
+    }
+}
+
+__global__ void k_resid_header(ResidState* st, const uint64_t* varint_total, int attr, int dims, int64_t rows,
+                               uint8_t* out, uint64_t* out_len) {
+    const int sparse = st->mode == 1;
+    const uint64_t k = st->count;
+    const int cb = st->bits / 8;
+    uint64_t V = 0;
+    if (sparse) V = *varint_total;
+    st->varint_bytes = V;
+    const uint64_t blen = sparse ? V + k * dims * cb : (uint64_t)rows * dims * cb;
+    out[0] = (uint8_t)attr;
+    out[1] = (uint8_t)(sparse ? 1 : 0);
+    out[2] = 0;  // compression id: raw
+    out[3] = (uint8_t)dims;
+    put_u32(out + 4, (uint32_t)rows);
+    const float mf = (float)st->m;
+    put_f32(out + 8, -mf);
+    put_f32(out + 12, mf);
+    int h = 16;
+    if (sparse) {
+        put_u32(out + 16, (uint32_t)k);
+        h = 20;
+    }
+    put_u32(out + h, (uint32_t)blen);
+    *out_len = h + 4 + blen;
+}
+
+// ---------------------------------------------------------------- absolute
+template <typename T>
+__global__ void k_abs_bytes(const T* __restrict__ x, int64_t n, QSpec q, uint8_t* __restrict__ block) {
+    const int cb = q.bits / 8;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        put_code(block + e * cb, quantize(ld(x, e), q.lo, q.hi, q.bits), q.bits);
+}
+
+// 10-bit LSB-first: every 4 codes form exactly 5 bytes (n % 4 == 0 here)
+template <typename T>
+__global__ void k_abs_pack10(const T* __restrict__ x, int64_t groups, QSpec q, uint8_t* __restrict__ block) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t w = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w |= (uint64_t)quantize(ld(x, g * 4 + j), q.lo, q.hi, 10) << (10 * j);
+        uint8_t* p = block + g * 5;
+#pragma unroll
+        for (int b = 0; b < 5; ++b) p[b] = (uint8_t)(w >> (8 * b));
+    }
+}
+
+// 1-bit LSB-first of (v >= 0.5): one byte per 8 elements
+template <typename T>
+__global__ void k_abs_pack1(const T* __restrict__ x, int64_t n, uint8_t* __restrict__ block) {
+    const int64_t nbytes = (n + 7) / 8;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nbytes; j += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t b = 0;
+        for (int t = 0; t < 8; ++t) {
+            int64_t e = j * 8 + t;
+            if (e < n && ld(x, e) >= 0.5) b |= (uint8_t)(1u << t);
+        }
+        block[j] = b;
+    }
+}
+
+__global__ void k_abs_header(int attr, int dims, int64_t rows, uint64_t blen, uint8_t* out, uint64_t* out_len) {
+    out[0] = (uint8_t)attr;
+    out[1] = 2;
+    out[2] = 0;
+    out[3] = (uint8_t)dims;
+    put_u32(out + 4, (uint32_t)rows);
+    put_u32(out + 8, (uint32_t)blen);
+    *out_len = 12 + blen;
+}
+
+inline int grid_for(ss_ctx* ctx, int64_t n, int block = 256) {
+    int64_t g = (n + block - 1) / block;
+    int64_t cap = (int64_t)ctx->num_sms * 16;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+template <typename T>
+int encode_delta_t(ss_ctx* ctx, int attr, const T* cur, const T* base, float* new_base, int64_t rows, int dims,
+                   double gate, uint8_t* out, uint64_t* out_len) {
+    const QSpec q = qspec(attr);
+    const int64_t n = rows * dims;
+    cudaStream_t s = ctx->stream;
+    if (attr == A_MEANS || attr == A_LS) {
+        ResidState* st = SS_SCRATCH(ctx, ResidState, 1);
+        uint8_t* keep = SS_SCRATCH(ctx, uint8_t, rows);
+        uint64_t* pos = SS_SCRATCH(ctx, uint64_t, rows);
+        uint32_t* idx = SS_SCRATCH(ctx, uint32_t, rows);
+        uint32_t* lens = SS_SCRATCH(ctx, uint32_t, rows);
+        uint64_t* voff = SS_SCRATCH(ctx, uint64_t, rows);
+        uint64_t* vtot = SS_SCRATCH(ctx, uint64_t, 1);
+        if (!st || !keep || !pos || !idx || !lens || !voff || !vtot) return SS_ERR_CUDA;
+        SS_CUDA(ctx, cudaMemsetAsync(st, 0, sizeof(ResidState), s));
+        if (rows) {
+            k_resid_stats<T><<<grid_for(ctx, rows), 256, 0, s>>>(cur, base, rows, dims, gate, keep, st);
+            SS_CHECK_LAUNCH(ctx);
+        }
+        k_resid_decide<<<1, 1, 0, s>>>(st, rows, q.bits);
+        SS_CHECK_LAUNCH(ctx);
+        // the block starts after a 20-byte (dense) or 24-byte (sparse) header;
+        // both paths are launched and each exits unless its mode was chosen
+        if (n) {
+            k_resid_dense<T><<<grid_for(ctx, n), 256, 0, s>>>(cur, base, n, q.bits, st, out + 20, new_base);
+            SS_CHECK_LAUNCH(ctx);
+            if (new_base && (void*)new_base != (const void*)base) {
+                k_copy_base<T><<<grid_for(ctx, n), 256, 0, s>>>(base, n, st, new_base);
+                SS_CHECK_LAUNCH(ctx);
+            }
+            SS_TRY(ss_scan_u8_to_u64(ctx, keep, pos, rows, nullptr));
+            k_sparse_compact<<<grid_for(ctx, rows), 256, 0, s>>>(keep, pos, rows, st, idx);
+            SS_CHECK_LAUNCH(ctx);
+            k_sparse_lens<<<grid_for(ctx, rows), 256, 0, s>>>(idx, rows, st, lens);
+            SS_CHECK_LAUNCH(ctx);
+            SS_TRY(ss_scan_u32_to_u64(ctx, lens, voff, rows, vtot));
+        } else {
+            SS_CUDA(ctx, cudaMemsetAsync(vtot, 0, sizeof(uint64_t), s));
+        }
+        k_resid_header<<<1, 1, 0, s>>>(st, vtot, attr, dims, rows, out, out_len);
+        SS_CHECK_LAUNCH(ctx);
+        if (n) {
+            k_sparse_write<T><<<grid_for(ctx, rows), 256, 0, s>>>(cur, base, dims, q.bits, idx, voff, rows, st,
+                                                                   out + 24, new_base);
+            SS_CHECK_LAUNCH(ctx);
+        }
+        return SS_OK;
+    }
+    uint8_t* block = out + 12;
+    uint64_t blen;
+    if (attr == A_VIS) {
+        blen = (uint64_t)(n + 7) / 8;
+        if (n) k_abs_pack1<T><<<grid_for(ctx, (n + 7) / 8), 256, 0, s>>>(cur, n, block);
+    } else if (q.bits == 10) {
+        if (n % 4) return ss_fail(ctx, SS_ERR_INVALID, "10-bit pack needs a multiple of 4 codes");
+        blen = (uint64_t)n / 4 * 5;
+        if (n) k_abs_pack10<T><<<grid_for(ctx, n / 4), 256, 0, s>>>(cur, n / 4, q, block);
+    } else {
+        blen = (uint64_t)n * (q.bits / 8);
+        if (n) k_abs_bytes<T><<<grid_for(ctx, n), 256, 0, s>>>(cur, n, q, block);
+    }
+    SS_CHECK_LAUNCH(ctx);
+    k_abs_header<<<1, 1, 0, s>>>(attr, dims, rows, blen, out, out_len);
+    SS_CHECK_LAUNCH(ctx);
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------- snapshot
+struct SnapState {
+    uint32_t lo_ord[3], hi_ord[3];
+};
+
+__global__ void k_aabb(const float* __restrict__ means, int64_t n, SnapState* st) {
+    uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0, 0, 0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            uint32_t o = f2ord(means[i * 3 + a]);
+            lo[a] = o < lo[a] ? o : lo[a];
+            hi[a] = o > hi[a] ? o : hi[a];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o; o >>= 1) {
+            uint32_t l = __shfl_xor_sync(0xffffffffu, lo[a], o), h = __shfl_xor_sync(0xffffffffu, hi[a], o);
+            lo[a] = l < lo[a] ? l : lo[a];
+            hi[a] = h > hi[a] ? h : hi[a];
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&st->lo_ord[a], lo[a]);
+            atomicMax(&st->hi_ord[a], hi[a]);
+        }
+    }
+}
+
+__global__ void k_snap_init(SnapState* st) {
+    for (int a = 0; a < 3; ++a) {
+        st->lo_ord[a] = 0xffffffffu;
+        st->hi_ord[a] = 0u;
+    }
+}
+
+struct SnapLayout {
+    int64_t n;
+    int B;
+    uint64_t off_means, off_ls, off_quat, off_opac, off_dc, off_rest, off_vis, off_ids;
+};
+
+__device__ __forceinline__ void aabb_of(const SnapState* st, int64_t n, double lo[3], double hi[3]) {
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = n ? (double)ord2f(st->lo_ord[a]) : 0.0;
+        hi[a] = n ? (double)ord2f(st->hi_ord[a]) : 0.0;
+    }
+}
+
+__global__ void k_snap_rows(ss_model m, SnapLayout L, const SnapState* st, uint8_t* __restrict__ blk,
+                            float* __restrict__ base_means, float* __restrict__ base_ls) {
+    double lo[3], hi[3];
+    aabb_of(st, L.n, lo, hi);
+    const QSpec qls = qspec(A_LS), qq = qspec(A_QUAT), qo = qspec(A_OPAC), qdc = qspec(A_DC), qr = qspec(A_REST);
+    const int B = L.B;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // loop bound rounded up to whole warps so the visibility ballot is convergent
+    const int64_t nw = (L.n + 31) & ~int64_t(31);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += stride) {
+        const bool ok = i < L.n;
+        if (ok) {
+            for (int a = 0; a < 3; ++a) {
+                uint32_t c = quantize((double)m.means[i * 3 + a], lo[a], hi[a], 16);
+                put_code(blk + L.off_means + (i * 3 + a) * 2, c, 16);
+                if (base_means) base_means[i * 3 + a] = __double2float_rn(dequantize(c, lo[a], hi[a], 16));
+                uint32_t cl = quantize((double)m.log_scales[i * 3 + a], qls.lo, qls.hi, 8);
+                blk[L.off_ls + i * 3 + a] = (uint8_t)cl;
+                if (base_ls) base_ls[i * 3 + a] = __double2float_rn(dequantize(cl, qls.lo, qls.hi, 8));
+            }
+            uint64_t w = 0;
+            for (int j = 0; j < 4; ++j)
+                w |= (uint64_t)quantize((double)m.quaternions[i * 4 + j], qq.lo, qq.hi, 10) << (10 * j);
+            for (int b = 0; b < 5; ++b) blk[L.off_quat + i * 5 + b] = (uint8_t)(w >> (8 * b));
+            blk[L.off_opac + i] = (uint8_t)quantize((double)m.logit_opacities[i], qo.lo, qo.hi, 8);
+            const float* sh = m.sh_coeffs + i * 3 * B;
+            for (int c = 0; c < 3; ++c) {
+                blk[L.off_dc + i * 3 + c] = (uint8_t)quantize((double)sh[c * B], qdc.lo, qdc.hi, 8);
+                for (int b = 1; b < B; ++b)
+                    blk[L.off_rest + (i * 3 + c) * (B - 1) + (b - 1)] =
+                        (uint8_t)quantize((double)sh[c * B + b], qr.lo, qr.hi, 8);
+            }
+        }
+        unsigned bal = __ballot_sync(0xffffffffu, ok && m.light_visibility[ok ? i : 0] >= 0.5f);
+        if ((threadIdx.x & 31) == 0) {
+            const int64_t i0 = i;  // warp base (i is lane 0's row)
+            int64_t nb = (L.n - i0 + 7) / 8;
+            if (nb > 4) nb = 4;
+            for (int b = 0; b < nb; ++b) blk[L.off_vis + i0 / 8 + b] = (uint8_t)(bal >> (8 * b));
+        }
+    }
+}
+
+__global__ void k_snap_id_lens(const int32_t* __restrict__ ids, int64_t n, uint32_t* __restrict__ lens) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        lens[i] = varint_len((uint64_t)(int64_t)ids[i]);
+}
+
+__global__ void k_snap_id_write(const int32_t* __restrict__ ids, int64_t n, const uint64_t* __restrict__ off,
+                                uint8_t* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        varint_put(dst + off[i], (uint64_t)(int64_t)ids[i]);
+}
+
+__global__ void k_snap_header(const SnapState* st, int64_t n, int active, int degree, int profile,
+                              uint64_t fixed_len, const uint64_t* var_len, uint8_t* out, uint64_t* out_len) {
+    double lo[3], hi[3];
+    aabb_of(st, n, lo, hi);
+    put_u32(out, (uint32_t)n);
+    put_u32(out + 4, (uint32_t)active);
+    out[8] = (uint8_t)degree;
+    out[9] = (uint8_t)profile;
+    out[10] = 0;  // compression id: raw
+    out[11] = 0;
+    for (int a = 0; a < 3; ++a) {
+        put_f32(out + 12 + 4 * a, (float)lo[a]);
+        put_f32(out + 24 + 4 * a, (float)hi[a]);
+    }
+    uint64_t blen = fixed_len + (var_len ? *var_len : 0);
+    put_u32(out + 36, (uint32_t)blen);
+    *out_len = 40 + blen;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t ss_delta_bound(int32_t attr, int64_t rows, int32_t dims) {
+    const int64_t n = rows * dims;
+    if (attr == A_MEANS || attr == A_LS) return 24 + 5 * (uint64_t)rows + 2 * (uint64_t)n;
+    if (attr == A_VIS) return 12 + (uint64_t)(n + 7) / 8;
+    QSpec q = qspec(attr);
+    return 12 + (uint64_t)(n * q.bits + 7) / 8;
+}
+
+int ss_encode_delta(ss_ctx* ctx, int32_t attr, const void* cur, int32_t in_dtype, const void* base,
+                    float* new_base, int64_t rows, int32_t dims, double gate, uint8_t* out, uint64_t out_cap,
+                    uint64_t* out_len) {
+    if (!ctx) return SS_ERR_INVALID;
+    if (attr < 0 || attr > A_VIS) return ss_fail(ctx, SS_ERR_PROTOCOL, "unknown attribute id %d", attr);
+    if (rows < 0 || dims < 1 || dims > 255) return ss_fail(ctx, SS_ERR_INVALID, "bad shape rows=%lld dims=%d",
+                                                           (long long)rows, dims);
+    if (rows > (int64_t)UINT32_MAX) return ss_fail(ctx, SS_ERR_INVALID, "too many rows");
+    const bool resid = attr == A_MEANS || attr == A_LS;
+    if (resid && !base && rows > 0) return ss_fail(ctx, SS_ERR_INVALID, "attribute %d is residual-coded and needs a baseline", attr);
+    if (out_cap < ss_delta_bound(attr, rows, dims)) return ss_fail(ctx, SS_ERR_CAPACITY, "delta output too small");
+    SS_TRY(ss_scratch_reset(ctx));
+    if (in_dtype != 0 && in_dtype != 1) return ss_fail(ctx, SS_ERR_INVALID, "in_dtype must be 0 (f32) or 1 (f64)");
+    ss_tic(ctx, KC_CODEC);
+    int rc = in_dtype == 0 ? encode_delta_t<float>(ctx, attr, (const float*)cur, (const float*)base, new_base, rows,
+                                                   dims, gate, out, out_len)
+                           : encode_delta_t<double>(ctx, attr, (const double*)cur, (const double*)base, new_base,
+                                                    rows, dims, gate, out, out_len);
+    ss_toc(ctx, KC_CODEC);
+    return rc;
+}
+
+uint64_t ss_snapshot_bound(int64_t n, int32_t degree, int32_t profile) {
+    const uint64_t B = (uint64_t)(degree + 1) * (degree + 1);
+    if (profile == 1) return 40 + (52 + 12 * B) * (uint64_t)n;
+    return 40 + (18 + 3 * (B - 1)) * (uint64_t)n + (uint64_t)(n + 7) / 8 + 10 * (uint64_t)n;
+}
+
+int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t* out, uint64_t out_cap,
+                       uint64_t* out_len, float* base_means, float* base_ls) {
+    if (!ctx || !m) return SS_ERR_INVALID;
+    if (profile != 0 && profile != 1) return ss_fail(ctx, SS_ERR_PROTOCOL, "unknown profile id %d", profile);
+    if (m->sh_degree < 0 || m->sh_degree > 3) return ss_fail(ctx, SS_ERR_INVALID, "sh_degree %d", m->sh_degree);
+    const int64_t n = m->count;
+    if (out_cap < ss_snapshot_bound(n, m->sh_degree, profile)) return ss_fail(ctx, SS_ERR_CAPACITY, "snapshot output too small");
+    SS_TRY(ss_scratch_reset(ctx));
+    cudaStream_t s = ctx->stream;
+    const int B = (m->sh_degree + 1) * (m->sh_degree + 1);
+    SnapState* st = SS_SCRATCH(ctx, SnapState, 1);
+    if (!st) return SS_ERR_CUDA;
+    k_snap_init<<<1, 1, 0, s>>>(st);
+    if (n) k_aabb<<<grid_for(ctx, n), 256, 0, s>>>(m->means, n, st);
+    SS_CHECK_LAUNCH(ctx);
+    uint8_t* blk = out + 40;
+    if (profile == 1) {
+        uint64_t o = 0;
+        const void* src[7] = {m->means, m->log_scales, m->quaternions, m->logit_opacities, m->sh_coeffs,
+                              m->light_visibility, m->object_ids};
+        const uint64_t sz[7] = {12ull * n, 12ull * n, 16ull * n, 4ull * n, 12ull * B * n, 4ull * n, 4ull * n};
+        for (int k = 0; k < 7; ++k) {
+            if (sz[k]) SS_CUDA(ctx, cudaMemcpyAsync(blk + o, src[k], sz[k], cudaMemcpyDeviceToDevice, s));
+            o += sz[k];
+        }
+        if (base_means && n) SS_CUDA(ctx, cudaMemcpyAsync(base_means, m->means, 12ull * n, cudaMemcpyDeviceToDevice, s));
+        if (base_ls && n) SS_CUDA(ctx, cudaMemcpyAsync(base_ls, m->log_scales, 12ull * n, cudaMemcpyDeviceToDevice, s));
+        k_snap_header<<<1, 1, 0, s>>>(st, n, m->active_count, m->sh_degree, 1, o, nullptr, out, out_len);
+        SS_CHECK_LAUNCH(ctx);
+        return SS_OK;
+    }
+    SnapLayout L;
+    L.n = n;
+    L.B = B;
+    L.off_means = 0;
+    L.off_ls = 6ull * n;
+    L.off_quat = 9ull * n;
+    L.off_opac = 14ull * n;
+    L.off_dc = 15ull * n;
+    L.off_rest = 18ull * n;
+    L.off_vis = L.off_rest + 3ull * (B - 1) * n;
+    L.off_ids = L.off_vis + (uint64_t)(n + 7) / 8;
+    uint32_t* lens = SS_SCRATCH(ctx, uint32_t, n);
+    uint64_t* offs = SS_SCRATCH(ctx, uint64_t, n);
+    uint64_t* vtot = SS_SCRATCH(ctx, uint64_t, 1);
+    if (!lens || !offs || !vtot) return SS_ERR_CUDA;
+    if (n) {
+        k_snap_rows<<<grid_for(ctx, n), 256, 0, s>>>(*m, L, st, blk, base_means, base_ls);
+        SS_CHECK_LAUNCH(ctx);
+        k_snap_id_lens<<<grid_for(ctx, n), 256, 0, s>>>(m->object_ids, n, lens);
+        SS_CHECK_LAUNCH(ctx);
+    }
+    SS_TRY(ss_scan_u32_to_u64(ctx, lens, offs, n, vtot));
+    if (n) {
+        k_snap_id_write<<<grid_for(ctx, n), 256, 0, s>>>(m->object_ids, n, offs, blk + L.off_ids);
+        SS_CHECK_LAUNCH(ctx);
+    }
+    k_snap_header<<<1, 1, 0, s>>>(st, n, m->active_count, m->sh_degree, 0, L.off_ids, vtot, out, out_len);
+    SS_CHECK_LAUNCH(ctx);
+    return SS_OK;
+}
+
+int ss_encode_light_visibility(ss_ctx* ctx, const float* vis, int64_t n, uint8_t* out, uint64_t out_cap,
+                               uint64_t* out_len) {
+    if (!ctx) return SS_ERR_INVALID;
+    if (out_cap < 4 + (uint64_t)(n + 7) / 8) return ss_fail(ctx, SS_ERR_CAPACITY, "visibility output too small");
+    SS_TRY(ss_scratch_reset(ctx));
+    cudaStream_t s = ctx->stream;
+    if (n) {
+        k_abs_pack1<float><<<grid_for(ctx, (n + 7) / 8), 256, 0, s>>>(vis, n, out + 4);
+        SS_CHECK_LAUNCH(ctx);
+    }
+    // '<I' count header and the length, written from the host-known size
+    uint8_t head[4] = {(uint8_t)(n & 0xff), (uint8_t)((n >> 8) & 0xff), (uint8_t)((n >> 16) & 0xff),
+                       (uint8_t)((n >> 24) & 0xff)};
+    uint64_t len = 4 + (uint64_t)(n + 7) / 8;
+    memcpy(ctx->pinned, head, 4);
+    memcpy((uint8_t*)ctx->pinned + 8, &len, 8);
+    SS_CUDA(ctx, cudaMemcpyAsync(out, ctx->pinned, 4, cudaMemcpyHostToDevice, s));
+    SS_CUDA(ctx, cudaMemcpyAsync(out_len, (uint8_t*)ctx->pinned + 8, 8, cudaMemcpyHostToDevice, s));
+    SS_CUDA(ctx, cudaStreamSynchronize(s));  // the pinned staging buffer is reused
+    return SS_OK;
+}
+
+}  // extern "C"

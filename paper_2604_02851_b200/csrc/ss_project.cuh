@@ -1,0 +1,236 @@
+// Per-Gaussian fp64 projection, covariance and shading, shared by the
+// preprocess kernel (K1) and the per-Gaussian chain rule (K7).
+//
+// The quantities that decide depth order and pixel windows (camera-space
+// position, Sigma2d, radius) use explicitly rounded double ops in the same
+// order as oracle/raster.py:prepare, so keys/windows are bit-identical to the
+// oracle.  Reference semantics: pkg/src/splatstream/render.py:226-290 (EWA
+// projection, 0.3 blur, explicit inverse, 3-sigma radius), render.py:139-151
+// (normal proxy), render.py:175-197 (shading), render.py:63-136 (SH).
+#pragma once
+
+#include "ss_internal.cuh"
+
+#define SS_SH_C0 0.2820947918
+#define SS_SH_C1 0.4886025119
+#define SS_BLUR 0.3
+#define SS_AXIS_MARGIN 5e-3
+
+struct Proj {
+    double mc[3];      // camera-space mean
+    double d[3];       // mean - camera position
+    double J[2][3];    // projection Jacobian (J[0][1] = J[1][0] = 0)
+    double Rq[3][3];   // rotation of the normalised quaternion
+    double u[4];       // normalised quaternion
+    double qn;         // |q|
+    double S2[3];      // exp(2 log_scale)
+    double cov[3][3];  // W Sigma3d W^T
+    double s00, s01, s11, det;
+    double mu[2];
+    double radius;
+};
+
+// world->camera with W = R_cw^T: mc_k = sum_i d_i R_cw[i][k]
+__device__ __forceinline__ void ss_cam_point(const ss_camera& cam, const float* mean, double d[3], double mc[3]) {
+    d[0] = ds((double)mean[0], cam.position[0]);
+    d[1] = ds((double)mean[1], cam.position[1]);
+    d[2] = ds((double)mean[2], cam.position[2]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        mc[k] = da(da(dm(d[0], cam.rot_cw[0 * 3 + k]), dm(d[1], cam.rot_cw[1 * 3 + k])), dm(d[2], cam.rot_cw[2 * 3 + k]));
+}
+
+__device__ __forceinline__ void ss_quat_rot(const float* qf, double u[4], double* qn, double R[3][3]) {
+    double w = qf[0], x = qf[1], y = qf[2], z = qf[3];
+    double n = dsq(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
+    w = dd(w, n);
+    x = dd(x, n);
+    y = dd(y, n);
+    z = dd(z, n);
+    u[0] = w; u[1] = x; u[2] = y; u[3] = z;
+    *qn = n;
+    R[0][0] = ds(1.0, dm(2.0, da(dm(y, y), dm(z, z))));
+    R[0][1] = dm(2.0, ds(dm(x, y), dm(w, z)));
+    R[0][2] = dm(2.0, da(dm(x, z), dm(w, y)));
+    R[1][0] = dm(2.0, da(dm(x, y), dm(w, z)));
+    R[1][1] = ds(1.0, dm(2.0, da(dm(x, x), dm(z, z))));
+    R[1][2] = dm(2.0, ds(dm(y, z), dm(w, x)));
+    R[2][0] = dm(2.0, ds(dm(x, z), dm(w, y)));
+    R[2][1] = dm(2.0, da(dm(y, z), dm(w, x)));
+    R[2][2] = ds(1.0, dm(2.0, da(dm(x, x), dm(y, y))));
+}
+
+// Full fp64 projection of one Gaussian whose camera-space point is known.
+__device__ __forceinline__ void ss_project(const ss_camera& cam, const float* ls, const float* q, bool cutoff, Proj& P) {
+    const double x = P.mc[0], y = P.mc[1], z = P.mc[2];
+    const double fx = cam.fx, fy = cam.fy;
+    const double zz = dm(z, z);
+    P.J[0][0] = dd(fx, z);
+    P.J[0][1] = 0.0;
+    P.J[0][2] = dd(dm(-fx, x), zz);
+    P.J[1][0] = 0.0;
+    P.J[1][1] = dd(fy, z);
+    P.J[1][2] = dd(dm(-fy, y), zz);
+    P.mu[0] = da(dd(dm(fx, x), z), cam.cx);
+    P.mu[1] = da(dd(dm(fy, y), z), cam.cy);
+    ss_quat_rot(q, P.u, &P.qn, P.Rq);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) P.S2[k] = ss_det_exp(dm(2.0, (double)ls[k]));
+    double S3[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            S3[i][j] = da(da(dm(dm(P.Rq[i][0], P.S2[0]), P.Rq[j][0]), dm(dm(P.Rq[i][1], P.S2[1]), P.Rq[j][1])),
+                          dm(dm(P.Rq[i][2], P.S2[2]), P.Rq[j][2]));
+    // W[i][k] = R_cw[k][i]
+    double Tm[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int l = 0; l < 3; ++l)
+            Tm[i][l] = da(da(dm(cam.rot_cw[0 * 3 + i], S3[0][l]), dm(cam.rot_cw[1 * 3 + i], S3[1][l])),
+                          dm(cam.rot_cw[2 * 3 + i], S3[2][l]));
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            P.cov[i][j] = da(da(dm(Tm[i][0], cam.rot_cw[0 * 3 + j]), dm(Tm[i][1], cam.rot_cw[1 * 3 + j])),
+                             dm(Tm[i][2], cam.rot_cw[2 * 3 + j]));
+    double U0[3], U1[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        U0[l] = da(dm(P.J[0][0], P.cov[0][l]), dm(P.J[0][2], P.cov[2][l]));
+        U1[l] = da(dm(P.J[1][1], P.cov[1][l]), dm(P.J[1][2], P.cov[2][l]));
+    }
+    P.s00 = da(da(dm(U0[0], P.J[0][0]), dm(U0[2], P.J[0][2])), SS_BLUR);
+    P.s01 = da(dm(U0[1], P.J[1][1]), dm(U0[2], P.J[1][2]));
+    P.s11 = da(da(dm(U1[1], P.J[1][1]), dm(U1[2], P.J[1][2])), SS_BLUR);
+    P.det = ds(dm(P.s00, P.s11), dm(P.s01, P.s01));
+    if (cutoff) {
+        double tr = da(P.s00, P.s11);
+        double disc = ds(dm(0.25, dm(tr, tr)), P.det);
+        double lam = da(dm(0.5, tr), dsq(disc > 0.0 ? disc : 0.0));
+        P.radius = dm(3.0, dsq(lam));
+    } else {
+        P.radius = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    }
+}
+
+// [x0, x1) x [y0, y1), clipped to the image (render.py:293-301); x0 >= x1 or y0 >= y1 = empty
+__device__ __forceinline__ void ss_window(const Proj& P, int W, int H, int win[4]) {
+    if (isinf(P.radius)) {
+        win[0] = 0; win[1] = W; win[2] = 0; win[3] = H;
+        return;
+    }
+    double lx = floor(ds(P.mu[0], P.radius)), hx = da(ceil(da(P.mu[0], P.radius)), 1.0);
+    double ly = floor(ds(P.mu[1], P.radius)), hy = da(ceil(da(P.mu[1], P.radius)), 1.0);
+    win[0] = (int)fmin(fmax(lx, 0.0), (double)W);
+    win[1] = (int)fmin(fmax(hx, 0.0), (double)W);
+    win[2] = (int)fmin(fmax(ly, 0.0), (double)H);
+    win[3] = (int)fmin(fmax(hy, 0.0), (double)H);
+}
+
+__device__ __forceinline__ int ss_sh_bases(int degree) { return (degree + 1) * (degree + 1); }
+
+__device__ __forceinline__ void ss_sh_eval(const double v[3], int degree, double Y[16]) {
+    Y[0] = SS_SH_C0;
+    if (degree < 1) return;
+    const double x = v[0], y = v[1], z = v[2];
+    Y[1] = -SS_SH_C1 * y;
+    Y[2] = SS_SH_C1 * z;
+    Y[3] = -SS_SH_C1 * x;
+    if (degree < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = 1.0925484306 * (x * y);
+    Y[5] = -1.0925484306 * (y * z);
+    Y[6] = 0.3153915653 * (2 * zz - xx - yy);
+    Y[7] = -1.0925484306 * (x * z);
+    Y[8] = 0.5462742153 * (xx - yy);
+    if (degree < 3) return;
+    Y[9] = -0.5900435899 * y * (3 * xx - yy);
+    Y[10] = 2.8906114426 * (x * y) * z;
+    Y[11] = -0.4570457995 * y * (4 * zz - xx - yy);
+    Y[12] = 0.3731763326 * z * (2 * zz - 3 * xx - 3 * yy);
+    Y[13] = -0.4570457995 * x * (4 * zz - xx - yy);
+    Y[14] = 1.4453057213 * z * (xx - yy);
+    Y[15] = -0.5900435899 * x * (xx - yy - 3 * zz);
+}
+
+// dY_b/dv_k (render.py:93-136)
+__device__ __forceinline__ void ss_sh_grad(const double v[3], int degree, double g[16][3]) {
+#pragma unroll
+    for (int b = 0; b < 16; ++b) g[b][0] = g[b][1] = g[b][2] = 0.0;
+    if (degree < 1) return;
+    const double x = v[0], y = v[1], z = v[2];
+    g[1][1] = -SS_SH_C1;
+    g[2][2] = SS_SH_C1;
+    g[3][0] = -SS_SH_C1;
+    if (degree >= 2) {
+        const double a = 1.0925484306, b = -1.0925484306, c = 0.3153915653, e = -1.0925484306, f = 0.5462742153;
+        g[4][0] = a * y; g[4][1] = a * x;
+        g[5][1] = b * z; g[5][2] = b * y;
+        g[6][0] = c * (-2 * x); g[6][1] = c * (-2 * y); g[6][2] = c * (4 * z);
+        g[7][0] = e * z; g[7][2] = e * x;
+        g[8][0] = f * (2 * x); g[8][1] = f * (-2 * y);
+    }
+    if (degree >= 3) {
+        const double c0 = -0.5900435899, c1 = 2.8906114426, c2 = -0.4570457995, c3 = 0.3731763326,
+                     c4 = -0.4570457995, c5 = 1.4453057213, c6 = -0.5900435899;
+        g[9][0] = c0 * 6 * x * y; g[9][1] = c0 * (3 * x * x - 3 * y * y);
+        g[10][0] = c1 * y * z; g[10][1] = c1 * x * z; g[10][2] = c1 * x * y;
+        g[11][0] = c2 * (-2 * x * y); g[11][1] = c2 * (4 * z * z - x * x - 3 * y * y); g[11][2] = c2 * (8 * y * z);
+        g[12][0] = c3 * (-6 * x * z); g[12][1] = c3 * (-6 * y * z); g[12][2] = c3 * (6 * z * z - 3 * x * x - 3 * y * y);
+        g[13][0] = c4 * (4 * z * z - 3 * x * x - y * y); g[13][1] = c4 * (-2 * x * y); g[13][2] = c4 * (8 * x * z);
+        g[14][0] = c5 * (2 * x * z); g[14][1] = c5 * (-2 * y * z); g[14][2] = c5 * (x * x - y * y);
+        g[15][0] = c6 * (3 * x * x - y * y - 3 * z * z); g[15][1] = c6 * (-2 * x * y); g[15][2] = c6 * (-6 * x * z);
+    }
+}
+
+struct Shade {
+    double vdir[3], dist;
+    double Y[16];
+    int axis;          // normal-proxy axis
+    double s, cosv;    // signed / absolute cosine
+    double albedo[3];
+    double vis;
+    double pre[3];     // colour before the [0,1] clamp
+};
+
+// ref render.py:175-197 and the normal proxy of render.py:139-151
+__device__ __forceinline__ void ss_shade(const ss_light& L, const float* ls, const float* sh, int B, int degree,
+                                         float visf, const double d[3], const double Rq[3][3], Shade& S) {
+    S.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    S.vdir[0] = d[0] / S.dist;
+    S.vdir[1] = d[1] / S.dist;
+    S.vdir[2] = d[2] / S.dist;
+    double l0 = ls[0], l1 = ls[1], l2 = ls[2];
+    double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
+    S.axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
+    const int k = S.axis;
+    S.s = Rq[0][k] * -L.direction[0] + Rq[1][k] * -L.direction[1] + Rq[2][k] * -L.direction[2];
+    S.cosv = fabs(S.s);
+    S.vis = visf;
+    ss_sh_eval(S.vdir, degree, S.Y);
+    for (int c = 0; c < 3; ++c) {
+        const float* shc = sh + c * B;
+        S.albedo[c] = SS_SH_C0 * shc[0] + 0.5;
+        double direct = S.albedo[c] * L.intensity[c] * (S.cosv * S.vis);
+        double base = 0.0;
+        if (L.ambient_bands == 0) {
+            for (int b = 0; b < B; ++b) base += shc[b] * S.Y[b];
+            base += 0.5;
+        } else {
+            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+            for (int b = 0; b < BL; ++b) {
+                double e = shc[b];
+                if (b == 0) e += 0.5 / SS_SH_C0;
+                base += e * L.ambient[c * L.ambient_bands + b];
+            }
+            double vd = 0.0;
+            for (int b = 1; b < B; ++b) vd += shc[b] * S.Y[b];
+            base += vd;
+        }
+        S.pre[c] = base + direct;
+    }
+}

@@ -1,0 +1,257 @@
+"""Wire encoders on the GPU: drop-in for the hot part of ref
+pkg/src/splatstream/protocol/ (delta.py:72 encode_delta, snapshot.py:47
+encode_snapshot, packets.py:73 encode_light_visibility).
+
+The payload bytes are produced by bit-exact CUDA kernels (csrc/ss_codec.cu)
+in the raw form (compression_id 0).  compression_id 1 runs the reference's
+compression stage -- zlib level 6 -- on the host via the library's libz
+wrapper, byte-identical to `zlib.compress(block, 6)`.  The `*_device`
+variants keep payloads, lengths and baselines in HBM with no host
+synchronisation (the throughput path).
+
+The envelope (`frame_bytes`, CRC32) and the constants follow
+protocol/framing.py and protocol/profiles.py.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+import zlib
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+from .. import _lib
+from ..errors import ProtocolError
+from ..model import as_device
+
+MAGIC = b"GS"
+MAX_PAYLOAD = 1 << 28
+MAX_ROWS = 1 << 24
+COMPRESSION_NONE = 0
+COMPRESSION_ZLIB = 1
+
+
+class PacketType(IntEnum):
+    OBJECT_ID_MAP = 0x01
+    OBJECT_TRANSFORMS = 0x02
+    MODEL_SNAPSHOT = 0x03
+    TENSOR_METADATA = 0x04
+    TENSOR_DELTA = 0x05
+    LIGHT_VISIBILITY = 0x06
+    GAUSSIAN_ID_ORDERING = 0x07
+    LIGHT_STATE = 0x08
+    CAMERA_POSE = 0x09
+
+
+class AttributeId(IntEnum):
+    MEANS = 0
+    LOG_SCALES = 1
+    QUATERNIONS = 2
+    LOGIT_OPACITIES = 3
+    SH_DC = 4
+    SH_REST = 5
+    LIGHT_VISIBILITY = 6
+
+
+@dataclass(frozen=True)
+class QuantizationProfile:
+    profile_id: int
+    compression_id: int = COMPRESSION_ZLIB
+
+
+PROFILE_DEFAULT = QuantizationProfile(0)
+PROFILE_LOSSLESS = QuantizationProfile(1)
+ATTRIBUTE_QUANTIZERS = {
+    AttributeId.MEANS: (16, None, None),
+    AttributeId.LOG_SCALES: (8, -10.0, 2.0),
+    AttributeId.QUATERNIONS: (10, -1.0, 1.0),
+    AttributeId.LOGIT_OPACITIES: (8, -8.0, 8.0),
+    AttributeId.SH_DC: (8, -4.0, 4.0),
+    AttributeId.SH_REST: (8, -1.0, 1.0),
+    AttributeId.LIGHT_VISIBILITY: (1, 0.0, 1.0),
+}
+RESIDUAL_ATTRIBUTES = frozenset({AttributeId.MEANS, AttributeId.LOG_SCALES})
+DEFAULT_GATING = {AttributeId.MEANS: 1e-3, AttributeId.LOG_SCALES: 1e-3}
+
+
+def frame_bytes(ptype: int, epoch: int, payload: bytes) -> bytes:
+    """ref protocol/framing.py:51-53."""
+    body = struct.pack("<BII", int(ptype), epoch, len(payload)) + payload
+    return MAGIC + body + struct.pack("<I", zlib.crc32(body))
+
+
+def host_zlib(block: bytes) -> bytes:
+    """The compression stage through the library's libz (compress2, level 6)."""
+    lib = _lib.load_library()
+    n = len(block)
+    cap = int(lib.ss_host_zlib_bound(n))
+    dst = (C.c_uint8 * cap)()
+    out = _lib.u64(0)
+    src = (C.c_uint8 * max(n, 1)).from_buffer_copy(block if n else b"\0")
+    if lib.ss_host_zlib_compress(src, n, dst, cap, C.byref(out)) != 0:
+        raise RuntimeError("zlib compress2 failed")
+    return bytes(dst[: out.value])
+
+
+def _recompress_delta(raw: bytes, compression_id: int) -> bytes:
+    if compression_id == COMPRESSION_NONE:
+        return raw
+    if compression_id != COMPRESSION_ZLIB:
+        raise ProtocolError(f"unknown compression id {compression_id}")
+    mode = raw[1]
+    head = 8 + (12 if mode == 1 else 8 if mode == 0 else 0)
+    (blen,) = struct.unpack_from("<I", raw, head)
+    block = host_zlib(raw[head + 4: head + 4 + blen])
+    hdr = bytearray(raw[:head])
+    hdr[2] = COMPRESSION_ZLIB
+    return bytes(hdr) + struct.pack("<I", len(block)) + block
+
+
+def _recompress_snapshot(raw: bytes, compression_id: int) -> bytes:
+    if compression_id == COMPRESSION_NONE:
+        return raw
+    if compression_id != COMPRESSION_ZLIB:
+        raise ProtocolError(f"unknown compression id {compression_id}")
+    (blen,) = struct.unpack_from("<I", raw, 36)
+    block = host_zlib(raw[40:40 + blen])
+    hdr = bytearray(raw[:36])
+    hdr[10] = COMPRESSION_ZLIB
+    return bytes(hdr) + struct.pack("<I", len(block)) + block
+
+
+class PayloadBuffer:
+    """Device output buffer + device length word, reused across calls."""
+
+    def __init__(self, capacity: int, device):
+        import torch
+        self.data = torch.empty(max(int(capacity), 64), dtype=torch.uint8, device=device)
+        self.length = torch.zeros(1, dtype=torch.int64, device=device)
+
+    def ensure(self, capacity: int):
+        import torch
+        if self.data.numel() < capacity:
+            self.data = torch.empty(int(capacity * 1.25) + 64, dtype=torch.uint8, device=self.data.device)
+
+    def to_bytes(self) -> bytes:
+        n = int(self.length.item())
+        return self.data[:n].cpu().numpy().tobytes()
+
+
+def _dims_of(shape):
+    return 1 if len(shape) == 1 else int(np.prod(shape[1:]))
+
+
+def encode_delta_device(attribute_id, current, baseline=None, new_baseline=None, gating_threshold=None,
+                        out: PayloadBuffer = None):
+    """Raw (compression 0) delta payload into `out` (device), no host sync.
+    current/baseline: torch CUDA float32/float64 tensors, (rows, ...)."""
+    import torch
+    attr = AttributeId(attribute_id)
+    rows = int(current.shape[0])
+    dims = _dims_of(tuple(current.shape))
+    c = _lib.ctx(current.device.index)
+    cur = current.contiguous()
+    dt = 1 if cur.dtype == torch.float64 else 0
+    if cur.dtype not in (torch.float32, torch.float64):
+        cur = cur.float()
+        dt = 0
+    base = None
+    if attr in RESIDUAL_ATTRIBUTES:
+        if baseline is None:
+            raise ValueError(f"{attr.name} is residual-coded and needs a baseline")
+        if tuple(baseline.shape[:1]) != (rows,) or _dims_of(tuple(baseline.shape)) != dims:
+            raise ValueError("baseline shape mismatch")
+        base = baseline.contiguous().to(cur.dtype)
+    gate = DEFAULT_GATING.get(attr, 0.0) if gating_threshold is None else float(gating_threshold)
+    bound = int(c.lib.ss_delta_bound(int(attr), rows, dims))
+    if out is None:
+        out = PayloadBuffer(bound, current.device)
+    out.ensure(bound)
+    c.check(c.lib.ss_encode_delta(c.handle, int(attr), _lib.ptr(cur), dt, _lib.ptr(base), _lib.ptr(new_baseline),
+                                  rows, dims, gate, _lib.ptr(out.data), out.data.numel(), _lib.ptr(out.length)))
+    return out
+
+
+def encode_delta(attribute_id, current, baseline=None, gating_threshold=None, compression_id: int = COMPRESSION_ZLIB):
+    """ref protocol/delta.py:72 -- returns (payload bytes, new baseline or None).
+
+    Host arrays are uploaded; float32 and float64 inputs are both encoded
+    exactly (a float64 residual of float32 values is computed in float64 either
+    way).  For CUDA tensor inputs the new baseline is returned as a tensor."""
+    import torch
+    attr = AttributeId(attribute_id)
+    dev = current.device if isinstance(current, torch.Tensor) and current.is_cuda else \
+        torch.device("cuda", torch.cuda.current_device())
+
+    def to_dev(x):
+        if isinstance(x, torch.Tensor):
+            return x.to(dev)
+        a = np.asarray(x)
+        return torch.from_numpy(np.ascontiguousarray(a, np.float32 if a.dtype == np.float32 else np.float64)).to(dev)
+
+    cur = to_dev(current)
+    base = new_base = None
+    if attr in RESIDUAL_ATTRIBUTES:
+        if baseline is None:
+            raise ValueError(f"{attr.name} is residual-coded and needs a baseline")
+        base = to_dev(baseline)
+        if base.shape[0] != cur.shape[0] or base.numel() != cur.numel():
+            raise ValueError("baseline shape mismatch")
+        if torch.float64 in (cur.dtype, base.dtype):
+            cur, base = cur.double(), base.double()
+        new_base = torch.empty(tuple(base.shape), dtype=torch.float32, device=dev)
+    out = encode_delta_device(attr, cur, base, new_base, gating_threshold)
+    payload = _recompress_delta(out.to_bytes(), compression_id)
+    if new_base is None:
+        return payload, None
+    if isinstance(baseline, torch.Tensor):
+        return payload, new_base
+    return payload, new_base.cpu().numpy().reshape(np.asarray(baseline).shape)
+
+
+def encode_snapshot_device(model, profile_id: int, out: PayloadBuffer = None, base_means=None, base_log_scales=None):
+    """Raw snapshot payload into `out` (device) plus the decoded means/log
+    scales (server baseline reset, ref server.py:481-484), no host sync."""
+    dm, _ = as_device(model)
+    c = _lib.ctx(dm.device.index)
+    bound = int(c.lib.ss_snapshot_bound(dm.count, dm.sh_degree, int(profile_id)))
+    if out is None:
+        out = PayloadBuffer(bound, dm.device)
+    out.ensure(bound)
+    c.check(c.lib.ss_encode_snapshot(c.handle, dm.struct(), int(profile_id), _lib.ptr(out.data), out.data.numel(),
+                                     _lib.ptr(out.length), _lib.ptr(base_means), _lib.ptr(base_log_scales)))
+    return out
+
+
+def encode_snapshot(model, profile: QuantizationProfile = PROFILE_DEFAULT, return_baselines: bool = False):
+    """ref protocol/snapshot.py:47 -- payload bytes [, (base_means, base_log_scales)]."""
+    import torch
+    dm, _ = as_device(model)
+    bm = torch.empty((dm.count, 3), dtype=torch.float32, device=dm.device) if return_baselines else None
+    bl = torch.empty((dm.count, 3), dtype=torch.float32, device=dm.device) if return_baselines else None
+    out = encode_snapshot_device(dm, profile.profile_id, None, bm, bl)
+    payload = _recompress_snapshot(out.to_bytes(), profile.compression_id)
+    if return_baselines:
+        return payload, (bm.cpu().numpy(), bl.cpu().numpy())
+    return payload
+
+
+def encode_light_visibility(visibility) -> bytes:
+    """ref protocol/packets.py:73-76."""
+    import torch
+    if isinstance(visibility, torch.Tensor) and visibility.is_cuda:
+        v = visibility.float().contiguous()
+    else:
+        v = torch.from_numpy(np.ascontiguousarray(np.asarray(visibility), np.float32)).cuda()
+    c = _lib.ctx(v.device.index)
+    n = v.numel()
+    out = PayloadBuffer(4 + (n + 7) // 8, v.device)
+    c.check(c.lib.ss_encode_light_visibility(c.handle, _lib.ptr(v), n, _lib.ptr(out.data), out.data.numel(),
+                                             _lib.ptr(out.length)))
+    return out.to_bytes()
+
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,225 @@
+"""Forward renderer API on the B200 rasterizer.
+
+Drop-in for ref pkg/src/splatstream/render.py: LightState (render.py:34),
+flat_ambient_sh (render.py:51), prepare_splats (render.py:226), render
+(render.py:339), update_light_visibility (render.py:350).  The compute runs in
+libsplat_b200.so (K1-K5, see csrc/ss_raster.cu); this module only marshals
+arguments.  `precision=1` selects the fp64 blend instantiation used for
+verbatim parity; the default fp32 blend is the throughput path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .geometry import quat_to_rotmat
+from .model import DeviceModel, as_device
+
+SH_C0 = 0.2820947918
+TRANSMITTANCE_CUTOFF = 1e-4
+ALPHA_CAP = 0.999
+COV2D_BLUR = 0.3
+
+
+@dataclass
+class LightState:
+    direction: np.ndarray
+    intensity: np.ndarray
+    ambient_sh: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        d = np.asarray(self.direction, dtype=np.float64)
+        self.direction = d / np.linalg.norm(d)
+        self.intensity = np.asarray(self.intensity, dtype=np.float64)
+        if self.ambient_sh is not None:
+            self.ambient_sh = np.asarray(self.ambient_sh, dtype=np.float64)
+
+
+def flat_ambient_sh(ambient_rgb) -> np.ndarray:
+    return (SH_C0 * np.asarray(ambient_rgb, np.float64))[:, None]
+
+
+def camera_struct(pose, intr) -> _lib.SSCamera:
+    c = _lib.SSCamera()
+    c.position = _lib.f64arr(pose.position, 3)
+    R = pose.rotation() if hasattr(pose, "rotation") else quat_to_rotmat(pose.quaternion)
+    c.rot_cw = _lib.f64arr(np.asarray(R, np.float64).ravel(), 9)
+    fy = (intr.height / 2.0) / np.tan(intr.fov_y / 2.0)
+    c.fx, c.fy = float(fy), float(fy)
+    c.cx, c.cy = intr.width / 2.0, intr.height / 2.0
+    c.near_plane = float(intr.near)
+    c.width, c.height = int(intr.width), int(intr.height)
+    return c
+
+
+def light_struct(light) -> _lib.SSLight:
+    s = _lib.SSLight()
+    s.direction = _lib.f64arr(light.direction, 3)
+    s.intensity = _lib.f64arr(light.intensity, 3)
+    amb = getattr(light, "ambient_sh", None)
+    if amb is None:
+        s.ambient_bands = 0
+    else:
+        amb = np.asarray(amb, np.float64)
+        if amb.ndim != 2 or amb.shape[0] != 3 or amb.shape[1] > 16:
+            raise ValueError("ambient SH must be (3, bands<=16)")
+        s.ambient_bands = amb.shape[1]
+        s.ambient = _lib.f64arr(amb.ravel(), 48)
+    return s
+
+
+def _subset_tensor(index_subset, device):
+    if index_subset is None:
+        return None
+    import torch
+    idx = np.sort(np.asarray(index_subset, np.int64).ravel())  # composite ties break by row (render.py:283)
+    return torch.from_numpy(idx).to(device)
+
+
+def render_opts(background, subset, extent_cutoff, precision, deterministic=1) -> _lib.SSRenderOpts:
+    o = _lib.SSRenderOpts()
+    o.background = _lib.f64arr(background, 3)
+    o.subset = subset.data_ptr() if subset is not None else None
+    o.subset_count = int(subset.numel()) if subset is not None else 0
+    o.extent_cutoff = 1 if extent_cutoff else 0
+    o.precision = int(precision)
+    o.deterministic = int(deterministic)
+    return o
+
+
+def render_device(model: DeviceModel, pose, intr, light_state, index_subset=None, background=(0.0, 0.0, 0.0),
+                  return_transmittance=False, extent_cutoff=True, precision=0, out=None):
+    """render() with the image left in HBM: returns a torch (H,W,3) tensor
+    (float32, or float64 for precision=1) [and T (H,W)]."""
+    import torch
+    c = _lib.ctx(model.device.index)
+    dt = torch.float64 if precision else torch.float32
+    H, W = intr.height, intr.width
+    img = out if out is not None else torch.empty((H, W, 3), dtype=dt, device=model.device)
+    T = torch.empty((H, W), dtype=dt, device=model.device) if return_transmittance else None
+    sub = _subset_tensor(index_subset, model.device)
+    m = model.struct()
+    cam = camera_struct(pose, intr)
+    L = light_struct(light_state)
+    o = render_opts(background, sub, extent_cutoff, precision)
+    st = _lib.SSRenderStats()
+    c.check(c.lib.ss_render(c.handle, m, cam, L, o, _lib.ptr(img), _lib.ptr(T), st))
+    return (img, T) if return_transmittance else img
+
+
+def render(model, pose, intr, light_state, index_subset=None, background=(0.0, 0.0, 0.0),
+           return_transmittance: bool = False, extent_cutoff: bool = True, precision: int = 0):
+    """ref render.py:339 -- returns a float64 numpy image [, T]."""
+    dm, _ = as_device(model)
+    r = render_device(dm, pose, intr, light_state, index_subset, background, return_transmittance, extent_cutoff,
+                      precision)
+    if return_transmittance:
+        return r[0].double().cpu().numpy(), r[1].double().cpu().numpy()
+    return r.double().cpu().numpy()
+
+
+@dataclass
+class PreparedSplats:
+    """Host view of the per-splat preprocess (ref render.py:200-223 field names)."""
+
+    rows: np.ndarray
+    depth: np.ndarray
+    mu2d: np.ndarray
+    Sigma2d: np.ndarray
+    inv2d: np.ndarray
+    opacity: np.ndarray
+    color: np.ndarray
+    color_pre: np.ndarray
+    order: np.ndarray
+    radius: np.ndarray
+    windows: np.ndarray
+    shade_inter: dict = field(default_factory=dict)
+
+
+def prepare_splats(model, pose, intr, light_state, index_subset=None, extent_cutoff: bool = True) -> PreparedSplats:
+    """ref render.py:226 -- computed by the fp64 preprocess kernel (K1) and the
+    depth sort (K3a); returned as host arrays for inspection."""
+    import torch
+    dm, _ = as_device(model)
+    c = _lib.ctx(dm.device.index)
+    dev = dm.device
+    sub = _subset_tensor(index_subset, dev)
+    n = int(sub.numel()) if sub is not None else dm.count
+    cap = max(n, 1)
+    buf = dict(rows=torch.empty(cap, dtype=torch.int64, device=dev),
+               depth=torch.empty(cap, dtype=torch.float64, device=dev),
+               mu2d=torch.empty((cap, 2), dtype=torch.float64, device=dev),
+               sigma2d=torch.empty((cap, 3), dtype=torch.float64, device=dev),
+               radius=torch.empty(cap, dtype=torch.float64, device=dev),
+               window=torch.empty((cap, 4), dtype=torch.int32, device=dev),
+               opacity=torch.empty(cap, dtype=torch.float64, device=dev),
+               color=torch.empty((cap, 3), dtype=torch.float64, device=dev),
+               color_pre=torch.empty((cap, 3), dtype=torch.float64, device=dev),
+               shade_s=torch.empty(cap, dtype=torch.float64, device=dev),
+               order=torch.empty(cap, dtype=torch.int64, device=dev))
+    p = _lib.SSPrepared()
+    for k, t in buf.items():
+        setattr(p, k, t.data_ptr())
+    p.capacity = cap
+    vis = _lib.i64(0)
+    c.check(c.lib.ss_prepare_splats(c.handle, dm.struct(), camera_struct(pose, intr), light_struct(light_state),
+                                    render_opts((0, 0, 0), sub, extent_cutoff, 1), p, _lib.C.byref(vis)))
+    M = int(vis.value)
+    h = {k: t[:M].cpu().numpy() for k, t in buf.items()}
+    s = h["sigma2d"]
+    Sig = np.stack([np.stack([s[:, 0], s[:, 1]], -1), np.stack([s[:, 1], s[:, 2]], -1)], -2)
+    det = s[:, 0] * s[:, 2] - s[:, 1] * s[:, 1]
+    inv = np.stack([np.stack([s[:, 2] / det, -s[:, 1] / det], -1), np.stack([-s[:, 1] / det, s[:, 0] / det], -1)], -2)
+    return PreparedSplats(rows=h["rows"], depth=h["depth"], mu2d=h["mu2d"], Sigma2d=Sig, inv2d=inv,
+                          opacity=h["opacity"], color=h["color"], color_pre=h["color_pre"], order=h["order"],
+                          radius=h["radius"], windows=h["window"].astype(np.int64), shade_inter={"s": h["shade_s"]})
+
+
+def tile_bins(model, pose, intr, index_subset=None, extent_cutoff=True):
+    """Sort keys / tile ranges of K2-K4 for parity tests: returns
+    (order_rows, ranges (T,2), pair_rank (P,))."""
+    import torch
+    dm, _ = as_device(model)
+    c = _lib.ctx(dm.device.index)
+    dev = dm.device
+    sub = _subset_tensor(index_subset, dev)
+    n = int(sub.numel()) if sub is not None else dm.count
+    tiles = -(-intr.width // 16) * -(-intr.height // 16)
+    o = render_opts((0, 0, 0), sub, extent_cutoff, 0)
+    st = _lib.SSRenderStats()
+    # first pass sizes the pair list
+    c.check(c.lib.ss_debug_bins(c.handle, dm.struct(), camera_struct(pose, intr), o, None, max(n, 1), None, tiles,
+                                None, 1 << 62, st))
+    P = int(st.pairs)
+    rows = torch.full((max(n, 1),), -1, dtype=torch.int64, device=dev)
+    ranges = torch.zeros((tiles, 2), dtype=torch.int64, device=dev)
+    ranks = torch.zeros(max(P, 1), dtype=torch.int64, device=dev)
+    c.check(c.lib.ss_debug_bins(c.handle, dm.struct(), camera_struct(pose, intr), o, _lib.ptr(rows), max(n, 1),
+                                _lib.ptr(ranges), tiles, _lib.ptr(ranks), max(P, 1), st))
+    r = rows.cpu().numpy()[:n]
+    return r[r >= 0], ranges.cpu().numpy(), ranks.cpu().numpy()[:P]
+
+
+def update_light_visibility(model, depth_map, light_cam, bias: float = 0.02) -> None:
+    """ref render.py:350 -- writes model.light_visibility (replaced for host models)."""
+    import torch
+    dm, uploaded = as_device(model)
+    if dm.count == 0:
+        return
+    c = _lib.ctx(dm.device.index)
+    cam = _lib.SSOrthoCamera()
+    cam.position = _lib.f64arr(light_cam.pose.position, 3)
+    R = light_cam.pose.rotation() if hasattr(light_cam.pose, "rotation") else quat_to_rotmat(light_cam.pose.quaternion)
+    cam.rot_cw = _lib.f64arr(np.asarray(R).ravel(), 9)
+    cam.half_width, cam.half_height = float(light_cam.half_width), float(light_cam.half_height)
+    cam.width, cam.height = int(light_cam.width), int(light_cam.height)
+    depth = depth_map if isinstance(depth_map, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(depth_map, np.float64))
+    depth = depth.to(dm.device, torch.float64).contiguous()
+    c.check(c.lib.ss_update_light_visibility(c.handle, dm.struct(), _lib.ptr(depth), cam, float(bias)))
+    if uploaded:
+        model.light_visibility = dm.light_visibility.cpu().numpy().astype(np.float32)

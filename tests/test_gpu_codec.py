@@ -1,0 +1,109 @@
+"""GPU encoders vs the reference's bytes (golden vectors) -- bit-exact."""
+
+import numpy as np
+import pytest
+
+from conftest import case_model, load_cases
+from gpu_util import require_gpu
+
+pytestmark = pytest.mark.gpu
+
+DELTAS = [c for c in load_cases("codec_cases") if c["kind"] == "delta"]
+SNAPS = [c for c in load_cases("codec_cases") if c["kind"] == "snapshot"]
+
+
+@pytest.mark.parametrize("c", DELTAS, ids=[c["name"] for c in DELTAS])
+def test_gpu_delta_bit_exact(c):
+    require_gpu()
+    from paper_2604_02851_b200.protocol import encode_delta
+    base = c.a("base") if c.has("base") else None
+    for comp in (0, 1):
+        got, nb = encode_delta(c["attr"], c.a("cur"), base, c["gate"], comp)
+        assert got == c.a(f"payload{comp}").tobytes(), comp
+        if base is not None:
+            assert nb.dtype == np.float32
+            np.testing.assert_array_equal(nb, c.a("new_base"))
+
+
+@pytest.mark.parametrize("c", SNAPS, ids=[c["name"] for c in SNAPS])
+def test_gpu_snapshot_bit_exact(c):
+    require_gpu()
+    from paper_2604_02851_b200.model import GaussianModel
+    from paper_2604_02851_b200.protocol import QuantizationProfile, encode_snapshot
+    m = case_model(c)
+    model = GaussianModel(m.means, m.log_scales, m.quaternions, m.logit_opacities, m.sh_coeffs,
+                          m.light_visibility, m.object_ids, m.active_count, m.sh_degree)
+    for prof in (0, 1):
+        for comp in (0, 1):
+            got, (bm, bl) = encode_snapshot(model, QuantizationProfile(prof, comp), return_baselines=True)
+            assert got == c.a(f"payload_p{prof}c{comp}").tobytes(), (prof, comp)
+            if prof == 0 and c.has("dec_means"):
+                np.testing.assert_array_equal(bm, c.a("dec_means"))
+                np.testing.assert_array_equal(bl, c.a("dec_log_scales"))
+            if prof == 1:
+                np.testing.assert_array_equal(bm, m.means)
+
+
+def test_gpu_delta_dual_ledger_random_walk():
+    """ref pkg/tests/test_protocol.py:360-392 restated: the GPU encoder's
+    baseline equals the oracle's bit for bit over 50 ticks."""
+    require_gpu()
+    from oracle import codec as oc
+    from paper_2604_02851_b200.protocol import encode_delta
+    rng = np.random.default_rng(15)
+    n = 600
+    cur = rng.uniform(-3, 3, (n, 3)).astype(np.float32)
+    base_gpu = cur.copy()
+    base_ref = cur.copy()
+    for tick in range(50):
+        moved = rng.random(n) < (0.3 if tick % 7 else 0.9)
+        cur[moved] += rng.normal(0, 0.01, (int(moved.sum()), 3)).astype(np.float32)
+        p_gpu, base_gpu = encode_delta(0, cur, base_gpu, 1e-3, 0)
+        p_ref, base_ref = oc.delta_payload(0, cur, base_ref, 1e-3, 0)
+        assert p_gpu == p_ref
+        np.testing.assert_array_equal(base_gpu, base_ref)
+
+
+def test_gpu_large_delta_and_snapshot_match_oracle():
+    """Sizes beyond the fixtures: 300k rows, both residual modes, all attributes."""
+    require_gpu()
+    from oracle import codec as oc
+    from paper_2604_02851_b200.model import GaussianModel
+    from paper_2604_02851_b200.protocol import QuantizationProfile, encode_delta, encode_snapshot
+    rng = np.random.default_rng(5)
+    n = 300_000
+    base = rng.uniform(-4, 4, (n, 3)).astype(np.float32)
+    for frac in (0.2, 0.9):
+        cur = base.copy()
+        mv = rng.random(n) < frac
+        cur[mv] += rng.normal(0, 0.02, (int(mv.sum()), 3)).astype(np.float32)
+        for attr in (0, 1):
+            g, gb = encode_delta(attr, cur, base, None, 0)
+            r, rb = oc.delta_payload(attr, cur, base, None, 0)
+            assert g == r
+            np.testing.assert_array_equal(gb, rb)
+    sh = rng.uniform(-1.2, 1.2, (n, 3, 16)).astype(np.float32)
+    for attr, x in ((2, rng.normal(0, 0.5, (n, 4)).astype(np.float32)), (3, rng.uniform(-9, 9, n).astype(np.float32)),
+                    (4, sh[:, :, 0]), (5, sh[:, :, 1:]), (6, rng.random(n).astype(np.float32))):
+        assert encode_delta(attr, x, None, None, 0)[0] == oc.delta_payload(attr, x, None, None, 0)[0]
+    q = rng.normal(size=(n, 4))
+    model = GaussianModel(base, rng.uniform(-6, 1, (n, 3)).astype(np.float32),
+                          (q / np.linalg.norm(q, axis=1, keepdims=True)).astype(np.float32),
+                          rng.uniform(-6, 6, n).astype(np.float32), sh, (rng.random(n) > 0.5).astype(np.float32),
+                          rng.integers(0, 300, n).astype(np.int32), n - 1000, 3)
+    for prof in (0, 1):
+        g = encode_snapshot(model, QuantizationProfile(prof, 0))
+        r = oc.snapshot_payload(model.means, model.log_scales, model.quaternions, model.logit_opacities,
+                                model.sh_coeffs, model.light_visibility, model.object_ids, model.active_count, 3,
+                                prof, 0)
+        assert g == r
+
+
+def test_gpu_light_visibility_packet():
+    require_gpu()
+    from oracle import codec as oc
+    from paper_2604_02851_b200.protocol import encode_light_visibility
+    rng = np.random.default_rng(2)
+    for n in (0, 1, 10, 33, 1000, 12345):
+        v = rng.random(n).astype(np.float32)
+        assert encode_light_visibility(v) == oc.light_visibility_payload(v)

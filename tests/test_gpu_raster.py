@@ -1,0 +1,136 @@
+"""GPU rasterizer vs the oracle and the reference's golden vectors.
+
+Bit-exact: depth order, pixel windows, tile lists / tile ranges (vs oracle,
+which mirrors the kernel's fp64 op order), and the reference's own windows /
+order.  Tolerances (stated per SURVEY.md §8c):
+  fp64 blend (precision=1): image |d| <= 1e-10; gradients within 2e-6 of the
+      largest entry per group (the gradient buffer is float32).
+  fp32 blend (precision=0): image max|d| <= 1e-4, mean|d| <= 1e-6; gradients
+      normwise ||d||/||g|| <= 1e-4 and max|d| <= 1e-4 * max|g| per group.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_cases
+from gpu_util import oracle_args, product_args, require_gpu
+from oracle import raster as orr
+
+pytestmark = pytest.mark.gpu
+
+RASTER = load_cases("raster_cases")
+GROUPS = ("means", "log_scales", "quaternions", "logit_opacities", "sh_coeffs")
+
+
+def _subset(c):
+    return c.a("subset") if c.has("subset") else None
+
+
+@pytest.mark.parametrize("c", RASTER, ids=[c["name"] for c in RASTER])
+def test_gpu_prepare_matches_reference_and_oracle(c):
+    require_gpu()
+    from paper_2604_02851_b200.render import prepare_splats
+    model, pose, intr, light = product_args(c)
+    p = prepare_splats(model, pose, intr, light, _subset(c), c["cutoff"])
+    np.testing.assert_array_equal(p.rows, c.a("rows"))
+    np.testing.assert_array_equal(p.order, c.a("order"))
+    np.testing.assert_array_equal(p.windows, c.a("windows"))
+    om, cam, ol = oracle_args(c, pose, intr)
+    o = orr.prepare(om, cam, ol, _subset(c), c["cutoff"])
+    np.testing.assert_array_equal(p.depth, o["depth"])           # bit-exact vs oracle
+    np.testing.assert_array_equal(p.windows, o["rect"])
+    np.testing.assert_array_equal(p.radius, o["radius"])
+    np.testing.assert_array_equal(p.mu2d, o["mu2d"])
+    np.testing.assert_array_equal(p.Sigma2d, o["Sigma2d"])
+    np.testing.assert_allclose(p.color_pre, c.a("color_pre"), rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(p.opacity, c.a("opacity"), rtol=1e-14)
+    np.testing.assert_allclose(p.shade_inter["s"], c.a("s"), rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("c", RASTER, ids=[c["name"] for c in RASTER])
+def test_gpu_tile_bins_bit_exact(c):
+    require_gpu()
+    from paper_2604_02851_b200.render import tile_bins
+    model, pose, intr, light = product_args(c)
+    rows, ranges, ranks = tile_bins(model, pose, intr, _subset(c), c["cutoff"])
+    om, cam, ol = oracle_args(c, pose, intr)
+    o = orr.tile_bins(orr.prepare(om, cam, ol, _subset(c), c["cutoff"]), c["W"], c["H"])
+    np.testing.assert_array_equal(rows, o["order_rows"])
+    np.testing.assert_array_equal(ranges, o["ranges"])
+    np.testing.assert_array_equal(ranks, o["pair_rank"])
+
+
+@pytest.mark.parametrize("c", RASTER, ids=[c["name"] for c in RASTER])
+@pytest.mark.parametrize("precision", [1, 0])
+def test_gpu_render(c, precision):
+    require_gpu()
+    from paper_2604_02851_b200.render import render
+    model, pose, intr, light = product_args(c)
+    img, T = render(model, pose, intr, light, _subset(c), c.a("bg"), True, c["cutoff"], precision)
+    d = np.abs(img - c.a("image"))
+    dT = np.abs(T - c.a("T"))
+    if precision == 1:
+        assert d.max(initial=0) <= 1e-10 and dT.max(initial=0) <= 1e-10
+    else:
+        assert d.max(initial=0) <= 1e-4 and d.mean() <= 1e-6, (d.max(), d.mean())
+        assert dT.max(initial=0) <= 1e-4
+
+
+@pytest.mark.parametrize("c", RASTER, ids=[c["name"] for c in RASTER])
+@pytest.mark.parametrize("precision", [1, 0])
+def test_gpu_backward(c, precision):
+    require_gpu()
+    from paper_2604_02851_b200.optim import ReferenceView, backward
+    model, pose, intr, light = product_args(c)
+    view = ReferenceView(pose, intr, c.a("gt"), light, c.a("bg"))
+    L, g, img = backward(model, view, _subset(c), c["cutoff"], precision)
+    tol = 1e-10 if precision else 1e-4
+    assert np.abs(img - c.a("image")).max(initial=0) <= tol
+    assert abs(L - c["loss"]) <= (1e-12 if precision else 1e-6)
+    for name in GROUPS:
+        ref = c.a(f"g_{name}")
+        got = getattr(g, name)
+        assert got.shape == ref.shape, name
+        scale = np.abs(ref).max(initial=0.0)
+        err = np.abs(got - ref)
+        if scale == 0:
+            assert err.max(initial=0) == 0, name
+            continue
+        if precision:
+            assert err.max() <= 2e-6 * scale, (name, err.max() / scale)
+        else:
+            assert np.linalg.norm(err) <= 1e-4 * np.linalg.norm(ref), (name, np.linalg.norm(err) / np.linalg.norm(ref))
+            assert err.max() <= 1e-4 * scale, (name, err.max() / scale)
+
+
+def test_gpu_capped_alpha_and_behind_camera_exact_zeros():
+    """ref pkg/tests/test_optim.py:173-228: masked paths are exact zeros."""
+    require_gpu()
+    from paper_2604_02851_b200.optim import ReferenceView, backward
+    c = [c for c in RASTER if c["name"] == "capped"][0]
+    model, pose, intr, light = product_args(c)
+    view = ReferenceView(pose, intr, c.a("gt"), light, c.a("bg"))
+    for prec in (0, 1):
+        _, g, _ = backward(model, view, None, True, prec)
+        ref = c.a("g_log_scales")
+        np.testing.assert_array_equal(g.log_scales[ref == 0.0], 0.0)
+    c = [c for c in RASTER if c["name"] == "frozen_tail"][0]
+    model, pose, intr, light = product_args(c)
+    view = ReferenceView(pose, intr, c.a("gt"), light, c.a("bg"))
+    _, g, _ = backward(model, view, None, True, 0)
+    for name in GROUPS:
+        assert np.all(getattr(g, name)[5] == 0.0)  # row 5 is behind the camera
+
+
+def test_gpu_backward_deterministic():
+    require_gpu()
+    from paper_2604_02851_b200.optim import ReferenceView, backward
+    c = [c for c in RASTER if c["name"] == "medium"][0]
+    model, pose, intr, light = product_args(c)
+    view = ReferenceView(pose, intr, c.a("gt"), light, c.a("bg"))
+    a = backward(model, view)
+    b = backward(model, view)
+    assert a[0] == b[0]
+    np.testing.assert_array_equal(a[2], b[2])
+    for name in GROUPS:
+        np.testing.assert_array_equal(getattr(a[1], name), getattr(b[1], name))
