@@ -131,104 +131,152 @@ __device__ __forceinline__ void ss_window(const Proj& P, int W, int H, int win[4
     win[3] = (int)fmin(fmax(hy, 0.0), (double)H);
 }
 
-__device__ __forceinline__ int ss_sh_bases(int degree) { return (degree + 1) * (degree + 1); }
+__host__ __device__ constexpr int ss_sh_bases(int degree) { return (degree + 1) * (degree + 1); }
 
-__device__ __forceinline__ void ss_sh_eval(const double v[3], int degree, double Y[16]) {
+template <int DEG, typename T = double>
+__device__ __forceinline__ void ss_sh_eval(const T v[3], T Y[ss_sh_bases(DEG)]) {
     Y[0] = SS_SH_C0;
-    if (degree < 1) return;
-    const double x = v[0], y = v[1], z = v[2];
-    Y[1] = -SS_SH_C1 * y;
-    Y[2] = SS_SH_C1 * z;
-    Y[3] = -SS_SH_C1 * x;
-    if (degree < 2) return;
-    const double xx = x * x, yy = y * y, zz = z * z;
-    Y[4] = 1.0925484306 * (x * y);
-    Y[5] = -1.0925484306 * (y * z);
-    Y[6] = 0.3153915653 * (2 * zz - xx - yy);
-    Y[7] = -1.0925484306 * (x * z);
-    Y[8] = 0.5462742153 * (xx - yy);
-    if (degree < 3) return;
-    Y[9] = -0.5900435899 * y * (3 * xx - yy);
-    Y[10] = 2.8906114426 * (x * y) * z;
-    Y[11] = -0.4570457995 * y * (4 * zz - xx - yy);
-    Y[12] = 0.3731763326 * z * (2 * zz - 3 * xx - 3 * yy);
-    Y[13] = -0.4570457995 * x * (4 * zz - xx - yy);
-    Y[14] = 1.4453057213 * z * (xx - yy);
-    Y[15] = -0.5900435899 * x * (xx - yy - 3 * zz);
-}
-
-// dY_b/dv_k (render.py:93-136)
-__device__ __forceinline__ void ss_sh_grad(const double v[3], int degree, double g[16][3]) {
-#pragma unroll
-    for (int b = 0; b < 16; ++b) g[b][0] = g[b][1] = g[b][2] = 0.0;
-    if (degree < 1) return;
-    const double x = v[0], y = v[1], z = v[2];
-    g[1][1] = -SS_SH_C1;
-    g[2][2] = SS_SH_C1;
-    g[3][0] = -SS_SH_C1;
-    if (degree >= 2) {
-        const double a = 1.0925484306, b = -1.0925484306, c = 0.3153915653, e = -1.0925484306, f = 0.5462742153;
-        g[4][0] = a * y; g[4][1] = a * x;
-        g[5][1] = b * z; g[5][2] = b * y;
-        g[6][0] = c * (-2 * x); g[6][1] = c * (-2 * y); g[6][2] = c * (4 * z);
-        g[7][0] = e * z; g[7][2] = e * x;
-        g[8][0] = f * (2 * x); g[8][1] = f * (-2 * y);
-    }
-    if (degree >= 3) {
-        const double c0 = -0.5900435899, c1 = 2.8906114426, c2 = -0.4570457995, c3 = 0.3731763326,
-                     c4 = -0.4570457995, c5 = 1.4453057213, c6 = -0.5900435899;
-        g[9][0] = c0 * 6 * x * y; g[9][1] = c0 * (3 * x * x - 3 * y * y);
-        g[10][0] = c1 * y * z; g[10][1] = c1 * x * z; g[10][2] = c1 * x * y;
-        g[11][0] = c2 * (-2 * x * y); g[11][1] = c2 * (4 * z * z - x * x - 3 * y * y); g[11][2] = c2 * (8 * y * z);
-        g[12][0] = c3 * (-6 * x * z); g[12][1] = c3 * (-6 * y * z); g[12][2] = c3 * (6 * z * z - 3 * x * x - 3 * y * y);
-        g[13][0] = c4 * (4 * z * z - 3 * x * x - y * y); g[13][1] = c4 * (-2 * x * y); g[13][2] = c4 * (8 * x * z);
-        g[14][0] = c5 * (2 * x * z); g[14][1] = c5 * (-2 * y * z); g[14][2] = c5 * (x * x - y * y);
-        g[15][0] = c6 * (3 * x * x - y * y - 3 * z * z); g[15][1] = c6 * (-2 * x * y); g[15][2] = c6 * (-6 * x * z);
+    if constexpr (DEG >= 1) {
+        const T x = v[0], y = v[1], z = v[2];
+        Y[1] = (T)-SS_SH_C1 * y;
+        Y[2] = (T)SS_SH_C1 * z;
+        Y[3] = (T)-SS_SH_C1 * x;
+        if constexpr (DEG >= 2) {
+            const T xx = x * x, yy = y * y, zz = z * z;
+            Y[4] = (T)1.0925484306 * (x * y);
+            Y[5] = (T)-1.0925484306 * (y * z);
+            Y[6] = (T)0.3153915653 * (2 * zz - xx - yy);
+            Y[7] = (T)-1.0925484306 * (x * z);
+            Y[8] = (T)0.5462742153 * (xx - yy);
+            if constexpr (DEG >= 3) {
+                Y[9] = (T)-0.5900435899 * y * (3 * xx - yy);
+                Y[10] = (T)2.8906114426 * (x * y) * z;
+                Y[11] = (T)-0.4570457995 * y * (4 * zz - xx - yy);
+                Y[12] = (T)0.3731763326 * z * (2 * zz - 3 * xx - 3 * yy);
+                Y[13] = (T)-0.4570457995 * x * (4 * zz - xx - yy);
+                Y[14] = (T)1.4453057213 * z * (xx - yy);
+                Y[15] = (T)-0.5900435899 * x * (xx - yy - 3 * zz);
+            }
+        }
     }
 }
 
+// g_v += sum_b coef[b] * dY_b/dv  (render.py:93-136), without materialising dY
+template <int DEG, typename T = double>
+__device__ __forceinline__ void ss_sh_grad_dot(const T v[3], const T coef[ss_sh_bases(DEG)], T gv[3]) {
+    if constexpr (DEG >= 1) {
+        const T x = v[0], y = v[1], z = v[2];
+        gv[1] += coef[1] * (T)-SS_SH_C1;
+        gv[2] += coef[2] * (T)SS_SH_C1;
+        gv[0] += coef[3] * (T)-SS_SH_C1;
+        if constexpr (DEG >= 2) {
+            const T a = 1.0925484306, b = -1.0925484306, c = 0.3153915653, e = -1.0925484306, f = 0.5462742153;
+            gv[0] += coef[4] * (a * y) + coef[6] * (c * (-2 * x)) + coef[7] * (e * z) + coef[8] * (f * (2 * x));
+            gv[1] += coef[4] * (a * x) + coef[5] * (b * z) + coef[6] * (c * (-2 * y)) + coef[8] * (f * (-2 * y));
+            gv[2] += coef[5] * (b * y) + coef[6] * (c * (4 * z)) + coef[7] * (e * x);
+            if constexpr (DEG >= 3) {
+                const T c0 = -0.5900435899, c1 = 2.8906114426, c2 = -0.4570457995, c3 = 0.3731763326,
+                        c4 = -0.4570457995, c5 = 1.4453057213, c6 = -0.5900435899;
+                gv[0] += coef[9] * (c0 * 6 * x * y) + coef[10] * (c1 * y * z) + coef[11] * (c2 * (-2 * x * y)) +
+                         coef[12] * (c3 * (-6 * x * z)) + coef[13] * (c4 * (4 * z * z - 3 * x * x - y * y)) +
+                         coef[14] * (c5 * (2 * x * z)) + coef[15] * (c6 * (3 * x * x - y * y - 3 * z * z));
+                gv[1] += coef[9] * (c0 * (3 * x * x - 3 * y * y)) + coef[10] * (c1 * x * z) +
+                         coef[11] * (c2 * (4 * z * z - x * x - 3 * y * y)) + coef[12] * (c3 * (-6 * y * z)) +
+                         coef[13] * (c4 * (-2 * x * y)) + coef[14] * (c5 * (-2 * y * z)) + coef[15] * (c6 * (-2 * x * y));
+                gv[2] += coef[10] * (c1 * x * y) + coef[11] * (c2 * (8 * y * z)) +
+                         coef[12] * (c3 * (6 * z * z - 3 * x * x - 3 * y * y)) + coef[13] * (c4 * (8 * x * z)) +
+                         coef[14] * (c5 * (x * x - y * y)) + coef[15] * (c6 * (-6 * x * z));
+            }
+        }
+    }
+}
+
+template <int DEG>
 struct Shade {
+    static constexpr int B = ss_sh_bases(DEG);
     double vdir[3], dist;
-    double Y[16];
+    double Y[B];
     int axis;          // normal-proxy axis
+    double nhat[3];    // Rq[:, axis]
     double s, cosv;    // signed / absolute cosine
     double albedo[3];
     double vis;
     double pre[3];     // colour before the [0,1] clamp
 };
 
+template <int DEG>
+__device__ __forceinline__ void ss_shade_v(const ss_light& L, const float* ls, const float* shv, float visf,
+                                           const double d[3], const double Rq[3][3], Shade<DEG>& S);
+
+// one row's SH coefficients (3 x B floats) into registers, 16-byte loads
+// when the row stride allows it (degrees 1 and 3)
+template <int DEG>
+__device__ __forceinline__ void ss_load_sh(const float* sh, float out[3 * ss_sh_bases(DEG)]) {
+    constexpr int N = 3 * ss_sh_bases(DEG);
+    if constexpr (N % 4 == 0) {
+        const float4* p = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i) {
+            const float4 v = __ldg(p + i);
+            out[4 * i] = v.x;
+            out[4 * i + 1] = v.y;
+            out[4 * i + 2] = v.z;
+            out[4 * i + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) out[i] = __ldg(sh + i);
+    }
+}
+
 // ref render.py:175-197 and the normal proxy of render.py:139-151
-__device__ __forceinline__ void ss_shade(const ss_light& L, const float* ls, const float* sh, int B, int degree,
-                                         float visf, const double d[3], const double Rq[3][3], Shade& S) {
+template <int DEG>
+__device__ __forceinline__ void ss_shade(const ss_light& L, const float* ls, const float* sh, float visf,
+                                         const double d[3], const double Rq[3][3], Shade<DEG>& S) {
+    float shv[3 * ss_sh_bases(DEG)];
+    ss_load_sh<DEG>(sh, shv);
+    ss_shade_v<DEG>(L, ls, shv, visf, d, Rq, S);
+}
+
+template <int DEG>
+__device__ __forceinline__ void ss_shade_v(const ss_light& L, const float* ls, const float* shv, float visf,
+                                           const double d[3], const double Rq[3][3], Shade<DEG>& S) {
+    constexpr int B = ss_sh_bases(DEG);
     S.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     S.vdir[0] = d[0] / S.dist;
     S.vdir[1] = d[1] / S.dist;
     S.vdir[2] = d[2] / S.dist;
-    double l0 = ls[0], l1 = ls[1], l2 = ls[2];
-    double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
+    const double l0 = ls[0], l1 = ls[1], l2 = ls[2];
+    const double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
     S.axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
-    const int k = S.axis;
-    S.s = Rq[0][k] * -L.direction[0] + Rq[1][k] * -L.direction[1] + Rq[2][k] * -L.direction[2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) S.nhat[i] = S.axis == 0 ? Rq[i][0] : (S.axis == 1 ? Rq[i][1] : Rq[i][2]);
+    S.s = S.nhat[0] * -L.direction[0] + S.nhat[1] * -L.direction[1] + S.nhat[2] * -L.direction[2];
     S.cosv = fabs(S.s);
     S.vis = visf;
-    ss_sh_eval(S.vdir, degree, S.Y);
+    ss_sh_eval<DEG>(S.vdir, S.Y);
+    const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+#pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const float* shc = sh + c * B;
-        S.albedo[c] = SS_SH_C0 * shc[0] + 0.5;
-        double direct = S.albedo[c] * L.intensity[c] * (S.cosv * S.vis);
+        const float* shc = shv + c * B;
+        double coef[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) coef[b] = shc[b];
+        S.albedo[c] = SS_SH_C0 * coef[0] + 0.5;
+        const double direct = S.albedo[c] * L.intensity[c] * (S.cosv * S.vis);
         double base = 0.0;
         if (L.ambient_bands == 0) {
-            for (int b = 0; b < B; ++b) base += shc[b] * S.Y[b];
+#pragma unroll
+            for (int b = 0; b < B; ++b) base += coef[b] * S.Y[b];
             base += 0.5;
         } else {
-            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
-            for (int b = 0; b < BL; ++b) {
-                double e = shc[b];
-                if (b == 0) e += 0.5 / SS_SH_C0;
-                base += e * L.ambient[c * L.ambient_bands + b];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (b < BL) base += (b == 0 ? coef[0] + 0.5 / SS_SH_C0 : coef[b]) * L.ambient[c * L.ambient_bands + b];
             }
             double vd = 0.0;
-            for (int b = 1; b < B; ++b) vd += shc[b] * S.Y[b];
+#pragma unroll
+            for (int b = 1; b < B; ++b) vd += coef[b] * S.Y[b];
             base += vd;
         }
         S.pre[c] = base + direct;

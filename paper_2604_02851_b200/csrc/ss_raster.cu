@@ -56,6 +56,7 @@ struct Bins {
     double2* rmu;            // [n_in] rank-ordered mu2d
     uint64_t* roff;          // [n_in] rank -> first pair (pre-sort position)
     uint32_t* rcnt;          // [n_in] tiles touched
+    uint32_t* rinv;          // [n_in] input index j -> depth rank (~0 if culled)
     void* rrec;              // [n_in] rank-ordered SplatRec<R>
     uint32_t* pkeys;         // [pairs] tile id (sorted)
     uint32_t* pvals;         // [pairs] rank (sorted)
@@ -77,10 +78,11 @@ __global__ void k_visible_flags(ss_model m, ss_camera cam, const int64_t* subset
     }
 }
 
-__global__ void k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
+template <int DEG>
+__global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
                              int cutoff, uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                              PerG* __restrict__ perg, DebugOut dbg) {
-    const int B = ss_sh_bases(m.sh_degree);
+    constexpr int B = ss_sh_bases(DEG);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = subset ? subset[j] : j;
         Proj P;
@@ -92,9 +94,8 @@ __global__ void k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_
         }
         dkeys[j] = (uint64_t)__double_as_longlong(P.mc[2]);  // z >= near > 0: bits order as the value
         ss_project(cam, m.log_scales + row * 3, m.quaternions + row * 4, cutoff != 0, P);
-        Shade S;
-        ss_shade(L, m.log_scales + row * 3, m.sh_coeffs + row * 3 * B, B, m.sh_degree, m.light_visibility[row], P.d,
-                 P.Rq, S);
+        Shade<DEG> S;
+        ss_shade<DEG>(L, m.log_scales + row * 3, m.sh_coeffs + row * 3 * B, m.light_visibility[row], P.d, P.Rq, S);
         PerG g;
         g.mu[0] = P.mu[0];
         g.mu[1] = P.mu[1];
@@ -133,13 +134,16 @@ __device__ __forceinline__ void win_tiles(const int w[4], int& tx0, int& tx1, in
 template <typename R>
 __global__ void k_count(const uint64_t* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
                         const PerG* __restrict__ perg, int64_t n_in, double2* __restrict__ rmu,
-                        SplatRec<R>* __restrict__ rrec, uint32_t* __restrict__ rcnt) {
+                        SplatRec<R>* __restrict__ rrec, uint32_t* __restrict__ rcnt, uint32_t* __restrict__ rinv) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = dvals[r];
         if (dkeys[r] == ~0ull) {
             rcnt[r] = 0;
+            rinv[j] = ~0u;
             continue;
         }
-        const PerG g = perg[dvals[r]];
+        rinv[j] = (uint32_t)r;
+        const PerG g = perg[j];
         rmu[r] = make_double2(g.mu[0], g.mu[1]);
         SplatRec<R> s;
         s.a = (R)g.a;
@@ -185,17 +189,33 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, int64_t n, uint2* __
 }
 
 // ---------------------------------------------------------------- blend math
+//
+// One warp owns one 16x16 tile; lane l holds the 8 pixels (l % 16, l / 16 + 2q),
+// q = 0..7.  A warp stages 32 splats at a time in shared memory and walks
+// them in depth order; no block-level barriers anywhere (blocks are just
+// WPB independent tiles).  Per-pixel liveness is an 8-bit mask; a pixel dies
+// when T drops below 1e-4 (the reference's T-gate: later splats skip it).
+constexpr int WPB = 4;   // tiles (warps) per block
+constexpr int PPT = 8;   // pixels per lane
+
 template <typename R> __device__ __forceinline__ R ss_exp(R x);
 template <> __device__ __forceinline__ float ss_exp<float>(float x) { return __expf(x); }
 template <> __device__ __forceinline__ double ss_exp<double>(double x) { return exp(x); }
 
-// Staged splat (shared memory).  For fp32 the centre is tile-relative
-// (computed in fp64 then rounded) so dx keeps full precision; for fp64 it
-// is absolute and dx = (px + 0.5) - mu exactly as the reference computes it.
+template <typename R> __device__ __forceinline__ R ss_rcp(R x);
+template <> __device__ __forceinline__ float ss_rcp<float>(float x) { return __fdividef(1.0f, x); }
+template <> __device__ __forceinline__ double ss_rcp<double>(double x) { return 1.0 / x; }
+
+// Staged splat.  fp32: centre relative to the tile origin (rounded from the
+// fp64 centre) so dx keeps full precision; fp64: absolute centre and
+// dx = (px + 0.5) - mu exactly as the reference computes it.
 template <typename R>
-struct Staged {
-    R mx, my, a, b, c, o, col0, col1, col2;
-    int wx0, wx1, wy0, wy1;  // window in tile-local pixel coords, clipped to [0, 16]
+struct __align__(16) Staged {
+    R mx, my, a, b;
+    R c, o, c0, c1;
+    R c2;
+    int wx0, wx1, qmask_lo;  // tile-local x window [wx0, wx1); wy packed below
+    int wy0, wy1, p, pad;    // tile-local y window [wy0, wy1); p = partial index
 };
 
 template <typename R>
@@ -211,17 +231,26 @@ __device__ __forceinline__ void stage(Staged<R>& s, const double2 mu, const Spla
     s.b = rec.b;
     s.c = rec.c;
     s.o = rec.o;
-    s.col0 = rec.col[0];
-    s.col1 = rec.col[1];
-    s.col2 = rec.col[2];
+    s.c0 = rec.col[0];
+    s.c1 = rec.col[1];
+    s.c2 = rec.col[2];
     s.wx0 = min(max(rec.win[0] - X0, 0), TILE);
     s.wx1 = min(max(rec.win[1] - X0, 0), TILE);
     s.wy0 = min(max(rec.win[2] - Y0, 0), TILE);
     s.wy1 = min(max(rec.win[3] - Y0, 0), TILE);
 }
 
+// 8-bit mask of this lane's pixels (rows ly0 + 2q) inside [wy0, wy1), if its column is inside [wx0, wx1)
 template <typename R>
-__device__ __forceinline__ void pixel_delta(const Staged<R>& s, int lx, int ly, int X0, int Y0, R& dx, R& dy) {
+__device__ __forceinline__ unsigned lane_mask(const Staged<R>& s, int lx, int ly0) {
+    if (lx < s.wx0 || lx >= s.wx1) return 0u;
+    const int qlo = max(0, (s.wy0 - ly0 + 1) >> 1);
+    const int qhi = max(0, (s.wy1 - ly0 + 1) >> 1);
+    return ((1u << qhi) - 1u) & ~((1u << qlo) - 1u);
+}
+
+template <typename R>
+__device__ __forceinline__ void deltas(const Staged<R>& s, int lx, int ly, int X0, int Y0, R& dx, R& dy) {
     if (sizeof(R) == 4) {
         dx = ((R)lx + (R)0.5) - s.mx;
         dy = ((R)ly + (R)0.5) - s.my;
@@ -231,85 +260,123 @@ __device__ __forceinline__ void pixel_delta(const Staged<R>& s, int lx, int ly, 
     }
 }
 
-// ---------------------------------------------------------------- K5 forward
-constexpr int FWD_THREADS = 256;
-
 template <typename R>
-__global__ void __launch_bounds__(FWD_THREADS) k_blend_fwd(const uint2* __restrict__ ranges,
-                                                           const uint32_t* __restrict__ pvals,
-                                                           const double2* __restrict__ rmu,
-                                                           const SplatRec<R>* __restrict__ rrec, int W, int H,
-                                                           int tiles_x, double bg0, double bg1, double bg2,
-                                                           R* __restrict__ img, R* __restrict__ Tout,
-                                                           uint32_t* __restrict__ tile_stop,
-                                                           unsigned long long* __restrict__ eval_count) {
-    __shared__ Staged<R> sm[FWD_THREADS];
-    __shared__ int s_last;
-    const int tile = blockIdx.x;
+__device__ __forceinline__ R gauss_power(const Staged<R>& s, R dx, R dy) {
+    return (R)-0.5 * (s.a * dx * dx + (R)2 * s.b * dx * dy + s.c * dy * dy);
+}
+
+// Per (splat, lane) geometry: the lane's column is fixed, so the conic's x
+// terms are hoisted; per pixel the exponent is two FMAs.  fp64 keeps the
+// reference's exact expression (render.py:311).
+template <typename R>
+struct PixelGeom {
+    R dx, dy0, Ax2, Bx2, adx0, bdx0;
+    __device__ __forceinline__ PixelGeom(const Staged<R>& s, int lx, int ly0, int X0, int Y0) {
+        R dyy;
+        deltas(s, lx, ly0, X0, Y0, dx, dyy);
+        dy0 = dyy;
+        Ax2 = s.a * dx * dx;
+        Bx2 = (R)2 * s.b * dx;
+        adx0 = s.a * dx;
+        bdx0 = s.b * dx;
+    }
+    __device__ __forceinline__ R dy(int q) const { return dy0 + (R)(2 * q); }
+    __device__ __forceinline__ R power(const Staged<R>& s, int q) const {
+        const R y = dy(q);
+        if (sizeof(R) == 4) return (R)-0.5 * ((s.c * y + Bx2) * y + Ax2);
+        return gauss_power(s, dx, y);
+    }
+    __device__ __forceinline__ R gauss(const Staged<R>& s, int q) const { return ss_exp<R>(power(s, q)); }
+};
+
+// ---------------------------------------------------------------- K5 forward
+template <typename R>
+__global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict__ ranges,
+                                                        const uint32_t* __restrict__ pvals,
+                                                        const double2* __restrict__ rmu,
+                                                        const SplatRec<R>* __restrict__ rrec, int W, int H,
+                                                        int tiles_x, int n_tiles, double bg0, double bg1, double bg2,
+                                                        R* __restrict__ img, R* __restrict__ Tout,
+                                                        uint32_t* __restrict__ tile_stop,
+                                                        unsigned long long* __restrict__ eval_count) {
+    __shared__ Staged<R> sm[WPB][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * WPB + warp;
+    if (tile >= n_tiles) return;
     const int X0 = (tile % tiles_x) * TILE, Y0 = (tile / tiles_x) * TILE;
-    const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
-    const int px = X0 + lx, py = Y0 + ly;
-    const bool inside = px < W && py < H;
+    const int lx = lane & 15, ly0 = lane >> 4;
+    unsigned alive = 0;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q)
+        if (X0 + lx < W && Y0 + ly0 + 2 * q < H) alive |= 1u << q;
+    R T[PPT], C0[PPT], C1[PPT], C2[PPT];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) T[q] = 1, C0[q] = 0, C1[q] = 0, C2[q] = 0;
     const uint2 rg = ranges[tile];
-    R T = 1, c0 = 0, c1 = 0, c2 = 0;
-    bool done = !inside;
     int last = -1;
     uint32_t evals = 0;
-    if (threadIdx.x == 0) s_last = -1;
-    for (uint32_t b0 = rg.x; b0 < rg.y; b0 += FWD_THREADS) {
-        if (__syncthreads_count(!done) == 0) break;
-        const uint32_t i = b0 + threadIdx.x;
+    Staged<R>* my = sm[warp];
+    for (uint32_t b0 = rg.x; b0 < rg.y; b0 += 32) {
+        if (!__any_sync(0xffffffffu, alive)) break;
+        const uint32_t i = b0 + lane;
         if (i < rg.y) {
             const uint32_t r = pvals[i];
-            stage(sm[threadIdx.x], rmu[r], rrec[r], X0, Y0);
+            stage(my[lane], rmu[r], rrec[r], X0, Y0);
         }
-        __syncthreads();
-        const int nb = min((uint32_t)FWD_THREADS, rg.y - b0);
-        for (int k = 0; k < nb && !done; ++k) {
-            const Staged<R>& s = sm[k];
-            if (lx < s.wx0 || lx >= s.wx1 || ly < s.wy0 || ly >= s.wy1) continue;
-            R dx, dy;
-            pixel_delta(s, lx, ly, X0, Y0, dx, dy);
-            const R power = (R)-0.5 * (s.a * dx * dx + (R)2 * s.b * dx * dy + s.c * dy * dy);
-            const R alpha = min(s.o * ss_exp<R>(power), (R)ALPHA_CAP);
-            const R w = alpha * T;
-            c0 += w * s.col0;
-            c1 += w * s.col1;
-            c2 += w * s.col2;
-            T = T * ((R)1 - alpha);
+        __syncwarp();
+        const int nb = (int)min(32u, rg.y - b0);
+        for (int k = 0; k < nb; ++k) {
+            const Staged<R> s = my[k];
+            const unsigned act = lane_mask(s, lx, ly0) & alive;
+            if (!act) continue;
             last = (int)(b0 - rg.x) + k;
-            ++evals;
-            if (T < (R)T_CUTOFF) done = true;
-        }
-    }
-    if (last >= 0) atomicMax(&s_last, last);
-    if (eval_count) {
+            evals += __popc(act);
+            // branch-free over the lane's 8 pixels: inactive ones get G = 0,
+            // which leaves C and T unchanged
+            PixelGeom<R> pg(s, lx, ly0, X0, Y0);
+            const unsigned wact = __reduce_or_sync(__activemask(), act);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
-        if ((threadIdx.x & 31) == 0 && evals) atomicAdd(eval_count, (unsigned long long)evals);
+            for (int q = 0; q < PPT; ++q) {
+                if (!((wact >> q) & 1u)) continue;  // warp-uniform: no lane needs this pixel row
+                const R G = (act >> q) & 1u ? pg.gauss(s, q) : (R)0;
+                const R alpha = min(s.o * G, (R)ALPHA_CAP);
+                const R w = alpha * T[q];
+                C0[q] += w * s.c0;
+                C1[q] += w * s.c1;
+                C2[q] += w * s.c2;
+                T[q] -= w;  // T (1 - alpha)
+            }
+#pragma unroll
+            for (int q = 0; q < PPT; ++q)
+                if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+        }
+        __syncwarp();
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && tile_stop) tile_stop[tile] = (uint32_t)(s_last + 1);
-    if (inside) {
-        const int64_t p = (int64_t)py * W + px;
-        img[3 * p + 0] = c0 + T * (R)bg0;
-        img[3 * p + 1] = c1 + T * (R)bg1;
-        img[3 * p + 2] = c2 + T * (R)bg2;
-        if (Tout) Tout[p] = T;
+    last = __reduce_max_sync(0xffffffffu, last + 1);
+    if (lane == 0 && tile_stop) tile_stop[tile] = (uint32_t)last;
+    if (eval_count) {
+        evals = __reduce_add_sync(0xffffffffu, evals);
+        if (lane == 0 && evals) atomicAdd(eval_count, (unsigned long long)evals);
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        const int px = X0 + lx, py = Y0 + ly0 + 2 * q;
+        if (px < W && py < H) {
+            const int64_t p = (int64_t)py * W + px;
+            img[3 * p + 0] = C0[q] + T[q] * (R)bg0;
+            img[3 * p + 1] = C1[q] + T[q] * (R)bg1;
+            img[3 * p + 2] = C2[q] + T[q] * (R)bg2;
+            if (Tout) Tout[p] = T[q];
+        }
     }
 }
 
 // ---------------------------------------------------------------- K6 backward
-constexpr int BWD_THREADS = 64;   // 4 pixels per thread: (lx, ly0 + 4 q)
-constexpr int BWD_PPT = 4;
-constexpr int BWD_BATCH = 64;
-constexpr int BWD_WARPS = BWD_THREADS / 32;
-
 // Transposed butterfly: reduces v[0..7] over the warp with 7+2 shuffles;
 // lane l with (l & 3) == 0 ends with the sum of value index
 // 4*bit4(l) + 2*bit3(l) + bit2(l).
 template <typename R>
-__device__ __forceinline__ R warp_reduce8(R v[8], int lane) {
+__device__ __forceinline__ R warp_reduce8(const R v[8], int lane) {
     R w[4];
     {
         const bool hi = lane & 16;
@@ -344,151 +411,142 @@ __device__ __forceinline__ R warp_sum(R v) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t pair_index(const uint64_t* roff, const int win[4], uint32_t r, int tx, int ty) {
+    int tx0, tx1, ty0, ty1;
+    win_tiles(win, tx0, tx1, ty0, ty1);
+    return (uint32_t)(roff[r] + (uint64_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0)));
+}
+
 template <typename R>
-__global__ void __launch_bounds__(BWD_THREADS) k_blend_bwd(const uint2* __restrict__ ranges,
-                                                           const uint32_t* __restrict__ pvals,
-                                                           const double2* __restrict__ rmu,
-                                                           const SplatRec<R>* __restrict__ rrec,
-                                                           const uint64_t* __restrict__ roff,
-                                                           const uint32_t* __restrict__ tile_stop, int W, int H,
-                                                           int tiles_x, const R* __restrict__ img,
-                                                           const float* __restrict__ gt, double npx3,
-                                                           R* __restrict__ partials, double* __restrict__ tile_loss) {
-    __shared__ Staged<R> sm[BWD_BATCH];
-    __shared__ uint64_t s_pidx[BWD_BATCH];
-    __shared__ R s_red[BWD_WARPS][BWD_BATCH][9];
-    __shared__ double s_loss[BWD_WARPS];
-    const int tile = blockIdx.x;
-    const int X0 = (tile % tiles_x) * TILE, Y0 = (tile / tiles_x) * TILE;
+__global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict__ ranges,
+                                                        const uint32_t* __restrict__ pvals,
+                                                        const double2* __restrict__ rmu,
+                                                        const SplatRec<R>* __restrict__ rrec,
+                                                        const uint64_t* __restrict__ roff,
+                                                        const uint32_t* __restrict__ tile_stop, int W, int H,
+                                                        int tiles_x, int n_tiles, const R* __restrict__ img,
+                                                        const float* __restrict__ gt, double npx3,
+                                                        R* __restrict__ partials, double* __restrict__ tile_loss) {
+    __shared__ Staged<R> sm[WPB][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * WPB + warp;
+    if (tile >= n_tiles) return;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = threadIdx.x % TILE, ly0 = threadIdx.x / TILE;
+    const int X0 = tx * TILE, Y0 = ty * TILE;
+    const int lx = lane & 15, ly0 = lane >> 4;
     const uint2 rg = ranges[tile];
     const uint32_t stop = rg.x + (tile_stop ? min(tile_stop[tile], rg.y - rg.x) : (rg.y - rg.x));
 
-    R T[BWD_PPT], pre[BWD_PPT][3], C[BWD_PPT][3], gC[BWD_PPT][3];
-    bool dn[BWD_PPT];
+    // per pixel: T, R = sum_c gC_c (C_c - prefix_c), dL/dC (gC), alive bit
+    R T[PPT], Rr[PPT], g0[PPT], g1[PPT], g2[PPT];
+    unsigned alive = 0;
     double loss = 0.0;
+    const R inv = sizeof(R) == 8 ? (R)0 : (R)(1.0 / npx3);
 #pragma unroll
-    for (int q = 0; q < BWD_PPT; ++q) {
-        const int ly = ly0 + 4 * q;
-        const int px = X0 + lx, py = Y0 + ly;
-        const bool in = px < W && py < H;
-        dn[q] = !in;
+    for (int q = 0; q < PPT; ++q) {
+        const int px = X0 + lx, py = Y0 + ly0 + 2 * q;
         T[q] = 1;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            pre[q][c] = 0;
-            C[q][c] = 0;
-            gC[q][c] = 0;
-        }
-        if (in) {
+        Rr[q] = 0;
+        g0[q] = g1[q] = g2[q] = 0;
+        if (px < W && py < H) {
+            alive |= 1u << q;
             const int64_t p = (int64_t)py * W + px;
+            R gg[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 const R v = img[3 * p + c];
                 const R diff = v - (R)gt[3 * p + c];
-                C[q][c] = v;
                 loss += fabs((double)diff);
                 const R sg = diff > (R)0 ? (R)1 : (diff < (R)0 ? (R)-1 : (R)0);
                 // dL/dC = sign(C - gt) / (H W 3)  (optim.py:124-125)
-                gC[q][c] = sizeof(R) == 8 ? (R)((double)sg / npx3) : sg * (R)(1.0 / npx3);
+                gg[c] = sizeof(R) == 8 ? (R)((double)sg / npx3) : sg * inv;
+                Rr[q] += gg[c] * v;
             }
+            g0[q] = gg[0];
+            g1[q] = gg[1];
+            g2[q] = gg[2];
         }
     }
-
-    for (uint32_t b0 = rg.x; b0 < stop; b0 += BWD_BATCH) {
-        __syncthreads();
-        const int nb = (int)min((uint32_t)BWD_BATCH, stop - b0);
-        for (int k = threadIdx.x; k < nb; k += BWD_THREADS) {
-            const uint32_t r = pvals[b0 + k];
+    Staged<R>* my = sm[warp];
+    for (uint32_t b0 = rg.x; b0 < stop; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        if (i < stop) {
+            const uint32_t r = pvals[i];
             const SplatRec<R> rec = rrec[r];
-            stage(sm[k], rmu[r], rec, X0, Y0);
-            int tx0, tx1, ty0, ty1;
-            win_tiles(rec.win, tx0, tx1, ty0, ty1);
-            s_pidx[k] = roff[r] + (uint64_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+            stage(my[lane], rmu[r], rec, X0, Y0);
+            my[lane].p = (int)pair_index(roff, rec.win, r, tx, ty);
         }
-        __syncthreads();
+        __syncwarp();
+        const int nb = (int)min(32u, stop - b0);
         for (int k = 0; k < nb; ++k) {
-            const Staged<R>& s = sm[k];
+            const Staged<R> s = my[k];
+            const unsigned act = lane_mask(s, lx, ly0) & alive;
             R acc[9];
 #pragma unroll
             for (int e = 0; e < 9; ++e) acc[e] = 0;
-            bool any = false;
-            const bool colin = lx >= s.wx0 && lx < s.wx1;
+            if (act) {
+                // branch-free over the lane's 8 pixels: inactive ones get
+                // G = 0, which zeroes every contribution and leaves T, R alone
+                PixelGeom<R> pg(s, lx, ly0, X0, Y0);
+                const unsigned wact = __reduce_or_sync(__activemask(), act);
 #pragma unroll
-            for (int q = 0; q < BWD_PPT; ++q) {
-                const int ly = ly0 + 4 * q;
-                if (dn[q] || !colin || ly < s.wy0 || ly >= s.wy1) continue;
-                any = true;
-                R dx, dy;
-                pixel_delta(s, lx, ly, X0, Y0, dx, dy);
-                const R power = (R)-0.5 * (s.a * dx * dx + (R)2 * s.b * dx * dy + s.c * dy * dy);
-                const R G = ss_exp<R>(power);
-                const R oG = s.o * G;
-                const R alpha = min(oG, (R)ALPHA_CAP);
-                const R w = alpha * T[q];
-                const R col[3] = {s.col0, s.col1, s.col2};
-                const R inv1m = (R)1 / ((R)1 - alpha);
-                R dal = 0;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    acc[c] += gC[q][c] * w;
-                    const R S = C[q][c] - pre[q][c] - w * col[c];
-                    dal += gC[q][c] * (col[c] * T[q] - S * inv1m);
+                for (int q = 0; q < PPT; ++q) {
+                    if (!((wact >> q) & 1u)) continue;  // warp-uniform skip
+                    const R G = (act >> q) & 1u ? pg.gauss(s, q) : (R)0;
+                    const R oG = s.o * G;
+                    const bool open = oG < (R)ALPHA_CAP;
+                    const R alpha = open ? oG : (R)ALPHA_CAP;
+                    const R w = alpha * T[q];
+                    const R gcol = g0[q] * s.c0 + g1[q] * s.c1 + g2[q] * s.c2;
+                    acc[0] += g0[q] * w;
+                    acc[1] += g1[q] * w;
+                    acc[2] += g2[q] * w;
+                    // dL/dalpha = sum_c gC_c (col_c T - S_c / (1 - alpha)), S = C - prefix - contrib
+                    const R rest = Rr[q] - w * gcol;
+                    const R dal = T[q] * gcol - rest * ss_rcp<R>((R)1 - alpha);
+                    Rr[q] = rest;
+                    const R dG = open ? dal * G : (R)0;
+                    const R gp = open ? dal * alpha : (R)0;
+                    const R y = pg.dy(q);
+                    const R adx = pg.adx0 + s.b * y;
+                    const R ady = pg.bdx0 + s.c * y;
+                    const R gpx = gp * adx, gpy = gp * ady;
+                    acc[3] += dG;
+                    acc[4] += gpx;
+                    acc[5] += gpy;
+                    acc[6] += gpx * adx;
+                    acc[7] += gpx * ady;
+                    acc[8] += gpy * ady;
+                    T[q] -= w;
                 }
-                if (oG < (R)ALPHA_CAP) {
-                    acc[3] += dal * G;
-                    const R gp = dal * alpha;
-                    const R adx = s.a * dx + s.b * dy;
-                    const R ady = s.b * dx + s.c * dy;
-                    acc[4] += gp * adx;
-                    acc[5] += gp * ady;
-                    acc[6] += (R)0.5 * gp * adx * adx;
-                    acc[7] += (R)0.5 * gp * adx * ady;
-                    acc[8] += (R)0.5 * gp * ady * ady;
-                }
 #pragma unroll
-                for (int c = 0; c < 3; ++c) pre[q][c] += w * col[c];
-                T[q] = T[q] * ((R)1 - alpha);
-                if (T[q] < (R)T_CUTOFF) dn[q] = true;
+                for (int q = 0; q < PPT; ++q)
+                    if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
             }
-            if (__any_sync(0xffffffffu, any)) {
+            R* out = partials + (uint64_t)(uint32_t)s.p * 9;
+            if (__any_sync(0xffffffffu, act != 0)) {
                 const R y = warp_reduce8<R>(acc, lane);
                 const R z = warp_sum<R>(acc[8]);
-                if ((lane & 3) == 0) s_red[warp][k][((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = y;
-                if (lane == 0) s_red[warp][k][8] = z;
+                if ((lane & 3) == 0) {
+                    const int e = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                    out[e] = e >= 6 ? (R)0.5 * y : y;
+                }
+                if (lane == 0) out[8] = (R)0.5 * z;
             } else if (lane < 9) {
-                s_red[warp][k][lane] = 0;
+                out[lane] = 0;
             }
         }
-        __syncthreads();
-        for (int e = threadIdx.x; e < nb * 9; e += BWD_THREADS) {
-            const int k = e / 9, q = e % 9;
-            R sum = 0;
-#pragma unroll
-            for (int w = 0; w < BWD_WARPS; ++w) sum += s_red[w][k][q];
-            partials[s_pidx[k] * 9 + q] = sum;
-        }
+        __syncwarp();
     }
     // pairs after every pixel of the tile saturated contribute nothing
-    for (uint32_t i = stop + threadIdx.x; i < rg.y; i += BWD_THREADS) {
+    for (uint32_t i = stop + lane; i < rg.y; i += 32) {
         const uint32_t r = pvals[i];
-        const SplatRec<R> rec = rrec[r];
-        int tx0, tx1, ty0, ty1;
-        win_tiles(rec.win, tx0, tx1, ty0, ty1);
-        const uint64_t p = roff[r] + (uint64_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+        const uint32_t p = pair_index(roff, rrec[r].win, r, tx, ty);
 #pragma unroll
-        for (int q = 0; q < 9; ++q) partials[p * 9 + q] = 0;
+        for (int q = 0; q < 9; ++q) partials[(uint64_t)p * 9 + q] = 0;
     }
     loss = warp_sum<double>(loss);
-    if (lane == 0) s_loss[warp] = loss;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0;
-        for (int w = 0; w < BWD_WARPS; ++w) t += s_loss[w];
-        tile_loss[tile] = t;
-    }
+    if (lane == 0) tile_loss[tile] = loss;
 }
 
 __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, double inv_npx, double* __restrict__ out) {
@@ -505,141 +563,294 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, doubl
 }
 
 // ---------------------------------------------------------------- K7 chain rule
+// (a) fixed-order sum of each splat's per-tile partials (rank order: a
+//     thread's pairs follow its neighbour's in memory) -> 9 floats per rank
 template <typename R>
-__global__ void k_chain(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset,
-                        const uint64_t* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
-                        const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
-                        const R* __restrict__ partials, int64_t n_in, int cutoff, float* __restrict__ grad) {
-    const int B = ss_sh_bases(m.sh_degree);
-    const int64_t a = m.active_count;
+__global__ void k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
+                               const R* __restrict__ partials, int64_t n_in, R* __restrict__ g9) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
-        if (dkeys[r] == ~0ull) continue;
-        const int64_t j = dvals[r];
-        const int64_t row = subset ? subset[j] : j;
-        if (row >= a) continue;
-        double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         const uint32_t cnt = rcnt[r];
+        double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         const R* pp = partials + roff[r] * 9;
         for (uint32_t i = 0; i < cnt; ++i)
 #pragma unroll
             for (int e = 0; e < 9; ++e) g[e] += (double)pp[i * 9 + e];
-        Proj P;
-        ss_cam_point(cam, m.means + row * 3, P.d, P.mc);
-        ss_project(cam, m.log_scales + row * 3, m.quaternions + row * 4, cutoff != 0, P);
-        Shade S;
-        const float* sh = m.sh_coeffs + row * 3 * B;
-        ss_shade(L, m.log_scales + row * 3, sh, B, m.sh_degree, m.light_visibility[row], P.d, P.Rq, S);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) g9[r * 9 + e] = (R)g[e];
+    }
+}
 
-        double gc[3];
-        for (int c = 0; c < 3; ++c) gc[c] = (S.pre[c] > 0.0 && S.pre[c] < 1.0) ? g[c] : 0.0;
-        const double go = g[3];
-        const double gm[2] = {g[4], g[5]};
-        const double G2[2][2] = {{g[6], g[7]}, {g[7], g[8]}};
-        const double(&J)[2][3] = P.J;
-        // gJ = (G2 + G2^T) J cov ; gV = J^T G2 J ; G3 = W^T gV W = R_cw gV R_cw^T
-        double JC[2][3], JG[2][3];
-        for (int l = 0; l < 3; ++l) {
-            JC[0][l] = J[0][0] * P.cov[0][l] + J[0][2] * P.cov[2][l];
-            JC[1][l] = J[1][1] * P.cov[1][l] + J[1][2] * P.cov[2][l];
+// (b) the chain rule in row order
+template <typename T> __device__ __forceinline__ T t_exp(T x);
+template <> __device__ __forceinline__ float t_exp<float>(float x) { return expf(x); }
+template <> __device__ __forceinline__ double t_exp<double>(double x) { return exp(x); }
+
+// Chain rule in the blend precision T (fp32 for the throughput path, fp64
+// for the parity path); the normal-proxy axis pick repeats the preprocess's
+// fp64 comparison so both passes agree on it.
+template <typename T, int DEG>
+__global__ void __launch_bounds__(128) k_chain(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset,
+                        const uint32_t* __restrict__ rinv, const T* __restrict__ g9, int64_t n_in, int cutoff,
+                        float* __restrict__ grad, float4* __restrict__ shrec) {
+    constexpr int B = ss_sh_bases(DEG);
+    const int64_t a = m.active_count;
+    T Rc[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Rc[i][k] = (T)cam.rot_cw[3 * i + k];
+    const T fx = (T)cam.fx, fy = (T)cam.fy;
+    const T ldir[3] = {(T)L.direction[0], (T)L.direction[1], (T)L.direction[2]};
+    // row order: parameter reads and gradient writes are coalesced
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = rinv[j];
+        if (r == ~0u) continue;
+        const int64_t row = subset ? subset[j] : j;
+        if (row >= a) continue;
+        T g[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) g[e] = g9[(int64_t)r * 9 + e];
+        // ---- appearance first (the SH registers die early)
+        T d[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d[i] = (T)((double)m.means[row * 3 + i] - cam.position[i]);
+        const T dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        const T vdir[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+        const float* lsp = m.log_scales + row * 3;
+        int axis;
+        {
+            const double l0 = lsp[0], l1 = lsp[1], l2 = lsp[2];
+            const double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
+            axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
         }
-        double gJ[2][3];
-        for (int aa = 0; aa < 2; ++aa)
-            for (int l = 0; l < 3; ++l) gJ[aa][l] = 2.0 * (G2[aa][0] * JC[0][l] + G2[aa][1] * JC[1][l]);
-        for (int aa = 0; aa < 2; ++aa)
-            for (int l = 0; l < 3; ++l) JG[aa][l] = G2[aa][0] * J[0][l] + G2[aa][1] * J[1][l];
-        double gV[3][3];
-        for (int k = 0; k < 3; ++k)
-            for (int l = 0; l < 3; ++l) gV[k][l] = J[0][k] * JG[0][l] + J[1][k] * JG[1][l];
-        const double* Rc = cam.rot_cw;
-        double tmp[3][3], G3[3][3];
-        for (int i = 0; i < 3; ++i)
-            for (int l = 0; l < 3; ++l)
-                tmp[i][l] = Rc[i * 3 + 0] * gV[0][l] + Rc[i * 3 + 1] * gV[1][l] + Rc[i * 3 + 2] * gV[2][l];
-        for (int i = 0; i < 3; ++i)
-            for (int k = 0; k < 3; ++k)
-                G3[i][k] = tmp[i][0] * Rc[k * 3 + 0] + tmp[i][1] * Rc[k * 3 + 1] + tmp[i][2] * Rc[k * 3 + 2];
-        // mean path through mu2d and J
-        const double x = P.mc[0], y = P.mc[1], z = P.mc[2];
-        const double fx = cam.fx, fy = cam.fy, z2 = z * z, z3 = z2 * z;
-        double gmc[3];
-        gmc[0] = J[0][0] * gm[0] + gJ[0][2] * (-fx / z2);
-        gmc[1] = J[1][1] * gm[1] + gJ[1][2] * (-fy / z2);
-        gmc[2] = J[0][2] * gm[0] + J[1][2] * gm[1] + gJ[0][0] * (-fx / z2) + gJ[1][1] * (-fy / z2) +
-                 gJ[0][2] * (2 * fx * x / z3) + gJ[1][2] * (2 * fy * y / z3);
-        double gmean[3];
-        for (int i = 0; i < 3; ++i) gmean[i] = Rc[i * 3 + 0] * gmc[0] + Rc[i * 3 + 1] * gmc[1] + Rc[i * 3 + 2] * gmc[2];
-        // scales and rotation
-        const double(&Rq)[3][3] = P.Rq;
-        double gls[3];
-        for (int k = 0; k < 3; ++k) {
-            double t = 0;
-            for (int b = 0; b < 3; ++b)
-                for (int c = 0; c < 3; ++c) t += Rq[b][k] * G3[b][c] * Rq[c][k];
-            gls[k] = t * 2.0 * P.S2[k];
+        T u[4];
+        T qn;
+        {
+            const float* qp = m.quaternions + row * 4;
+            const T q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
+            qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+            u[0] = q0 / qn; u[1] = q1 / qn; u[2] = q2 / qn; u[3] = q3 / qn;
         }
-        double gR[3][3];
-        for (int aa = 0; aa < 3; ++aa)
+        const T w = u[0], qx = u[1], qy = u[2], qz = u[3];
+        T Rq[3][3];
+        Rq[0][0] = 1 - 2 * (qy * qy + qz * qz); Rq[0][1] = 2 * (qx * qy - w * qz); Rq[0][2] = 2 * (qx * qz + w * qy);
+        Rq[1][0] = 2 * (qx * qy + w * qz); Rq[1][1] = 1 - 2 * (qx * qx + qz * qz); Rq[1][2] = 2 * (qy * qz - w * qx);
+        Rq[2][0] = 2 * (qx * qz - w * qy); Rq[2][1] = 2 * (qy * qz + w * qx); Rq[2][2] = 1 - 2 * (qx * qx + qy * qy);
+        T nh[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) nh[i] = axis == 0 ? Rq[i][0] : (axis == 1 ? Rq[i][1] : Rq[i][2]);
+        const T sgn_s = nh[0] * -ldir[0] + nh[1] * -ldir[1] + nh[2] * -ldir[2];
+        const T cosv = fabs(sgn_s);
+        const T vis = (T)m.light_visibility[row];
+        T gc[3], albedo[3];
+        T gv[3] = {0, 0, 0};
+        {
+            float sh[3 * B];
+            ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, sh);
+            T Y[B];
+            ss_sh_eval<DEG, T>(vdir, Y);
+            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+#pragma unroll
             for (int c = 0; c < 3; ++c) {
-                double t = 0;
-                for (int b = 0; b < 3; ++b) t += (G3[aa][b] + G3[b][aa]) * Rq[b][c];
-                gR[aa][c] = t * P.S2[c];
+                albedo[c] = (T)SS_SH_C0 * sh[c * B] + (T)0.5;
+                T base = 0;
+                if (L.ambient_bands == 0) {
+#pragma unroll
+                    for (int k = 0; k < B; ++k) base += sh[c * B + k] * Y[k];
+                    base += (T)0.5;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < B; ++k)
+                        if (k < BL) base += (k == 0 ? sh[c * B] + (T)(0.5 / SS_SH_C0) : (T)sh[c * B + k]) *
+                                            (T)L.ambient[c * L.ambient_bands + k];
+#pragma unroll
+                    for (int k = 1; k < B; ++k) base += sh[c * B + k] * Y[k];
+                }
+                const T pre = base + albedo[c] * (T)L.intensity[c] * (cosv * vis);
+                gc[c] = (pre > (T)0 && pre < (T)1) ? g[c] : (T)0;  // clamp mask (optim.py:176-177)
             }
-        double gcos = 0;
-        for (int c = 0; c < 3; ++c) gcos += gc[c] * (S.albedo[c] * L.intensity[c]);
-        gcos *= S.vis;
-        const double gs = gcos * (S.s > 0 ? 1.0 : (S.s < 0 ? -1.0 : 0.0));
-        for (int i = 0; i < 3; ++i) gR[i][S.axis] += gs * -L.direction[i];
-        // quaternion through R(u), u = q/|q|
-        const double w = P.u[0], qx = P.u[1], qy = P.u[2], qz = P.u[3];
-        const double dR[4][3][3] = {
+            if constexpr (DEG > 0) {
+                T coef[B];
+#pragma unroll
+                for (int k = 0; k < B; ++k) coef[k] = sh[k] * gc[0] + sh[B + k] * gc[1] + sh[2 * B + k] * gc[2];
+                ss_sh_grad_dot<DEG, T>(vdir, coef, gv);
+            }
+        }
+        // SH coefficient gradients: written by k_sh_grad from this compact record
+        shrec[row * 2] = make_float4((float)gc[0], (float)gc[1], (float)gc[2], (float)(cosv * vis));
+        shrec[row * 2 + 1] = make_float4((float)vdir[0], (float)vdir[1], (float)vdir[2], 1.0f);
+
+        // ---- geometry: mu_cam, J, Sigma3d, cov (render.py:246-267)
+        T mc[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) mc[k] = d[0] * Rc[0][k] + d[1] * Rc[1][k] + d[2] * Rc[2][k];
+        const T x = mc[0], y = mc[1], z = mc[2];
+        const T iz = (T)1 / z, z2 = z * z;
+        const T J00 = fx * iz, J02 = -fx * x / z2, J11 = fy * iz, J12 = -fy * y / z2;
+        T S2[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) S2[k] = t_exp<T>((T)2 * (T)lsp[k]);
+        T S3[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = i; k < 3; ++k) {
+                S3[i][k] = Rq[i][0] * S2[0] * Rq[k][0] + Rq[i][1] * S2[1] * Rq[k][1] + Rq[i][2] * S2[2] * Rq[k][2];
+                S3[k][i] = S3[i][k];
+            }
+        T tm[3][3], cov[3][3];  // cov = W S3 W^T, W[i][k] = Rc[k][i]
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int l = 0; l < 3; ++l) tm[i][l] = Rc[0][i] * S3[0][l] + Rc[1][i] * S3[1][l] + Rc[2][i] * S3[2][l];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = i; k < 3; ++k) {
+                cov[i][k] = tm[i][0] * Rc[0][k] + tm[i][1] * Rc[1][k] + tm[i][2] * Rc[2][k];
+                cov[k][i] = cov[i][k];
+            }
+        // ---- optim.py:180-195
+        const T g00 = g[6], g01 = g[7], g11 = g[8];
+        T JC0[3], JC1[3];
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            JC0[l] = J00 * cov[0][l] + J02 * cov[2][l];
+            JC1[l] = J11 * cov[1][l] + J12 * cov[2][l];
+        }
+        T gJ0[3], gJ1[3];
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            gJ0[l] = 2 * (g00 * JC0[l] + g01 * JC1[l]);
+            gJ1[l] = 2 * (g01 * JC0[l] + g11 * JC1[l]);
+        }
+        // gV = J^T G2 J (J rows: [J00, 0, J02], [0, J11, J12])
+        const T Jr0[3] = {J00, 0, J02}, Jr1[3] = {0, J11, J12};
+        T JG0[3], JG1[3];
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            JG0[l] = g00 * Jr0[l] + g01 * Jr1[l];
+            JG1[l] = g01 * Jr0[l] + g11 * Jr1[l];
+        }
+        T gV[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int l = 0; l < 3; ++l) gV[k][l] = Jr0[k] * JG0[l] + Jr1[k] * JG1[l];
+        T G3[3][3];  // R_cw gV R_cw^T
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int l = 0; l < 3; ++l) tm[i][l] = Rc[i][0] * gV[0][l] + Rc[i][1] * gV[1][l] + Rc[i][2] * gV[2][l];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) G3[i][k] = tm[i][0] * Rc[k][0] + tm[i][1] * Rc[k][1] + tm[i][2] * Rc[k][2];
+        const T gm0 = g[4], gm1 = g[5];
+        const T z3 = z2 * z;
+        T gmc[3];
+        gmc[0] = J00 * gm0 + gJ0[2] * (-fx / z2);
+        gmc[1] = J11 * gm1 + gJ1[2] * (-fy / z2);
+        gmc[2] = J02 * gm0 + J12 * gm1 + gJ0[0] * (-fx / z2) + gJ1[1] * (-fy / z2) + gJ0[2] * (2 * fx * x / z3) +
+                 gJ1[2] * (2 * fy * y / z3);
+        T gmean[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) gmean[i] = Rc[i][0] * gmc[0] + Rc[i][1] * gmc[1] + Rc[i][2] * gmc[2];
+        if constexpr (DEG > 0) {  // view-direction path (optim.py:235-240)
+            const T vg = vdir[0] * gv[0] + vdir[1] * gv[1] + vdir[2] * gv[2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) gmean[i] += (gv[i] - vdir[i] * vg) / dist;
+        }
+        // ---- scales and rotation (optim.py:204-218)
+        T gls[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            T t = 0;
+#pragma unroll
+            for (int b2 = 0; b2 < 3; ++b2)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) t += Rq[b2][k] * G3[b2][c] * Rq[c][k];
+            gls[k] = t * 2 * S2[k];
+        }
+        T gR[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                T t = 0;
+#pragma unroll
+                for (int b2 = 0; b2 < 3; ++b2) t += (G3[i][b2] + G3[b2][i]) * Rq[b2][c];
+                gR[i][c] = t * S2[c];
+            }
+        T gcos = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gcos += gc[c] * (albedo[c] * (T)L.intensity[c]);
+        gcos *= vis;
+        const T gs = gcos * (sgn_s > 0 ? (T)1 : (sgn_s < 0 ? (T)-1 : (T)0));
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (k == axis) gR[i][k] += gs * -ldir[i];
+        // quaternion through R(u), u = q / |q| (optim.py:87-110)
+        const T dR[4][3][3] = {
             {{0, -2 * qz, 2 * qy}, {2 * qz, 0, -2 * qx}, {-2 * qy, 2 * qx, 0}},
             {{0, 2 * qy, 2 * qz}, {2 * qy, -4 * qx, -2 * w}, {2 * qz, 2 * w, -4 * qx}},
             {{-4 * qy, 2 * qx, 2 * w}, {2 * qx, 0, 2 * qz}, {-2 * w, 2 * qz, -4 * qy}},
             {{-4 * qz, -2 * w, 2 * qx}, {2 * w, -4 * qz, 2 * qy}, {2 * qx, 2 * qy, 0}}};
-        double h[4];
+        T h[4];
+#pragma unroll
         for (int c = 0; c < 4; ++c) {
-            double t = 0;
+            T t = 0;
+#pragma unroll
             for (int i = 0; i < 3; ++i)
+#pragma unroll
                 for (int jj = 0; jj < 3; ++jj) t += gR[i][jj] * dR[c][i][jj];
             h[c] = t;
         }
-        double gq[4];
-        const double udh = P.u[0] * h[0] + P.u[1] * h[1] + P.u[2] * h[2] + P.u[3] * h[3];
-        for (int k = 0; k < 4; ++k) gq[k] = (h[k] - P.u[k] * udh) / P.qn;
-        // appearance: SH coefficients
-        const int64_t off_sh = 11 * a + row * 3 * B;
-        const int BL = L.ambient_bands < B ? L.ambient_bands : B;
-        for (int c = 0; c < 3; ++c) {
-            for (int b = 0; b < B; ++b) {
-                double v;
-                if (L.ambient_bands == 0) v = gc[c] * S.Y[b];
-                else v = (b < BL ? gc[c] * L.ambient[c * L.ambient_bands + b] : 0.0) + (b >= 1 ? gc[c] * S.Y[b] : 0.0);
-                if (b == 0) v += gc[c] * (SS_SH_C0 * L.intensity[c]) * (S.cosv * S.vis);
-                grad[off_sh + c * B + b] += (float)v;
-            }
-        }
-        // view-direction path
-        if (m.sh_degree > 0) {
-            double dY[16][3];
-            ss_sh_grad(S.vdir, m.sh_degree, dY);
-            double gv[3] = {0, 0, 0};
-            for (int c = 0; c < 3; ++c)
-                for (int b = 1; b < B; ++b) {
-                    const double t = sh[c * B + b] * gc[c];
-                    gv[0] += t * dY[b][0];
-                    gv[1] += t * dY[b][1];
-                    gv[2] += t * dY[b][2];
-                }
-            const double vg = S.vdir[0] * gv[0] + S.vdir[1] * gv[1] + S.vdir[2] * gv[2];
-            for (int i = 0; i < 3; ++i) gmean[i] += (gv[i] - S.vdir[i] * vg) / S.dist;
-        }
-        const double op = 1.0 / (1.0 + exp(-(double)m.logit_opacities[row]));
+        const T udh = u[0] * h[0] + u[1] * h[1] + u[2] * h[2] + u[3] * h[3];
+        const T op = (T)1 / ((T)1 + t_exp<T>(-(T)m.logit_opacities[row]));
+#pragma unroll
         for (int i = 0; i < 3; ++i) {
             grad[row * 3 + i] += (float)gmean[i];
             grad[3 * a + row * 3 + i] += (float)gls[i];
         }
-        for (int k = 0; k < 4; ++k) grad[6 * a + row * 4 + k] += (float)gq[k];
-        grad[10 * a + row] += (float)(go * op * (1.0 - op));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) grad[6 * a + row * 4 + k] += (float)((h[k] - u[k] * udh) / qn);
+        grad[10 * a + row] += (float)(g[3] * op * (1 - op));
+    }
+}
+
+// SH coefficient gradients, one thread per (row, channel, basis) entry
+// (ref optim.py:221-233): ambient product, view-dependent basis and the
+// direct-light term through albedo_est = C0 dc + 0.5.
+template <int DEG>
+__global__ void k_sh_grad(ss_light L, const float4* __restrict__ shrec, int64_t a, float* __restrict__ grad_sh) {
+    constexpr int B = ss_sh_bases(DEG);
+    const int64_t n = a * 3 * B;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / (3 * B);
+        const int rem = (int)(e - row * 3 * B), c = rem / B, b = rem - c * B;
+        const float4 r0 = shrec[2 * row];
+        if (r0.x == 0.f && r0.y == 0.f && r0.z == 0.f) continue;  // no colour gradient (or not visible)
+        const float4 r1 = shrec[2 * row + 1];
+        const double gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
+        const double v3[3] = {r1.x, r1.y, r1.z};
+        double Y[B];
+        ss_sh_eval<DEG>(v3, Y);
+        double yb = Y[0];
+#pragma unroll
+        for (int k = 1; k < B; ++k)
+            if (k == b) yb = Y[k];
+        double v;
+        if (L.ambient_bands == 0) {
+            v = gcc * yb;
+        } else {
+            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+            v = (b < BL ? gcc * L.ambient[c * L.ambient_bands + b] : 0.0) + (b >= 1 ? gcc * yb : 0.0);
+        }
+        if (b == 0) v += gcc * (SS_SH_C0 * L.intensity[c]) * (double)r0.w;
+        grad_sh[e] += (float)v;
     }
 }
 
@@ -682,10 +893,11 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     b.rmu = SS_SCRATCH(ctx, double2, na);
     b.roff = SS_SCRATCH(ctx, uint64_t, na);
     b.rcnt = SS_SCRATCH(ctx, uint32_t, na);
+    b.rinv = SS_SCRATCH(ctx, uint32_t, na);
     b.rrec = ss_scratch(ctx, sizeof(SplatRec<R>) * na);
     b.ranges = SS_SCRATCH(ctx, uint2, b.n_tiles);
     uint64_t* total = SS_SCRATCH(ctx, uint64_t, 1);
-    if (!b.dkeys || !b.dvals || !kalt || !valt || !b.perg || !b.rmu || !b.roff || !b.rcnt || !b.rrec || !b.ranges ||
+    if (!b.dkeys || !b.dvals || !kalt || !valt || !b.perg || !b.rmu || !b.roff || !b.rcnt || !b.rinv || !b.rrec || !b.ranges ||
         !total)
         return SS_ERR_CUDA;
     SS_CUDA(ctx, cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.n_tiles, s));
@@ -693,15 +905,24 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     memset(&none, 0, sizeof(none));
     if (n > 0) {
         ss_tic(ctx, KC_PREPROCESS);
-        k_preprocess<<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkeys, b.dvals,
-                                                        b.perg, dbg ? *dbg : none);
+#define SS_PRE(DEG)                                                                                      \
+    k_preprocess<DEG><<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkeys, \
+                                                         b.dvals, b.perg, dbg ? *dbg : none)
+        switch (m->sh_degree) {
+            case 0: SS_PRE(0); break;
+            case 1: SS_PRE(1); break;
+            case 2: SS_PRE(2); break;
+            default: SS_PRE(3); break;
+        }
+#undef SS_PRE
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_PREPROCESS);
         ss_tic(ctx, KC_DEPTH_SORT);
         SS_TRY(ss_radix_sort_u64(ctx, b.dkeys, b.dvals, kalt, valt, n, 64));
         ss_toc(ctx, KC_DEPTH_SORT);
         ss_tic(ctx, KC_BIN);
-        k_count<R><<<gridn(ctx, n), 256, 0, s>>>(b.dkeys, b.dvals, b.perg, n, b.rmu, (SplatRec<R>*)b.rrec, b.rcnt);
+        k_count<R><<<gridn(ctx, n), 256, 0, s>>>(b.dkeys, b.dvals, b.perg, n, b.rmu, (SplatRec<R>*)b.rrec, b.rcnt,
+                                                 b.rinv);
         SS_CHECK_LAUNCH(ctx);
     } else {
         ss_tic(ctx, KC_BIN);
@@ -739,8 +960,9 @@ template <typename R>
 int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bins& b, R* img, R* T,
             uint32_t* tile_stop) {
     ss_tic(ctx, KC_FORWARD);
-    k_blend_fwd<R><<<b.n_tiles, FWD_THREADS, 0, ctx->stream>>>(
-        b.ranges, b.pvals, b.rmu, (const SplatRec<R>*)b.rrec, cam->width, cam->height, b.tiles_x, o->background[0],
+    k_blend_fwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
+        b.ranges, b.pvals, b.rmu, (const SplatRec<R>*)b.rrec, cam->width, cam->height, b.tiles_x, b.n_tiles,
+        o->background[0],
         o->background[1], o->background[2], img, T, tile_stop, ss_timing_on(ctx) ? ctx->dev_counters : nullptr);
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_FORWARD);
@@ -776,17 +998,33 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     SS_TRY(forward<R>(ctx, cam, o, b, img, (R*)nullptr, stop));
     const double inv_npx = 1.0 / (double)(3 * npx);
     ss_tic(ctx, KC_BACKWARD);
-    k_blend_bwd<R><<<b.n_tiles, BWD_THREADS, 0, s>>>(b.ranges, b.pvals, b.rmu, (const SplatRec<R>*)b.rrec, b.roff, stop,
-                                                      cam->width, cam->height, b.tiles_x, img, gt, (double)(3 * npx),
-                                                      partials, tloss);
+    k_blend_bwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, s>>>(
+        b.ranges, b.pvals, b.rmu, (const SplatRec<R>*)b.rrec, b.roff, stop, cam->width, cam->height, b.tiles_x,
+        b.n_tiles, img, gt, (double)(3 * npx), partials, tloss);
     SS_CHECK_LAUNCH(ctx);
     k_loss_reduce<<<1, 256, 0, s>>>(tloss, b.n_tiles, inv_npx, loss);
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_BACKWARD);
     if (b.n_in > 0 && m->active_count > 0) {
         ss_tic(ctx, KC_CHAIN);
-        k_chain<R><<<gridn(ctx, b.n_in, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, b.dkeys, b.dvals, b.roff, b.rcnt,
-                                                           partials, b.n_in, o->extent_cutoff, grad);
+        R* g9 = SS_SCRATCH(ctx, R, 9 * b.n_in);
+        float4* shrec = SS_SCRATCH(ctx, float4, 2 * (int64_t)m->active_count);
+        if (!g9 || !shrec) return SS_ERR_CUDA;
+        SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)m->active_count, s));
+        k_sum_partials<R><<<gridn(ctx, b.n_in), 256, 0, s>>>(b.roff, b.rcnt, partials, b.n_in, g9);
+        SS_CHECK_LAUNCH(ctx);
+#define SS_CHAIN(DEG)                                                                                     \
+    k_chain<R, DEG><<<gridn(ctx, b.n_in, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
+                                                            o->extent_cutoff, grad, shrec);                      \
+    k_sh_grad<DEG><<<gridn(ctx, (int64_t)m->active_count * 3 * ss_sh_bases(DEG)), 256, 0, s>>>(                  \
+        *L, shrec, m->active_count, grad + 11 * (int64_t)m->active_count)
+        switch (m->sh_degree) {
+            case 0: SS_CHAIN(0); break;
+            case 1: SS_CHAIN(1); break;
+            case 2: SS_CHAIN(2); break;
+            default: SS_CHAIN(3); break;
+        }
+#undef SS_CHAIN
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_CHAIN);
     }
