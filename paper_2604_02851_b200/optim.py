@@ -22,7 +22,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _lib
+from . import _lib, parallel
 from .model import TRAINABLE, DeviceModel, as_device
 from .render import _subset_tensor, camera_struct, light_struct, render_opts
 
@@ -267,13 +267,8 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     a = dm.active_count
     n_local = len(ready)
     if process_group is not None:
-        import torch.distributed as dist
-        cnt = torch.tensor([n_local], dtype=torch.int64, device=dm.device)
-        if total_views is None:
-            dist.all_reduce(cnt, group=process_group)
-            total = int(cnt.item())
-        else:
-            total = int(total_views)
+        total = int(total_views) if total_views is not None else \
+            parallel.global_view_count(n_local, process_group, dm.device)
     else:
         total = n_local
     if total == 0:
@@ -285,9 +280,7 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     for v in ready:
         backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub)
     if process_group is not None:
-        import torch.distributed as dist
-        dist.all_reduce(ws.grad, group=process_group)
-        dist.all_reduce(ws.loss, group=process_group)
+        parallel.reduce_gradients(ws.grad, ws.loss, process_group)
     if a > 0:
         c = _lib.ctx(dm.device.index)
         st = _lib.SSAdamState()
