@@ -189,6 +189,31 @@ int ss_encode_delta(ss_ctx* ctx, int32_t attribute_id, const void* cur, int32_t 
                     double gating_threshold, uint8_t* out, uint64_t out_cap, uint64_t* out_len);
 uint64_t ss_delta_bound(int32_t attribute_id, int64_t rows, int32_t dims);
 
+/* One server tick's deltas in one call (ref server.py:488-493 ->
+ * protocol/delta.py:72): three kernel launches whatever the number of jobs,
+ * no host synchronisation.  Inputs may be strided views: element (row, d)
+ * of cur/base is read at  row*row_stride + (d / inner)*outer + d % inner + col0
+ * (row_stride 0 = dims, inner 0 = dims), e.g. SH DC of an (N,3,B) array:
+ * row_stride 3B, inner 1, outer B, col0 0.  new_base is dense (rows, dims). */
+typedef struct {
+    int32_t attribute_id;
+    int32_t in_dtype;        /* 0 float32, 1 float64 */
+    const void* cur;
+    const void* base;        /* MEANS / LOG_SCALES */
+    float* new_base;         /* may alias base when base is dense float32 */
+    int64_t rows;
+    int32_t dims;
+    int32_t inner;
+    int64_t row_stride;
+    int32_t outer;
+    int32_t col0;
+    double gating_threshold;
+    uint8_t* out;
+    uint64_t out_cap;
+    uint64_t* out_len;
+} ss_delta_job;
+int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int32_t njobs);
+
 /* encode_snapshot(): ref protocol/snapshot.py:47 with compression_id 0.
  * profile 0 = quantized, 1 = lossless.  base_means_out / base_log_scales_out
  * (float32, may be NULL) receive the decoded means / log scales -- the

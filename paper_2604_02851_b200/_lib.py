@@ -65,6 +65,12 @@ class SSPrepared(C.Structure):
                 ("capacity", i64)]
 
 
+class SSDeltaJob(C.Structure):
+    _fields_ = [("attribute_id", i32), ("in_dtype", i32), ("cur", vp), ("base", vp), ("new_base", vp),
+                ("rows", i64), ("dims", i32), ("inner", i32), ("row_stride", i64), ("outer", i32), ("col0", i32),
+                ("gating_threshold", f64), ("out", vp), ("out_cap", u64), ("out_len", vp)]
+
+
 class SSOrthoCamera(C.Structure):
     _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("half_width", f64), ("half_height", f64),
                 ("width", i32), ("height", i32)]
@@ -91,6 +97,7 @@ _SIGS = {
     "ss_adam_step": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSAdamState), vp, i32, C.POINTER(SSAdamHparams)]),
     "ss_encode_delta": (i32, [vp, i32, vp, i32, vp, vp, i64, i32, f64, vp, u64, vp]),
     "ss_delta_bound": (u64, [i32, i64, i32]),
+    "ss_encode_delta_batch": (i32, [vp, C.POINTER(SSDeltaJob), i32]),
     "ss_encode_snapshot": (i32, [vp, C.POINTER(SSModel), i32, vp, u64, vp, vp, vp]),
     "ss_snapshot_bound": (u64, [i64, i32, i32]),
     "ss_encode_light_visibility": (i32, [vp, vp, i64, vp, u64, vp]),

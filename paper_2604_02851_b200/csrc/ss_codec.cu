@@ -1,6 +1,7 @@
 // Bit-exact wire encoders (compression_id 0) for the splatstream protocol.
 //
 //   ss_encode_delta     ref pkg/src/splatstream/protocol/delta.py:72-137
+//                       (a one-job ss_encode_delta_batch, ss_delta_tick.cu)
 //   ss_encode_snapshot  ref protocol/snapshot.py:47-82 (+ server baseline
 //                       reset, server.py:481-484, computed from the codes)
 //   ss_encode_light_visibility  ref protocol/packets.py:73-76
@@ -105,169 +106,6 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
-// ---------------------------------------------------------------- residual
-struct ResidState {
-    unsigned long long count;    // rows with max|r| >= gate
-    unsigned long long max_all;  // bits of max |r| over all rows (>= 0 doubles order as ints)
-    unsigned long long max_keep; // bits of max |r| over gated rows
-    unsigned long long varint_bytes;
-    int mode;                    // 0 dense, 1 sparse
-    int bits;
-    double m;                    // f32-rounded symmetric range
-};
-
-template <typename T>
-__global__ void k_resid_stats(const T* __restrict__ cur, const T* __restrict__ base, int64_t rows, int dims,
-                              double gate, uint8_t* __restrict__ keep, ResidState* st) {
-    unsigned long long cnt = 0, mall = 0, mkeep = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
-        double rmax = 0.0;
-        for (int d = 0; d < dims; ++d) {
-            double r = ds(ld(cur, i * dims + d), ld(base, i * dims + d));
-            rmax = fmax(rmax, fabs(r));
-        }
-        bool k = rmax >= gate;
-        keep[i] = k;
-        unsigned long long b = (unsigned long long)__double_as_longlong(rmax);
-        cnt += k;
-        mall = b > mall ? b : mall;
-        if (k) mkeep = b > mkeep ? b : mkeep;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    mall = warp_max_u64(mall);
-    mkeep = warp_max_u64(mkeep);
-    if ((threadIdx.x & 31) == 0) {
-        if (cnt) atomicAdd(&st->count, cnt);
-        atomicMax(&st->max_all, mall);
-        atomicMax(&st->max_keep, mkeep);
-    }
-}
-
-__global__ void k_resid_decide(ResidState* st, int64_t rows, int bits) {
-    const unsigned long long k = st->count;
-    const bool sparse = 2 * (int64_t)k < rows;  // k < rows * 0.5 (delta.py:101)
-    double m;
-    if (sparse) m = k ? (double)__double2float_rn(__longlong_as_double((long long)st->max_keep)) : 0.0;
-    else m = rows ? (double)__double2float_rn(__longlong_as_double((long long)st->max_all)) : 0.0;
-    st->mode = sparse ? 1 : 0;
-    st->m = m;
-    st->bits = bits;
-}
-
-template <typename T>
-__global__ void k_resid_dense(const T* __restrict__ cur, const T* __restrict__ base, int64_t n, int bits,
-                              const ResidState* st, uint8_t* __restrict__ block, float* __restrict__ new_base) {
-    if (st->mode != 0) return;
-    const double m = st->m, lo = -m;
-    const int cb = bits / 8;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        double b = ld(base, e);
-        double r = ds(ld(cur, e), b);
-        uint32_t code = quantize(r, lo, m, bits);
-        put_code(block + e * cb, code, bits);
-        if (new_base) new_base[e] = __double2float_rn(da(b, dequantize(code, lo, m, bits)));
-    }
-}
-
-template <typename T>
-__global__ void k_copy_base(const T* __restrict__ base, int64_t n, const ResidState* st, float* __restrict__ out) {
-    if (st->mode != 1) return;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-        out[e] = (float)base[e];
-}
-
-__global__ void k_sparse_compact(const uint8_t* __restrict__ keep, const uint64_t* __restrict__ pos, int64_t rows,
-                                 const ResidState* st, uint32_t* __restrict__ idx) {
-    if (st->mode != 1) return;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
-        if (keep[i]) idx[pos[i]] = (uint32_t)i;
-}
-
-__global__ void k_sparse_lens(const uint32_t* __restrict__ idx, int64_t rows, const ResidState* st,
-                              uint32_t* __restrict__ lens) {
-    const int64_t k = st->mode == 1 ? (int64_t)st->count : 0;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < rows; s += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t L = 0;
-        if (s < k) {
-            int64_t prev = s ? (int64_t)idx[s - 1] : -1;
-            L = varint_len((uint64_t)((int64_t)idx[s] - prev - 1));
-        }
-        lens[s] = L;
-    }
-}
-
-template <typename T>
-__global__ void k_sparse_write(const T* __restrict__ cur, const T* __restrict__ base, int dims, int bits,
-                               const uint32_t* __restrict__ idx, const uint64_t* __restrict__ voff, int64_t rows,
-                               const ResidState* st, uint8_t* __restrict__ block, float* __restrict__ new_base) {
-    if (st->mode != 1) return;
-    const int64_t k = (int64_t)st->count;
-    const uint64_t V = st->varint_bytes;
-    const double m = st->m, lo = -m;
-    const int cb = bits / 8;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < k; s += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = idx[s];
-        const int64_t prev = s ? (int64_t)idx[s - 1] : -1;
-        varint_put(block + voff[s], (uint64_t)(i - prev - 1));
-        uint8_t* cp = block + V + (uint64_t)s * dims * cb;
-        for (int d = 0; d < dims; ++d) {
-            double b = ld(base, i * dims + d);
-            double r = ds(ld(cur, i * dims + d), b);
-            uint32_t code = quantize(r, lo, m, bits);
-            put_code(cp + d * cb, code, bits);
-            if (new_base) new_base[i * dims + d] = __double2float_rn(da(b, dequantize(code, lo, m, bits)));
-        }
-    }
-}
-
-__global__ void k_resid_header(ResidState* st, const uint64_t* varint_total, int attr, int dims, int64_t rows,
-                               uint8_t* out, uint64_t* out_len) {
-    const int sparse = st->mode == 1;
-    const uint64_t k = st->count;
-    const int cb = st->bits / 8;
-    uint64_t V = 0;
-    if (sparse) V = *varint_total;
-    st->varint_bytes = V;
-    const uint64_t blen = sparse ? V + k * dims * cb : (uint64_t)rows * dims * cb;
-    out[0] = (uint8_t)attr;
-    out[1] = (uint8_t)(sparse ? 1 : 0);
-    out[2] = 0;  // compression id: raw
-    out[3] = (uint8_t)dims;
-    put_u32(out + 4, (uint32_t)rows);
-    const float mf = (float)st->m;
-    put_f32(out + 8, -mf);
-    put_f32(out + 12, mf);
-    int h = 16;
-    if (sparse) {
-        put_u32(out + 16, (uint32_t)k);
-        h = 20;
-    }
-    put_u32(out + h, (uint32_t)blen);
-    *out_len = h + 4 + blen;
-}
-
-// ---------------------------------------------------------------- absolute
-template <typename T>
-__global__ void k_abs_bytes(const T* __restrict__ x, int64_t n, QSpec q, uint8_t* __restrict__ block) {
-    const int cb = q.bits / 8;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-        put_code(block + e * cb, quantize(ld(x, e), q.lo, q.hi, q.bits), q.bits);
-}
-
-// 10-bit LSB-first: every 4 codes form exactly 5 bytes (n % 4 == 0 here)
-template <typename T>
-__global__ void k_abs_pack10(const T* __restrict__ x, int64_t groups, QSpec q, uint8_t* __restrict__ block) {
-    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t w = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) w |= (uint64_t)quantize(ld(x, g * 4 + j), q.lo, q.hi, 10) << (10 * j);
-        uint8_t* p = block + g * 5;
-#pragma unroll
-        for (int b = 0; b < 5; ++b) p[b] = (uint8_t)(w >> (8 * b));
-    }
-}
-
 // 1-bit LSB-first of (v >= 0.5): one byte per 8 elements
 template <typename T>
 __global__ void k_abs_pack1(const T* __restrict__ x, int64_t n, uint8_t* __restrict__ block) {
@@ -282,89 +120,11 @@ __global__ void k_abs_pack1(const T* __restrict__ x, int64_t n, uint8_t* __restr
     }
 }
 
-__global__ void k_abs_header(int attr, int dims, int64_t rows, uint64_t blen, uint8_t* out, uint64_t* out_len) {
-    out[0] = (uint8_t)attr;
-    out[1] = 2;
-    out[2] = 0;
-    out[3] = (uint8_t)dims;
-    put_u32(out + 4, (uint32_t)rows);
-    put_u32(out + 8, (uint32_t)blen);
-    *out_len = 12 + blen;
-}
-
 inline int grid_for(ss_ctx* ctx, int64_t n, int block = 256) {
     int64_t g = (n + block - 1) / block;
     int64_t cap = (int64_t)ctx->num_sms * 16;
     if (g > cap) g = cap;
     return g < 1 ? 1 : (int)g;
-}
-
-template <typename T>
-int encode_delta_t(ss_ctx* ctx, int attr, const T* cur, const T* base, float* new_base, int64_t rows, int dims,
-                   double gate, uint8_t* out, uint64_t* out_len) {
-    const QSpec q = qspec(attr);
-    const int64_t n = rows * dims;
-    cudaStream_t s = ctx->stream;
-    if (attr == A_MEANS || attr == A_LS) {
-        ResidState* st = SS_SCRATCH(ctx, ResidState, 1);
-        uint8_t* keep = SS_SCRATCH(ctx, uint8_t, rows);
-        uint64_t* pos = SS_SCRATCH(ctx, uint64_t, rows);
-        uint32_t* idx = SS_SCRATCH(ctx, uint32_t, rows);
-        uint32_t* lens = SS_SCRATCH(ctx, uint32_t, rows);
-        uint64_t* voff = SS_SCRATCH(ctx, uint64_t, rows);
-        uint64_t* vtot = SS_SCRATCH(ctx, uint64_t, 1);
-        if (!st || !keep || !pos || !idx || !lens || !voff || !vtot) return SS_ERR_CUDA;
-        SS_CUDA(ctx, cudaMemsetAsync(st, 0, sizeof(ResidState), s));
-        if (rows) {
-            k_resid_stats<T><<<grid_for(ctx, rows), 256, 0, s>>>(cur, base, rows, dims, gate, keep, st);
-            SS_CHECK_LAUNCH(ctx);
-        }
-        k_resid_decide<<<1, 1, 0, s>>>(st, rows, q.bits);
-        SS_CHECK_LAUNCH(ctx);
-        // the block starts after a 20-byte (dense) or 24-byte (sparse) header;
-        // both paths are launched and each exits unless its mode was chosen
-        if (n) {
-            k_resid_dense<T><<<grid_for(ctx, n), 256, 0, s>>>(cur, base, n, q.bits, st, out + 20, new_base);
-            SS_CHECK_LAUNCH(ctx);
-            if (new_base && (void*)new_base != (const void*)base) {
-                k_copy_base<T><<<grid_for(ctx, n), 256, 0, s>>>(base, n, st, new_base);
-                SS_CHECK_LAUNCH(ctx);
-            }
-            SS_TRY(ss_scan_u8_to_u64(ctx, keep, pos, rows, nullptr));
-            k_sparse_compact<<<grid_for(ctx, rows), 256, 0, s>>>(keep, pos, rows, st, idx);
-            SS_CHECK_LAUNCH(ctx);
-            k_sparse_lens<<<grid_for(ctx, rows), 256, 0, s>>>(idx, rows, st, lens);
-            SS_CHECK_LAUNCH(ctx);
-            SS_TRY(ss_scan_u32_to_u64(ctx, lens, voff, rows, vtot));
-        } else {
-            SS_CUDA(ctx, cudaMemsetAsync(vtot, 0, sizeof(uint64_t), s));
-        }
-        k_resid_header<<<1, 1, 0, s>>>(st, vtot, attr, dims, rows, out, out_len);
-        SS_CHECK_LAUNCH(ctx);
-        if (n) {
-            k_sparse_write<T><<<grid_for(ctx, rows), 256, 0, s>>>(cur, base, dims, q.bits, idx, voff, rows, st,
-                                                                   out + 24, new_base);
-            SS_CHECK_LAUNCH(ctx);
-        }
-        return SS_OK;
-    }
-    uint8_t* block = out + 12;
-    uint64_t blen;
-    if (attr == A_VIS) {
-        blen = (uint64_t)(n + 7) / 8;
-        if (n) k_abs_pack1<T><<<grid_for(ctx, (n + 7) / 8), 256, 0, s>>>(cur, n, block);
-    } else if (q.bits == 10) {
-        if (n % 4) return ss_fail(ctx, SS_ERR_INVALID, "10-bit pack needs a multiple of 4 codes");
-        blen = (uint64_t)n / 4 * 5;
-        if (n) k_abs_pack10<T><<<grid_for(ctx, n / 4), 256, 0, s>>>(cur, n / 4, q, block);
-    } else {
-        blen = (uint64_t)n * (q.bits / 8);
-        if (n) k_abs_bytes<T><<<grid_for(ctx, n), 256, 0, s>>>(cur, n, q, block);
-    }
-    SS_CHECK_LAUNCH(ctx);
-    k_abs_header<<<1, 1, 0, s>>>(attr, dims, rows, blen, out, out_len);
-    SS_CHECK_LAUNCH(ctx);
-    return SS_OK;
 }
 
 // ---------------------------------------------------------------- snapshot
@@ -505,22 +265,21 @@ int ss_encode_delta(ss_ctx* ctx, int32_t attr, const void* cur, int32_t in_dtype
                     float* new_base, int64_t rows, int32_t dims, double gate, uint8_t* out, uint64_t out_cap,
                     uint64_t* out_len) {
     if (!ctx) return SS_ERR_INVALID;
-    if (attr < 0 || attr > A_VIS) return ss_fail(ctx, SS_ERR_PROTOCOL, "unknown attribute id %d", attr);
-    if (rows < 0 || dims < 1 || dims > 255) return ss_fail(ctx, SS_ERR_INVALID, "bad shape rows=%lld dims=%d",
-                                                           (long long)rows, dims);
-    if (rows > (int64_t)UINT32_MAX) return ss_fail(ctx, SS_ERR_INVALID, "too many rows");
-    const bool resid = attr == A_MEANS || attr == A_LS;
-    if (resid && !base && rows > 0) return ss_fail(ctx, SS_ERR_INVALID, "attribute %d is residual-coded and needs a baseline", attr);
-    if (out_cap < ss_delta_bound(attr, rows, dims)) return ss_fail(ctx, SS_ERR_CAPACITY, "delta output too small");
-    SS_TRY(ss_scratch_reset(ctx));
     if (in_dtype != 0 && in_dtype != 1) return ss_fail(ctx, SS_ERR_INVALID, "in_dtype must be 0 (f32) or 1 (f64)");
-    ss_tic(ctx, KC_CODEC);
-    int rc = in_dtype == 0 ? encode_delta_t<float>(ctx, attr, (const float*)cur, (const float*)base, new_base, rows,
-                                                   dims, gate, out, out_len)
-                           : encode_delta_t<double>(ctx, attr, (const double*)cur, (const double*)base, new_base,
-                                                    rows, dims, gate, out, out_len);
-    ss_toc(ctx, KC_CODEC);
-    return rc;
+    ss_delta_job j;
+    memset(&j, 0, sizeof(j));
+    j.attribute_id = attr;
+    j.in_dtype = in_dtype;
+    j.cur = cur;
+    j.base = base;
+    j.new_base = new_base;
+    j.rows = rows;
+    j.dims = dims;
+    j.gating_threshold = gate;
+    j.out = out;
+    j.out_cap = out_cap;
+    j.out_len = out_len;
+    return ss_encode_delta_batch(ctx, &j, 1);
 }
 
 uint64_t ss_snapshot_bound(int64_t n, int32_t degree, int32_t profile) {

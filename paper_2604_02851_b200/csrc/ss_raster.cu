@@ -824,33 +824,44 @@ __global__ void __launch_bounds__(128) k_chain(ss_model m, ss_camera cam, ss_lig
 // SH coefficient gradients, one thread per (row, channel, basis) entry
 // (ref optim.py:221-233): ambient product, view-dependent basis and the
 // direct-light term through albedo_est = C0 dc + 0.5.
+constexpr int SHG_ROWS = 64;  // rows per block in k_sh_grad
+
 template <int DEG>
-__global__ void k_sh_grad(ss_light L, const float4* __restrict__ shrec, int64_t a, float* __restrict__ grad_sh) {
+__global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __restrict__ shrec, int64_t a,
+                                                 float* __restrict__ grad_sh) {
     constexpr int B = ss_sh_bases(DEG);
-    const int64_t n = a * 3 * B;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = e / (3 * B);
-        const int rem = (int)(e - row * 3 * B), c = rem / B, b = rem - c * B;
-        const float4 r0 = shrec[2 * row];
-        if (r0.x == 0.f && r0.y == 0.f && r0.z == 0.f) continue;  // no colour gradient (or not visible)
-        const float4 r1 = shrec[2 * row + 1];
-        const double gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
-        const double v3[3] = {r1.x, r1.y, r1.z};
-        double Y[B];
-        ss_sh_eval<DEG>(v3, Y);
-        double yb = Y[0];
+    __shared__ float s_y[SHG_ROWS][B + 1];
+    __shared__ float4 s_r0[SHG_ROWS];
+    const int64_t row0 = (int64_t)blockIdx.x * SHG_ROWS;
+    const int nrows = (int)min((int64_t)SHG_ROWS, a - row0);
+    if (threadIdx.x < nrows) {  // one thread per row: the basis values once
+        const float4 r0 = shrec[2 * (row0 + threadIdx.x)];
+        const float4 r1 = shrec[2 * (row0 + threadIdx.x) + 1];
+        const float v[3] = {r1.x, r1.y, r1.z};
+        float Y[B];
+        ss_sh_eval<DEG, float>(v, Y);
 #pragma unroll
-        for (int k = 1; k < B; ++k)
-            if (k == b) yb = Y[k];
-        double v;
+        for (int k = 0; k < B; ++k) s_y[threadIdx.x][k] = Y[k];
+        s_r0[threadIdx.x] = r0;
+    }
+    __syncthreads();
+    const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+    const int n = nrows * 3 * B;
+    float* out = grad_sh + row0 * 3 * B;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {  // coalesced over the block's contiguous rows
+        const int r = e / (3 * B), rem = e - r * 3 * B, c = rem / B, b = rem - c * B;
+        const float4 r0 = s_r0[r];
+        const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
+        if (gcc == 0.f) continue;  // clamped colour or row not visible in this view
+        const float yb = s_y[r][b];
+        float v;
         if (L.ambient_bands == 0) {
             v = gcc * yb;
         } else {
-            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
-            v = (b < BL ? gcc * L.ambient[c * L.ambient_bands + b] : 0.0) + (b >= 1 ? gcc * yb : 0.0);
+            v = (b < BL ? gcc * (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? gcc * yb : 0.f);
         }
-        if (b == 0) v += gcc * (SS_SH_C0 * L.intensity[c]) * (double)r0.w;
-        grad_sh[e] += (float)v;
+        if (b == 0) v += gcc * (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
+        out[e] += v;
     }
 }
 
@@ -1016,7 +1027,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
 #define SS_CHAIN(DEG)                                                                                     \
     k_chain<R, DEG><<<gridn(ctx, b.n_in, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
                                                             o->extent_cutoff, grad, shrec);                      \
-    k_sh_grad<DEG><<<gridn(ctx, (int64_t)m->active_count * 3 * ss_sh_bases(DEG)), 256, 0, s>>>(                  \
+    k_sh_grad<DEG><<<(unsigned)(((int64_t)m->active_count + SHG_ROWS - 1) / SHG_ROWS), 256, 0, s>>>(             \
         *L, shrec, m->active_count, grad + 11 * (int64_t)m->active_count)
         switch (m->sh_degree) {
             case 0: SS_CHAIN(0); break;

@@ -175,6 +175,69 @@ def encode_delta_device(attribute_id, current, baseline=None, new_baseline=None,
     return out
 
 
+class DeltaTicker:
+    """One server tick's deltas for a DeviceModel in ONE library call
+    (3 kernel launches, no host sync): attributes in emission order (ref
+    server.py:67-74, 488-493), residual baselines advanced in place, payloads
+    into `outs[attr]` (PayloadBuffer).  SH DC / SH rest are read in place from
+    the (N, 3, B) coefficients.  The ctypes job array is built once per set of
+    attributes, so a 60 Hz loop pays one foreign call per tick."""
+
+    def __init__(self, model, baselines, outs, gating=None):
+        self.model, self.baselines, self.outs, self.gating = model, baselines, outs, gating
+        self._jobs = {}
+        self._ctx = _lib.ctx(model.device.index)
+
+    def _build(self, attributes):
+        model = self.model
+        a = model.active_count
+        B = (model.sh_degree + 1) ** 2
+        jobs = (_lib.SSDeltaJob * len(attributes))()
+        for i, attr in enumerate(attributes):
+            attr = AttributeId(attr)
+            j = jobs[i]
+            j.attribute_id = int(attr)
+            j.in_dtype = 0
+            j.rows = a
+            j.gating_threshold = DEFAULT_GATING.get(attr, 0.0) if self.gating is None else float(self.gating)
+            if attr == AttributeId.MEANS or attr == AttributeId.LOG_SCALES:
+                src = model.means if attr == AttributeId.MEANS else model.log_scales
+                base = self.baselines[int(attr)]
+                j.cur, j.base, j.new_base, j.dims = src.data_ptr(), base.data_ptr(), base.data_ptr(), 3
+            elif attr == AttributeId.QUATERNIONS:
+                j.cur, j.dims = model.quaternions.data_ptr(), 4
+            elif attr == AttributeId.LOGIT_OPACITIES:
+                j.cur, j.dims = model.logit_opacities.data_ptr(), 1
+            elif attr == AttributeId.SH_DC:
+                j.cur, j.dims, j.row_stride, j.inner, j.outer, j.col0 = model.sh_coeffs.data_ptr(), 3, 3 * B, 1, B, 0
+            elif attr == AttributeId.SH_REST:
+                if B == 1:
+                    raise ValueError("sh_rest needs sh_degree > 0")
+                j.cur, j.dims, j.row_stride, j.inner, j.outer, j.col0 = (model.sh_coeffs.data_ptr(), 3 * (B - 1),
+                                                                         3 * B, B - 1, B, 1)
+            else:
+                j.cur, j.dims = model.light_visibility.data_ptr(), 1
+            buf = self.outs[int(attr)]
+            buf.ensure(int(self._ctx.lib.ss_delta_bound(int(attr), a, j.dims)))
+            j.out, j.out_cap, j.out_len = buf.data.data_ptr(), buf.data.numel(), buf.length.data_ptr()
+        return jobs
+
+    def __call__(self, attributes):
+        key = tuple(int(x) for x in attributes)
+        jobs = self._jobs.get(key)
+        if jobs is None:
+            jobs = self._jobs[key] = self._build(key)
+        c = self._ctx
+        c.bind_stream()
+        c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
+        return self.model.active_count * len(key)
+
+
+def delta_tick_device(model, attributes, baselines, outs, gating=None):
+    """One-shot DeltaTicker call (see DeltaTicker)."""
+    return DeltaTicker(model, baselines, outs, gating)(attributes)
+
+
 def encode_delta(attribute_id, current, baseline=None, gating_threshold=None, compression_id: int = COMPRESSION_ZLIB):
     """ref protocol/delta.py:72 -- returns (payload bytes, new baseline or None).
 
