@@ -93,12 +93,59 @@ def _gt_tensor(view, device):
     return t.contiguous()
 
 
+_COPY_STREAMS = {}
+
+
+def _stage_ground_truth(views, device):
+    """Device ground truth per view.  Host images (pinned CPU tensors or
+    numpy) are all uploaded up front on a side stream, each view's kernels
+    waiting only for its own copy, so H2D overlaps the previous views'
+    backward passes."""
+    import torch
+    if all(isinstance(v.image, torch.Tensor) and v.image.is_cuda for v in views):
+        return [_gt_tensor(v, device) for v in views]
+    cur = torch.cuda.current_stream(device)
+    cs = _COPY_STREAMS.get(device.index)
+    if cs is None:
+        cs = _COPY_STREAMS[device.index] = torch.cuda.Stream(device)
+    cs.wait_stream(cur)
+    out = []
+    with torch.cuda.stream(cs):
+        for v in views:
+            img = v.image
+            if not isinstance(img, torch.Tensor):
+                img = torch.from_numpy(np.ascontiguousarray(img, np.float32))
+            t = img.to(device=device, dtype=torch.float32, non_blocking=True).contiguous()
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            out.append((t, ev))
+    staged = []
+    for t, ev in out:
+        t.record_stream(cur)
+        staged.append((t, ev))
+    return [_Pending(t, ev, cur) for t, ev in staged]
+
+
+class _Pending:
+    """A device tensor whose producing copy must complete before use."""
+
+    def __init__(self, t, ev, stream):
+        self.t, self.ev, self.stream = t, ev, stream
+
+    def wait(self):
+        self.stream.wait_event(self.ev)
+        return self.t
+
+
 def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subset=None, extent_cutoff=True,
-                    precision=0, image_out=None, subset_tensor=None):
+                    precision=0, image_out=None, subset_tensor=None, gt=None):
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
     its loss into `loss_accum` (float64 CUDA scalar)."""
     c = _lib.ctx(model.device.index)
-    gt = _gt_tensor(view, model.device)
+    if gt is None:
+        gt = _gt_tensor(view, model.device)
+    elif isinstance(gt, _Pending):
+        gt = gt.wait()
     sub = subset_tensor if subset_tensor is not None else _subset_tensor(index_subset, model.device)
     st = _lib.SSRenderStats()
     c.check(c.lib.ss_backward(c.handle, model.struct(), camera_struct(view.pose, view.intrinsics),
@@ -277,8 +324,9 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     ws.grad.zero_()
     ws.loss.zero_()
     sub = _subset_tensor(index_subset, dm.device)
-    for v in ready:
-        backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub)
+    gts = _stage_ground_truth(ready, dm.device)
+    for v, gt in zip(ready, gts):
+        backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub, gt=gt)
     if process_group is not None:
         parallel.reduce_gradients(ws.grad, ws.loss, process_group)
     if a > 0:
