@@ -203,7 +203,16 @@ template <> __device__ __forceinline__ float ss_exp<float>(float x) { return __e
 template <> __device__ __forceinline__ double ss_exp<double>(double x) { return exp(x); }
 
 template <typename R> __device__ __forceinline__ R ss_rcp(R x);
-template <> __device__ __forceinline__ float ss_rcp<float>(float x) { return __fdividef(1.0f, x); }
+template <> __device__ __forceinline__ float ss_rcp<float>(float x) {  // x = 1 - alpha >= 0.001
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ss_ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 template <> __device__ __forceinline__ double ss_rcp<double>(double x) { return 1.0 / x; }
 
 // Staged splat.  fp32: centre relative to the tile origin (rounded from the
@@ -270,23 +279,31 @@ __device__ __forceinline__ R gauss_power(const Staged<R>& s, R dx, R dy) {
 // reference's exact expression (render.py:311).
 template <typename R>
 struct PixelGeom {
-    R dx, dy0, Ax2, Bx2, adx0, bdx0;
+    // fp32: exponent pre-scaled by K = -0.5 log2(e) so G = ex2((cK y + BK) y + AK)
+    R dx, dy0, Ax2, Bx2, adx0, bdx0, cK;
     __device__ __forceinline__ PixelGeom(const Staged<R>& s, int lx, int ly0, int X0, int Y0) {
         R dyy;
         deltas(s, lx, ly0, X0, Y0, dx, dyy);
         dy0 = dyy;
-        Ax2 = s.a * dx * dx;
-        Bx2 = (R)2 * s.b * dx;
         adx0 = s.a * dx;
         bdx0 = s.b * dx;
+        if (sizeof(R) == 4) {
+            const R K = (R)(-0.5 * 1.4426950408889634);
+            Ax2 = adx0 * dx * K;
+            Bx2 = (R)2 * bdx0 * K;
+            cK = s.c * K;
+        } else {
+            Ax2 = s.a * dx * dx;
+            Bx2 = (R)2 * s.b * dx;
+            cK = s.c;
+        }
     }
     __device__ __forceinline__ R dy(int q) const { return dy0 + (R)(2 * q); }
-    __device__ __forceinline__ R power(const Staged<R>& s, int q) const {
+    __device__ __forceinline__ R gauss(const Staged<R>& s, int q) const {
         const R y = dy(q);
-        if (sizeof(R) == 4) return (R)-0.5 * ((s.c * y + Bx2) * y + Ax2);
-        return gauss_power(s, dx, y);
+        if constexpr (sizeof(R) == 4) return ss_ex2((cK * y + Bx2) * y + Ax2);
+        else return ss_exp<R>(gauss_power(s, dx, y));
     }
-    __device__ __forceinline__ R gauss(const Staged<R>& s, int q) const { return ss_exp<R>(power(s, q)); }
 };
 
 // ---------------------------------------------------------------- K5 forward
@@ -345,10 +362,8 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
                 C1[q] += w * s.c1;
                 C2[q] += w * s.c2;
                 T[q] -= w;  // T (1 - alpha)
-            }
-#pragma unroll
-            for (int q = 0; q < PPT; ++q)
                 if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+            }
         }
         __syncwarp();
     }
@@ -518,10 +533,8 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict_
                     acc[7] += gpx * ady;
                     acc[8] += gpy * ady;
                     T[q] -= w;
-                }
-#pragma unroll
-                for (int q = 0; q < PPT; ++q)
                     if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+                }
             }
             R* out = partials + (uint64_t)(uint32_t)s.p * 9;
             if (__any_sync(0xffffffffu, act != 0)) {
