@@ -50,7 +50,8 @@ struct Bins {
     int64_t visible;
     int64_t pairs;
     int tiles_x, tiles_y, n_tiles, tile_bits;
-    uint64_t* dkeys;         // [n_in] depth keys, sorted
+    uint64_t* dkey64;        // [n_in] exact depth key (fp64 bits, ~0 = culled), by input index j
+    uint32_t* dkeys;         // [n_in] 32-bit depth keys, sorted (0xffffffff = culled)
     uint32_t* dvals;         // [n_in] input index j, sorted by depth
     PerG* perg;              // [n_in]
     double2* rmu;            // [n_in] rank-ordered mu2d
@@ -81,7 +82,8 @@ __global__ void k_visible_flags(ss_model m, ss_camera cam, const int64_t* subset
 template <int DEG>
 __global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
                              int cutoff, uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
-                             PerG* __restrict__ perg, DebugOut dbg) {
+                             PerG* __restrict__ perg, DebugOut dbg, unsigned long long* __restrict__ kminmax) {
+    unsigned long long kmin = ~0ull, kmax = 0;
     constexpr int B = ss_sh_bases(DEG);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = subset ? subset[j] : j;
@@ -93,6 +95,8 @@ __global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, s
             continue;
         }
         dkeys[j] = (uint64_t)__double_as_longlong(P.mc[2]);  // z >= near > 0: bits order as the value
+        kmin = min(kmin, (unsigned long long)dkeys[j]);
+        kmax = max(kmax, (unsigned long long)dkeys[j]);
         ss_project(cam, m.log_scales + row * 3, m.quaternions + row * 4, cutoff != 0, P);
         Shade<DEG> S;
         ss_shade<DEG>(L, m.log_scales + row * 3, m.sh_coeffs + row * 3 * B, m.light_visibility[row], P.d, P.Rq, S);
@@ -121,6 +125,64 @@ __global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, s
             if (o.shade_s) o.shade_s[v] = S.s;
         }
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = min(kmin, a);
+        kmax = max(kmax, b);
+    }
+    if ((threadIdx.x & 31) == 0 && kmin != ~0ull) {
+        atomicMin(&kminmax[0], kmin);
+        atomicMax(&kminmax[1], kmax);
+    }
+}
+
+__global__ void k_init_minmax(unsigned long long* kminmax) {
+    kminmax[0] = ~0ull;
+    kminmax[1] = 0ull;
+}
+
+// 32-bit depth keys: the exact fp64-bit key minus the minimum, shifted so the
+// range fits 32 bits.  The shift can merge nearly equal depths; k_fix_ties
+// restores the exact order inside such runs.
+__global__ void k_key32(const uint64_t* __restrict__ dkey64, int64_t n, const unsigned long long* __restrict__ kminmax,
+                        uint32_t* __restrict__ key32) {
+    const unsigned long long lo = kminmax[0], hi = kminmax[1];
+    const unsigned long long range = hi > lo ? hi - lo : 0;
+    const int bits = range ? 64 - __clzll((long long)range) : 0;
+    const int shift = bits > 32 ? bits - 32 : 0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = dkey64[j];
+        uint32_t v = 0xffffffffu;
+        if (k != ~0ull) {
+            const unsigned long long d = (k - lo) >> shift;
+            v = d > 0xfffffffeull ? 0xfffffffeu : (uint32_t)d;
+        }
+        key32[j] = v;
+    }
+}
+
+// Runs of equal 32-bit keys (rare: depths equal to ~2^-32 relative) are put
+// in exact (depth, row) order by one thread each; the sort was stable, so a
+// stable insertion sort on the exact key gives lexsort((rows, depth)).
+__global__ void k_fix_ties(const uint32_t* __restrict__ key32, uint32_t* __restrict__ vals,
+                           const uint64_t* __restrict__ dkey64, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = key32[i];
+        if (k == 0xffffffffu || key32[i + 1] != k || (i > 0 && key32[i - 1] == k)) continue;
+        int64_t e = i + 1;
+        while (e < n && key32[e] == k) ++e;
+        for (int64_t a = i + 1; a < e; ++a) {
+            const uint32_t v = vals[a];
+            const uint64_t kv = dkey64[v];
+            int64_t b = a - 1;
+            while (b >= i && dkey64[vals[b]] > kv) {
+                vals[b + 1] = vals[b];
+                --b;
+            }
+            vals[b + 1] = v;
+        }
+    }
 }
 
 // ---------------------------------------------------------------- K2
@@ -132,12 +194,12 @@ __device__ __forceinline__ void win_tiles(const int w[4], int& tx0, int& tx1, in
 }
 
 template <typename R>
-__global__ void k_count(const uint64_t* __restrict__ dkeys, const uint32_t* __restrict__ dvals,
+__global__ void k_count(const uint64_t* __restrict__ dkey64, const uint32_t* __restrict__ dvals,
                         const PerG* __restrict__ perg, int64_t n_in, double2* __restrict__ rmu,
                         SplatRec<R>* __restrict__ rrec, uint32_t* __restrict__ rcnt, uint32_t* __restrict__ rinv) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = dvals[r];
-        if (dkeys[r] == ~0ull) {
+        if (dkey64[j] == ~0ull) {
             rcnt[r] = 0;
             rinv[j] = ~0u;
             continue;
@@ -909,9 +971,11 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     while ((1 << b.tile_bits) < b.n_tiles) ++b.tile_bits;
     const int64_t n = b.n_in;
     const int64_t na = n > 0 ? n : 1;
-    b.dkeys = SS_SCRATCH(ctx, uint64_t, na);
+    b.dkey64 = SS_SCRATCH(ctx, uint64_t, na);
+    b.dkeys = SS_SCRATCH(ctx, uint32_t, na);
+    unsigned long long* kminmax = SS_SCRATCH(ctx, unsigned long long, 2);
     b.dvals = SS_SCRATCH(ctx, uint32_t, na);
-    uint64_t* kalt = SS_SCRATCH(ctx, uint64_t, na);
+    uint32_t* kalt = SS_SCRATCH(ctx, uint32_t, na);
     uint32_t* valt = SS_SCRATCH(ctx, uint32_t, na);
     b.perg = SS_SCRATCH(ctx, PerG, na);
     b.rmu = SS_SCRATCH(ctx, double2, na);
@@ -921,7 +985,7 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     b.rrec = ss_scratch(ctx, sizeof(SplatRec<R>) * na);
     b.ranges = SS_SCRATCH(ctx, uint2, b.n_tiles);
     uint64_t* total = SS_SCRATCH(ctx, uint64_t, 1);
-    if (!b.dkeys || !b.dvals || !kalt || !valt || !b.perg || !b.rmu || !b.roff || !b.rcnt || !b.rinv || !b.rrec || !b.ranges ||
+    if (!b.dkey64 || !kminmax || !b.dkeys || !b.dvals || !kalt || !valt || !b.perg || !b.rmu || !b.roff || !b.rcnt || !b.rinv || !b.rrec || !b.ranges ||
         !total)
         return SS_ERR_CUDA;
     SS_CUDA(ctx, cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.n_tiles, s));
@@ -929,9 +993,11 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     memset(&none, 0, sizeof(none));
     if (n > 0) {
         ss_tic(ctx, KC_PREPROCESS);
+        k_init_minmax<<<1, 1, 0, s>>>(kminmax);
+        SS_CHECK_LAUNCH(ctx);
 #define SS_PRE(DEG)                                                                                      \
-    k_preprocess<DEG><<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkeys, \
-                                                         b.dvals, b.perg, dbg ? *dbg : none)
+    k_preprocess<DEG><<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
+                                                         b.dvals, b.perg, dbg ? *dbg : none, kminmax)
         switch (m->sh_degree) {
             case 0: SS_PRE(0); break;
             case 1: SS_PRE(1); break;
@@ -942,10 +1008,14 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_PREPROCESS);
         ss_tic(ctx, KC_DEPTH_SORT);
-        SS_TRY(ss_radix_sort_u64(ctx, b.dkeys, b.dvals, kalt, valt, n, 64));
+        k_key32<<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, n, kminmax, b.dkeys);
+        SS_CHECK_LAUNCH(ctx);
+        SS_TRY(ss_radix_sort_u32(ctx, b.dkeys, b.dvals, kalt, valt, n, 32));
+        k_fix_ties<<<gridn(ctx, n), 256, 0, s>>>(b.dkeys, b.dvals, b.dkey64, n);
+        SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_DEPTH_SORT);
         ss_tic(ctx, KC_BIN);
-        k_count<R><<<gridn(ctx, n), 256, 0, s>>>(b.dkeys, b.dvals, b.perg, n, b.rmu, (SplatRec<R>*)b.rrec, b.rcnt,
+        k_count<R><<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, b.dvals, b.perg, n, b.rmu, (SplatRec<R>*)b.rrec, b.rcnt,
                                                  b.rinv);
         SS_CHECK_LAUNCH(ctx);
     } else {
@@ -1060,17 +1130,17 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     return SS_OK;
 }
 
-__global__ void k_order_out(const uint64_t* dkeys, const uint32_t* dvals, const uint64_t* vpos, int64_t n,
+__global__ void k_order_out(const uint64_t* dkey64, const uint32_t* dvals, const uint64_t* vpos, int64_t n,
                             int64_t* order) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-        if (dkeys[r] != ~0ull) order[r] = (int64_t)vpos[dvals[r]];
+        if (dkey64[dvals[r]] != ~0ull) order[r] = (int64_t)vpos[dvals[r]];
 }
 
 __global__ void k_debug_bins(const Bins b, int64_t* order_rows, const int64_t* subset, int64_t* ranges_out,
                              int64_t* pair_rank) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = tid; r < b.n_in; r += nt)
-        if (order_rows && b.dkeys[r] != ~0ull) order_rows[r] = subset ? subset[b.dvals[r]] : (int64_t)b.dvals[r];
+        if (order_rows && b.dkey64[b.dvals[r]] != ~0ull) order_rows[r] = subset ? subset[b.dvals[r]] : (int64_t)b.dvals[r];
     for (int64_t t = tid; t < b.n_tiles; t += nt)
         if (ranges_out) {
             ranges_out[2 * t] = b.ranges[t].x;
@@ -1131,7 +1201,7 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
     Bins b;
     SS_TRY(build_bins<double>(ctx, m, cam, L, o, b, &dbg));
     if (out->order && n > 0) {
-        k_order_out<<<gridn(ctx, n), 256, 0, s>>>(b.dkeys, b.dvals, vpos, n, out->order);
+        k_order_out<<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, b.dvals, vpos, n, out->order);
         SS_CHECK_LAUNCH(ctx);
     }
     if (visible_out) *visible_out = (int64_t)M;

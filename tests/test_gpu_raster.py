@@ -134,3 +134,27 @@ def test_gpu_backward_deterministic():
     np.testing.assert_array_equal(a[2], b[2])
     for name in GROUPS:
         np.testing.assert_array_equal(getattr(a[1], name), getattr(b[1], name))
+
+
+def test_gpu_depth_order_exact_at_scale_with_near_ties():
+    """300k Gaussians over a 3 m depth range (the 32-bit sort key drops ~21
+    low bits there) plus planted depth ties and 1-ulp neighbours: the composite
+    order must still equal the exact lexsort((rows, depth)) of the oracle."""
+    require_gpu()
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.render import tile_bins
+    model = synth.random_field(300_000, 1, 640, 360, seed=11)
+    z = model.means[:, 2]
+    z[1000:1100] = z[0]                                   # exact ties
+    z[2000:2050] = np.nextafter(z[3000], np.float32(10))  # 1-ulp (float32) neighbours
+    z[2050:2100] = z[3000]
+    intr = synth.intrinsics(640, 360)
+    pose = synth.ring_poses(4)[0]
+    rows, ranges, ranks = tile_bins(model, pose, intr)
+    cam = orr.camera(pose, intr)
+    light = dict(direction=np.array([0.0, -1.0, 0.0]), intensity=np.zeros(3), ambient=None)
+    o = orr.prepare(model, cam, light)
+    np.testing.assert_array_equal(rows, o["rows"][o["order"]])
+    b = orr.tile_bins(o, 640, 360)
+    np.testing.assert_array_equal(ranges, b["ranges"])
+    np.testing.assert_array_equal(ranks, b["pair_rank"])
