@@ -191,22 +191,22 @@ __device__ __forceinline__ void ss_sh_grad_dot(const T v[3], const T coef[ss_sh_
     }
 }
 
-template <int DEG>
+template <int DEG, typename T = double>
 struct Shade {
     static constexpr int B = ss_sh_bases(DEG);
-    double vdir[3], dist;
-    double Y[B];
-    int axis;          // normal-proxy axis
-    double nhat[3];    // Rq[:, axis]
-    double s, cosv;    // signed / absolute cosine
-    double albedo[3];
-    double vis;
-    double pre[3];     // colour before the [0,1] clamp
+    T vdir[3], dist;
+    T Y[B];
+    int axis;     // normal-proxy axis
+    T nhat[3];    // Rq[:, axis]
+    T s, cosv;    // signed / absolute cosine
+    T albedo[3];
+    T vis;
+    T pre[3];     // colour before the [0,1] clamp
 };
 
-template <int DEG>
+template <int DEG, typename T>
 __device__ __forceinline__ void ss_shade_v(const ss_light& L, const float* ls, const float* shv, float visf,
-                                           const double d[3], const double Rq[3][3], Shade<DEG>& S);
+                                           const T d[3], const T Rq[3][3], Shade<DEG, T>& S);
 
 // one row's SH coefficients (3 x B floats) into registers, 16-byte loads
 // when the row stride allows it (degrees 1 and 3)
@@ -229,54 +229,44 @@ __device__ __forceinline__ void ss_load_sh(const float* sh, float out[3 * ss_sh_
     }
 }
 
-// ref render.py:175-197 and the normal proxy of render.py:139-151
-template <int DEG>
-__device__ __forceinline__ void ss_shade(const ss_light& L, const float* ls, const float* sh, float visf,
-                                         const double d[3], const double Rq[3][3], Shade<DEG>& S) {
-    float shv[3 * ss_sh_bases(DEG)];
-    ss_load_sh<DEG>(sh, shv);
-    ss_shade_v<DEG>(L, ls, shv, visf, d, Rq, S);
-}
-
-template <int DEG>
+// ref render.py:175-197 and the normal proxy of render.py:139-151, in compute
+// type T (fp64 for the parity path, fp32 for the throughput path; preprocess
+// and chain rule call the same code, so they agree on the clamp mask)
+template <int DEG, typename T>
 __device__ __forceinline__ void ss_shade_v(const ss_light& L, const float* ls, const float* shv, float visf,
-                                           const double d[3], const double Rq[3][3], Shade<DEG>& S) {
+                                           const T d[3], const T Rq[3][3], Shade<DEG, T>& S) {
     constexpr int B = ss_sh_bases(DEG);
     S.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     S.vdir[0] = d[0] / S.dist;
     S.vdir[1] = d[1] / S.dist;
     S.vdir[2] = d[2] / S.dist;
-    const double l0 = ls[0], l1 = ls[1], l2 = ls[2];
+    const double l0 = ls[0], l1 = ls[1], l2 = ls[2];  // axis pick in fp64 for every T
     const double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
     S.axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
 #pragma unroll
     for (int i = 0; i < 3; ++i) S.nhat[i] = S.axis == 0 ? Rq[i][0] : (S.axis == 1 ? Rq[i][1] : Rq[i][2]);
-    S.s = S.nhat[0] * -L.direction[0] + S.nhat[1] * -L.direction[1] + S.nhat[2] * -L.direction[2];
+    S.s = S.nhat[0] * (T)-L.direction[0] + S.nhat[1] * (T)-L.direction[1] + S.nhat[2] * (T)-L.direction[2];
     S.cosv = fabs(S.s);
-    S.vis = visf;
-    ss_sh_eval<DEG>(S.vdir, S.Y);
+    S.vis = (T)visf;
+    ss_sh_eval<DEG, T>(S.vdir, S.Y);
     const int BL = L.ambient_bands < B ? L.ambient_bands : B;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const float* shc = shv + c * B;
-        double coef[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) coef[b] = shc[b];
-        S.albedo[c] = SS_SH_C0 * coef[0] + 0.5;
-        const double direct = S.albedo[c] * L.intensity[c] * (S.cosv * S.vis);
-        double base = 0.0;
+        S.albedo[c] = (T)SS_SH_C0 * (T)shc[0] + (T)0.5;
+        const T direct = S.albedo[c] * (T)L.intensity[c] * (S.cosv * S.vis);
+        T base = 0;
         if (L.ambient_bands == 0) {
 #pragma unroll
-            for (int b = 0; b < B; ++b) base += coef[b] * S.Y[b];
-            base += 0.5;
+            for (int b = 0; b < B; ++b) base += (T)shc[b] * S.Y[b];
+            base += (T)0.5;
         } else {
 #pragma unroll
-            for (int b = 0; b < B; ++b) {
-                if (b < BL) base += (b == 0 ? coef[0] + 0.5 / SS_SH_C0 : coef[b]) * L.ambient[c * L.ambient_bands + b];
-            }
-            double vd = 0.0;
+            for (int b = 0; b < B; ++b)
+                if (b < BL) base += (b == 0 ? (T)shc[0] + (T)(0.5 / SS_SH_C0) : (T)shc[b]) * (T)L.ambient[c * L.ambient_bands + b];
+            T vd = 0;
 #pragma unroll
-            for (int b = 1; b < B; ++b) vd += coef[b] * S.Y[b];
+            for (int b = 1; b < B; ++b) vd += (T)shc[b] * S.Y[b];
             base += vd;
         }
         S.pre[c] = base + direct;

@@ -79,7 +79,7 @@ __global__ void k_visible_flags(ss_model m, ss_camera cam, const int64_t* subset
     }
 }
 
-template <int DEG>
+template <int DEG, typename R>
 __global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
                              int cutoff, uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                              PerG* __restrict__ perg, DebugOut dbg, unsigned long long* __restrict__ kminmax) {
@@ -98,16 +98,27 @@ __global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, s
         kmin = min(kmin, (unsigned long long)dkeys[j]);
         kmax = max(kmax, (unsigned long long)dkeys[j]);
         ss_project(cam, m.log_scales + row * 3, m.quaternions + row * 4, cutoff != 0, P);
-        Shade<DEG> S;
-        ss_shade<DEG>(L, m.log_scales + row * 3, m.sh_coeffs + row * 3 * B, m.light_visibility[row], P.d, P.Rq, S);
+        Shade<DEG, R> S;
+        {
+            float shv[3 * B];
+            ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, shv);
+            const R dR[3] = {(R)P.d[0], (R)P.d[1], (R)P.d[2]};
+            R RqR[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) RqR[i][k] = (R)P.Rq[i][k];
+            ss_shade_v<DEG, R>(L, m.log_scales + row * 3, shv, m.light_visibility[row], dR, RqR, S);
+        }
         PerG g;
         g.mu[0] = P.mu[0];
         g.mu[1] = P.mu[1];
         g.a = P.s11 / P.det;
         g.b = -P.s01 / P.det;
         g.c = P.s00 / P.det;
-        g.o = 1.0 / (1.0 + exp(-(double)m.logit_opacities[row]));
-        for (int c = 0; c < 3; ++c) g.col[c] = fmin(fmax(S.pre[c], 0.0), 1.0);
+        g.o = sizeof(R) == 4 ? (double)(1.0f / (1.0f + expf(-m.logit_opacities[row])))
+                             : 1.0 / (1.0 + exp(-(double)m.logit_opacities[row]));
+        for (int c = 0; c < 3; ++c) g.col[c] = fmin(fmax((double)S.pre[c], 0.0), 1.0);
         ss_window(P, cam.width, cam.height, g.win);
         perg[j] = g;
         if (dbg.vpos) {
@@ -711,39 +722,16 @@ __global__ void __launch_bounds__(128) k_chain(ss_model m, ss_camera cam, ss_lig
         Rq[0][0] = 1 - 2 * (qy * qy + qz * qz); Rq[0][1] = 2 * (qx * qy - w * qz); Rq[0][2] = 2 * (qx * qz + w * qy);
         Rq[1][0] = 2 * (qx * qy + w * qz); Rq[1][1] = 1 - 2 * (qx * qx + qz * qz); Rq[1][2] = 2 * (qy * qz - w * qx);
         Rq[2][0] = 2 * (qx * qz - w * qy); Rq[2][1] = 2 * (qy * qz + w * qx); Rq[2][2] = 1 - 2 * (qx * qx + qy * qy);
-        T nh[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) nh[i] = axis == 0 ? Rq[i][0] : (axis == 1 ? Rq[i][1] : Rq[i][2]);
-        const T sgn_s = nh[0] * -ldir[0] + nh[1] * -ldir[1] + nh[2] * -ldir[2];
-        const T cosv = fabs(sgn_s);
-        const T vis = (T)m.light_visibility[row];
-        T gc[3], albedo[3];
+        T gc[3];
         T gv[3] = {0, 0, 0};
+        Shade<DEG, T> S;
         {
             float sh[3 * B];
             ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, sh);
-            T Y[B];
-            ss_sh_eval<DEG, T>(vdir, Y);
-            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+            ss_shade_v<DEG, T>(L, lsp, sh, m.light_visibility[row], d, Rq, S);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                albedo[c] = (T)SS_SH_C0 * sh[c * B] + (T)0.5;
-                T base = 0;
-                if (L.ambient_bands == 0) {
-#pragma unroll
-                    for (int k = 0; k < B; ++k) base += sh[c * B + k] * Y[k];
-                    base += (T)0.5;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < B; ++k)
-                        if (k < BL) base += (k == 0 ? sh[c * B] + (T)(0.5 / SS_SH_C0) : (T)sh[c * B + k]) *
-                                            (T)L.ambient[c * L.ambient_bands + k];
-#pragma unroll
-                    for (int k = 1; k < B; ++k) base += sh[c * B + k] * Y[k];
-                }
-                const T pre = base + albedo[c] * (T)L.intensity[c] * (cosv * vis);
-                gc[c] = (pre > (T)0 && pre < (T)1) ? g[c] : (T)0;  // clamp mask (optim.py:176-177)
-            }
+            for (int c = 0; c < 3; ++c)
+                gc[c] = (S.pre[c] > (T)0 && S.pre[c] < (T)1) ? g[c] : (T)0;  // clamp mask (optim.py:176-177)
             if constexpr (DEG > 0) {
                 T coef[B];
 #pragma unroll
@@ -751,6 +739,8 @@ __global__ void __launch_bounds__(128) k_chain(ss_model m, ss_camera cam, ss_lig
                 ss_sh_grad_dot<DEG, T>(vdir, coef, gv);
             }
         }
+        const T* albedo = S.albedo;
+        const T cosv = S.cosv, vis = S.vis, sgn_s = S.s;
         // SH coefficient gradients: written by k_sh_grad from this compact record
         shrec[row * 2] = make_float4((float)gc[0], (float)gc[1], (float)gc[2], (float)(cosv * vis));
         shrec[row * 2 + 1] = make_float4((float)vdir[0], (float)vdir[1], (float)vdir[2], 1.0f);
@@ -996,7 +986,7 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         k_init_minmax<<<1, 1, 0, s>>>(kminmax);
         SS_CHECK_LAUNCH(ctx);
 #define SS_PRE(DEG)                                                                                      \
-    k_preprocess<DEG><<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
+    k_preprocess<DEG, R><<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
                                                          b.dvals, b.perg, dbg ? *dbg : none, kminmax)
         switch (m->sh_degree) {
             case 0: SS_PRE(0); break;
