@@ -31,19 +31,14 @@ constexpr double T_CUTOFF = 1e-4;
 constexpr double ALPHA_CAP = 0.999;
 
 template <typename R>
-struct SplatRec {
+struct __align__(16) SplatRec {
+    int win[4];     // x0, x1, y0, y1 (first: 16-byte aligned for vector loads)
     R a, b, c;      // inverse 2D covariance [[a, b], [b, c]]
     R o;            // opacity
     R col[3];       // clamped colour
-    int win[4];     // x0, x1, y0, y1
 };
 
-struct PerG {      // per-Gaussian preprocess output (index j = position in the input rows)
-    double mu[2];
-    double a, b, c, o;
-    double col[3];
-    int win[4];
-};
+
 
 struct Bins {
     int64_t n_in;            // rows considered (subset or all)
@@ -53,14 +48,14 @@ struct Bins {
     uint64_t* dkey64;        // [n_in] exact depth key (fp64 bits, ~0 = culled), by input index j
     uint32_t* dkeys;         // [n_in] 32-bit depth keys, sorted (0xffffffff = culled)
     uint32_t* dvals;         // [n_in] input index j, sorted by depth
-    PerG* perg;              // [n_in]
-    double2* rmu;            // [n_in] rank-ordered mu2d
+    double2* mu;             // [n_in] fp64 centre, by input index j
     uint64_t* roff;          // [n_in] rank -> first pair (pre-sort position)
     uint32_t* rcnt;          // [n_in] tiles touched
     uint32_t* rinv;          // [n_in] input index j -> depth rank (~0 if culled)
-    void* rrec;              // [n_in] rank-ordered SplatRec<R>
+    void* rec;               // [n_in] SplatRec<R>, by input index j
+    uint64_t* roffj;         // [n_in] first pair of input j (= roff[rank(j)])
     uint32_t* pkeys;         // [pairs] tile id (sorted)
-    uint32_t* pvals;         // [pairs] rank (sorted)
+    uint32_t* pvals;         // [pairs] input index j of the splat (sorted by (tile, depth rank))
     uint2* ranges;           // [n_tiles]
 };
 
@@ -82,7 +77,8 @@ __global__ void k_visible_flags(ss_model m, ss_camera cam, const int64_t* subset
 template <int DEG, typename R>
 __global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
                              int cutoff, uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
-                             PerG* __restrict__ perg, DebugOut dbg, unsigned long long* __restrict__ kminmax) {
+                             SplatRec<R>* __restrict__ rec, double2* __restrict__ mu, DebugOut dbg,
+                             unsigned long long* __restrict__ kminmax) {
     unsigned long long kmin = ~0ull, kmax = 0;
     constexpr int B = ss_sh_bases(DEG);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
@@ -110,17 +106,16 @@ __global__ void __launch_bounds__(128) k_preprocess(ss_model m, ss_camera cam, s
                 for (int k = 0; k < 3; ++k) RqR[i][k] = (R)P.Rq[i][k];
             ss_shade_v<DEG, R>(L, m.log_scales + row * 3, shv, m.light_visibility[row], dR, RqR, S);
         }
-        PerG g;
-        g.mu[0] = P.mu[0];
-        g.mu[1] = P.mu[1];
-        g.a = P.s11 / P.det;
-        g.b = -P.s01 / P.det;
-        g.c = P.s00 / P.det;
-        g.o = sizeof(R) == 4 ? (double)(1.0f / (1.0f + expf(-m.logit_opacities[row])))
-                             : 1.0 / (1.0 + exp(-(double)m.logit_opacities[row]));
-        for (int c = 0; c < 3; ++c) g.col[c] = fmin(fmax((double)S.pre[c], 0.0), 1.0);
+        SplatRec<R> g;
+        g.a = (R)(P.s11 / P.det);
+        g.b = (R)(-P.s01 / P.det);
+        g.c = (R)(P.s00 / P.det);
+        g.o = sizeof(R) == 4 ? (R)(1.0f / (1.0f + expf(-m.logit_opacities[row])))
+                             : (R)(1.0 / (1.0 + exp(-(double)m.logit_opacities[row])));
+        for (int c = 0; c < 3; ++c) g.col[c] = (R)fmin(fmax((double)S.pre[c], 0.0), 1.0);
         ss_window(P, cam.width, cam.height, g.win);
-        perg[j] = g;
+        rec[j] = g;
+        mu[j] = make_double2(P.mu[0], P.mu[1]);
         if (dbg.vpos) {
             const int64_t v = (int64_t)dbg.vpos[j];
             const ss_prepared& o = dbg.p;
@@ -206,8 +201,8 @@ __device__ __forceinline__ void win_tiles(const int w[4], int& tx0, int& tx1, in
 
 template <typename R>
 __global__ void k_count(const uint64_t* __restrict__ dkey64, const uint32_t* __restrict__ dvals,
-                        const PerG* __restrict__ perg, int64_t n_in, double2* __restrict__ rmu,
-                        SplatRec<R>* __restrict__ rrec, uint32_t* __restrict__ rcnt, uint32_t* __restrict__ rinv) {
+                        const SplatRec<R>* __restrict__ rec, int64_t n_in, uint32_t* __restrict__ rcnt,
+                        uint32_t* __restrict__ rinv) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = dvals[r];
         if (dkey64[j] == ~0ull) {
@@ -216,20 +211,12 @@ __global__ void k_count(const uint64_t* __restrict__ dkey64, const uint32_t* __r
             continue;
         }
         rinv[j] = (uint32_t)r;
-        const PerG g = perg[j];
-        rmu[r] = make_double2(g.mu[0], g.mu[1]);
-        SplatRec<R> s;
-        s.a = (R)g.a;
-        s.b = (R)g.b;
-        s.c = (R)g.c;
-        s.o = (R)g.o;
-        for (int c = 0; c < 3; ++c) s.col[c] = (R)g.col[c];
-        for (int k = 0; k < 4; ++k) s.win[k] = g.win[k];
-        rrec[r] = s;
+        const int4 w = *reinterpret_cast<const int4*>(rec[j].win);
+        const int win[4] = {w.x, w.y, w.z, w.w};
         uint32_t cnt = 0;
-        if (g.win[0] < g.win[1] && g.win[2] < g.win[3]) {
+        if (win[0] < win[1] && win[2] < win[3]) {
             int tx0, tx1, ty0, ty1;
-            win_tiles(g.win, tx0, tx1, ty0, ty1);
+            win_tiles(win, tx0, tx1, ty0, ty1);
             cnt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         }
         rcnt[r] = cnt;
@@ -237,18 +224,20 @@ __global__ void k_count(const uint64_t* __restrict__ dkey64, const uint32_t* __r
 }
 
 template <typename R>
-__global__ void k_emit(const SplatRec<R>* __restrict__ rrec, const uint32_t* __restrict__ rcnt,
-                       const uint64_t* __restrict__ roff, int64_t n_in, int tiles_x, uint32_t* __restrict__ pkeys,
-                       uint32_t* __restrict__ pvals) {
+__global__ void k_emit(const SplatRec<R>* __restrict__ rec, const uint32_t* __restrict__ dvals,
+                       const uint32_t* __restrict__ rcnt, const uint64_t* __restrict__ roff, int64_t n_in, int tiles_x,
+                       uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals, uint64_t* __restrict__ roffj) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
         if (!rcnt[r]) continue;
+        const uint32_t j = dvals[r];
         int tx0, tx1, ty0, ty1;
-        win_tiles(rrec[r].win, tx0, tx1, ty0, ty1);
+        win_tiles(rec[j].win, tx0, tx1, ty0, ty1);
         uint64_t p = roff[r];
+        roffj[j] = p;
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx, ++p) {
                 pkeys[p] = (uint32_t)(ty * tiles_x + tx);
-                pvals[p] = (uint32_t)r;
+                pvals[p] = j;
             }
     }
 }
@@ -383,8 +372,8 @@ struct PixelGeom {
 template <typename R>
 __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict__ ranges,
                                                         const uint32_t* __restrict__ pvals,
-                                                        const double2* __restrict__ rmu,
-                                                        const SplatRec<R>* __restrict__ rrec, int W, int H,
+                                                        const double2* __restrict__ mu,
+                                                        const SplatRec<R>* __restrict__ rec, int W, int H,
                                                         int tiles_x, int n_tiles, double bg0, double bg1, double bg2,
                                                         R* __restrict__ img, R* __restrict__ Tout,
                                                         uint32_t* __restrict__ tile_stop,
@@ -410,8 +399,8 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
         if (!__any_sync(0xffffffffu, alive)) break;
         const uint32_t i = b0 + lane;
         if (i < rg.y) {
-            const uint32_t r = pvals[i];
-            stage(my[lane], rmu[r], rrec[r], X0, Y0);
+            const uint32_t j = pvals[i];
+            stage(my[lane], mu[j], rec[j], X0, Y0);
         }
         __syncwarp();
         const int nb = (int)min(32u, rg.y - b0);
@@ -508,9 +497,9 @@ __device__ __forceinline__ uint32_t pair_index(const uint64_t* roff, const int w
 template <typename R>
 __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict__ ranges,
                                                         const uint32_t* __restrict__ pvals,
-                                                        const double2* __restrict__ rmu,
-                                                        const SplatRec<R>* __restrict__ rrec,
-                                                        const uint64_t* __restrict__ roff,
+                                                        const double2* __restrict__ mu,
+                                                        const SplatRec<R>* __restrict__ rec_,
+                                                        const uint64_t* __restrict__ roffj,
                                                         const uint32_t* __restrict__ tile_stop, int W, int H,
                                                         int tiles_x, int n_tiles, const R* __restrict__ img,
                                                         const float* __restrict__ gt, double npx3,
@@ -559,10 +548,10 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict_
     for (uint32_t b0 = rg.x; b0 < stop; b0 += 32) {
         const uint32_t i = b0 + lane;
         if (i < stop) {
-            const uint32_t r = pvals[i];
-            const SplatRec<R> rec = rrec[r];
-            stage(my[lane], rmu[r], rec, X0, Y0);
-            my[lane].p = (int)pair_index(roff, rec.win, r, tx, ty);
+            const uint32_t j = pvals[i];
+            const SplatRec<R> rec = rec_[j];
+            stage(my[lane], mu[j], rec, X0, Y0);
+            my[lane].p = (int)pair_index(roffj, rec.win, j, tx, ty);
         }
         __syncwarp();
         const int nb = (int)min(32u, stop - b0);
@@ -626,8 +615,8 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict_
     }
     // pairs after every pixel of the tile saturated contribute nothing
     for (uint32_t i = stop + lane; i < rg.y; i += 32) {
-        const uint32_t r = pvals[i];
-        const uint32_t p = pair_index(roff, rrec[r].win, r, tx, ty);
+        const uint32_t j = pvals[i];
+        const uint32_t p = pair_index(roffj, rec_[j].win, j, tx, ty);
 #pragma unroll
         for (int q = 0; q < 9; ++q) partials[(uint64_t)p * 9 + q] = 0;
     }
@@ -967,15 +956,15 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     b.dvals = SS_SCRATCH(ctx, uint32_t, na);
     uint32_t* kalt = SS_SCRATCH(ctx, uint32_t, na);
     uint32_t* valt = SS_SCRATCH(ctx, uint32_t, na);
-    b.perg = SS_SCRATCH(ctx, PerG, na);
-    b.rmu = SS_SCRATCH(ctx, double2, na);
+    b.mu = SS_SCRATCH(ctx, double2, na);
+    b.roffj = SS_SCRATCH(ctx, uint64_t, na);
     b.roff = SS_SCRATCH(ctx, uint64_t, na);
     b.rcnt = SS_SCRATCH(ctx, uint32_t, na);
     b.rinv = SS_SCRATCH(ctx, uint32_t, na);
-    b.rrec = ss_scratch(ctx, sizeof(SplatRec<R>) * na);
+    b.rec = ss_scratch(ctx, sizeof(SplatRec<R>) * na);
     b.ranges = SS_SCRATCH(ctx, uint2, b.n_tiles);
     uint64_t* total = SS_SCRATCH(ctx, uint64_t, 1);
-    if (!b.dkey64 || !kminmax || !b.dkeys || !b.dvals || !kalt || !valt || !b.perg || !b.rmu || !b.roff || !b.rcnt || !b.rinv || !b.rrec || !b.ranges ||
+    if (!b.dkey64 || !kminmax || !b.dkeys || !b.dvals || !kalt || !valt || !b.mu || !b.roffj || !b.roff || !b.rcnt || !b.rinv || !b.rec || !b.ranges ||
         !total)
         return SS_ERR_CUDA;
     SS_CUDA(ctx, cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.n_tiles, s));
@@ -987,7 +976,8 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         SS_CHECK_LAUNCH(ctx);
 #define SS_PRE(DEG)                                                                                      \
     k_preprocess<DEG, R><<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
-                                                         b.dvals, b.perg, dbg ? *dbg : none, kminmax)
+                                                         b.dvals, (SplatRec<R>*)b.rec, b.mu, dbg ? *dbg : none,  \
+                                                         kminmax)
         switch (m->sh_degree) {
             case 0: SS_PRE(0); break;
             case 1: SS_PRE(1); break;
@@ -1005,8 +995,7 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_DEPTH_SORT);
         ss_tic(ctx, KC_BIN);
-        k_count<R><<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, b.dvals, b.perg, n, b.rmu, (SplatRec<R>*)b.rrec, b.rcnt,
-                                                 b.rinv);
+        k_count<R><<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, b.dvals, (const SplatRec<R>*)b.rec, n, b.rcnt, b.rinv);
         SS_CHECK_LAUNCH(ctx);
     } else {
         ss_tic(ctx, KC_BIN);
@@ -1025,8 +1014,8 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (!b.pkeys || !b.pvals || !pk2 || !pv2) return SS_ERR_CUDA;
     if (P > 0) {
         ss_tic(ctx, KC_BIN);
-        k_emit<R><<<gridn(ctx, n), 256, 0, s>>>((const SplatRec<R>*)b.rrec, b.rcnt, b.roff, n, b.tiles_x, b.pkeys,
-                                                b.pvals);
+        k_emit<R><<<gridn(ctx, n), 256, 0, s>>>((const SplatRec<R>*)b.rec, b.dvals, b.rcnt, b.roff, n, b.tiles_x,
+                                                b.pkeys, b.pvals, b.roffj);
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_BIN);
         ss_tic(ctx, KC_TILE_SORT);
@@ -1045,7 +1034,7 @@ int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bi
             uint32_t* tile_stop) {
     ss_tic(ctx, KC_FORWARD);
     k_blend_fwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
-        b.ranges, b.pvals, b.rmu, (const SplatRec<R>*)b.rrec, cam->width, cam->height, b.tiles_x, b.n_tiles,
+        b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
         o->background[0],
         o->background[1], o->background[2], img, T, tile_stop, ss_timing_on(ctx) ? ctx->dev_counters : nullptr);
     SS_CHECK_LAUNCH(ctx);
@@ -1083,7 +1072,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     const double inv_npx = 1.0 / (double)(3 * npx);
     ss_tic(ctx, KC_BACKWARD);
     k_blend_bwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, s>>>(
-        b.ranges, b.pvals, b.rmu, (const SplatRec<R>*)b.rrec, b.roff, stop, cam->width, cam->height, b.tiles_x,
+        b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
         b.n_tiles, img, gt, (double)(3 * npx), partials, tloss);
     SS_CHECK_LAUNCH(ctx);
     k_loss_reduce<<<1, 256, 0, s>>>(tloss, b.n_tiles, inv_npx, loss);
@@ -1137,7 +1126,7 @@ __global__ void k_debug_bins(const Bins b, int64_t* order_rows, const int64_t* s
             ranges_out[2 * t + 1] = b.ranges[t].y;
         }
     for (int64_t p = tid; p < b.pairs; p += nt)
-        if (pair_rank) pair_rank[p] = b.pvals[p];
+        if (pair_rank) pair_rank[p] = b.rinv[b.pvals[p]];
 }
 
 }  // namespace
