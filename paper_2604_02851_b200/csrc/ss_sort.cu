@@ -1,14 +1,18 @@
-// Stable LSD radix sort of (key, uint32 value) pairs, 8-bit digits.
+// Stable LSD radix sort of (key, uint32 value) pairs, 8-bit digits, one
+// kernel per digit pass ("onesweep": Adinets & Merrill, 2022).
 //
-// Per pass: (1) upsweep -- per-block digit histogram (digit-major so one scan
-// yields every block's global offset per digit); (2) exclusive scan of the
-// histogram; (3) downsweep -- stable in-block ranking with warp
-// __match_any_sync, local scatter into shared memory in digit order, then a
-// coalesced write of each digit run to its global offset.
+//   k_hist_all   one read of the keys -> global digit histograms of every pass
+//   k_base_scan  exclusive scan of each pass's 256 counts -> digit base offsets
+//   k_onesweep   per pass: a block takes the next 2048-key tile (atomic tile
+//                counter, so every earlier tile is already running), ranks its
+//                keys stably with warp __match_any_sync, publishes its
+//                per-digit counts, looks back over earlier tiles' published
+//                counts/prefixes (decoupled look-back) to get its global digit
+//                offsets, then writes each digit run coalesced from shared memory
 //
-// Used twice per view: the depth sort of Gaussians (64-bit fp64-depth keys,
-// exact reference order) and the tile sort of (tile, splat) pairs (only
-// ceil(log2 tiles) key bits).
+// Per pass the keys and values are read once and written once.  Used for the
+// depth sort of Gaussians (32-bit range-shifted keys, 4 passes) and the tile
+// sort of (tile, splat) pairs (ceil(log2 tiles) bits, 2 passes at 1080p).
 #include "ss_internal.cuh"
 
 namespace {
@@ -17,6 +21,8 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_ITEMS = 8;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_MAX_PASSES = 8;
+constexpr uint32_t FLAG_AGG = 1u << 30, FLAG_INC = 2u << 30, CNT_MASK = (1u << 30) - 1;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -25,26 +31,48 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 template <typename K>
-__global__ void __launch_bounds__(RS_THREADS) k_upsweep(const K* __restrict__ keys, int64_t n, int shift,
-                                                        unsigned mask, int nb, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t cnt[256];
-    cnt[threadIdx.x] = 0;
+__global__ void __launch_bounds__(RS_THREADS) k_hist_all(const K* __restrict__ keys, int64_t n, int key_bits,
+                                                         uint32_t* __restrict__ hist) {
+    __shared__ uint32_t cnt[RS_MAX_PASSES][256];
+    const int passes = (key_bits + 7) / 8;
+    for (int p = 0; p < passes; ++p) cnt[p][threadIdx.x] = 0;
     __syncthreads();
-    int64_t base = (int64_t)blockIdx.x * RS_TILE;
-#pragma unroll
-    for (int r = 0; r < RS_ITEMS; ++r) {
-        int64_t i = base + r * RS_THREADS + threadIdx.x;
-        if (i < n) atomicAdd(&cnt[(unsigned)(keys[i] >> shift) & mask], 1u);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const K k = keys[i];
+        for (int p = 0; p < passes; ++p) {
+            const int bits = key_bits - 8 * p < 8 ? key_bits - 8 * p : 8;
+            atomicAdd(&cnt[p][(unsigned)(k >> (8 * p)) & ((1u << bits) - 1u)], 1u);
+        }
     }
     __syncthreads();
-    hist[(int64_t)threadIdx.x * nb + blockIdx.x] = cnt[threadIdx.x];
+    for (int p = 0; p < passes; ++p)
+        if (cnt[p][threadIdx.x]) atomicAdd(&hist[p * 256 + threadIdx.x], cnt[p][threadIdx.x]);
+}
+
+__global__ void k_base_scan(const uint32_t* __restrict__ hist, int passes, uint64_t* __restrict__ base) {
+    // one warp per pass
+    const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (p >= passes) return;
+    uint64_t run = 0;
+    for (int c = 0; c < 256; c += 32) {
+        const uint64_t v = hist[p * 256 + c + lane];
+        uint64_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        base[p * 256 + c + lane] = run + incl - v;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
 }
 
 template <typename K>
-__global__ void __launch_bounds__(RS_THREADS) k_downsweep(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
-                                                          int64_t n, int shift, unsigned mask, int nb,
-                                                          const uint64_t* __restrict__ offsets,
-                                                          K* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+__global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                         int64_t n, int shift, unsigned mask,
+                                                         const uint64_t* __restrict__ digit_base,
+                                                         uint32_t* __restrict__ part, unsigned* __restrict__ tile_ctr,
+                                                         K* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
     __shared__ K s_keys[RS_TILE];
     __shared__ uint32_t s_vals[RS_TILE];
     __shared__ uint32_t s_wcnt[RS_WARPS][256];
@@ -52,53 +80,96 @@ __global__ void __launch_bounds__(RS_THREADS) k_downsweep(const K* __restrict__ 
     __shared__ uint32_t s_start[256];
     __shared__ uint64_t s_goff[256];
     __shared__ uint32_t s_wsum[RS_WARPS];
+    __shared__ unsigned s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
     s_run[tid] = 0;
 #pragma unroll
     for (int w = 0; w < RS_WARPS; ++w) s_wcnt[w][tid] = 0;
-    s_goff[tid] = offsets[(int64_t)tid * nb + blockIdx.x];
     __syncthreads();
+    const unsigned tile = s_tile;
+    const int64_t base = (int64_t)tile * RS_TILE;
 
+    // ---- warp w owns keys [w*256, (w+1)*256) of the tile (item r at r*32 + lane):
+    // load them all first, then rank within the warp without block barriers
     K k[RS_ITEMS];
     uint32_t v[RS_ITEMS];
+    const int64_t wbase = base + (int64_t)warp * (RS_ITEMS * 32);
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        const bool ok = i < n;
+        k[r] = ok ? keys[i] : K(0);
+        v[r] = ok ? vals[i] : 0u;
+    }
     uint32_t rank[RS_ITEMS];
     unsigned dig[RS_ITEMS];
 #pragma unroll
     for (int r = 0; r < RS_ITEMS; ++r) {
-        int64_t i = base + r * RS_THREADS + tid;
-        bool ok = i < n;
-        k[r] = ok ? keys[i] : K(0);
-        v[r] = ok ? vals[i] : 0u;
-        unsigned d = ok ? ((unsigned)(k[r] >> shift) & mask) : 256u + lane;  // invalid lanes match only themselves
+        const int64_t i = wbase + r * 32 + lane;
+        const bool ok = i < n;
+        const unsigned d = ok ? ((unsigned)(k[r] >> shift) & mask) : 256u + lane;  // invalid lanes match only themselves
         dig[r] = d;
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        unsigned below = __popc(peers & lanemask_lt());
-        if (ok && below == 0) s_wcnt[warp][d] = __popc(peers);
-        __syncthreads();
-        if (ok) {
-            uint32_t pre = s_run[d];
-            for (int w = 0; w < warp; ++w) pre += s_wcnt[w][d];
-            rank[r] = pre + below;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned below = __popc(peers & lanemask_lt());
+        const int leader = __ffs(peers) - 1;
+        uint32_t prior = 0;
+        if (ok && lane == leader) {
+            prior = s_wcnt[warp][d];
+            s_wcnt[warp][d] = prior + __popc(peers);
         }
-        __syncthreads();
-        uint32_t add = 0;
+        prior = __shfl_sync(0xffffffffu, prior, leader);
+        rank[r] = prior + below;  // rank among the warp's keys of digit d
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: offsets of each warp's run inside the tile's digit run, and the tile total
+    {
+        uint32_t acc = 0;
 #pragma unroll
         for (int w = 0; w < RS_WARPS; ++w) {
-            add += s_wcnt[w][tid];
-            s_wcnt[w][tid] = 0;
+            const uint32_t c = s_wcnt[w][tid];
+            s_wcnt[w][tid] = acc;
+            acc += c;
         }
-        s_run[tid] += add;
-        __syncthreads();
+        s_run[tid] = acc;
     }
-    // exclusive scan of the block's per-digit totals -> local run starts
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r)
+        if (dig[r] < 256u) rank[r] += s_wcnt[warp][dig[r]];
+
+    // ---- decoupled look-back: this tile's global offset for digit `tid`
     {
-        uint32_t c = s_run[tid];
+        const uint32_t mine = s_run[tid];
+        volatile uint32_t* slot = part + (int64_t)tile * 256 + tid;
+        if (tile == 0) {
+            *slot = FLAG_INC | mine;
+            s_goff[tid] = digit_base[tid];
+        } else {
+            *slot = FLAG_AGG | mine;
+            uint64_t excl = 0;
+            for (int64_t t = (int64_t)tile - 1; t >= 0; --t) {
+                const volatile uint32_t* prev = part + t * 256 + tid;
+                uint32_t w;
+                do {
+                    w = *prev;
+                } while ((w & ~CNT_MASK) == 0);
+                excl += w & CNT_MASK;
+                if (w & FLAG_INC) break;
+            }
+            *slot = FLAG_INC | (uint32_t)(excl + mine);
+            s_goff[tid] = digit_base[tid] + excl;
+        }
+    }
+    // exclusive scan of the tile's per-digit counts -> local run starts
+    {
+        const uint32_t c = s_run[tid];
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
         if (lane == 31) s_wsum[warp] = incl;
@@ -111,7 +182,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_downsweep(const K* __restrict__ 
 #pragma unroll
     for (int r = 0; r < RS_ITEMS; ++r) {
         if (dig[r] < 256u) {
-            uint32_t p = s_start[dig[r]] + rank[r];
+            const uint32_t p = s_start[dig[r]] + rank[r];
             s_keys[p] = k[r];
             s_vals[p] = v[r];
         }
@@ -119,9 +190,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_downsweep(const K* __restrict__ 
     __syncthreads();
     const int64_t cnt = (n - base) < RS_TILE ? (n - base) : RS_TILE;
     for (int i = tid; i < cnt; i += RS_THREADS) {
-        K key = s_keys[i];
-        unsigned d = (unsigned)(key >> shift) & mask;
-        uint64_t o = s_goff[d] + (uint64_t)(i - s_start[d]);
+        const K key = s_keys[i];
+        const unsigned d = (unsigned)(key >> shift) & mask;
+        const uint64_t o = s_goff[d] + (uint64_t)(i - s_start[d]);
         keys_out[o] = key;
         vals_out[o] = s_vals[i];
     }
@@ -130,28 +201,41 @@ __global__ void __launch_bounds__(RS_THREADS) k_downsweep(const K* __restrict__ 
 template <typename K>
 int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, int key_bits) {
     if (n <= 1 || key_bits <= 0) return SS_OK;
-    const int nb = (int)((n + RS_TILE - 1) / RS_TILE);
-    uint32_t* hist = SS_SCRATCH(ctx, uint32_t, (int64_t)256 * nb);
-    uint64_t* offs = SS_SCRATCH(ctx, uint64_t, (int64_t)256 * nb);
-    if (!hist || !offs) return SS_ERR_CUDA;
+    if (n > (int64_t)CNT_MASK) return ss_fail(ctx, SS_ERR_CAPACITY, "radix sort limited to 2^30 keys");
+    const int passes = (key_bits + 7) / 8;
+    const int64_t tiles = (n + RS_TILE - 1) / RS_TILE;
+    uint32_t* hist = SS_SCRATCH(ctx, uint32_t, RS_MAX_PASSES * 256);
+    uint64_t* base = SS_SCRATCH(ctx, uint64_t, RS_MAX_PASSES * 256);
+    uint32_t* part = SS_SCRATCH(ctx, uint32_t, tiles * 256 * passes);
+    unsigned* ctr = SS_SCRATCH(ctx, unsigned, RS_MAX_PASSES);
+    if (!hist || !base || !part || !ctr) return SS_ERR_CUDA;
+    cudaStream_t s = ctx->stream;
+    SS_CUDA(ctx, cudaMemsetAsync(hist, 0, sizeof(uint32_t) * RS_MAX_PASSES * 256, s));
+    SS_CUDA(ctx, cudaMemsetAsync(part, 0, sizeof(uint32_t) * tiles * 256 * passes, s));
+    SS_CUDA(ctx, cudaMemsetAsync(ctr, 0, sizeof(unsigned) * RS_MAX_PASSES, s));
+    int hb = (int)((n + RS_THREADS * 16 - 1) / (RS_THREADS * 16));
+    if (hb > ctx->num_sms * 8) hb = ctx->num_sms * 8;
+    k_hist_all<K><<<hb, RS_THREADS, 0, s>>>(keys, n, key_bits, hist);
+    SS_CHECK_LAUNCH(ctx);
+    k_base_scan<<<1, 32 * RS_MAX_PASSES, 0, s>>>(hist, passes, base);
+    SS_CHECK_LAUNCH(ctx);
     K* src_k = keys;
     uint32_t* src_v = vals;
     K* dst_k = keys_alt;
     uint32_t* dst_v = vals_alt;
-    for (int shift = 0; shift < key_bits; shift += 8) {
-        int bits = key_bits - shift < 8 ? key_bits - shift : 8;
-        unsigned mask = (1u << bits) - 1u;
-        k_upsweep<K><<<nb, RS_THREADS, 0, ctx->stream>>>(src_k, n, shift, mask, nb, hist);
-        SS_CHECK_LAUNCH(ctx);
-        SS_TRY(ss_scan_u32_to_u64(ctx, hist, offs, (int64_t)256 * nb, nullptr));
-        k_downsweep<K><<<nb, RS_THREADS, 0, ctx->stream>>>(src_k, src_v, n, shift, mask, nb, offs, dst_k, dst_v);
+    for (int p = 0; p < passes; ++p) {
+        const int shift = 8 * p;
+        const int bits = key_bits - shift < 8 ? key_bits - shift : 8;
+        const unsigned mask = (1u << bits) - 1u;
+        k_onesweep<K><<<(unsigned)tiles, RS_THREADS, 0, s>>>(src_k, src_v, n, shift, mask, base + p * 256,
+                                                             part + (int64_t)p * tiles * 256, ctr + p, dst_k, dst_v);
         SS_CHECK_LAUNCH(ctx);
         K* tk = src_k; src_k = dst_k; dst_k = tk;
         uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
     }
     if (src_k != keys) {
-        SS_CUDA(ctx, cudaMemcpyAsync(keys, src_k, sizeof(K) * n, cudaMemcpyDeviceToDevice, ctx->stream));
-        SS_CUDA(ctx, cudaMemcpyAsync(vals, src_v, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        SS_CUDA(ctx, cudaMemcpyAsync(keys, src_k, sizeof(K) * n, cudaMemcpyDeviceToDevice, s));
+        SS_CUDA(ctx, cudaMemcpyAsync(vals, src_v, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
     }
     return SS_OK;
 }
