@@ -281,26 +281,22 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
     }
     __syncthreads();
     // varint bytes of the gaps inside the chunk (first survivor excluded):
-    // thread w < 64 owns bitmap word w; the previous survivor comes from the
-    // nearest non-empty earlier word
+    // gaps inside a 32-row word are < 32 (one byte each), so a word costs
+    // popc(bits) bytes plus the extra bytes of its first survivor's gap to
+    // the nearest survivor in an earlier word
     uint32_t var = 0;
     if (threadIdx.x < TK_CHUNK / 32) {
         const int w = threadIdx.x;
-        uint32_t bits = s_keep[w];
+        const uint32_t bits = s_keep[w];
         if (bits) {
             int64_t prev = -1;
-            for (int k = w - 1; k >= 0; --k)
-                if (s_keep[k]) {
-                    prev = r0 + 32 * k + (31 - __clz(s_keep[k]));
+            for (int k2 = w - 1; k2 >= 0; --k2)
+                if (s_keep[k2]) {
+                    prev = r0 + 32 * k2 + (31 - __clz(s_keep[k2]));
                     break;
                 }
-            while (bits) {
-                const int b = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int64_t row = r0 + 32 * w + b;
-                if (prev >= 0) var += vlen((uint64_t)(row - prev - 1));
-                prev = row;
-            }
+            const int64_t first = r0 + 32 * w + (__ffs(bits) - 1);
+            var = __popc(bits) - 1 + (prev >= 0 ? vlen((uint64_t)(first - prev - 1)) : 0);
         }
     }
 #pragma unroll
@@ -334,8 +330,8 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
     }
 }
 
-__global__ void __launch_bounds__(TK_THREADS) k_tick_scan(Batch B) {
-    const int64_t chunk = blockIdx.x;
+__global__ void __launch_bounds__(TK_THREADS) k_tick_scan(Batch B, int64_t chunk_begin) {
+    const int64_t chunk = chunk_begin + blockIdx.x;
     const Job& J = B.j[find_job(B, chunk)];
     const int64_t c = chunk - J.chunk0;
     const int64_t r0 = c * TK_CHUNK;
@@ -363,19 +359,73 @@ __global__ void __launch_bounds__(TK_THREADS) k_tick_scan(Batch B) {
 }
 
 // ---------------------------------------------------------------- plan
-__global__ void __launch_bounds__(TK_THREADS) k_tick_plan(Batch B) {
+constexpr int PLAN_THREADS = 1024;
+
+// inclusive block scan (sum) over PLAN_THREADS threads; returns the block total in *tot
+__device__ __forceinline__ uint64_t plan_scan_sum(uint64_t v, uint64_t* tot) {
+    __shared__ uint64_t ws[PLAN_THREADS / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) ws[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        uint64_t x = ws[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        ws[lane] = x;
+    }
+    __syncthreads();
+    const uint64_t out = v + (w ? ws[w - 1] : 0);
+    *tot = ws[PLAN_THREADS / 32 - 1];
+    __syncthreads();
+    return out;
+}
+
+// inclusive block scan (max) of signed values
+__device__ __forceinline__ long long plan_scan_max(long long v, long long* tot) {
+    __shared__ long long ws[PLAN_THREADS / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o && t > v) v = t;
+    }
+    if (lane == 31) ws[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        long long x = ws[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o && t > x) x = t;
+        }
+        ws[lane] = x;
+    }
+    __syncthreads();
+    const long long pw = w ? ws[w - 1] : -1;
+    const long long out = pw > v ? pw : v;
+    *tot = ws[PLAN_THREADS / 32 - 1];
+    __syncthreads();
+    return out;
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS) k_tick_plan(Batch B, int only) {
+    if (only >= 0 && (int)blockIdx.x != only) return;
     const Job& J = B.j[blockIdx.x];
     if (!J.residual) return;
-    __shared__ int s_mode;
-    __shared__ double s_m;
+    const unsigned long long k = J.g[0];
+    const int sparse = 2 * (int64_t)k < J.rows;  // k < rows * 0.5 (delta.py:101)
+    double m;
+    if (sparse) m = k ? (double)__double2float_rn(__longlong_as_double((long long)J.g[2])) : 0.0;
+    else m = J.rows ? (double)__double2float_rn(__longlong_as_double((long long)J.g[1])) : 0.0;
     if (threadIdx.x == 0) {
-        const unsigned long long k = J.g[0];
-        const int sparse = 2 * (int64_t)k < J.rows;  // k < rows * 0.5 (delta.py:101)
-        double m;
-        if (sparse) m = k ? (double)__double2float_rn(__longlong_as_double((long long)J.g[2])) : 0.0;
-        else m = J.rows ? (double)__double2float_rn(__longlong_as_double((long long)J.g[1])) : 0.0;
-        s_mode = sparse;
-        s_m = m;
         *J.mode = sparse;
         *J.m = m;
         QParams rq;
@@ -389,85 +439,56 @@ __global__ void __launch_bounds__(TK_THREADS) k_tick_plan(Batch B) {
         rq.dspan = q_ds(m, -m);
         *J.rq = rq;
     }
-    __syncthreads();
-    const int sparse = s_mode;
-    // per-chunk prefixes: survivors, varint bytes, last kept row before each
-    // chunk.  Thread t owns a contiguous run of chunks; block scans combine
-    // the runs (sum for counts/bytes, max for the last kept row).
-    __shared__ uint64_t s_V;
-    __shared__ uint64_t s_k[TK_THREADS], s_v[TK_THREADS];
-    __shared__ long long s_l[TK_THREADS];
-    const int64_t nc = J.nchunks;
-    const int64_t per = (nc + TK_THREADS - 1) / TK_THREADS;
-    const int64_t c0 = threadIdx.x * per, c1 = min(c0 + per, nc);
-    // pass 1: run totals (the varint of a run's first gap depends on the last
-    // kept row before the run, so bytes are first counted without it)
-    uint64_t K = 0, Vin = 0;
-    long long last = -1, first = -1;
-    for (int64_t c = c0; c < c1; ++c) {
-        if (!J.ck[c]) continue;
-        if (first < 0) first = J.cfirst[c];
-        else Vin += (uint64_t)vlen((uint64_t)(J.cfirst[c] - last - 1));
-        Vin += J.cvar[c];
-        K += J.ck[c];
-        last = J.clast[c];
-    }
-    s_k[threadIdx.x] = K;
-    s_l[threadIdx.x] = last;
-    __syncthreads();
-    // exclusive prefix of counts and inclusive running max of last kept rows
-    if (threadIdx.x == 0) {
-        uint64_t acc = 0;
-        long long mx = -1;
-        for (int t = 0; t < TK_THREADS; ++t) {
-            const uint64_t k = s_k[t];
-            const long long l = s_l[t];
-            s_k[t] = acc;
-            s_l[t] = mx;  // last kept row before run t
-            acc += k;
-            if (l > mx) mx = l;
-        }
-    }
-    __syncthreads();
-    const long long prev_run = s_l[threadIdx.x];
-    s_v[threadIdx.x] = first >= 0 ? Vin + (uint64_t)vlen((uint64_t)(first - prev_run - 1)) : 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t acc = 0;
-        for (int t = 0; t < TK_THREADS; ++t) {
-            const uint64_t v = s_v[t];
-            s_v[t] = acc;
-            acc += v;
-        }
-        s_V = acc;
-    }
-    __syncthreads();
-    // pass 2: per-chunk prefixes inside the run
-    {
-        uint64_t k = s_k[threadIdx.x], v = s_v[threadIdx.x];
-        long long l = prev_run;
-        for (int64_t c = c0; c < c1; ++c) {
-            J.cnt_pre[c] = (uint32_t)k;
-            J.var_pre[c] = v;
-            J.prev_last[c] = l;
-            if (J.ck[c]) {
-                v += (uint64_t)vlen((uint64_t)(J.cfirst[c] - l - 1)) + J.cvar[c];
-                k += J.ck[c];
-                l = J.clast[c];
+    uint64_t V = 0;
+    if (sparse) {
+        // per-chunk prefixes for the sparse writer: survivors, varint bytes
+        // and the last kept row before each chunk (block scans, carried over
+        // rounds of PLAN_THREADS chunks)
+        uint64_t kc = 0, vc = 0;
+        long long lc = -1;
+        for (int64_t c0 = 0; c0 < J.nchunks; c0 += PLAN_THREADS) {
+            const int64_t c = c0 + threadIdx.x;
+            const bool in = c < J.nchunks;
+            const uint32_t ck = in ? J.ck[c] : 0;
+            const long long cl = in && ck ? (long long)J.clast[c] : -1;
+            uint64_t ktot;
+            const uint64_t kin = plan_scan_sum(ck, &ktot);
+            long long ltot;
+            const long long lin = plan_scan_max(cl, &ltot);
+            // last kept row before chunk c: inclusive max of earlier chunks
+            long long prev = __shfl_up_sync(0xffffffffu, lin, 1);
+            {
+                __shared__ long long wl[PLAN_THREADS / 32];
+                if ((threadIdx.x & 31) == 31) wl[threadIdx.x >> 5] = lin;
+                __syncthreads();
+                if ((threadIdx.x & 31) == 0) prev = threadIdx.x ? wl[(threadIdx.x >> 5) - 1] : -1;
+                __syncthreads();
             }
+            if (prev < lc) prev = lc;
+            const uint64_t vbytes = in && ck ? (uint64_t)vlen((uint64_t)(J.cfirst[c] - prev - 1)) + J.cvar[c] : 0;
+            uint64_t vtot;
+            const uint64_t vin = plan_scan_sum(vbytes, &vtot);
+            if (in) {
+                J.cnt_pre[c] = (uint32_t)(kc + kin - ck);
+                J.var_pre[c] = vc + vin - vbytes;
+                J.prev_last[c] = prev;
+            }
+            kc += ktot;
+            vc += vtot;
+            if (ltot > lc) lc = ltot;
         }
+        V = vc;
     }
     if (threadIdx.x == 0) {
         const int cb = J.bits / 8;
-        const uint64_t k = J.g[0];
-        const uint64_t blen = sparse ? s_V + k * J.dims * cb : (uint64_t)J.rows * J.dims * cb;
+        const uint64_t blen = sparse ? V + k * J.dims * cb : (uint64_t)J.rows * J.dims * cb;
         uint8_t* o = J.out;
         o[0] = (uint8_t)J.attr;
         o[1] = (uint8_t)sparse;
         o[2] = 0;
         o[3] = (uint8_t)J.dims;
         put32(o + 4, (uint32_t)J.rows);
-        const float mf = (float)s_m;
+        const float mf = (float)m;
         put32(o + 8, __float_as_uint(-mf));
         put32(o + 12, __float_as_uint(mf));
         int h = 16;
@@ -477,7 +498,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_tick_plan(Batch B) {
         }
         put32(o + h, (uint32_t)blen);
         *J.out_len = h + 4 + blen;
-        J.var_pre[J.nchunks] = s_V;  // total varint bytes (sparse code offset)
+        J.var_pre[J.nchunks] = V;  // total varint bytes (sparse code offset)
     }
 }
 
@@ -488,6 +509,49 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
     const T* cur = (const T*)J.cur;
     const T* base = (const T*)J.base;
     const int64_t e1 = r1 * J.dims;
+    if (sizeof(T) == 4 && J.bits == 8 && J.new_base &&
+        (((uintptr_t)cur | (uintptr_t)base | (uintptr_t)J.new_base) & 15) == 0 && ((r0 * J.dims) & 3) == 0) {
+        const int64_t v0 = r0 * J.dims / 4, v1 = e1 / 4;
+        const float4* c4 = (const float4*)cur;
+        const float4* b4 = (const float4*)base;
+        float4* n4 = (float4*)J.new_base;
+        uint8_t* blk = J.out + 20;
+        for (int64_t v = v0 + threadIdx.x; v < v1; v += 4 * TK_THREADS) {
+            float4 cc[4], bb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t w = v + u * TK_THREADS;
+                if (w < v1) {
+                    cc[u] = c4[w];
+                    bb[u] = b4[w];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t w = v + u * TK_THREADS;
+                if (w >= v1) continue;
+                const float cs[4] = {cc[u].x, cc[u].y, cc[u].z, cc[u].w};
+                const float bs[4] = {bb[u].x, bb[u].y, bb[u].z, bb[u].w};
+                uint32_t packed = 0;
+                float nb[4];
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t code = quant(q_ds((double)cs[kk], (double)bs[kk]), rq);
+                    packed |= code << (8 * kk);
+                    nb[kk] = __double2float_rn(q_da((double)bs[kk], dequant(code, rq)));
+                }
+                n4[w] = make_float4(nb[0], nb[1], nb[2], nb[3]);
+                *reinterpret_cast<uint32_t*>(blk + 4 * w) = packed;  // 20 + 4w: 4-byte aligned
+            }
+        }
+        for (int64_t e = 4 * v1 + threadIdx.x; e < e1; e += TK_THREADS) {
+            const double b = (double)base[e];
+            const uint32_t code = quant(q_ds((double)cur[e], b), rq);
+            blk[e] = (uint8_t)code;
+            J.new_base[e] = __double2float_rn(q_da(b, dequant(code, rq)));
+        }
+        return;
+    }
     if (sizeof(T) == 4 && J.bits == 16 && J.new_base &&
         (((uintptr_t)cur | (uintptr_t)base | (uintptr_t)J.new_base) & 15) == 0 && ((r0 * J.dims) & 3) == 0) {
         // 4 elements per thread-step: float4 loads/stores, 8-byte code stores; 4 steps in flight
@@ -642,8 +706,8 @@ __device__ __forceinline__ void emit_sparse(const Job& J, const QParams& rq, int
     }
 }
 
-__global__ void __launch_bounds__(TK_THREADS) k_tick_emit(Batch B) {
-    const int64_t chunk = blockIdx.x;
+__global__ void __launch_bounds__(TK_THREADS) k_tick_emit(Batch B, int64_t chunk_begin) {
+    const int64_t chunk = chunk_begin + blockIdx.x;
     const Job& J = B.j[find_job(B, chunk)];
     if (!J.residual) return;
     const int64_t c = chunk - J.chunk0;
@@ -740,17 +804,29 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         scratch += 1;
     }
     ss_tic(ctx, KC_CODEC);
-    if (chunks) {
-        k_tick_scan<<<(unsigned)chunks, TK_THREADS, 0, ctx->stream>>>(B);
-        SS_CHECK_LAUNCH(ctx);
-    }
-    if (any_resid) {
-        k_tick_plan<<<njobs, TK_THREADS, 0, ctx->stream>>>(B);
-        SS_CHECK_LAUNCH(ctx);
-        if (chunks) {
-            k_tick_emit<<<(unsigned)chunks, TK_THREADS, 0, ctx->stream>>>(B);
+    // residual jobs one at a time: stats -> plan -> emit back to back, so the
+    // emit pass re-reads that job's cur/base (24 B/row) from L2
+    for (int i = 0; i < njobs; ++i) {
+        const Job& J = B.j[i];
+        if (!J.residual) continue;
+        if (J.nchunks) {
+            k_tick_scan<<<(unsigned)J.nchunks, TK_THREADS, 0, ctx->stream>>>(B, J.chunk0);
             SS_CHECK_LAUNCH(ctx);
         }
+        k_tick_plan<<<njobs, PLAN_THREADS, 0, ctx->stream>>>(B, i);
+        SS_CHECK_LAUNCH(ctx);
+        if (J.nchunks) {
+            k_tick_emit<<<(unsigned)J.nchunks, TK_THREADS, 0, ctx->stream>>>(B, J.chunk0);
+            SS_CHECK_LAUNCH(ctx);
+        }
+    }
+    // absolute jobs: one streaming launch over their chunks (numbered first)
+    int64_t abs_chunks = 0;
+    for (int i = 0; i < njobs; ++i)
+        if (!B.j[i].residual) abs_chunks += B.j[i].nchunks;
+    if (abs_chunks) {
+        k_tick_scan<<<(unsigned)abs_chunks, TK_THREADS, 0, ctx->stream>>>(B, 0);
+        SS_CHECK_LAUNCH(ctx);
     }
     // jobs with zero rows and no chunk still need their header
     for (int i = 0; i < njobs; ++i) {
