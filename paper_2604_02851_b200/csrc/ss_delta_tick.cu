@@ -91,17 +91,35 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
     return __fma_rn(r, y, q);
 }
 
-// ref quantize.py:8-17, bit-exact
+// numpy's maximum/minimum for non-NaN inputs (a >= b ? a : b), as plain
+// compare + select: fmax/fmin compile to ~6 instructions each for doubles
+__device__ __forceinline__ double np_max(double a, double b) { return a >= b ? a : b; }
+__device__ __forceinline__ double np_min(double a, double b) { return a <= b ? a : b; }
+
+// ref quantize.py:8-17, bit-exact.  For hi >= lo, clip(v) - lo <= RN(hi - lo)
+// by monotone rounding, so t already lies in [0, 1] and its clip is a no-op.
 __device__ __forceinline__ uint32_t quant(double v, const QParams& p) {
-    const double c = fmin(fmax(v, p.lo), p.hi);
+    const double c = np_min(np_max(v, p.lo), p.hi);
     double t = div_rn(q_ds(c, p.lo), p.span, p.inv_span);
-    t = fmin(fmax(t, 0.0), 1.0);
+    if (!(p.hi >= p.lo)) t = np_min(np_max(t, 0.0), 1.0);
     return (uint32_t)rint(q_dm(t, p.levels));
 }
 
 // ref quantize.py:20-24, bit-exact
 __device__ __forceinline__ double dequant(uint32_t code, const QParams& p) {
     return q_da(p.lo, q_dm(div_rn((double)code, p.levels, p.inv_levels), p.dspan));
+}
+
+// the code as an integer-valued double (skips the int round trip when the
+// dequantised value is needed right away)
+__device__ __forceinline__ double quant_d(double v, const QParams& p) {
+    const double c = np_min(np_max(v, p.lo), p.hi);
+    double t = div_rn(q_ds(c, p.lo), p.span, p.inv_span);
+    if (!(p.hi >= p.lo)) t = np_min(np_max(t, 0.0), 1.0);
+    return rint(q_dm(t, p.levels));
+}
+__device__ __forceinline__ double dequant_d(double cd, const QParams& p) {
+    return q_da(p.lo, q_dm(div_rn(cd, p.levels, p.inv_levels), p.dspan));
 }
 
 __device__ __forceinline__ int vlen(uint64_t v) {
@@ -247,7 +265,7 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
         for (int it = 0; it < TK_ITEMS; ++it) {
             double rmax = 0.0;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) rmax = fmax(rmax, fabs(q_ds((double)cv[it][d], (double)bv[it][d])));
+            for (int d = 0; d < 3; ++d) rmax = np_max(rmax, fabs(q_ds((double)cv[it][d], (double)bv[it][d])));
             const bool keep = rmax >= J.gate;
             const unsigned long long bits = (unsigned long long)__double_as_longlong(rmax);
             mall = bits > mall ? bits : mall;
@@ -263,7 +281,7 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
             double rmax = 0.0;
             for (int d = 0; d < dims; ++d) {
                 const int64_t e = row * dims + d;
-                rmax = fmax(rmax, fabs(q_ds((double)cur[e], (double)base[e])));
+                rmax = np_max(rmax, fabs(q_ds((double)cur[e], (double)base[e])));
             }
             keep = rmax >= J.gate;
             const unsigned long long bits = (unsigned long long)__double_as_longlong(rmax);
@@ -303,23 +321,23 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
     for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
     if (lane == 0) s_var[warp] = var;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t cnt = 0, vs = 0;
+    if (warp == 0) {  // chunk summary from the 64 bitmap words, warp-parallel
+        const uint32_t w0 = s_keep[lane], w1 = s_keep[32 + lane];
+        const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(w0) + __popc(w1));
+        const unsigned nz0 = __ballot_sync(0xffffffffu, w0 != 0), nz1 = __ballot_sync(0xffffffffu, w1 != 0);
         int64_t first = -1, last = -1;
-        unsigned long long ma = 0, mk = 0;
-        for (int k = 0; k < TK_CHUNK / 32; ++k) {
-            const uint32_t w = s_keep[k];
-            cnt += __popc(w);
-            if (w) {
-                if (first < 0) first = r0 + 32 * k + (__ffs(w) - 1);
-                last = r0 + 32 * k + (31 - __clz(w));
-            }
+        if (nz0 | nz1) {
+            const int fw = nz0 ? __ffs(nz0) - 1 : 32 + __ffs(nz1) - 1;
+            const int lw = nz1 ? 32 + 31 - __clz(nz1) : 31 - __clz(nz0);
+            first = r0 + 32 * fw + (__ffs(s_keep[fw]) - 1);
+            last = r0 + 32 * lw + (31 - __clz(s_keep[lw]));
         }
-        for (int k = 0; k < TK_THREADS / 32; ++k) {
-            vs += s_var[k];
-            ma = s_mall[k] > ma ? s_mall[k] : ma;
-            mk = s_mkeep[k] > mk ? s_mkeep[k] : mk;
-        }
+        uint32_t vs = lane < TK_THREADS / 32 ? s_var[lane] : 0;
+        vs = __reduce_add_sync(0xffffffffu, vs);
+        unsigned long long ma = lane < TK_THREADS / 32 ? s_mall[lane] : 0, mk = lane < TK_THREADS / 32 ? s_mkeep[lane] : 0;
+        ma = warp_max64(ma);
+        mk = warp_max64(mk);
+        if (lane != 0) return;
         J.ck[c] = cnt;
         J.cfirst[c] = first;
         J.clast[c] = last;
@@ -536,9 +554,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                 float nb[4];
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const uint32_t code = quant(q_ds((double)cs[kk], (double)bs[kk]), rq);
-                    packed |= code << (8 * kk);
-                    nb[kk] = __double2float_rn(q_da((double)bs[kk], dequant(code, rq)));
+                    const double cd = quant_d(q_ds((double)cs[kk], (double)bs[kk]), rq);
+                    packed |= (uint32_t)cd << (8 * kk);
+                    nb[kk] = __double2float_rn(q_da((double)bs[kk], dequant_d(cd, rq)));
                 }
                 n4[w] = make_float4(nb[0], nb[1], nb[2], nb[3]);
                 *reinterpret_cast<uint32_t*>(blk + 4 * w) = packed;  // 20 + 4w: 4-byte aligned
@@ -581,8 +599,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                 float nb[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    code[k] = quant(q_ds((double)cs[k], (double)bs[k]), rq);
-                    nb[k] = __double2float_rn(q_da((double)bs[k], dequant(code[k], rq)));
+                    const double cd = quant_d(q_ds((double)cs[k], (double)bs[k]), rq);
+                    code[k] = (uint32_t)cd;
+                    nb[k] = __double2float_rn(q_da((double)bs[k], dequant_d(cd, rq)));
                 }
                 n4[w] = make_float4(nb[0], nb[1], nb[2], nb[3]);
                 const int64_t e = 4 * w;
@@ -644,7 +663,7 @@ __device__ __forceinline__ void emit_sparse(const Job& J, const QParams& rq, int
             double rmax = 0.0;
             for (int d = 0; d < dims; ++d) {
                 const int64_t e = row * dims + d;
-                rmax = fmax(rmax, fabs(q_ds((double)cur[e], (double)base[e])));
+                rmax = np_max(rmax, fabs(q_ds((double)cur[e], (double)base[e])));
             }
             keep = rmax >= J.gate;
             if (!keep && copy_base)
