@@ -14,7 +14,7 @@ that delta tick.
 
 Metric: optimize views/s (views per step x steps/s, ref cli.py:370-372);
 whole-job aggregate over ranks.  `e2e` is the same metric through the
-public API (optim.step + protocol.encode_delta) with the step's ground-truth
+public API (optim.step + protocol.DeltaTicker, payloads read back to host) with the step's ground-truth
 images copied from pinned host memory every step and the loss and delta
 payload bytes read back.  The reference arm times the CPU oracle port of the
 reference algorithm (oracle/, numpy float64) on the host's cores.
@@ -45,7 +45,7 @@ CROP = 12  # CPU sample: a centre crop of 1/CROP^2 of every view
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1_000_000)
@@ -60,48 +60,74 @@ def parse():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi polled every 50 ms on a reader thread; each sample is stamped
+    with the host clock so only the samples inside the timed window count."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.samples = []
+        self.thread = None
 
     def start(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
 
-    def stop(self):
+        def read():
+            for line in self.proc.stdout:
+                self.samples.append((time.time(), line))
+        self.thread = threading.Thread(target=read, daemon=True)
+        self.thread.start()
+
+    def wait_first(self, timeout=5.0):
+        t = time.time() + timeout
+        while self.proc is not None and not self.samples and time.time() < t:
+            time.sleep(0.02)
+
+    def stop(self, t_begin, t_end):
         if self.proc is None:
             return None
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-            out, _ = self.proc.communicate()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
         sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in out.strip().splitlines():
+        import datetime
+        for ts, line in self.samples:
             p = [x.strip() for x in line.split(",")]
-            if len(p) < 9:
+            if len(p) < 10:
+                continue
+            try:  # nvidia-smi's own sample time (stdout may arrive in bursts)
+                ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                pass
+            if not (t_begin <= ts <= t_end):
                 continue
             try:
-                sm.append(float(p[1]))
-                mx = max(mx, float(p[2]))
+                sm.append(float(p[2]))
+                mx = max(mx, float(p[3]))
             except ValueError:
                 continue
-            for name, v in zip(names, p[5:9]):
+            for name, v in zip(names, p[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "window_s": round(t_end - t_begin, 3)}
 
 
 # ---------------------------------------------------------------- CPU oracle sample
@@ -238,7 +264,7 @@ def run_ours(args):
     from paper_2604_02851_b200 import _lib
     from paper_2604_02851_b200.model import DeviceModel
     from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
-    from paper_2604_02851_b200.protocol import DeltaTicker, PayloadBuffer, encode_delta, encode_snapshot_device
+    from paper_2604_02851_b200.protocol import DeltaTicker, PayloadBuffer, encode_snapshot_device
     from paper_2604_02851_b200.render import render_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -269,19 +295,6 @@ def run_ours(args):
     encode_snapshot_device(dm, 0, None, base_m, base_l)
     bufs = {attr: PayloadBuffer(1 << 20, dev) for attr in DELTA_ORDER}
 
-    def delta_attr_tensors(attr):
-        if attr == 0:
-            return dm.means[:a], base_m[:a]
-        if attr == 1:
-            return dm.log_scales[:a], base_l[:a]
-        if attr == 2:
-            return dm.quaternions[:a], None
-        if attr == 3:
-            return dm.logit_opacities[:a], None
-        if attr == 4:
-            return dm.sh_coeffs[:a, :, 0].contiguous(), None
-        return dm.sh_coeffs[:a, :, 1:].contiguous(), None
-
     baselines = {0: base_m[:a], 1: base_l[:a]}
     ticker = DeltaTicker(dm, baselines, bufs)
 
@@ -292,14 +305,8 @@ def run_ours(args):
         due = [attr for attr in DELTA_ORDER if tick % DELTA_PERIODS[attr] == 0]
         if device_only:  # one batched library call, payloads stay in HBM
             return ticker(due), 0
-        nbytes = 0  # public API: payload bytes read back per attribute
-        for attr in due:
-            cur, base = delta_attr_tensors(attr)
-            payload, new_base = encode_delta(attr, cur, base, None, 0)
-            nbytes += len(payload)
-            if base is not None:
-                base.copy_(new_base)
-        return a * len(due), nbytes
+        ticker(due)  # public API: batched encode, then every payload read back to host
+        return a * len(due), sum(len(p) for p in ticker.read(due))
 
     c = _lib.ctx(local)
     fp32_peak = ctypes_peak(c)
@@ -308,13 +315,14 @@ def run_ours(args):
         step(dm, state, views, process_group=pg, total_views=args.views, workspace=ws, sync_loss=False)
         return delta_tick(i)
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for i in range(args.warmup):
         one_step(i)
+    clocks.wait_first()
     torch.cuda.synchronize()
     if pg is not None:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     _lib.set_timing(c, True)
     _lib.get_timing(c, reset=True)
     t0 = torch.cuda.Event(enable_timing=True)
@@ -322,6 +330,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if pg is not None:
         dist.barrier()
+    w0 = time.time()
     t0.record()
     delta_rows = 0
     for i in range(args.steps):
@@ -331,10 +340,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     if pg is not None:
         dist.barrier()
+    w1 = time.time()
     ms = t0.elapsed_time(t1)
     kt, counters = _lib.get_timing(c, reset=True)
     _lib.set_timing(c, False)
-    clock_rec = clocks.stop()
+    clock_rec = clocks.stop(w0, w1)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if pg is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -398,7 +408,7 @@ def run_ours(args):
            "kernel_ms_per_step": {k: round(v, 4) for k, v in per_step.items()},
            "evaluated_pairs_per_view": evals_per_view,
            "delta_encode": enc, "fp32_peak_tflops_measured": fp32_peak,
-           "precision": "fp64 preprocess/windows/depth keys, fp32 blend, fp64 chain rule, fp64 Adam moments"}
+           "precision": "fp64 preprocess/windows/depth keys, fp32 blend + chain rule, fp64 Adam moments"}
     print(json.dumps(out), flush=True)
     if pg is not None:
         dist.destroy_process_group()

@@ -638,20 +638,24 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, doubl
 }
 
 // ---------------------------------------------------------------- K7 chain rule
-// (a) fixed-order sum of each splat's per-tile partials (rank order: a
-//     thread's pairs follow its neighbour's in memory) -> 9 floats per rank
+// (a) fixed-order sum of each splat's per-tile partials, in input order j
+//     (a splat's partials are contiguous from roffj[j]) -> 9 values per row
 template <typename R>
-__global__ void k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
-                               const R* __restrict__ partials, int64_t n_in, R* __restrict__ g9) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t cnt = rcnt[r];
+__global__ void k_sum_partials(const uint64_t* __restrict__ roffj, const uint32_t* __restrict__ rcnt,
+                               const uint32_t* __restrict__ rinv, const R* __restrict__ partials, int64_t n_in,
+                               R* __restrict__ g9) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = rinv[j];
+        const uint32_t cnt = r == ~0u ? 0u : rcnt[r];
         double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        const R* pp = partials + roff[r] * 9;
-        for (uint32_t i = 0; i < cnt; ++i)
+        if (cnt) {
+            const R* pp = partials + roffj[j] * 9;
+            for (uint32_t i = 0; i < cnt; ++i)
 #pragma unroll
-            for (int e = 0; e < 9; ++e) g[e] += (double)pp[i * 9 + e];
+                for (int e = 0; e < 9; ++e) g[e] += (double)pp[i * 9 + e];
+        }
 #pragma unroll
-        for (int e = 0; e < 9; ++e) g9[r * 9 + e] = (R)g[e];
+        for (int e = 0; e < 9; ++e) g9[j * 9 + e] = (R)g[e];
     }
 }
 
@@ -684,7 +688,7 @@ __global__ void __launch_bounds__(128) k_chain(ss_model m, ss_camera cam, ss_lig
         if (row >= a) continue;
         T g[9];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) g[e] = g9[(int64_t)r * 9 + e];
+        for (int e = 0; e < 9; ++e) g[e] = g9[j * 9 + e];
         // ---- appearance first (the SH registers die early)
         T d[3];
 #pragma unroll
@@ -902,6 +906,34 @@ __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __res
     const int BL = L.ambient_bands < B ? L.ambient_bands : B;
     const int n = nrows * 3 * B;
     float* out = grad_sh + row0 * 3 * B;
+    if constexpr (B % 4 == 0) {  // float4 per thread: 4 bases of one (row, channel)
+        if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            for (int e4 = threadIdx.x; e4 < n / 4; e4 += blockDim.x) {
+                const int e = 4 * e4;
+                const int r = e / (3 * B), rem = e - r * 3 * B, c = rem / B, b0 = rem - c * B;
+                const float4 r0 = s_r0[r];
+                const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
+                if (gcc == 0.f) continue;
+                float v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int b = b0 + k;
+                    const float yb = s_y[r][b];
+                    if (L.ambient_bands == 0) {
+                        v[k] = gcc * yb;
+                    } else {
+                        v[k] = (b < BL ? gcc * (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? gcc * yb : 0.f);
+                    }
+                }
+                if (b0 == 0) v[0] += gcc * (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
+                float4* o4 = reinterpret_cast<float4*>(out + e);
+                float4 cur = *o4;
+                cur.x += v[0]; cur.y += v[1]; cur.z += v[2]; cur.w += v[3];
+                *o4 = cur;
+            }
+            return;
+        }
+    }
     for (int e = threadIdx.x; e < n; e += blockDim.x) {  // coalesced over the block's contiguous rows
         const int r = e / (3 * B), rem = e - r * 3 * B, c = rem / B, b = rem - c * B;
         const float4 r0 = s_r0[r];
@@ -1084,7 +1116,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         float4* shrec = SS_SCRATCH(ctx, float4, 2 * (int64_t)m->active_count);
         if (!g9 || !shrec) return SS_ERR_CUDA;
         SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)m->active_count, s));
-        k_sum_partials<R><<<gridn(ctx, b.n_in), 256, 0, s>>>(b.roff, b.rcnt, partials, b.n_in, g9);
+        k_sum_partials<R><<<gridn(ctx, b.n_in), 256, 0, s>>>(b.roffj, b.rcnt, b.rinv, partials, b.n_in, g9);
         SS_CHECK_LAUNCH(ctx);
 #define SS_CHAIN(DEG)                                                                                     \
     k_chain<R, DEG><<<gridn(ctx, b.n_in, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \

@@ -232,6 +232,30 @@ class DeltaTicker:
         c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
         return self.model.active_count * len(key)
 
+    def read(self, attributes):
+        """Payload bytes of the last call for `attributes`, read back with two
+        host syncs in total (lengths, then every payload into pinned memory)."""
+        import torch
+        key = [int(x) for x in attributes]
+        if not key:
+            return []
+        lens = torch.cat([self.outs[a].length for a in key]).cpu().tolist()
+        total = int(sum(lens))
+        host = getattr(self, "_pinned", None)
+        if host is None or host.numel() < total:
+            host = self._pinned = torch.empty(max(total, 1 << 16) * 5 // 4, dtype=torch.uint8, pin_memory=True)
+        off = 0
+        for a, n in zip(key, lens):
+            host[off:off + n].copy_(self.outs[a].data[:n], non_blocking=True)
+            off += n
+        torch.cuda.current_stream(self.model.device).synchronize()
+        raw = host[:total].numpy().tobytes()
+        out, off = [], 0
+        for n in lens:
+            out.append(raw[off:off + n])
+            off += n
+        return out
+
 
 def delta_tick_device(model, attributes, baselines, outs, gating=None):
     """One-shot DeltaTicker call (see DeltaTicker)."""
