@@ -259,6 +259,10 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, int64_t n, uint2* __
 // when T drops below 1e-4 (the reference's T-gate: later splats skip it).
 constexpr int WPB = 4;   // tiles (warps) per block
 constexpr int PPT = 8;   // pixels per lane
+// pixel rows per warp-uniform skip test: rows of one group form one basic
+// block, so their independent chains interleave (helps the longer backward
+// body; the short forward body prefers the finer skip)
+constexpr int QG_FWD = 1, QG_BWD = 2;
 
 template <typename R> __device__ __forceinline__ R ss_exp(R x);
 template <> __device__ __forceinline__ float ss_exp<float>(float x) { return __expf(x); }
@@ -415,16 +419,19 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
             PixelGeom<R> pg(s, lx, ly0, X0, Y0);
             const unsigned wact = __reduce_or_sync(__activemask(), act);
 #pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-                if (!((wact >> q) & 1u)) continue;  // warp-uniform: no lane needs this pixel row
-                const R G = (act >> q) & 1u ? pg.gauss(s, q) : (R)0;
-                const R alpha = min(s.o * G, (R)ALPHA_CAP);
-                const R w = alpha * T[q];
-                C0[q] += w * s.c0;
-                C1[q] += w * s.c1;
-                C2[q] += w * s.c2;
-                T[q] -= w;  // T (1 - alpha)
-                if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+            for (int g = 0; g < PPT; g += QG_FWD) {
+                if (!((wact >> g) & ((1u << QG_FWD) - 1u))) continue;  // warp-uniform: no lane needs these rows
+#pragma unroll
+                for (int q = g; q < g + QG_FWD; ++q) {
+                    const R G = (act >> q) & 1u ? pg.gauss(s, q) : (R)0;
+                    const R alpha = min(s.o * G, (R)ALPHA_CAP);
+                    const R w = alpha * T[q];
+                    C0[q] += w * s.c0;
+                    C1[q] += w * s.c1;
+                    C2[q] += w * s.c2;
+                    T[q] -= w;  // T (1 - alpha)
+                    if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+                }
             }
         }
         __syncwarp();
@@ -567,35 +574,39 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict_
                 PixelGeom<R> pg(s, lx, ly0, X0, Y0);
                 const unsigned wact = __reduce_or_sync(__activemask(), act);
 #pragma unroll
-                for (int q = 0; q < PPT; ++q) {
-                    if (!((wact >> q) & 1u)) continue;  // warp-uniform skip
-                    const R G = (act >> q) & 1u ? pg.gauss(s, q) : (R)0;
-                    const R oG = s.o * G;
-                    const bool open = oG < (R)ALPHA_CAP;
-                    const R alpha = open ? oG : (R)ALPHA_CAP;
-                    const R w = alpha * T[q];
-                    const R gcol = g0[q] * s.c0 + g1[q] * s.c1 + g2[q] * s.c2;
-                    acc[0] += g0[q] * w;
-                    acc[1] += g1[q] * w;
-                    acc[2] += g2[q] * w;
-                    // dL/dalpha = sum_c gC_c (col_c T - S_c / (1 - alpha)), S = C - prefix - contrib
-                    const R rest = Rr[q] - w * gcol;
-                    const R dal = T[q] * gcol - rest * ss_rcp<R>((R)1 - alpha);
-                    Rr[q] = rest;
-                    const R dG = open ? dal * G : (R)0;
-                    const R gp = open ? dal * alpha : (R)0;
-                    const R y = pg.dy(q);
-                    const R adx = pg.adx0 + s.b * y;
-                    const R ady = pg.bdx0 + s.c * y;
-                    const R gpx = gp * adx, gpy = gp * ady;
-                    acc[3] += dG;
-                    acc[4] += gpx;
-                    acc[5] += gpy;
-                    acc[6] += gpx * adx;
-                    acc[7] += gpx * ady;
-                    acc[8] += gpy * ady;
-                    T[q] -= w;
-                    if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+                for (int g = 0; g < PPT; g += QG_BWD) {
+                    if (!((wact >> g) & ((1u << QG_BWD) - 1u))) continue;  // warp-uniform skip
+#pragma unroll
+                    for (int q = g; q < g + QG_BWD; ++q) {
+                        const R G = (act >> q) & 1u ? pg.gauss(s, q) : (R)0;
+                        const R oG = s.o * G;
+                        const bool open = oG < (R)ALPHA_CAP;
+                        const R alpha = open ? oG : (R)ALPHA_CAP;
+                        const R w = alpha * T[q];
+                        const R gcol = g0[q] * s.c0 + g1[q] * s.c1 + g2[q] * s.c2;
+                        acc[0] += g0[q] * w;
+                        acc[1] += g1[q] * w;
+                        acc[2] += g2[q] * w;
+                        // dL/dalpha = sum_c gC_c (col_c T - S_c / (1 - alpha)), S = C - prefix - contrib
+                        const R rest = Rr[q] - w * gcol;
+                        const R dal = T[q] * gcol - rest * ss_rcp<R>((R)1 - alpha);
+                        Rr[q] = rest;
+                        const R dalm = open ? dal : (R)0;  // capped alpha: no gradient
+                        const R dG = dalm * G;
+                        const R gp = dalm * alpha;
+                        const R y = pg.dy(q);
+                        const R adx = pg.adx0 + s.b * y;
+                        const R ady = pg.bdx0 + s.c * y;
+                        const R gpx = gp * adx, gpy = gp * ady;
+                        acc[3] += dG;
+                        acc[4] += gpx;
+                        acc[5] += gpy;
+                        acc[6] += gpx * adx;
+                        acc[7] += gpx * ady;
+                        acc[8] += gpy * ady;
+                        T[q] -= w;
+                        if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+                    }
                 }
             }
             R* out = partials + (uint64_t)(uint32_t)s.p * 9;
