@@ -54,11 +54,12 @@ struct Job {
     int dims, inner, outer, col0;
     int attr, bits, residual, f64;
     double gate, qlo, qhi;
+    float gate_lo, gate_hi;  // float32 bracket of gate: rmax32 > hi keeps, < lo drops, else exact fp64 test
     QParams q;             // absolute quantizer
     int64_t chunk0;        // first global chunk of this job
     int64_t nchunks;
     // residual scratch
-    unsigned long long* g;  // [0] count, [1] max_all bits, [2] max_keep bits
+    unsigned long long* g;  // [0] count, [1] max_all, [2] max_keep (f32 bits of max|r|), [3] finished chunks
     uint32_t* ck;           // per chunk: kept rows
     int64_t* cfirst;        // per chunk: first kept row (-1)
     int64_t* clast;         // per chunk: last kept row (-1)
@@ -164,16 +165,6 @@ __device__ __forceinline__ int find_job(const Batch& B, int64_t chunk) {
 }
 
 // ---------------------------------------------------------------- scan
-// warp-aggregated block reductions (one shared atomic per warp)
-__device__ __forceinline__ unsigned long long warp_max64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
-        v = t > v ? t : v;
-    }
-    return v;
-}
-
 template <typename T>
 __device__ __forceinline__ void scan_absolute(const Job& J, const int* s_col, int64_t r0, int64_t r1) {
     uint8_t* blk = J.out + 12;
@@ -239,6 +230,30 @@ __device__ __forceinline__ void scan_absolute(const Job& J, const int* s_col, in
     }
 }
 
+// exact fp64 gate test of one row (ref delta.py:95-96)
+template <typename T>
+__device__ __forceinline__ bool keep_exact(const T* cur, const T* base, int64_t row, int dims, double gate) {
+    double rmax = 0.0;
+    for (int d = 0; d < dims; ++d)
+        rmax = np_max(rmax, fabs(q_ds((double)cur[row * dims + d], (double)base[row * dims + d])));
+    return rmax >= gate;
+}
+
+// Per-row statistics: rm = RN32(max_d |r_d|) and keep = (max_d |r_d| >= gate)
+// with r = f64(cur) - f64(base).  For float32 inputs the residual is formed in
+// float32: RN32(a - b) = RN32(RN64(a - b)) for float32 a, b (the difference is
+// exact in fp64 unless |b| < 2^-29 |a|, and then no float32 rounding boundary
+// lies within an fp64 ulp of it), |.| and max commute with monotone
+// rounding, so rm is exactly RN32 of the fp64 maximum; the gate is decided in
+// float32 outside a 2^-20 relative band around it and in fp64 inside.
+__device__ __forceinline__ float f_max(float a, float b) { return a >= b ? a : b; }
+
+__device__ __forceinline__ bool gate_keep(float rm, const Job& J, const float* cur, const float* base, int64_t row) {
+    if (rm > J.gate_hi) return true;
+    if (rm < J.gate_lo) return false;
+    return keep_exact<float>(cur, base, row, J.dims, J.gate);
+}
+
 template <typename T>
 __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r0, int64_t r1) {
     __shared__ uint32_t s_keep[TK_CHUNK / 32];  // kept-row bitmap of this chunk
@@ -248,26 +263,29 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
     const T* base = (const T*)J.base;
     const int dims = J.dims;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long mall = 0, mkeep = 0;
-    if (dims == 3 && r1 - r0 == TK_CHUNK) {
+    uint32_t mall = 0, mkeep = 0;  // f32 bits of non-negative maxima (ordered as integers)
+    if (sizeof(T) == 4 && dims == 3 && r1 - r0 == TK_CHUNK) {
         // full chunk, dims 3: issue all 48 loads of the thread's 8 rows first
-        T cv[TK_ITEMS][3], bv[TK_ITEMS][3];
+        const float* cf = (const float*)cur;
+        const float* bf = (const float*)base;
+        float cv[TK_ITEMS][3], bv[TK_ITEMS][3];
 #pragma unroll
         for (int it = 0; it < TK_ITEMS; ++it) {
             const int64_t row = r0 + it * TK_THREADS + threadIdx.x;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                cv[it][d] = cur[row * 3 + d];
-                bv[it][d] = base[row * 3 + d];
+                cv[it][d] = cf[row * 3 + d];
+                bv[it][d] = bf[row * 3 + d];
             }
         }
 #pragma unroll
         for (int it = 0; it < TK_ITEMS; ++it) {
-            double rmax = 0.0;
+            const int64_t row = r0 + it * TK_THREADS + threadIdx.x;
+            float rm = 0.f;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) rmax = np_max(rmax, fabs(q_ds((double)cv[it][d], (double)bv[it][d])));
-            const bool keep = rmax >= J.gate;
-            const unsigned long long bits = (unsigned long long)__double_as_longlong(rmax);
+            for (int d = 0; d < 3; ++d) rm = f_max(rm, fabsf(cv[it][d] - bv[it][d]));
+            const bool keep = gate_keep(rm, J, cf, bf, row);
+            const uint32_t bits = __float_as_uint(rm);
             mall = bits > mall ? bits : mall;
             if (keep) mkeep = bits > mkeep ? bits : mkeep;
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -278,21 +296,29 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
         const int64_t row = r0 + it * TK_THREADS + threadIdx.x;  // striped: coalesced per item
         bool keep = false;
         if (row < r1) {
-            double rmax = 0.0;
-            for (int d = 0; d < dims; ++d) {
-                const int64_t e = row * dims + d;
-                rmax = np_max(rmax, fabs(q_ds((double)cur[e], (double)base[e])));
+            float rm;
+            if constexpr (sizeof(T) == 4) {
+                rm = 0.f;
+                for (int d = 0; d < dims; ++d) rm = f_max(rm, fabsf(cur[row * dims + d] - base[row * dims + d]));
+                keep = gate_keep(rm, J, (const float*)cur, (const float*)base, row);
+            } else {
+                double rmax = 0.0;
+                for (int d = 0; d < dims; ++d) {
+                    const int64_t e = row * dims + d;
+                    rmax = np_max(rmax, fabs(q_ds((double)cur[e], (double)base[e])));
+                }
+                keep = rmax >= J.gate;
+                rm = __double2float_rn(rmax);
             }
-            keep = rmax >= J.gate;
-            const unsigned long long bits = (unsigned long long)__double_as_longlong(rmax);
+            const uint32_t bits = __float_as_uint(rm);
             mall = bits > mall ? bits : mall;
             if (keep) mkeep = bits > mkeep ? bits : mkeep;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) s_keep[it * (TK_THREADS / 32) + warp] = bal;
     }
-    mall = warp_max64(mall);
-    mkeep = warp_max64(mkeep);
+    mall = __reduce_max_sync(0xffffffffu, mall);
+    mkeep = __reduce_max_sync(0xffffffffu, mkeep);
     if (lane == 0) {
         s_mall[warp] = mall;
         s_mkeep[warp] = mkeep;
@@ -334,54 +360,29 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
         }
         uint32_t vs = lane < TK_THREADS / 32 ? s_var[lane] : 0;
         vs = __reduce_add_sync(0xffffffffu, vs);
-        unsigned long long ma = lane < TK_THREADS / 32 ? s_mall[lane] : 0, mk = lane < TK_THREADS / 32 ? s_mkeep[lane] : 0;
-        ma = warp_max64(ma);
-        mk = warp_max64(mk);
-        if (lane != 0) return;
-        J.ck[c] = cnt;
-        J.cfirst[c] = first;
-        J.clast[c] = last;
-        J.cvar[c] = vs;
-        if (cnt) atomicAdd(&J.g[0], (unsigned long long)cnt);
-        atomicMax(&J.g[1], ma);
-        atomicMax(&J.g[2], mk);
-    }
-}
-
-__global__ void __launch_bounds__(TK_THREADS) k_tick_scan(Batch B, int64_t chunk_begin) {
-    const int64_t chunk = chunk_begin + blockIdx.x;
-    const Job& J = B.j[find_job(B, chunk)];
-    const int64_t c = chunk - J.chunk0;
-    const int64_t r0 = c * TK_CHUNK;
-    const int64_t r1 = min(r0 + TK_CHUNK, J.rows);
-    if (J.residual) {
-        if (J.f64) scan_residual<double>(J, c, r0, r1);
-        else scan_residual<float>(J, c, r0, r1);
-        return;
-    }
-    __shared__ int s_col[TK_MAX_DIMS];
-    build_cols(J, s_col);
-    if (J.f64) scan_absolute<double>(J, s_col, r0, r1);
-    else scan_absolute<float>(J, s_col, r0, r1);
-    if (c == 0 && threadIdx.x == 0) {
-        const uint64_t blen = J.attr == 6 ? (uint64_t)(J.rows + 7) / 8 : (uint64_t)(J.rows * J.dims * J.bits + 7) / 8;
-        uint8_t* o = J.out;
-        o[0] = (uint8_t)J.attr;
-        o[1] = 2;
-        o[2] = 0;
-        o[3] = (uint8_t)J.dims;
-        put32(o + 4, (uint32_t)J.rows);
-        put32(o + 8, (uint32_t)blen);
-        *J.out_len = 12 + blen;
+        const uint32_t ma = __reduce_max_sync(0xffffffffu, lane < TK_THREADS / 32 ? (uint32_t)s_mall[lane] : 0u);
+        const uint32_t mk = __reduce_max_sync(0xffffffffu, lane < TK_THREADS / 32 ? (uint32_t)s_mkeep[lane] : 0u);
+        if (lane == 0) {
+            J.ck[c] = cnt;
+            J.cfirst[c] = first;
+            J.clast[c] = last;
+            J.cvar[c] = vs;
+            if (cnt) atomicAdd(&J.g[0], (unsigned long long)cnt);
+            atomicMax(&J.g[1], (unsigned long long)ma);
+            atomicMax(&J.g[2], (unsigned long long)mk);
+        }
     }
 }
 
 // ---------------------------------------------------------------- plan
-constexpr int PLAN_THREADS = 1024;
+// Run by the last block to finish a residual job's scan (or by k_tick_plan
+// for a job without rows): mode decision (k < rows/2, delta.py:101), f32
+// range m, per-chunk prefixes for the sparse writer, header, payload length.
+// Chunk statistics written by other blocks are read with ld.global.cg (L2).
 
-// inclusive block scan (sum) over PLAN_THREADS threads; returns the block total in *tot
+// inclusive block scan (sum) over TK_THREADS threads; returns the block total in *tot
 __device__ __forceinline__ uint64_t plan_scan_sum(uint64_t v, uint64_t* tot) {
-    __shared__ uint64_t ws[PLAN_THREADS / 32];
+    __shared__ uint64_t ws[TK_THREADS / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -390,25 +391,21 @@ __device__ __forceinline__ uint64_t plan_scan_sum(uint64_t v, uint64_t* tot) {
     }
     if (lane == 31) ws[w] = v;
     __syncthreads();
-    if (w == 0) {
-        uint64_t x = ws[lane];
+    uint64_t pre = 0, all = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t t = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += t;
-        }
-        ws[lane] = x;
+    for (int k = 0; k < TK_THREADS / 32; ++k) {
+        const uint64_t x = ws[k];
+        if (k < w) pre += x;
+        all += x;
     }
+    *tot = all;
     __syncthreads();
-    const uint64_t out = v + (w ? ws[w - 1] : 0);
-    *tot = ws[PLAN_THREADS / 32 - 1];
-    __syncthreads();
-    return out;
+    return v + pre;
 }
 
 // inclusive block scan (max) of signed values
-__device__ __forceinline__ long long plan_scan_max(long long v, long long* tot) {
-    __shared__ long long ws[PLAN_THREADS / 32];
+__device__ __forceinline__ long long plan_scan_max(long long v, long long* tot, long long* excl) {
+    __shared__ long long ws[TK_THREADS / 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -417,32 +414,27 @@ __device__ __forceinline__ long long plan_scan_max(long long v, long long* tot) 
     }
     if (lane == 31) ws[w] = v;
     __syncthreads();
-    if (w == 0) {
-        long long x = ws[lane];
+    long long pre = -1, all = -1;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long t = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o && t > x) x = t;
-        }
-        ws[lane] = x;
+    for (int k = 0; k < TK_THREADS / 32; ++k) {
+        const long long x = ws[k];
+        if (k < w && x > pre) pre = x;
+        if (x > all) all = x;
     }
+    long long up = __shfl_up_sync(0xffffffffu, v, 1);
+    if (lane == 0) up = -1;
+    *excl = up > pre ? up : pre;  // exclusive max (earlier threads of the block)
+    *tot = all;
     __syncthreads();
-    const long long pw = w ? ws[w - 1] : -1;
-    const long long out = pw > v ? pw : v;
-    *tot = ws[PLAN_THREADS / 32 - 1];
-    __syncthreads();
-    return out;
+    return v > pre ? v : pre;
 }
 
-__global__ void __launch_bounds__(PLAN_THREADS) k_tick_plan(Batch B, int only) {
-    if (only >= 0 && (int)blockIdx.x != only) return;
-    const Job& J = B.j[blockIdx.x];
-    if (!J.residual) return;
-    const unsigned long long k = J.g[0];
+__device__ void plan_job(const Job& J) {
+    const unsigned long long k = __ldcg(&J.g[0]);
     const int sparse = 2 * (int64_t)k < J.rows;  // k < rows * 0.5 (delta.py:101)
     double m;
-    if (sparse) m = k ? (double)__double2float_rn(__longlong_as_double((long long)J.g[2])) : 0.0;
-    else m = J.rows ? (double)__double2float_rn(__longlong_as_double((long long)J.g[1])) : 0.0;
+    if (sparse) m = k ? (double)__uint_as_float((uint32_t)__ldcg(&J.g[2])) : 0.0;
+    else m = J.rows ? (double)__uint_as_float((uint32_t)__ldcg(&J.g[1])) : 0.0;
     if (threadIdx.x == 0) {
         *J.mode = sparse;
         *J.m = m;
@@ -459,31 +451,21 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_tick_plan(Batch B, int only) {
     }
     uint64_t V = 0;
     if (sparse) {
-        // per-chunk prefixes for the sparse writer: survivors, varint bytes
-        // and the last kept row before each chunk (block scans, carried over
-        // rounds of PLAN_THREADS chunks)
+        // per-chunk prefixes: survivors, varint bytes and the last kept row
+        // before each chunk (block scans carried over rounds of TK_THREADS chunks)
         uint64_t kc = 0, vc = 0;
         long long lc = -1;
-        for (int64_t c0 = 0; c0 < J.nchunks; c0 += PLAN_THREADS) {
+        for (int64_t c0 = 0; c0 < J.nchunks; c0 += TK_THREADS) {
             const int64_t c = c0 + threadIdx.x;
             const bool in = c < J.nchunks;
-            const uint32_t ck = in ? J.ck[c] : 0;
-            const long long cl = in && ck ? (long long)J.clast[c] : -1;
+            const uint32_t ck = in ? __ldcg(&J.ck[c]) : 0;
+            const long long cl = in && ck ? (long long)__ldcg(&J.clast[c]) : -1;
             uint64_t ktot;
             const uint64_t kin = plan_scan_sum(ck, &ktot);
-            long long ltot;
-            const long long lin = plan_scan_max(cl, &ltot);
-            // last kept row before chunk c: inclusive max of earlier chunks
-            long long prev = __shfl_up_sync(0xffffffffu, lin, 1);
-            {
-                __shared__ long long wl[PLAN_THREADS / 32];
-                if ((threadIdx.x & 31) == 31) wl[threadIdx.x >> 5] = lin;
-                __syncthreads();
-                if ((threadIdx.x & 31) == 0) prev = threadIdx.x ? wl[(threadIdx.x >> 5) - 1] : -1;
-                __syncthreads();
-            }
+            long long ltot, prev;
+            plan_scan_max(cl, &ltot, &prev);
             if (prev < lc) prev = lc;
-            const uint64_t vbytes = in && ck ? (uint64_t)vlen((uint64_t)(J.cfirst[c] - prev - 1)) + J.cvar[c] : 0;
+            const uint64_t vbytes = in && ck ? (uint64_t)vlen((uint64_t)(__ldcg(&J.cfirst[c]) - prev - 1)) + __ldcg(&J.cvar[c]) : 0;
             uint64_t vtot;
             const uint64_t vin = plan_scan_sum(vbytes, &vtot);
             if (in) {
@@ -519,6 +501,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_tick_plan(Batch B, int only) {
         J.var_pre[J.nchunks] = V;  // total varint bytes (sparse code offset)
     }
 }
+
+// a residual job without rows (no scan block runs its plan)
+__global__ void __launch_bounds__(TK_THREADS) k_tick_plan(Batch B, int job) { plan_job(B.j[job]); }
 
 // ---------------------------------------------------------------- emit
 template <typename T>
@@ -725,11 +710,17 @@ __device__ __forceinline__ void emit_sparse(const Job& J, const QParams& rq, int
     }
 }
 
-__global__ void __launch_bounds__(TK_THREADS) k_tick_emit(Batch B, int64_t chunk_begin) {
-    const int64_t chunk = chunk_begin + blockIdx.x;
-    const Job& J = B.j[find_job(B, chunk)];
-    if (!J.residual) return;
-    const int64_t c = chunk - J.chunk0;
+// One launch = [emit blocks of one residual job] + [scan blocks of the next
+// residual job, or of every absolute job].  The emit part reads the plan the
+// previous launch's last scan block wrote.
+struct Phase {
+    int emit_job;          // -1: no emit part
+    int64_t emit_chunks;
+    int64_t scan_chunk0;   // global chunk of the first scan block
+    int64_t scan_chunks;
+};
+
+__device__ __forceinline__ void emit_chunk(const Job& J, int64_t c) {
     const int64_t r0 = c * TK_CHUNK;
     const int64_t r1 = min(r0 + TK_CHUNK, J.rows);
     const QParams rq = *J.rq;
@@ -740,6 +731,54 @@ __global__ void __launch_bounds__(TK_THREADS) k_tick_emit(Batch B, int64_t chunk
         if (J.f64) emit_sparse<double>(J, rq, c, r0, r1);
         else emit_sparse<float>(J, rq, c, r0, r1);
     }
+}
+
+__device__ __forceinline__ void scan_chunk(const Job& J, int64_t c) {
+    const int64_t r0 = c * TK_CHUNK;
+    const int64_t r1 = min(r0 + TK_CHUNK, J.rows);
+    if (J.residual) {
+        if (J.f64) scan_residual<double>(J, c, r0, r1);
+        else scan_residual<float>(J, c, r0, r1);
+        // the last block to finish this job's scan plans it
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&J.g[3], 1ull) == (unsigned long long)(J.nchunks - 1);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            plan_job(J);
+        }
+        return;
+    }
+    __shared__ int s_col[TK_MAX_DIMS];
+    build_cols(J, s_col);
+    if (J.f64) scan_absolute<double>(J, s_col, r0, r1);
+    else scan_absolute<float>(J, s_col, r0, r1);
+    if (c == 0 && threadIdx.x == 0) {
+        const uint64_t blen = J.attr == 6 ? (uint64_t)(J.rows + 7) / 8 : (uint64_t)(J.rows * J.dims * J.bits + 7) / 8;
+        uint8_t* o = J.out;
+        o[0] = (uint8_t)J.attr;
+        o[1] = 2;
+        o[2] = 0;
+        o[3] = (uint8_t)J.dims;
+        put32(o + 4, (uint32_t)J.rows);
+        put32(o + 8, (uint32_t)blen);
+        *J.out_len = 12 + blen;
+    }
+}
+
+__global__ void __launch_bounds__(TK_THREADS) k_tick(Batch B, Phase P) {
+    const int64_t b = blockIdx.x;
+    if (b < P.emit_chunks) {
+        emit_chunk(B.j[P.emit_job], b);
+        return;
+    }
+    const int64_t chunk = P.scan_chunk0 + (b - P.emit_chunks);
+    const Job& J = B.j[find_job(B, chunk)];
+    scan_chunk(J, chunk - J.chunk0);
 }
 
 }  // namespace
@@ -789,6 +828,13 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         J.col0 = s.col0;
         J.f64 = s.in_dtype == 1;
         J.gate = s.gating_threshold;
+        if (!(J.gate > 1e-30)) {  // gate <= 0: rmax >= 0 >= gate keeps every row; tiny or NaN gates take the exact test
+            J.gate_hi = J.gate <= 0.0 ? -1.0f : INFINITY;
+            J.gate_lo = J.gate <= 0.0 ? -2.0f : -INFINITY;
+        } else {
+            J.gate_hi = nextafterf((float)(J.gate * (1.0 + 0x1p-20)), INFINITY);
+            J.gate_lo = nextafterf((float)(J.gate * (1.0 - 0x1p-20)), -INFINITY);
+        }
         J.nchunks = (s.rows + TK_CHUNK - 1) / TK_CHUNK;
         if (J.residual) any_resid = true;
     }
@@ -805,7 +851,7 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         Job& J = B.j[i];
         if (!J.residual) continue;
         const int64_t nc = J.nchunks + 1;
-        J.g = SS_SCRATCH(ctx, unsigned long long, 3);
+        J.g = SS_SCRATCH(ctx, unsigned long long, 4);
         J.ck = SS_SCRATCH(ctx, uint32_t, nc);
         J.cfirst = SS_SCRATCH(ctx, int64_t, nc);
         J.clast = SS_SCRATCH(ctx, int64_t, nc);
@@ -819,33 +865,39 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         if (!J.g || !J.ck || !J.cfirst || !J.clast || !J.cvar || !J.cnt_pre || !J.var_pre || !J.prev_last || !J.m || !J.rq ||
             !J.mode)
             return SS_ERR_CUDA;
-        SS_CUDA(ctx, cudaMemsetAsync(J.g, 0, 3 * sizeof(unsigned long long), ctx->stream));
+        SS_CUDA(ctx, cudaMemsetAsync(J.g, 0, 4 * sizeof(unsigned long long), ctx->stream));
         scratch += 1;
     }
     ss_tic(ctx, KC_CODEC);
-    // residual jobs one at a time: stats -> plan -> emit back to back, so the
-    // emit pass re-reads that job's cur/base (24 B/row) from L2
-    for (int i = 0; i < njobs; ++i) {
-        const Job& J = B.j[i];
-        if (!J.residual) continue;
-        if (J.nchunks) {
-            k_tick_scan<<<(unsigned)J.nchunks, TK_THREADS, 0, ctx->stream>>>(B, J.chunk0);
-            SS_CHECK_LAUNCH(ctx);
-        }
-        k_tick_plan<<<njobs, PLAN_THREADS, 0, ctx->stream>>>(B, i);
-        SS_CHECK_LAUNCH(ctx);
-        if (J.nchunks) {
-            k_tick_emit<<<(unsigned)J.nchunks, TK_THREADS, 0, ctx->stream>>>(B, J.chunk0);
-            SS_CHECK_LAUNCH(ctx);
-        }
-    }
-    // absolute jobs: one streaming launch over their chunks (numbered first)
+    // launches: [scan r0], [emit r0 + scan r1], ..., [emit r_last + scan absolute]:
+    // each residual job's emit re-reads its cur/base (24 B/row) from L2 right
+    // after its scan, and its plan runs at the end of its scan launch
     int64_t abs_chunks = 0;
     for (int i = 0; i < njobs; ++i)
         if (!B.j[i].residual) abs_chunks += B.j[i].nchunks;
-    if (abs_chunks) {
-        k_tick_scan<<<(unsigned)abs_chunks, TK_THREADS, 0, ctx->stream>>>(B, 0);
-        SS_CHECK_LAUNCH(ctx);
+    int prev = -1;
+    for (int i = 0; i <= njobs; ++i) {
+        if (i < njobs && !B.j[i].residual) continue;
+        Phase P;
+        P.emit_job = prev;
+        P.emit_chunks = prev >= 0 ? B.j[prev].nchunks : 0;
+        if (i < njobs) {
+            P.scan_chunk0 = B.j[i].chunk0;
+            P.scan_chunks = B.j[i].nchunks;
+        } else {
+            P.scan_chunk0 = 0;
+            P.scan_chunks = abs_chunks;
+        }
+        const int64_t blocks = P.emit_chunks + P.scan_chunks;
+        if (blocks) {
+            k_tick<<<(unsigned)blocks, TK_THREADS, 0, ctx->stream>>>(B, P);
+            SS_CHECK_LAUNCH(ctx);
+        }
+        if (i < njobs && B.j[i].nchunks == 0) {  // no scan block: plan it here
+            k_tick_plan<<<1, TK_THREADS, 0, ctx->stream>>>(B, i);
+            SS_CHECK_LAUNCH(ctx);
+        }
+        if (i < njobs) prev = i;
     }
     // jobs with zero rows and no chunk still need their header
     for (int i = 0; i < njobs; ++i) {

@@ -147,3 +147,32 @@ def test_gpu_batched_delta_tick_matches_oracle(degree):
                          5: h.sh_coeffs[:, :, 1:]}[attr][:a]
                     r = oc.delta_payload(attr, x, None, None, 0)[0]
                 assert g == r, (tick, attr)
+
+
+def test_gpu_delta_gate_boundary_exact():
+    """Residuals within a few float32 ulps of the gating threshold (the
+    float32 fast path defers to the exact float64 test there), gates equal to
+    a residual, zero and negative gates, both modes."""
+    require_gpu()
+    from oracle import codec as oc
+    from paper_2604_02851_b200.protocol import encode_delta
+    rng = np.random.default_rng(17)
+    n = 5000
+    for gate in (1e-3, float(np.float32(1e-3)), 2.5e-4, 0.0, -1.0):
+        g32 = np.float32(gate) if gate > 0 else np.float32(1e-3)
+        near = np.array([g32, np.nextafter(g32, np.float32(0)), np.nextafter(g32, np.float32(1)),
+                         np.nextafter(np.nextafter(g32, np.float32(0)), np.float32(0))], np.float32)
+        for frac in (0.1, 0.8):
+            base = rng.uniform(-2, 2, (n, 3)).astype(np.float32)
+            cur = base.copy()
+            mv = rng.random(n) < frac
+            cur[mv] += rng.normal(0, 0.01, (int(mv.sum()), 3)).astype(np.float32)
+            # rows whose largest |residual| sits on the gate (base 0 keeps the residual exact)
+            idx = rng.choice(n, 400, replace=False)
+            base[idx] = 0.0
+            cur[idx] = rng.choice(near, (400, 3)) * rng.choice([-1, 1], (400, 3)).astype(np.float32)
+            for attr in (0, 1):
+                g, gb = encode_delta(attr, cur, base, gate, 0)
+                r, rb = oc.delta_payload(attr, cur, base, gate, 0)
+                assert g == r, (gate, frac, attr)
+                np.testing.assert_array_equal(gb, rb)
