@@ -24,6 +24,7 @@ constexpr int TK_THREADS = 256;
 constexpr int TK_ITEMS = 8;
 constexpr int TK_CHUNK = TK_THREADS * TK_ITEMS;  // rows per block
 constexpr int TK_MAX_JOBS = 8;
+constexpr int EMIT_U = 3;  // float4 steps in flight per thread: 3 x 2 rounds = a full dims-3 chunk
 
 struct QParams {
     double lo, hi, span, inv_span, levels, inv_levels, dspan;  // dspan = hi - lo (dequantizer)
@@ -121,6 +122,21 @@ __device__ __forceinline__ double quant_d(double v, const QParams& p) {
 }
 __device__ __forceinline__ double dequant_d(double cd, const QParams& p) {
     return q_da(p.lo, q_dm(div_rn(cd, p.levels, p.inv_levels), p.dspan));
+}
+
+// Residual quantizer over [-m, m] (ref quantize.py:8-24 via delta.py:109-110,
+// 117-118), bit-exact with the clip moved after the rounding: RN is monotone,
+// so r > m gives t >= 1 and a code >= levels, r < -m gives t <= 0 and a code
+// <= 0, and clamping the integer code reproduces clip-then-quantize; m == 0
+// (span 1, every residual below the smallest subnormal) codes 0.
+__device__ __forceinline__ int rquant(double r, const QParams& p) {
+    const double t = div_rn(q_ds(r, p.lo), p.span, p.inv_span);
+    const int code = __double2int_rn(q_dm(t, p.levels));
+    return min(max(code, 0), (int)p.levels);
+}
+// advanced baseline f32(f64(base) + dequant(code))
+__device__ __forceinline__ float radvance(double b, int code, const QParams& p) {
+    return __double2float_rn(q_da(b, dequant_d((double)code, p)));
 }
 
 __device__ __forceinline__ int vlen(uint64_t v) {
@@ -519,10 +535,10 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
         const float4* b4 = (const float4*)base;
         float4* n4 = (float4*)J.new_base;
         uint8_t* blk = J.out + 20;
-        for (int64_t v = v0 + threadIdx.x; v < v1; v += 4 * TK_THREADS) {
-            float4 cc[4], bb[4];
+        for (int64_t v = v0 + threadIdx.x; v < v1; v += EMIT_U * TK_THREADS) {
+            float4 cc[EMIT_U], bb[EMIT_U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < EMIT_U; ++u) {
                 const int64_t w = v + u * TK_THREADS;
                 if (w < v1) {
                     cc[u] = c4[w];
@@ -530,7 +546,7 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < EMIT_U; ++u) {
                 const int64_t w = v + u * TK_THREADS;
                 if (w >= v1) continue;
                 const float cs[4] = {cc[u].x, cc[u].y, cc[u].z, cc[u].w};
@@ -539,9 +555,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                 float nb[4];
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const double cd = quant_d(q_ds((double)cs[kk], (double)bs[kk]), rq);
-                    packed |= (uint32_t)cd << (8 * kk);
-                    nb[kk] = __double2float_rn(q_da((double)bs[kk], dequant_d(cd, rq)));
+                    const int code = rquant(q_ds((double)cs[kk], (double)bs[kk]), rq);
+                    packed |= (uint32_t)code << (8 * kk);
+                    nb[kk] = radvance((double)bs[kk], code, rq);
                 }
                 n4[w] = make_float4(nb[0], nb[1], nb[2], nb[3]);
                 *reinterpret_cast<uint32_t*>(blk + 4 * w) = packed;  // 20 + 4w: 4-byte aligned
@@ -549,9 +565,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
         }
         for (int64_t e = 4 * v1 + threadIdx.x; e < e1; e += TK_THREADS) {
             const double b = (double)base[e];
-            const uint32_t code = quant(q_ds((double)cur[e], b), rq);
+            const int code = rquant(q_ds((double)cur[e], b), rq);
             blk[e] = (uint8_t)code;
-            J.new_base[e] = __double2float_rn(q_da(b, dequant(code, rq)));
+            J.new_base[e] = radvance(b, code, rq);
         }
         return;
     }
@@ -564,10 +580,10 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
         float4* n4 = (float4*)J.new_base;
         uint2* code4 = (uint2*)(J.out + 24);  // 8-byte aligned view starting 4 bytes past the block
         uint16_t* blk = (uint16_t*)(J.out + 20);
-        for (int64_t v = v0 + threadIdx.x; v < v1; v += 4 * TK_THREADS) {
-            float4 cc[4], bb[4];
+        for (int64_t v = v0 + threadIdx.x; v < v1; v += EMIT_U * TK_THREADS) {
+            float4 cc[EMIT_U], bb[EMIT_U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < EMIT_U; ++u) {
                 const int64_t w = v + u * TK_THREADS;
                 if (w < v1) {
                     cc[u] = c4[w];
@@ -575,7 +591,7 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < EMIT_U; ++u) {
                 const int64_t w = v + u * TK_THREADS;
                 if (w >= v1) continue;
                 const float cs[4] = {cc[u].x, cc[u].y, cc[u].z, cc[u].w};
@@ -584,9 +600,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                 float nb[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const double cd = quant_d(q_ds((double)cs[k], (double)bs[k]), rq);
-                    code[k] = (uint32_t)cd;
-                    nb[k] = __double2float_rn(q_da((double)bs[k], dequant_d(cd, rq)));
+                    const int cq = rquant(q_ds((double)cs[k], (double)bs[k]), rq);
+                    code[k] = (uint32_t)cq;
+                    nb[k] = radvance((double)bs[k], cq, rq);
                 }
                 n4[w] = make_float4(nb[0], nb[1], nb[2], nb[3]);
                 const int64_t e = 4 * w;
@@ -598,9 +614,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
         // tail elements (e1 not a multiple of 4)
         for (int64_t e = 4 * v1 + threadIdx.x; e < e1; e += TK_THREADS) {
             const double b = (double)base[e];
-            const uint32_t code = quant(q_ds((double)cur[e], b), rq);
+            const int code = rquant(q_ds((double)cur[e], b), rq);
             blk[e] = (uint16_t)code;
-            J.new_base[e] = __double2float_rn(q_da(b, dequant(code, rq)));
+            J.new_base[e] = radvance(b, code, rq);
         }
         return;
     }
@@ -608,17 +624,17 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
         uint16_t* blk = (uint16_t*)(J.out + 20);  // 2-byte aligned (out is 256-byte aligned)
         for (int64_t e = r0 * J.dims + threadIdx.x; e < e1; e += TK_THREADS) {
             const double b = (double)base[e];
-            const uint32_t code = quant(q_ds((double)cur[e], b), rq);
+            const int code = rquant(q_ds((double)cur[e], b), rq);
             blk[e] = (uint16_t)code;
-            if (J.new_base) J.new_base[e] = __double2float_rn(q_da(b, dequant(code, rq)));
+            if (J.new_base) J.new_base[e] = radvance(b, code, rq);
         }
     } else {
         uint8_t* blk = J.out + 20;
         for (int64_t e = r0 * J.dims + threadIdx.x; e < e1; e += TK_THREADS) {
             const double b = (double)base[e];
-            const uint32_t code = quant(q_ds((double)cur[e], b), rq);
+            const int code = rquant(q_ds((double)cur[e], b), rq);
             blk[e] = (uint8_t)code;
-            if (J.new_base) J.new_base[e] = __double2float_rn(q_da(b, dequant(code, rq)));
+            if (J.new_base) J.new_base[e] = radvance(b, code, rq);
         }
     }
 }
@@ -696,14 +712,14 @@ __device__ __forceinline__ void emit_sparse(const Job& J, const QParams& rq, int
             for (int d = 0; d < dims; ++d) {
                 const int64_t e = row * dims + d;
                 const double bb = (double)base[e];
-                const uint32_t code = quant(q_ds((double)cur[e], bb), rq);
+                const uint32_t code = (uint32_t)rquant(q_ds((double)cur[e], bb), rq);
                 if (cb == 2) {
                     cp[2 * d] = code & 0xff;
                     cp[2 * d + 1] = code >> 8;
                 } else {
                     cp[d] = (uint8_t)code;
                 }
-                if (J.new_base) J.new_base[e] = __double2float_rn(q_da(bb, dequant(code, rq)));
+                if (J.new_base) J.new_base[e] = radvance(bb, (int)code, rq);
             }
             ++k;
         }
