@@ -730,7 +730,7 @@ __device__ __forceinline__ void emit_sparse(const Job& J, const QParams& rq, int
 // residual job, or of every absolute job].  The emit part reads the plan the
 // previous launch's last scan block wrote.
 struct Phase {
-    int emit_job;          // -1: no emit part
+    int64_t emit_chunk0;   // global chunk of the first emit block
     int64_t emit_chunks;
     int64_t scan_chunk0;   // global chunk of the first scan block
     int64_t scan_chunks;
@@ -789,7 +789,9 @@ __device__ __forceinline__ void scan_chunk(const Job& J, int64_t c) {
 __global__ void __launch_bounds__(TK_THREADS) k_tick(Batch B, Phase P) {
     const int64_t b = blockIdx.x;
     if (b < P.emit_chunks) {
-        emit_chunk(B.j[P.emit_job], b);
+        const int64_t chunk = P.emit_chunk0 + b;
+        const Job& J = B.j[find_job(B, chunk)];
+        emit_chunk(J, chunk - J.chunk0);
         return;
     }
     const int64_t chunk = P.scan_chunk0 + (b - P.emit_chunks);
@@ -885,35 +887,25 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         scratch += 1;
     }
     ss_tic(ctx, KC_CODEC);
-    // launches: [scan r0], [emit r0 + scan r1], ..., [emit r_last + scan absolute]:
-    // each residual job's emit re-reads its cur/base (24 B/row) from L2 right
-    // after its scan, and its plan runs at the end of its scan launch
-    int64_t abs_chunks = 0;
+    // two launches: [scan of every residual job] (each job's last block
+    // plans it), then [emit of every residual job + every absolute job]; the
+    // emit re-reads the residual inputs (24 B/row) from L2
+    int64_t abs_chunks = 0, res_chunks = 0;
+    for (int i = 0; i < njobs; ++i) (B.j[i].residual ? res_chunks : abs_chunks) += B.j[i].nchunks;
+    if (res_chunks) {
+        Phase P{0, 0, abs_chunks, res_chunks};
+        k_tick<<<(unsigned)res_chunks, TK_THREADS, 0, ctx->stream>>>(B, P);
+        SS_CHECK_LAUNCH(ctx);
+    }
     for (int i = 0; i < njobs; ++i)
-        if (!B.j[i].residual) abs_chunks += B.j[i].nchunks;
-    int prev = -1;
-    for (int i = 0; i <= njobs; ++i) {
-        if (i < njobs && !B.j[i].residual) continue;
-        Phase P;
-        P.emit_job = prev;
-        P.emit_chunks = prev >= 0 ? B.j[prev].nchunks : 0;
-        if (i < njobs) {
-            P.scan_chunk0 = B.j[i].chunk0;
-            P.scan_chunks = B.j[i].nchunks;
-        } else {
-            P.scan_chunk0 = 0;
-            P.scan_chunks = abs_chunks;
-        }
-        const int64_t blocks = P.emit_chunks + P.scan_chunks;
-        if (blocks) {
-            k_tick<<<(unsigned)blocks, TK_THREADS, 0, ctx->stream>>>(B, P);
-            SS_CHECK_LAUNCH(ctx);
-        }
-        if (i < njobs && B.j[i].nchunks == 0) {  // no scan block: plan it here
+        if (B.j[i].residual && B.j[i].nchunks == 0) {  // no scan block: plan it here
             k_tick_plan<<<1, TK_THREADS, 0, ctx->stream>>>(B, i);
             SS_CHECK_LAUNCH(ctx);
         }
-        if (i < njobs) prev = i;
+    if (res_chunks + abs_chunks) {
+        Phase P{abs_chunks, res_chunks, 0, abs_chunks};
+        k_tick<<<(unsigned)(res_chunks + abs_chunks), TK_THREADS, 0, ctx->stream>>>(B, P);
+        SS_CHECK_LAUNCH(ctx);
     }
     // jobs with zero rows and no chunk still need their header
     for (int i = 0; i < njobs; ++i) {
