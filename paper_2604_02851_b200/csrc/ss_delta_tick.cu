@@ -192,7 +192,7 @@ __device__ __forceinline__ void scan_absolute(const Job& J, const int* s_col, in
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const int64_t row = byte * 8 + t;
-                if (row < r1 && (double)cur[row * J.row_stride + s_col[0]] >= 0.5) v |= (uint8_t)(1u << t);
+                if (row < r1 && (double)__ldcs(&cur[row * J.row_stride + s_col[0]]) >= 0.5) v |= (uint8_t)(1u << t);
             }
             blk[byte] = v;
         }
@@ -200,7 +200,7 @@ __device__ __forceinline__ void scan_absolute(const Job& J, const int* s_col, in
         for (int64_t row = r0 + threadIdx.x; row < r1; row += TK_THREADS) {
             uint64_t w = 0;
 #pragma unroll
-            for (int d = 0; d < 4; ++d) w |= (uint64_t)quant((double)cur[row * J.row_stride + s_col[d]], J.q) << (10 * d);
+            for (int d = 0; d < 4; ++d) w |= (uint64_t)quant((double)__ldcs(&cur[row * J.row_stride + s_col[d]]), J.q) << (10 * d);
 #pragma unroll
             for (int b = 0; b < 5; ++b) blk[row * 5 + b] = (uint8_t)(w >> (8 * b));
         }
@@ -210,7 +210,7 @@ __device__ __forceinline__ void scan_absolute(const Job& J, const int* s_col, in
             T v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (e + u * TK_THREADS < e1) v[u] = cur[e + u * TK_THREADS];
+                if (e + u * TK_THREADS < e1) v[u] = __ldcs(&cur[e + u * TK_THREADS]);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (e + u * TK_THREADS < e1) blk[e + u * TK_THREADS] = (uint8_t)quant((double)v[u], J.q);
@@ -224,9 +224,9 @@ __device__ __forceinline__ void scan_absolute(const Job& J, const int* s_col, in
                 const int64_t rr = row + u * TK_THREADS;
                 if (rr < r1) {
                     const T* src = cur + rr * J.row_stride;
-                    v[u][0] = src[c0];
-                    v[u][1] = src[c1];
-                    v[u][2] = src[c2];
+                    v[u][0] = __ldcs(&src[c0]);
+                    v[u][1] = __ldcs(&src[c1]);
+                    v[u][2] = __ldcs(&src[c2]);
                 }
             }
 #pragma unroll
@@ -540,9 +540,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
 #pragma unroll
             for (int u = 0; u < EMIT_U; ++u) {
                 const int64_t w = v + u * TK_THREADS;
-                if (w < v1) {
-                    cc[u] = c4[w];
-                    bb[u] = b4[w];
+                if (w < v1) {  // last use of cur/base: evict-first
+                    cc[u] = __ldcs(&c4[w]);
+                    bb[u] = __ldcs(&b4[w]);
                 }
             }
 #pragma unroll
@@ -559,7 +559,7 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                     packed |= (uint32_t)code << (8 * kk);
                     nb[kk] = radvance((double)bs[kk], code, rq);
                 }
-                n4[w] = make_float4(nb[0], nb[1], nb[2], nb[3]);
+                __stcs(&n4[w], make_float4(nb[0], nb[1], nb[2], nb[3]));
                 *reinterpret_cast<uint32_t*>(blk + 4 * w) = packed;  // 20 + 4w: 4-byte aligned
             }
         }
@@ -585,9 +585,9 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
 #pragma unroll
             for (int u = 0; u < EMIT_U; ++u) {
                 const int64_t w = v + u * TK_THREADS;
-                if (w < v1) {
-                    cc[u] = c4[w];
-                    bb[u] = b4[w];
+                if (w < v1) {  // last use of cur/base: evict-first
+                    cc[u] = __ldcs(&c4[w]);
+                    bb[u] = __ldcs(&b4[w]);
                 }
             }
 #pragma unroll
@@ -604,7 +604,7 @@ __device__ __forceinline__ void emit_dense(const Job& J, const QParams& rq, int6
                     code[k] = (uint32_t)cq;
                     nb[k] = radvance((double)bs[k], cq, rq);
                 }
-                n4[w] = make_float4(nb[0], nb[1], nb[2], nb[3]);
+                __stcs(&n4[w], make_float4(nb[0], nb[1], nb[2], nb[3]));
                 const int64_t e = 4 * w;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) blk[e + k] = (uint16_t)code[k];
