@@ -22,6 +22,7 @@ constexpr int RS_ITEMS = 8;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_MAX_PASSES = 8;
+constexpr int LB = 8;  // look-back window (tiles per step)
 constexpr uint32_t FLAG_AGG = 1u << 30, FLAG_INC = 2u << 30, CNT_MASK = (1u << 30) - 1;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -149,15 +150,30 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ k
             s_goff[tid] = digit_base[tid];
         } else {
             *slot = FLAG_AGG | mine;
+            // look back LB tiles per step with independent loads (the chain of
+            // dependent L2 round trips shrinks LB-fold); a window is used only
+            // once every tile up to its nearest inclusive prefix has published
             uint64_t excl = 0;
-            for (int64_t t = (int64_t)tile - 1; t >= 0; --t) {
-                const volatile uint32_t* prev = part + t * 256 + tid;
-                uint32_t w;
-                do {
-                    w = *prev;
-                } while ((w & ~CNT_MASK) == 0);
-                excl += w & CNT_MASK;
-                if (w & FLAG_INC) break;
+            for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+                uint32_t w[LB];
+#pragma unroll
+                for (int k = 0; k < LB; ++k)
+                    w[k] = t - k >= 0 ? *(const volatile uint32_t*)(part + (t - k) * 256 + tid) : (FLAG_INC | 0u);
+                int stop = LB;
+                bool ready = true;
+#pragma unroll
+                for (int k = LB - 1; k >= 0; --k) {
+                    if ((w[k] & ~CNT_MASK) == 0) ready = false, stop = k;  // unpublished: must wait for it
+                    else if (w[k] & FLAG_INC) ready = true, stop = k;
+                }
+                if (!ready) continue;
+                uint64_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < LB; ++k)
+                    if (k <= stop) acc += w[k] & CNT_MASK;
+                excl += acc;
+                if (stop < LB) break;
+                t -= LB;
             }
             *slot = FLAG_INC | (uint32_t)(excl + mine);
             s_goff[tid] = digit_base[tid] + excl;
