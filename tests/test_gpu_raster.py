@@ -158,3 +158,26 @@ def test_gpu_depth_order_exact_at_scale_with_near_ties():
     b = orr.tile_bins(o, 640, 360)
     np.testing.assert_array_equal(ranges, b["ranges"])
     np.testing.assert_array_equal(ranks, b["pair_rank"])
+
+
+def test_gpu_long_tile_lists():
+    """Tiles holding thousands of splats: 9000 Gaussians on a 40x24 frame
+    (6 tiles), with planted depth ties; lists, ranges and ranks equal the
+    oracle's exact order."""
+    require_gpu()
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.render import tile_bins
+    model = synth.random_field(9000, 1, 40, 24, seed=21)
+    z = model.means[:, 2]
+    z[100:400] = z[0]
+    intr = synth.intrinsics(40, 24)
+    pose = synth.ring_poses(4)[1]
+    rows, ranges, ranks = tile_bins(model, pose, intr)
+    cam = orr.camera(pose, intr)
+    light = dict(direction=np.array([0.0, -1.0, 0.0]), intensity=np.zeros(3), ambient=None)
+    o = orr.prepare(model, cam, light)
+    b = orr.tile_bins(o, 40, 24)
+    assert (np.diff(b["ranges"], axis=1).max()) > 2048
+    np.testing.assert_array_equal(rows, o["rows"][o["order"]])
+    np.testing.assert_array_equal(ranges, b["ranges"])
+    np.testing.assert_array_equal(ranks, b["pair_rank"])
