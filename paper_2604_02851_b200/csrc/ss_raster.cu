@@ -635,6 +635,107 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict_
     if (lane == 0) tile_loss[tile] = loss;
 }
 
+// ---------------------------------------------------------------- K5, float32 with paired rows
+// The float32 forward walks a lane's 8 pixels as 4 row pairs (q = 2g, 2g + 1).
+// The two pixels of a pair are independent chains of identical arithmetic,
+// so they share one packed FFMA2 / FMUL2 / FADD2 (sm_100 paired fp32): the
+// per-pixel arithmetic issues half the instructions, with per-component
+// results identical to k_blend_fwd<float>.  (The backward keeps scalar rows:
+// its packed form needs ~115 registers and loses more to occupancy than it
+// saves in issue slots, measured.)
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float& comp(float2& v, int h) { return h ? v.y : v.x; }
+
+__global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restrict__ ranges,
+                                                         const uint32_t* __restrict__ pvals,
+                                                         const double2* __restrict__ mu,
+                                                         const SplatRec<float>* __restrict__ rec, int W, int H,
+                                                         int tiles_x, int n_tiles, double bg0, double bg1, double bg2,
+                                                         float* __restrict__ img, float* __restrict__ Tout,
+                                                         uint32_t* __restrict__ tile_stop,
+                                                         unsigned long long* __restrict__ eval_count) {
+    __shared__ Staged<float> sm[WPB][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * WPB + warp;
+    if (tile >= n_tiles) return;
+    const int X0 = (tile % tiles_x) * TILE, Y0 = (tile / tiles_x) * TILE;
+    const int lx = lane & 15, ly0 = lane >> 4;
+    unsigned alive = 0;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q)
+        if (X0 + lx < W && Y0 + ly0 + 2 * q < H) alive |= 1u << q;
+    float2 T[PPT / 2], C0[PPT / 2], C1[PPT / 2], C2[PPT / 2];
+#pragma unroll
+    for (int g = 0; g < PPT / 2; ++g) T[g] = f2(1.f), C0[g] = f2(0.f), C1[g] = f2(0.f), C2[g] = f2(0.f);
+    const uint2 rg = ranges[tile];
+    int last = -1;
+    uint32_t evals = 0;
+    Staged<float>* my = sm[warp];
+    const float2 cap = f2((float)ALPHA_CAP);
+    for (uint32_t b0 = rg.x; b0 < rg.y; b0 += 32) {
+        if (!__any_sync(0xffffffffu, alive)) break;
+        const uint32_t i = b0 + lane;
+        if (i < rg.y) {
+            const uint32_t j = pvals[i];
+            stage(my[lane], mu[j], rec[j], X0, Y0);
+        }
+        __syncwarp();
+        const int nb = (int)min(32u, rg.y - b0);
+        for (int k = 0; k < nb; ++k) {
+            const Staged<float> s = my[k];
+            const unsigned act = lane_mask(s, lx, ly0) & alive;
+            if (!act) continue;
+            last = (int)(b0 - rg.x) + k;
+            evals += __popc(act);
+            PixelGeom<float> pg(s, lx, ly0, X0, Y0);
+            const unsigned wact = __reduce_or_sync(__activemask(), act);
+            const float2 cK = f2(pg.cK), Bx = f2(pg.Bx2), Ax = f2(pg.Ax2), o = f2(s.o);
+#pragma unroll
+            for (int g = 0; g < PPT / 2; ++g) {
+                if (!((wact >> (2 * g)) & 3u)) continue;  // warp-uniform: no lane needs these rows
+                const float2 y = add2(f2(pg.dy0), make_float2((float)(4 * g), (float)(4 * g + 2)));
+                const float2 e = fma2(fma2(cK, y, Bx), y, Ax);
+                float2 G;
+                G.x = (act >> (2 * g)) & 1u ? ss_ex2(e.x) : 0.f;
+                G.y = (act >> (2 * g + 1)) & 1u ? ss_ex2(e.y) : 0.f;
+                float2 alpha = mul2(o, G);
+                alpha.x = fminf(alpha.x, cap.x);
+                alpha.y = fminf(alpha.y, cap.y);
+                const float2 w = mul2(alpha, T[g]);
+                C0[g] = fma2(w, f2(s.c0), C0[g]);
+                C1[g] = fma2(w, f2(s.c1), C1[g]);
+                C2[g] = fma2(w, f2(s.c2), C2[g]);
+                T[g] = add2(T[g], neg2(w));
+                if (T[g].x < (float)T_CUTOFF) alive &= ~(1u << (2 * g));
+                if (T[g].y < (float)T_CUTOFF) alive &= ~(1u << (2 * g + 1));
+            }
+        }
+        __syncwarp();
+    }
+    last = __reduce_max_sync(0xffffffffu, last + 1);
+    if (lane == 0 && tile_stop) tile_stop[tile] = (uint32_t)last;
+    if (eval_count) {
+        evals = __reduce_add_sync(0xffffffffu, evals);
+        if (lane == 0 && evals) atomicAdd(eval_count, (unsigned long long)evals);
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        const int px = X0 + lx, py = Y0 + ly0 + 2 * q;
+        if (px < W && py < H) {
+            const int64_t p = (int64_t)py * W + px;
+            const float t = comp(T[q >> 1], q & 1);
+            img[3 * p + 0] = comp(C0[q >> 1], q & 1) + t * (float)bg0;
+            img[3 * p + 1] = comp(C1[q >> 1], q & 1) + t * (float)bg1;
+            img[3 * p + 2] = comp(C2[q >> 1], q & 1) + t * (float)bg2;
+            if (Tout) Tout[p] = t;
+        }
+    }
+}
+
 __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, double inv_npx, double* __restrict__ out) {
     __shared__ double s[256];
     double t = 0;
@@ -1076,10 +1177,16 @@ template <typename R>
 int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bins& b, R* img, R* T,
             uint32_t* tile_stop) {
     ss_tic(ctx, KC_FORWARD);
-    k_blend_fwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
-        b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
-        o->background[0],
-        o->background[1], o->background[2], img, T, tile_stop, ss_timing_on(ctx) ? ctx->dev_counters : nullptr);
+    if constexpr (sizeof(R) == 4)
+        k_blend_fwd2<<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
+            b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
+            o->background[0], o->background[1], o->background[2], img, T, tile_stop,
+            ss_timing_on(ctx) ? ctx->dev_counters : nullptr);
+    else
+        k_blend_fwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
+            b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
+            o->background[0], o->background[1], o->background[2], img, T, tile_stop,
+            ss_timing_on(ctx) ? ctx->dev_counters : nullptr);
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_FORWARD);
     return SS_OK;
