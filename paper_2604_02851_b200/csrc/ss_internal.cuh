@@ -107,8 +107,6 @@ int ss_scan_u32_to_u64(ss_ctx* ctx, const uint32_t* in, uint64_t* out, int64_t n
 int ss_scan_u8_to_u64(ss_ctx* ctx, const uint8_t* in, uint64_t* out, int64_t n, uint64_t* total);
 // Stable LSD radix sort of (key, value) pairs on bits [0, key_bits).
 // keys/vals are sorted in place; alt buffers are scratch of the same size.
-int ss_radix_sort_u64(ss_ctx* ctx, uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
-                      int64_t n, int key_bits);
 int ss_radix_sort_u32(ss_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
                       int64_t n, int key_bits);
 

@@ -3,7 +3,7 @@
 //
 //   k_hist_all   one read of the keys -> global digit histograms of every pass
 //   k_base_scan  exclusive scan of each pass's 256 counts -> digit base offsets
-//   k_onesweep   per pass: a block takes the next 2048-key tile (atomic tile
+//   k_onesweep   per pass: a block takes the next 2048/4096-key tile (atomic tile
 //                counter, so every earlier tile is already running), ranks its
 //                keys stably with warp __match_any_sync, publishes its
 //                per-digit counts, looks back over earlier tiles' published
@@ -18,8 +18,6 @@
 namespace {
 
 constexpr int RS_THREADS = 256;
-constexpr int RS_ITEMS = 8;
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_MAX_PASSES = 8;
 constexpr int LB = 8;  // look-back window (tiles per step)
@@ -68,12 +66,13 @@ __global__ void k_base_scan(const uint32_t* __restrict__ hist, int passes, uint6
     }
 }
 
-template <typename K>
+template <typename K, int RS_ITEMS>
 __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
                                                          int64_t n, int shift, unsigned mask,
                                                          const uint64_t* __restrict__ digit_base,
                                                          uint32_t* __restrict__ part, unsigned* __restrict__ tile_ctr,
                                                          K* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+    constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
     __shared__ K s_keys[RS_TILE];
     __shared__ uint32_t s_vals[RS_TILE];
     __shared__ uint32_t s_wcnt[RS_WARPS][256];
@@ -214,8 +213,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ k
     }
 }
 
-template <typename K>
+template <typename K, int RS_ITEMS>
 int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, int key_bits) {
+    constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
     if (n <= 1 || key_bits <= 0) return SS_OK;
     if (n > (int64_t)CNT_MASK) return ss_fail(ctx, SS_ERR_CAPACITY, "radix sort limited to 2^30 keys");
     const int passes = (key_bits + 7) / 8;
@@ -243,7 +243,7 @@ int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_
         const int shift = 8 * p;
         const int bits = key_bits - shift < 8 ? key_bits - shift : 8;
         const unsigned mask = (1u << bits) - 1u;
-        k_onesweep<K><<<(unsigned)tiles, RS_THREADS, 0, s>>>(src_k, src_v, n, shift, mask, base + p * 256,
+        k_onesweep<K, RS_ITEMS><<<(unsigned)tiles, RS_THREADS, 0, s>>>(src_k, src_v, n, shift, mask, base + p * 256,
                                                              part + (int64_t)p * tiles * 256, ctr + p, dst_k, dst_v);
         SS_CHECK_LAUNCH(ctx);
         K* tk = src_k; src_k = dst_k; dst_k = tk;
@@ -258,12 +258,11 @@ int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_
 
 }  // namespace
 
-int ss_radix_sort_u64(ss_ctx* ctx, uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
-                      int64_t n, int key_bits) {
-    return sort_impl<uint64_t>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits);
-}
-
 int ss_radix_sort_u32(ss_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
                       int64_t n, int key_bits) {
-    return sort_impl<uint32_t>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits);
+    // tile size: 4096 keys when there are few keys per digit bin to scatter
+    // (the 32-bit depth keys: fewer tiles, shorter look-back chains), 2048
+    // for the short tile-id keys of the (tile, splat) pairs (measured)
+    if (key_bits > 16) return sort_impl<uint32_t, 16>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits);
+    return sort_impl<uint32_t, 8>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits);
 }
