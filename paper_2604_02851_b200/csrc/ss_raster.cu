@@ -750,24 +750,51 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, doubl
 }
 
 // ---------------------------------------------------------------- K7 chain rule
-// (a) fixed-order sum of each splat's per-tile partials, in input order j
-//     (a splat's partials are contiguous from roffj[j]) -> 9 values per row
+// (a) fixed-order sum of each splat's per-tile partials -> 9 values per input
+//     row j.  Partials are stored in depth-rank order (a rank's pairs follow
+//     its predecessor's), so a warp takes 32 consecutive ranks, stages their
+//     contiguous partials through shared memory in chunks of whole pairs
+//     (coalesced loads), and each lane sums its own rank's pairs in pair order.
 template <typename R>
-__global__ void k_sum_partials(const uint64_t* __restrict__ roffj, const uint32_t* __restrict__ rcnt,
-                               const uint32_t* __restrict__ rinv, const R* __restrict__ partials, int64_t n_in,
-                               R* __restrict__ g9) {
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t r = rinv[j];
-        const uint32_t cnt = r == ~0u ? 0u : rcnt[r];
-        double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        if (cnt) {
-            const R* pp = partials + roffj[j] * 9;
-            for (uint32_t i = 0; i < cnt; ++i)
+__global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
+                                                      const uint32_t* __restrict__ dvals, const R* __restrict__ partials,
+                                                      int64_t n_in, R* __restrict__ g9) {
+    constexpr int PW = 4096 / (9 * sizeof(R));  // pairs per staged chunk (4 KB per warp)
+    __shared__ R buf[8][PW * 9];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    R* sb = buf[warp];
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * 32; r0 < n_in; r0 += nwarps * 32) {
+        const int64_t r = r0 + lane;
+        const bool valid = r < n_in;
+        const uint64_t off = valid ? roff[r] : 0, cnt = valid ? rcnt[r] : 0;
+        const uint64_t P0 = __shfl_sync(0xffffffffu, off, 0);
+        uint64_t end = valid ? off + cnt : 0;
 #pragma unroll
-                for (int e = 0; e < 9; ++e) g[e] += (double)pp[i * 9 + e];
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t t = __shfl_xor_sync(0xffffffffu, end, o);
+            end = t > end ? t : end;
         }
+        double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint64_t c0 = P0; c0 < end; c0 += PW) {
+            const uint64_t c1 = min(c0 + PW, end);
+            const int nf = (int)(c1 - c0) * 9;
+            const R* src = partials + c0 * 9;
+            for (int k = lane; k < nf; k += 32) sb[k] = src[k];
+            __syncwarp();
+            const uint64_t a = off > c0 ? off : c0, b = off + cnt < c1 ? off + cnt : c1;
+            for (uint64_t p = a; p < b; ++p) {
+                const R* q = sb + (p - c0) * 9;
 #pragma unroll
-        for (int e = 0; e < 9; ++e) g9[j * 9 + e] = (R)g[e];
+                for (int e = 0; e < 9; ++e) g[e] += (double)q[e];
+            }
+            __syncwarp();
+        }
+        if (valid) {
+            R* o = g9 + (int64_t)dvals[r] * 9;
+#pragma unroll
+            for (int e = 0; e < 9; ++e) o[e] = (R)g[e];
+        }
     }
 }
 
@@ -1234,7 +1261,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         float4* shrec = SS_SCRATCH(ctx, float4, 2 * (int64_t)m->active_count);
         if (!g9 || !shrec) return SS_ERR_CUDA;
         SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)m->active_count, s));
-        k_sum_partials<R><<<gridn(ctx, b.n_in), 256, 0, s>>>(b.roffj, b.rcnt, b.rinv, partials, b.n_in, g9);
+        k_sum_partials<R><<<gridn(ctx, b.n_in), 256, 0, s>>>(b.roff, b.rcnt, b.dvals, partials, b.n_in, g9);
         SS_CHECK_LAUNCH(ctx);
 #define SS_CHAIN(DEG)                                                                                     \
     k_chain<R, DEG><<<gridn(ctx, b.n_in, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
