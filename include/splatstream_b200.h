@@ -77,6 +77,8 @@ typedef struct {
     int32_t extent_cutoff;   /* 1 = 3-sigma windows, 0 = every splat covers the image */
     int32_t precision;       /* 0 = fp32 blend (throughput); 1 = fp64 blend (verbatim parity) */
     int32_t deterministic;   /* backward: 1 = fixed-order per-(tile,splat) partials, 0 = atomics */
+    void* gt_ready;          /* backward: cudaEvent_t the stream waits on right before the first read of
+                                the ground truth (its upload may overlap the forward pass); NULL = none */
 } ss_render_opts;
 
 /* Host-readable summary of the last render/backward call. */

@@ -1247,6 +1247,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (!img || !stop || !tloss || !partials) return SS_ERR_CUDA;
     SS_TRY(forward<R>(ctx, cam, o, b, img, (R*)nullptr, stop));
     const double inv_npx = 1.0 / (double)(3 * npx);
+    if (o->gt_ready) SS_CUDA(ctx, cudaStreamWaitEvent(s, (cudaEvent_t)o->gt_ready, 0));
     ss_tic(ctx, KC_BACKWARD);
     k_blend_bwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, s>>>(
         b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,

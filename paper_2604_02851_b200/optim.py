@@ -142,15 +142,17 @@ def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subs
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
     its loss into `loss_accum` (float64 CUDA scalar)."""
     c = _lib.ctx(model.device.index)
+    ready = None
     if gt is None:
         gt = _gt_tensor(view, model.device)
-    elif isinstance(gt, _Pending):
-        gt = gt.wait()
+    elif isinstance(gt, _Pending):  # the library waits for the upload just before the backward blend
+        ready = gt.ev.cuda_event
+        gt = gt.t
     sub = subset_tensor if subset_tensor is not None else _subset_tensor(index_subset, model.device)
     st = _lib.SSRenderStats()
     c.check(c.lib.ss_backward(c.handle, model.struct(), camera_struct(view.pose, view.intrinsics),
                               light_struct(view.light_state),
-                              render_opts(view.background, sub, extent_cutoff, precision),
+                              render_opts(view.background, sub, extent_cutoff, precision, gt_ready=ready),
                               _lib.ptr(gt), _lib.ptr(grad_accum), _lib.ptr(loss_accum), _lib.ptr(image_out), st))
     return st
 

@@ -177,7 +177,7 @@ def encode_delta_device(attribute_id, current, baseline=None, new_baseline=None,
 
 class DeltaTicker:
     """One server tick's deltas for a DeviceModel in ONE library call
-    (3 kernel launches, no host sync): attributes in emission order (ref
+    (two kernel launches, no host sync): attributes in emission order (ref
     server.py:67-74, 488-493), residual baselines advanced in place, payloads
     into `outs[attr]` (PayloadBuffer).  SH DC / SH rest are read in place from
     the (N, 3, B) coefficients.  The ctypes job array is built once per set of
@@ -232,9 +232,11 @@ class DeltaTicker:
         c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
         return self.model.active_count * len(key)
 
-    def read(self, attributes):
-        """Payload bytes of the last call for `attributes`, read back with two
-        host syncs in total (lengths, then every payload into pinned memory)."""
+    def read(self, attributes, copy: bool = True):
+        """Payloads of the last call for `attributes`, read back with two host
+        syncs in total (lengths, then every payload into pinned memory).
+        copy=False returns memoryviews of that pinned buffer (no host-side
+        copy; valid until the next read)."""
         import torch
         key = [int(x) for x in attributes]
         if not key:
@@ -249,10 +251,10 @@ class DeltaTicker:
             host[off:off + n].copy_(self.outs[a].data[:n], non_blocking=True)
             off += n
         torch.cuda.current_stream(self.model.device).synchronize()
-        raw = host[:total].numpy().tobytes()
+        mv = memoryview(host.numpy())
         out, off = [], 0
         for n in lens:
-            out.append(raw[off:off + n])
+            out.append(mv[off:off + n].tobytes() if copy else mv[off:off + n])
             off += n
         return out
 

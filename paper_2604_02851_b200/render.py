@@ -80,8 +80,9 @@ def _subset_tensor(index_subset, device):
     return torch.from_numpy(idx).to(device)
 
 
-def render_opts(background, subset, extent_cutoff, precision, deterministic=1) -> _lib.SSRenderOpts:
+def render_opts(background, subset, extent_cutoff, precision, deterministic=1, gt_ready=None) -> _lib.SSRenderOpts:
     o = _lib.SSRenderOpts()
+    o.gt_ready = gt_ready
     o.background = _lib.f64arr(background, 3)
     o.subset = subset.data_ptr() if subset is not None else None
     o.subset_count = int(subset.numel()) if subset is not None else 0
