@@ -466,7 +466,8 @@ def encoder_bench(c, _lib, args, torch, reps=20):
            "kernel_ms_per_tick": dev_ms, "payload_bytes_per_tick": payload,
            "set": "means+log_scales (dense residual, baseline advanced) + opacity + DC, raw, one batched call",
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                        "traffic": None, "bytes_per_row": bytes_per_row,
+                        "traffic": committed_traffic("delta_encode"), "traffic_unit": "bytes/tick (ncu, profiles/)",
+                        "algorithmic_bytes_per_tick": bytes_per_row * a, "bytes_per_row": bytes_per_row,
                         "note": "achieved = algorithmic bytes / kernel time of the tick's 3 launches"}}
     del dm
     return out
@@ -478,6 +479,19 @@ def measured_peaks():
         with open(p) as f:
             return json.load(f)
     return {}
+
+
+def committed_traffic(key):
+    """DRAM bytes per launch of a kernel class from this round's committed ncu
+    capture (profiles/r01_traffic.json); None when absent."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(key, {})
+        return e.get("bytes_per_launch", e.get("bytes_per_tick"))
+    except (OSError, ValueError):
+        return None
 
 
 def roofline(dom, per_step, kt, counters, args, local_views, fp32_peak):
@@ -492,7 +506,8 @@ def roofline(dom, per_step, kt, counters, args, local_views, fp32_peak):
     if flops is not None:
         tf = flops / (ms_launch * 1e-3) / 1e12
         return {"bound": "fp32", "kernel": dom, "achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": tf / fp32_peak, "traffic": None, "ms_per_launch": ms_launch,
+                "frac": tf / fp32_peak, "traffic": committed_traffic(dom), "traffic_unit": "bytes/launch (ncu, profiles/)",
+                "ms_per_launch": ms_launch,
                 "work_per_launch": f"{evals:.4g} T-gated (pixel, splat) pairs x {22 if dom == 'blend_forward' else 60} FLOP",
                 "peak_source": "measured FMA probe (ss_measure_fp32_peak)",
                 "hbm_peak_gbs": hbm}

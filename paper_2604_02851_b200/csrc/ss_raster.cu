@@ -807,7 +807,7 @@ template <> __device__ __forceinline__ double t_exp<double>(double x) { return e
 // for the parity path); the normal-proxy axis pick repeats the preprocess's
 // fp64 comparison so both passes agree on it.
 template <typename T, int DEG>
-__global__ void __launch_bounds__(128, 5) k_chain(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset,
+__global__ void __launch_bounds__(128, 4) k_chain(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset,
                         const uint32_t* __restrict__ rinv, const T* __restrict__ g9, int64_t n_in, int cutoff,
                         float* __restrict__ grad, float4* __restrict__ shrec) {
     constexpr int B = ss_sh_bases(DEG);
