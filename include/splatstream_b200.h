@@ -255,6 +255,59 @@ int ss_apply_object_transform(ss_ctx* ctx, ss_model* model, int32_t object_id, c
 int ss_refresh_object_locals(ss_ctx* ctx, const ss_model* model, int32_t object_id, int32_t active_only,
                              double* local_means, double* local_rots, const double q[4], const double t[3]);
 
+/* ---- client ingestion: the decode side of the codec ----
+ * The host parses the header and decompresses (zlib) exactly like the
+ * reference and checks every size it can know from the header; the device
+ * checks what needs the block's bytes and reports it in a status word
+ * (nothing is written to the replica when it is non-zero). */
+enum {
+    SS_INGEST_OK = 0,
+    SS_INGEST_VARINT_TRUNCATED = 1,  /* ValueError("truncated varint"), quantize.py:85-90 */
+    SS_INGEST_VARINT_TOO_LONG = 2,   /* ValueError("varint too long"), quantize.py:94-95 */
+    SS_INGEST_INDEX_RANGE = 3,       /* ProtocolError("sparse delta index out of range"), delta.py:181-182 */
+    SS_INGEST_CODES_TRUNCATED = 4    /* ProtocolError("delta codes truncated"), delta.py:58-60 */
+};
+typedef struct {
+    int32_t code;            /* SS_INGEST_* */
+    int32_t _pad;
+    int64_t offset;          /* end of the varint run inside the block */
+} ss_ingest_status;
+
+/* One decoded delta block: ref protocol/delta.py:150-205 (decode_delta). */
+typedef struct {
+    int32_t attribute_id, mode, dims, bits;  /* mode 0 dense residual, 1 sparse residual, 2 dense absolute */
+    int64_t count;           /* rows covered (the header's count) */
+    int64_t k;               /* sparse: survivors (header) */
+    double lo, hi;           /* residual: the header's f32 range; absolute: the attribute's fixed range */
+    const uint8_t* block;    /* device: decompressed block */
+    int64_t block_len;
+    float* baseline;         /* residual: (count, dims) float32 baseline rows, advanced in place */
+    float* target;           /* element (row, d) at target + row*row_stride + (d/inner)*outer + d%inner + col0 */
+    int64_t row_stride;
+    int32_t inner, outer, col0, _pad;
+    ss_ingest_status* status;  /* device */
+} ss_delta_apply;
+/* Validate the block and decode: sparse survivor indices (k, device) and,
+ * when values_out != NULL, the dequantised float64 values (rows x dims). */
+int ss_decode_delta(ss_ctx* ctx, const ss_delta_apply* d, int64_t* indices_out, double* values_out);
+/* advance_baseline + apply_delta (ref delta.py:259-303) after ss_decode_delta
+ * on the same block: residual attributes advance baseline rows
+ * f32(f64(base) + dequant) and copy baseline[:count] into the target;
+ * absolute attributes store f32(dequant) into the target columns. */
+int ss_apply_delta(ss_ctx* ctx, const ss_delta_apply* d, const int64_t* indices);
+
+/* decode_snapshot: ref protocol/snapshot.py:85-168.  `model` holds
+ * preallocated device arrays for count rows at sh_degree. */
+typedef struct {
+    ss_model model;
+    int32_t profile_id, _pad;
+    double aabb_lo[3], aabb_hi[3];  /* the header's f32 AABB */
+    const uint8_t* block;           /* device: decompressed block */
+    int64_t block_len;
+    ss_ingest_status* status;       /* device */
+} ss_snapshot_decode;
+int ss_decode_snapshot(ss_ctx* ctx, const ss_snapshot_decode* d);
+
 #ifdef __cplusplus
 }
 #endif

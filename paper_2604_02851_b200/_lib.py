@@ -71,6 +71,21 @@ class SSDeltaJob(C.Structure):
                 ("gating_threshold", f64), ("out", vp), ("out_cap", u64), ("out_len", vp)]
 
 
+class SSIngestStatus(C.Structure):
+    _fields_ = [("code", i32), ("_pad", i32), ("offset", i64)]
+
+
+class SSDeltaApply(C.Structure):
+    _fields_ = [("attribute_id", i32), ("mode", i32), ("dims", i32), ("bits", i32), ("count", i64), ("k", i64),
+                ("lo", f64), ("hi", f64), ("block", vp), ("block_len", i64), ("baseline", vp), ("target", vp),
+                ("row_stride", i64), ("inner", i32), ("outer", i32), ("col0", i32), ("_pad", i32), ("status", vp)]
+
+
+class SSSnapshotDecode(C.Structure):
+    _fields_ = [("model", SSModel), ("profile_id", i32), ("_pad", i32), ("aabb_lo", f64 * 3), ("aabb_hi", f64 * 3),
+                ("block", vp), ("block_len", i64), ("status", vp)]
+
+
 class SSOrthoCamera(C.Structure):
     _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("half_width", f64), ("half_height", f64),
                 ("width", i32), ("height", i32)]
@@ -107,6 +122,9 @@ _SIGS = {
     "ss_apply_object_transform": (i32, [vp, C.POINTER(SSModel), i32, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
     "ss_refresh_object_locals": (i32, [vp, C.POINTER(SSModel), i32, i32, vp, vp, C.POINTER(f64),
                                        C.POINTER(f64)]),
+    "ss_decode_delta": (i32, [vp, C.POINTER(SSDeltaApply), vp, vp]),
+    "ss_apply_delta": (i32, [vp, C.POINTER(SSDeltaApply), vp]),
+    "ss_decode_snapshot": (i32, [vp, C.POINTER(SSSnapshotDecode)]),
 }
 
 _lib = None

@@ -10,7 +10,9 @@ variants keep payloads, lengths and baselines in HBM with no host
 synchronisation (the throughput path).
 
 The envelope (`frame_bytes`, CRC32) and the constants follow
-protocol/framing.py and protocol/profiles.py.
+protocol/framing.py and protocol/profiles.py.  The decode side (client
+replica ingestion: decode_delta, apply_delta, decode_snapshot on a device
+replica) lives in protocol/ingest.py.
 """
 
 from __future__ import annotations
@@ -342,5 +344,8 @@ def encode_light_visibility(visibility) -> bytes:
                                              _lib.ptr(out.length)))
     return out.to_bytes()
 
+
+# client-side ingestion on the GPU
+from .ingest import DeltaUpdate, DeviceBaselines, apply_delta, decode_delta, decode_snapshot  # noqa: E402
 
 __all__ = [n for n in dir() if not n.startswith("_")]

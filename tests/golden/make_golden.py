@@ -12,8 +12,12 @@ the build container only -- it does not exist on the GPU box) and writes:
   raster_cases.npz/json prepare_splats / render / backward inputs and outputs
   step_cases.npz/json   optim.step trajectories (model + OptimizerState)
   dyn_cases.npz/json    update_light_visibility / ObjectRegistry transforms
+  ingest_cases.npz/json client ingestion: apply_delta onto a
+                        replica + its baselines, decode_snapshot, and the
+                        reference's exception (type, message) for corrupted
+                        payloads
 
-Usage:  python tests/golden/make_golden.py [--ref /root/reference/pkg]
+Usage:  python tests/golden/make_golden.py [--ref /root/reference/pkg] [--only NAME ...]
 """
 
 from __future__ import annotations
@@ -33,22 +37,24 @@ HERE = pathlib.Path(__file__).resolve().parent
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
+    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest")
     args = ap.parse_args()
     ref = pathlib.Path(args.ref)
     sys.path.insert(0, str(ref / "src"))
     import splatstream  # noqa: F401  (the reference)
 
-    wire = HERE / "wire"
-    if wire.exists():
-        shutil.rmtree(wire)
-    subprocess.run([sys.executable, str(ref / "scripts" / "make_golden_packets.py"), str(wire)], check=True)
-    shipped = (ref / "tests" / "golden" / "manifest.json").read_bytes()
-    assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
-
-    codec_cases()
-    raster_cases()
-    step_cases()
-    dyn_cases()
+    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest"}
+    if "wire" in want:
+        wire = HERE / "wire"
+        if wire.exists():
+            shutil.rmtree(wire)
+        subprocess.run([sys.executable, str(ref / "scripts" / "make_golden_packets.py"), str(wire)], check=True)
+        shipped = (ref / "tests" / "golden" / "manifest.json").read_bytes()
+        assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
+    for name, fn in (("codec", codec_cases), ("raster", raster_cases), ("step", step_cases), ("dyn", dyn_cases),
+                     ("ingest", ingest_cases)):
+        if name in want:
+            fn()
     print("golden vectors written to", HERE)
 
 
@@ -375,6 +381,167 @@ def dyn_cases():
                local_means=reg.local_means, local_rots=reg.local_rotations, q=q, t=t, rows=rows,
                out_means=mm.means, out_quats=mm.quaternions)
     st.save("dyn_cases")
+
+
+# ------------------------------------------------------------------ ingestion (§8f rank 1)
+def ingest_cases():
+    """apply_delta / decode_snapshot on the client side, run by the reference."""
+    import copy
+    from splatstream.protocol import (PROFILE_DEFAULT, PROFILE_LOSSLESS, AttributeId, QuantizationProfile,
+                                      encode_delta, encode_snapshot, decode_snapshot)
+    from splatstream.protocol.delta import DeltaBaselines, apply_delta
+    st = Store()
+    rng = np.random.default_rng(4321)
+    A = AttributeId
+
+    groups = []
+
+    def replica(n, deg, frozen):
+        """A replica + drifted baselines, stored once (group) for its cases."""
+        m = random_model(rng, n, deg, frozen)
+        b = DeltaBaselines()
+        b.reset_from_model(m, 3)
+        # baselines drift from the model the way they do between ticks
+        b.means = (b.means + rng.normal(0, 0.004, b.means.shape)).astype(np.float32)
+        b.log_scales = (b.log_scales + rng.normal(0, 0.004, b.log_scales.shape)).astype(np.float32)
+        g = len(groups)
+        groups.append(g)
+        st.add(dict(kind="replica", name=f"replica_{g}", group=g, active=int(m.active_count), degree=int(deg)),
+               base_means=b.means, base_log_scales=b.log_scales, **model_arrays(m))
+        m._golden_group = g
+        return m, b
+
+    ATTR_FIELD = {0: "means", 1: "log_scales", 2: "quaternions", 3: "logit_opacities", 4: "sh_coeffs",
+                  5: "sh_coeffs", 6: "light_visibility"}
+
+    def outcome(m, b, payload):
+        mm, bb = copy.deepcopy(m), copy.deepcopy(b)
+        try:
+            ok = apply_delta(mm, bb, payload, 3, 3)
+            return dict(ok=bool(ok)), mm, bb
+        except Exception as e:  # noqa: BLE001 -- recorded for the drop-in's error parity
+            return dict(error=type(e).__name__, message=str(e)), None, None
+
+    def add_delta(name, m, b, payload, **extra):
+        res, mm, bb = outcome(m, b, payload)
+        arrays = dict(payload=b2a(payload))
+        field_ = ATTR_FIELD.get(payload[0]) if len(payload) else None
+        if mm is not None and field_ is not None:
+            arrays[f"after_{field_}"] = getattr(mm, field_)
+            arrays.update(after_base_means=bb.means, after_base_log_scales=bb.log_scales)
+        st.add(dict(kind="delta", name=name, group=m._golden_group, field=field_, **res, **extra), **arrays)
+        return res
+
+    for (n, deg, frozen) in ((1, 0, 0), (9, 1, 2), (300, 2, 40), (1500, 3, 0), (2000, 1, 300)):
+        for comp in (0, 1):
+            m, b = replica(n, deg, frozen)
+            a = m.active_count
+            cur = (b.means[:a] + rng.uniform(-0.02, 0.02, (a, 3))).astype(np.float32)
+            add_delta(f"means_dense_{n}_c{comp}", m, b, encode_delta(A.MEANS, cur, b.means[:a], compression_id=comp)[0])
+            cur = b.means[:a].copy()
+            mv = rng.random(a) < 0.1
+            cur[mv] += rng.normal(0, 0.02, (int(mv.sum()), 3)).astype(np.float32)
+            add_delta(f"means_sparse_{n}_c{comp}", m, b, encode_delta(A.MEANS, cur, b.means[:a], compression_id=comp)[0])
+            cur = b.log_scales[:a].copy()
+            cur[rng.random(a) < 0.3] += np.float32(0.05)
+            add_delta(f"ls_sparse_{n}_c{comp}", m, b,
+                      encode_delta(A.LOG_SCALES, cur, b.log_scales[:a], compression_id=comp)[0])
+            add_delta(f"ls_nochange_{n}_c{comp}", m, b,
+                      encode_delta(A.LOG_SCALES, b.log_scales[:a].copy(), b.log_scales[:a], compression_id=comp)[0])
+            add_delta(f"quat_{n}_c{comp}", m, b,
+                      encode_delta(A.QUATERNIONS, rng.normal(0, 0.6, (a, 4)).astype(np.float32), compression_id=comp)[0])
+            add_delta(f"opac_{n}_c{comp}", m, b,
+                      encode_delta(A.LOGIT_OPACITIES, rng.uniform(-10, 10, a).astype(np.float32), compression_id=comp)[0])
+            add_delta(f"dc_{n}_c{comp}", m, b,
+                      encode_delta(A.SH_DC, rng.uniform(-5, 5, (a, 3)).astype(np.float32), compression_id=comp)[0])
+            if deg > 0:
+                B = (deg + 1) ** 2
+                add_delta(f"rest_{n}_c{comp}", m, b, encode_delta(
+                    A.SH_REST, rng.uniform(-1.2, 1.2, (a, 3, B - 1)).astype(np.float32), compression_id=comp)[0])
+            add_delta(f"vis_{n}_c{comp}", m, b,
+                      encode_delta(A.LIGHT_VISIBILITY, rng.random(a).astype(np.float32), compression_id=comp)[0])
+    # survivor gaps needing multi-byte varints, huge residuals
+    m, b = replica(17000, 0, 0)
+    cur = b.means.copy()
+    cur[[0, 5, 200, 16500, 16999]] += np.float32(0.5)  # gaps of 1, 2 and 3 varint bytes
+    add_delta("means_sparse_gaps", m, b, encode_delta(A.MEANS, cur, b.means, compression_id=0)[0])
+    cur = b.means.copy()
+    cur[::2] += np.float32(40.0)
+    add_delta("means_dense_huge", m, b, encode_delta(A.MEANS, cur, b.means, compression_id=0)[0])
+    # corrupted / inconsistent payloads: the reference's exception is the expectation
+    m, b = replica(40, 2, 0)
+    cur = b.means.copy()
+    cur[[3, 17, 30]] += np.float32(0.01)
+    good = encode_delta(A.MEANS, cur, b.means, compression_id=0)[0]   # sparse, 3 survivors
+    dense = encode_delta(A.MEANS, (b.means + 0.01).astype(np.float32), b.means, compression_id=0)[0]
+    opac = encode_delta(A.LOGIT_OPACITIES, rng.uniform(-3, 3, 40).astype(np.float32), compression_id=0)[0]
+    quat = encode_delta(A.QUATERNIONS, rng.normal(0, 0.5, (40, 4)).astype(np.float32), compression_id=0)[0]
+    import struct as _st
+
+    def with_block(p, head_len, block):
+        return p[:head_len] + _st.pack("<I", len(block)) + block
+
+    bad = {
+        "err_short": good[:5],
+        "err_attr": bytes([9]) + good[1:],
+        "err_mode": good[:1] + bytes([7]) + good[2:],
+        "err_rows_huge": good[:4] + _st.pack("<I", (1 << 24) + 1) + good[8:],
+        "err_count_mismatch": good[:4] + _st.pack("<I", 39) + good[8:],
+        "err_k_gt_count": good[:16] + _st.pack("<I", 41) + good[20:],
+        "err_range_nan": good[:8] + _st.pack("<ff", float("nan"), 1.0) + good[16:],
+        "err_varint_truncated": with_block(good, 20, b"\x80\x80"),
+        "err_varint_too_long": with_block(good, 20, b"\xff" * 12 + b"\x01" * 30),
+        "err_index_range": with_block(good, 20, bytes([0, 0, 60]) + bytes(18)),
+        "err_codes_truncated": with_block(good, 20, good[24:24 + 5]),
+        "err_dense_codes_truncated": with_block(dense, 16, dense[20:60]),
+        "err_block_oversize": with_block(opac, 8, opac[12:] + bytes(9)),
+        "err_abs_truncated": with_block(quat, 8, quat[12:40]),
+        "err_zlib_corrupt": good[:2] + bytes([1]) + good[3:20] + _st.pack("<I", 4) + b"\x00\x01\x02\x03",
+        "err_unknown_compression": good[:2] + bytes([5]) + good[3:],
+        "err_residual_absolute_attr": opac[:1] + bytes([0]) + opac[2:],
+        "err_absolute_means": good[:1] + bytes([2]) + good[2:],
+    }
+    for name, p in bad.items():
+        add_delta(name, m, b, p)
+    # stale epoch: untouched, returns False
+    mm, bb = copy.deepcopy(m), copy.deepcopy(b)
+    assert apply_delta(mm, bb, good, 2, 3) is False
+
+    # snapshots
+    for (n, deg, frozen) in ((1, 0, 0), (9, 1, 2), (64, 2, 0), (777, 3, 100), (3000, 1, 0)):
+        m = random_model(rng, n, deg, frozen)
+        m.object_ids = rng.integers(0, 1 << 20, n).astype(np.int32)  # multi-byte varints
+        if n == 64:
+            m.means[:, 1] = np.float32(0.25)  # degenerate AABB axis
+        for prof in (PROFILE_DEFAULT, PROFILE_LOSSLESS, QuantizationProfile(0, 0), QuantizationProfile(1, 0)):
+            payload = encode_snapshot(m, prof)
+            dec, info = decode_snapshot(payload)
+            st.add(dict(kind="snapshot", name=f"snap_{n}_{deg}_p{prof.profile_id}c{prof.compression_id}",
+                        active=int(dec.active_count), degree=int(dec.sh_degree)),
+                   payload=b2a(payload), aabb_lo=info["aabb_lo"], aabb_hi=info["aabb_hi"],
+                   **{f"dec_{k}": v for k, v in model_arrays(dec).items()})
+    m = random_model(rng, 50, 1, 0)
+    p0 = encode_snapshot(m, QuantizationProfile(0, 0))
+    p1 = encode_snapshot(m, QuantizationProfile(1, 0))
+    sbad = {
+        "serr_short": p0[:30],
+        "serr_truncated_block": p0[:-7],
+        "serr_active": p0[:4] + _st.pack("<I", 51) + p0[8:],
+        "serr_degree": p0[:8] + bytes([4]) + p0[9:],
+        "serr_profile": p0[:9] + bytes([3]) + p0[10:],
+        "serr_aabb_inf": p0[:12] + _st.pack("<f", float("inf")) + p0[16:],
+        "serr_section": p0[:36] + _st.pack("<I", 100) + p0[40:140],
+        "serr_ids_truncated": p0[:36] + _st.pack("<I", len(p0) - 40 - 20) + p0[40:-20],
+        "serr_lossless_section": p1[:36] + _st.pack("<I", 400) + p1[40:440],
+    }
+    for name, p in sbad.items():
+        try:
+            decode_snapshot(p)
+            res = dict(ok=True)
+        except Exception as e:  # noqa: BLE001
+            res = dict(error=type(e).__name__, message=str(e))
+        st.add(dict(kind="snapshot_error", name=name, **res), payload=b2a(p))
+    st.save("ingest_cases")
 
 
 if __name__ == "__main__":
