@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict
             const uint64_t t = __shfl_xor_sync(0xffffffffu, end, o);
             end = t > end ? t : end;
         }
-        double g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        R g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // in the blend precision (fixed order: deterministic)
         for (uint64_t c0 = P0; c0 < end; c0 += PW) {
             const uint64_t c1 = min(c0 + PW, end);
             const int nf = (int)(c1 - c0) * 9;
@@ -786,14 +786,14 @@ __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict
             for (uint64_t p = a; p < b; ++p) {
                 const R* q = sb + (p - c0) * 9;
 #pragma unroll
-                for (int e = 0; e < 9; ++e) g[e] += (double)q[e];
+                for (int e = 0; e < 9; ++e) g[e] += q[e];
             }
             __syncwarp();
         }
         if (valid) {
             R* o = g9 + (int64_t)dvals[r] * 9;
 #pragma unroll
-            for (int e = 0; e < 9; ++e) o[e] = (R)g[e];
+            for (int e = 0; e < 9; ++e) o[e] = g[e];
         }
     }
 }
