@@ -65,6 +65,7 @@ struct Job {
     int64_t* cfirst;        // per chunk: first kept row (-1)
     int64_t* clast;         // per chunk: last kept row (-1)
     uint32_t* cvar;         // per chunk: varint bytes of gaps after the chunk's first survivor
+    uint32_t* cmax;         // per chunk: [2c] f32 bits of max|r| over all rows, [2c+1] over kept rows
     uint32_t* cnt_pre;      // per chunk: survivors before the chunk
     uint64_t* var_pre;      // per chunk: varint bytes before the chunk
     int64_t* prev_last;     // per chunk: last kept row before the chunk (-1)
@@ -383,9 +384,8 @@ __device__ __forceinline__ void scan_residual(const Job& J, int64_t c, int64_t r
             J.cfirst[c] = first;
             J.clast[c] = last;
             J.cvar[c] = vs;
-            if (cnt) atomicAdd(&J.g[0], (unsigned long long)cnt);
-            atomicMax(&J.g[1], (unsigned long long)ma);
-            atomicMax(&J.g[2], (unsigned long long)mk);
+            J.cmax[2 * c] = ma;  // reduced by the job's plan (no contended global atomics)
+            J.cmax[2 * c + 1] = mk;
         }
     }
 }
@@ -446,11 +446,34 @@ __device__ __forceinline__ long long plan_scan_max(long long v, long long* tot, 
 }
 
 __device__ void plan_job(const Job& J) {
-    const unsigned long long k = __ldcg(&J.g[0]);
+    // survivors and maxima over the job's chunks (float bits order as integers)
+    __shared__ unsigned long long s_k;
+    __shared__ uint32_t s_ma, s_mk;
+    {
+        uint64_t kk = 0;
+        uint32_t ma = 0, mk = 0;
+        for (int64_t c = threadIdx.x; c < J.nchunks; c += TK_THREADS) {
+            kk += __ldcg(&J.ck[c]);
+            ma = max(ma, __ldcg(&J.cmax[2 * c]));
+            mk = max(mk, __ldcg(&J.cmax[2 * c + 1]));
+        }
+        uint64_t tot;
+        plan_scan_sum(kk, &tot);
+        ma = __reduce_max_sync(0xffffffffu, ma);
+        mk = __reduce_max_sync(0xffffffffu, mk);
+        if (threadIdx.x == 0) s_ma = 0, s_mk = 0, s_k = tot;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(&s_ma, ma);
+            atomicMax(&s_mk, mk);
+        }
+        __syncthreads();
+    }
+    const unsigned long long k = s_k;
     const int sparse = 2 * (int64_t)k < J.rows;  // k < rows * 0.5 (delta.py:101)
     double m;
-    if (sparse) m = k ? (double)__uint_as_float((uint32_t)__ldcg(&J.g[2])) : 0.0;
-    else m = J.rows ? (double)__uint_as_float((uint32_t)__ldcg(&J.g[1])) : 0.0;
+    if (sparse) m = k ? (double)__uint_as_float(s_mk) : 0.0;
+    else m = J.rows ? (double)__uint_as_float(s_ma) : 0.0;
     if (threadIdx.x == 0) {
         *J.mode = sparse;
         *J.m = m;
@@ -874,13 +897,14 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         J.cfirst = SS_SCRATCH(ctx, int64_t, nc);
         J.clast = SS_SCRATCH(ctx, int64_t, nc);
         J.cvar = SS_SCRATCH(ctx, uint32_t, nc);
+        J.cmax = SS_SCRATCH(ctx, uint32_t, 2 * nc);
         J.cnt_pre = SS_SCRATCH(ctx, uint32_t, nc);
         J.var_pre = SS_SCRATCH(ctx, uint64_t, nc);
         J.prev_last = SS_SCRATCH(ctx, int64_t, nc);
         J.m = SS_SCRATCH(ctx, double, 1);
         J.rq = SS_SCRATCH(ctx, QParams, 1);
         J.mode = SS_SCRATCH(ctx, int, 1);
-        if (!J.g || !J.ck || !J.cfirst || !J.clast || !J.cvar || !J.cnt_pre || !J.var_pre || !J.prev_last || !J.m || !J.rq ||
+        if (!J.g || !J.ck || !J.cfirst || !J.clast || !J.cvar || !J.cmax || !J.cnt_pre || !J.var_pre || !J.prev_last || !J.m || !J.rq ||
             !J.mode)
             return SS_ERR_CUDA;
         SS_CUDA(ctx, cudaMemsetAsync(J.g, 0, 4 * sizeof(unsigned long long), ctx->stream));
