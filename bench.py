@@ -469,8 +469,38 @@ def encoder_bench(c, _lib, args, torch, reps=20):
                         "traffic": committed_traffic("delta_encode"), "traffic_unit": "bytes/tick (ncu, profiles/)",
                         "algorithmic_bytes_per_tick": bytes_per_row * a, "bytes_per_row": bytes_per_row,
                         "note": "achieved = algorithmic bytes / kernel time of the tick's 3 launches"}}
+    out["client_apply"] = ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch)
     del dm
     return out
+
+
+def ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch, reps=10):
+    """Client side of the same tick: the payloads applied
+    to a device replica through protocol.apply_delta (host bytes in, parse +
+    H2D + device validate + apply), rows/s over the per-frame set."""
+    from paper_2604_02851_b200.protocol import DeviceBaselines, apply_delta
+    bm.copy_(ref_m)
+    bl.copy_(ref_l)
+    tick(per_frame)
+    payloads = tick.read(per_frame)
+    rep_model = dm.clone()
+    base = DeviceBaselines(ref_m.clone(), ref_l.clone(), 0)
+    for p in payloads:  # warm-up
+        apply_delta(rep_model, base, p, 0, 0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        base.means.copy_(ref_m)
+        base.log_scales.copy_(ref_l)
+        for p in payloads:
+            apply_delta(rep_model, base, p, 0, 0)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / reps
+    same = bool(torch.equal(rep_model.means[:dm.active_count], bm[:dm.active_count]))
+    return {"value": dm.active_count / (ms * 1e-3), "unit": "Gaussians/s", "ms_per_tick": ms,
+            "payload_bytes_per_tick": sum(len(p) for p in payloads),
+            "replica_equals_server_baseline": same,
+            "note": "wall clock per tick of 4 apply_delta calls (host payload bytes -> device replica), incl. baseline re-arm copies"}
 
 
 def measured_peaks():

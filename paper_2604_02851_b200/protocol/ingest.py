@@ -134,6 +134,32 @@ def parse_delta(payload: bytes) -> _Parsed:
     raise ProtocolError(f"unknown delta mode {mode}")
 
 
+_STAGING = {}
+
+
+def _upload(data: bytes, device):
+    """bytes -> device uint8 tensor through a reused pinned staging buffer
+    (one host memcpy + one async H2D copy)."""
+    import torch
+    n = max(len(data), 1)
+    key = device.index
+    st = _STAGING.get(key)
+    if st is None or st[0].numel() < n:
+        if st is not None:
+            st[1].synchronize()
+        st = _STAGING[key] = (torch.empty(max(n, 1 << 20) * 5 // 4, dtype=torch.uint8, pin_memory=True),
+                              torch.cuda.Event())
+    else:
+        st[1].synchronize()  # the previous upload from this buffer has been consumed
+    host, ev = st
+    if data:
+        host.numpy()[:len(data)] = np.frombuffer(data, dtype=np.uint8)
+    out = torch.empty(n, dtype=torch.uint8, device=device)
+    out.copy_(host[:n], non_blocking=True)
+    ev.record(torch.cuda.current_stream(device))
+    return out
+
+
 class _Block:
     """A parsed block on the device plus its status word."""
 
@@ -141,11 +167,7 @@ class _Block:
         import torch
         self.p = p
         self.device = device
-        n = max(len(p.block), 1)
-        host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-        if p.block:
-            host[:len(p.block)] = torch.frombuffer(bytearray(p.block), dtype=torch.uint8)
-        self.data = host.to(device, non_blocking=True)
+        self.data = _upload(p.block, device)
         self.status = torch.zeros(2, dtype=torch.int64, device=device)  # ss_ingest_status (16 B)
         self.indices = torch.empty(max(p.k if p.mode == MODE_SPARSE_RESIDUAL else 0, 1), dtype=torch.int64,
                                    device=device)
@@ -336,10 +358,7 @@ def decode_snapshot(payload: bytes, device=None):
                     torch.empty(n, dtype=torch.float32, device=dev),
                     torch.empty(n, dtype=torch.int32, device=dev), int(active), int(degree))
     if n:
-        host = torch.empty(max(len(data), 1), dtype=torch.uint8, pin_memory=True)
-        if data:
-            host[:len(data)] = torch.frombuffer(bytearray(data), dtype=torch.uint8)
-        blk = host.to(dev, non_blocking=True)
+        blk = _upload(data, dev)
         status = torch.zeros(2, dtype=torch.int64, device=dev)
         d = _lib.SSSnapshotDecode()
         d.model = m.struct()
