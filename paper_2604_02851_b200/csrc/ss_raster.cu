@@ -381,11 +381,13 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
                                                         int tiles_x, int n_tiles, double bg0, double bg1, double bg2,
                                                         R* __restrict__ img, R* __restrict__ Tout,
                                                         uint32_t* __restrict__ tile_stop,
-                                                        unsigned long long* __restrict__ eval_count) {
+                                                        unsigned long long* __restrict__ eval_count,
+                                                        const uint32_t* __restrict__ order) {
     __shared__ Staged<R> sm[WPB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x * WPB + warp;
-    if (tile >= n_tiles) return;
+    const int slot = blockIdx.x * WPB + warp;
+    if (slot >= n_tiles) return;
+    const int tile = order ? (int)order[slot] : slot;
     const int X0 = (tile % tiles_x) * TILE, Y0 = (tile / tiles_x) * TILE;
     const int lx = lane & 15, ly0 = lane >> 4;
     unsigned alive = 0;
@@ -510,11 +512,13 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict_
                                                         const uint32_t* __restrict__ tile_stop, int W, int H,
                                                         int tiles_x, int n_tiles, const R* __restrict__ img,
                                                         const float* __restrict__ gt, double npx3,
-                                                        R* __restrict__ partials, double* __restrict__ tile_loss) {
+                                                        R* __restrict__ partials, double* __restrict__ tile_loss,
+                                                        const uint32_t* __restrict__ order) {
     __shared__ Staged<R> sm[WPB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x * WPB + warp;
-    if (tile >= n_tiles) return;
+    const int slot = blockIdx.x * WPB + warp;
+    if (slot >= n_tiles) return;
+    const int tile = order ? (int)order[slot] : slot;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int X0 = tx * TILE, Y0 = ty * TILE;
     const int lx = lane & 15, ly0 = lane >> 4;
@@ -657,11 +661,13 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
                                                          int tiles_x, int n_tiles, double bg0, double bg1, double bg2,
                                                          float* __restrict__ img, float* __restrict__ Tout,
                                                          uint32_t* __restrict__ tile_stop,
-                                                         unsigned long long* __restrict__ eval_count) {
+                                                         unsigned long long* __restrict__ eval_count,
+                                                         const uint32_t* __restrict__ order) {
     __shared__ Staged<float> sm[WPB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x * WPB + warp;
-    if (tile >= n_tiles) return;
+    const int slot = blockIdx.x * WPB + warp;
+    if (slot >= n_tiles) return;
+    const int tile = order ? (int)order[slot] : slot;
     const int X0 = (tile % tiles_x) * TILE, Y0 = (tile / tiles_x) * TILE;
     const int lx = lane & 15, ly0 = lane >> 4;
     unsigned alive = 0;
@@ -1090,6 +1096,60 @@ __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __res
     }
 }
 
+// ---------------------------------------------------------------- tile order
+// Tiles are walked longest-first (work = list length, or the forward's stop
+// index for the backward): the blocks holding the longest walks start in the
+// first wave instead of forming the tail, and tiles of similar length share a
+// block (a block retires with its slowest tile).  Counting sort on the work,
+// one block; ties in any order (every tile's results are independent of the
+// schedule).
+constexpr int ORDER_BUCKETS = 4096;
+
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges,
+                                                     const uint32_t* __restrict__ stop, int n_tiles,
+                                                     uint32_t* __restrict__ order) {
+    __shared__ uint32_t h[ORDER_BUCKETS];
+    __shared__ uint32_t ws[32];
+    for (int i = threadIdx.x; i < ORDER_BUCKETS; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    auto bucket = [&](int t) {
+        const uint2 r = ranges[t];
+        uint32_t w = r.y - r.x;
+        if (stop) w = min(w, stop[t]);
+        return ORDER_BUCKETS - 1 - (int)min(w, (uint32_t)(ORDER_BUCKETS - 1));  // descending work
+    };
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&h[bucket(t)], 1u);
+    __syncthreads();
+    // exclusive scan of the 4096 buckets: 4 per thread
+    constexpr int PER = ORDER_BUCKETS / 1024;
+    uint32_t v[PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        v[k] = h[threadIdx.x * PER + k];
+        sum += v[k];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int w = 0; w < warp; ++w) pre += ws[w];
+    uint32_t run = pre + incl - sum;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        h[threadIdx.x * PER + k] = run;
+        run += v[k];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&h[bucket(t)], 1u)] = (uint32_t)t;
+}
+
 // ---------------------------------------------------------------- host
 inline int gridn(ss_ctx* ctx, int64_t n, int block = 256) {
     int64_t g = (n + block - 1) / block;
@@ -1204,16 +1264,20 @@ template <typename R>
 int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bins& b, R* img, R* T,
             uint32_t* tile_stop) {
     ss_tic(ctx, KC_FORWARD);
+    uint32_t* order = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
+    if (!order) return SS_ERR_CUDA;
+    k_tile_order<<<1, 1024, 0, ctx->stream>>>(b.ranges, nullptr, b.n_tiles, order);
+    SS_CHECK_LAUNCH(ctx);
     if constexpr (sizeof(R) == 4)
         k_blend_fwd2<<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
             b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
             o->background[0], o->background[1], o->background[2], img, T, tile_stop,
-            ss_timing_on(ctx) ? ctx->dev_counters : nullptr);
+            ss_timing_on(ctx) ? ctx->dev_counters : nullptr, order);
     else
         k_blend_fwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
             b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
             o->background[0], o->background[1], o->background[2], img, T, tile_stop,
-            ss_timing_on(ctx) ? ctx->dev_counters : nullptr);
+            ss_timing_on(ctx) ? ctx->dev_counters : nullptr, order);
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_FORWARD);
     return SS_OK;
@@ -1249,9 +1313,13 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     const double inv_npx = 1.0 / (double)(3 * npx);
     if (o->gt_ready) SS_CUDA(ctx, cudaStreamWaitEvent(s, (cudaEvent_t)o->gt_ready, 0));
     ss_tic(ctx, KC_BACKWARD);
+    uint32_t* order = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
+    if (!order) return SS_ERR_CUDA;
+    k_tile_order<<<1, 1024, 0, s>>>(b.ranges, stop, b.n_tiles, order);
+    SS_CHECK_LAUNCH(ctx);
     k_blend_bwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, s>>>(
         b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
-        b.n_tiles, img, gt, (double)(3 * npx), partials, tloss);
+        b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order);
     SS_CHECK_LAUNCH(ctx);
     k_loss_reduce<<<1, 256, 0, s>>>(tloss, b.n_tiles, inv_npx, loss);
     SS_CHECK_LAUNCH(ctx);
