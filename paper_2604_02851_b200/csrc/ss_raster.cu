@@ -257,7 +257,8 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, int64_t n, uint2* __
 // them in depth order; no block-level barriers anywhere (blocks are just
 // WPB independent tiles).  Per-pixel liveness is an 8-bit mask; a pixel dies
 // when T drops below 1e-4 (the reference's T-gate: later splats skip it).
-constexpr int WPB = 4;   // tiles (warps) per block
+constexpr int WPB = 4;   // tiles (warps) per block of the forward kernels
+constexpr int WPB_BWD = 2;  // ... of the backward (fewer tiles per block: less waiting on a block's slowest tile)
 constexpr int PPT = 8;   // pixels per lane
 // pixel rows per warp-uniform skip test: rows of one group form one basic
 // block, so their independent chains interleave (helps the longer backward
@@ -504,7 +505,7 @@ __device__ __forceinline__ uint32_t pair_index(const uint64_t* roff, const int w
 }
 
 template <typename R>
-__global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restrict__ ranges,
                                                         const uint32_t* __restrict__ pvals,
                                                         const double2* __restrict__ mu,
                                                         const SplatRec<R>* __restrict__ rec_,
@@ -514,9 +515,9 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_bwd(const uint2* __restrict_
                                                         const float* __restrict__ gt, double npx3,
                                                         R* __restrict__ partials, double* __restrict__ tile_loss,
                                                         const uint32_t* __restrict__ order) {
-    __shared__ Staged<R> sm[WPB][32];
+    __shared__ Staged<R> sm[WPB_BWD][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slot = blockIdx.x * WPB + warp;
+    const int slot = blockIdx.x * WPB_BWD + warp;
     if (slot >= n_tiles) return;
     const int tile = order ? (int)order[slot] : slot;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -1317,7 +1318,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (!order) return SS_ERR_CUDA;
     k_tile_order<<<1, 1024, 0, s>>>(b.ranges, stop, b.n_tiles, order);
     SS_CHECK_LAUNCH(ctx);
-    k_blend_bwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, s>>>(
+    k_blend_bwd<R><<<(b.n_tiles + WPB_BWD - 1) / WPB_BWD, 32 * WPB_BWD, 0, s>>>(
         b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
         b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order);
     SS_CHECK_LAUNCH(ctx);
