@@ -281,6 +281,14 @@ __device__ __forceinline__ float ss_ex2(float x) {
     return r;
 }
 template <> __device__ __forceinline__ double ss_rcp<double>(double x) { return 1.0 / x; }
+// alive &= ~bit when T < 1e-4 (the T-gate), as one predicated AND
+__device__ __forceinline__ void gate_t(unsigned& alive, float t, unsigned bit) {
+    asm("{\n .reg .pred p;\n setp.lt.f32 p, %1, 0f38D1B717;\n @p and.b32 %0, %0, %2;\n}\n"
+        : "+r"(alive) : "f"(t), "r"(~bit));
+}
+__device__ __forceinline__ void gate_t(unsigned& alive, double t, unsigned bit) {
+    if (t < T_CUTOFF) alive &= ~bit;
+}
 
 // Staged splat.  fp32: centre relative to the tile origin (rounded from the
 // fp64 centre) so dx keeps full precision; fp64: absolute centre and
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
                     C1[q] += w * s.c1;
                     C2[q] += w * s.c2;
                     T[q] -= w;  // T (1 - alpha)
-                    if (T[q] < (R)T_CUTOFF) alive &= ~(1u << q);
+                    gate_t(alive, T[q], 1u << q);
                 }
             }
         }
@@ -717,8 +725,8 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
                 C1[g] = fma2(w, f2(s.c1), C1[g]);
                 C2[g] = fma2(w, f2(s.c2), C2[g]);
                 T[g] = add2(T[g], neg2(w));
-                if (T[g].x < (float)T_CUTOFF) alive &= ~(1u << (2 * g));
-                if (T[g].y < (float)T_CUTOFF) alive &= ~(1u << (2 * g + 1));
+                gate_t(alive, T[g].x, 1u << (2 * g));
+                gate_t(alive, T[g].y, 1u << (2 * g + 1));
             }
         }
         __syncwarp();
