@@ -224,11 +224,20 @@ class DeltaTicker:
             j.out, j.out_cap, j.out_len = buf.data.data_ptr(), buf.data.numel(), buf.length.data_ptr()
         return jobs
 
+    def _key(self, attributes):
+        m = self.model
+        ptrs = tuple(t.data_ptr() for t in (m.means, m.log_scales, m.quaternions, m.logit_opacities, m.sh_coeffs,
+                                            m.light_visibility))
+        bptrs = tuple(int(b.data_ptr()) for b in self.baselines.values())
+        return tuple(int(x) for x in attributes), m.active_count, ptrs, bptrs
+
     def __call__(self, attributes):
-        key = tuple(int(x) for x in attributes)
-        jobs = self._jobs.get(key)
+        # the job array is rebuilt when the active prefix or a buffer changes
+        full = self._key(attributes)
+        key = full[0]
+        jobs = self._jobs.get(full)
         if jobs is None:
-            jobs = self._jobs[key] = self._build(key)
+            jobs = self._jobs[full] = self._build(key)
         c = self._ctx
         c.bind_stream()
         c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
@@ -259,6 +268,60 @@ class DeltaTicker:
             out.append(mv[off:off + n].tobytes() if copy else mv[off:off + n])
             off += n
         return out
+
+
+# ref server.py:57-74: per-attribute periods (ticks) and the fixed emission order
+DEFAULT_DELTA_PERIODS = {AttributeId.LOGIT_OPACITIES: 1, AttributeId.SH_DC: 1, AttributeId.MEANS: 1,
+                         AttributeId.LOG_SCALES: 1, AttributeId.QUATERNIONS: 10, AttributeId.SH_REST: 30}
+DELTA_ORDER = (AttributeId.MEANS, AttributeId.LOG_SCALES, AttributeId.QUATERNIONS, AttributeId.LOGIT_OPACITIES,
+               AttributeId.SH_DC, AttributeId.SH_REST)
+
+
+def due_attributes(tick_index: int, periods=None, appended: bool = False, sh_degree: int = 3):
+    """Attributes StreamServer emits at `tick_index`, in emission order (ref
+    server.py:89-91 DeltaSchedule.due, 488-493; SH rest is skipped at degree
+    0, server.py:352-354)."""
+    periods = DEFAULT_DELTA_PERIODS if periods is None else periods
+    out = []
+    for attr in DELTA_ORDER:
+        p = periods.get(attr)
+        if appended or (p is not None and tick_index % p == 0):
+            if attr == AttributeId.SH_REST and sh_degree == 0:
+                continue
+            out.append(attr)
+    return out
+
+
+class DeltaEmitter:
+    """StreamServer's per-tick delta emission (ref server.py:336-358 +
+    488-493) on a DeviceModel: the due attributes encoded in one batched
+    library call, residual baselines (rows [:a] of the server's
+    DeviceBaselines) advanced in HBM, payloads read back and passed through
+    the compression stage -- byte-identical to the reference server's
+    TENSOR_DELTA payloads."""
+
+    def __init__(self, model, baselines, compression_id: int = COMPRESSION_ZLIB, periods=None):
+        self.model, self.baselines, self.compression_id, self.periods = model, baselines, compression_id, periods
+        self._outs = {int(a): PayloadBuffer(1 << 16, model.device) for a in AttributeId}
+        self._ticker = None
+        self._state = None
+
+    def tick(self, tick_index: int, appended: bool = False):
+        """[(attribute_id, payload bytes)] for the attributes due at this tick."""
+        m = self.model
+        a = m.active_count
+        if a == 0:  # server.py:491: no deltas without active rows
+            return []
+        due = [int(x) for x in due_attributes(tick_index, self.periods, appended, m.sh_degree)]
+        if not due:
+            return []
+        state = (a, self.baselines.means.data_ptr(), self.baselines.log_scales.data_ptr())
+        if self._ticker is None or self._state != state:  # new active prefix or baselines (snapshot reset)
+            self._ticker = DeltaTicker(m, {0: self.baselines.means[:a], 1: self.baselines.log_scales[:a]}, self._outs)
+            self._state = state
+        self._ticker(due)
+        raw = self._ticker.read(due)
+        return [(attr, _recompress_delta(p, self.compression_id)) for attr, p in zip(due, raw)]
 
 
 def delta_tick_device(model, attributes, baselines, outs, gating=None):

@@ -176,3 +176,49 @@ def test_gpu_delta_gate_boundary_exact():
                 r, rb = oc.delta_payload(attr, cur, base, gate, 0)
                 assert g == r, (gate, frac, attr)
                 np.testing.assert_array_equal(gb, rb)
+
+
+def test_gpu_delta_emitter_server_ticks_match_oracle():
+    """DeltaEmitter over 31 server ticks (zlib payloads) of a model that moves
+    like an optimised one, vs the oracle's encode_delta + baseline advance
+    for the same schedule; a replica fed the payloads tracks the baselines."""
+    require_gpu()
+    import torch
+    from oracle import codec as oc
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.protocol import DeltaEmitter, DeviceBaselines, apply_delta, due_attributes
+    rng = np.random.default_rng(12)
+    host = synth.random_field(20_000, 2, 320, 180, seed=4)
+    host.active_count = 19_000
+    a = host.active_count
+    dm = DeviceModel.from_host(host, 0)
+    base = DeviceBaselines()
+    base.reset_from_model(dm, 1)
+    em = DeltaEmitter(dm, base)
+    replica = dm.clone()
+    rbase = DeviceBaselines()
+    rbase.reset_from_model(replica, 1)
+    hb_m, hb_l = host.means.copy(), host.log_scales.copy()
+    for tick in range(31):
+        with torch.no_grad():
+            for t, s in ((dm.means, 2e-3), (dm.log_scales, 3e-3), (dm.quaternions, 1e-2), (dm.sh_coeffs, 1e-2)):
+                mv = torch.from_numpy(rng.random(t.shape[0]) < 0.4).cuda()
+                t[:a][mv[:a]] += torch.randn_like(t[:a][mv[:a]]) * s
+        out = em.tick(tick)
+        assert [p[0] for p in out] == [int(x) for x in due_attributes(tick, sh_degree=2)]
+        h = dm.to_host()
+        for attr, payload in out:
+            if attr == 0:
+                ref, hb_m[:a] = oc.delta_payload(0, h.means[:a], hb_m[:a], None, 1)
+            elif attr == 1:
+                ref, hb_l[:a] = oc.delta_payload(1, h.log_scales[:a], hb_l[:a], None, 1)
+            else:
+                x = {2: h.quaternions, 3: h.logit_opacities, 4: h.sh_coeffs[:, :, 0], 5: h.sh_coeffs[:, :, 1:]}[attr]
+                ref = oc.delta_payload(attr, x[:a], None, None, 1)[0]
+            assert payload == ref, (tick, attr)
+            assert apply_delta(replica, rbase, payload, 1, 1)
+        np.testing.assert_array_equal(base.means.cpu().numpy(), hb_m)
+        np.testing.assert_array_equal(base.log_scales.cpu().numpy(), hb_l)
+        np.testing.assert_array_equal(rbase.means.cpu().numpy(), hb_m)
+        np.testing.assert_array_equal(replica.means[:a].cpu().numpy(), hb_m[:a])

@@ -205,3 +205,14 @@ def test_gpu_decode_snapshot_errors_match_reference(c):
     with pytest.raises(Exception) as ei:
         decode_snapshot(c.a("payload").tobytes())
     assert (_exc_name(ei.value), str(ei.value)) == (c["error"], c["message"])
+
+
+def test_due_attributes_follow_server_schedule():
+    """ref server.py:57-74, 89-91, 488-493, 352-354."""
+    from paper_2604_02851_b200.protocol import due_attributes
+    assert [int(a) for a in due_attributes(0)] == [0, 1, 2, 3, 4, 5]
+    assert [int(a) for a in due_attributes(1)] == [0, 1, 3, 4]
+    assert [int(a) for a in due_attributes(10)] == [0, 1, 2, 3, 4]
+    assert [int(a) for a in due_attributes(30)] == [0, 1, 2, 3, 4, 5]
+    assert [int(a) for a in due_attributes(7, appended=True)] == [0, 1, 2, 3, 4, 5]
+    assert [int(a) for a in due_attributes(0, sh_degree=0)] == [0, 1, 2, 3, 4]
