@@ -357,6 +357,11 @@ def run_ours(args):
     if rank == 0:
         enc = encoder_bench(c, _lib, args, torch)
 
+    # ---- pool maintenance of this model, rank 0
+    pool_rec = None
+    if rank == 0:
+        pool_rec = pool_bench(dm, state, poses, intr, torch)
+
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -407,7 +412,7 @@ def run_ours(args):
            "gpu_launches": launches, "clocks": clock_rec,
            "kernel_ms_per_step": {k: round(v, 4) for k, v in per_step.items()},
            "evaluated_pairs_per_view": evals_per_view,
-           "delta_encode": enc, "fp32_peak_tflops_measured": fp32_peak,
+           "delta_encode": enc, "pool_maintenance": pool_rec, "fp32_peak_tflops_measured": fp32_peak,
            "precision": "fp64 preprocess/windows/depth keys, fp32 blend + chain rule, fp64 Adam moments"}
     print(json.dumps(out), flush=True)
     if pg is not None:
@@ -445,9 +450,15 @@ def encoder_bench(c, _lib, args, torch, reps=20):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     _lib.set_timing(c, True)
     _lib.get_timing(c, reset=True)
+    # between ticks: re-arm the baselines, then stream a 256 MB buffer through
+    # L2 so the re-arm's dirty lines are written back outside the timed
+    # region (in the server loop the optimizer step sits between two ticks)
+    # and every tick starts with the inputs in DRAM
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dm.device)
     for e0, e1 in ev:
         bm.copy_(ref_m)
         bl.copy_(ref_l)
+        flush.add_(1.0)
         e0.record()
         tick(per_frame)
         e1.record()
@@ -465,6 +476,7 @@ def encoder_bench(c, _lib, args, torch, reps=20):
     out = {"value": a / (ms * 1e-3), "unit": "Gaussians/s", "rows": a, "sh_degree": 1, "ms_per_tick": ms,
            "kernel_ms_per_tick": dev_ms, "payload_bytes_per_tick": payload,
            "set": "means+log_scales (dense residual, baseline advanced) + opacity + DC, raw, one batched call",
+           "l2": "flushed between ticks (256 MB read-modify-write after the baseline re-arm)",
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "traffic": committed_traffic("delta_encode"), "traffic_unit": "bytes/tick (ncu, profiles/)",
                         "algorithmic_bytes_per_tick": bytes_per_row * a, "bytes_per_row": bytes_per_row,
@@ -501,6 +513,32 @@ def ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch, reps=10):
             "payload_bytes_per_tick": sum(len(p) for p in payloads),
             "replica_equals_server_baseline": same,
             "note": "wall clock per tick of 4 apply_delta calls (host payload bytes -> device replica), incl. baseline re-arm copies"}
+
+
+def pool_bench(dm, state, poses, intr, torch, reps=5):
+    """Per-tick pool maintenance on the 1M-row model:
+    GridIndex.rebuild, precull against the step's 8 cameras and
+    freeze_policy, each as the reference API call (host result)."""
+    from paper_2604_02851_b200 import pool
+    from paper_2604_02851_b200.geometry import CameraIntrinsics
+    g = pool.GridIndex(cell_size=0.5, origin=(0.0, 0.0, 0.0))
+    ci = CameraIntrinsics(width=intr.width, height=intr.height, fov_y=intr.fov_y, near=intr.near, far=100.0)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            out = fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3 / reps, out
+
+    t_grid, _ = timed(lambda: g.rebuild(dm))
+    t_pre, kept = timed(lambda: pool.precull(dm, g, poses, ci))
+    t_frz, frz = timed(lambda: pool.freeze_policy(dm, state, 100, 1e-4))
+    return {"rows": dm.count, "cells": int(g.cell_lens.shape[0]), "grid_rebuild_ms": t_grid, "precull_ms": t_pre,
+            "precull_rows": int(kept.size), "freeze_policy_ms": t_frz,
+            "note": "wall clock per call incl. the host readback of the result (reference: ~1.08 s per 1M-row rebuild on CPU, SURVEY §8f)"}
 
 
 def measured_peaks():

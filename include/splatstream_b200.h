@@ -308,6 +308,47 @@ typedef struct {
 } ss_snapshot_decode;
 int ss_decode_snapshot(ss_ctx* ctx, const ss_snapshot_decode* d);
 
+/* ---- pool maintenance ---- */
+enum { SS_SELECT_FREEZE = 0, SS_SELECT_PRUNE = 1, SS_SELECT_PRECULL = 2 };
+typedef struct {
+    double position[3];
+    double rot_cw[9];        /* camera->world rotation, row major (world_to_camera = (p - position) @ rot_cw) */
+    double fx, fy, cx, cy, near_plane, far_plane;
+    double tx, ty, nx, ny;   /* (W/2)/fx, (H/2)/fy, 1/sqrt(1+tx^2), 1/sqrt(1+ty^2)  (expansion.py:156-159) */
+    int32_t width, height;
+    const double* depth;     /* device (height, width) engine depth, or NULL */
+} ss_pool_camera;
+typedef struct {
+    int32_t kind, n_cameras;
+    int64_t n;                                      /* rows tested */
+    const int64_t* age; const double* grad_ema;     /* freeze_policy: ref expansion.py:134-142 */
+    int64_t age_threshold; double grad_threshold;
+    const float* logits; double opacity_floor;      /* prune: ref expansion.py:184-197 */
+    const int64_t* cells;                           /* precull: (n, 3) cell per row from the last rebuild */
+    double origin[3], cell_size, margin;            /* ... cell geometry, margin = cell diagonal / 2 */
+    const ss_pool_camera* cameras;                  /* ... host array of n_cameras (expansion.py:145-181) */
+    const int64_t* row_ids;                         /* optional: report row_ids[i] instead of i */
+} ss_select;
+/* Rows passing the predicate, ascending, into `out` (device, n entries); the
+ * count is returned on the host (the call synchronises). */
+int ss_select_rows(ss_ctx* ctx, const ss_select* s, int64_t* out, int64_t* count_out);
+/* dst row i = src row map[i] for every column (map[i] < 0: row (-1 - map[i]) of `fill`):
+ * permute / remove_rows / client-side placeholder appends (ref model.py:134-165, 291-305). */
+int ss_gather_rows(ss_ctx* ctx, const ss_model* src, ss_model* dst, const int64_t* map, int64_t n_out,
+                   const ss_model* fill);
+typedef struct {
+    double origin[3];
+    double cell_size;
+} ss_grid_spec;
+/* GridIndex.rebuild (ref model.py:418-426): per-row cells (n,3), and the cells in
+ * first-appearance order with their member rows (ascending): cell_keys (C,3),
+ * cell_lens (C,), cell_rows (n,) concatenated; the cell count C on the host. */
+int ss_grid_rebuild(ss_ctx* ctx, const float* means, int64_t n, const ss_grid_spec* g, int64_t* cells,
+                    int64_t* cell_keys, int64_t* cell_lens, int64_t* cell_rows, int64_t* n_cells);
+/* Zigzag LEB128 of (perm[i] - i): the permutation block of an ordering
+ * packet before its zlib stage (ref protocol/packets.py:153-158). */
+int ss_zigzag_varints(ss_ctx* ctx, const int64_t* perm, int64_t n, uint8_t* out, uint64_t out_cap, uint64_t* len_out);
+
 #ifdef __cplusplus
 }
 #endif

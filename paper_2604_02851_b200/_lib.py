@@ -86,6 +86,23 @@ class SSSnapshotDecode(C.Structure):
                 ("block", vp), ("block_len", i64), ("status", vp)]
 
 
+class SSPoolCamera(C.Structure):
+    _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64),
+                ("near_plane", f64), ("far_plane", f64), ("tx", f64), ("ty", f64), ("nx", f64), ("ny", f64),
+                ("width", i32), ("height", i32), ("depth", vp)]
+
+
+class SSSelect(C.Structure):
+    _fields_ = [("kind", i32), ("n_cameras", i32), ("n", i64), ("age", vp), ("grad_ema", vp),
+                ("age_threshold", i64), ("grad_threshold", f64), ("logits", vp), ("opacity_floor", f64),
+                ("cells", vp), ("origin", f64 * 3), ("cell_size", f64), ("margin", f64),
+                ("cameras", C.POINTER(SSPoolCamera)), ("row_ids", vp)]
+
+
+class SSGridSpec(C.Structure):
+    _fields_ = [("origin", f64 * 3), ("cell_size", f64)]
+
+
 class SSOrthoCamera(C.Structure):
     _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("half_width", f64), ("half_height", f64),
                 ("width", i32), ("height", i32)]
@@ -125,6 +142,10 @@ _SIGS = {
     "ss_decode_delta": (i32, [vp, C.POINTER(SSDeltaApply), vp, vp]),
     "ss_apply_delta": (i32, [vp, C.POINTER(SSDeltaApply), vp]),
     "ss_decode_snapshot": (i32, [vp, C.POINTER(SSSnapshotDecode)]),
+    "ss_select_rows": (i32, [vp, C.POINTER(SSSelect), vp, C.POINTER(i64)]),
+    "ss_gather_rows": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSModel), vp, i64, C.POINTER(SSModel)]),
+    "ss_grid_rebuild": (i32, [vp, vp, i64, C.POINTER(SSGridSpec), vp, vp, vp, vp, C.POINTER(i64)]),
+    "ss_zigzag_varints": (i32, [vp, vp, i64, vp, u64, C.POINTER(u64)]),
 }
 
 _lib = None

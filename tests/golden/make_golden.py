@@ -12,6 +12,10 @@ the build container only -- it does not exist on the GPU box) and writes:
   raster_cases.npz/json prepare_splats / render / backward inputs and outputs
   step_cases.npz/json   optim.step trajectories (model + OptimizerState)
   dyn_cases.npz/json    update_light_visibility / ObjectRegistry transforms
+  pool_cases.npz/json   pool maintenance: GridIndex.rebuild,
+                        precull, freeze_policy/freeze_range, prune,
+                        OptimizerState.resize, encode_ordering, apply_mutation,
+                        DeltaBaselines.apply_record
   ingest_cases.npz/json client ingestion: apply_delta onto a
                         replica + its baselines, decode_snapshot, and the
                         reference's exception (type, message) for corrupted
@@ -37,13 +41,13 @@ HERE = pathlib.Path(__file__).resolve().parent
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
-    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest")
+    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool")
     args = ap.parse_args()
     ref = pathlib.Path(args.ref)
     sys.path.insert(0, str(ref / "src"))
     import splatstream  # noqa: F401  (the reference)
 
-    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest"}
+    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool"}
     if "wire" in want:
         wire = HERE / "wire"
         if wire.exists():
@@ -52,7 +56,7 @@ def main():
         shipped = (ref / "tests" / "golden" / "manifest.json").read_bytes()
         assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
     for name, fn in (("codec", codec_cases), ("raster", raster_cases), ("step", step_cases), ("dyn", dyn_cases),
-                     ("ingest", ingest_cases)):
+                     ("ingest", ingest_cases), ("pool", pool_cases)):
         if name in want:
             fn()
     print("golden vectors written to", HERE)
@@ -542,6 +546,99 @@ def ingest_cases():
             res = dict(error=type(e).__name__, message=str(e))
         st.add(dict(kind="snapshot_error", name=name, **res), payload=b2a(p))
     st.save("ingest_cases")
+
+
+# ------------------------------------------------------------------ pool maintenance (§8f rank 2)
+def pool_cases():
+    import copy
+    from splatstream.expansion import freeze_policy, precull, prune
+    from splatstream.geometry import CameraIntrinsics, Pose
+    from splatstream.model import (AppendRecord, GridIndex, PermuteRecord, PruneRecord, apply_mutation,
+                                   freeze_range)
+    from splatstream.optim import OptimizerState
+    from splatstream.protocol.delta import DeltaBaselines
+    from splatstream.protocol.packets import encode_ordering
+    st = Store()
+    rng = np.random.default_rng(777)
+
+    def opt_state(m):
+        o = OptimizerState(m, scene_extent=3.0)
+        a = m.active_count
+        for k in o.m:  # integer-valued moments: row moves are what is checked, and they compress
+            o.m[k] = rng.integers(-1000, 1000, o.m[k].shape).astype(np.float64)
+            o.v[k] = rng.integers(0, 1000, o.v[k].shape).astype(np.float64)
+        o.age = rng.integers(0, 300, a).astype(np.int64)
+        o.grad_ema = 10.0 ** rng.uniform(-7, -2, a)
+        return o
+
+    def opt_arrays(prefix, o):
+        out = {f"{prefix}age": o.age, f"{prefix}grad_ema": o.grad_ema}
+        for k in o.m:
+            out[f"{prefix}m_{k}"] = o.m[k]
+            out[f"{prefix}v_{k}"] = o.v[k]
+        return out
+
+    for (n, deg, frozen, cell) in ((1, 0, 0, 2.0), (50, 1, 10, 1.5), (3000, 2, 400, 1.0), (8000, 1, 900, 0.7)):
+        m = random_model(rng, n, deg, frozen, spread=4.0)
+        m.logit_opacities[:] = rng.uniform(-6, 3, n).astype(np.float32)  # some below the 0.01 floor
+        o = opt_state(m)
+        b = DeltaBaselines()
+        b.reset_from_model(m, 1)
+        base_arrays = dict(**model_arrays(m), **opt_arrays("opt_", o), base_means=b.means, base_log_scales=b.log_scales)
+        # grid + precull
+        grid = GridIndex(cell_size=cell, origin=(0.1, -0.2, 0.3))
+        grid.rebuild(m)
+        keys = np.array(list(grid.cell_map.keys()), np.int64).reshape(-1, 3)
+        lens = np.array([len(v) for v in grid.cell_map.values()], np.int64)
+        rows = np.concatenate([np.array(v, np.int64) for v in grid.cell_map.values()]) if n else np.zeros(0, np.int64)
+        intr = CameraIntrinsics(width=96, height=64, fov_y=np.deg2rad(60), near=0.2, far=9.0)
+        poses = [Pose(np.array([0.0, 0.0, -6.0]), np.array([1.0, 0.0, 0.0, 0.0])),
+                 Pose(np.array([5.0, 1.0, 0.0]), np.array([0.7071, 0.0, -0.7071, 0.0]))]
+        keep = precull(m, grid, poses, intr)
+        depth = [rng.uniform(2.0, 9.0, (64, 96)), rng.uniform(2.0, 9.0, (64, 96))]
+        keep_d = precull(m, grid, poses, intr, depth)
+        pose_arr = np.array([np.concatenate([p.position, p.quaternion]) for p in poses])
+        # freeze
+        frz = freeze_policy(m, o, age_threshold=120, grad_threshold=3e-4)
+        mf, of, bf = copy.deepcopy(m), copy.deepcopy(o), copy.deepcopy(b)
+        prec = freeze_range(mf, frz)
+        if prec is not None:
+            of.resize(prec)
+            bf.apply_record(prec)
+        # prune
+        mp, op_, bp = copy.deepcopy(m), copy.deepcopy(o), copy.deepcopy(b)
+        removed, rrec = prune(mp, opacity_floor=0.01)
+        if rrec is not None:
+            op_.resize(rrec)
+            bp.apply_record(rrec)
+        # append (placeholders on the client) + ordering packet over all three records
+        ids = rng.integers(0, 5, 7).astype(np.int32)
+        arec = AppendRecord(insert_at=int(m.active_count), count=7, object_ids=ids,
+                            new_active_count=int(m.active_count) + 7)
+        recs = [r for r in (prec,) if r is not None]
+        packet = encode_ordering(recs + [arec] + ([rrec] if rrec is not None else []))
+        ma = copy.deepcopy(m)
+        apply_mutation(ma, arec)
+        ba = copy.deepcopy(b)
+        ba.apply_record(arec)
+        oa = copy.deepcopy(o)
+        oa.resize(arec)
+        arrays = dict(base_arrays, cell_keys=keys, cell_lens=lens, cell_rows=rows, precull=keep, precull_depth=keep_d,
+                      depth0=depth[0], depth1=depth[1], poses=pose_arr, freeze=frz, removed=removed,
+                      append_ids=ids, packet=b2a(packet),
+                      **{f"frozen_{k}": v for k, v in model_arrays(mf).items()}, **opt_arrays("frozen_opt_", of),
+                      frozen_base_means=bf.means, frozen_base_log_scales=bf.log_scales,
+                      **{f"pruned_{k}": v for k, v in model_arrays(mp).items()}, **opt_arrays("pruned_opt_", op_),
+                      pruned_base_means=bp.means, pruned_base_log_scales=bp.log_scales,
+                      **{f"appended_{k}": v for k, v in model_arrays(ma).items()}, **opt_arrays("appended_opt_", oa),
+                      appended_base_means=ba.means, appended_base_log_scales=ba.log_scales)
+        if prec is not None:
+            arrays["permutation"] = prec.permutation
+        st.add(dict(kind="pool", name=f"pool_{n}_{deg}", n=n, degree=deg, active=int(m.active_count), cell=cell,
+                    origin=[0.1, -0.2, 0.3], width=96, height=64, fov_y=float(np.deg2rad(60)), near=0.2, far=9.0,
+                    frozen_active=int(mf.active_count), pruned_active=int(mp.active_count),
+                    has_permute=prec is not None, has_prune=rrec is not None), **arrays)
+    st.save("pool_cases")
 
 
 if __name__ == "__main__":
