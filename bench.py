@@ -358,9 +358,10 @@ def run_ours(args):
         enc = encoder_bench(c, _lib, args, torch)
 
     # ---- pool maintenance of this model, rank 0
-    pool_rec = None
+    pool_rec = zlib_rec = None
     if rank == 0:
         pool_rec = pool_bench(dm, state, poses, intr, torch)
+        zlib_rec = zlib_tick_bench(dm, base_m, base_l, torch)
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -412,7 +413,7 @@ def run_ours(args):
            "gpu_launches": launches, "clocks": clock_rec,
            "kernel_ms_per_step": {k: round(v, 4) for k, v in per_step.items()},
            "evaluated_pairs_per_view": evals_per_view,
-           "delta_encode": enc, "pool_maintenance": pool_rec, "fp32_peak_tflops_measured": fp32_peak,
+           "delta_encode": enc, "pool_maintenance": pool_rec, "server_tick_zlib": zlib_rec, "fp32_peak_tflops_measured": fp32_peak,
            "precision": "fp64 preprocess/windows/depth keys, fp32 blend + chain rule, fp64 Adam moments"}
     print(json.dumps(out), flush=True)
     if pg is not None:
@@ -513,6 +514,40 @@ def ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch, reps=10):
             "payload_bytes_per_tick": sum(len(p) for p in payloads),
             "replica_equals_server_baseline": same,
             "note": "wall clock per tick of 4 apply_delta calls (host payload bytes -> device replica), incl. baseline re-arm copies"}
+
+
+def zlib_tick_bench(dm, base_m, base_l, torch, reps=3):
+    """The reference server's default stream (compression_id 1) for tick 0
+    (all six attributes) of the 1M-row model: DeltaEmitter with the blocks
+    deflated serially vs on parallel host threads."""
+    from paper_2604_02851_b200 import protocol as P
+    base = P.DeviceBaselines(base_m.clone(), base_l.clone(), 0)
+    em = P.DeltaEmitter(dm, base, compression_id=1)
+    em.tick(0)
+    ref_m, ref_l = base.means.clone(), base.log_scales.clone()
+    a = dm.active_count
+    raws = None
+    t_par = t_ser = 0.0
+    for _ in range(reps):
+        base.means.copy_(ref_m)
+        base.log_scales.copy_(ref_l)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = em.tick(0)
+        t_par += time.perf_counter() - t0
+    em_raw = P.DeltaEmitter(dm, base, compression_id=0)
+    base.means.copy_(ref_m)
+    base.log_scales.copy_(ref_l)
+    raws = [p for _, p in em_raw.tick(0)]
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ser = [P._recompress_delta(r, 1) for r in raws]
+        t_ser += time.perf_counter() - t0
+    assert ser == [p for _, p in out]
+    return {"rows": a, "attributes": len(out), "raw_bytes": sum(len(r) for r in raws),
+            "zlib_bytes": sum(len(p) for _, p in out), "tick_ms_parallel_zlib": t_par * 1e3 / reps,
+            "zlib_stage_ms_serial": t_ser * 1e3 / reps,
+            "note": "tick = device encode + readback + per-attribute deflate on host threads (byte-identical)"}
 
 
 def pool_bench(dm, state, poses, intr, torch, reps=5):

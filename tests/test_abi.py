@@ -38,3 +38,14 @@ def test_bounds_and_host_zlib_match_python():
     for n in (0, 1, 1000, 100000):
         blk = rng.integers(0, 40, n).astype(np.uint8).tobytes()
         assert host_zlib(blk) == zlib.compress(blk, 6)
+
+
+def test_parallel_host_zlib_is_byte_identical():
+    """blocks deflated on parallel threads equal Python's
+    zlib.compress(block, 6), the reference's compression stage."""
+    import os
+    import zlib
+    from paper_2604_02851_b200.protocol import compress_blocks, host_zlib
+    blocks = [os.urandom(5000) * 40 + bytes(100000), b"", b"\x00", os.urandom(70000)]
+    assert compress_blocks(blocks) == [zlib.compress(b, 6) for b in blocks]
+    assert host_zlib(blocks[0]) == zlib.compress(blocks[0], 6)
