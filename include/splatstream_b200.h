@@ -79,6 +79,10 @@ typedef struct {
     int32_t deterministic;   /* backward: 1 = fixed-order per-(tile,splat) partials, 0 = atomics */
     void* gt_ready;          /* backward: cudaEvent_t the stream waits on right before the first read of
                                 the ground truth (its upload may overlap the forward pass); NULL = none */
+    uint32_t* tile_hint;     /* optional device (tiles,): per-tile walk lengths of an earlier call for the
+                                same camera (0xffffffff = unknown); orders the forward's tiles longest-first
+                                and is overwritten with this call's lengths.  NULL = list lengths */
+    int64_t tile_hint_len;   /* entries in tile_hint (must equal the tile count, else it is ignored) */
 } ss_render_opts;
 
 /* Host-readable summary of the last render/backward call. */

@@ -42,7 +42,8 @@ class SSLight(C.Structure):
 
 class SSRenderOpts(C.Structure):
     _fields_ = [("background", f64 * 3), ("subset", vp), ("subset_count", i32), ("extent_cutoff", i32),
-                ("precision", i32), ("deterministic", i32), ("gt_ready", vp)]
+                ("precision", i32), ("deterministic", i32), ("gt_ready", vp), ("tile_hint", vp),
+                ("tile_hint_len", i64)]
 
 
 class SSRenderStats(C.Structure):

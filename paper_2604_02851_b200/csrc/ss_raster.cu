@@ -1275,7 +1275,8 @@ int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bi
     ss_tic(ctx, KC_FORWARD);
     uint32_t* order = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
     if (!order) return SS_ERR_CUDA;
-    k_tile_order<<<1, 1024, 0, ctx->stream>>>(b.ranges, nullptr, b.n_tiles, order);
+    const bool hint = o->tile_hint && o->tile_hint_len == b.n_tiles;
+    k_tile_order<<<1, 1024, 0, ctx->stream>>>(b.ranges, hint ? o->tile_hint : nullptr, b.n_tiles, order);
     SS_CHECK_LAUNCH(ctx);
     if constexpr (sizeof(R) == 4)
         k_blend_fwd2<<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
@@ -1319,6 +1320,8 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     R* partials = SS_SCRATCH(ctx, R, 9 * (b.pairs > 0 ? b.pairs : 1));
     if (!img || !stop || !tloss || !partials) return SS_ERR_CUDA;
     SS_TRY(forward<R>(ctx, cam, o, b, img, (R*)nullptr, stop));
+    if (o->tile_hint && o->tile_hint_len == b.n_tiles)  // this call's walk lengths order the next forward
+        SS_CUDA(ctx, cudaMemcpyAsync(o->tile_hint, stop, sizeof(uint32_t) * b.n_tiles, cudaMemcpyDeviceToDevice, s));
     const double inv_npx = 1.0 / (double)(3 * npx);
     if (o->gt_ready) SS_CUDA(ctx, cudaStreamWaitEvent(s, (cudaEvent_t)o->gt_ready, 0));
     ss_tic(ctx, KC_BACKWARD);

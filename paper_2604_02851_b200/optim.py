@@ -137,6 +137,19 @@ class _Pending:
         return self.t
 
 
+def _tile_hint(view, device):
+    """Per-view device buffer of the last walk length of every tile (the
+    library orders the next forward of this camera longest-first with it)."""
+    import torch
+    intr = view.intrinsics
+    n = ((intr.width + 15) // 16) * ((intr.height + 15) // 16)
+    h = view.__dict__.get("_tile_hint")
+    if h is None or h.numel() != n or h.device != device:
+        h = torch.full((n,), -1, dtype=torch.int32, device=device)  # 0xffffffff: unknown
+        view.__dict__["_tile_hint"] = h
+    return h
+
+
 def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subset=None, extent_cutoff=True,
                     precision=0, image_out=None, subset_tensor=None, gt=None):
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
@@ -152,7 +165,8 @@ def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subs
     st = _lib.SSRenderStats()
     c.check(c.lib.ss_backward(c.handle, model.struct(), camera_struct(view.pose, view.intrinsics),
                               light_struct(view.light_state),
-                              render_opts(view.background, sub, extent_cutoff, precision, gt_ready=ready),
+                              render_opts(view.background, sub, extent_cutoff, precision, gt_ready=ready,
+                                          tile_hint=_tile_hint(view, model.device)),
                               _lib.ptr(gt), _lib.ptr(grad_accum), _lib.ptr(loss_accum), _lib.ptr(image_out), st))
     return st
 

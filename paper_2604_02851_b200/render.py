@@ -80,9 +80,13 @@ def _subset_tensor(index_subset, device):
     return torch.from_numpy(idx).to(device)
 
 
-def render_opts(background, subset, extent_cutoff, precision, deterministic=1, gt_ready=None) -> _lib.SSRenderOpts:
+def render_opts(background, subset, extent_cutoff, precision, deterministic=1, gt_ready=None,
+                tile_hint=None) -> _lib.SSRenderOpts:
     o = _lib.SSRenderOpts()
     o.gt_ready = gt_ready
+    if tile_hint is not None:
+        o.tile_hint = tile_hint.data_ptr()
+        o.tile_hint_len = int(tile_hint.numel())
     o.background = _lib.f64arr(background, 3)
     o.subset = subset.data_ptr() if subset is not None else None
     o.subset_count = int(subset.numel()) if subset is not None else 0
