@@ -298,7 +298,7 @@ struct __align__(16) Staged {
     R mx, my, a, b;
     R c, o, c0, c1;
     R c2;
-    int wx0, wx1, qmask_lo;  // tile-local x window [wx0, wx1); wy packed below
+    int wx0, wx1, rows;      // tile-local x window [wx0, wx1); rows: pixel-row masks (bits 0-7 even, 8-15 odd lanes)
     int wy0, wy1, p, pad;    // tile-local y window [wy0, wy1); p = partial index
 };
 
@@ -322,15 +322,21 @@ __device__ __forceinline__ void stage(Staged<R>& s, const double2 mu, const Spla
     s.wx1 = min(max(rec.win[1] - X0, 0), TILE);
     s.wy0 = min(max(rec.win[2] - Y0, 0), TILE);
     s.wy1 = min(max(rec.win[3] - Y0, 0), TILE);
+    unsigned rows = 0;
+#pragma unroll
+    for (int ly0 = 0; ly0 < 2; ++ly0) {  // rows ly0 + 2q inside [wy0, wy1), once per staged splat
+        const int qlo = max(0, (s.wy0 - ly0 + 1) >> 1);
+        const int qhi = max(0, (s.wy1 - ly0 + 1) >> 1);
+        rows |= (((1u << qhi) - 1u) & ~((1u << qlo) - 1u)) << (8 * ly0);
+    }
+    s.rows = (int)rows;
 }
 
 // 8-bit mask of this lane's pixels (rows ly0 + 2q) inside [wy0, wy1), if its column is inside [wx0, wx1)
 template <typename R>
 __device__ __forceinline__ unsigned lane_mask(const Staged<R>& s, int lx, int ly0) {
-    if (lx < s.wx0 || lx >= s.wx1) return 0u;
-    const int qlo = max(0, (s.wy0 - ly0 + 1) >> 1);
-    const int qhi = max(0, (s.wy1 - ly0 + 1) >> 1);
-    return ((1u << qhi) - 1u) & ~((1u << qlo) - 1u);
+    if ((unsigned)(lx - s.wx0) >= (unsigned)(s.wx1 - s.wx0)) return 0u;
+    return ((unsigned)s.rows >> (8 * ly0)) & 0xFFu;
 }
 
 template <typename R>
