@@ -299,7 +299,9 @@ struct __align__(16) Staged {
     R c, o, c0, c1;
     R c2;
     int wx0, wx1, rows;      // tile-local x window [wx0, wx1); rows: pixel-row masks (bits 0-7 even, 8-15 odd lanes)
-    int wy0, wy1, p, pad;    // tile-local y window [wy0, wy1); p = partial index
+    int wy0, wy1, p;         // tile-local y window [wy0, wy1); p = partial index
+    R aK;                    // fp32: a K, 2 b K, c K with K = -0.5 log2(e) (the exponent's prescale), once per splat
+    R bK2, cK, pad;
 };
 
 template <typename R>
@@ -322,6 +324,12 @@ __device__ __forceinline__ void stage(Staged<R>& s, const double2 mu, const Spla
     s.wx1 = min(max(rec.win[1] - X0, 0), TILE);
     s.wy0 = min(max(rec.win[2] - Y0, 0), TILE);
     s.wy1 = min(max(rec.win[3] - Y0, 0), TILE);
+    if (sizeof(R) == 4) {
+        const R K = (R)(-0.5 * 1.4426950408889634);
+        s.aK = rec.a * K;
+        s.bK2 = (R)2 * rec.b * K;
+        s.cK = rec.c * K;
+    }
     unsigned rows = 0;
 #pragma unroll
     for (int ly0 = 0; ly0 < 2; ++ly0) {  // rows ly0 + 2q inside [wy0, wy1), once per staged splat
@@ -358,9 +366,10 @@ __device__ __forceinline__ R gauss_power(const Staged<R>& s, R dx, R dy) {
 // Per (splat, lane) geometry: the lane's column is fixed, so the conic's x
 // terms are hoisted; per pixel the exponent is two FMAs.  fp64 keeps the
 // reference's exact expression (render.py:311).
-template <typename R>
+template <typename R, bool STAGED_K = false>
 struct PixelGeom {
-    // fp32: exponent pre-scaled by K = -0.5 log2(e) so G = ex2((cK y + BK) y + AK)
+    // fp32: exponent pre-scaled by K = -0.5 log2(e) so G = ex2((cK y + BK) y + AK);
+    // STAGED_K: the prescaled conic comes from the staging (forward)
     R dx, dy0, Ax2, Bx2, adx0, bdx0, cK;
     __device__ __forceinline__ PixelGeom(const Staged<R>& s, int lx, int ly0, int X0, int Y0) {
         R dyy;
@@ -368,7 +377,11 @@ struct PixelGeom {
         dy0 = dyy;
         adx0 = s.a * dx;
         bdx0 = s.b * dx;
-        if (sizeof(R) == 4) {
+        if (sizeof(R) == 4 && STAGED_K) {
+            Ax2 = s.aK * dx * dx;
+            Bx2 = s.bK2 * dx;
+            cK = s.cK;
+        } else if (sizeof(R) == 4) {
             const R K = (R)(-0.5 * 1.4426950408889634);
             Ax2 = adx0 * dx * K;
             Bx2 = (R)2 * bdx0 * K;
@@ -712,7 +725,7 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
             if (!act) continue;
             last = (int)(b0 - rg.x) + k;
             evals += __popc(act);
-            PixelGeom<float> pg(s, lx, ly0, X0, Y0);
+            PixelGeom<float, true> pg(s, lx, ly0, X0, Y0);
             const unsigned wact = __reduce_or_sync(__activemask(), act);
             const float2 cK = f2(pg.cK), Bx = f2(pg.Bx2), Ax = f2(pg.Ax2), o = f2(s.o);
 #pragma unroll
