@@ -298,10 +298,10 @@ struct __align__(16) Staged {
     R mx, my, a, b;
     R c, o, c0, c1;
     R c2;
-    int wx0, wx1, rows;      // tile-local x window [wx0, wx1); rows: pixel-row masks (bits 0-7 even, 8-15 odd lanes)
-    int wy0, wy1, p;         // tile-local y window [wy0, wy1); p = partial index
-    R aK;                    // fp32: a K, 2 b K, c K with K = -0.5 log2(e) (the exponent's prescale), once per splat
-    R bK2, cK, pad;
+    R aK, bK2, cK;           // fp32: a K, 2 b K, c K with K = -0.5 log2(e) (the exponent's prescale), once per splat
+    int wx;                  // tile-local x window: wx0 | (wx1 - wx0) << 16
+    int rows;                // pixel-row masks of the y window: bits 0-7 even lanes, 8-15 odd lanes
+    int p, pad;              // p = partial index (backward)
 };
 
 template <typename R>
@@ -320,30 +320,29 @@ __device__ __forceinline__ void stage(Staged<R>& s, const double2 mu, const Spla
     s.c0 = rec.col[0];
     s.c1 = rec.col[1];
     s.c2 = rec.col[2];
-    s.wx0 = min(max(rec.win[0] - X0, 0), TILE);
-    s.wx1 = min(max(rec.win[1] - X0, 0), TILE);
-    s.wy0 = min(max(rec.win[2] - Y0, 0), TILE);
-    s.wy1 = min(max(rec.win[3] - Y0, 0), TILE);
     if (sizeof(R) == 4) {
         const R K = (R)(-0.5 * 1.4426950408889634);
         s.aK = rec.a * K;
         s.bK2 = (R)2 * rec.b * K;
         s.cK = rec.c * K;
     }
+    const int wx0 = min(max(rec.win[0] - X0, 0), TILE), wx1 = min(max(rec.win[1] - X0, 0), TILE);
+    const int wy0 = min(max(rec.win[2] - Y0, 0), TILE), wy1 = min(max(rec.win[3] - Y0, 0), TILE);
+    s.wx = wx0 | ((wx1 - wx0) << 16);
     unsigned rows = 0;
 #pragma unroll
     for (int ly0 = 0; ly0 < 2; ++ly0) {  // rows ly0 + 2q inside [wy0, wy1), once per staged splat
-        const int qlo = max(0, (s.wy0 - ly0 + 1) >> 1);
-        const int qhi = max(0, (s.wy1 - ly0 + 1) >> 1);
+        const int qlo = max(0, (wy0 - ly0 + 1) >> 1);
+        const int qhi = max(0, (wy1 - ly0 + 1) >> 1);
         rows |= (((1u << qhi) - 1u) & ~((1u << qlo) - 1u)) << (8 * ly0);
     }
     s.rows = (int)rows;
 }
 
-// 8-bit mask of this lane's pixels (rows ly0 + 2q) inside [wy0, wy1), if its column is inside [wx0, wx1)
+// 8-bit mask of this lane's pixels (rows ly0 + 2q) inside the y window, if its column is inside the x window
 template <typename R>
 __device__ __forceinline__ unsigned lane_mask(const Staged<R>& s, int lx, int ly0) {
-    if ((unsigned)(lx - s.wx0) >= (unsigned)(s.wx1 - s.wx0)) return 0u;
+    if ((unsigned)(lx - (s.wx & 0xFFFF)) >= ((unsigned)s.wx >> 16)) return 0u;
     return ((unsigned)s.rows >> (8 * ly0)) & 0xFFu;
 }
 
@@ -603,7 +602,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
             if (act) {
                 // branch-free over the lane's 8 pixels: inactive ones get
                 // G = 0, which zeroes every contribution and leaves T, R alone
-                PixelGeom<R> pg(s, lx, ly0, X0, Y0);
+                PixelGeom<R, true> pg(s, lx, ly0, X0, Y0);
                 const unsigned wact = __reduce_or_sync(__activemask(), act);
 #pragma unroll
                 for (int g = 0; g < PPT; g += QG_BWD) {
