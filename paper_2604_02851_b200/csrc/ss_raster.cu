@@ -346,15 +346,11 @@ __device__ __forceinline__ unsigned lane_mask(const Staged<R>& s, int lx, int ly
     return ((unsigned)s.rows >> (8 * ly0)) & 0xFFu;
 }
 
+// the lane's pixel-centre coordinate: fp32 relative to the tile origin (the
+// staged centre is too), fp64 absolute, (i + 0.5) as the reference (render.py:306-307)
 template <typename R>
-__device__ __forceinline__ void deltas(const Staged<R>& s, int lx, int ly, int X0, int Y0, R& dx, R& dy) {
-    if (sizeof(R) == 4) {
-        dx = ((R)lx + (R)0.5) - s.mx;
-        dy = ((R)ly + (R)0.5) - s.my;
-    } else {
-        dx = ((R)(X0 + lx) + (R)0.5) - s.mx;
-        dy = ((R)(Y0 + ly) + (R)0.5) - s.my;
-    }
+__device__ __forceinline__ R lane_centre(int l, int origin) {
+    return sizeof(R) == 4 ? (R)l + (R)0.5 : (R)(origin + l) + (R)0.5;
 }
 
 template <typename R>
@@ -370,10 +366,11 @@ struct PixelGeom {
     // fp32: exponent pre-scaled by K = -0.5 log2(e) so G = ex2((cK y + BK) y + AK);
     // STAGED_K: the prescaled conic comes from the staging (forward)
     R dx, dy0, Ax2, Bx2, adx0, bdx0, cK;
-    __device__ __forceinline__ PixelGeom(const Staged<R>& s, int lx, int ly0, int X0, int Y0) {
-        R dyy;
-        deltas(s, lx, ly0, X0, Y0, dx, dyy);
-        dy0 = dyy;
+    // (pxc, pyc): the lane's first pixel centre (tile-relative for fp32,
+    // absolute for fp64), computed once per kernel by lane_centre
+    __device__ __forceinline__ PixelGeom(const Staged<R>& s, R pxc, R pyc) {
+        dx = pxc - s.mx;
+        dy0 = pyc - s.my;
         adx0 = s.a * dx;
         bdx0 = s.b * dx;
         if (sizeof(R) == 4 && STAGED_K) {
@@ -417,6 +414,7 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
     const int tile = order ? (int)order[slot] : slot;
     const int X0 = (tile % tiles_x) * TILE, Y0 = (tile / tiles_x) * TILE;
     const int lx = lane & 15, ly0 = lane >> 4;
+    const R pxc = lane_centre<R>(lx, X0), pyc = lane_centre<R>(ly0, Y0);
     unsigned alive = 0;
 #pragma unroll
     for (int q = 0; q < PPT; ++q)
@@ -445,7 +443,7 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
             evals += __popc(act);
             // branch-free over the lane's 8 pixels: inactive ones get G = 0,
             // which leaves C and T unchanged
-            PixelGeom<R> pg(s, lx, ly0, X0, Y0);
+            PixelGeom<R> pg(s, pxc, pyc);
             const unsigned wact = __reduce_or_sync(__activemask(), act);
 #pragma unroll
             for (int g = 0; g < PPT; g += QG_FWD) {
@@ -549,6 +547,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int X0 = tx * TILE, Y0 = ty * TILE;
     const int lx = lane & 15, ly0 = lane >> 4;
+    const R pxc = lane_centre<R>(lx, X0), pyc = lane_centre<R>(ly0, Y0);
     const uint2 rg = ranges[tile];
     const uint32_t stop = rg.x + (tile_stop ? min(tile_stop[tile], rg.y - rg.x) : (rg.y - rg.x));
 
@@ -602,7 +601,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
             if (act) {
                 // branch-free over the lane's 8 pixels: inactive ones get
                 // G = 0, which zeroes every contribution and leaves T, R alone
-                PixelGeom<R, true> pg(s, lx, ly0, X0, Y0);
+                PixelGeom<R, true> pg(s, pxc, pyc);
                 const unsigned wact = __reduce_or_sync(__activemask(), act);
 #pragma unroll
                 for (int g = 0; g < PPT; g += QG_BWD) {
@@ -697,6 +696,7 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
     const int tile = order ? (int)order[slot] : slot;
     const int X0 = (tile % tiles_x) * TILE, Y0 = (tile / tiles_x) * TILE;
     const int lx = lane & 15, ly0 = lane >> 4;
+    const float pxc = lane_centre<float>(lx, X0), pyc = lane_centre<float>(ly0, Y0);
     unsigned alive = 0;
 #pragma unroll
     for (int q = 0; q < PPT; ++q)
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
             if (!act) continue;
             last = (int)(b0 - rg.x) + k;
             evals += __popc(act);
-            PixelGeom<float, true> pg(s, lx, ly0, X0, Y0);
+            PixelGeom<float, true> pg(s, pxc, pyc);
             const unsigned wact = __reduce_or_sync(__activemask(), act);
             const float2 cK = f2(pg.cK), Bx = f2(pg.Bx2), Ax = f2(pg.Ax2), o = f2(s.o);
 #pragma unroll
