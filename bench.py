@@ -584,17 +584,20 @@ def measured_peaks():
     return {}
 
 
-def committed_traffic(key):
-    """DRAM bytes per launch of a kernel class from this round's committed ncu
-    capture (profiles/r01_traffic.json); None when absent."""
+def _committed(key):
     p = os.path.join(ROOT, "profiles", "r01_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        e = d.get(key, {})
-        return e.get("bytes_per_launch", e.get("bytes_per_tick"))
+            return json.load(f).get(key, {})
     except (OSError, ValueError):
-        return None
+        return {}
+
+
+def committed_traffic(key):
+    """DRAM bytes per launch of a kernel class from this round's committed ncu
+    capture (profiles/r01_traffic.json); None when absent."""
+    e = _committed(key)
+    return e.get("bytes_per_launch", e.get("bytes_per_tick"))
 
 
 def roofline(dom, per_step, kt, counters, args, local_views, fp32_peak):
@@ -613,7 +616,7 @@ def roofline(dom, per_step, kt, counters, args, local_views, fp32_peak):
                 "ms_per_launch": ms_launch,
                 "work_per_launch": f"{evals:.4g} T-gated (pixel, splat) pairs x {22 if dom == 'blend_forward' else 60} FLOP",
                 "peak_source": "measured FMA probe (ss_measure_fp32_peak)",
-                "hbm_peak_gbs": hbm}
+                "hbm_peak_gbs": hbm, "ncu": _committed(dom).get("ncu")}
     return {"bound": "hbm", "kernel": dom, "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
             "traffic": None, "ms_per_launch": ms_launch}
 
