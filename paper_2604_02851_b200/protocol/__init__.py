@@ -282,6 +282,41 @@ class DeltaTicker:
         c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
         return self.model.active_count * len(key)
 
+    def read_async(self, attributes):
+        """Start reading the last call's payloads for `attributes` back without
+        a host sync: lengths and each payload's bound-sized buffer are copied
+        into pinned memory on the current stream; `.result()` waits for that
+        copy only (the GPU keeps running whatever was queued after it)."""
+        import torch
+        key = [int(x) for x in attributes]
+        m = self.model
+        bounds = [int(self._ctx.lib.ss_delta_bound(a, m.active_count, self._dims(a))) for a in key]
+        need = sum(bounds)
+        slot = getattr(self, "_slot", 0) ^ 1  # two pinned buffers: one may still be pending
+        self._slot = slot
+        bufs = getattr(self, "_async", None)
+        if bufs is None:
+            bufs = self._async = [None, None]
+        st = bufs[slot]
+        if st is not None:
+            st[2].synchronize()  # its previous reader has finished with it
+        if st is None or st[0].numel() < need:
+            st = bufs[slot] = (torch.empty(max(need, 1 << 16) * 5 // 4, dtype=torch.uint8, pin_memory=True),
+                               torch.empty(8, dtype=torch.int64, pin_memory=True), torch.cuda.Event())
+        host, lens, ev = st
+        off = 0
+        for i, (a, b) in enumerate(zip(key, bounds)):
+            host[off:off + b].copy_(self.outs[a].data[:b], non_blocking=True)
+            lens[i:i + 1].copy_(self.outs[a].length, non_blocking=True)
+            off += b
+        ev.record(torch.cuda.current_stream(m.device))
+        return _PendingPayloads(host, lens, ev, bounds)
+
+    def _dims(self, attr):
+        m = self.model
+        B = (m.sh_degree + 1) ** 2
+        return {0: 3, 1: 3, 2: 4, 3: 1, 4: 3, 5: 3 * (B - 1), 6: 1}[int(attr)]
+
     def read(self, attributes, copy: bool = True):
         """Payloads of the last call for `attributes`, read back with two host
         syncs in total (lengths, then every payload into pinned memory).
@@ -306,6 +341,24 @@ class DeltaTicker:
         for n in lens:
             out.append(mv[off:off + n].tobytes() if copy else mv[off:off + n])
             off += n
+        return out
+
+
+class _PendingPayloads:
+    """Payload bytes of one tick, copied back asynchronously (DeltaTicker.read_async)."""
+
+    def __init__(self, host, lens, ev, bounds):
+        self.host, self.lens, self.ev, self.bounds = host, lens, ev, bounds
+
+    def result(self, copy: bool = True):
+        self.ev.synchronize()
+        mv = memoryview(self.host.numpy())
+        ln = self.lens.numpy()
+        out, off = [], 0
+        for i, b in enumerate(self.bounds):
+            n = int(ln[i])
+            out.append(mv[off:off + n].tobytes() if copy else mv[off:off + n])
+            off += b
         return out
 
 

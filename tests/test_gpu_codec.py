@@ -222,3 +222,24 @@ def test_gpu_delta_emitter_server_ticks_match_oracle():
         np.testing.assert_array_equal(base.log_scales.cpu().numpy(), hb_l)
         np.testing.assert_array_equal(rbase.means.cpu().numpy(), hb_m)
         np.testing.assert_array_equal(replica.means[:a].cpu().numpy(), hb_m[:a])
+
+
+def test_gpu_ticker_read_async_matches_read():
+    """read_async (bound-sized copies, no host sync) returns the same bytes as read()."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.protocol import DeltaTicker, PayloadBuffer
+    host = synth.random_field(30_000, 1, 320, 180, seed=8)
+    dm = DeviceModel.from_host(host, 0)
+    base = {0: (dm.means - 1e-3).contiguous(), 1: dm.log_scales.clone()}
+    t = DeltaTicker(dm, base, {k: PayloadBuffer(64, dm.device) for k in range(7)})
+    attrs = [0, 1, 3, 4, 5]
+    t(attrs)
+    p1 = t.read_async(attrs)
+    sync = t.read(attrs)
+    t(attrs)  # second tick while the first readback may be pending
+    p2 = t.read_async(attrs)
+    assert p1.result() == sync
+    assert p2.result() == t.read(attrs)
