@@ -47,6 +47,28 @@ int ss_fail(ss_ctx* ctx, int code, const char* fmt, ...);
     } while (0)
 
 // every kernel launch site is followed by SS_CHECK_LAUNCH, which also counts it
+// Programmatic dependent launch (sm_90+): a kernel launched with ss_launch
+// may be scheduled while its predecessor on the stream is still finishing;
+// it waits at SS_PDL_WAIT() (its first statement) until the predecessor's
+// results are visible, so the launch latency overlaps the predecessor's tail.
+#define SS_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t ss_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                             Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 #define SS_CHECK_LAUNCH(ctx)           \
     do {                               \
         ++(ctx)->launches;             \

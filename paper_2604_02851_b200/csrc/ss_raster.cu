@@ -66,6 +66,7 @@ struct DebugOut {
 };
 
 __global__ void k_visible_flags(ss_model m, ss_camera cam, const int64_t* subset, int64_t n_in, uint8_t* flag) {
+    SS_PDL_WAIT();
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
         int64_t row = subset ? subset[j] : j;
         double d[3], mc[3];
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(128, 4) k_preprocess(ss_model m, ss_camera cam
                              int cutoff, uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                              SplatRec<R>* __restrict__ rec, double2* __restrict__ mu, DebugOut dbg,
                              unsigned long long* __restrict__ kminmax) {
+    SS_PDL_WAIT();
     unsigned long long kmin = ~0ull, kmax = 0;
     constexpr int B = ss_sh_bases(DEG);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
@@ -144,6 +146,7 @@ __global__ void __launch_bounds__(128, 4) k_preprocess(ss_model m, ss_camera cam
 }
 
 __global__ void k_init_minmax(unsigned long long* kminmax) {
+    SS_PDL_WAIT();
     kminmax[0] = ~0ull;
     kminmax[1] = 0ull;
 }
@@ -153,6 +156,7 @@ __global__ void k_init_minmax(unsigned long long* kminmax) {
 // restores the exact order inside such runs.
 __global__ void k_key32(const uint64_t* __restrict__ dkey64, int64_t n, const unsigned long long* __restrict__ kminmax,
                         uint32_t* __restrict__ key32) {
+    SS_PDL_WAIT();
     const unsigned long long lo = kminmax[0], hi = kminmax[1];
     const unsigned long long range = hi > lo ? hi - lo : 0;
     const int bits = range ? 64 - __clzll((long long)range) : 0;
@@ -173,6 +177,7 @@ __global__ void k_key32(const uint64_t* __restrict__ dkey64, int64_t n, const un
 // stable insertion sort on the exact key gives lexsort((rows, depth)).
 __global__ void k_fix_ties(const uint32_t* __restrict__ key32, uint32_t* __restrict__ vals,
                            const uint64_t* __restrict__ dkey64, int64_t n) {
+    SS_PDL_WAIT();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = key32[i];
         if (k == 0xffffffffu || key32[i + 1] != k || (i > 0 && key32[i - 1] == k)) continue;
@@ -203,6 +208,7 @@ template <typename R>
 __global__ void k_count(const uint64_t* __restrict__ dkey64, const uint32_t* __restrict__ dvals,
                         const SplatRec<R>* __restrict__ rec, int64_t n_in, uint32_t* __restrict__ rcnt,
                         uint32_t* __restrict__ rinv) {
+    SS_PDL_WAIT();
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = dvals[r];
         if (dkey64[j] == ~0ull) {
@@ -227,6 +233,7 @@ template <typename R>
 __global__ void k_emit(const SplatRec<R>* __restrict__ rec, const uint32_t* __restrict__ dvals,
                        const uint32_t* __restrict__ rcnt, const uint64_t* __restrict__ roff, int64_t n_in, int tiles_x,
                        uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals, uint64_t* __restrict__ roffj) {
+    SS_PDL_WAIT();
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
         if (!rcnt[r]) continue;
         const uint32_t j = dvals[r];
@@ -243,6 +250,7 @@ __global__ void k_emit(const SplatRec<R>* __restrict__ rec, const uint32_t* __re
 }
 
 __global__ void k_ranges(const uint32_t* __restrict__ keys, int64_t n, uint2* __restrict__ ranges) {
+    SS_PDL_WAIT();
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t t = keys[s];
         if (s == 0 || keys[s - 1] != t) ranges[t].x = (uint32_t)s;
@@ -407,6 +415,7 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
                                                         uint32_t* __restrict__ tile_stop,
                                                         unsigned long long* __restrict__ eval_count,
                                                         const uint32_t* __restrict__ order) {
+    SS_PDL_WAIT();
     __shared__ Staged<R> sm[WPB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = blockIdx.x * WPB + warp;
@@ -539,6 +548,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
                                                         const float* __restrict__ gt, double npx3,
                                                         R* __restrict__ partials, double* __restrict__ tile_loss,
                                                         const uint32_t* __restrict__ order) {
+    SS_PDL_WAIT();
     __shared__ Staged<R> sm[WPB_BWD][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = blockIdx.x * WPB_BWD + warp;
@@ -689,6 +699,7 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
                                                          uint32_t* __restrict__ tile_stop,
                                                          unsigned long long* __restrict__ eval_count,
                                                          const uint32_t* __restrict__ order) {
+    SS_PDL_WAIT();
     __shared__ Staged<float> sm[WPB][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = blockIdx.x * WPB + warp;
@@ -770,6 +781,7 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
 }
 
 __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, double inv_npx, double* __restrict__ out) {
+    SS_PDL_WAIT();
     __shared__ double s[256];
     double t = 0;
     for (int i = threadIdx.x; i < n; i += 256) t += tile_loss[i];
@@ -792,6 +804,7 @@ template <typename R>
 __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
                                                       const uint32_t* __restrict__ dvals, const R* __restrict__ partials,
                                                       int64_t n_in, R* __restrict__ g9) {
+    SS_PDL_WAIT();
     constexpr int PW = 4096 / (9 * sizeof(R));  // pairs per staged chunk (4 KB per warp)
     __shared__ R buf[8][PW * 9];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -843,6 +856,7 @@ template <typename T, int DEG>
 __global__ void __launch_bounds__(128, 4) k_chain(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset,
                         const uint32_t* __restrict__ rinv, const T* __restrict__ g9, int64_t n_in, int cutoff,
                         float* __restrict__ grad, float4* __restrict__ shrec) {
+    SS_PDL_WAIT();
     constexpr int B = ss_sh_bases(DEG);
     const int64_t a = m.active_count;
     T Rc[3][3];
@@ -1059,6 +1073,7 @@ constexpr int SHG_ROWS = 64;  // rows per block in k_sh_grad
 template <int DEG>
 __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __restrict__ shrec, int64_t a,
                                                  float* __restrict__ grad_sh) {
+    SS_PDL_WAIT();
     constexpr int B = ss_sh_bases(DEG);
     __shared__ float s_y[SHG_ROWS][B + 1];
     __shared__ float4 s_r0[SHG_ROWS];
@@ -1135,6 +1150,7 @@ constexpr int ORDER_BUCKETS = 4096;
 __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges,
                                                      const uint32_t* __restrict__ stop, int n_tiles,
                                                      uint32_t* __restrict__ order) {
+    SS_PDL_WAIT();
     __shared__ uint32_t h[ORDER_BUCKETS];
     __shared__ uint32_t ws[32];
     for (int i = threadIdx.x; i < ORDER_BUCKETS; i += blockDim.x) h[i] = 0;
@@ -1230,12 +1246,12 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     memset(&none, 0, sizeof(none));
     if (n > 0) {
         ss_tic(ctx, KC_PREPROCESS);
-        k_init_minmax<<<1, 1, 0, s>>>(kminmax);
+        SS_CUDA(ctx, ss_launch((k_init_minmax), dim3(1), dim3(1), 0, s, kminmax));
         SS_CHECK_LAUNCH(ctx);
 #define SS_PRE(DEG)                                                                                      \
-    k_preprocess<DEG, R><<<gridn(ctx, n, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
+    SS_CUDA(ctx, ss_launch((k_preprocess<DEG, R>), dim3(gridn(ctx, n, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
                                                          b.dvals, (SplatRec<R>*)b.rec, b.mu, dbg ? *dbg : none,  \
-                                                         kminmax)
+                                                         kminmax))
         switch (m->sh_degree) {
             case 0: SS_PRE(0); break;
             case 1: SS_PRE(1); break;
@@ -1246,14 +1262,14 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_PREPROCESS);
         ss_tic(ctx, KC_DEPTH_SORT);
-        k_key32<<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, n, kminmax, b.dkeys);
+        SS_CUDA(ctx, ss_launch((k_key32), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkey64, n, kminmax, b.dkeys));
         SS_CHECK_LAUNCH(ctx);
         SS_TRY(ss_radix_sort_u32(ctx, b.dkeys, b.dvals, kalt, valt, n, 32));
-        k_fix_ties<<<gridn(ctx, n), 256, 0, s>>>(b.dkeys, b.dvals, b.dkey64, n);
+        SS_CUDA(ctx, ss_launch((k_fix_ties), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkeys, b.dvals, b.dkey64, n));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_DEPTH_SORT);
         ss_tic(ctx, KC_BIN);
-        k_count<R><<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, b.dvals, (const SplatRec<R>*)b.rec, n, b.rcnt, b.rinv);
+        SS_CUDA(ctx, ss_launch((k_count<R>), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkey64, b.dvals, (const SplatRec<R>*)b.rec, n, b.rcnt, b.rinv));
         SS_CHECK_LAUNCH(ctx);
     } else {
         ss_tic(ctx, KC_BIN);
@@ -1272,15 +1288,15 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (!b.pkeys || !b.pvals || !pk2 || !pv2) return SS_ERR_CUDA;
     if (P > 0) {
         ss_tic(ctx, KC_BIN);
-        k_emit<R><<<gridn(ctx, n), 256, 0, s>>>((const SplatRec<R>*)b.rec, b.dvals, b.rcnt, b.roff, n, b.tiles_x,
-                                                b.pkeys, b.pvals, b.roffj);
+        SS_CUDA(ctx, ss_launch((k_emit<R>), dim3(gridn(ctx, n)), dim3(256), 0, s, (const SplatRec<R>*)b.rec, b.dvals, b.rcnt, b.roff, n, b.tiles_x,
+                                                b.pkeys, b.pvals, b.roffj));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_BIN);
         ss_tic(ctx, KC_TILE_SORT);
         SS_TRY(ss_radix_sort_u32(ctx, b.pkeys, b.pvals, pk2, pv2, (int64_t)P, b.tile_bits));
         ss_toc(ctx, KC_TILE_SORT);
         ss_tic(ctx, KC_BIN);
-        k_ranges<<<gridn(ctx, (int64_t)P), 256, 0, s>>>(b.pkeys, (int64_t)P, b.ranges);
+        SS_CUDA(ctx, ss_launch((k_ranges), dim3(gridn(ctx, (int64_t)P)), dim3(256), 0, s, b.pkeys, (int64_t)P, b.ranges));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_BIN);
     }
@@ -1294,18 +1310,18 @@ int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bi
     uint32_t* order = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
     if (!order) return SS_ERR_CUDA;
     const bool hint = o->tile_hint && o->tile_hint_len == b.n_tiles;
-    k_tile_order<<<1, 1024, 0, ctx->stream>>>(b.ranges, hint ? o->tile_hint : nullptr, b.n_tiles, order);
+    SS_CUDA(ctx, ss_launch((k_tile_order), dim3(1), dim3(1024), 0, ctx->stream, b.ranges, hint ? o->tile_hint : nullptr, b.n_tiles, order));
     SS_CHECK_LAUNCH(ctx);
     if constexpr (sizeof(R) == 4)
-        k_blend_fwd2<<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
+        SS_CUDA(ctx, ss_launch((k_blend_fwd2), dim3((b.n_tiles + WPB - 1) / WPB), dim3(32 * WPB), 0, ctx->stream, 
             b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
             o->background[0], o->background[1], o->background[2], img, T, tile_stop,
-            ss_timing_on(ctx) ? ctx->dev_counters : nullptr, order);
+            ss_timing_on(ctx) ? ctx->dev_counters : nullptr, order));
     else
-        k_blend_fwd<R><<<(b.n_tiles + WPB - 1) / WPB, 32 * WPB, 0, ctx->stream>>>(
+        SS_CUDA(ctx, ss_launch((k_blend_fwd<R>), dim3((b.n_tiles + WPB - 1) / WPB), dim3(32 * WPB), 0, ctx->stream, 
             b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
             o->background[0], o->background[1], o->background[2], img, T, tile_stop,
-            ss_timing_on(ctx) ? ctx->dev_counters : nullptr, order);
+            ss_timing_on(ctx) ? ctx->dev_counters : nullptr, order));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_FORWARD);
     return SS_OK;
@@ -1345,13 +1361,13 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     ss_tic(ctx, KC_BACKWARD);
     uint32_t* order = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
     if (!order) return SS_ERR_CUDA;
-    k_tile_order<<<1, 1024, 0, s>>>(b.ranges, stop, b.n_tiles, order);
+    SS_CUDA(ctx, ss_launch((k_tile_order), dim3(1), dim3(1024), 0, s, b.ranges, stop, b.n_tiles, order));
     SS_CHECK_LAUNCH(ctx);
-    k_blend_bwd<R><<<(b.n_tiles + WPB_BWD - 1) / WPB_BWD, 32 * WPB_BWD, 0, s>>>(
+    SS_CUDA(ctx, ss_launch((k_blend_bwd<R>), dim3((b.n_tiles + WPB_BWD - 1) / WPB_BWD), dim3(32 * WPB_BWD), 0, s, 
         b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
-        b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order);
+        b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order));
     SS_CHECK_LAUNCH(ctx);
-    k_loss_reduce<<<1, 256, 0, s>>>(tloss, b.n_tiles, inv_npx, loss);
+    SS_CUDA(ctx, ss_launch((k_loss_reduce), dim3(1), dim3(256), 0, s, tloss, b.n_tiles, inv_npx, loss));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_BACKWARD);
     if (b.n_in > 0 && m->active_count > 0) {
@@ -1360,13 +1376,13 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         float4* shrec = SS_SCRATCH(ctx, float4, 2 * (int64_t)m->active_count);
         if (!g9 || !shrec) return SS_ERR_CUDA;
         SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)m->active_count, s));
-        k_sum_partials<R><<<gridn(ctx, b.n_in), 256, 0, s>>>(b.roff, b.rcnt, b.dvals, partials, b.n_in, g9);
+        SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals, partials, b.n_in, g9));
         SS_CHECK_LAUNCH(ctx);
 #define SS_CHAIN(DEG)                                                                                     \
-    k_chain<R, DEG><<<gridn(ctx, b.n_in, 128), 128, 0, s>>>(*m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
-                                                            o->extent_cutoff, grad, shrec);                      \
-    k_sh_grad<DEG><<<(unsigned)(((int64_t)m->active_count + SHG_ROWS - 1) / SHG_ROWS), 256, 0, s>>>(             \
-        *L, shrec, m->active_count, grad + 11 * (int64_t)m->active_count)
+    SS_CUDA(ctx, ss_launch((k_chain<R, DEG>), dim3(gridn(ctx, b.n_in, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
+                                                            o->extent_cutoff, grad, shrec));                      \
+    SS_CUDA(ctx, ss_launch((k_sh_grad<DEG>), dim3((unsigned)(((int64_t)m->active_count + SHG_ROWS - 1) / SHG_ROWS)), dim3(256), 0, s,              \
+        *L, shrec, m->active_count, grad + 11 * (int64_t)m->active_count))
         switch (m->sh_degree) {
             case 0: SS_CHAIN(0); break;
             case 1: SS_CHAIN(1); break;
@@ -1387,12 +1403,14 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
 
 __global__ void k_order_out(const uint64_t* dkey64, const uint32_t* dvals, const uint64_t* vpos, int64_t n,
                             int64_t* order) {
+    SS_PDL_WAIT();
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
         if (dkey64[dvals[r]] != ~0ull) order[r] = (int64_t)vpos[dvals[r]];
 }
 
 __global__ void k_debug_bins(const Bins b, int64_t* order_rows, const int64_t* subset, int64_t* ranges_out,
                              int64_t* pair_rank) {
+    SS_PDL_WAIT();
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = tid; r < b.n_in; r += nt)
         if (order_rows && b.dkey64[b.dvals[r]] != ~0ull) order_rows[r] = subset ? subset[b.dvals[r]] : (int64_t)b.dvals[r];
@@ -1442,7 +1460,7 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
     uint64_t* vtot = SS_SCRATCH(ctx, uint64_t, 1);
     if (!flag || !vpos || !vtot) return SS_ERR_CUDA;
     if (n > 0) {
-        k_visible_flags<<<gridn(ctx, n), 256, 0, s>>>(*m, *cam, o->subset, n, flag);
+        SS_CUDA(ctx, ss_launch((k_visible_flags), dim3(gridn(ctx, n)), dim3(256), 0, s, *m, *cam, o->subset, n, flag));
         SS_CHECK_LAUNCH(ctx);
     }
     SS_TRY(ss_scan_u8_to_u64(ctx, flag, vpos, n, vtot));
@@ -1456,7 +1474,7 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
     Bins b;
     SS_TRY(build_bins<double>(ctx, m, cam, L, o, b, &dbg));
     if (out->order && n > 0) {
-        k_order_out<<<gridn(ctx, n), 256, 0, s>>>(b.dkey64, b.dvals, vpos, n, out->order);
+        SS_CUDA(ctx, ss_launch((k_order_out), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkey64, b.dvals, vpos, n, out->order));
         SS_CHECK_LAUNCH(ctx);
     }
     if (visible_out) *visible_out = (int64_t)M;
@@ -1478,8 +1496,8 @@ int ss_debug_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss
     if (b.n_in > rows_cap || b.n_tiles > tiles_cap || b.pairs > pairs_cap)
         return ss_fail(ctx, SS_ERR_CAPACITY, "debug output too small (rows %lld tiles %d pairs %lld)",
                        (long long)b.n_in, b.n_tiles, (long long)b.pairs);
-    k_debug_bins<<<gridn(ctx, b.n_in > b.pairs ? b.n_in : b.pairs), 256, 0, ctx->stream>>>(b, order_rows, o->subset,
-                                                                                          ranges_out, pair_rank);
+    SS_CUDA(ctx, ss_launch((k_debug_bins), dim3(gridn(ctx, b.n_in > b.pairs ? b.n_in : b.pairs)), dim3(256), 0, ctx->stream, b, order_rows, o->subset,
+                                                                                          ranges_out, pair_rank));
     SS_CHECK_LAUNCH(ctx);
     if (st) {
         st->visible = -1;

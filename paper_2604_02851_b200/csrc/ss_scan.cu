@@ -40,6 +40,7 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* total)
 
 template <typename Tin>
 __global__ void k_block_sums(const Tin* __restrict__ in, int64_t n, uint64_t* __restrict__ sums) {
+    SS_PDL_WAIT();
     int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     uint64_t s = 0;
 #pragma unroll
@@ -53,6 +54,7 @@ __global__ void k_block_sums(const Tin* __restrict__ in, int64_t n, uint64_t* __
 template <typename Tin>
 __global__ void k_block_scan(const Tin* __restrict__ in, int64_t n, const uint64_t* __restrict__ offsets,
                              uint64_t* __restrict__ out, uint64_t* __restrict__ total) {
+    SS_PDL_WAIT();
     int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     uint64_t v[SCAN_ITEMS];
     uint64_t s = 0;
@@ -71,13 +73,14 @@ __global__ void k_block_scan(const Tin* __restrict__ in, int64_t n, const uint64
     if (total && blockIdx.x == gridDim.x - 1 && threadIdx.x == SCAN_THREADS - 1) *total = run;
 }
 
-__global__ void k_zero_u64(uint64_t* p) { *p = 0; }
+__global__ void k_zero_u64(uint64_t* p) {
+    SS_PDL_WAIT(); *p = 0; }
 
 template <typename Tin>
 int scan_impl(ss_ctx* ctx, const Tin* in, uint64_t* out, int64_t n, uint64_t* total) {
     if (n <= 0) {
         if (total) {
-            k_zero_u64<<<1, 1, 0, ctx->stream>>>(total);
+            SS_CUDA(ctx, ss_launch((k_zero_u64), dim3(1), dim3(1), 0, ctx->stream, total));
             SS_CHECK_LAUNCH(ctx);
         }
         return SS_OK;
@@ -88,11 +91,11 @@ int scan_impl(ss_ctx* ctx, const Tin* in, uint64_t* out, int64_t n, uint64_t* to
         uint64_t* sums = SS_SCRATCH(ctx, uint64_t, nb);
         offs = SS_SCRATCH(ctx, uint64_t, nb);
         if (!sums || !offs) return SS_ERR_CUDA;
-        k_block_sums<Tin><<<(unsigned)nb, SCAN_THREADS, 0, ctx->stream>>>(in, n, sums);
+        SS_CUDA(ctx, ss_launch((k_block_sums<Tin>), dim3((unsigned)nb), dim3(SCAN_THREADS), 0, ctx->stream, in, n, sums));
         SS_CHECK_LAUNCH(ctx);
         SS_TRY(scan_impl<uint64_t>(ctx, sums, offs, nb, nullptr));
     }
-    k_block_scan<Tin><<<(unsigned)nb, SCAN_THREADS, 0, ctx->stream>>>(in, n, offs, out, total);
+    SS_CUDA(ctx, ss_launch((k_block_scan<Tin>), dim3((unsigned)nb), dim3(SCAN_THREADS), 0, ctx->stream, in, n, offs, out, total));
     SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }

@@ -32,6 +32,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_hist_all(const K* __restrict__ keys, int64_t n, int key_bits,
                                                          uint32_t* __restrict__ hist) {
+    SS_PDL_WAIT();
     __shared__ uint32_t cnt[RS_MAX_PASSES][256];
     const int passes = (key_bits + 7) / 8;
     for (int p = 0; p < passes; ++p) cnt[p][threadIdx.x] = 0;
@@ -49,6 +50,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_hist_all(const K* __restrict__ k
 }
 
 __global__ void k_base_scan(const uint32_t* __restrict__ hist, int passes, uint64_t* __restrict__ base) {
+    SS_PDL_WAIT();
     // one warp per pass
     const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (p >= passes) return;
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ k
                                                          const uint64_t* __restrict__ digit_base,
                                                          uint32_t* __restrict__ part, unsigned* __restrict__ tile_ctr,
                                                          K* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+    SS_PDL_WAIT();
     constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
     __shared__ K s_keys[RS_TILE];
     __shared__ uint32_t s_vals[RS_TILE];
@@ -231,9 +234,9 @@ int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_
     SS_CUDA(ctx, cudaMemsetAsync(ctr, 0, sizeof(unsigned) * RS_MAX_PASSES, s));
     int hb = (int)((n + RS_THREADS * 16 - 1) / (RS_THREADS * 16));
     if (hb > ctx->num_sms * 8) hb = ctx->num_sms * 8;
-    k_hist_all<K><<<hb, RS_THREADS, 0, s>>>(keys, n, key_bits, hist);
+    SS_CUDA(ctx, ss_launch((k_hist_all<K>), dim3(hb), dim3(RS_THREADS), 0, s, keys, n, key_bits, hist));
     SS_CHECK_LAUNCH(ctx);
-    k_base_scan<<<1, 32 * RS_MAX_PASSES, 0, s>>>(hist, passes, base);
+    SS_CUDA(ctx, ss_launch((k_base_scan), dim3(1), dim3(32 * RS_MAX_PASSES), 0, s, hist, passes, base));
     SS_CHECK_LAUNCH(ctx);
     K* src_k = keys;
     uint32_t* src_v = vals;
@@ -243,8 +246,8 @@ int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_
         const int shift = 8 * p;
         const int bits = key_bits - shift < 8 ? key_bits - shift : 8;
         const unsigned mask = (1u << bits) - 1u;
-        k_onesweep<K, RS_ITEMS><<<(unsigned)tiles, RS_THREADS, 0, s>>>(src_k, src_v, n, shift, mask, base + p * 256,
-                                                             part + (int64_t)p * tiles * 256, ctr + p, dst_k, dst_v);
+        SS_CUDA(ctx, ss_launch((k_onesweep<K, RS_ITEMS>), dim3((unsigned)tiles), dim3(RS_THREADS), 0, s, src_k, src_v, n, shift, mask, base + p * 256,
+                                                             part + (int64_t)p * tiles * 256, ctr + p, dst_k, dst_v));
         SS_CHECK_LAUNCH(ctx);
         K* tk = src_k; src_k = dst_k; dst_k = tk;
         uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
