@@ -22,6 +22,7 @@ struct AdamConst {
 __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float* __restrict__ quats,
                        float* __restrict__ logits, float* __restrict__ sh, double* __restrict__ m,
                        double* __restrict__ v, const float* __restrict__ g, AdamConst c) {
+    SS_PDL_WAIT();
     const int64_t a = c.a, total = a * (11 + 3 * (int64_t)c.B);
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         float* p;
@@ -57,6 +58,7 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
 
 __global__ void k_adam_rows(float* __restrict__ quats, const float* __restrict__ g, double* __restrict__ ema,
                             int64_t* __restrict__ age, AdamConst c) {
+    SS_PDL_WAIT();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.a; i += (int64_t)gridDim.x * blockDim.x) {
         float* q = quats + 4 * i;
         const double w = q[0], x = q[1], y = q[2], z = q[3];
@@ -105,12 +107,12 @@ extern "C" int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* st, con
     int64_t grid = (total + 255) / 256;
     if (grid > (int64_t)ctx->num_sms * 32) grid = (int64_t)ctx->num_sms * 32;
     ss_tic(ctx, KC_ADAM);
-    k_adam<<<(int)grid, 256, 0, ctx->stream>>>(model->means, model->log_scales, model->quaternions,
-                                                model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c);
+    SS_CUDA(ctx, ss_launch((k_adam), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales, model->quaternions,
+                                                model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c));
     SS_CHECK_LAUNCH(ctx);
     int64_t rg = (a + 255) / 256;
     if (rg > (int64_t)ctx->num_sms * 32) rg = (int64_t)ctx->num_sms * 32;
-    k_adam_rows<<<(int)rg, 256, 0, ctx->stream>>>(model->quaternions, grad, st->grad_ema, st->age, c);
+    SS_CUDA(ctx, ss_launch((k_adam_rows), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions, grad, st->grad_ema, st->age, c));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_ADAM);
     st->step_count = t;

@@ -542,7 +542,8 @@ __device__ void plan_job(const Job& J) {
 }
 
 // a residual job without rows (no scan block runs its plan)
-__global__ void __launch_bounds__(TK_THREADS) k_tick_plan(Batch B, int job) { plan_job(B.j[job]); }
+__global__ void __launch_bounds__(TK_THREADS) k_tick_plan(Batch B, int job) {
+    SS_PDL_WAIT(); plan_job(B.j[job]); }
 
 // ---------------------------------------------------------------- emit
 template <typename T>
@@ -810,6 +811,7 @@ __device__ __forceinline__ void scan_chunk(const Job& J, int64_t c) {
 }
 
 __global__ void __launch_bounds__(TK_THREADS) k_tick(Batch B, Phase P) {
+    SS_PDL_WAIT();
     const int64_t b = blockIdx.x;
     if (b < P.emit_chunks) {
         const int64_t chunk = P.emit_chunk0 + b;
@@ -918,17 +920,17 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
     for (int i = 0; i < njobs; ++i) (B.j[i].residual ? res_chunks : abs_chunks) += B.j[i].nchunks;
     if (res_chunks) {
         Phase P{0, 0, abs_chunks, res_chunks};
-        k_tick<<<(unsigned)res_chunks, TK_THREADS, 0, ctx->stream>>>(B, P);
+        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)res_chunks), dim3(TK_THREADS), 0, ctx->stream, B, P));
         SS_CHECK_LAUNCH(ctx);
     }
     for (int i = 0; i < njobs; ++i)
         if (B.j[i].residual && B.j[i].nchunks == 0) {  // no scan block: plan it here
-            k_tick_plan<<<1, TK_THREADS, 0, ctx->stream>>>(B, i);
+            SS_CUDA(ctx, ss_launch((k_tick_plan), dim3(1), dim3(TK_THREADS), 0, ctx->stream, B, i));
             SS_CHECK_LAUNCH(ctx);
         }
     if (res_chunks + abs_chunks) {
         Phase P{abs_chunks, res_chunks, 0, abs_chunks};
-        k_tick<<<(unsigned)(res_chunks + abs_chunks), TK_THREADS, 0, ctx->stream>>>(B, P);
+        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)(res_chunks + abs_chunks)), dim3(TK_THREADS), 0, ctx->stream, B, P));
         SS_CHECK_LAUNCH(ctx);
     }
     // jobs with zero rows and no chunk still need their header
