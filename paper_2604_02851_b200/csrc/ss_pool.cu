@@ -100,17 +100,35 @@ __global__ void k_gather_col(const T* __restrict__ src, T* __restrict__ dst, con
 // ---------------------------------------------------------------- grid
 __global__ void k_cells(const float* __restrict__ means, int64_t n, ss_grid_spec g, int64_t* __restrict__ cells,
                         unsigned long long* __restrict__ mm) {
+    SS_PDL_WAIT();
+    // per-axis min / max of the order-preserving offsets: thread -> warp -> one atomic per block and value
+    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t c[3];
         cell_of(means + 3 * i, g.origin, g.cell_size, c);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             cells[3 * i + k] = c[k];
-            const unsigned long long o = (unsigned long long)(c[k] + (1ll << 62));  // order-preserving offset
-            atomicMin(&mm[k], o);
-            atomicMax(&mm[3 + k], o);
+            const unsigned long long o = (unsigned long long)(c[k] + (1ll << 62));
+            lo[k] = o < lo[k] ? o : lo[k];
+            hi[k] = o > hi[k] ? o : hi[k];
         }
     }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo[k], off);
+            const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi[k], off);
+            lo[k] = a < lo[k] ? a : lo[k];
+            hi[k] = b > hi[k] ? b : hi[k];
+        }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (lo[k] != ~0ull) atomicMin(&mm[k], lo[k]);
+            if (hi[k]) atomicMax(&mm[3 + k], hi[k]);
+        }
 }
 
 __global__ void k_cell_keys(const int64_t* __restrict__ cells, int64_t n, const unsigned long long* __restrict__ mm,
