@@ -82,7 +82,6 @@ struct Batch {
 __device__ __forceinline__ double q_dm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double q_da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double q_ds(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double q_dd(double a, double b) { return __ddiv_rn(a, b); }
 
 // Correctly rounded a / b from y = RN(1/b): q = RN(a y), r = a - b q (exact
 // by FMA), RN(q + r y) = RN(a / b)  (Markstein's theorem; our quotients are
@@ -113,14 +112,7 @@ __device__ __forceinline__ double dequant(uint32_t code, const QParams& p) {
     return q_da(p.lo, q_dm(div_rn((double)code, p.levels, p.inv_levels), p.dspan));
 }
 
-// the code as an integer-valued double (skips the int round trip when the
-// dequantised value is needed right away)
-__device__ __forceinline__ double quant_d(double v, const QParams& p) {
-    const double c = np_min(np_max(v, p.lo), p.hi);
-    double t = div_rn(q_ds(c, p.lo), p.span, p.inv_span);
-    if (!(p.hi >= p.lo)) t = np_min(np_max(t, 0.0), 1.0);
-    return rint(q_dm(t, p.levels));
-}
+// dequantised value of an integer-valued code held as a double
 __device__ __forceinline__ double dequant_d(double cd, const QParams& p) {
     return q_da(p.lo, q_dm(div_rn(cd, p.levels, p.inv_levels), p.dspan));
 }
