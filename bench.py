@@ -385,13 +385,27 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
+        # The loss is read back like the payloads: an async copy into pinned
+        # memory collected one step later (the last one inside the region), so
+        # the host never stalls the stream between steps.
+        loss_h = torch.zeros(2, dtype=torch.float64).pin_memory()
+        loss_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        losses = []
         for i in range(args.steps):
-            step(dm, state, hviews, process_group=pg, total_views=args.views, workspace=ws)
+            lt = step(dm, state, hviews, process_group=pg, total_views=args.views, workspace=ws, sync_loss=False)
+            loss_h[i % 2:i % 2 + 1].copy_(lt, non_blocking=True)
+            loss_ev[i % 2].record()
+            if i > 0:
+                loss_ev[(i - 1) % 2].synchronize()
+                losses.append(float(loss_h[(i - 1) % 2]))
             _, nb = delta_tick(i, device_only=False)
             d2h += nb + 8
         if pend[0] is not None:  # the last tick's payloads, inside the timed region
             d2h += sum(len(p) for p in pend[0].result(copy=False))
             pend[0] = None
+        loss_ev[(args.steps - 1) % 2].synchronize()
+        losses.append(float(loss_h[(args.steps - 1) % 2]))
+        assert len(losses) == args.steps and all(np.isfinite(losses))
         e1.record()
         torch.cuda.synchronize()
         ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
