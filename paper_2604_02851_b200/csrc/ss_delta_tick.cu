@@ -1,16 +1,15 @@
 // Batched delta encoder: one server tick's attribute deltas (ref
-// pkg/src/splatstream/server.py:488-493 -> protocol/delta.py:72-137) in three
-// launches, whatever the number of attributes:
+// pkg/src/splatstream/server.py:488-493 -> protocol/delta.py:72-137) in two
+// launches of k_tick, whatever the number of attributes:
 //
-//   k_tick_scan   every (job, 2048-row chunk): residual jobs -> chunk stats
-//                 (kept rows, max|r| over all / kept rows, first / last kept
-//                 row, varint bytes of the chunk's internal gaps); absolute
-//                 jobs -> quantize + pack straight into the payload
-//   k_tick_plan   one block per residual job: mode decision (k < rows/2),
-//                 f32 range m, per-chunk prefixes (survivors, varint bytes,
-//                 last kept row before the chunk), header, payload length
-//   k_tick_emit   residual jobs: dense quantize, or sparse varint gaps +
-//                 codes; advanced baseline f32(f64(base) + deq)
+//   launch 1  every residual (job, 2048-row chunk): chunk stats (kept rows,
+//             max|r| over all / kept rows, first / last kept row, varint
+//             bytes of the chunk's internal gaps); the last chunk of a job to
+//             finish plans it (mode k < rows/2, f32 range m, per-chunk
+//             prefixes, header, payload length).  Then every absolute
+//             (job, chunk): quantize + pack straight into the payload.
+//   launch 2  every residual (job, chunk): dense quantize, or sparse varint
+//             gaps + codes; advanced baseline f32(f64(base) + deq)
 //
 // Inputs may be strided views of the model (SH DC / SH rest are read in place
 // from the (N, 3, B) coefficient array).  Arithmetic is the bit-exact float64
@@ -873,12 +872,12 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         J.nchunks = (s.rows + TK_CHUNK - 1) / TK_CHUNK;
         if (J.residual) any_resid = true;
     }
-    // absolute jobs' chunks first, residual last: the residual inputs are then
-    // the most recently read data when k_tick_emit re-reads them (L2 hits)
+    // residual jobs' chunks first, absolute after: launch 1 runs the residual
+    // scans and then the absolute jobs, whose streaming overlaps the plan tail
     for (int pass = 0; pass < 2; ++pass)
         for (int i = 0; i < njobs; ++i) {
             Job& J = B.j[i];
-            if (J.residual != pass) continue;
+            if (J.residual != 1 - pass) continue;
             J.chunk0 = chunks;
             chunks += J.nchunks;
         }
@@ -905,14 +904,14 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         scratch += 1;
     }
     ss_tic(ctx, KC_CODEC);
-    // two launches: [scan of every residual job] (each job's last block
-    // plans it), then [emit of every residual job + every absolute job]; the
-    // emit re-reads the residual inputs (24 B/row) from L2
+    // two launches: [scan of every residual job (each job's last block plans
+    // it) + every absolute job], then [emit of every residual job]; the emit
+    // re-reads the residual inputs (24 B/row), partly from L2
     int64_t abs_chunks = 0, res_chunks = 0;
     for (int i = 0; i < njobs; ++i) (B.j[i].residual ? res_chunks : abs_chunks) += B.j[i].nchunks;
-    if (res_chunks) {
-        Phase P{0, 0, abs_chunks, res_chunks};
-        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)res_chunks), dim3(TK_THREADS), 0, ctx->stream, B, P));
+    if (res_chunks + abs_chunks) {  // residual chunks are [0, res), absolute [res, res + abs)
+        Phase P{0, 0, 0, res_chunks + abs_chunks};
+        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)(res_chunks + abs_chunks)), dim3(TK_THREADS), 0, ctx->stream, B, P));
         SS_CHECK_LAUNCH(ctx);
     }
     for (int i = 0; i < njobs; ++i)
@@ -920,9 +919,9 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
             SS_CUDA(ctx, ss_launch((k_tick_plan), dim3(1), dim3(TK_THREADS), 0, ctx->stream, B, i));
             SS_CHECK_LAUNCH(ctx);
         }
-    if (res_chunks + abs_chunks) {
-        Phase P{abs_chunks, res_chunks, 0, abs_chunks};
-        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)(res_chunks + abs_chunks)), dim3(TK_THREADS), 0, ctx->stream, B, P));
+    if (res_chunks) {
+        Phase P{0, res_chunks, 0, 0};
+        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)res_chunks), dim3(TK_THREADS), 0, ctx->stream, B, P));
         SS_CHECK_LAUNCH(ctx);
     }
     // jobs with zero rows and no chunk still need their header
