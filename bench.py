@@ -504,7 +504,7 @@ def encoder_bench(c, _lib, args, torch, reps=20):
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "traffic": committed_traffic("delta_encode"), "traffic_unit": "bytes/tick (ncu, profiles/)",
                         "algorithmic_bytes_per_tick": bytes_per_row * a, "bytes_per_row": bytes_per_row,
-                        "note": "achieved = algorithmic bytes / kernel time of the tick's 2 launches"}}
+                        "note": "achieved = algorithmic bytes / kernel time of the tick's launch"}}
     out["client_apply"] = ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch)
     del dm
     return out

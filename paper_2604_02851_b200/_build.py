@@ -48,6 +48,7 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> pathlib.Path:
     sources = sorted(CSRC.glob("*.cu"))
     headers = sorted(CSRC.glob("*.cuh")) + sorted((ROOT / "include").glob("*.h"))
     extra = ["-Xptxas", "-v"] if verbose_ptxas else []
+    extra += os.environ.get("SS_NVCC_EXTRA", "").split()  # experiments: -D overrides of tuning constants
     cc = nvcc()
 
     def compile_one(src: pathlib.Path):

@@ -1,15 +1,22 @@
 // Batched delta encoder: one server tick's attribute deltas (ref
-// pkg/src/splatstream/server.py:488-493 -> protocol/delta.py:72-137) in two
-// launches of k_tick, whatever the number of attributes:
+// pkg/src/splatstream/server.py:488-493 -> protocol/delta.py:72-137) in ONE
+// launch of k_tick_fused, whatever the number of attributes.  Blocks, in
+// dispatch order:
 //
-//   launch 1  every residual (job, 2048-row chunk): chunk stats (kept rows,
-//             max|r| over all / kept rows, first / last kept row, varint
-//             bytes of the chunk's internal gaps); the last chunk of a job to
-//             finish plans it (mode k < rows/2, f32 range m, per-chunk
-//             prefixes, header, payload length).  Then every absolute
-//             (job, chunk): quantize + pack straight into the payload.
-//   launch 2  every residual (job, chunk): dense quantize, or sparse varint
-//             gaps + codes; advanced baseline f32(f64(base) + deq)
+//   residual scans  every residual (job, 2048-row chunk): chunk stats (kept
+//                   rows, max|r| over all / kept rows, first / last kept row,
+//                   varint bytes of the chunk's internal gaps); the last chunk
+//                   of a job to finish plans it (mode k < rows/2, f32 range m,
+//                   per-chunk prefixes, header, payload length) and releases
+//                   the job's flag
+//   absolute jobs   every absolute (job, chunk): quantize + pack straight
+//                   into the payload (covers the plan tail)
+//   residual emits  wait for their job's flag, then dense quantize, or sparse
+//                   varint gaps + codes; advanced baseline f32(f64(base) + deq)
+//
+// The emit blocks' wait relies on in-order block dispatch (every scan block
+// is resident or done before any emit block starts), the same forward-progress
+// assumption as the radix sort's decoupled look-back.
 //
 // Inputs may be strided views of the model (SH DC / SH rest are read in place
 // from the (N, 3, B) coefficient array).  Arithmetic is the bit-exact float64
@@ -23,7 +30,10 @@ constexpr int TK_THREADS = 256;
 constexpr int TK_ITEMS = 8;
 constexpr int TK_CHUNK = TK_THREADS * TK_ITEMS;  // rows per block
 constexpr int TK_MAX_JOBS = 8;
-constexpr int EMIT_U = 3;  // float4 steps in flight per thread: 3 x 2 rounds = a full dims-3 chunk
+#ifndef EMIT_U
+#define EMIT_U 3
+#endif
+// EMIT_U: float4 steps in flight per thread: 3 x 2 rounds = a full dims-3 chunk
 
 struct QParams {
     double lo, hi, span, inv_span, levels, inv_levels, dspan;  // dspan = hi - lo (dequantizer)
@@ -530,6 +540,25 @@ __device__ void plan_job(const Job& J) {
         *J.out_len = h + 4 + blen;
         J.var_pre[J.nchunks] = V;  // total varint bytes (sparse code offset)
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // planned: release the job to its emit blocks
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&J.g[2]), "l"(1ull) : "memory");
+    }
+}
+
+// an emit block of the fused launch waits for its job's plan
+__device__ __forceinline__ void wait_planned(const Job& J) {
+    unsigned long long f;
+    if (threadIdx.x == 0) {
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(&J.g[2]) : "memory");
+            if (f) break;
+            __nanosleep(256);
+        }
+    }
+    __syncthreads();
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(&J.g[2]) : "memory");
 }
 
 // a residual job without rows (no scan block runs its plan)
@@ -744,12 +773,6 @@ __device__ __forceinline__ void emit_sparse(const Job& J, const QParams& rq, int
 // One launch = [emit blocks of one residual job] + [scan blocks of the next
 // residual job, or of every absolute job].  The emit part reads the plan the
 // previous launch's last scan block wrote.
-struct Phase {
-    int64_t emit_chunk0;   // global chunk of the first emit block
-    int64_t emit_chunks;
-    int64_t scan_chunk0;   // global chunk of the first scan block
-    int64_t scan_chunks;
-};
 
 __device__ __forceinline__ void emit_chunk(const Job& J, int64_t c) {
     const int64_t r0 = c * TK_CHUNK;
@@ -801,18 +824,24 @@ __device__ __forceinline__ void scan_chunk(const Job& J, int64_t c) {
     }
 }
 
-__global__ void __launch_bounds__(TK_THREADS) k_tick(Batch B, Phase P) {
+#ifndef TK_EMIT_MINB
+#define TK_EMIT_MINB 3  // <= 80 registers: 3 blocks per SM
+#endif
+// one launch: [residual scans][absolute jobs][residual emits]; the emit
+// blocks are dispatched after every scan block and wait on their job's plan
+// flag (the absolute jobs in between cover the plan tail)
+__global__ void __launch_bounds__(TK_THREADS, TK_EMIT_MINB) k_tick_fused(Batch B, int64_t scan_chunks) {
     SS_PDL_WAIT();
     const int64_t b = blockIdx.x;
-    if (b < P.emit_chunks) {
-        const int64_t chunk = P.emit_chunk0 + b;
-        const Job& J = B.j[find_job(B, chunk)];
-        emit_chunk(J, chunk - J.chunk0);
+    if (b < scan_chunks) {
+        const Job& J = B.j[find_job(B, b)];
+        scan_chunk(J, b - J.chunk0);
         return;
     }
-    const int64_t chunk = P.scan_chunk0 + (b - P.emit_chunks);
+    const int64_t chunk = b - scan_chunks;
     const Job& J = B.j[find_job(B, chunk)];
-    scan_chunk(J, chunk - J.chunk0);
+    wait_planned(J);
+    emit_chunk(J, chunk - J.chunk0);
 }
 
 }  // namespace
@@ -904,24 +933,19 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         scratch += 1;
     }
     ss_tic(ctx, KC_CODEC);
-    // two launches: [scan of every residual job (each job's last block plans
-    // it) + every absolute job], then [emit of every residual job]; the emit
-    // re-reads the residual inputs (24 B/row), partly from L2
+    // one launch: [scan of every residual job (each job's last block plans
+    // it)][every absolute job][emit of every residual job]; the emit re-reads
+    // the residual inputs (24 B/row), partly from L2
     int64_t abs_chunks = 0, res_chunks = 0;
     for (int i = 0; i < njobs; ++i) (B.j[i].residual ? res_chunks : abs_chunks) += B.j[i].nchunks;
-    if (res_chunks + abs_chunks) {  // residual chunks are [0, res), absolute [res, res + abs)
-        Phase P{0, 0, 0, res_chunks + abs_chunks};
-        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)(res_chunks + abs_chunks)), dim3(TK_THREADS), 0, ctx->stream, B, P));
-        SS_CHECK_LAUNCH(ctx);
-    }
     for (int i = 0; i < njobs; ++i)
         if (B.j[i].residual && B.j[i].nchunks == 0) {  // no scan block: plan it here
             SS_CUDA(ctx, ss_launch((k_tick_plan), dim3(1), dim3(TK_THREADS), 0, ctx->stream, B, i));
             SS_CHECK_LAUNCH(ctx);
         }
-    if (res_chunks) {
-        Phase P{0, res_chunks, 0, 0};
-        SS_CUDA(ctx, ss_launch((k_tick), dim3((unsigned)res_chunks), dim3(TK_THREADS), 0, ctx->stream, B, P));
+    if (res_chunks + abs_chunks) {  // residual chunks are [0, res), absolute [res, res + abs)
+        SS_CUDA(ctx, ss_launch((k_tick_fused), dim3((unsigned)(2 * res_chunks + abs_chunks)), dim3(TK_THREADS), 0, ctx->stream, B,
+                               res_chunks + abs_chunks));
         SS_CHECK_LAUNCH(ctx);
     }
     // jobs with zero rows and no chunk still need their header
