@@ -306,8 +306,10 @@ def run_ours(args):
         due = [attr for attr in DELTA_ORDER if tick % DELTA_PERIODS[attr] == 0]
         if device_only:  # one batched library call, payloads stay in HBM
             return ticker(due), 0
-        ticker(due)  # public API: batched encode, then every payload read back into pinned host memory
-        pending = ticker.read_async(due)  # collected after the next step is queued (one tick of latency)
+        # public API: batched encode, device CRC of each payload, then every
+        # TENSOR_DELTA frame (envelope + payload + CRC) assembled in pinned host memory
+        ticker(due)
+        pending = ticker.read_async(due, frame_epoch=1)  # collected after the next step is queued (one tick of latency)
         done, pend[0] = pend[0], pending
         return a * len(due), (sum(len(p) for p in done.result(copy=False)) if done is not None else 0)
 
@@ -412,7 +414,9 @@ def run_ours(args):
         if pg is not None:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": args.views * args.steps / (float(ems.item()) / 1e3), "unit": "views/s",
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h // args.steps}
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h // args.steps,
+               "path": "optim.step (ground truth H2D from pinned host memory, loss read back) + the tick's "
+                       "TENSOR_DELTA frames (device CRC-32) read back into pinned host memory"}
 
     if rank != 0:
         if pg is not None:

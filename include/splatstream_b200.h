@@ -238,6 +238,15 @@ int ss_encode_light_visibility(ss_ctx* ctx, const float* vis, int64_t n, uint8_t
 int ss_host_zlib_compress(const uint8_t* src, uint64_t n, uint8_t* dst, uint64_t cap, uint64_t* out_len);
 uint64_t ss_host_zlib_bound(uint64_t n);
 
+/* Frame envelope CRC (ref protocol/framing.py:51-53, zlib.crc32 of header +
+ * payload).  ss_crc32 writes zlib.crc32(data[:n]) of a
+ * DEVICE buffer to the device word *crc_out, n = min(*len_dev, len) when
+ * len_dev is given (a payload length left on the device by an encoder), else
+ * len; async on the context's stream.  ss_crc32_combine is host arithmetic
+ * (zlib crc32_combine): the CRC of A + B from crc32(A), crc32(B) and |B|. */
+int ss_crc32(ss_ctx* ctx, const uint8_t* data, const uint64_t* len_dev, uint64_t len, uint32_t* crc_out);
+uint32_t ss_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2);
+
 /* ---- dynamics ------------------------------------------------------------ */
 /* update_light_visibility(): ref render.py:350-368 with the orthographic
  * projection of ref geometry.py:267-271.  Writes model->light_visibility. */

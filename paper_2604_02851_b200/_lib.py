@@ -136,6 +136,8 @@ _SIGS = {
     "ss_encode_light_visibility": (i32, [vp, vp, i64, vp, u64, vp]),
     "ss_host_zlib_compress": (i32, [vp, u64, vp, u64, C.POINTER(u64)]),
     "ss_host_zlib_bound": (u64, [u64]),
+    "ss_crc32": (i32, [vp, vp, vp, u64, vp]),
+    "ss_crc32_combine": (C.c_uint32, [C.c_uint32, C.c_uint32, u64]),
     "ss_update_light_visibility": (i32, [vp, C.POINTER(SSModel), vp, C.POINTER(SSOrthoCamera), f64]),
     "ss_apply_object_transform": (i32, [vp, C.POINTER(SSModel), i32, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
     "ss_refresh_object_locals": (i32, [vp, C.POINTER(SSModel), i32, i32, vp, vp, C.POINTER(f64),

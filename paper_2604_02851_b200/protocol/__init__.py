@@ -85,6 +85,33 @@ def frame_bytes(ptype: int, epoch: int, payload: bytes) -> bytes:
     return MAGIC + body + struct.pack("<I", zlib.crc32(body))
 
 
+FRAME_HEAD = 2 + 9  # magic + '<BII' (ptype, epoch, length)
+FRAME_TAIL = 4      # '<I' CRC-32 of header + payload
+FRAME_OVERHEAD = FRAME_HEAD + FRAME_TAIL
+
+
+def crc32_combine(crc1: int, crc2: int, len2: int) -> int:
+    """zlib.crc32(A + B) from crc32(A), crc32(B) and len(B) (host arithmetic
+    in the library, no data access)."""
+    return int(_lib.load_library().ss_crc32_combine(crc1 & 0xFFFFFFFF, crc2 & 0xFFFFFFFF, int(len2)))
+
+
+def crc32_device(data, length=None):
+    """zlib.crc32 of a device uint8 tensor's first `length` bytes (an int, or
+    a device int64 scalar tensor such as PayloadBuffer.length; default: all),
+    computed on the GPU; returns a device int32 tensor (the CRC's bits)."""
+    import torch
+    c = _lib.ctx(data.device.index)
+    c.bind_stream()
+    out = torch.empty(1, dtype=torch.int32, device=data.device)
+    n = data.numel()
+    if isinstance(length, int):
+        n, length = min(n, length), None
+    c.check(c.lib.ss_crc32(c.handle, data.data_ptr(), length.data_ptr() if length is not None else None, n,
+                           out.data_ptr()))
+    return out
+
+
 def host_zlib(block: bytes) -> bytes:
     """The compression stage through the library's libz (compress2, level 6).
     No Python-side copies; ctypes releases the GIL for the call, so blocks
@@ -218,7 +245,7 @@ def encode_delta_device(attribute_id, current, baseline=None, new_baseline=None,
 
 class DeltaTicker:
     """One server tick's deltas for a DeviceModel in ONE library call
-    (two kernel launches, no host sync): attributes in emission order (ref
+    (one kernel launch, no host sync): attributes in emission order (ref
     server.py:67-74, 488-493), residual baselines advanced in place, payloads
     into `outs[attr]` (PayloadBuffer).  SH DC / SH rest are read in place from
     the (N, 3, B) coefficients.  The ctypes job array is built once per set of
@@ -282,15 +309,22 @@ class DeltaTicker:
         c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
         return self.model.active_count * len(key)
 
-    def read_async(self, attributes):
+    def read_async(self, attributes, frame_epoch=None):
         """Start reading the last call's payloads for `attributes` back without
         a host sync: lengths and each payload's bound-sized buffer are copied
         into pinned memory on the current stream; `.result()` waits for that
-        copy only (the GPU keeps running whatever was queued after it)."""
+        copy only (the GPU keeps running whatever was queued after it).
+
+        With `frame_epoch`, `.result()` returns TENSOR_DELTA frames instead
+        (ref framing.py:51-53): each payload lands in pinned memory between
+        its envelope header and CRC, and the CRC of the payload is computed on
+        the device (ss_crc32), so the host never reads the payload bytes."""
         import torch
         key = [int(x) for x in attributes]
         m = self.model
-        bounds = [int(self._ctx.lib.ss_delta_bound(a, m.active_count, self._dims(a))) for a in key]
+        frames = frame_epoch is not None
+        pad = FRAME_OVERHEAD if frames else 0
+        bounds = [int(self._ctx.lib.ss_delta_bound(a, m.active_count, self._dims(a))) + pad for a in key]
         need = sum(bounds)
         slot = getattr(self, "_slot", 0) ^ 1  # two pinned buffers: one may still be pending
         self._slot = slot
@@ -302,15 +336,30 @@ class DeltaTicker:
             st[2].synchronize()  # its previous reader has finished with it
         if st is None or st[0].numel() < need:
             st = bufs[slot] = (torch.empty(max(need, 1 << 16) * 5 // 4, dtype=torch.uint8, pin_memory=True),
-                               torch.empty(8, dtype=torch.int64, pin_memory=True), torch.cuda.Event())
-        host, lens, ev = st
+                               torch.empty(8, dtype=torch.int64, pin_memory=True), torch.cuda.Event(),
+                               torch.empty(8, dtype=torch.int32, pin_memory=True))
+        host, lens, ev, crcs = st
+        if frames:
+            dcrc = getattr(self, "_dcrc", None)
+            if dcrc is None:
+                dcrc = self._dcrc = torch.empty(8, dtype=torch.int32, device=m.device)
+            c = self._ctx
+            c.bind_stream()
         off = 0
         for i, (a, b) in enumerate(zip(key, bounds)):
-            host[off:off + b].copy_(self.outs[a].data[:b], non_blocking=True)
-            lens[i:i + 1].copy_(self.outs[a].length, non_blocking=True)
+            out = self.outs[a]
+            if frames:
+                c.check(c.lib.ss_crc32(c.handle, out.data.data_ptr(), out.length.data_ptr(), b - pad,
+                                       dcrc[i:].data_ptr()))
+            # payload bytes between the frame's header and CRC slots
+            host[off + (FRAME_HEAD if frames else 0):off + b - (FRAME_TAIL if frames else 0)].copy_(
+                out.data[:b - pad], non_blocking=True)
+            lens[i:i + 1].copy_(out.length, non_blocking=True)
             off += b
+        if frames:
+            crcs[:len(key)].copy_(dcrc[:len(key)], non_blocking=True)
         ev.record(torch.cuda.current_stream(m.device))
-        return _PendingPayloads(host, lens, ev, bounds)
+        return _PendingPayloads(host, lens, ev, bounds, crcs if frames else None, frame_epoch)
 
     def _dims(self, attr):
         m = self.model
@@ -345,19 +394,29 @@ class DeltaTicker:
 
 
 class _PendingPayloads:
-    """Payload bytes of one tick, copied back asynchronously (DeltaTicker.read_async)."""
+    """Payload bytes (or frames) of one tick, copied back asynchronously
+    (DeltaTicker.read_async)."""
 
-    def __init__(self, host, lens, ev, bounds):
-        self.host, self.lens, self.ev, self.bounds = host, lens, ev, bounds
+    def __init__(self, host, lens, ev, bounds, crcs=None, epoch=None):
+        self.host, self.lens, self.ev, self.bounds, self.crcs, self.epoch = host, lens, ev, bounds, crcs, epoch
 
     def result(self, copy: bool = True):
         self.ev.synchronize()
-        mv = memoryview(self.host.numpy())
+        hv = self.host.numpy()
+        mv = memoryview(hv)
         ln = self.lens.numpy()
         out, off = [], 0
         for i, b in enumerate(self.bounds):
             n = int(ln[i])
-            out.append(mv[off:off + n].tobytes() if copy else mv[off:off + n])
+            if self.crcs is None:
+                out.append(mv[off:off + n].tobytes() if copy else mv[off:off + n])
+            else:
+                head = struct.pack("<BII", int(PacketType.TENSOR_DELTA), self.epoch, n)
+                crc = crc32_combine(zlib.crc32(head), int(self.crcs[i]) & 0xFFFFFFFF, n)
+                hv[off:off + FRAME_HEAD] = np.frombuffer(MAGIC + head, np.uint8)
+                hv[off + FRAME_HEAD + n:off + FRAME_HEAD + n + FRAME_TAIL] = np.frombuffer(struct.pack("<I", crc), np.uint8)
+                k = FRAME_HEAD + n + FRAME_TAIL
+                out.append(mv[off:off + k].tobytes() if copy else mv[off:off + k])
             off += b
         return out
 
