@@ -571,7 +571,25 @@ def zlib_tick_bench(dm, base_m, base_l, torch, reps=3):
         ser = [P._recompress_delta(r, 1) for r in raws]
         t_ser += time.perf_counter() - t0
     assert ser == [p for _, p in out]
+    # frame envelope CRC of the raw stream's payloads: device (ss_crc32) vs host zlib.crc32
+    import zlib
+    base.means.copy_(ref_m)
+    base.log_scales.copy_(ref_l)
+    bufs = [em_raw._outs[int(at)] for at, _ in em_raw.tick(0)]  # the same payloads as `raws`, still in HBM
+    for b in bufs:
+        P.crc32_device(b.data, b.length)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dev_crc = [P.crc32_device(b.data, b.length) for b in bufs]
+    e1.record()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    host_crc = [zlib.crc32(r) for r in raws]
+    t_crc = time.perf_counter() - t0
+    assert [int(c.item()) & 0xFFFFFFFF for c in dev_crc] == host_crc
     return {"rows": a, "attributes": len(out), "raw_bytes": sum(len(r) for r in raws),
+            "frame_crc_us_device": e0.elapsed_time(e1) * 1e3, "frame_crc_ms_host_zlib": t_crc * 1e3,
             "zlib_bytes": sum(len(p) for _, p in out), "tick_ms_parallel_zlib": t_par * 1e3 / reps,
             "zlib_stage_ms_serial": t_ser * 1e3 / reps,
             "note": "tick = device encode + readback + per-attribute deflate on host threads (byte-identical)"}

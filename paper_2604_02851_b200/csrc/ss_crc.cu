@@ -92,6 +92,8 @@ __device__ __forceinline__ uint32_t crc_word(uint32_t s, uint32_t w, const uint3
 __global__ void __launch_bounds__(CRC_THREADS) k_crc32(const uint8_t* __restrict__ data, const uint64_t* __restrict__ len_dev,
                                                        uint64_t len, uint32_t* __restrict__ out, X2N x2n, XTab xt) {
     SS_PDL_WAIT();
+    const uint64_t n = len_dev ? min(*len_dev, len) : len;  // grids are sized for the bound
+    if (blockIdx.x && (uint64_t)blockIdx.x * CRC_THREADS * CRC_SEG >= n) return;
     __shared__ uint32_t T[4][256];
     __shared__ uint32_t s_x2n[64];
     __shared__ uint32_t s_acc[CRC_THREADS / 32];
@@ -112,7 +114,6 @@ __global__ void __launch_bounds__(CRC_THREADS) k_crc32(const uint8_t* __restrict
         T[j][t] = (p >> 8) ^ T[0][p & 0xffu];
         __syncthreads();
     }
-    const uint64_t n = len_dev ? min(*len_dev, len) : len;
     const uint64_t e = (uint64_t)blockIdx.x * CRC_THREADS + t;  // segment index from the end
     uint32_t contrib = 0;
     if (e * CRC_SEG < n) {
