@@ -362,6 +362,73 @@ int ss_grid_rebuild(ss_ctx* ctx, const float* means, int64_t n, const ss_grid_sp
  * packet before its zlib stage (ref protocol/packets.py:153-158). */
 int ss_zigzag_varints(ss_ctx* ctx, const int64_t* perm, int64_t n, uint8_t* out, uint64_t out_cap, uint64_t* len_out);
 
+/* ---- scene engine ------------------------------------- */
+/* The ray-cast game-engine stand-in: ref engine.py:88-205 (trace, shadow
+ * rays, Lambertian shading, render_ground_truth, capture_input_buffers,
+ * render_depth, render_ortho_depth) over the primitives of ref
+ * scene.py:28-161.  One thread per pixel, float64 mirroring the reference's
+ * numpy arithmetic.  Scene and camera are HOST structs; outputs are device
+ * buffers, every one optional. */
+#define SS_SHAPE_PLANE 0
+#define SS_SHAPE_SPHERE 1
+#define SS_SHAPE_BOX 2
+typedef struct {
+    int32_t shape;          /* SS_SHAPE_* */
+    int32_t object_id;
+    int32_t albedo_kind;    /* 0 solid, 1 checker (scene.py:152-158) */
+    int32_t has_extent;     /* plane: finite rectangle */
+    int32_t has_transform;  /* local -> world rigid transform applies */
+    int32_t _pad;
+    double a[3];            /* plane point | sphere centre | box centre */
+    double b[3];            /* plane unit normal | box half extents */
+    double radius;          /* sphere */
+    double extent[2];       /* plane half sizes along u, v */
+    double u[3], v[3];      /* plane tangents (scene.py:41-46, computed by the caller) */
+    double color[3], color2[3];
+    double scale;           /* checker cell size */
+    double R[9];            /* local -> world rotation, row-major (quat_to_rotmat of the transform) */
+    double t[3];            /* local -> world translation */
+} ss_scene_object;
+
+typedef struct {
+    const ss_scene_object* objects;  /* host array, scene order */
+    int32_t n_objects;
+    int32_t _pad;
+    double light_direction[3];       /* unit, from the light into the scene */
+    double light_intensity[3];
+    double ambient[3];
+    double background[3];
+} ss_scene;
+
+typedef struct {
+    int32_t kind;                    /* 0 pinhole (geometry.py:238), 1 orthographic (geometry.py:273) */
+    int32_t width, height;
+    int32_t _pad;
+    double position[3];
+    double R[9];                     /* camera -> world rotation, row-major */
+    double fx, fy, cx, cy;           /* pinhole */
+    double half_width, half_height;  /* orthographic */
+    double far;                      /* depth_or_far where a ray misses */
+    double footprint_scale;          /* 2 tan(fov_y / 2) / height (capture buffers) */
+} ss_engine_camera;
+
+typedef struct {  /* (H, W[, 3]) row-major device buffers; NULL = not written */
+    float* gt_f32;          /* render_ground_truth as float32 (the optimiser's ground truth) */
+    double* gt_f64;         /* render_ground_truth */
+    double* depth_or_far;   /* pinhole: render_depth; orthographic: render_ortho_depth */
+    double* world_pos;      /* capture_input_buffers channels (engine.py:161-189) */
+    uint8_t* valid;
+    double* normal;
+    double* albedo;
+    double* shaded;
+    int32_t* object_id;
+    double* depth;
+    double* footprint;
+    uint8_t* lit;
+} ss_engine_out;
+
+int ss_engine_render(ss_ctx* ctx, const ss_scene* scene, const ss_engine_camera* cam, const ss_engine_out* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -104,6 +104,28 @@ class SSGridSpec(C.Structure):
     _fields_ = [("origin", f64 * 3), ("cell_size", f64)]
 
 
+class SSSceneObject(C.Structure):
+    _fields_ = [("shape", i32), ("object_id", i32), ("albedo_kind", i32), ("has_extent", i32), ("has_transform", i32),
+                ("_pad", i32), ("a", f64 * 3), ("b", f64 * 3), ("radius", f64), ("extent", f64 * 2), ("u", f64 * 3),
+                ("v", f64 * 3), ("color", f64 * 3), ("color2", f64 * 3), ("scale", f64), ("R", f64 * 9), ("t", f64 * 3)]
+
+
+class SSScene(C.Structure):
+    _fields_ = [("objects", C.POINTER(SSSceneObject)), ("n_objects", i32), ("_pad", i32), ("light_direction", f64 * 3),
+                ("light_intensity", f64 * 3), ("ambient", f64 * 3), ("background", f64 * 3)]
+
+
+class SSEngineCamera(C.Structure):
+    _fields_ = [("kind", i32), ("width", i32), ("height", i32), ("_pad", i32), ("position", f64 * 3), ("R", f64 * 9),
+                ("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64), ("half_width", f64), ("half_height", f64),
+                ("far", f64), ("footprint_scale", f64)]
+
+
+class SSEngineOut(C.Structure):
+    _fields_ = [(n, vp) for n in ("gt_f32", "gt_f64", "depth_or_far", "world_pos", "valid", "normal", "albedo",
+                                  "shaded", "object_id", "depth", "footprint", "lit")]
+
+
 class SSOrthoCamera(C.Structure):
     _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("half_width", f64), ("half_height", f64),
                 ("width", i32), ("height", i32)]
@@ -147,6 +169,7 @@ _SIGS = {
     "ss_decode_snapshot": (i32, [vp, C.POINTER(SSSnapshotDecode)]),
     "ss_select_rows": (i32, [vp, C.POINTER(SSSelect), vp, C.POINTER(i64)]),
     "ss_gather_rows": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSModel), vp, i64, C.POINTER(SSModel)]),
+    "ss_engine_render": (i32, [vp, C.POINTER(SSScene), C.POINTER(SSEngineCamera), C.POINTER(SSEngineOut)]),
     "ss_grid_rebuild": (i32, [vp, vp, i64, C.POINTER(SSGridSpec), vp, vp, vp, vp, C.POINTER(i64)]),
     "ss_zigzag_varints": (i32, [vp, vp, i64, vp, u64, C.POINTER(u64)]),
 }

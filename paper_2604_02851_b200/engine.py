@@ -1,0 +1,239 @@
+"""Ray-cast scene engine on the GPU: the game-engine
+stand-in that renders the optimiser's ground truth and the expansion inputs.
+
+Drop-in for ref engine.py: `render_ground_truth` (engine.py:151),
+`capture_input_buffers` (engine.py:161), `render_depth` (engine.py:192),
+`render_ortho_depth` (engine.py:200) with the reference's signatures and host
+numpy results, plus `render_ground_truth_device`, which leaves a float32
+(H, W, 3) image in HBM for `optim.ReferenceView` (no host round trip in a
+live loop).  One library call (`ss_engine_render`, one kernel) per image;
+scenes are duck-typed (the reference's SceneDescription or
+paper_2604_02851_b200.scene).  `build_dome_rig` / `build_light_camera` are
+host camera-rig helpers (ref engine.py:208-246).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .geometry import CameraIntrinsics, OrthoCamera, look_at, quat_to_rotmat
+
+GOLDEN_ANGLE = np.pi * (3.0 - np.sqrt(5.0))
+
+
+@dataclass
+class InputBuffers:
+    """Per-pixel engine channels of one input camera (ref engine.py:36-51)."""
+
+    pose: object
+    intrinsics: object
+    world_pos: np.ndarray
+    valid: np.ndarray
+    normal: np.ndarray
+    albedo: np.ndarray
+    shaded: np.ndarray
+    object_id: np.ndarray
+    depth: np.ndarray
+    footprint: np.ndarray
+    lit: np.ndarray
+
+
+def _shape_kind(shape):
+    if hasattr(shape, "radius"):
+        return 1
+    if hasattr(shape, "half_extents"):
+        return 2
+    if hasattr(shape, "normal"):
+        return 0
+    raise TypeError(f"unsupported shape {type(shape).__name__}")
+
+
+def _tangents(shape):
+    if hasattr(shape, "tangents"):
+        return shape.tangents()
+    n = np.asarray(shape.normal, np.float64)  # ref scene.py:41-46
+    helper = np.array([1.0, 0, 0]) if abs(n[1]) > 0.9 else np.array([0, 1.0, 0])
+    u = np.cross(helper, n)
+    u = u / np.linalg.norm(u)
+    return u, np.cross(n, u)
+
+
+def scene_struct(scene, light=None, transforms=None):
+    """(SSScene, keep-alive) for a scene; `transforms` {object_id: (q, t)}
+    places dynamic objects (ref engine.py:81-84, 99-107)."""
+    objs = scene.objects
+    arr = (_lib.SSSceneObject * max(1, len(objs)))()
+    for k, ob in enumerate(objs):
+        s = arr[k]
+        sh = ob.shape
+        s.shape = _shape_kind(sh)
+        s.object_id = int(ob.object_id)
+        if s.shape == 0:
+            s.a[:] = [float(x) for x in sh.point]
+            s.b[:] = [float(x) for x in sh.normal]
+            if sh.extent is not None:
+                s.has_extent = 1
+                s.extent[:] = [float(sh.extent[0]), float(sh.extent[1])]
+                u, v = _tangents(sh)
+                s.u[:] = [float(x) for x in u]
+                s.v[:] = [float(x) for x in v]
+        elif s.shape == 1:
+            s.a[:] = [float(x) for x in sh.center]
+            s.radius = float(sh.radius)
+        else:
+            s.a[:] = [float(x) for x in sh.center]
+            s.b[:] = [float(x) for x in sh.half_extents]
+        al = ob.albedo
+        s.albedo_kind = 0 if al.kind == "solid" else 1
+        s.color[:] = [float(x) for x in al.color]
+        s.color2[:] = [float(x) for x in al.color2]
+        s.scale = float(al.scale)
+        if ob.object_id > 0 and transforms and ob.object_id in transforms:
+            q, t = transforms[ob.object_id]
+            s.has_transform = 1
+            s.R[:] = [float(x) for x in np.asarray(quat_to_rotmat(q), np.float64).reshape(-1)]
+            s.t[:] = [float(x) for x in np.asarray(t, np.float64)]
+    lt = light if light is not None else scene.light
+    sc = _lib.SSScene()
+    sc.objects = C.cast(arr, C.POINTER(_lib.SSSceneObject))
+    sc.n_objects = len(objs)
+    sc.light_direction[:] = [float(x) for x in lt.direction]
+    sc.light_intensity[:] = [float(x) for x in lt.intensity]
+    sc.ambient[:] = [float(x) for x in lt.ambient]
+    sc.background[:] = [float(x) for x in scene.background]
+    return sc, arr
+
+
+def _pinhole(pose, intr):
+    cam = _lib.SSEngineCamera()
+    cam.kind = 0
+    cam.width, cam.height = int(intr.width), int(intr.height)
+    cam.position[:] = [float(x) for x in np.asarray(pose.position, np.float64)]
+    cam.R[:] = [float(x) for x in np.asarray(pose.rotation(), np.float64).reshape(-1)]
+    cam.fx, cam.fy, cam.cx, cam.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
+    cam.far = float(intr.far)
+    cam.footprint_scale = float(2.0 * np.tan(intr.fov_y / 2.0) / intr.height)  # ref engine.py:167
+    return cam
+
+
+def _ortho(oc):
+    cam = _lib.SSEngineCamera()
+    cam.kind = 1
+    cam.width, cam.height = int(oc.width), int(oc.height)
+    cam.position[:] = [float(x) for x in np.asarray(oc.pose.position, np.float64)]
+    cam.R[:] = [float(x) for x in np.asarray(oc.pose.rotation(), np.float64).reshape(-1)]
+    cam.half_width, cam.half_height, cam.far = float(oc.half_width), float(oc.half_height), float(oc.far)
+    return cam
+
+
+def _run(scene, cam, bufs, light=None, transforms=None, device=None):
+    c = _lib.ctx(device)
+    c.bind_stream()
+    sc, keep = scene_struct(scene, light, transforms)
+    out = _lib.SSEngineOut()
+    for k, t in bufs.items():
+        setattr(out, k, t.data_ptr())
+    c.check(c.lib.ss_engine_render(c.handle, C.byref(sc), C.byref(cam), C.byref(out)))
+    del keep
+
+
+def _dev(device):
+    import torch
+    return torch.device("cuda", torch.cuda.current_device() if device is None else device)
+
+
+def render_ground_truth_device(scene, pose, intr, light=None, transforms=None, device=None, out=None):
+    """(H, W, 3) float32 ground truth in HBM (ref engine.py:151-158, cast
+    to float32 as the optimiser's views hold it).  `out` may be reused."""
+    import torch
+    dev = _dev(device)
+    if out is None:
+        out = torch.empty((intr.height, intr.width, 3), dtype=torch.float32, device=dev)
+    _run(scene, _pinhole(pose, intr), {"gt_f32": out}, light, transforms, dev.index)
+    return out
+
+
+def render_ground_truth(scene, pose, intr, light=None, transforms=None, device=None) -> np.ndarray:
+    """ref engine.py:151: (H, W, 3) float64, clipped to [0, 1]."""
+    import torch
+    dev = _dev(device)
+    img = torch.empty((intr.height, intr.width, 3), dtype=torch.float64, device=dev)
+    _run(scene, _pinhole(pose, intr), {"gt_f64": img}, light, transforms, dev.index)
+    return img.cpu().numpy()
+
+
+def capture_input_buffers(scene, pose, intr, light=None, transforms=None, device=None, as_tensors=False):
+    """ref engine.py:161-189: every channel of one input camera (host numpy,
+    or device tensors with `as_tensors`)."""
+    import torch
+    dev = _dev(device)
+    H, W = intr.height, intr.width
+    f64 = dict(dtype=torch.float64, device=dev)
+    b = {"world_pos": torch.empty((H, W, 3), **f64), "valid": torch.empty((H, W), dtype=torch.uint8, device=dev),
+         "normal": torch.empty((H, W, 3), **f64), "albedo": torch.empty((H, W, 3), **f64),
+         "shaded": torch.empty((H, W, 3), **f64), "object_id": torch.empty((H, W), dtype=torch.int32, device=dev),
+         "depth": torch.empty((H, W), **f64), "footprint": torch.empty((H, W), **f64),
+         "lit": torch.empty((H, W), dtype=torch.uint8, device=dev)}
+    _run(scene, _pinhole(pose, intr), b, light, transforms, dev.index)
+    if as_tensors:
+        b["valid"] = b["valid"].bool()
+        b["lit"] = b["lit"].bool()
+        return InputBuffers(pose=pose, intrinsics=intr, **b)
+    h = {k: v.cpu().numpy() for k, v in b.items()}
+    h["valid"] = h["valid"].astype(bool)
+    h["lit"] = h["lit"].astype(bool)
+    return InputBuffers(pose=pose, intrinsics=intr, **h)
+
+
+def render_depth(scene, pose, intr, transforms=None, device=None) -> np.ndarray:
+    """ref engine.py:192-197: camera-space z per pixel, intr.far where no hit."""
+    import torch
+    dev = _dev(device)
+    d = torch.empty((intr.height, intr.width), dtype=torch.float64, device=dev)
+    _run(scene, _pinhole(pose, intr), {"depth_or_far": d}, None, transforms, dev.index)
+    return d.cpu().numpy()
+
+
+def render_ortho_depth(scene, cam, transforms=None, device=None) -> np.ndarray:
+    """ref engine.py:200-205: distance along the projection direction, cam.far where no hit."""
+    import torch
+    dev = _dev(device)
+    d = torch.empty((cam.height, cam.width), dtype=torch.float64, device=dev)
+    _run(scene, _ortho(cam), {"depth_or_far": d}, None, transforms, dev.index)
+    return d.cpu().numpy()
+
+
+def build_light_camera(aabb_lo, aabb_hi, direction, resolution: int = 256) -> OrthoCamera:
+    """Orthographic camera along the light covering the AABB (ref engine.py:208-219)."""
+    lo = np.asarray(aabb_lo, dtype=np.float64)
+    hi = np.asarray(aabb_hi, dtype=np.float64)
+    centre = (lo + hi) / 2
+    r = float(np.linalg.norm(hi - lo) / 2) * 1.1 + 1e-3
+    d = np.asarray(direction, dtype=np.float64)
+    d = d / np.linalg.norm(d)
+    eye = centre - d * (r + 1.0)
+    return OrthoCamera(pose=look_at(eye, eye + d), half_width=r, half_height=r, width=resolution,
+                       height=resolution, far=2 * r + 2.0)
+
+
+def build_dome_rig(center, heading: float, n_cameras: int, radius: float, width: int = 64, height: int = 64,
+                   fov_y: float = np.pi / 2, near: float = 0.05, far: float = 100.0):
+    """Inward-looking cameras on the upper Fibonacci hemisphere (ref engine.py:222-246)."""
+    if n_cameras < 1:
+        raise ValueError("n_cameras must be >= 1")
+    c = np.asarray(center, dtype=np.float64)
+    poses = []
+    for i in range(n_cameras):
+        ct = 1.0 - i / n_cameras
+        st = np.sqrt(max(0.0, 1.0 - ct * ct))
+        phi = i * GOLDEN_ANGLE + heading
+        poses.append(look_at(c + radius * np.array([st * np.cos(phi), ct, st * np.sin(phi)]), c))
+    return poses, CameraIntrinsics(width=width, height=height, fov_y=fov_y, near=near, far=far)
+
+
+__all__ = ["InputBuffers", "scene_struct", "render_ground_truth", "render_ground_truth_device",
+           "capture_input_buffers", "render_depth", "render_ortho_depth", "build_light_camera", "build_dome_rig"]

@@ -41,13 +41,13 @@ HERE = pathlib.Path(__file__).resolve().parent
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
-    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool")
+    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool engine")
     args = ap.parse_args()
     ref = pathlib.Path(args.ref)
     sys.path.insert(0, str(ref / "src"))
     import splatstream  # noqa: F401  (the reference)
 
-    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool"}
+    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool", "engine"}
     if "wire" in want:
         wire = HERE / "wire"
         if wire.exists():
@@ -56,7 +56,7 @@ def main():
         shipped = (ref / "tests" / "golden" / "manifest.json").read_bytes()
         assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
     for name, fn in (("codec", codec_cases), ("raster", raster_cases), ("step", step_cases), ("dyn", dyn_cases),
-                     ("ingest", ingest_cases), ("pool", pool_cases)):
+                     ("ingest", ingest_cases), ("pool", pool_cases), ("engine", engine_cases)):
         if name in want:
             fn()
     print("golden vectors written to", HERE)
@@ -640,6 +640,77 @@ def pool_cases():
                     has_permute=prec is not None, has_prune=rrec is not None), **arrays)
     st.save("pool_cases")
 
+
+
+ENGINE_SCENES = {
+    "floor_ball_box": {
+        "background": [0.05, 0.05, 0.08],
+        "light": {"direction": [-0.4, -1.0, 0.3], "intensity": [0.8, 0.8, 0.8], "ambient": [0.2, 0.2, 0.2]},
+        "objects": [
+            {"id": 0, "shape": {"kind": "plane", "point": [0, 0, 0], "normal": [0, 1, 0], "extent": [4.0, 4.0]},
+             "albedo": {"kind": "checker", "colors": [[0.9, 0.9, 0.9], [0.2, 0.25, 0.35]], "scale": 1.0}},
+            {"id": 1, "shape": {"kind": "sphere", "center": [0, 0.5, 0], "radius": 0.5},
+             "albedo": {"kind": "solid", "color": [0.8, 0.2, 0.15]},
+             "animation": {"kind": "bounce", "height": 1.0, "period": 2.0}},
+            {"id": 2, "shape": {"kind": "box", "center": [1.2, 0.4, -0.6], "half_extents": [0.3, 0.4, 0.25]},
+             "albedo": {"kind": "checker", "colors": [[0.1, 0.7, 0.2], [0.9, 0.8, 0.1]], "scale": 0.25},
+             "animation": {"kind": "rotate", "axis": [0.2, 1.0, 0.1], "deg_per_s": 40.0, "anchor": [1.2, 0.4, -0.6]}},
+            {"id": 0, "shape": {"kind": "box", "center": [-1.3, 0.3, 0.9], "half_extents": [0.3, 0.3, 0.3]},
+             "albedo": {"kind": "solid", "color": [0.3, 0.4, 0.9]}},
+        ],
+    },
+    "walls": {
+        "background": [0.3, 0.1, 0.2],
+        "light": {"direction": [0.5, -0.7, -0.2], "intensity": [1.0, 0.9, 0.8], "ambient": [0.15, 0.2, 0.25]},
+        "objects": [
+            {"id": 0, "shape": {"kind": "plane", "point": [0, -0.5, 0], "normal": [0.0, 1.0, 0.05]},
+             "albedo": {"kind": "checker", "colors": [[0.8, 0.8, 0.7], [0.3, 0.3, 0.3]], "scale": 0.5}},
+            {"id": 0, "shape": {"kind": "plane", "point": [0, 0, 3], "normal": [0.1, 0, -1], "extent": [2.0, 1.5]},
+             "albedo": {"kind": "solid", "color": [0.6, 0.5, 0.4]}},
+            {"id": 3, "shape": {"kind": "sphere", "center": [0.4, 0.2, 1.0], "radius": 0.45},
+             "albedo": {"kind": "checker", "colors": [[1.0, 0.2, 0.2], [0.2, 0.2, 1.0]], "scale": 0.2},
+             "animation": {"kind": "oscillate", "axis": [1, 0, 0], "amplitude": 0.3, "period": 1.5}},
+        ],
+    },
+}
+
+
+def engine_cases():
+    """The reference engine (ref engine.py) on scenes built by its own
+    scene_from_dict: ground truth, capture buffers, render depth, ortho depth.
+    Poses are stored as (position, rotation matrix) so the device sees the
+    reference's exact camera frame."""
+    from splatstream.engine import (build_light_camera, capture_input_buffers, render_depth, render_ground_truth,
+                                    render_ortho_depth)
+    from splatstream.geometry import CameraIntrinsics, look_at
+    from splatstream.scene import scene_from_dict
+    st = Store()
+    cams = [((2.5, 2.5, 2.5), (0, 0.3, 0), 64, 48, 1.2), ((0.3, 1.2, -3.0), (0, 0.4, 0.5), 40, 40, 0.9),
+            ((-2.0, 3.5, 1.0), (0.2, 0, 0.1), 33, 27, 1.4)]
+    for name, sd in ENGINE_SCENES.items():
+        scene = scene_from_dict(sd)
+        for time in (None, 0.7):
+            tfs = scene.transforms_at(time) if time is not None else None
+            tf_arr = np.array([[oid] + list(q) + list(t) for oid, (q, t) in sorted(tfs.items())]) if tfs else \
+                np.zeros((0, 8))
+            for ci, (eye, tgt, w, h, fov) in enumerate(cams):
+                pose = look_at(np.array(eye, float), np.array(tgt, float))
+                intr = CameraIntrinsics(width=w, height=h, fov_y=fov, near=0.05, far=30.0)
+                gt = render_ground_truth(scene, pose, intr, transforms=tfs)
+                b = capture_input_buffers(scene, pose, intr, transforms=tfs)
+                dep = render_depth(scene, pose, intr, transforms=tfs)
+                st.add(dict(kind="pinhole", name=f"{name}_t{time}_c{ci}", scene=sd, width=w, height=h, fov_y=fov,
+                            near=0.05, far=30.0),
+                       transforms=tf_arr, position=pose.position, R=pose.rotation(), gt=gt, world_pos=b.world_pos,
+                       valid=b.valid, normal=b.normal, albedo=b.albedo, shaded=b.shaded, object_id=b.object_id,
+                       depth=b.depth, footprint=b.footprint, lit=b.lit, render_depth=dep)
+            lo, hi = scene.aabb(tfs)
+            lc = build_light_camera(lo, hi, scene.light.direction, resolution=32)
+            od = render_ortho_depth(scene, lc, transforms=tfs)
+            st.add(dict(kind="ortho", name=f"{name}_t{time}_light", scene=sd, width=lc.width, height=lc.height,
+                        half_width=lc.half_width, half_height=lc.half_height, far=lc.far),
+                   transforms=tf_arr, position=lc.pose.position, R=lc.pose.rotation(), ortho_depth=od)
+    st.save("engine_cases")
 
 if __name__ == "__main__":
     main()
