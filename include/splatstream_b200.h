@@ -429,6 +429,41 @@ typedef struct {  /* (H, W[, 3]) row-major device buffers; NULL = not written */
 
 int ss_engine_render(ss_ctx* ctx, const ss_scene* scene, const ss_engine_camera* cam, const ss_engine_out* out);
 
+/* Expansion inputs: ref engine.py:249-303 cull_input_samples and
+ * expansion.py:39-64 init_gaussians.  Device buffers. */
+typedef struct {  /* one input camera's capture buffers (H*W pixels, row-major) */
+    const double* world_pos;   /* (pixels, 3) */
+    const uint8_t* valid;
+    const double* normal;      /* (pixels, 3) */
+    const double* albedo;      /* (pixels, 3) */
+    const int32_t* object_id;
+    const double* footprint;
+    const uint8_t* lit;
+    double position[3];        /* the camera's pose.position */
+    int64_t pixels;
+} ss_cull_camera;
+
+typedef struct {  /* SampleBatch (engine.py:54-78), device arrays of capacity rows */
+    double* positions;         /* (n, 3) */
+    double* normals;           /* (n, 3) */
+    double* albedo;            /* (n, 3) */
+    int32_t* object_ids;
+    double* footprints;
+    uint8_t* lit;
+    int32_t* camera_indices;
+} ss_sample_batch;
+
+/* Pools the valid pixels of `cams` (HOST array, camera order), keeps per voxel
+ * (side 2 x median footprint) the samples of the best-scoring camera, writes
+ * them to `out` in pool order; *count_out (host) = kept samples, *side_out
+ * (host, may be NULL) = voxel side.  Synchronises the stream. */
+int ss_cull_input_samples(ss_ctx* ctx, const ss_cull_camera* cams, int32_t n_cams, const ss_sample_batch* out,
+                          int64_t capacity, int64_t* count_out, double* side_out);
+/* init_gaussians: rows [row0, row0 + n) of `model` from the first n samples
+ * (isotropic log(max(footprint, 1e-6) / 2) scales, identity rotation, opacity
+ * logit 0, SH DC = (albedo - 0.5) / C0, rest 0, visibility = lit). */
+int ss_init_gaussians(ss_ctx* ctx, const ss_sample_batch* samples, int64_t n, const ss_model* model, int64_t row0);
+
 #ifdef __cplusplus
 }
 #endif

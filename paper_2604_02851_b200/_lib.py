@@ -126,6 +126,16 @@ class SSEngineOut(C.Structure):
                                   "shaded", "object_id", "depth", "footprint", "lit")]
 
 
+class SSCullCamera(C.Structure):
+    _fields_ = [(n, vp) for n in ("world_pos", "valid", "normal", "albedo", "object_id", "footprint", "lit")] + \
+               [("position", f64 * 3), ("pixels", i64)]
+
+
+class SSSampleBatch(C.Structure):
+    _fields_ = [(n, vp) for n in ("positions", "normals", "albedo", "object_ids", "footprints", "lit",
+                                  "camera_indices")]
+
+
 class SSOrthoCamera(C.Structure):
     _fields_ = [("position", f64 * 3), ("rot_cw", f64 * 9), ("half_width", f64), ("half_height", f64),
                 ("width", i32), ("height", i32)]
@@ -169,6 +179,9 @@ _SIGS = {
     "ss_decode_snapshot": (i32, [vp, C.POINTER(SSSnapshotDecode)]),
     "ss_select_rows": (i32, [vp, C.POINTER(SSSelect), vp, C.POINTER(i64)]),
     "ss_gather_rows": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSModel), vp, i64, C.POINTER(SSModel)]),
+    "ss_cull_input_samples": (i32, [vp, C.POINTER(SSCullCamera), i32, C.POINTER(SSSampleBatch), i64, C.POINTER(i64),
+                                    C.POINTER(f64)]),
+    "ss_init_gaussians": (i32, [vp, C.POINTER(SSSampleBatch), i64, C.POINTER(SSModel), i64]),
     "ss_engine_render": (i32, [vp, C.POINTER(SSScene), C.POINTER(SSEngineCamera), C.POINTER(SSEngineOut)]),
     "ss_grid_rebuild": (i32, [vp, vp, i64, C.POINTER(SSGridSpec), vp, vp, vp, vp, C.POINTER(i64)]),
     "ss_zigzag_varints": (i32, [vp, vp, i64, vp, u64, C.POINTER(u64)]),

@@ -207,6 +207,106 @@ def render_ortho_depth(scene, cam, transforms=None, device=None) -> np.ndarray:
     return d.cpu().numpy()
 
 
+@dataclass
+class SampleBatch:
+    """Culled surface samples pooled across input cameras (ref engine.py:54-78)."""
+
+    positions: object
+    normals: object
+    albedo: object
+    object_ids: object
+    footprints: object
+    lit: object
+    camera_indices: object
+
+    @property
+    def count(self) -> int:
+        return int(self.positions.shape[0])
+
+
+def _as_dev(a, dtype, dev):
+    import torch
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a))).to(device=dev, dtype=dtype)
+
+
+def cull_input_samples(buffers, device=None, as_tensors=False) -> SampleBatch:
+    """ref engine.py:249-303 on the GPU: pool the valid samples of every input
+    camera, voxel side 2 x the median footprint, per voxel only the samples of
+    the least oblique camera (ties to the lower index).  `buffers` are
+    InputBuffers with host (numpy) or device (torch) channels."""
+    import torch
+    dev = _dev(device)
+    c = _lib.ctx(dev.index)
+    c.bind_stream()
+    cams = (_lib.SSCullCamera * max(1, len(buffers)))()
+    keep = []
+    total = 0
+    for k, b in enumerate(buffers):
+        ch = {"world_pos": _as_dev(b.world_pos, torch.float64, dev), "valid": _as_dev(b.valid, torch.uint8, dev),
+              "normal": _as_dev(b.normal, torch.float64, dev), "albedo": _as_dev(b.albedo, torch.float64, dev),
+              "object_id": _as_dev(b.object_id, torch.int32, dev), "footprint": _as_dev(b.footprint, torch.float64, dev),
+              "lit": _as_dev(b.lit, torch.uint8, dev)}
+        keep.append(ch)
+        for name, t in ch.items():
+            setattr(cams[k], name, t.data_ptr())
+        cams[k].position[:] = [float(x) for x in np.asarray(b.pose.position, np.float64)]
+        cams[k].pixels = int(ch["valid"].numel())
+        total += cams[k].pixels
+    cap = max(1, total)
+    f64 = dict(dtype=torch.float64, device=dev)
+    out = {"positions": torch.empty((cap, 3), **f64), "normals": torch.empty((cap, 3), **f64),
+           "albedo": torch.empty((cap, 3), **f64), "object_ids": torch.empty(cap, dtype=torch.int32, device=dev),
+           "footprints": torch.empty(cap, **f64), "lit": torch.empty(cap, dtype=torch.uint8, device=dev),
+           "camera_indices": torch.empty(cap, dtype=torch.int32, device=dev)}
+    sb = _lib.SSSampleBatch(*(out[k].data_ptr() for k in ("positions", "normals", "albedo", "object_ids", "footprints",
+                                                          "lit", "camera_indices")))
+    n = _lib.i64(0)
+    side = _lib.f64(0.0)
+    c.check(c.lib.ss_cull_input_samples(c.handle, cams, len(buffers), C.byref(sb), cap, C.byref(n), C.byref(side)))
+    del keep
+    n = int(n.value)
+    res = {k: v[:n] for k, v in out.items()}
+    res["lit"] = res["lit"].bool()
+    if not as_tensors:
+        res = {k: v.cpu().numpy() for k, v in res.items()}
+    return SampleBatch(**res)
+
+
+def init_gaussians(samples, sh_degree: int = 0, device=None, as_device: bool = False):
+    """ref expansion.py:39-64 on the GPU: a batch of fresh Gaussians (one row
+    per sample; isotropic scales log(max(footprint, 1e-6) / 2), identity
+    rotation, opacity 0.5, SH DC reproducing the albedo).  Returns a host
+    GaussianModel (all rows active), or a DeviceModel with `as_device`."""
+    import torch
+    from .model import DeviceModel
+    dev = _dev(device)
+    n = samples.count
+    B = (sh_degree + 1) ** 2
+    f32 = dict(dtype=torch.float32, device=dev)
+    m = DeviceModel(torch.empty((n, 3), **f32), torch.empty((n, 3), **f32), torch.empty((n, 4), **f32),
+                    torch.empty(n, **f32), torch.empty((n, 3, B), **f32), torch.empty(n, **f32),
+                    torch.empty(n, dtype=torch.int32, device=dev), n, sh_degree)
+    if n:
+        c = _lib.ctx(dev.index)
+        c.bind_stream()
+        cols = {"positions": _as_dev(samples.positions, torch.float64, dev),
+                "normals": _as_dev(samples.normals, torch.float64, dev),
+                "albedo": _as_dev(samples.albedo, torch.float64, dev),
+                "object_ids": _as_dev(samples.object_ids, torch.int32, dev),
+                "footprints": _as_dev(samples.footprints, torch.float64, dev),
+                "lit": _as_dev(samples.lit, torch.uint8, dev),
+                "camera_indices": _as_dev(samples.camera_indices, torch.int32, dev)}
+        sb = _lib.SSSampleBatch(*(cols[k].data_ptr() for k in ("positions", "normals", "albedo", "object_ids",
+                                                                "footprints", "lit", "camera_indices")))
+        st = m.struct()
+        c.check(c.lib.ss_init_gaussians(c.handle, C.byref(sb), n, C.byref(st), 0))
+        torch.cuda.current_stream(dev).synchronize()
+        del cols
+    return m if as_device else m.to_host()
+
+
 def build_light_camera(aabb_lo, aabb_hi, direction, resolution: int = 256) -> OrthoCamera:
     """Orthographic camera along the light covering the AABB (ref engine.py:208-219)."""
     lo = np.asarray(aabb_lo, dtype=np.float64)
@@ -235,5 +335,5 @@ def build_dome_rig(center, heading: float, n_cameras: int, radius: float, width:
     return poses, CameraIntrinsics(width=width, height=height, fov_y=fov_y, near=near, far=far)
 
 
-__all__ = ["InputBuffers", "scene_struct", "render_ground_truth", "render_ground_truth_device",
+__all__ = ["InputBuffers", "SampleBatch", "cull_input_samples", "init_gaussians", "scene_struct", "render_ground_truth", "render_ground_truth_device",
            "capture_input_buffers", "render_depth", "render_ortho_depth", "build_light_camera", "build_dome_rig"]

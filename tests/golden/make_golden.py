@@ -41,13 +41,13 @@ HERE = pathlib.Path(__file__).resolve().parent
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
-    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool engine")
+    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool engine expand")
     args = ap.parse_args()
     ref = pathlib.Path(args.ref)
     sys.path.insert(0, str(ref / "src"))
     import splatstream  # noqa: F401  (the reference)
 
-    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool", "engine"}
+    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool", "engine", "expand"}
     if "wire" in want:
         wire = HERE / "wire"
         if wire.exists():
@@ -56,7 +56,8 @@ def main():
         shipped = (ref / "tests" / "golden" / "manifest.json").read_bytes()
         assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
     for name, fn in (("codec", codec_cases), ("raster", raster_cases), ("step", step_cases), ("dyn", dyn_cases),
-                     ("ingest", ingest_cases), ("pool", pool_cases), ("engine", engine_cases)):
+                     ("ingest", ingest_cases), ("pool", pool_cases), ("engine", engine_cases),
+                     ("expand", expand_cases)):
         if name in want:
             fn()
     print("golden vectors written to", HERE)
@@ -711,6 +712,41 @@ def engine_cases():
                         half_width=lc.half_width, half_height=lc.half_height, far=lc.far),
                    transforms=tf_arr, position=lc.pose.position, R=lc.pose.rotation(), ortho_depth=od)
     st.save("engine_cases")
+
+
+def expand_cases():
+    """cull_input_samples + init_gaussians, run by the reference on its own
+    capture buffers (dome rigs; one rig with a duplicated camera for ties)."""
+    from splatstream.engine import build_dome_rig, capture_input_buffers, cull_input_samples
+    from splatstream.expansion import init_gaussians
+    from splatstream.scene import scene_from_dict
+    st = Store()
+    chans = ("world_pos", "valid", "normal", "albedo", "object_id", "footprint", "lit")
+    rigs = [("floor_ball_box", (0, 0.3, 0), 0.4, 5, 2.8, 40, 32, None),
+            ("walls", (0.2, 0.0, 1.2), 1.1, 3, 2.0, 36, 30, None),
+            ("floor_ball_box", (0.5, 0.2, -0.2), 2.0, 3, 3.0, 32, 32, 1)]  # camera 1 duplicated as camera 3
+    for name, centre, heading, ncam, radius, w, h, dup in rigs:
+        scene = scene_from_dict(ENGINE_SCENES[name])
+        poses, intr = build_dome_rig(np.array(centre, float), heading, ncam, radius, width=w, height=h, fov_y=1.3)
+        if dup is not None:
+            poses = list(poses) + [poses[dup]]
+        bufs = [capture_input_buffers(scene, p, intr) for p in poses]
+        sb = cull_input_samples(bufs)
+        arrays = {}
+        for ci, b in enumerate(bufs):
+            for ch in chans:
+                arrays[f"cam{ci}_{ch}"] = getattr(b, ch)
+            arrays[f"cam{ci}_position"] = b.pose.position
+        for k in ("positions", "normals", "albedo", "object_ids", "footprints", "lit", "camera_indices"):
+            arrays[f"out_{k}"] = getattr(sb, k)
+        for deg in (0, 1):
+            g = init_gaussians(sb, sh_degree=deg)
+            for k in ("means", "log_scales", "quaternions", "logit_opacities", "sh_coeffs", "light_visibility",
+                      "object_ids"):
+                arrays[f"init{deg}_{k}"] = getattr(g, k)
+        st.add(dict(kind="expand", name=f"{name}_{ncam}cams" + ("_dup" if dup is not None else ""), n_cams=len(bufs),
+                    kept=int(sb.count)), **arrays)
+    st.save("expand_cases")
 
 if __name__ == "__main__":
     main()

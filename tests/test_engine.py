@@ -134,3 +134,46 @@ def test_gpu_ground_truth_feeds_the_optimiser():
     loss = step(dm, st, [view])
     assert np.isfinite(loss)
     torch.cuda.synchronize()
+
+
+EXPAND = load_cases("expand_cases")
+SAMPLE_FIELDS = ("positions", "normals", "albedo", "object_ids", "footprints", "lit", "camera_indices")
+INIT_FIELDS = ("means", "log_scales", "quaternions", "logit_opacities", "sh_coeffs", "light_visibility", "object_ids")
+
+
+def _buffers(c):
+    from paper_2604_02851_b200.engine import InputBuffers
+
+    class _P:
+        def __init__(self, position):
+            self.position = position
+
+    chans = ("world_pos", "valid", "normal", "albedo", "object_id", "footprint", "lit")
+    return [InputBuffers(pose=_P(c.a(f"cam{i}_position")), intrinsics=None, shaded=None, depth=None,
+                         **{ch: c.a(f"cam{i}_{ch}") for ch in chans})
+            for i in range(c["n_cams"])]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", EXPAND, ids=lambda c: c["name"])
+def test_gpu_cull_input_samples_matches_reference(c):
+    """The reference's own capture buffers in, its SampleBatch out (exact,
+    including pool order and the lower-camera tie break)."""
+    require_gpu()
+    from paper_2604_02851_b200 import engine
+    sb = engine.cull_input_samples(_buffers(c))
+    assert sb.count == c["kept"]
+    for k in SAMPLE_FIELDS:
+        _eq(np.asarray(getattr(sb, k)), c.a(f"out_{k}"), k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", EXPAND, ids=lambda c: c["name"])
+def test_gpu_init_gaussians_matches_reference(c):
+    require_gpu()
+    from paper_2604_02851_b200 import engine
+    sb = engine.SampleBatch(**{k: c.a(f"out_{k}") for k in SAMPLE_FIELDS})
+    for deg in (0, 1):
+        g = engine.init_gaussians(sb, sh_degree=deg)
+        for k in INIT_FIELDS:
+            _eq(np.asarray(getattr(g, k)), c.a(f"init{deg}_{k}"), f"deg{deg} {k}")
