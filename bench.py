@@ -363,10 +363,11 @@ def run_ours(args):
         enc = encoder_bench(c, _lib, args, torch)
 
     # ---- pool maintenance of this model, rank 0
-    pool_rec = zlib_rec = None
+    pool_rec = zlib_rec = engine_rec = None
     if rank == 0:
         pool_rec = pool_bench(dm, state, poses, intr, torch)
         zlib_rec = zlib_tick_bench(dm, base_m, base_l, torch)
+        engine_rec = engine_bench(poses, intr, torch)
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -440,7 +441,7 @@ def run_ours(args):
            "gpu_launches": launches, "clocks": clock_rec,
            "kernel_ms_per_step": {k: round(v, 4) for k, v in per_step.items()},
            "evaluated_pairs_per_view": evals_per_view,
-           "delta_encode": enc, "pool_maintenance": pool_rec, "server_tick_zlib": zlib_rec, "fp32_peak_tflops_measured": fp32_peak,
+           "delta_encode": enc, "pool_maintenance": pool_rec, "server_tick_zlib": zlib_rec, "engine": engine_rec, "fp32_peak_tflops_measured": fp32_peak,
            "precision": "fp64 preprocess/windows/depth keys, fp32 blend + chain rule, fp64 Adam moments"}
     print(json.dumps(out), flush=True)
     if pg is not None:
@@ -593,6 +594,57 @@ def zlib_tick_bench(dm, base_m, base_l, torch, reps=3):
             "zlib_bytes": sum(len(p) for _, p in out), "tick_ms_parallel_zlib": t_par * 1e3 / reps,
             "zlib_stage_ms_serial": t_ser * 1e3 / reps,
             "note": "tick = device encode + readback + per-attribute deflate on host threads (byte-identical)"}
+
+
+ENGINE_SCENE = {  # the engine stand-in's test scene (tests/golden/make_golden.py ENGINE_SCENES)
+    "background": [0.05, 0.05, 0.08],
+    "light": {"direction": [-0.4, -1.0, 0.3], "intensity": [0.8, 0.8, 0.8], "ambient": [0.2, 0.2, 0.2]},
+    "objects": [
+        {"id": 0, "shape": {"kind": "plane", "point": [0, 0, 0], "normal": [0, 1, 0], "extent": [4.0, 4.0]},
+         "albedo": {"kind": "checker", "colors": [[0.9, 0.9, 0.9], [0.2, 0.25, 0.35]], "scale": 1.0}},
+        {"id": 1, "shape": {"kind": "sphere", "center": [0, 0.5, 0], "radius": 0.5},
+         "albedo": {"kind": "solid", "color": [0.8, 0.2, 0.15]}},
+        {"id": 2, "shape": {"kind": "box", "center": [1.2, 0.4, -0.6], "half_extents": [0.3, 0.4, 0.25]},
+         "albedo": {"kind": "checker", "colors": [[0.1, 0.7, 0.2], [0.9, 0.8, 0.1]], "scale": 0.25}},
+    ]}
+
+
+def engine_bench(poses, intr, torch, reps=5):
+    """SURVEY §8f rank 4 on the device: the ray-cast ground truth of the
+    step's 8 views at 1080p (float32, left in HBM for the optimiser), and one
+    expansion round (8 dome cameras at 256x256: capture buffers, cull, init)."""
+    from paper_2604_02851_b200 import engine
+    from paper_2604_02851_b200.geometry import look_at
+    from paper_2604_02851_b200.scene import scene_from_dict
+    scene = scene_from_dict(ENGINE_SCENE)
+    views = [look_at(np.array([3.0 * np.cos(a), 2.2, 3.0 * np.sin(a)]), np.array([0.0, 0.3, 0.0]))
+             for a in np.linspace(0, 2 * np.pi, len(poses), endpoint=False)]
+    outs = [engine.render_ground_truth_device(scene, p, intr) for p in views]
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        for p, o in zip(views, outs):
+            engine.render_ground_truth_device(scene, p, intr, out=o)
+    e1.record()
+    torch.cuda.synchronize()
+    gt_ms = e0.elapsed_time(e1) / (reps * len(views))
+    rig, rintr = engine.build_dome_rig(np.array([0.0, 0.3, 0.0]), 0.4, 8, 3.0, width=256, height=256, fov_y=1.3)
+    t = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bufs = [engine.capture_input_buffers(scene, p, rintr, as_tensors=True) for p in rig]
+        sb = engine.cull_input_samples(bufs, as_tensors=True)
+        batch = engine.init_gaussians(sb, sh_degree=3, as_device=True)
+        torch.cuda.synchronize()
+        t.append(time.perf_counter() - t0)
+    return {"gt_ms_per_view": gt_ms, "gt_megapixels_per_s": intr.width * intr.height / (gt_ms * 1e3),
+            "resolution": [intr.width, intr.height], "objects": len(scene.objects),
+            "expansion_round_ms": min(t) * 1e3, "expansion_cameras": len(rig), "expansion_samples": sb.count,
+            "new_gaussians": batch.count,
+            "note": "device time per 1080p ground-truth view (primary + shadow ray per pixel, float64); expansion = "
+                    "wall clock of capture_input_buffers x8 + cull_input_samples + init_gaussians"}
 
 
 def pool_bench(dm, state, poses, intr, torch, reps=5):
