@@ -368,6 +368,7 @@ def run_ours(args):
         pool_rec = pool_bench(dm, state, poses, intr, torch)
         zlib_rec = zlib_tick_bench(dm, base_m, base_l, torch)
         engine_rec = engine_bench(poses, intr, torch)
+        engine_rec["live_tick"] = live_tick_bench(dm, state, poses, intr, light, torch)
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -645,6 +646,79 @@ def engine_bench(poses, intr, torch, reps=5):
             "new_gaussians": batch.count,
             "note": "device time per 1080p ground-truth view (primary + shadow ray per pixel, float64); expansion = "
                     "wall clock of capture_input_buffers x8 + cull_input_samples + init_gaussians"}
+
+
+def live_tick_bench(dm, state, poses, intr, light_state, torch, ticks=6):
+    """One server tick (ref server.py:364-493) with every stage on the device,
+    through the public APIs: (3) light-camera ortho depth + light visibility,
+    (4) expansion inputs (4 input cameras at 256x256: capture buffers, cull,
+    init -- the grid-gated append policy itself is host logic, not timed),
+    (5) ray-cast ground truth of the step's views straight into HBM, precull,
+    optimize step, grid rebuild, (6) freeze policy, (8) the due deltas as
+    TENSOR_DELTA frames read back to pinned host memory.  The engine scene is
+    the stand-in test scene (the model is the synthetic 1M field, so the
+    images do not depict it: the stage costs are what is measured)."""
+    from paper_2604_02851_b200 import engine, pool
+    from paper_2604_02851_b200.optim import ReferenceView, StepWorkspace, step
+    from paper_2604_02851_b200.protocol import DELTA_ORDER, DeltaTicker, PayloadBuffer
+    from paper_2604_02851_b200.render import update_light_visibility
+    from paper_2604_02851_b200.scene import scene_from_dict
+    scene = scene_from_dict(ENGINE_SCENE)
+    gts = [torch.empty((intr.height, intr.width, 3), dtype=torch.float32, device=dm.device) for _ in poses]
+    views = [ReferenceView(p, intr, g, light_state, np.zeros(3)) for p, g in zip(poses, gts)]
+    lcam = engine.build_light_camera(np.array([-5.0, -1.0, -1.0]), np.array([5.0, 3.0, 9.0]), light_state.direction, 256)
+    rig, rintr = engine.build_dome_rig(np.array([0.0, 0.3, 0.0]), 0.4, 4, 3.0, width=256, height=256, fov_y=1.3)
+    grid = pool.GridIndex(cell_size=0.5, origin=(0.0, 0.0, 0.0))
+    base = {0: dm.means.clone(), 1: dm.log_scales.clone()}
+    ticker = DeltaTicker(dm, base, {k: PayloadBuffer(1 << 20, dm.device) for k in range(7)})
+    ws = StepWorkspace(dm)
+    periods = {0: 1, 1: 1, 2: 10, 3: 1, 4: 1, 5: 30}
+    pend = None
+    times, stages = [], {}
+
+    def tick(i, record):
+        nonlocal pend
+        marks = [time.perf_counter()]
+        ld = engine.render_ortho_depth(scene, lcam, as_tensor=True)
+        update_light_visibility(dm, ld, lcam)
+        marks.append(time.perf_counter())
+        bufs = [engine.capture_input_buffers(scene, p, rintr, as_tensors=True) for p in rig]
+        batch = engine.init_gaussians(engine.cull_input_samples(bufs, as_tensors=True), sh_degree=dm.sh_degree,
+                                      as_device=True)
+        marks.append(time.perf_counter())
+        for p, g in zip(poses, gts):
+            engine.render_ground_truth_device(scene, p, intr, out=g)
+        subset = pool.precull(dm, grid, poses, intr) if grid.cells is not None else None
+        step(dm, state, views, index_subset=subset, workspace=ws, sync_loss=False)
+        grid.rebuild(dm)
+        pool.freeze_policy(dm, state, age_threshold=120, grad_threshold=3e-4)
+        marks.append(time.perf_counter())
+        due = [int(a) for a in DELTA_ORDER if i % periods[int(a)] == 0]
+        ticker(due)
+        done, pend = pend, ticker.read_async(due, frame_epoch=1)
+        nbytes = sum(len(f) for f in done.result(copy=False)) if done is not None else 0
+        marks.append(time.perf_counter())
+        if record:
+            for k, (a, b) in zip(("light", "expansion_inputs", "ground_truth+optimize+pool", "delta_frames"),
+                                 zip(marks, marks[1:])):
+                stages.setdefault(k, []).append((b - a) * 1e3)
+        return batch.count, nbytes
+
+    for i in range(2):
+        tick(i, False)
+    torch.cuda.synchronize()
+    for i in range(ticks):
+        t0 = time.perf_counter()
+        new_rows, nbytes = tick(i, True)
+        times.append(time.perf_counter() - t0)
+    pend.result(copy=False)
+    torch.cuda.synchronize()
+    ms = float(np.median(times)) * 1e3
+    return {"tick_ms": ms, "ticks_per_s": 1e3 / ms, "views": len(poses), "resolution": [intr.width, intr.height],
+            "gaussians": dm.active_count, "new_gaussians_per_tick": new_rows, "frame_bytes_read": nbytes,
+            "stage_ms_host_wall": {k: float(np.median(v)) for k, v in stages.items()},
+            "note": "wall clock per tick (median of %d), host enqueue included; stages are host wall clock per "
+                    "stage (asynchronous GPU work can land in a later stage)" % ticks}
 
 
 def pool_bench(dm, state, poses, intr, torch, reps=5):

@@ -189,22 +189,25 @@ def capture_input_buffers(scene, pose, intr, light=None, transforms=None, device
     return InputBuffers(pose=pose, intrinsics=intr, **h)
 
 
-def render_depth(scene, pose, intr, transforms=None, device=None) -> np.ndarray:
-    """ref engine.py:192-197: camera-space z per pixel, intr.far where no hit."""
+def render_depth(scene, pose, intr, transforms=None, device=None, as_tensor=False):
+    """ref engine.py:192-197: camera-space z per pixel, intr.far where no hit
+    (host numpy, or the device tensor with `as_tensor`)."""
     import torch
     dev = _dev(device)
     d = torch.empty((intr.height, intr.width), dtype=torch.float64, device=dev)
     _run(scene, _pinhole(pose, intr), {"depth_or_far": d}, None, transforms, dev.index)
-    return d.cpu().numpy()
+    return d if as_tensor else d.cpu().numpy()
 
 
-def render_ortho_depth(scene, cam, transforms=None, device=None) -> np.ndarray:
-    """ref engine.py:200-205: distance along the projection direction, cam.far where no hit."""
+def render_ortho_depth(scene, cam, transforms=None, device=None, as_tensor=False):
+    """ref engine.py:200-205: distance along the projection direction, cam.far
+    where no hit (host numpy, or the device tensor with `as_tensor`, e.g. for
+    render.update_light_visibility)."""
     import torch
     dev = _dev(device)
     d = torch.empty((cam.height, cam.width), dtype=torch.float64, device=dev)
     _run(scene, _ortho(cam), {"depth_or_far": d}, None, transforms, dev.index)
-    return d.cpu().numpy()
+    return d if as_tensor else d.cpu().numpy()
 
 
 @dataclass
