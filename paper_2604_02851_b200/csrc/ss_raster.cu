@@ -4,7 +4,7 @@
 //                       window, depth key, relit colour     (render.py:226-290)
 //   K3a depth sort      stable radix sort of fp64-depth bits -> exact
 //                       lexsort((rows, depth)) order         (render.py:283)
-//   K2  k_count/k_emit  rank-ordered splat records, tile-overlap counts,
+//   K2  k_count/k_emit_warp rank-ordered splat records, tile-overlap counts,
 //                       exclusive scan, (tile, rank) pair emission
 //   K3b tile sort       stable radix sort on ceil(log2 tiles) key bits
 //   K4  k_ranges        per-tile [start, end)
@@ -229,23 +229,59 @@ __global__ void k_count(const uint64_t* __restrict__ dkey64, const uint32_t* __r
     }
 }
 
+// Pair emission: every (tile, splat) pair, splats in rank order, a splat's
+// tiles row-major from roff[rank].  A warp takes 32
+// consecutive ranks, whose pairs form one contiguous output range, and writes
+// that range 32 pairs at a time; each lane finds the rank owning its pair by
+// a 5-step binary search over the lanes' start offsets (shuffles), so the
+// stores are coalesced and a large splat no longer serialises one thread.
 template <typename R>
-__global__ void k_emit(const SplatRec<R>* __restrict__ rec, const uint32_t* __restrict__ dvals,
-                       const uint32_t* __restrict__ rcnt, const uint64_t* __restrict__ roff, int64_t n_in, int tiles_x,
-                       uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals, uint64_t* __restrict__ roffj) {
+__global__ void __launch_bounds__(256) k_emit_warp(const SplatRec<R>* __restrict__ rec, const uint32_t* __restrict__ dvals,
+                                                   const uint32_t* __restrict__ rcnt, const uint64_t* __restrict__ roff,
+                                                   int64_t n_in, int tiles_x, uint32_t* __restrict__ pkeys,
+                                                   uint32_t* __restrict__ pvals, uint64_t* __restrict__ roffj) {
     SS_PDL_WAIT();
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
-        if (!rcnt[r]) continue;
-        const uint32_t j = dvals[r];
-        int tx0, tx1, ty0, ty1;
-        win_tiles(rec[j].win, tx0, tx1, ty0, ty1);
-        uint64_t p = roff[r];
-        roffj[j] = p;
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx, ++p) {
-                pkeys[p] = (uint32_t)(ty * tiles_x + tx);
-                pvals[p] = j;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < n_in; r0 += nwarps * 32) {
+        const int64_t r = r0 + lane;
+        const uint32_t cnt = r < n_in ? rcnt[r] : 0u;
+        const uint64_t off = r < n_in ? roff[r] : ~0ull;
+        uint32_t j = 0;
+        int tx0 = 0, ty0 = 0, w = 1;
+        if (cnt) {
+            j = dvals[r];
+            int tx1, ty1;
+            win_tiles(rec[j].win, tx0, tx1, ty0, ty1);
+            w = tx1 - tx0 + 1;
+            roffj[j] = off;
+        }
+        const uint64_t p0 = __shfl_sync(0xffffffffu, off, 0);
+        uint64_t p1 = cnt ? off + cnt : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t t = __shfl_xor_sync(0xffffffffu, p1, o);
+            p1 = t > p1 ? t : p1;
+        }
+        for (uint64_t base = p0; base < p1; base += 32) {
+            const uint64_t p = base + lane;
+            int src = 0;  // the last lane whose range starts at or before p
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const uint64_t o = __shfl_sync(0xffffffffu, off, src + step);
+                if (o <= p) src += step;
             }
+            const uint64_t so = __shfl_sync(0xffffffffu, off, src);
+            const uint32_t sj = __shfl_sync(0xffffffffu, j, src);
+            const int sx = __shfl_sync(0xffffffffu, tx0, src), sy = __shfl_sync(0xffffffffu, ty0, src);
+            const int sw = __shfl_sync(0xffffffffu, w, src);
+            if (p < p1) {
+                const uint32_t q = (uint32_t)(p - so);
+                const uint32_t qy = q / (uint32_t)sw;
+                pkeys[p] = (uint32_t)((sy + (int)qy) * tiles_x + sx + (int)(q - qy * (uint32_t)sw));
+                pvals[p] = sj;
+            }
+        }
     }
 }
 
@@ -1288,8 +1324,8 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (!b.pkeys || !b.pvals || !pk2 || !pv2) return SS_ERR_CUDA;
     if (P > 0) {
         ss_tic(ctx, KC_BIN);
-        SS_CUDA(ctx, ss_launch((k_emit<R>), dim3(gridn(ctx, n)), dim3(256), 0, s, (const SplatRec<R>*)b.rec, b.dvals, b.rcnt, b.roff, n, b.tiles_x,
-                                                b.pkeys, b.pvals, b.roffj));
+        SS_CUDA(ctx, ss_launch((k_emit_warp<R>), dim3(gridn(ctx, n)), dim3(256), 0, s, (const SplatRec<R>*)b.rec, b.dvals, b.rcnt, b.roff, n,
+                               b.tiles_x, b.pkeys, b.pvals, b.roffj));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_BIN);
         ss_tic(ctx, KC_TILE_SORT);
