@@ -20,7 +20,10 @@ namespace {
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_MAX_PASSES = 8;
-constexpr int LB = 8;  // look-back window (tiles per step)
+#ifndef RS_LB
+#define RS_LB 8
+#endif
+constexpr int LB = RS_LB;  // look-back window (tiles per step)
 constexpr uint32_t FLAG_AGG = 1u << 30, FLAG_INC = 2u << 30, CNT_MASK = (1u << 30) - 1;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
