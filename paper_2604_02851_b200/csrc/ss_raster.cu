@@ -1232,7 +1232,10 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
 // ---------------------------------------------------------------- host
 inline int gridn(ss_ctx* ctx, int64_t n, int block = 256) {
     int64_t g = (n + block - 1) / block;
-    int64_t cap = (int64_t)ctx->num_sms * 32;
+#ifndef SS_GRID_CAP
+#define SS_GRID_CAP 32
+#endif
+    int64_t cap = (int64_t)ctx->num_sms * SS_GRID_CAP;
     if (g > cap) g = cap;
     return g < 1 ? 1 : (int)g;
 }
