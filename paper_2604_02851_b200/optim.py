@@ -94,6 +94,7 @@ def _gt_tensor(view, device):
 
 
 _COPY_STREAMS = {}
+_GT_POOL = {}  # device index -> persistent ground-truth staging buffers
 
 
 def _stage_ground_truth(views, device):
@@ -108,22 +109,28 @@ def _stage_ground_truth(views, device):
     cs = _COPY_STREAMS.get(device.index)
     if cs is None:
         cs = _COPY_STREAMS[device.index] = torch.cuda.Stream(device)
+    # the copies wait for everything queued before this step, so one
+    # persistent device buffer per view slot is safe to refill every step (no
+    # allocator churn: fresh blocks would mean synchronising cudaMallocs)
     cs.wait_stream(cur)
+    pool = _GT_POOL.setdefault(device.index, [])
     out = []
     with torch.cuda.stream(cs):
-        for v in views:
+        for i, v in enumerate(views):
             img = v.image
             if not isinstance(img, torch.Tensor):
                 img = torch.from_numpy(np.ascontiguousarray(img, np.float32))
-            t = img.to(device=device, dtype=torch.float32, non_blocking=True).contiguous()
+            shape = tuple(img.shape)
+            if i >= len(pool):
+                pool.append(None)
+            if pool[i] is None or tuple(pool[i].shape) != shape:
+                pool[i] = torch.empty(shape, dtype=torch.float32, device=device)
+            t = pool[i]
+            t.copy_(img, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(cs)
             out.append((t, ev))
-    staged = []
-    for t, ev in out:
-        t.record_stream(cur)
-        staged.append((t, ev))
-    return [_Pending(t, ev, cur) for t, ev in staged]
+    return [_Pending(t, ev, cur) for t, ev in out]
 
 
 class _Pending:
