@@ -83,7 +83,24 @@ typedef struct {
                                 same camera (0xffffffff = unknown); orders the forward's tiles longest-first
                                 and is overwritten with this call's lengths.  NULL = list lengths */
     int64_t tile_hint_len;   /* entries in tile_hint (must equal the tile count, else it is ignored) */
+    float* defer_g9;         /* backward, fp32 blend only: if set, the per-row screen-space gradients
+                                (n_in x 9) go here and defer_rinv (n_in) receives each row's depth
+                                rank (0xffffffff = culled); the chain rule is left to one
+                                ss_chain_views call over all the step's views.  NULL = immediate */
+    uint32_t* defer_rinv;
 } ss_render_opts;
+
+/* The chain rule of a step's views in one pass over the rows (ref
+ * optim.py:170-268 per view, summed over views in view order as the
+ * per-view backward would): g9[v] / rinv[v] are the defer_g9 / defer_rinv
+ * buffers of n_views ss_backward calls (same model, subset and n_in);
+ * cams / lights / g9 / rinv are HOST arrays of n_views (<= 16) entries.
+ * Adds into grad (the ss_backward layout) with the same per-element fp32
+ * additions in the same order, reading the parameters and writing the
+ * gradient once per step instead of once per view. */
+int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights, int32_t n_views,
+                   const float* const* g9, const uint32_t* const* rinv, const int64_t* subset, int64_t n_in,
+                   float* grad);
 
 /* Host-readable summary of the last render/backward call. */
 typedef struct {

@@ -43,7 +43,7 @@ class SSLight(C.Structure):
 class SSRenderOpts(C.Structure):
     _fields_ = [("background", f64 * 3), ("subset", vp), ("subset_count", i32), ("extent_cutoff", i32),
                 ("precision", i32), ("deterministic", i32), ("gt_ready", vp), ("tile_hint", vp),
-                ("tile_hint_len", i64)]
+                ("tile_hint_len", i64), ("defer_g9", vp), ("defer_rinv", vp)]
 
 
 class SSRenderStats(C.Structure):
@@ -182,6 +182,7 @@ _SIGS = {
     "ss_cull_input_samples": (i32, [vp, C.POINTER(SSCullCamera), i32, C.POINTER(SSSampleBatch), i64, C.POINTER(i64),
                                     C.POINTER(f64)]),
     "ss_init_gaussians": (i32, [vp, C.POINTER(SSSampleBatch), i64, C.POINTER(SSModel), i64]),
+    "ss_chain_views": (i32, [vp, C.POINTER(SSModel), vp, vp, i32, C.POINTER(vp), C.POINTER(vp), vp, i64, vp]),
     "ss_engine_render": (i32, [vp, C.POINTER(SSScene), C.POINTER(SSEngineCamera), C.POINTER(SSEngineOut)]),
     "ss_grid_rebuild": (i32, [vp, vp, i64, C.POINTER(SSGridSpec), vp, vp, vp, vp, C.POINTER(i64)]),
     "ss_zigzag_varints": (i32, [vp, vp, i64, vp, u64, C.POINTER(u64)]),

@@ -885,6 +885,232 @@ template <typename T> __device__ __forceinline__ T t_exp(T x);
 template <> __device__ __forceinline__ float t_exp<float>(float x) { return expf(x); }
 template <> __device__ __forceinline__ double t_exp<double>(double x) { return exp(x); }
 
+// The chain rule of one (row, view) (ref optim.py:170-268): adds the row's
+// parameter gradients of this view into acc (means 3, log scales 3,
+// quaternion 4, opacity 1) with the same fp32 additions the gradient buffer
+// would see, and writes the row's SH record for k_sh_grad.
+template <typename T, int DEG>
+__device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& cam, const ss_light& L, int64_t row,
+                                          const T* g, float* acc, float4* __restrict__ shrec_row) {
+    constexpr int B = ss_sh_bases(DEG);
+    T Rc[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Rc[i][k] = (T)cam.rot_cw[3 * i + k];
+    const T fx = (T)cam.fx, fy = (T)cam.fy;
+    const T ldir[3] = {(T)L.direction[0], (T)L.direction[1], (T)L.direction[2]};
+    // ---- appearance first (the SH registers die early)
+    T d[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) d[i] = (T)((double)m.means[row * 3 + i] - cam.position[i]);
+    const T dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    const T vdir[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+    const float* lsp = m.log_scales + row * 3;
+    int axis;
+    {
+        const double l0 = lsp[0], l1 = lsp[1], l2 = lsp[2];
+        const double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
+        axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
+    }
+    T u[4];
+    T qn;
+    {
+        const float* qp = m.quaternions + row * 4;
+        const T q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
+        qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+        u[0] = q0 / qn; u[1] = q1 / qn; u[2] = q2 / qn; u[3] = q3 / qn;
+    }
+    const T w = u[0], qx = u[1], qy = u[2], qz = u[3];
+    T Rq[3][3];
+    Rq[0][0] = 1 - 2 * (qy * qy + qz * qz); Rq[0][1] = 2 * (qx * qy - w * qz); Rq[0][2] = 2 * (qx * qz + w * qy);
+    Rq[1][0] = 2 * (qx * qy + w * qz); Rq[1][1] = 1 - 2 * (qx * qx + qz * qz); Rq[1][2] = 2 * (qy * qz - w * qx);
+    Rq[2][0] = 2 * (qx * qz - w * qy); Rq[2][1] = 2 * (qy * qz + w * qx); Rq[2][2] = 1 - 2 * (qx * qx + qy * qy);
+    T gc[3];
+    T gv[3] = {0, 0, 0};
+    Shade<DEG, T> S;
+    {
+        float sh[3 * B];
+        ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, sh);
+        ss_shade_v<DEG, T>(L, lsp, sh, m.light_visibility[row], d, Rq, S);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            gc[c] = (S.pre[c] > (T)0 && S.pre[c] < (T)1) ? g[c] : (T)0;  // clamp mask (optim.py:176-177)
+        if constexpr (DEG > 0) {
+            T coef[B];
+#pragma unroll
+            for (int k = 0; k < B; ++k) coef[k] = sh[k] * gc[0] + sh[B + k] * gc[1] + sh[2 * B + k] * gc[2];
+            ss_sh_grad_dot<DEG, T>(vdir, coef, gv);
+        }
+    }
+    const T* albedo = S.albedo;
+    const T cosv = S.cosv, vis = S.vis, sgn_s = S.s;
+    // SH coefficient gradients: written by k_sh_grad from this compact record
+    shrec_row[0] = make_float4((float)gc[0], (float)gc[1], (float)gc[2], (float)(cosv * vis));
+    shrec_row[1] = make_float4((float)vdir[0], (float)vdir[1], (float)vdir[2], 1.0f);
+
+    // ---- geometry: mu_cam, J, Sigma3d, cov (render.py:246-267)
+    T mc[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mc[k] = d[0] * Rc[0][k] + d[1] * Rc[1][k] + d[2] * Rc[2][k];
+    const T x = mc[0], y = mc[1], z = mc[2];
+    const T iz = (T)1 / z, z2 = z * z;
+    const T J00 = fx * iz, J02 = -fx * x / z2, J11 = fy * iz, J12 = -fy * y / z2;
+    T S2[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) S2[k] = t_exp<T>((T)2 * (T)lsp[k]);
+    T S3[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = i; k < 3; ++k) {
+            S3[i][k] = Rq[i][0] * S2[0] * Rq[k][0] + Rq[i][1] * S2[1] * Rq[k][1] + Rq[i][2] * S2[2] * Rq[k][2];
+            S3[k][i] = S3[i][k];
+        }
+    T tm[3][3], cov[3][3];  // cov = W S3 W^T, W[i][k] = Rc[k][i]
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) tm[i][l] = Rc[0][i] * S3[0][l] + Rc[1][i] * S3[1][l] + Rc[2][i] * S3[2][l];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = i; k < 3; ++k) {
+            cov[i][k] = tm[i][0] * Rc[0][k] + tm[i][1] * Rc[1][k] + tm[i][2] * Rc[2][k];
+            cov[k][i] = cov[i][k];
+        }
+    // ---- optim.py:180-195
+    const T g00 = g[6], g01 = g[7], g11 = g[8];
+    T JC0[3], JC1[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        JC0[l] = J00 * cov[0][l] + J02 * cov[2][l];
+        JC1[l] = J11 * cov[1][l] + J12 * cov[2][l];
+    }
+    T gJ0[3], gJ1[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        gJ0[l] = 2 * (g00 * JC0[l] + g01 * JC1[l]);
+        gJ1[l] = 2 * (g01 * JC0[l] + g11 * JC1[l]);
+    }
+    // gV = J^T G2 J (J rows: [J00, 0, J02], [0, J11, J12])
+    const T Jr0[3] = {J00, 0, J02}, Jr1[3] = {0, J11, J12};
+    T JG0[3], JG1[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        JG0[l] = g00 * Jr0[l] + g01 * Jr1[l];
+        JG1[l] = g01 * Jr0[l] + g11 * Jr1[l];
+    }
+    T gV[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) gV[k][l] = Jr0[k] * JG0[l] + Jr1[k] * JG1[l];
+    T G3[3][3];  // R_cw gV R_cw^T
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) tm[i][l] = Rc[i][0] * gV[0][l] + Rc[i][1] * gV[1][l] + Rc[i][2] * gV[2][l];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) G3[i][k] = tm[i][0] * Rc[k][0] + tm[i][1] * Rc[k][1] + tm[i][2] * Rc[k][2];
+    const T gm0 = g[4], gm1 = g[5];
+    const T z3 = z2 * z;
+    T gmc[3];
+    gmc[0] = J00 * gm0 + gJ0[2] * (-fx / z2);
+    gmc[1] = J11 * gm1 + gJ1[2] * (-fy / z2);
+    gmc[2] = J02 * gm0 + J12 * gm1 + gJ0[0] * (-fx / z2) + gJ1[1] * (-fy / z2) + gJ0[2] * (2 * fx * x / z3) +
+             gJ1[2] * (2 * fy * y / z3);
+    T gmean[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) gmean[i] = Rc[i][0] * gmc[0] + Rc[i][1] * gmc[1] + Rc[i][2] * gmc[2];
+    if constexpr (DEG > 0) {  // view-direction path (optim.py:235-240)
+        const T vg = vdir[0] * gv[0] + vdir[1] * gv[1] + vdir[2] * gv[2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) gmean[i] += (gv[i] - vdir[i] * vg) / dist;
+    }
+    // ---- scales and rotation (optim.py:204-218)
+    T gls[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T t = 0;
+#pragma unroll
+        for (int b2 = 0; b2 < 3; ++b2)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) t += Rq[b2][k] * G3[b2][c] * Rq[c][k];
+        gls[k] = t * 2 * S2[k];
+    }
+    T gR[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T t = 0;
+#pragma unroll
+            for (int b2 = 0; b2 < 3; ++b2) t += (G3[i][b2] + G3[b2][i]) * Rq[b2][c];
+            gR[i][c] = t * S2[c];
+        }
+    T gcos = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) gcos += gc[c] * (albedo[c] * (T)L.intensity[c]);
+    gcos *= vis;
+    const T gs = gcos * (sgn_s > 0 ? (T)1 : (sgn_s < 0 ? (T)-1 : (T)0));
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (k == axis) gR[i][k] += gs * -ldir[i];
+    // quaternion through R(u), u = q / |q| (optim.py:87-110)
+    const T dR[4][3][3] = {
+        {{0, -2 * qz, 2 * qy}, {2 * qz, 0, -2 * qx}, {-2 * qy, 2 * qx, 0}},
+        {{0, 2 * qy, 2 * qz}, {2 * qy, -4 * qx, -2 * w}, {2 * qz, 2 * w, -4 * qx}},
+        {{-4 * qy, 2 * qx, 2 * w}, {2 * qx, 0, 2 * qz}, {-2 * w, 2 * qz, -4 * qy}},
+        {{-4 * qz, -2 * w, 2 * qx}, {2 * w, -4 * qz, 2 * qy}, {2 * qx, 2 * qy, 0}}};
+    T h[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        T t = 0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) t += gR[i][jj] * dR[c][i][jj];
+        h[c] = t;
+    }
+    const T udh = u[0] * h[0] + u[1] * h[1] + u[2] * h[2] + u[3] * h[3];
+    const T op = (T)1 / ((T)1 + t_exp<T>(-(T)m.logit_opacities[row]));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        acc[i] += (float)gmean[i];
+        acc[3 + i] += (float)gls[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[6 + k] += (float)((h[k] - u[k] * udh) / qn);
+    acc[10] += (float)(g[3] * op * (1 - op));
+}
+
+// gradient layout offsets of a row's 11 non-SH entries (see ss_grad_layout)
+__device__ __forceinline__ void grad_row_load(const float* grad, int64_t a, int64_t row, float* acc) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        acc[i] = grad[row * 3 + i];
+        acc[3 + i] = grad[3 * a + row * 3 + i];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[6 + k] = grad[6 * a + row * 4 + k];
+    acc[10] = grad[10 * a + row];
+}
+__device__ __forceinline__ void grad_row_store(float* grad, int64_t a, int64_t row, const float* acc) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        grad[row * 3 + i] = acc[i];
+        grad[3 * a + row * 3 + i] = acc[3 + i];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) grad[6 * a + row * 4 + k] = acc[6 + k];
+    grad[10 * a + row] = acc[10];
+}
+
 // Chain rule in the blend precision T (fp32 for the throughput path, fp64
 // for the parity path); the normal-proxy axis pick repeats the preprocess's
 // fp64 comparison so both passes agree on it.
@@ -893,15 +1119,7 @@ __global__ void __launch_bounds__(128, 4) k_chain(ss_model m, ss_camera cam, ss_
                         const uint32_t* __restrict__ rinv, const T* __restrict__ g9, int64_t n_in, int cutoff,
                         float* __restrict__ grad, float4* __restrict__ shrec) {
     SS_PDL_WAIT();
-    constexpr int B = ss_sh_bases(DEG);
     const int64_t a = m.active_count;
-    T Rc[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) Rc[i][k] = (T)cam.rot_cw[3 * i + k];
-    const T fx = (T)cam.fx, fy = (T)cam.fy;
-    const T ldir[3] = {(T)L.direction[0], (T)L.direction[1], (T)L.direction[2]};
     // row order: parameter reads and gradient writes are coalesced
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t r = rinv[j];
@@ -911,193 +1129,49 @@ __global__ void __launch_bounds__(128, 4) k_chain(ss_model m, ss_camera cam, ss_
         T g[9];
 #pragma unroll
         for (int e = 0; e < 9; ++e) g[e] = g9[j * 9 + e];
-        // ---- appearance first (the SH registers die early)
-        T d[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) d[i] = (T)((double)m.means[row * 3 + i] - cam.position[i]);
-        const T dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-        const T vdir[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
-        const float* lsp = m.log_scales + row * 3;
-        int axis;
-        {
-            const double l0 = lsp[0], l1 = lsp[1], l2 = lsp[2];
-            const double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
-            axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
-        }
-        T u[4];
-        T qn;
-        {
-            const float* qp = m.quaternions + row * 4;
-            const T q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
-            qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-            u[0] = q0 / qn; u[1] = q1 / qn; u[2] = q2 / qn; u[3] = q3 / qn;
-        }
-        const T w = u[0], qx = u[1], qy = u[2], qz = u[3];
-        T Rq[3][3];
-        Rq[0][0] = 1 - 2 * (qy * qy + qz * qz); Rq[0][1] = 2 * (qx * qy - w * qz); Rq[0][2] = 2 * (qx * qz + w * qy);
-        Rq[1][0] = 2 * (qx * qy + w * qz); Rq[1][1] = 1 - 2 * (qx * qx + qz * qz); Rq[1][2] = 2 * (qy * qz - w * qx);
-        Rq[2][0] = 2 * (qx * qz - w * qy); Rq[2][1] = 2 * (qy * qz + w * qx); Rq[2][2] = 1 - 2 * (qx * qx + qy * qy);
-        T gc[3];
-        T gv[3] = {0, 0, 0};
-        Shade<DEG, T> S;
-        {
-            float sh[3 * B];
-            ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, sh);
-            ss_shade_v<DEG, T>(L, lsp, sh, m.light_visibility[row], d, Rq, S);
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                gc[c] = (S.pre[c] > (T)0 && S.pre[c] < (T)1) ? g[c] : (T)0;  // clamp mask (optim.py:176-177)
-            if constexpr (DEG > 0) {
-                T coef[B];
-#pragma unroll
-                for (int k = 0; k < B; ++k) coef[k] = sh[k] * gc[0] + sh[B + k] * gc[1] + sh[2 * B + k] * gc[2];
-                ss_sh_grad_dot<DEG, T>(vdir, coef, gv);
-            }
-        }
-        const T* albedo = S.albedo;
-        const T cosv = S.cosv, vis = S.vis, sgn_s = S.s;
-        // SH coefficient gradients: written by k_sh_grad from this compact record
-        shrec[row * 2] = make_float4((float)gc[0], (float)gc[1], (float)gc[2], (float)(cosv * vis));
-        shrec[row * 2 + 1] = make_float4((float)vdir[0], (float)vdir[1], (float)vdir[2], 1.0f);
+        float acc[11];
+        grad_row_load(grad, a, row, acc);
+        chain_row<T, DEG>(m, cam, L, row, g, acc, shrec + row * 2);
+        grad_row_store(grad, a, row, acc);
+    }
+}
 
-        // ---- geometry: mu_cam, J, Sigma3d, cov (render.py:246-267)
-        T mc[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) mc[k] = d[0] * Rc[0][k] + d[1] * Rc[1][k] + d[2] * Rc[2][k];
-        const T x = mc[0], y = mc[1], z = mc[2];
-        const T iz = (T)1 / z, z2 = z * z;
-        const T J00 = fx * iz, J02 = -fx * x / z2, J11 = fy * iz, J12 = -fy * y / z2;
-        T S2[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) S2[k] = t_exp<T>((T)2 * (T)lsp[k]);
-        T S3[3][3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int k = i; k < 3; ++k) {
-                S3[i][k] = Rq[i][0] * S2[0] * Rq[k][0] + Rq[i][1] * S2[1] * Rq[k][1] + Rq[i][2] * S2[2] * Rq[k][2];
-                S3[k][i] = S3[i][k];
+// The step's views in one pass (ss_chain_views): per row, every view in
+// order, the gradient read and written once.
+constexpr int CV_MAX_VIEWS = 16;
+struct ChainViews {
+    ss_camera cam[CV_MAX_VIEWS];
+    ss_light light[CV_MAX_VIEWS];
+    const float* g9[CV_MAX_VIEWS];
+    const uint32_t* rinv[CV_MAX_VIEWS];
+};
+
+#ifndef CV_MINB
+#define CV_MINB 4
+#endif
+template <int DEG>
+__global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const ChainViews* __restrict__ V, int nv,
+                                                        const int64_t* __restrict__ subset, int64_t n_in,
+                                                        float* __restrict__ grad, float4* __restrict__ shrec) {
+    SS_PDL_WAIT();
+    const int64_t a = m.active_count;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = subset ? subset[j] : j;
+        if (row >= a) continue;
+        float acc[11];
+        bool any = false;
+        for (int v = 0; v < nv; ++v) {
+            if (V->rinv[v][j] == ~0u) continue;
+            if (!any) {
+                grad_row_load(grad, a, row, acc);
+                any = true;
             }
-        T tm[3][3], cov[3][3];  // cov = W S3 W^T, W[i][k] = Rc[k][i]
+            float g[9];
 #pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int l = 0; l < 3; ++l) tm[i][l] = Rc[0][i] * S3[0][l] + Rc[1][i] * S3[1][l] + Rc[2][i] * S3[2][l];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int k = i; k < 3; ++k) {
-                cov[i][k] = tm[i][0] * Rc[0][k] + tm[i][1] * Rc[1][k] + tm[i][2] * Rc[2][k];
-                cov[k][i] = cov[i][k];
-            }
-        // ---- optim.py:180-195
-        const T g00 = g[6], g01 = g[7], g11 = g[8];
-        T JC0[3], JC1[3];
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-            JC0[l] = J00 * cov[0][l] + J02 * cov[2][l];
-            JC1[l] = J11 * cov[1][l] + J12 * cov[2][l];
+            for (int e = 0; e < 9; ++e) g[e] = V->g9[v][j * 9 + e];
+            chain_row<float, DEG>(m, V->cam[v], V->light[v], row, g, acc, shrec + ((int64_t)v * a + row) * 2);
         }
-        T gJ0[3], gJ1[3];
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-            gJ0[l] = 2 * (g00 * JC0[l] + g01 * JC1[l]);
-            gJ1[l] = 2 * (g01 * JC0[l] + g11 * JC1[l]);
-        }
-        // gV = J^T G2 J (J rows: [J00, 0, J02], [0, J11, J12])
-        const T Jr0[3] = {J00, 0, J02}, Jr1[3] = {0, J11, J12};
-        T JG0[3], JG1[3];
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-            JG0[l] = g00 * Jr0[l] + g01 * Jr1[l];
-            JG1[l] = g01 * Jr0[l] + g11 * Jr1[l];
-        }
-        T gV[3][3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-            for (int l = 0; l < 3; ++l) gV[k][l] = Jr0[k] * JG0[l] + Jr1[k] * JG1[l];
-        T G3[3][3];  // R_cw gV R_cw^T
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int l = 0; l < 3; ++l) tm[i][l] = Rc[i][0] * gV[0][l] + Rc[i][1] * gV[1][l] + Rc[i][2] * gV[2][l];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) G3[i][k] = tm[i][0] * Rc[k][0] + tm[i][1] * Rc[k][1] + tm[i][2] * Rc[k][2];
-        const T gm0 = g[4], gm1 = g[5];
-        const T z3 = z2 * z;
-        T gmc[3];
-        gmc[0] = J00 * gm0 + gJ0[2] * (-fx / z2);
-        gmc[1] = J11 * gm1 + gJ1[2] * (-fy / z2);
-        gmc[2] = J02 * gm0 + J12 * gm1 + gJ0[0] * (-fx / z2) + gJ1[1] * (-fy / z2) + gJ0[2] * (2 * fx * x / z3) +
-                 gJ1[2] * (2 * fy * y / z3);
-        T gmean[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) gmean[i] = Rc[i][0] * gmc[0] + Rc[i][1] * gmc[1] + Rc[i][2] * gmc[2];
-        if constexpr (DEG > 0) {  // view-direction path (optim.py:235-240)
-            const T vg = vdir[0] * gv[0] + vdir[1] * gv[1] + vdir[2] * gv[2];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) gmean[i] += (gv[i] - vdir[i] * vg) / dist;
-        }
-        // ---- scales and rotation (optim.py:204-218)
-        T gls[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            T t = 0;
-#pragma unroll
-            for (int b2 = 0; b2 < 3; ++b2)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) t += Rq[b2][k] * G3[b2][c] * Rq[c][k];
-            gls[k] = t * 2 * S2[k];
-        }
-        T gR[3][3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                T t = 0;
-#pragma unroll
-                for (int b2 = 0; b2 < 3; ++b2) t += (G3[i][b2] + G3[b2][i]) * Rq[b2][c];
-                gR[i][c] = t * S2[c];
-            }
-        T gcos = 0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) gcos += gc[c] * (albedo[c] * (T)L.intensity[c]);
-        gcos *= vis;
-        const T gs = gcos * (sgn_s > 0 ? (T)1 : (sgn_s < 0 ? (T)-1 : (T)0));
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                if (k == axis) gR[i][k] += gs * -ldir[i];
-        // quaternion through R(u), u = q / |q| (optim.py:87-110)
-        const T dR[4][3][3] = {
-            {{0, -2 * qz, 2 * qy}, {2 * qz, 0, -2 * qx}, {-2 * qy, 2 * qx, 0}},
-            {{0, 2 * qy, 2 * qz}, {2 * qy, -4 * qx, -2 * w}, {2 * qz, 2 * w, -4 * qx}},
-            {{-4 * qy, 2 * qx, 2 * w}, {2 * qx, 0, 2 * qz}, {-2 * w, 2 * qz, -4 * qy}},
-            {{-4 * qz, -2 * w, 2 * qx}, {2 * w, -4 * qz, 2 * qy}, {2 * qx, 2 * qy, 0}}};
-        T h[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            T t = 0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int jj = 0; jj < 3; ++jj) t += gR[i][jj] * dR[c][i][jj];
-            h[c] = t;
-        }
-        const T udh = u[0] * h[0] + u[1] * h[1] + u[2] * h[2] + u[3] * h[3];
-        const T op = (T)1 / ((T)1 + t_exp<T>(-(T)m.logit_opacities[row]));
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            grad[row * 3 + i] += (float)gmean[i];
-            grad[3 * a + row * 3 + i] += (float)gls[i];
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) grad[6 * a + row * 4 + k] += (float)((h[k] - u[k] * udh) / qn);
-        grad[10 * a + row] += (float)(g[3] * op * (1 - op));
+        if (any) grad_row_store(grad, a, row, acc);
     }
 }
 
@@ -1171,6 +1245,62 @@ __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __res
         }
         if (b == 0) v += gcc * (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
         out[e] += v;
+    }
+}
+
+// SH gradients of all the step's views (ss_chain_views): per (row, channel,
+// basis) entry, the views' contributions in view order, the entry read and
+// written once.  Same per-entry arithmetic as k_sh_grad.
+constexpr int SHGV_ROWS = 32;
+
+template <int DEG>
+__global__ void __launch_bounds__(256) k_sh_grad_views(const ChainViews* __restrict__ V, int nv,
+                                                       const float4* __restrict__ shrec, int64_t a,
+                                                       float* __restrict__ grad_sh) {
+    SS_PDL_WAIT();
+    constexpr int B = ss_sh_bases(DEG);
+    extern __shared__ float4 s_dyn[];
+    float4* s_r0 = s_dyn;                                          // [nv][SHGV_ROWS]
+    float* s_y = reinterpret_cast<float*>(s_dyn + nv * SHGV_ROWS);  // [nv][SHGV_ROWS][B + 1]
+    const int64_t row0 = (int64_t)blockIdx.x * SHGV_ROWS;
+    const int nrows = (int)min((int64_t)SHGV_ROWS, a - row0);
+    for (int t = threadIdx.x; t < nv * SHGV_ROWS; t += blockDim.x) {
+        const int v = t / SHGV_ROWS, r = t - v * SHGV_ROWS;
+        if (r >= nrows) continue;
+        const float4* rec = shrec + ((int64_t)v * a + row0 + r) * 2;
+        const float4 r0 = rec[0], r1 = rec[1];
+        const float dir[3] = {r1.x, r1.y, r1.z};
+        float Y[B];
+        ss_sh_eval<DEG, float>(dir, Y);
+#pragma unroll
+        for (int k = 0; k < B; ++k) s_y[(v * SHGV_ROWS + r) * (B + 1) + k] = Y[k];
+        s_r0[v * SHGV_ROWS + r] = r0;
+    }
+    __syncthreads();
+    const int n = nrows * 3 * B;
+    float* out = grad_sh + row0 * 3 * B;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int r = e / (3 * B), rem = e - r * 3 * B, c = rem / B, b = rem - c * B;
+        float acc = out[e];
+        bool touched = false;
+        for (int v = 0; v < nv; ++v) {
+            const float4 r0 = s_r0[v * SHGV_ROWS + r];
+            const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
+            if (gcc == 0.f) continue;  // clamped colour or row not visible in this view
+            const ss_light& L = V->light[v];
+            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+            const float yb = s_y[(v * SHGV_ROWS + r) * (B + 1) + b];
+            float val;
+            if (L.ambient_bands == 0) {
+                val = gcc * yb;
+            } else {
+                val = (b < BL ? gcc * (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? gcc * yb : 0.f);
+            }
+            if (b == 0) val += gcc * (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
+            acc += val;
+            touched = true;
+        }
+        if (touched) out[e] = acc;
     }
 }
 
@@ -1409,7 +1539,14 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     SS_CUDA(ctx, ss_launch((k_loss_reduce), dim3(1), dim3(256), 0, s, tloss, b.n_tiles, inv_npx, loss));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_BACKWARD);
-    if (b.n_in > 0 && m->active_count > 0) {
+    if (b.n_in > 0 && m->active_count > 0 && o->defer_g9) {  // chain rule left to ss_chain_views
+        ss_tic(ctx, KC_CHAIN);
+        SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals, partials, b.n_in,
+                               (R*)o->defer_g9));
+        SS_CHECK_LAUNCH(ctx);
+        SS_CUDA(ctx, cudaMemcpyAsync(o->defer_rinv, b.rinv, sizeof(uint32_t) * (size_t)b.n_in, cudaMemcpyDeviceToDevice, s));
+        ss_toc(ctx, KC_CHAIN);
+    } else if (b.n_in > 0 && m->active_count > 0) {
         ss_tic(ctx, KC_CHAIN);
         R* g9 = SS_SCRATCH(ctx, R, 9 * b.n_in);
         float4* shrec = SS_SCRATCH(ctx, float4, 2 * (int64_t)m->active_count);
@@ -1480,9 +1617,58 @@ int ss_backward(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_l
     if (!ctx) return SS_ERR_INVALID;
     SS_TRY(validate(ctx, m, cam, o));
     if (!gt || !grad || !loss) return ss_fail(ctx, SS_ERR_INVALID, "gt, grad_accum and loss_accum are required");
+    if (o->defer_g9 && (o->precision || !o->defer_rinv))
+        return ss_fail(ctx, SS_ERR_INVALID, "defer_g9 needs the fp32 blend and defer_rinv");
     SS_TRY(ss_scratch_reset(ctx));
     return o->precision ? backward_t<double>(ctx, m, cam, L, o, gt, grad, loss, img, st)
                         : backward_t<float>(ctx, m, cam, L, o, gt, grad, loss, img, st);
+}
+
+int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights, int32_t n_views,
+                   const float* const* g9, const uint32_t* const* rinv, const int64_t* subset, int64_t n_in,
+                   float* grad) {
+    if (!ctx || !m || !cams || !lights || !g9 || !rinv || !grad) return SS_ERR_INVALID;
+    if (n_views < 1 || n_views > CV_MAX_VIEWS) return ss_fail(ctx, SS_ERR_INVALID, "1..%d views", CV_MAX_VIEWS);
+    if (m->sh_degree < 0 || m->sh_degree > 3 || n_in < 0) return ss_fail(ctx, SS_ERR_INVALID, "bad model or row count");
+    const int64_t a = m->active_count;
+    if (a <= 0 || n_in == 0) return SS_OK;
+    SS_TRY(ss_scratch_reset(ctx));
+    cudaStream_t s = ctx->stream;
+    ChainViews hv;
+    memset(&hv, 0, sizeof(hv));
+    for (int v = 0; v < n_views; ++v) {
+        if (!g9[v] || !rinv[v]) return ss_fail(ctx, SS_ERR_INVALID, "view %d: missing deferred buffers", v);
+        hv.cam[v] = cams[v];
+        hv.light[v] = lights[v];
+        hv.g9[v] = g9[v];
+        hv.rinv[v] = rinv[v];
+    }
+    ChainViews* dv = SS_SCRATCH(ctx, ChainViews, 1);
+    float4* shrec = SS_SCRATCH(ctx, float4, 2 * a * n_views);
+    if (!dv || !shrec) return SS_ERR_CUDA;
+    SS_CUDA(ctx, cudaMemcpyAsync(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice, s));
+    SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)a * n_views, s));
+    ss_tic(ctx, KC_CHAIN);
+#define SS_CHAINV(DEG)                                                                                                     \
+    do {                                                                                                                   \
+        constexpr int B = ss_sh_bases(DEG);                                                                                \
+        SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, n_in, 128)), dim3(128), 0, s, *m, (const ChainViews*)dv, \
+                               (int)n_views, subset, n_in, grad, shrec));                                                  \
+        SS_CHECK_LAUNCH(ctx);                                                                                              \
+        const size_t smem = (size_t)n_views * SHGV_ROWS * (sizeof(float4) + sizeof(float) * (B + 1));                      \
+        SS_CUDA(ctx, ss_launch((k_sh_grad_views<DEG>), dim3((unsigned)((a + SHGV_ROWS - 1) / SHGV_ROWS)), dim3(256), smem, s,  \
+                               (const ChainViews*)dv, (int)n_views, (const float4*)shrec, a, grad + 11 * a));              \
+        SS_CHECK_LAUNCH(ctx);                                                                                              \
+    } while (0)
+    switch (m->sh_degree) {
+        case 0: SS_CHAINV(0); break;
+        case 1: SS_CHAINV(1); break;
+        case 2: SS_CHAINV(2); break;
+        default: SS_CHAINV(3); break;
+    }
+#undef SS_CHAINV
+    ss_toc(ctx, KC_CHAIN);
+    return SS_OK;
 }
 
 int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L,

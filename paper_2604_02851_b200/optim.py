@@ -158,9 +158,11 @@ def _tile_hint(view, device):
 
 
 def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subset=None, extent_cutoff=True,
-                    precision=0, image_out=None, subset_tensor=None, gt=None):
+                    precision=0, image_out=None, subset_tensor=None, gt=None, defer=None):
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
-    its loss into `loss_accum` (float64 CUDA scalar)."""
+    its loss into `loss_accum` (float64 CUDA scalar).  With `defer` =
+    (g9, rinv) device buffers the view's screen-space gradients are left
+    there for one `chain_views` call over all the step's views."""
     c = _lib.ctx(model.device.index)
     ready = None
     if gt is None:
@@ -173,7 +175,7 @@ def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subs
     c.check(c.lib.ss_backward(c.handle, model.struct(), camera_struct(view.pose, view.intrinsics),
                               light_struct(view.light_state),
                               render_opts(view.background, sub, extent_cutoff, precision, gt_ready=ready,
-                                          tile_hint=_tile_hint(view, model.device)),
+                                          tile_hint=_tile_hint(view, model.device), defer=defer),
                               _lib.ptr(gt), _lib.ptr(grad_accum), _lib.ptr(loss_accum), _lib.ptr(image_out), st))
     return st
 
@@ -306,7 +308,8 @@ class OptimizerState:
 
 
 class StepWorkspace:
-    """Reusable per-model device buffers for step() (gradient sum, loss)."""
+    """Reusable per-model device buffers for step() (gradient sum, loss, and
+    the per-view screen-space gradients of the deferred chain rule)."""
 
     def __init__(self, model: DeviceModel):
         import torch
@@ -315,6 +318,39 @@ class StepWorkspace:
         self.n = n
         self.grad = torch.zeros(max(n, 1), dtype=torch.float32, device=model.device)
         self.loss = torch.zeros(1, dtype=torch.float64, device=model.device)
+        self._defer = None
+
+    def defer_buffers(self, views: int, n_in: int, device):
+        """Per view: g9 (n_in, 9) float32 and rinv (n_in,) int32 device buffers
+        (contiguous slices of one allocation, grown on demand)."""
+        import torch
+        d = self._defer
+        if d is None or d[0].shape[0] < views or d[0].shape[1] < n_in:
+            cap = max(n_in, 1, d[0].shape[1] if d is not None else 0)
+            d = self._defer = (torch.empty((max(views, d[0].shape[0] if d is not None else 0), cap, 9),
+                                           dtype=torch.float32, device=device),
+                               torch.empty((max(views, d[0].shape[0] if d is not None else 0), cap), dtype=torch.int32,
+                                           device=device))
+        return [d[0][i, :n_in] for i in range(views)], [d[1][i, :n_in] for i in range(views)]
+
+
+CHAIN_MAX_VIEWS = 16  # ss_chain_views
+
+
+def chain_views(model: DeviceModel, views, g9, rinv, grad, subset_tensor=None):
+    """The deferred chain rule of `views` (their backward_device calls got
+    defer=(g9[i], rinv[i])): one pass over the rows, the gradient read and
+    written once (ss_chain_views)."""
+    import ctypes as C
+    c = _lib.ctx(model.device.index)
+    k = len(views)
+    cams = (_lib.SSCamera * k)(*[camera_struct(v.pose, v.intrinsics) for v in views])
+    lights = (_lib.SSLight * k)(*[light_struct(v.light_state) for v in views])
+    gp = (C.c_void_p * k)(*[g9[i].data_ptr() for i in range(k)])
+    rp = (C.c_void_p * k)(*[rinv[i].data_ptr() for i in range(k)])
+    n_in = int(subset_tensor.numel()) if subset_tensor is not None else model.count
+    c.check(c.lib.ss_chain_views(c.handle, model.struct(), cams, lights, k, gp, rp,
+                                 _lib.ptr(subset_tensor) if subset_tensor is not None else None, n_in, _lib.ptr(grad)))
 
 
 def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: bool = True, precision: int = 0,
@@ -348,8 +384,20 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     ws.loss.zero_()
     sub = _subset_tensor(index_subset, dm.device)
     gts = _stage_ground_truth(ready, dm.device)
-    for v, gt in zip(ready, gts):
-        backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub, gt=gt)
+    n_in = int(sub.numel()) if sub is not None else dm.count
+    if precision == 0 and a > 0 and n_in > 0:
+        # chain rule of every view in one pass over the rows (ss_chain_views),
+        # in batches of at most CHAIN_MAX_VIEWS views
+        for b0 in range(0, len(ready), CHAIN_MAX_VIEWS):
+            batch = list(zip(ready, gts))[b0:b0 + CHAIN_MAX_VIEWS]
+            g9, rinv = ws.defer_buffers(len(batch), n_in, dm.device)
+            for i, (v, gt) in enumerate(batch):
+                backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub,
+                                gt=gt, defer=(g9[i], rinv[i]))
+            chain_views(dm, [v for v, _ in batch], g9, rinv, ws.grad, sub)
+    else:
+        for v, gt in zip(ready, gts):
+            backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub, gt=gt)
     if process_group is not None:
         parallel.reduce_gradients(ws.grad, ws.loss, process_group)
     if a > 0:
