@@ -92,3 +92,46 @@ def test_gpu_step_batch_average():
     step(ma, OptimizerState(ma), [views[0]])
     step(mb, OptimizerState(mb), [views[0], views[0]])
     np.testing.assert_allclose(ma.means, mb.means, atol=1e-7)
+
+
+@pytest.mark.parametrize("degree", [0, 3])
+def test_gpu_deferred_chain_equals_per_view_chain(degree):
+    """step()'s deferred chain rule (ss_chain_views: every view in one pass
+    over the rows) adds the same fp32 terms in the same order as the
+    per-view chain of ss_backward: the gradient is bit-identical, with and
+    without a row subset, including rows culled in some views."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.optim import StepWorkspace, backward_device, chain_views
+    from paper_2604_02851_b200.render import _subset_tensor
+    W, H = 256, 144
+    host = synth.random_field(40_000, degree, W, H, seed=5)
+    host.active_count = 38_000
+    dm = DeviceModel.from_host(host, 0)
+    tgt = DeviceModel.from_host(synth.target_model(host, seed=6), 0)
+    intr = synth.intrinsics(W, H)
+    light = synth.light()
+    poses = synth.ring_poses(5, radius=1.5)
+    from paper_2604_02851_b200.optim import ReferenceView
+    from paper_2604_02851_b200.render import render_device
+    views = [ReferenceView(p, intr, render_device(tgt, p, intr, light), light, np.zeros(3)) for p in poses]
+    rng = np.random.default_rng(0)
+    for subset in (None, np.sort(rng.choice(40_000, 25_000, replace=False))):
+        sub = _subset_tensor(subset, dm.device)
+        ws = StepWorkspace(dm)
+        g_ref = torch.zeros_like(ws.grad)
+        loss = torch.zeros(1, dtype=torch.float64, device=dm.device)
+        for v in views:
+            backward_device(dm, v, g_ref, loss, subset_tensor=sub)
+        n_in = int(sub.numel()) if sub is not None else dm.count
+        g9, rinv = ws.defer_buffers(len(views), n_in, dm.device)
+        g_def = torch.zeros_like(ws.grad)
+        loss2 = torch.zeros(1, dtype=torch.float64, device=dm.device)
+        for i, v in enumerate(views):
+            backward_device(dm, v, g_def, loss2, subset_tensor=sub, defer=(g9[i], rinv[i]))
+        chain_views(dm, views, g9, rinv, g_def, sub)
+        assert torch.equal(loss, loss2)
+        assert torch.equal(g_ref.view(torch.int32), g_def.view(torch.int32))
+        assert bool((g_ref != 0).any())
