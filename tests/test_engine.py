@@ -177,3 +177,89 @@ def test_gpu_init_gaussians_matches_reference(c):
         g = engine.init_gaussians(sb, sh_degree=deg)
         for k in INIT_FIELDS:
             _eq(np.asarray(getattr(g, k)), c.a(f"init{deg}_{k}"), f"deg{deg} {k}")
+
+
+# ---- the reference's own engine tests (pkg/tests/test_scene_engine.py:149-300) on the device path
+
+def _light():
+    from paper_2604_02851_b200.scene import DirectionalLight
+    return DirectionalLight(direction=(-0.4, -1.0, 0.3), intensity=[0.8, 0.8, 0.8], ambient=[0.2, 0.2, 0.2])
+
+
+def _floor(extra=()):
+    from paper_2604_02851_b200.scene import Albedo, Plane, SceneDescription, SceneObject
+    objs = [SceneObject(0, Plane([0, 0, 0], [0, 1, 0], (4.0, 4.0)),
+                        Albedo("checker", [0.9, 0.9, 0.9], [0.2, 0.25, 0.35], 1.0))] + list(extra)
+    return SceneDescription(tuple(objs), _light(), np.array([0.05, 0.05, 0.08]))
+
+
+def test_dome_rig_degenerate_and_hemisphere():
+    from paper_2604_02851_b200.engine import build_dome_rig
+    poses, _ = build_dome_rig([1, 0, 2], heading=0.0, n_cameras=1, radius=3.0)
+    np.testing.assert_allclose(poses[0].position, [1, 3, 2], atol=1e-12)
+    np.testing.assert_allclose(poses[0].forward(), [0, -1, 0], atol=1e-12)
+    poses, _ = build_dome_rig([1, 0, 2], heading=0.3, n_cameras=10, radius=3.0)
+    for p in poses:
+        off = p.position - np.array([1, 0, 2.0])
+        assert np.linalg.norm(off) == pytest.approx(3.0) and off[1] >= 0
+        np.testing.assert_allclose(p.forward(), -off / np.linalg.norm(off), atol=1e-9)
+
+
+def test_duplicate_dynamic_ids_rejected():
+    from paper_2604_02851_b200.scene import Albedo, SceneDescription, SceneObject, Sphere
+    b = SceneObject(3, Sphere([0, 0.5, 0], 0.5), Albedo("solid", [0.8, 0.2, 0.15]))
+    with pytest.raises(ValueError):
+        SceneDescription((b, b), _light())
+
+
+@pytest.mark.gpu
+def test_gpu_rotating_checker_box_texture_is_rest_frame():
+    require_gpu()
+    from paper_2604_02851_b200 import engine
+    from paper_2604_02851_b200.geometry import CameraIntrinsics, look_at
+    from paper_2604_02851_b200.scene import Albedo, Animation, Box, SceneDescription, SceneObject
+    box = SceneObject(2, Box([0, 0.5, 0], [0.5, 0.5, 0.5]), Albedo("checker", [1, 1, 1], [0, 0, 0], 0.25),
+                      Animation(kind="rotate", axis=[0, 1, 0], deg_per_s=90.0, anchor=[0, 0, 0]))
+    scene = SceneDescription((box,), _light())
+    pose, intr = look_at([0, 2, -3], [0, 0.5, 0]), CameraIntrinsics(32, 32, 1.0)
+    img0 = engine.render_ground_truth(scene, pose, intr, transforms=scene.transforms_at(0.0))
+    img4 = engine.render_ground_truth(scene, pose, intr, transforms=scene.transforms_at(4.0))
+    img1 = engine.render_ground_truth(scene, pose, intr, transforms=scene.transforms_at(0.5))
+    np.testing.assert_allclose(img0, img4, atol=1e-9)
+    assert np.abs(img0 - img1).max() > 0.1  # 45 degrees later the pattern moved
+
+
+@pytest.mark.gpu
+def test_gpu_cull_single_identical_and_fronto_parallel():
+    require_gpu()
+    from paper_2604_02851_b200 import engine
+    from paper_2604_02851_b200.geometry import CameraIntrinsics, look_at
+    from paper_2604_02851_b200.scene import Albedo, Plane, SceneDescription, SceneObject
+    scene = _floor()
+    intr = CameraIntrinsics(16, 16, 1.2)
+    pose = look_at([0, 3, -3], [0, 0, 0])
+    b1 = engine.capture_input_buffers(scene, pose, intr)
+    assert engine.cull_input_samples([b1]).count == int(b1.valid.sum())
+    b2 = engine.capture_input_buffers(scene, pose, intr)
+    batch = engine.cull_input_samples([b1, b2])
+    assert batch.count == int(b1.valid.sum()) and (batch.camera_indices == 0).all()
+    plane = SceneDescription((SceneObject(0, Plane([0, 0, 0], [0, 1, 0], (3, 3)), Albedo("solid", [0.5] * 3)),), _light())
+    intr = CameraIntrinsics(24, 24, 1.2)
+    top = engine.capture_input_buffers(plane, look_at([0, 4, 0.01], [0, 0, 0]), intr)
+    grazing = engine.capture_input_buffers(plane, look_at([0, 0.3, -4.5], [0, 0, 0]), intr)
+    batch = engine.cull_input_samples([grazing, top])  # grazing gets the lower index on purpose
+    assert (batch.camera_indices == 1).mean() > 0.95
+
+
+@pytest.mark.gpu
+def test_gpu_ortho_depth_light_camera_and_depth_far():
+    require_gpu()
+    from paper_2604_02851_b200 import engine
+    from paper_2604_02851_b200.geometry import CameraIntrinsics, look_at
+    from paper_2604_02851_b200.scene import Albedo, SceneObject, Sphere
+    scene = _floor([SceneObject(1, Sphere([0, 0.5, 0], 0.5), Albedo("solid", [0.8, 0.2, 0.15]))])
+    cam = engine.build_light_camera([-4, 0, -4], [4, 1, 4], scene.light.direction, resolution=64)
+    depth = engine.render_ortho_depth(scene, cam)
+    assert depth.shape == (64, 64) and (depth < cam.far).any() and (depth == cam.far).any()
+    d = engine.render_depth(_floor(), look_at([0, 2, -4], [0, 0, 4]), CameraIntrinsics(16, 16, 1.2, far=50.0))
+    assert (d == 50.0).any() and (d < 50.0).any()
