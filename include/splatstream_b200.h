@@ -418,7 +418,7 @@ typedef struct {
 } ss_scene;
 
 typedef struct {
-    int32_t kind;                    /* 0 pinhole (geometry.py:238), 1 orthographic (geometry.py:273) */
+    int32_t kind;                    /* 0 pinhole (geometry.py:238), 1 orthographic (geometry.py:273), 2 rays */
     int32_t width, height;
     int32_t _pad;
     double position[3];
@@ -427,6 +427,11 @@ typedef struct {
     double half_width, half_height;  /* orthographic */
     double far;                      /* depth_or_far where a ray misses */
     double footprint_scale;          /* 2 tan(fov_y / 2) / height (capture buffers) */
+    /* kind 2, explicit rays (engine.py:88 trace): width = ray count, height = 1;
+     * device (n, 3) arrays, stride 3 per ray or 0 = one vector broadcast to all */
+    const double* ray_origins;
+    const double* ray_dirs;
+    int32_t origin_stride, dir_stride;
 } ss_engine_camera;
 
 typedef struct {  /* (H, W[, 3]) row-major device buffers; NULL = not written */
@@ -442,6 +447,8 @@ typedef struct {  /* (H, W[, 3]) row-major device buffers; NULL = not written */
     double* depth;
     double* footprint;
     uint8_t* lit;
+    double* t;              /* trace: hit distance, inf where missed */
+    int32_t* object_index;  /* trace: index into scene.objects, -1 where missed */
 } ss_engine_out;
 
 int ss_engine_render(ss_ctx* ctx, const ss_scene* scene, const ss_engine_camera* cam, const ss_engine_out* out);

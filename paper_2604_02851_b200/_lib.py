@@ -118,12 +118,13 @@ class SSScene(C.Structure):
 class SSEngineCamera(C.Structure):
     _fields_ = [("kind", i32), ("width", i32), ("height", i32), ("_pad", i32), ("position", f64 * 3), ("R", f64 * 9),
                 ("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64), ("half_width", f64), ("half_height", f64),
-                ("far", f64), ("footprint_scale", f64)]
+                ("far", f64), ("footprint_scale", f64), ("ray_origins", vp), ("ray_dirs", vp), ("origin_stride", i32),
+                ("dir_stride", i32)]
 
 
 class SSEngineOut(C.Structure):
     _fields_ = [(n, vp) for n in ("gt_f32", "gt_f64", "depth_or_far", "world_pos", "valid", "normal", "albedo",
-                                  "shaded", "object_id", "depth", "footprint", "lit")]
+                                  "shaded", "object_id", "depth", "footprint", "lit", "t", "object_index")]
 
 
 class SSCullCamera(C.Structure):

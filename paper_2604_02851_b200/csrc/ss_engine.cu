@@ -238,6 +238,13 @@ __global__ void __launch_bounds__(EN_THREADS) k_engine(SceneArgs S, ss_engine_ca
             o[k] = cam.position[k];
         }
         d_bcast = false;
+    } else if (cam.kind == 2) {  // explicit rays (trace, engine.py:88): origins broadcast against dirs
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            o[k] = cam.ray_origins[(int64_t)cam.origin_stride * p + k];
+            d[k] = cam.ray_dirs[(int64_t)cam.dir_stride * p + k];
+        }
+        d_bcast = cam.dir_stride == 0;
     } else {  // OrthoCamera.pixel_origins (geometry.py:273-281), rays along +Z
         const double u = dvd(add((double)i, 0.5), (double)cam.width);
         const double v = dvd(add((double)jrow, 0.5), (double)cam.height);
@@ -294,6 +301,8 @@ __global__ void __launch_bounds__(EN_THREADS) k_engine(SceneArgs S, ss_engine_ca
         }
         if (out.lit) out.lit[p] = valid && lit;
     }
+    if (out.t) out.t[p] = h.t;
+    if (out.object_index) out.object_index[p] = h.k;
     if (out.valid) out.valid[p] = valid;
     if (out.world_pos)
         for (int k = 0; k < 3; ++k) out.world_pos[3 * p + k] = valid ? wp[k] : 0.0;
@@ -315,7 +324,10 @@ __global__ void __launch_bounds__(EN_THREADS) k_engine(SceneArgs S, ss_engine_ca
 
 extern "C" int ss_engine_render(ss_ctx* ctx, const ss_scene* scene, const ss_engine_camera* cam, const ss_engine_out* out) {
     if (!ctx || !scene || !cam || !out) return SS_ERR_INVALID;
-    if (cam->width < 1 || cam->height < 1 || (cam->kind != 0 && cam->kind != 1)) return ss_fail(ctx, SS_ERR_INVALID, "bad camera");
+    if (cam->width < 1 || cam->height < 1 || cam->kind < 0 || cam->kind > 2) return ss_fail(ctx, SS_ERR_INVALID, "bad camera");
+    if (cam->kind == 2 && (!cam->ray_origins || !cam->ray_dirs || cam->height != 1 ||
+                           (cam->origin_stride != 0 && cam->origin_stride != 3) || (cam->dir_stride != 0 && cam->dir_stride != 3)))
+        return ss_fail(ctx, SS_ERR_INVALID, "rays: device origins/dirs with stride 0 or 3, height 1");
     if (scene->n_objects < 0 || scene->n_objects > 256 || (scene->n_objects && !scene->objects))
         return ss_fail(ctx, SS_ERR_INVALID, "0..256 scene objects");
     for (int k = 0; k < scene->n_objects; ++k) {

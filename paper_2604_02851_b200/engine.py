@@ -130,6 +130,78 @@ def _ortho(oc):
     return cam
 
 
+@dataclass
+class Hits:
+    """Nearest hits of a ray batch (ref engine.py:24-33)."""
+
+    t: np.ndarray             # ray parameter, inf where missed
+    object_index: np.ndarray  # index into scene.objects, -1 where missed
+    world_point: np.ndarray
+    normal: np.ndarray        # world frame, unit, facing the ray origin
+    albedo: np.ndarray
+
+    @property
+    def valid(self) -> np.ndarray:
+        return np.isfinite(self.t)
+
+
+def _broadcast_row(a):
+    """The single (3,) vector a (..., 3) array repeats, or None."""
+    flat = a.reshape(-1, 3) if a.flags.c_contiguous else None
+    if flat is not None:
+        return None
+    st = a.strides[:-1]
+    return a.reshape(-1)[:3].copy() if all(x == 0 for x in st) else None
+
+
+def trace(scene, origins, dirs, transforms=None, device=None) -> Hits:
+    """ref engine.py:88-127 on the GPU: nearest hit of every ray; `origins`
+    broadcasts against `dirs`.  A `dirs` that is one broadcast vector (the
+    shadow rays' -light.direction) follows numpy's broadcast-matmul order;
+    anything else is taken row by row (numpy's BLAS order for >= 2 rays)."""
+    import torch
+    dev = _dev(device)
+    dirs = np.asarray(dirs, dtype=np.float64)
+    shape = dirs.shape[:-1]
+    n = int(np.prod(shape)) if shape else 1
+    out = {"t": torch.empty(max(n, 1), dtype=torch.float64, device=dev),
+           "object_index": torch.empty(max(n, 1), dtype=torch.int32, device=dev),
+           "world_pos": torch.empty((max(n, 1), 3), dtype=torch.float64, device=dev),
+           "normal": torch.empty((max(n, 1), 3), dtype=torch.float64, device=dev),
+           "albedo": torch.empty((max(n, 1), 3), dtype=torch.float64, device=dev)}
+    if n:
+        cam = _lib.SSEngineCamera()
+        cam.kind, cam.width, cam.height = 2, n, 1
+        drow = _broadcast_row(dirs)
+        d_t = torch.from_numpy(drow if drow is not None else np.array(dirs, copy=True).reshape(-1, 3)).to(dev)
+        o = np.asarray(origins, dtype=np.float64)
+        orow = o.reshape(3) if o.shape == (3,) else _broadcast_row(np.broadcast_to(o, dirs.shape))
+        o_t = torch.from_numpy(orow.copy() if orow is not None else
+                               np.array(np.broadcast_to(o, dirs.shape), copy=True).reshape(-1, 3)).to(dev)
+        cam.ray_origins, cam.ray_dirs = o_t.data_ptr(), d_t.data_ptr()
+        cam.origin_stride = 0 if orow is not None else 3
+        cam.dir_stride = 0 if drow is not None else 3
+        _run(scene, cam, {"t": out["t"], "object_index": out["object_index"], "world_pos": out["world_pos"],
+                          "normal": out["normal"], "albedo": out["albedo"]}, None, transforms, dev.index)
+    h = {k: v[:n].cpu().numpy() for k, v in out.items()}
+    # world_pos is written as 0 for misses; trace's world_point is origin + 0 * dir there
+    t = h["t"].reshape(shape)
+    ob = np.broadcast_to(np.asarray(origins, dtype=np.float64), dirs.shape)
+    wp = np.where(np.isfinite(t)[..., None], h["world_pos"].reshape(dirs.shape), ob)
+    return Hits(t=t, object_index=h["object_index"].reshape(shape).astype(np.int64), world_point=wp,
+                normal=h["normal"].reshape(dirs.shape), albedo=h["albedo"].reshape(dirs.shape))
+
+
+def light_occluded(scene, points, normals, light, transforms=None, device=None) -> np.ndarray:
+    """ref engine.py:130-137: a shadow ray from p + 1e-5 n toward the light hits geometry."""
+    points = np.asarray(points, dtype=np.float64)
+    if points.size == 0:
+        return np.zeros(points.shape[:-1], dtype=bool)
+    origins = points + 1e-5 * np.asarray(normals, dtype=np.float64)
+    d = np.broadcast_to(-np.asarray(light.direction, dtype=np.float64), points.shape)
+    return trace(scene, origins, d, transforms, device).valid
+
+
 def _run(scene, cam, bufs, light=None, transforms=None, device=None):
     c = _lib.ctx(device)
     c.bind_stream()
@@ -338,5 +410,5 @@ def build_dome_rig(center, heading: float, n_cameras: int, radius: float, width:
     return poses, CameraIntrinsics(width=width, height=height, fov_y=fov_y, near=near, far=far)
 
 
-__all__ = ["InputBuffers", "SampleBatch", "cull_input_samples", "init_gaussians", "scene_struct", "render_ground_truth", "render_ground_truth_device",
+__all__ = ["Hits", "trace", "light_occluded", "InputBuffers", "SampleBatch", "cull_input_samples", "init_gaussians", "scene_struct", "render_ground_truth", "render_ground_truth_device",
            "capture_input_buffers", "render_depth", "render_ortho_depth", "build_light_camera", "build_dome_rig"]

@@ -711,6 +711,25 @@ def engine_cases():
             st.add(dict(kind="ortho", name=f"{name}_t{time}_light", scene=sd, width=lc.width, height=lc.height,
                         half_width=lc.half_width, half_height=lc.half_height, far=lc.far),
                    transforms=tf_arr, position=lc.pose.position, R=lc.pose.rotation(), ortho_depth=od)
+    # trace (engine.py:88) on arbitrary rays: per-ray directions, and shadow-style rays
+    # sharing one broadcast direction (light_occluded, engine.py:130-137)
+    from splatstream.engine import light_occluded, trace
+    rng = np.random.default_rng(99)
+    for name, sd in ENGINE_SCENES.items():
+        scene = scene_from_dict(sd)
+        tfs = scene.transforms_at(0.7)
+        tf_arr = np.array([[oid] + list(q) + list(t) for oid, (q, t) in sorted(tfs.items())])
+        org = rng.uniform(-3, 3, (500, 3)) + np.array([0, 2.5, 0])
+        tgt = rng.uniform(-1.5, 1.5, (500, 3)) * np.array([1, 0.5, 1])
+        dirs = tgt - org
+        dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+        h = trace(scene, org, dirs, tfs)
+        pts = org[:200] * np.array([1, 0, 1])
+        nrm = np.tile([0.0, 1.0, 0.0], (200, 1))
+        occ = light_occluded(scene, pts, nrm, scene.light, tfs)
+        st.add(dict(kind="trace", name=f"{name}_trace", scene=sd), transforms=tf_arr, origins=org, dirs=dirs,
+               t=h.t, object_index=h.object_index, world_point=h.world_point, normal=h.normal, albedo=h.albedo,
+               occ_points=pts, occ_normals=nrm, occluded=occ)
     st.save("engine_cases")
 
 

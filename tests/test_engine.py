@@ -263,3 +263,22 @@ def test_gpu_ortho_depth_light_camera_and_depth_far():
     assert depth.shape == (64, 64) and (depth < cam.far).any() and (depth == cam.far).any()
     d = engine.render_depth(_floor(), look_at([0, 2, -4], [0, 0, 4]), CameraIntrinsics(16, 16, 1.2, far=50.0))
     assert (d == 50.0).any() and (d < 50.0).any()
+
+
+TRACE = [c for c in CASES if c["kind"] == "trace"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", TRACE, ids=lambda c: c["name"])
+def test_gpu_trace_and_light_occluded_match_reference(c):
+    require_gpu()
+    from paper_2604_02851_b200 import engine
+    from paper_2604_02851_b200.scene import scene_from_dict
+    scene = scene_from_dict(c["scene"])
+    tf = c.a("transforms")
+    tfs = {int(r[0]): (r[1:5], r[5:8]) for r in tf}
+    h = engine.trace(scene, c.a("origins"), c.a("dirs"), tfs)
+    for k in ("t", "object_index", "world_point", "normal", "albedo"):
+        _eq(np.asarray(getattr(h, k)), c.a(k), k)
+    occ = engine.light_occluded(scene, c.a("occ_points"), c.a("occ_normals"), scene.light, tfs)
+    _eq(occ, c.a("occluded"), "occluded")
