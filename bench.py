@@ -423,6 +423,11 @@ def run_ours(args):
                "path": "optim.step (ground truth H2D from pinned host memory, loss read back) + the tick's "
                        "TENSOR_DELTA frames (device CRC-32) read back into pinned host memory"}
 
+    # ---- config 5: client-viewpoint rendering, views sharded over the ranks (no collective)
+    client_rec = None
+    if not args.no_e2e:
+        client_rec = client_render_bench(args, rank, world, pg, dev, torch)
+
     # ---- the engine stand-in and a full server tick on the device (§8f rank 4), rank 0,
     # after the timed runs (it trains the model further and holds its own buffers)
     if rank == 0:
@@ -451,7 +456,7 @@ def run_ours(args):
            "gpu_launches": launches, "clocks": clock_rec,
            "kernel_ms_per_step": {k: round(v, 4) for k, v in per_step.items()},
            "evaluated_pairs_per_view": evals_per_view,
-           "delta_encode": enc, "pool_maintenance": pool_rec, "server_tick_zlib": zlib_rec, "engine": engine_rec, "fp32_peak_tflops_measured": fp32_peak,
+           "delta_encode": enc, "pool_maintenance": pool_rec, "server_tick_zlib": zlib_rec, "engine": engine_rec, "client_render": client_rec, "fp32_peak_tflops_measured": fp32_peak,
            "precision": "fp64 preprocess/windows/depth keys, fp32 blend + chain rule, fp64 Adam moments"}
     print(json.dumps(out), flush=True)
     if pg is not None:
@@ -617,6 +622,44 @@ ENGINE_SCENE = {  # the engine stand-in's test scene (tests/golden/make_golden.p
         {"id": 2, "shape": {"kind": "box", "center": [1.2, 0.4, -0.6], "half_extents": [0.3, 0.4, 0.25]},
          "albedo": {"kind": "checker", "colors": [[0.1, 0.7, 0.2], [0.9, 0.8, 0.1]], "scale": 0.25}},
     ]}
+
+
+def client_render_bench(args, rank, world, pg, dev, torch, n=2_000_000, views=64, reps=2):
+    """Config 5: 64 client viewpoints of a 2M-Gaussian SH3 model at 1080p,
+    the viewpoints sharded round-robin over the ranks with no collective
+    (SURVEY §8e); frames/s of the whole job, timed on the device (max over
+    ranks).  The model is the synthetic field, replicated per rank."""
+    import torch.distributed as dist
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.render import render_device
+    m = DeviceModel.from_host(synth.random_field(n, 3, args.width, args.height, seed=7), dev.index)
+    intr = synth.intrinsics(args.width, args.height)
+    light = synth.light()
+    allp = synth.ring_poses(views, radius=0.6)
+    mine = allp[rank::world]
+    out = torch.empty((args.height, args.width, 3), dtype=torch.float32, device=dev)
+    for p in mine[:2]:
+        render_device(m, p, intr, light, out=out)
+    torch.cuda.synchronize()
+    if pg is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        for p in mine:
+            render_device(m, p, intr, light, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    del m
+    return {"value": views * reps / (ms / 1e3), "unit": "frames/s", "viewpoints": views, "gaussians": n,
+            "sh_degree": 3, "resolution": [args.width, args.height], "ms_per_frame_per_gpu": ms / (reps * len(mine)),
+            "note": "render_device (preprocess, depth sort, binning, tile sort, forward) per viewpoint; sharded "
+                    "round-robin over the ranks, no collective; device time, max over ranks"}
 
 
 def engine_bench(poses, intr, torch, reps=5):
