@@ -284,6 +284,11 @@ int ss_apply_object_transform(ss_ctx* ctx, ss_model* model, int32_t object_id, c
 /* ObjectRegistry.refresh_locals(): ref model.py:539-555, for rows of one object. */
 int ss_refresh_object_locals(ss_ctx* ctx, const ss_model* model, int32_t object_id, int32_t active_only,
                              double* local_means, double* local_rots, const double q[4], const double t[3]);
+/* The same for the rows listed in `rows` (device, n_rows entries) that belong to
+ * object_id (ref model.py:371-387 with an explicit row set). */
+int ss_refresh_object_locals_rows(ss_ctx* ctx, const ss_model* model, int32_t object_id, const int64_t* rows,
+                                  int64_t n_rows, double* local_means, double* local_rots, const double q[4],
+                                  const double t[3]);
 
 /* ---- client ingestion: the decode side of the codec ----
  * The host parses the header and decompresses (zlib) exactly like the

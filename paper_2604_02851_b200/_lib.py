@@ -175,6 +175,8 @@ _SIGS = {
     "ss_apply_object_transform": (i32, [vp, C.POINTER(SSModel), i32, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
     "ss_refresh_object_locals": (i32, [vp, C.POINTER(SSModel), i32, i32, vp, vp, C.POINTER(f64),
                                        C.POINTER(f64)]),
+    "ss_refresh_object_locals_rows": (i32, [vp, C.POINTER(SSModel), i32, vp, i64, vp, vp, C.POINTER(f64),
+                                            C.POINTER(f64)]),
     "ss_decode_delta": (i32, [vp, C.POINTER(SSDeltaApply), vp, vp]),
     "ss_apply_delta": (i32, [vp, C.POINTER(SSDeltaApply), vp]),
     "ss_decode_snapshot": (i32, [vp, C.POINTER(SSSnapshotDecode)]),

@@ -59,9 +59,10 @@ __global__ void k_apply_transform(float* __restrict__ means, float* __restrict__
 
 __global__ void k_refresh_locals(const float* __restrict__ means, const float* __restrict__ quats,
                                  const int32_t* __restrict__ ids, int64_t n, double* __restrict__ lm,
-                                 double* __restrict__ lr, RigidConst c) {
+                                 double* __restrict__ lr, RigidConst c, const int64_t* __restrict__ rows) {
     const double qc[4] = {c.q[0], -c.q[1], -c.q[2], -c.q[3]};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t ii = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = rows ? rows[ii] : ii;
         if (ids[i] != c.oid) continue;
         double d[3];
         for (int k = 0; k < 3; ++k) d[k] = (double)means[3 * i + k] - c.t[k];
@@ -123,7 +124,20 @@ int ss_refresh_object_locals(ss_ctx* ctx, const ss_model* m, int32_t oid, int32_
     if (n == 0) return SS_OK;
     RigidConst c;
     rigid_const(q, t, oid, c);
-    k_refresh_locals<<<gridn(ctx, n), 256, 0, ctx->stream>>>(m->means, m->quaternions, m->object_ids, n, lm, lr, c);
+    k_refresh_locals<<<gridn(ctx, n), 256, 0, ctx->stream>>>(m->means, m->quaternions, m->object_ids, n, lm, lr, c,
+                                                            nullptr);
+    SS_CHECK_LAUNCH(ctx);
+    return SS_OK;
+}
+
+int ss_refresh_object_locals_rows(ss_ctx* ctx, const ss_model* m, int32_t oid, const int64_t* rows, int64_t n_rows,
+                                  double* lm, double* lr, const double q[4], const double t[3]) {
+    if (!ctx || !m || !lm || !lr || (n_rows && !rows) || n_rows < 0) return SS_ERR_INVALID;
+    if (n_rows == 0) return SS_OK;
+    RigidConst c;
+    rigid_const(q, t, oid, c);
+    k_refresh_locals<<<gridn(ctx, n_rows), 256, 0, ctx->stream>>>(m->means, m->quaternions, m->object_ids, n_rows, lm, lr,
+                                                                 c, rows);
     SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }

@@ -41,13 +41,13 @@ HERE = pathlib.Path(__file__).resolve().parent
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
-    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool engine expand")
+    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool engine expand objects")
     args = ap.parse_args()
     ref = pathlib.Path(args.ref)
     sys.path.insert(0, str(ref / "src"))
     import splatstream  # noqa: F401  (the reference)
 
-    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool", "engine", "expand"}
+    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool", "engine", "expand", "objects"}
     if "wire" in want:
         wire = HERE / "wire"
         if wire.exists():
@@ -57,7 +57,7 @@ def main():
         assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
     for name, fn in (("codec", codec_cases), ("raster", raster_cases), ("step", step_cases), ("dyn", dyn_cases),
                      ("ingest", ingest_cases), ("pool", pool_cases), ("engine", engine_cases),
-                     ("expand", expand_cases)):
+                     ("expand", expand_cases), ("objects", objects_cases)):
         if name in want:
             fn()
     print("golden vectors written to", HERE)
@@ -766,6 +766,44 @@ def expand_cases():
         st.add(dict(kind="expand", name=f"{name}_{ncam}cams" + ("_dup" if dup is not None else ""), n_cams=len(bufs),
                     kept=int(sb.count)), **arrays)
     st.save("expand_cases")
+
+
+def objects_cases():
+    """ObjectRegistry (ref model.py:326-404) through a server-like sequence:
+    refresh all, move object 1, optimizer-style edits of object 2 rows and a
+    refresh of just those rows, a row permutation, then move object 2."""
+    from splatstream.geometry import quat_from_axis_angle
+    from splatstream.model import ObjectRegistry, PermuteRecord, apply_mutation
+    st = Store()
+    rng = np.random.default_rng(2024)
+    for n, deg in ((3000, 0), (20000, 1)):
+        m = random_model(rng, n, deg)
+        m.object_ids[:] = rng.choice([0, 0, 1, 2], n).astype(np.int32)
+        reg = ObjectRegistry()
+        reg.set_transform(1, quat_from_axis_angle([0, 1, 0], 0.3), [0.5, 0.0, -0.2])
+        reg.set_transform(2, quat_from_axis_angle([1, 0.2, 0], -0.7), [0.0, 0.4, 0.1])
+        arrays = {f"init_{k}": np.array(v, copy=True) for k, v in model_arrays(m).items()}
+        reg.refresh_locals(m)
+        arrays.update(lm0=reg.local_means.copy(), lr0=reg.local_rotations.copy())
+        q1, t1 = quat_from_axis_angle([0.3, 1, 0], 0.9), np.array([0.2, -0.1, 0.7])
+        rows1 = reg.apply_transform(m, 1, q1, t1)
+        arrays.update(q1=q1, t1=t1, rows1=rows1, means1=m.means.copy(), quats1=m.quaternions.copy())
+        sub = np.sort(rng.choice(n, n // 5, replace=False))
+        m.means[sub] += rng.normal(0, 1e-2, (len(sub), 3)).astype(np.float32)
+        arrays.update(sub=sub, means_edit=m.means.copy())
+        reg.refresh_locals(m, sub)
+        arrays.update(lm2=reg.local_means.copy(), lr2=reg.local_rotations.copy())
+        perm = rng.permutation(n)
+        rec = PermuteRecord(perm, m.active_count)
+        apply_mutation(m, rec)
+        reg.resize(rec)
+        q2, t2 = quat_from_axis_angle([0, 0, 1], 1.3), np.array([-0.3, 0.2, 0.0])
+        rows2 = reg.apply_transform(m, 2, q2, t2)
+        arrays.update(perm=perm, q2=q2, t2=t2, rows2=rows2, means3=m.means.copy(), quats3=m.quaternions.copy(),
+                      lm3=reg.local_means.copy(), lr3=reg.local_rotations.copy())
+        st.add(dict(kind="objects", name=f"objects_{n}_deg{deg}", n=n, degree=deg, active=int(m.active_count)),
+               **arrays)
+    st.save("objects_cases")
 
 if __name__ == "__main__":
     main()
