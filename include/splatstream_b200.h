@@ -102,6 +102,15 @@ int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const 
                    const float* const* g9, const uint32_t* const* rinv, const int64_t* subset, int64_t n_in,
                    float* grad);
 
+/* composite(): ref render.py:317-336 on prepared splats (device arrays, n
+ * splats already in draw order = prep.order): fp64 front-to-back blend of the
+ * given windows (x0, x1, y0, y1; ref render.py:293-301), centres, inverse
+ * covariances (a, b, c) = (inv[0][0], inv[0][1], inv[1][1]), opacities and
+ * colours.  img (H, W, 3) and T (H, W, may be NULL) are float64 device. */
+int ss_composite(ss_ctx* ctx, int64_t n, const double* mu2d, const double* inv2d, const double* opacity,
+                 const double* color, const int32_t* windows, int32_t width, int32_t height, const double* background,
+                 double* img, double* T);
+
 /* Host-readable summary of the last render/backward call. */
 typedef struct {
     int64_t visible;         /* splats passing the near test */

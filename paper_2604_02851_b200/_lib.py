@@ -185,6 +185,7 @@ _SIGS = {
     "ss_cull_input_samples": (i32, [vp, C.POINTER(SSCullCamera), i32, C.POINTER(SSSampleBatch), i64, C.POINTER(i64),
                                     C.POINTER(f64)]),
     "ss_init_gaussians": (i32, [vp, C.POINTER(SSSampleBatch), i64, C.POINTER(SSModel), i64]),
+    "ss_composite": (i32, [vp, i64, vp, vp, vp, vp, vp, i32, i32, C.POINTER(f64), vp, vp]),
     "ss_chain_views": (i32, [vp, C.POINTER(SSModel), vp, vp, i32, C.POINTER(vp), C.POINTER(vp), vp, i64, vp]),
     "ss_engine_render": (i32, [vp, C.POINTER(SSScene), C.POINTER(SSEngineCamera), C.POINTER(SSEngineOut)]),
     "ss_grid_rebuild": (i32, [vp, vp, i64, C.POINTER(SSGridSpec), vp, vp, vp, vp, C.POINTER(i64)]),

@@ -1381,67 +1381,19 @@ int validate(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_rend
 }
 
 // K1..K4: preprocess, depth sort, count/scan/emit, tile sort, ranges.
+// (tile, splat) pairs of a depth-ordered splat set: counts per rank, scan,
+// warp-cooperative emission, stable tile sort, per-tile ranges.  Needs b's
+// dkey64 (~0 = culled), dvals (input index by rank), rec and the geometry.
 template <typename R>
-int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L, const ss_render_opts* o,
-               Bins& b, DebugOut* dbg) {
+int bin_pairs(ss_ctx* ctx, Bins& b) {
     cudaStream_t s = ctx->stream;
-    b.n_in = o->subset ? o->subset_count : m->count;
-    b.tiles_x = (cam->width + TILE - 1) / TILE;
-    b.tiles_y = (cam->height + TILE - 1) / TILE;
-    b.n_tiles = b.tiles_x * b.tiles_y;
-    b.tile_bits = 1;
-    while ((1 << b.tile_bits) < b.n_tiles) ++b.tile_bits;
     const int64_t n = b.n_in;
-    const int64_t na = n > 0 ? n : 1;
-    b.dkey64 = SS_SCRATCH(ctx, uint64_t, na);
-    b.dkeys = SS_SCRATCH(ctx, uint32_t, na);
-    unsigned long long* kminmax = SS_SCRATCH(ctx, unsigned long long, 2);
-    b.dvals = SS_SCRATCH(ctx, uint32_t, na);
-    uint32_t* kalt = SS_SCRATCH(ctx, uint32_t, na);
-    uint32_t* valt = SS_SCRATCH(ctx, uint32_t, na);
-    b.mu = SS_SCRATCH(ctx, double2, na);
-    b.roffj = SS_SCRATCH(ctx, uint64_t, na);
-    b.roff = SS_SCRATCH(ctx, uint64_t, na);
-    b.rcnt = SS_SCRATCH(ctx, uint32_t, na);
-    b.rinv = SS_SCRATCH(ctx, uint32_t, na);
-    b.rec = ss_scratch(ctx, sizeof(SplatRec<R>) * na);
-    b.ranges = SS_SCRATCH(ctx, uint2, b.n_tiles);
     uint64_t* total = SS_SCRATCH(ctx, uint64_t, 1);
-    if (!b.dkey64 || !kminmax || !b.dkeys || !b.dvals || !kalt || !valt || !b.mu || !b.roffj || !b.roff || !b.rcnt || !b.rinv || !b.rec || !b.ranges ||
-        !total)
-        return SS_ERR_CUDA;
-    SS_CUDA(ctx, cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.n_tiles, s));
-    DebugOut none;
-    memset(&none, 0, sizeof(none));
+    if (!total) return SS_ERR_CUDA;
+    ss_tic(ctx, KC_BIN);
     if (n > 0) {
-        ss_tic(ctx, KC_PREPROCESS);
-        SS_CUDA(ctx, ss_launch((k_init_minmax), dim3(1), dim3(1), 0, s, kminmax));
-        SS_CHECK_LAUNCH(ctx);
-#define SS_PRE(DEG)                                                                                      \
-    SS_CUDA(ctx, ss_launch((k_preprocess<DEG, R>), dim3(gridn(ctx, n, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
-                                                         b.dvals, (SplatRec<R>*)b.rec, b.mu, dbg ? *dbg : none,  \
-                                                         kminmax))
-        switch (m->sh_degree) {
-            case 0: SS_PRE(0); break;
-            case 1: SS_PRE(1); break;
-            case 2: SS_PRE(2); break;
-            default: SS_PRE(3); break;
-        }
-#undef SS_PRE
-        SS_CHECK_LAUNCH(ctx);
-        ss_toc(ctx, KC_PREPROCESS);
-        ss_tic(ctx, KC_DEPTH_SORT);
-        SS_CUDA(ctx, ss_launch((k_key32), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkey64, n, kminmax, b.dkeys));
-        SS_CHECK_LAUNCH(ctx);
-        SS_TRY(ss_radix_sort_u32(ctx, b.dkeys, b.dvals, kalt, valt, n, 32));
-        SS_CUDA(ctx, ss_launch((k_fix_ties), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkeys, b.dvals, b.dkey64, n));
-        SS_CHECK_LAUNCH(ctx);
-        ss_toc(ctx, KC_DEPTH_SORT);
-        ss_tic(ctx, KC_BIN);
         SS_CUDA(ctx, ss_launch((k_count<R>), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkey64, b.dvals, (const SplatRec<R>*)b.rec, n, b.rcnt, b.rinv));
         SS_CHECK_LAUNCH(ctx);
-    } else {
-        ss_tic(ctx, KC_BIN);
     }
     SS_TRY(ss_scan_u32_to_u64(ctx, b.rcnt, b.roff, n, total));
     ss_toc(ctx, KC_BIN);
@@ -1470,6 +1422,64 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         ss_toc(ctx, KC_BIN);
     }
     return SS_OK;
+}
+
+template <typename R>
+int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L, const ss_render_opts* o,
+               Bins& b, DebugOut* dbg) {
+    cudaStream_t s = ctx->stream;
+    b.n_in = o->subset ? o->subset_count : m->count;
+    b.tiles_x = (cam->width + TILE - 1) / TILE;
+    b.tiles_y = (cam->height + TILE - 1) / TILE;
+    b.n_tiles = b.tiles_x * b.tiles_y;
+    b.tile_bits = 1;
+    while ((1 << b.tile_bits) < b.n_tiles) ++b.tile_bits;
+    const int64_t n = b.n_in;
+    const int64_t na = n > 0 ? n : 1;
+    b.dkey64 = SS_SCRATCH(ctx, uint64_t, na);
+    b.dkeys = SS_SCRATCH(ctx, uint32_t, na);
+    unsigned long long* kminmax = SS_SCRATCH(ctx, unsigned long long, 2);
+    b.dvals = SS_SCRATCH(ctx, uint32_t, na);
+    uint32_t* kalt = SS_SCRATCH(ctx, uint32_t, na);
+    uint32_t* valt = SS_SCRATCH(ctx, uint32_t, na);
+    b.mu = SS_SCRATCH(ctx, double2, na);
+    b.roffj = SS_SCRATCH(ctx, uint64_t, na);
+    b.roff = SS_SCRATCH(ctx, uint64_t, na);
+    b.rcnt = SS_SCRATCH(ctx, uint32_t, na);
+    b.rinv = SS_SCRATCH(ctx, uint32_t, na);
+    b.rec = ss_scratch(ctx, sizeof(SplatRec<R>) * na);
+    b.ranges = SS_SCRATCH(ctx, uint2, b.n_tiles);
+    if (!b.dkey64 || !kminmax || !b.dkeys || !b.dvals || !kalt || !valt || !b.mu || !b.roffj || !b.roff || !b.rcnt || !b.rinv || !b.rec || !b.ranges)
+        return SS_ERR_CUDA;
+    SS_CUDA(ctx, cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.n_tiles, s));
+    DebugOut none;
+    memset(&none, 0, sizeof(none));
+    if (n > 0) {
+        ss_tic(ctx, KC_PREPROCESS);
+        SS_CUDA(ctx, ss_launch((k_init_minmax), dim3(1), dim3(1), 0, s, kminmax));
+        SS_CHECK_LAUNCH(ctx);
+#define SS_PRE(DEG)                                                                                      \
+    SS_CUDA(ctx, ss_launch((k_preprocess<DEG, R>), dim3(gridn(ctx, n, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
+                                                         b.dvals, (SplatRec<R>*)b.rec, b.mu, dbg ? *dbg : none,  \
+                                                         kminmax))
+        switch (m->sh_degree) {
+            case 0: SS_PRE(0); break;
+            case 1: SS_PRE(1); break;
+            case 2: SS_PRE(2); break;
+            default: SS_PRE(3); break;
+        }
+#undef SS_PRE
+        SS_CHECK_LAUNCH(ctx);
+        ss_toc(ctx, KC_PREPROCESS);
+        ss_tic(ctx, KC_DEPTH_SORT);
+        SS_CUDA(ctx, ss_launch((k_key32), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkey64, n, kminmax, b.dkeys));
+        SS_CHECK_LAUNCH(ctx);
+        SS_TRY(ss_radix_sort_u32(ctx, b.dkeys, b.dvals, kalt, valt, n, 32));
+        SS_CUDA(ctx, ss_launch((k_fix_ties), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkeys, b.dvals, b.dkey64, n));
+        SS_CHECK_LAUNCH(ctx);
+        ss_toc(ctx, KC_DEPTH_SORT);
+    }
+    return bin_pairs<R>(ctx, b);
 }
 
 template <typename R>
@@ -1577,6 +1587,27 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     return SS_OK;
 }
 
+// composite() of prepared splats already in draw order (ss_composite)
+__global__ void k_prep_recs(int64_t n, const double* __restrict__ mu2d, const double* __restrict__ inv2d,
+                            const double* __restrict__ opacity, const double* __restrict__ color,
+                            const int32_t* __restrict__ windows, SplatRec<double>* __restrict__ rec, double2* __restrict__ mu,
+                            uint64_t* __restrict__ dkey64, uint32_t* __restrict__ dvals) {
+    SS_PDL_WAIT();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        SplatRec<double> g;
+        for (int k = 0; k < 4; ++k) g.win[k] = windows[4 * j + k];
+        g.a = inv2d[3 * j];
+        g.b = inv2d[3 * j + 1];
+        g.c = inv2d[3 * j + 2];
+        g.o = opacity[j];
+        for (int c = 0; c < 3; ++c) g.col[c] = color[3 * j + c];
+        rec[j] = g;
+        mu[j] = make_double2(mu2d[2 * j], mu2d[2 * j + 1]);
+        dkey64[j] = 0;            // visible
+        dvals[j] = (uint32_t)j;   // rank = position in the draw order
+    }
+}
+
 __global__ void k_order_out(const uint64_t* dkey64, const uint32_t* dvals, const uint64_t* vpos, int64_t n,
                             int64_t* order) {
     SS_PDL_WAIT();
@@ -1622,6 +1653,51 @@ int ss_backward(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_l
     SS_TRY(ss_scratch_reset(ctx));
     return o->precision ? backward_t<double>(ctx, m, cam, L, o, gt, grad, loss, img, st)
                         : backward_t<float>(ctx, m, cam, L, o, gt, grad, loss, img, st);
+}
+
+int ss_composite(ss_ctx* ctx, int64_t n, const double* mu2d, const double* inv2d, const double* opacity, const double* color,
+                 const int32_t* windows, int32_t width, int32_t height, const double* background, double* img, double* T) {
+    if (!ctx || !img || !background || width < 1 || height < 1 || n < 0) return SS_ERR_INVALID;
+    if (n > 0 && (!mu2d || !inv2d || !opacity || !color || !windows)) return SS_ERR_INVALID;
+    if (n > 0xffffffffll) return ss_fail(ctx, SS_ERR_CAPACITY, "too many splats");
+    SS_TRY(ss_scratch_reset(ctx));
+    cudaStream_t s = ctx->stream;
+    Bins b;
+    memset(&b, 0, sizeof(b));
+    b.n_in = n;
+    b.tiles_x = (width + TILE - 1) / TILE;
+    b.tiles_y = (height + TILE - 1) / TILE;
+    b.n_tiles = b.tiles_x * b.tiles_y;
+    b.tile_bits = 1;
+    while ((1 << b.tile_bits) < b.n_tiles) ++b.tile_bits;
+    const int64_t na = n > 0 ? n : 1;
+    b.dkey64 = SS_SCRATCH(ctx, uint64_t, na);
+    b.dvals = SS_SCRATCH(ctx, uint32_t, na);
+    b.mu = SS_SCRATCH(ctx, double2, na);
+    b.roffj = SS_SCRATCH(ctx, uint64_t, na);
+    b.roff = SS_SCRATCH(ctx, uint64_t, na);
+    b.rcnt = SS_SCRATCH(ctx, uint32_t, na);
+    b.rinv = SS_SCRATCH(ctx, uint32_t, na);
+    b.rec = ss_scratch(ctx, sizeof(SplatRec<double>) * na);
+    b.ranges = SS_SCRATCH(ctx, uint2, b.n_tiles);
+    uint32_t* stop = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
+    if (!b.dkey64 || !b.dvals || !b.mu || !b.roffj || !b.roff || !b.rcnt || !b.rinv || !b.rec || !b.ranges || !stop)
+        return SS_ERR_CUDA;
+    SS_CUDA(ctx, cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.n_tiles, s));
+    if (n > 0) {
+        SS_CUDA(ctx, ss_launch((k_prep_recs), dim3(gridn(ctx, n)), dim3(256), 0, s, n, mu2d, inv2d, opacity, color, windows,
+                               (SplatRec<double>*)b.rec, b.mu, b.dkey64, b.dvals));
+        SS_CHECK_LAUNCH(ctx);
+    }
+    SS_TRY(bin_pairs<double>(ctx, b));
+    ss_camera cam;
+    memset(&cam, 0, sizeof(cam));
+    cam.width = width;
+    cam.height = height;
+    ss_render_opts o;
+    memset(&o, 0, sizeof(o));
+    for (int k = 0; k < 3; ++k) o.background[k] = background[k];
+    return forward<double>(ctx, &cam, &o, b, img, T, stop);
 }
 
 int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights, int32_t n_views,

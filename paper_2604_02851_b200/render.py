@@ -186,6 +186,55 @@ def prepare_splats(model, pose, intr, light_state, index_subset=None, extent_cut
                           radius=h["radius"], windows=h["window"].astype(np.int64), shade_inter={"s": h["shade_s"]})
 
 
+def splat_windows(mu2d, radius, width: int, height: int) -> np.ndarray:
+    """(n, 4) int32 windows x0, x1, y0, y1 of ref render.py:293-301
+    (splat_window), vectorised; an infinite radius covers the image."""
+    mu2d = np.asarray(mu2d, np.float64).reshape(-1, 2)
+    r = np.asarray(radius, np.float64).reshape(-1)
+    big = 1 << 30
+    fin = np.isfinite(r)
+    rr = np.where(fin, r, 0.0)
+    def lo(v):
+        return np.clip(np.floor(v), -big, big).astype(np.int64)
+    def hi(v):
+        return np.clip(np.ceil(v), -big, big).astype(np.int64)
+    x0 = np.maximum(lo(mu2d[:, 0] - rr), 0)
+    x1 = np.minimum(hi(mu2d[:, 0] + rr) + 1, width)
+    y0 = np.maximum(lo(mu2d[:, 1] - rr), 0)
+    y1 = np.minimum(hi(mu2d[:, 1] + rr) + 1, height)
+    w = np.stack([x0, x1, y0, y1], -1)
+    w[~fin] = (0, width, 0, height)
+    return w.astype(np.int32)
+
+
+def composite(prep, intr, background, device=None):
+    """ref render.py:317 -- front-to-back float64 composite of prepared
+    splats on the GPU (ss_composite); returns (image (H, W, 3), T (H, W)) as
+    host float64 arrays.  Uses prep.order, mu2d, radius, inv2d, opacity and
+    color, exactly the fields the reference reads."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    order = np.asarray(prep.order, np.int64)
+    mu = np.asarray(prep.mu2d, np.float64)[order]
+    inv = np.asarray(prep.inv2d, np.float64)[order]
+    win = splat_windows(mu, np.asarray(prep.radius, np.float64)[order], intr.width, intr.height)
+    t = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt)
+    n = int(order.size)
+    args = dict(mu=t(mu), inv=t(np.stack([inv[:, 0, 0], inv[:, 0, 1], inv[:, 1, 1]], -1) if n else np.zeros((0, 3))),
+                op=t(np.asarray(prep.opacity, np.float64)[order]),
+                col=t(np.asarray(prep.color, np.float64)[order]), win=t(win, torch.int32))
+    H, W = intr.height, intr.width
+    img = torch.empty((H, W, 3), dtype=torch.float64, device=dev)
+    T = torch.empty((H, W), dtype=torch.float64, device=dev)
+    c = _lib.ctx(dev.index)
+    c.bind_stream()
+    bg = (_lib.f64 * 3)(*[float(x) for x in np.asarray(background, np.float64).reshape(3)])
+    p = (lambda k: args[k].data_ptr() if n else None)
+    c.check(c.lib.ss_composite(c.handle, n, p("mu"), p("inv"), p("op"), p("col"), p("win"), W, H, bg,
+                               img.data_ptr(), T.data_ptr()))
+    return img.cpu().numpy(), T.cpu().numpy()
+
+
 def tile_bins(model, pose, intr, index_subset=None, extent_cutoff=True):
     """Sort keys / tile ranges of K2-K4 for parity tests: returns
     (order_rows, ranges (T,2), pair_rank (P,))."""

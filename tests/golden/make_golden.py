@@ -41,13 +41,13 @@ HERE = pathlib.Path(__file__).resolve().parent
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
-    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool engine expand objects")
+    ap.add_argument("--only", nargs="*", default=None, help="subset of: wire codec raster step dyn ingest pool engine expand objects composite")
     args = ap.parse_args()
     ref = pathlib.Path(args.ref)
     sys.path.insert(0, str(ref / "src"))
     import splatstream  # noqa: F401  (the reference)
 
-    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool", "engine", "expand", "objects"}
+    want = set(args.only) if args.only else {"wire", "codec", "raster", "step", "dyn", "ingest", "pool", "engine", "expand", "objects", "composite"}
     if "wire" in want:
         wire = HERE / "wire"
         if wire.exists():
@@ -57,7 +57,7 @@ def main():
         assert (wire / "manifest.json").read_bytes() == shipped, "regenerated manifest differs from the shipped one"
     for name, fn in (("codec", codec_cases), ("raster", raster_cases), ("step", step_cases), ("dyn", dyn_cases),
                      ("ingest", ingest_cases), ("pool", pool_cases), ("engine", engine_cases),
-                     ("expand", expand_cases), ("objects", objects_cases)):
+                     ("expand", expand_cases), ("objects", objects_cases), ("composite", composite_cases)):
         if name in want:
             fn()
     print("golden vectors written to", HERE)
@@ -804,6 +804,35 @@ def objects_cases():
         st.add(dict(kind="objects", name=f"objects_{n}_deg{deg}", n=n, degree=deg, active=int(m.active_count)),
                **arrays)
     st.save("objects_cases")
+
+
+def composite_cases():
+    """render.composite (ref render.py:317-336) on the reference's own
+    PreparedSplats, as prepared and after edits (opacity, colour, draw order,
+    an infinite radius), so the device blend is checked on arbitrary inputs."""
+    from splatstream.geometry import CameraIntrinsics, look_at
+    from splatstream.render import LightState, composite, prepare_splats
+    st = Store()
+    rng = np.random.default_rng(31)
+    for n, deg, W, H in ((2000, 1, 96, 64), (6000, 3, 130, 70)):
+        m = random_model(rng, n, deg, spread=1.5)
+        m.means[:, 2] += 4.0
+        pose = look_at(np.array([0.2, -0.1, -1.0]), np.array([0.0, 0.0, 4.0]))
+        intr = CameraIntrinsics(width=W, height=H, fov_y=1.0, near=0.05)
+        light = LightState(direction=np.array([-0.3, -1.0, 0.2]), intensity=np.array([0.8, 0.8, 0.8]))
+        prep = prepare_splats(m, pose, intr, light)
+        for variant in ("as_prepared", "edited"):
+            if variant == "edited":
+                prep.opacity = prep.opacity * 0.5
+                prep.color = prep.color[:, ::-1].copy()
+                prep.order = prep.order[::-1].copy()
+                prep.radius = prep.radius.copy()
+                prep.radius[prep.order[:3]] = np.inf
+            img, T = composite(prep, intr, np.array([0.1, 0.2, 0.3]))
+            st.add(dict(kind="composite", name=f"composite_{n}_{variant}", W=W, H=H),
+                   order=prep.order, mu2d=prep.mu2d, radius=prep.radius, inv2d=prep.inv2d, opacity=prep.opacity,
+                   color=prep.color, img=img, T=T)
+    st.save("composite_cases")
 
 if __name__ == "__main__":
     main()

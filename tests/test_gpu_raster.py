@@ -181,3 +181,24 @@ def test_gpu_long_tile_lists():
     np.testing.assert_array_equal(rows, o["rows"][o["order"]])
     np.testing.assert_array_equal(ranges, b["ranges"])
     np.testing.assert_array_equal(ranks, b["pair_rank"])
+
+
+COMPOSITE = load_cases("composite_cases")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", COMPOSITE, ids=lambda c: c["name"])
+def test_gpu_composite_of_reference_prepared_splats(c):
+    """render.composite on the reference's own PreparedSplats (as prepared,
+    and with edited opacity / colour / draw order / infinite radii) equals the
+    reference's composite: image and transmittance within the fp64 blend
+    tolerance (the only differences are exp's last bits)."""
+    require_gpu()
+    from types import SimpleNamespace
+    from paper_2604_02851_b200.geometry import CameraIntrinsics
+    from paper_2604_02851_b200.render import composite
+    prep = SimpleNamespace(**{k: c.a(k) for k in ("order", "mu2d", "radius", "inv2d", "opacity", "color")})
+    intr = CameraIntrinsics(width=c["W"], height=c["H"], fov_y=1.0)
+    img, T = composite(prep, intr, np.array([0.1, 0.2, 0.3]))
+    np.testing.assert_allclose(img, c.a("img"), rtol=0, atol=1e-9)
+    np.testing.assert_allclose(T, c.a("T"), rtol=0, atol=1e-9)
