@@ -43,6 +43,11 @@ def flat_ambient_sh(ambient_rgb) -> np.ndarray:
     return (SH_C0 * np.asarray(ambient_rgb, np.float64))[:, None]
 
 
+def light_state_from_scene(light) -> LightState:
+    """ref render.py:58-60: the scene's directional light with its flat ambient term."""
+    return LightState(direction=light.direction, intensity=light.intensity, ambient_sh=flat_ambient_sh(light.ambient))
+
+
 def camera_struct(pose, intr) -> _lib.SSCamera:
     c = _lib.SSCamera()
     c.position = _lib.f64arr(pose.position, 3)
