@@ -362,6 +362,7 @@ def run_ours(args):
     enc = None
     if rank == 0:
         enc = encoder_bench(c, _lib, args, torch)
+        enc["snapshot"] = snapshot_bench(dm, torch)
 
     # ---- pool maintenance of this model, rank 0
     pool_rec = zlib_rec = engine_rec = None
@@ -528,6 +529,40 @@ def encoder_bench(c, _lib, args, torch, reps=20):
     out["client_apply"] = ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch)
     del dm
     return out
+
+
+def snapshot_bench(dm, torch, reps=10):
+    """K11 on the bench model (1M rows, SH degree 3): the profile-0 snapshot
+    (raw, compression 0) plus the server's baseline reset outputs, device time
+    per encode with L2 flushed before each; roofline on the algorithmic bytes
+    of DESIGN.md K11 (244 B read + 38 B written per row at degree 3)."""
+    from paper_2604_02851_b200.protocol import PayloadBuffer, encode_snapshot_device
+    out = PayloadBuffer(1 << 20, dm.device)
+    bm = torch.empty_like(dm.means)
+    bl = torch.empty_like(dm.log_scales)
+    for _ in range(2):
+        encode_snapshot_device(dm, 0, out, bm, bl)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dm.device)
+    ts = []
+    for _ in range(reps):
+        flush.add_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        encode_snapshot_device(dm, 0, out, bm, bl)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    rows = dm.count
+    alg = rows * (244 + 38)
+    peak = measured_peaks().get("hbm_gbs", 6551.4)
+    gbs = alg / (ms * 1e-3) / 1e9
+    return {"value": rows / (ms * 1e-3), "unit": "Gaussians/s", "rows": rows, "sh_degree": dm.sh_degree,
+            "ms_per_snapshot": ms, "payload_bytes": int(out.length.item()),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "algorithmic_bytes": alg},
+            "note": "device time per encode (profile 0, raw) incl. the decoded means/log-scales for the baseline "
+                    "reset; L2 flushed before each"}
 
 
 def ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch, reps=10):

@@ -45,6 +45,17 @@ __device__ __forceinline__ uint32_t quantize(double v, double lo, double hi, int
     return (uint32_t)rint(dm(t, levels));
 }
 
+// quantize() for a float32 input and a power-of-two span (quaternions 2,
+// opacity 16, DC 8, SH rest 2), bit-identical with fewer fp64 operations:
+// the clip is exact in float32 (lo, hi are floats); x = RN64(c - lo) as in
+// quantize(); x / span is exact, so RN64(RN64(x / span) * levels) ==
+// RN64(x * (levels / span)) with levels / span exact; t already lies in
+// [0, 1]; rint + convert is one round-to-nearest-even conversion
+__device__ __forceinline__ uint32_t quantize_p2(float v, float lo, float hi, double scale) {
+    const float c = fminf(fmaxf(v, lo), hi);
+    return (uint32_t)__double2int_rn(dm(ds((double)c, (double)lo), scale));
+}
+
 // ref quantize.py:20-24
 __device__ __forceinline__ double dequantize(uint32_t code, double lo, double hi, int bits) {
     const double levels = (double)((1u << bits) - 1u);
@@ -142,17 +153,22 @@ __global__ void k_aabb(const float* __restrict__ means, int64_t n, SnapState* st
             hi[a] = o > hi[a] ? o : hi[a];
         }
     }
+    __shared__ uint32_t s_lo[3], s_hi[3];
+    if (threadIdx.x < 3) s_lo[threadIdx.x] = 0xffffffffu, s_hi[threadIdx.x] = 0;
+    __syncthreads();
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        for (int o = 16; o; o >>= 1) {
-            uint32_t l = __shfl_xor_sync(0xffffffffu, lo[a], o), h = __shfl_xor_sync(0xffffffffu, hi[a], o);
-            lo[a] = l < lo[a] ? l : lo[a];
-            hi[a] = h > hi[a] ? h : hi[a];
-        }
+        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
         if ((threadIdx.x & 31) == 0) {
-            atomicMin(&st->lo_ord[a], lo[a]);
-            atomicMax(&st->hi_ord[a], hi[a]);
+            atomicMin(&s_lo[a], lo[a]);
+            atomicMax(&s_hi[a], hi[a]);
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {  // one global atomic per block and component
+        atomicMin(&st->lo_ord[threadIdx.x], s_lo[threadIdx.x]);
+        atomicMax(&st->hi_ord[threadIdx.x], s_hi[threadIdx.x]);
     }
 }
 
@@ -180,7 +196,7 @@ __global__ void k_snap_rows(ss_model m, SnapLayout L, const SnapState* st, uint8
                             float* __restrict__ base_means, float* __restrict__ base_ls) {
     double lo[3], hi[3];
     aabb_of(st, L.n, lo, hi);
-    const QSpec qls = qspec(A_LS), qq = qspec(A_QUAT), qo = qspec(A_OPAC), qdc = qspec(A_DC), qr = qspec(A_REST);
+    const QSpec qls = qspec(A_LS);  // the power-of-two spans go through quantize_p2
     const int B = L.B;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // loop bound rounded up to whole warps so the visibility ballot is convergent
@@ -198,16 +214,12 @@ __global__ void k_snap_rows(ss_model m, SnapLayout L, const SnapState* st, uint8
             }
             uint64_t w = 0;
             for (int j = 0; j < 4; ++j)
-                w |= (uint64_t)quantize((double)m.quaternions[i * 4 + j], qq.lo, qq.hi, 10) << (10 * j);
+                w |= (uint64_t)quantize_p2(m.quaternions[i * 4 + j], -1.f, 1.f, 1023.0 / 2.0) << (10 * j);
             for (int b = 0; b < 5; ++b) blk[L.off_quat + i * 5 + b] = (uint8_t)(w >> (8 * b));
-            blk[L.off_opac + i] = (uint8_t)quantize((double)m.logit_opacities[i], qo.lo, qo.hi, 8);
+            blk[L.off_opac + i] = (uint8_t)quantize_p2(m.logit_opacities[i], -8.f, 8.f, 255.0 / 16.0);
             const float* sh = m.sh_coeffs + i * 3 * B;
-            for (int c = 0; c < 3; ++c) {
-                blk[L.off_dc + i * 3 + c] = (uint8_t)quantize((double)sh[c * B], qdc.lo, qdc.hi, 8);
-                for (int b = 1; b < B; ++b)
-                    blk[L.off_rest + (i * 3 + c) * (B - 1) + (b - 1)] =
-                        (uint8_t)quantize((double)sh[c * B + b], qr.lo, qr.hi, 8);
-            }
+            for (int c = 0; c < 3; ++c)  // the SH rest bytes: k_snap_rest, element-parallel
+                blk[L.off_dc + i * 3 + c] = (uint8_t)quantize_p2(sh[c * B], -4.f, 4.f, 255.0 / 8.0);
         }
         unsigned bal = __ballot_sync(0xffffffffu, ok && m.light_visibility[ok ? i : 0] >= 0.5f);
         if ((threadIdx.x & 31) == 0) {
@@ -215,6 +227,24 @@ __global__ void k_snap_rows(ss_model m, SnapLayout L, const SnapState* st, uint8
             int64_t nb = (L.n - i0 + 7) / 8;
             if (nb > 4) nb = 4;
             for (int b = 0; b < nb; ++b) blk[L.off_vis + i0 / 8 + b] = (uint8_t)(bal >> (8 * b));
+        }
+    }
+}
+
+// SH rest section, one thread per output byte (coalesced reads of the
+// coefficient rows, coalesced byte stores): 3 (B - 1) codes per row
+template <int B>
+__global__ void k_snap_rest(const float* __restrict__ sh, int64_t n, uint8_t* __restrict__ dst) {
+    constexpr uint32_t per = 3u * (uint32_t)(B - 1);  // compile-time divisors: multiply + shift
+    // rows in blocks of 2^20 keep the index arithmetic in 32 bits
+    for (int64_t r0 = 0; r0 < n; r0 += 1 << 20) {
+        const uint32_t rows = (uint32_t)min((int64_t)1 << 20, n - r0);
+        const uint32_t total = rows * per;
+        const float* src = sh + r0 * 3 * B;
+        uint8_t* out = dst + r0 * per;
+        for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+            const uint32_t i = e / per, r = e - i * per, c = r / (uint32_t)(B - 1), b = r - c * (uint32_t)(B - 1) + 1;
+            out[e] = (uint8_t)quantize_p2(__ldg(&src[((uint64_t)i * 3 + c) * B + b]), -1.f, 1.f, 255.0 / 2.0);
         }
     }
 }
@@ -337,6 +367,13 @@ int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t*
     if (n) {
         k_snap_rows<<<grid_for(ctx, n), 256, 0, s>>>(*m, L, st, blk, base_means, base_ls);
         SS_CHECK_LAUNCH(ctx);
+        if (B > 1) {
+            const int g = grid_for(ctx, n * 3 * (B - 1));
+            if (B == 4) k_snap_rest<4><<<g, 256, 0, s>>>(m->sh_coeffs, n, blk + L.off_rest);
+            else if (B == 9) k_snap_rest<9><<<g, 256, 0, s>>>(m->sh_coeffs, n, blk + L.off_rest);
+            else k_snap_rest<16><<<g, 256, 0, s>>>(m->sh_coeffs, n, blk + L.off_rest);
+            SS_CHECK_LAUNCH(ctx);
+        }
         k_snap_id_lens<<<grid_for(ctx, n), 256, 0, s>>>(m->object_ids, n, lens);
         SS_CHECK_LAUNCH(ctx);
     }
