@@ -37,6 +37,7 @@ constexpr int TK_MAX_JOBS = 8;
 
 struct QParams {
     double lo, hi, span, inv_span, levels, inv_levels, dspan;  // dspan = hi - lo (dequantizer)
+    double p2scale;  // levels / span when hi > lo and span is a power of two (exact), else 0
     int bits;
 };
 
@@ -50,6 +51,8 @@ __host__ __device__ inline QParams make_q(double lo, double hi, int bits) {
     p.span = hi > lo ? hi - lo : 1.0;
     p.inv_span = 1.0 / p.span;
     p.dspan = hi - lo;
+    int ex = 0;
+    p.p2scale = (hi > lo && frexp(p.span, &ex) == 0.5) ? p.levels * p.inv_span : 0.0;
     return p;
 }
 
@@ -111,6 +114,9 @@ __device__ __forceinline__ double np_min(double a, double b) { return a <= b ? a
 // by monotone rounding, so t already lies in [0, 1] and its clip is a no-op.
 __device__ __forceinline__ uint32_t quant(double v, const QParams& p) {
     const double c = np_min(np_max(v, p.lo), p.hi);
+    // power-of-two span: x / span is exact, so RN(RN(x / span) * levels) ==
+    // RN(x * (levels / span)) -- one multiply, and rint + convert in one step
+    if (p.p2scale != 0.0) return (uint32_t)__double2int_rn(q_dm(q_ds(c, p.lo), p.p2scale));
     double t = div_rn(q_ds(c, p.lo), p.span, p.inv_span);
     if (!(p.hi >= p.lo)) t = np_min(np_max(t, 0.0), 1.0);
     return (uint32_t)rint(q_dm(t, p.levels));
@@ -487,6 +493,7 @@ __device__ void plan_job(const Job& J) {
         rq.span = m > -m ? q_ds(m, -m) : 1.0;
         rq.inv_span = 1.0 / rq.span;
         rq.dspan = q_ds(m, -m);
+        rq.p2scale = 0.0;  // residual codes use rquant
         *J.rq = rq;
     }
     uint64_t V = 0;
