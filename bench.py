@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--degree", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--step-only", action="store_true",
+                    help="profiling: only the timed optimize steps (no encoder / pool / engine / e2e records)")
     return ap.parse_args()
 
 
@@ -360,19 +362,20 @@ def run_ours(args):
 
     # ---- delta encoder alone (rank 0): per-frame set, raw, device-resident
     enc = None
-    if rank == 0:
+    extras = rank == 0 and not args.step_only
+    if extras:
         enc = encoder_bench(c, _lib, args, torch)
         enc["snapshot"] = snapshot_bench(dm, torch)
 
     # ---- pool maintenance of this model, rank 0
     pool_rec = zlib_rec = engine_rec = None
-    if rank == 0:
+    if extras:
         pool_rec = pool_bench(dm, state, poses, intr, torch)
         zlib_rec = zlib_tick_bench(dm, base_m, base_l, torch)
 
     # ---- e2e through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.step_only:
         host_gt = [g.cpu().pin_memory() for g in gts]
         hviews = [ReferenceView(poses[v], intr, hg, light, bg) for v, hg in zip(mine, host_gt)]
         h2d = sum(int(g.numel()) * 4 for g in host_gt)
@@ -426,12 +429,12 @@ def run_ours(args):
 
     # ---- config 5: client-viewpoint rendering, views sharded over the ranks (no collective)
     client_rec = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.step_only:
         client_rec = client_render_bench(args, rank, world, pg, dev, torch)
 
     # ---- the engine stand-in and a full server tick on the device (§8f rank 4), rank 0,
     # after the timed runs (it trains the model further and holds its own buffers)
-    if rank == 0:
+    if extras:
         engine_rec = engine_bench(poses, intr, torch)
         engine_rec["live_tick"] = live_tick_bench(dm, state, poses, intr, light, torch)
 
