@@ -301,8 +301,14 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, int64_t n, uint2* __
 // them in depth order; no block-level barriers anywhere (blocks are just
 // WPB independent tiles).  Per-pixel liveness is an 8-bit mask; a pixel dies
 // when T drops below 1e-4 (the reference's T-gate: later splats skip it).
-constexpr int WPB = 4;   // tiles (warps) per block of the forward kernels
-constexpr int WPB_BWD = 2;  // ... of the backward (fewer tiles per block: less waiting on a block's slowest tile)
+#ifndef SS_WPB
+#define SS_WPB 4
+#endif
+constexpr int WPB = SS_WPB;   // tiles (warps) per block of the forward kernels
+#ifndef SS_WPB_BWD
+#define SS_WPB_BWD 2
+#endif
+constexpr int WPB_BWD = SS_WPB_BWD;  // ... of the backward (fewer tiles per block: less waiting on a block's slowest tile)
 constexpr int PPT = 8;   // pixels per lane
 // pixel rows per warp-uniform skip test: rows of one group form one basic
 // block, so their independent chains interleave (helps the longer backward
