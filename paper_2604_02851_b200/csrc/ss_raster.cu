@@ -76,7 +76,10 @@ __global__ void k_visible_flags(ss_model m, ss_camera cam, const int64_t* subset
 }
 
 template <int DEG, typename R>
-__global__ void __launch_bounds__(128, 4) k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
+#ifndef SS_PRE_MINB
+#define SS_PRE_MINB 4
+#endif
+__global__ void __launch_bounds__(128, SS_PRE_MINB) k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
                              int cutoff, uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                              SplatRec<R>* __restrict__ rec, double2* __restrict__ mu, DebugOut dbg,
                              unsigned long long* __restrict__ kminmax) {
