@@ -832,7 +832,7 @@ __device__ __forceinline__ void scan_chunk(const Job& J, int64_t c) {
 }
 
 #ifndef TK_EMIT_MINB
-#define TK_EMIT_MINB 3  // <= 80 registers: 3 blocks per SM
+#define TK_EMIT_MINB 5  // <= 51 registers: 5 blocks per SM (measured dense tick 3/4/5/6 blocks: 76.8/74.7/72.7/80.9 us)
 #endif
 // one launch: [residual scans][absolute jobs][residual emits]; the emit
 // blocks are dispatched after every scan block and wait on their job's plan
