@@ -79,6 +79,9 @@ template <int DEG, typename R>
 #ifndef SS_PRE_MINB
 #define SS_PRE_MINB 4
 #endif
+#ifndef SS_PRE_PREFETCH
+#define SS_PRE_PREFETCH 1
+#endif
 __global__ void __launch_bounds__(128, SS_PRE_MINB) k_preprocess(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset, int64_t n_in,
                              int cutoff, uint64_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                              SplatRec<R>* __restrict__ rec, double2* __restrict__ mu, DebugOut dbg,
@@ -88,6 +91,19 @@ __global__ void __launch_bounds__(128, SS_PRE_MINB) k_preprocess(ss_model m, ss_
     constexpr int B = ss_sh_bases(DEG);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = subset ? subset[j] : j;
+#if SS_PRE_PREFETCH
+        // every parameter load of the row first (the stores below would otherwise hold them back)
+        float lsv[3], qv[4], shv[3 * B];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) lsv[k] = m.log_scales[row * 3 + k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) qv[k] = m.quaternions[row * 4 + k];
+        ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, shv);
+        const float logit = m.logit_opacities[row], visv = m.light_visibility[row];
+#else
+        const float* lsv = m.log_scales + row * 3;
+        const float* qv = m.quaternions + row * 4;
+#endif
         Proj P;
         ss_cam_point(cam, m.means + row * 3, P.d, P.mc);
         dvals[j] = (uint32_t)j;
@@ -98,25 +114,30 @@ __global__ void __launch_bounds__(128, SS_PRE_MINB) k_preprocess(ss_model m, ss_
         dkeys[j] = (uint64_t)__double_as_longlong(P.mc[2]);  // z >= near > 0: bits order as the value
         kmin = min(kmin, (unsigned long long)dkeys[j]);
         kmax = max(kmax, (unsigned long long)dkeys[j]);
-        ss_project(cam, m.log_scales + row * 3, m.quaternions + row * 4, cutoff != 0, P);
+        ss_project(cam, lsv, qv, cutoff != 0, P);
         Shade<DEG, R> S;
         {
+#if !SS_PRE_PREFETCH
             float shv[3 * B];
             ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, shv);
+            const float visv = m.light_visibility[row];
+#endif
             const R dR[3] = {(R)P.d[0], (R)P.d[1], (R)P.d[2]};
             R RqR[3][3];
 #pragma unroll
             for (int i = 0; i < 3; ++i)
 #pragma unroll
                 for (int k = 0; k < 3; ++k) RqR[i][k] = (R)P.Rq[i][k];
-            ss_shade_v<DEG, R>(L, m.log_scales + row * 3, shv, m.light_visibility[row], dR, RqR, S);
+            ss_shade_v<DEG, R>(L, lsv, shv, visv, dR, RqR, S);
         }
         SplatRec<R> g;
         g.a = (R)(P.s11 / P.det);
         g.b = (R)(-P.s01 / P.det);
         g.c = (R)(P.s00 / P.det);
-        g.o = sizeof(R) == 4 ? (R)(1.0f / (1.0f + expf(-m.logit_opacities[row])))
-                             : (R)(1.0 / (1.0 + exp(-(double)m.logit_opacities[row])));
+#if !SS_PRE_PREFETCH
+        const float logit = m.logit_opacities[row];
+#endif
+        g.o = sizeof(R) == 4 ? (R)(1.0f / (1.0f + expf(-logit))) : (R)(1.0 / (1.0 + exp(-(double)logit)));
         for (int c = 0; c < 3; ++c) g.col[c] = (R)fmin(fmax((double)S.pre[c], 0.0), 1.0);
         ss_window(P, cam.width, cam.height, g.win);
         rec[j] = g;
