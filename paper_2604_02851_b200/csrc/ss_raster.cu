@@ -235,13 +235,14 @@ __global__ void k_count(const uint64_t* __restrict__ dkey64, const uint32_t* __r
     SS_PDL_WAIT();
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = dvals[r];
-        if (dkey64[j] == ~0ull) {
+        const uint64_t key = dkey64[j];
+        const int4 w = *reinterpret_cast<const int4*>(rec[j].win);  // both loads before any store
+        if (key == ~0ull) {
             rcnt[r] = 0;
             rinv[j] = ~0u;
             continue;
         }
         rinv[j] = (uint32_t)r;
-        const int4 w = *reinterpret_cast<const int4*>(rec[j].win);
         const int win[4] = {w.x, w.y, w.z, w.w};
         uint32_t cnt = 0;
         if (win[0] < win[1] && win[2] < win[3]) {
