@@ -88,6 +88,11 @@ typedef struct {
                                 rank (0xffffffff = culled); the chain rule is left to one
                                 ss_chain_views call over all the step's views.  NULL = immediate */
     uint32_t* defer_rinv;
+    uint32_t* tile_order;    /* optional device (tiles,): the backward stores its tile walk order here; it
+                                equals the order the next forward derives from tile_hint, so a call with
+                                tile_order_valid = 1 uses it instead of re-sorting (needs tile_hint) */
+    int32_t tile_order_valid;
+    int32_t _pad2;
 } ss_render_opts;
 
 /* The chain rule of a step's views in one pass over the rows (ref

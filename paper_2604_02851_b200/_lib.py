@@ -43,7 +43,8 @@ class SSLight(C.Structure):
 class SSRenderOpts(C.Structure):
     _fields_ = [("background", f64 * 3), ("subset", vp), ("subset_count", i32), ("extent_cutoff", i32),
                 ("precision", i32), ("deterministic", i32), ("gt_ready", vp), ("tile_hint", vp),
-                ("tile_hint_len", i64), ("defer_g9", vp), ("defer_rinv", vp)]
+                ("tile_hint_len", i64), ("defer_g9", vp), ("defer_rinv", vp), ("tile_order", vp),
+                ("tile_order_valid", i32), ("_pad2", i32)]
 
 
 class SSRenderStats(C.Structure):

@@ -1520,8 +1520,13 @@ int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bi
     uint32_t* order = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
     if (!order) return SS_ERR_CUDA;
     const bool hint = o->tile_hint && o->tile_hint_len == b.n_tiles;
-    SS_CUDA(ctx, ss_launch((k_tile_order), dim3(1), dim3(1024), 0, ctx->stream, b.ranges, hint ? o->tile_hint : nullptr, b.n_tiles, order));
-    SS_CHECK_LAUNCH(ctx);
+    if (hint && o->tile_order && o->tile_order_valid) {
+        order = o->tile_order;  // the previous backward's order = the order of this hint
+    } else {
+        SS_CUDA(ctx, ss_launch((k_tile_order), dim3(1), dim3(1024), 0, ctx->stream, b.ranges, hint ? o->tile_hint : nullptr, b.n_tiles,
+                               order));
+        SS_CHECK_LAUNCH(ctx);
+    }
     if constexpr (sizeof(R) == 4)
         SS_CUDA(ctx, ss_launch((k_blend_fwd2), dim3((b.n_tiles + WPB - 1) / WPB), dim3(32 * WPB), 0, ctx->stream, 
             b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
@@ -1573,6 +1578,8 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (!order) return SS_ERR_CUDA;
     SS_CUDA(ctx, ss_launch((k_tile_order), dim3(1), dim3(1024), 0, s, b.ranges, stop, b.n_tiles, order));
     SS_CHECK_LAUNCH(ctx);
+    if (o->tile_order && o->tile_hint && o->tile_hint_len == b.n_tiles)  // reused by the next forward of this camera
+        SS_CUDA(ctx, cudaMemcpyAsync(o->tile_order, order, sizeof(uint32_t) * b.n_tiles, cudaMemcpyDeviceToDevice, s));
     SS_CUDA(ctx, ss_launch((k_blend_bwd<R>), dim3((b.n_tiles + WPB_BWD - 1) / WPB_BWD), dim3(32 * WPB_BWD), 0, s, 
         b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
         b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order));

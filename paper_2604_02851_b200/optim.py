@@ -157,6 +157,19 @@ def _tile_hint(view, device):
     return h
 
 
+def _tile_order(view, device):
+    """(per-view device buffer of the backward's tile walk order, valid?):
+    the next forward of this camera reuses it instead of re-sorting."""
+    import torch
+    n = _tile_hint(view, device).numel()
+    o = view.__dict__.get("_tile_order")
+    if o is None or o.numel() != n or o.device != device:
+        o = torch.zeros(n, dtype=torch.int32, device=device)
+        view.__dict__["_tile_order"] = o
+        view.__dict__["_tile_order_valid"] = False
+    return o, view.__dict__.get("_tile_order_valid", False)
+
+
 def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subset=None, extent_cutoff=True,
                     precision=0, image_out=None, subset_tensor=None, gt=None, defer=None):
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
@@ -175,8 +188,10 @@ def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subs
     c.check(c.lib.ss_backward(c.handle, model.struct(), camera_struct(view.pose, view.intrinsics),
                               light_struct(view.light_state),
                               render_opts(view.background, sub, extent_cutoff, precision, gt_ready=ready,
-                                          tile_hint=_tile_hint(view, model.device), defer=defer),
+                                          tile_hint=_tile_hint(view, model.device), defer=defer,
+                                          tile_order=_tile_order(view, model.device)),
                               _lib.ptr(gt), _lib.ptr(grad_accum), _lib.ptr(loss_accum), _lib.ptr(image_out), st))
+    view.__dict__["_tile_order_valid"] = True
     return st
 
 
