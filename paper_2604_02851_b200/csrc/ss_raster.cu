@@ -1180,6 +1180,9 @@ struct ChainViews {
 #ifndef CV_MINB
 #define CV_MINB 4
 #endif
+#ifndef CV_PREFETCH
+#define CV_PREFETCH 1
+#endif
 template <int DEG>
 __global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const ChainViews* __restrict__ V, int nv,
                                                         const int64_t* __restrict__ subset, int64_t n_in,
@@ -1191,6 +1194,10 @@ __global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const 
         if (row >= a) continue;
         float acc[11];
         bool any = false;
+#if CV_PREFETCH
+        // the next views' screen-space gradients into L1 while this view's chain runs
+        for (int v = 1; v < nv; ++v) asm volatile("prefetch.global.L1 [%0];" ::"l"(V->g9[v] + j * 9));
+#endif
         for (int v = 0; v < nv; ++v) {
             if (V->rinv[v][j] == ~0u) continue;
             if (!any) {
