@@ -867,6 +867,9 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, doubl
 //     its predecessor's), so a warp takes 32 consecutive ranks, stages their
 //     contiguous partials through shared memory in chunks of whole pairs
 //     (coalesced loads), and each lane sums its own rank's pairs in pair order.
+#ifndef SP_PREFETCH
+#define SP_PREFETCH 1
+#endif
 template <typename R>
 __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
                                                       const uint32_t* __restrict__ dvals, const R* __restrict__ partials,
@@ -893,6 +896,13 @@ __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict
             const uint64_t c1 = min(c0 + PW, end);
             const int nf = (int)(c1 - c0) * 9;
             const R* src = partials + c0 * 9;
+#if SP_PREFETCH
+            if (c1 < end) {  // the next chunk into L1 while this one is summed
+                const int nn = (int)(min(c1 + PW, end) - c1) * 9;
+                for (int k = lane * (32 / (int)sizeof(R)); k < nn; k += 32 * (32 / (int)sizeof(R)))
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(partials + c1 * 9 + k));
+            }
+#endif
             for (int k = lane; k < nf; k += 32) sb[k] = src[k];
             __syncwarp();
             const uint64_t a = off > c0 ? off : c0, b = off + cnt < c1 ? off + cnt : c1;
