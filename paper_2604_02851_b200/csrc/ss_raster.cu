@@ -1188,7 +1188,7 @@ struct ChainViews {
 };
 
 #ifndef CV_MINB
-#define CV_MINB 4
+#define CV_MINB 3  // measured 3 / 4 / 5: 2.43 / 2.45 / 2.57 ms chain per step
 #endif
 #ifndef CV_PREFETCH
 #define CV_PREFETCH 1
