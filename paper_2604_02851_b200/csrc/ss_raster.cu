@@ -1299,7 +1299,10 @@ __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __res
 // SH gradients of all the step's views (ss_chain_views): per (row, channel,
 // basis) entry, the views' contributions in view order, the entry read and
 // written once.  Same per-entry arithmetic as k_sh_grad.
-constexpr int SHGV_ROWS = 32;
+#ifndef SS_SHGV_ROWS
+#define SS_SHGV_ROWS 32
+#endif
+constexpr int SHGV_ROWS = SS_SHGV_ROWS;
 
 template <int DEG>
 __global__ void __launch_bounds__(256) k_sh_grad_views(const ChainViews* __restrict__ V, int nv,
