@@ -87,6 +87,7 @@ int ss_ctx_create(int device, ss_ctx** out) {
     c->timer_state = nullptr;
     c->dev_counters = nullptr;
     c->launches = 0;
+    c->stream_switch = nullptr;
     if (cudaMallocHost(&c->pinned, 4096) != cudaSuccess) {
         delete (Arena*)c->arena_state;
         delete c;
@@ -105,6 +106,7 @@ void ss_ctx_destroy(ss_ctx* ctx) {
     delete a;
     cudaFreeHost(ctx->pinned);
     if (ctx->dev_counters) cudaFree(ctx->dev_counters);
+    if (ctx->stream_switch) cudaEventDestroy(ctx->stream_switch);
     // timer events are released with the context's device state
     delete ctx;
 }
@@ -113,7 +115,16 @@ const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err : "null con
 
 int ss_set_stream(ss_ctx* ctx, void* stream) {
     if (!ctx) return SS_ERR_INVALID;
-    ctx->stream = (cudaStream_t)stream;
+    cudaStream_t next = (cudaStream_t)stream;
+    if (next != ctx->stream) {
+        // work already queued on the old stream may still read or write the
+        // scratch arena the next call reuses: the new stream waits for it
+        if (!ctx->stream_switch)
+            SS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->stream_switch, cudaEventDisableTiming));
+        SS_CUDA(ctx, cudaEventRecord(ctx->stream_switch, ctx->stream));
+        SS_CUDA(ctx, cudaStreamWaitEvent(next, ctx->stream_switch, 0));
+        ctx->stream = next;
+    }
     return SS_OK;
 }
 

@@ -14,9 +14,11 @@
 //   residual emits  wait for their job's flag, then dense quantize, or sparse
 //                   varint gaps + codes; advanced baseline f32(f64(base) + deq)
 //
-// The emit blocks' wait relies on in-order block dispatch (every scan block
-// is resident or done before any emit block starts), the same forward-progress
-// assumption as the radix sort's decoupled look-back.
+// A block's role is its ticket from an atomic counter taken when it starts
+// (not blockIdx.x, whose dispatch order CUDA does not guarantee): every scan
+// block an emit block waits for holds a smaller ticket, so it has already
+// started and will finish -- the forward-progress argument of the radix
+// sort's decoupled look-back (ss_sort.cu takes its tiles the same way).
 //
 // Inputs may be strided views of the model (SH DC / SH rest are read in place
 // from the (N, 3, B) coefficient array).  Arithmetic is the bit-exact float64
@@ -568,6 +570,19 @@ __device__ __forceinline__ void wait_planned(const Job& J) {
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(&J.g[2]) : "memory");
 }
 
+// an absolute job without rows: header only (mode 2, zero-length block)
+__global__ void k_empty_header(Batch B, int job) {
+    SS_PDL_WAIT();
+    const Job& J = B.j[job];
+    uint8_t* o = J.out;
+    o[0] = (uint8_t)J.attr;
+    o[1] = 2;
+    o[2] = 0;
+    o[3] = (uint8_t)J.dims;
+    for (int k = 4; k < 12; ++k) o[k] = 0;
+    *J.out_len = 12;
+}
+
 // a residual job without rows (no scan block runs its plan)
 __global__ void __launch_bounds__(TK_THREADS) k_tick_plan(Batch B, int job) {
     SS_PDL_WAIT(); plan_job(B.j[job]); }
@@ -837,9 +852,13 @@ __device__ __forceinline__ void scan_chunk(const Job& J, int64_t c) {
 // one launch: [residual scans][absolute jobs][residual emits]; the emit
 // blocks are dispatched after every scan block and wait on their job's plan
 // flag (the absolute jobs in between cover the plan tail)
-__global__ void __launch_bounds__(TK_THREADS, TK_EMIT_MINB) k_tick_fused(Batch B, int64_t scan_chunks) {
+__global__ void __launch_bounds__(TK_THREADS, TK_EMIT_MINB) k_tick_fused(Batch B, int64_t scan_chunks,
+                                                                          unsigned* __restrict__ ticket) {
     SS_PDL_WAIT();
-    const int64_t b = blockIdx.x;
+    __shared__ unsigned s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t b = s_ticket;
     if (b < scan_chunks) {
         const Job& J = B.j[find_job(B, b)];
         scan_chunk(J, b - J.chunk0);
@@ -951,23 +970,19 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
             SS_CHECK_LAUNCH(ctx);
         }
     if (res_chunks + abs_chunks) {  // residual chunks are [0, res), absolute [res, res + abs)
+        unsigned* ticket = SS_SCRATCH(ctx, unsigned, 1);
+        if (!ticket) return SS_ERR_CUDA;
+        SS_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(unsigned), ctx->stream));
         SS_CUDA(ctx, ss_launch((k_tick_fused), dim3((unsigned)(2 * res_chunks + abs_chunks)), dim3(TK_THREADS), 0, ctx->stream, B,
-                               res_chunks + abs_chunks));
+                               res_chunks + abs_chunks, ticket));
         SS_CHECK_LAUNCH(ctx);
     }
     // jobs with zero rows and no chunk still need their header
-    for (int i = 0; i < njobs; ++i) {
-        const Job& J = B.j[i];
-        if (J.rows == 0 && !J.residual) {
-            uint8_t h[12] = {(uint8_t)J.attr, 2, 0, (uint8_t)J.dims, 0, 0, 0, 0, 0, 0, 0, 0};
-            uint64_t len = 12;
-            memcpy(ctx->pinned, h, 12);
-            memcpy((uint8_t*)ctx->pinned + 16, &len, 8);
-            SS_CUDA(ctx, cudaMemcpyAsync(J.out, ctx->pinned, 12, cudaMemcpyHostToDevice, ctx->stream));
-            SS_CUDA(ctx, cudaMemcpyAsync(J.out_len, (uint8_t*)ctx->pinned + 16, 8, cudaMemcpyHostToDevice, ctx->stream));
-            SS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < njobs; ++i)
+        if (B.j[i].rows == 0 && !B.j[i].residual) {
+            SS_CUDA(ctx, ss_launch((k_empty_header), dim3(1), dim3(1), 0, ctx->stream, B, i));
+            SS_CHECK_LAUNCH(ctx);
         }
-    }
     ss_toc(ctx, KC_CODEC);
     return SS_OK;
 }

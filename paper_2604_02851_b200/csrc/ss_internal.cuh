@@ -23,6 +23,9 @@ struct ss_ctx {
     void* timer_state;
     unsigned long long* dev_counters;  // [0] T-gated (pixel, splat) evaluations
     unsigned long long launches;       // kernels launched through this context
+    // orders a new stream after the previous one when ss_set_stream switches
+    // (the scratch arena is shared by every call on the ctx)
+    cudaEvent_t stream_switch;
 };
 
 enum ss_kernel_class {

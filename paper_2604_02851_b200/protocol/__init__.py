@@ -295,7 +295,10 @@ class DeltaTicker:
         ptrs = tuple(t.data_ptr() for t in (m.means, m.log_scales, m.quaternions, m.logit_opacities, m.sh_coeffs,
                                             m.light_visibility))
         bptrs = tuple(int(b.data_ptr()) for b in self.baselines.values())
-        return tuple(int(x) for x in attributes), m.active_count, ptrs, bptrs
+        # the output buffers too: PayloadBuffer.ensure() may reallocate one, and
+        # a cached job array must never point at a freed payload buffer
+        optrs = tuple(int(self.outs[int(x)].data.data_ptr()) for x in attributes)
+        return tuple(int(x) for x in attributes), m.active_count, ptrs, bptrs, optrs
 
     def __call__(self, attributes):
         # the job array is rebuilt when the active prefix or a buffer changes
@@ -303,7 +306,11 @@ class DeltaTicker:
         key = full[0]
         jobs = self._jobs.get(full)
         if jobs is None:
-            jobs = self._jobs[full] = self._build(key)
+            if len(self._jobs) > 32:
+                self._jobs.clear()
+            jobs = self._build(key)  # may grow (reallocate) output buffers:
+            full = self._key(attributes)  # key the jobs by the pointers they hold
+            self._jobs[full] = jobs
         c = self._ctx
         c.bind_stream()
         c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
