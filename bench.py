@@ -287,11 +287,21 @@ def run_ours(args):
     bg = np.array([0.05, 0.05, 0.08])
     gts = [render_device(tgt, poses[v], intr, light, background=bg) for v in mine]
     del tgt
-    views = [ReferenceView(poses[v], intr, g, light, bg) for v, g in zip(mine, gts)]
+    # every rank passes all the step's views (step() shards them); a view
+    # rendered elsewhere only needs its camera here: a stride-0 placeholder image
+    placeholder = torch.zeros((1, 1, 1), dtype=torch.float32, device=dev).expand(intr.height, intr.width, 3)
+    img_of = dict(zip(mine, gts))
+    views = [ReferenceView(poses[v], intr, img_of.get(v, placeholder), light, bg) for v in range(args.views)]
     lo, hi = model_h.means.min(0), model_h.means.max(0)
-    state = OptimizerState(dm, scene_extent=float(np.linalg.norm(hi - lo) / 2), device=dev)
+    state = OptimizerState(dm, scene_extent=float(np.linalg.norm(hi - lo) / 2), device=dev, process_group=pg)
     ws = StepWorkspace(dm)
     a = dm.active_count
+
+    def solo_state():
+        """Rank 0's single-GPU records run without the other ranks: their own state."""
+        if pg is None:
+            return state
+        return OptimizerState(dm, scene_extent=state.scene_extent, device=dev)
     # delta baselines from the decoded snapshot (server.py:481-484), computed on device
     base_m = torch.empty((dm.count, 3), dtype=torch.float32, device=dev)
     base_l = torch.empty((dm.count, 3), dtype=torch.float32, device=dev)
@@ -320,7 +330,7 @@ def run_ours(args):
     fp32_peak = ctypes_peak(c)
 
     def one_step(i):
-        step(dm, state, views, process_group=pg, total_views=args.views, workspace=ws, sync_loss=False)
+        step(dm, state, views, workspace=ws, sync_loss=False)
         return delta_tick(i)
 
     clocks = ClockSampler(local)
@@ -370,18 +380,19 @@ def run_ours(args):
     # ---- pool maintenance of this model, rank 0
     pool_rec = zlib_rec = engine_rec = None
     if extras:
-        pool_rec = pool_bench(dm, state, poses, intr, torch)
+        pool_rec = pool_bench(dm, solo_state(), poses, intr, torch)
         zlib_rec = zlib_tick_bench(dm, base_m, base_l, torch)
 
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e and not args.step_only:
         host_gt = [g.cpu().pin_memory() for g in gts]
-        hviews = [ReferenceView(poses[v], intr, hg, light, bg) for v, hg in zip(mine, host_gt)]
+        himg = dict(zip(mine, host_gt))
+        hviews = [ReferenceView(poses[v], intr, himg.get(v, placeholder), light, bg) for v in range(args.views)]
         h2d = sum(int(g.numel()) * 4 for g in host_gt)
         d2h = 0
         for i in range(2):
-            step(dm, state, hviews, process_group=pg, total_views=args.views, workspace=ws)
+            step(dm, state, hviews, workspace=ws)
             delta_tick(i, device_only=False)
         if pend[0] is not None:
             pend[0].result(copy=False)
@@ -402,7 +413,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(args.steps):
-            lt = step(dm, state, hviews, process_group=pg, total_views=args.views, workspace=ws, sync_loss=False)
+            lt = step(dm, state, hviews, workspace=ws, sync_loss=False)
             loss_h[i % 2:i % 2 + 1].copy_(lt, non_blocking=True)
             loss_ev[i % 2].record()
             if i > 0:
@@ -436,7 +447,7 @@ def run_ours(args):
     # after the timed runs (it trains the model further and holds its own buffers)
     if extras:
         engine_rec = engine_bench(poses, intr, torch)
-        engine_rec["live_tick"] = live_tick_bench(dm, state, poses, intr, light, torch)
+        engine_rec["live_tick"] = live_tick_bench(dm, solo_state(), poses, intr, light, torch)
 
     if rank != 0:
         if pg is not None:
@@ -895,8 +906,29 @@ def cpu_baseline(model, tgt, poses, intr, light_state):
                        f"1920x1080 frame ({len(rows)} rows meet it), {t:.2f} s, extrapolated x{factor:.0f}")}
 
 
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: re-run this script
+    under torch.distributed.run with N ranks (one per GPU) and return its
+    exit code (rank 0 prints the JSON line)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines (NVLS / NVLink paths) go to stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 if __name__ == "__main__":
     a = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if a.impl == "ours" and a.gpus > 1 and world_env is None:
+        sys.exit(launch_ranks(a))
+    if world_env is not None and a.impl == "ours" and int(world_env) != a.gpus:
+        sys.exit(f"--gpus {a.gpus} but WORLD_SIZE={world_env}")
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -107,6 +107,22 @@ int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const 
                    const float* const* g9, const uint32_t* const* rinv, const int64_t* subset, int64_t n_in,
                    float* grad);
 
+/* ss_chain_views over inputs j in [j0, j1) (row = subset[j], or j) into a
+ * gradient layout of `ld` rows per group whose first row is row0 and which
+ * covers `rows` rows (ss_chain_views: j0 = 0, j1 = n_in, row0 = 0,
+ * rows = ld = active_count).  The view-sharded step runs it on
+ * one GPU's row shard [row0, row0 + rows) with ld = the shard length, every
+ * view of the step in view order, g9[v] / rinv[v] offset so that entry j is
+ * row j's: per row the arithmetic and order are those of ss_chain_views, so
+ * the sharded gradient is bit-identical to the single-GPU one. */
+int ss_chain_views_range(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights,
+                         int32_t n_views, const float* const* g9, const uint32_t* const* rinv, const int64_t* subset,
+                         int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld);
+
+/* *out = ((x[0] + x[1]) + x[2]) + ... (device doubles): the per-view loss sum
+ * in the reference's order (optim.py:366-367). */
+int ss_sum_f64(ss_ctx* ctx, const double* x, int64_t n, double* out);
+
 /* composite(): ref render.py:317-336 on prepared splats (device arrays, n
  * splats already in draw order = prep.order): fp64 front-to-back blend of the
  * given windows (x0, x1, y0, y1; ref render.py:293-301), centres, inverse
@@ -193,6 +209,30 @@ typedef struct {
 int ss_prepare_splats(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, const ss_light* light,
                       const ss_render_opts* opts, ss_prepared* out, int64_t* visible_out);
 
+/* The rest of the reference's PreparedSplats (ref render.py:200-223) for the
+ * M prepared splats whose model rows are rows[0..M) (device int64, e.g. the
+ * `rows` output of ss_prepare_splats), fp64, each output (device) optional:
+ * camera-space mean, projection Jacobian, Sigma3d, W Sigma3d W^T, view
+ * direction / distance, normal proxy and its axis, and the shading
+ * intermediates of ref render.py:196 (Y, albedo_est, cos, vis; s is in
+ * ss_prepared).  Computed by the same device functions as K1. */
+typedef struct {
+    double* mu_cam;      /* (M,3)   */
+    double* J;           /* (M,2,3) */
+    double* sigma3d;     /* (M,3,3) */
+    double* cov_cam;     /* (M,3,3) */
+    double* view_dir;    /* (M,3)   */
+    double* view_dist;   /* (M,)    */
+    double* n_hat;       /* (M,3)   */
+    int64_t* n_axis;     /* (M,)    */
+    double* Y;           /* (M,B)   */
+    double* albedo_est;  /* (M,3)   */
+    double* cos;         /* (M,)    */
+    double* vis;         /* (M,)    */
+} ss_prepared_extras;
+int ss_prepare_extras(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, const ss_light* light,
+                      const int64_t* rows, int64_t M, ss_prepared_extras* out);
+
 /* Tile-binning products for parity tests (sort keys / tile ranges,
  * SURVEY §8c): depth-ordered rows, per-tile [start, end) and the depth rank
  * of every sorted (tile, splat) pair. */
@@ -213,6 +253,13 @@ int ss_backward(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, const 
  * [0, active) in place, renormalises quaternions, advances EMA and age. */
 int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* state, const float* grad_sum,
                  int32_t n_views, const ss_adam_hparams* hp);
+/* ss_adam_step on a gradient / moment layout of `ld` >= active_count rows per
+ * group (padding rows skipped).  The view-sharded step passes a row shard of
+ * the model (pointers offset to the shard's first row, active_count = its
+ * length, possibly 0) with the shard's moments; step_count advances even for
+ * an empty shard. */
+int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* state, const float* grad_sum, int64_t ld,
+                    int32_t n_views, const ss_adam_hparams* hp);
 
 /* ---- encoders (ref protocol/) -------------------------------------------- */
 /* encode_delta(): ref protocol/delta.py:72 with compression_id 0 (raw).

@@ -67,6 +67,11 @@ class SSPrepared(C.Structure):
                 ("capacity", i64)]
 
 
+class SSPreparedExtras(C.Structure):
+    _fields_ = [(k, vp) for k in ("mu_cam", "J", "sigma3d", "cov_cam", "view_dir", "view_dist", "n_hat", "n_axis", "Y",
+                                  "albedo_est", "cos", "vis")]
+
+
 class SSDeltaJob(C.Structure):
     _fields_ = [("attribute_id", i32), ("in_dtype", i32), ("cur", vp), ("base", vp), ("new_base", vp),
                 ("rows", i64), ("dims", i32), ("inner", i32), ("row_stride", i64), ("outer", i32), ("col0", i32),
@@ -188,6 +193,13 @@ _SIGS = {
     "ss_init_gaussians": (i32, [vp, C.POINTER(SSSampleBatch), i64, C.POINTER(SSModel), i64]),
     "ss_composite": (i32, [vp, i64, vp, vp, vp, vp, vp, i32, i32, C.POINTER(f64), vp, vp]),
     "ss_chain_views": (i32, [vp, C.POINTER(SSModel), vp, vp, i32, C.POINTER(vp), C.POINTER(vp), vp, i64, vp]),
+    "ss_chain_views_range": (i32, [vp, C.POINTER(SSModel), vp, vp, i32, C.POINTER(vp), C.POINTER(vp), vp, i64, i64,
+                                   i64, i64, vp, i64]),
+    "ss_sum_f64": (i32, [vp, vp, i64, vp]),
+    "ss_prepare_extras": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSCamera), C.POINTER(SSLight), vp, i64,
+                                C.POINTER(SSPreparedExtras)]),
+    "ss_adam_step_ld": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSAdamState), vp, i64, i32,
+                              C.POINTER(SSAdamHparams)]),
     "ss_engine_render": (i32, [vp, C.POINTER(SSScene), C.POINTER(SSEngineCamera), C.POINTER(SSEngineOut)]),
     "ss_grid_rebuild": (i32, [vp, vp, i64, C.POINTER(SSGridSpec), vp, vp, vp, vp, C.POINTER(i64)]),
     "ss_zigzag_varints": (i32, [vp, vp, i64, vp, u64, C.POINTER(u64)]),

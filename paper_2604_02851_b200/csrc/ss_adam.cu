@@ -15,32 +15,31 @@ namespace {
 struct AdamConst {
     double scale, b1, b2, omb1, omb2, bc1, bc2, eps, ema_beta, omema;
     double lr[6];  // means, log_scales, quaternions, logit_opacities, sh_dc, sh_rest
-    int64_t a;
+    int64_t a;     // rows updated
+    int64_t ld;    // rows per group in the gradient / moment layout (>= a; padding rows are skipped)
     int B;
 };
 
-// parameter pointer and learning rate of flat element e (ss_grad_layout)
+// parameter pointer and learning rate of flat element e (ss_grad_layout with
+// `a` = ld rows per group); NULL for an element of a padding row (>= c.a)
 __device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float* means, float* ls, float* quats,
                                              float* logits, float* sh, const AdamConst& c, double& lr) {
+    int64_t k, w;
+    float* p;
     if (e < 3 * a) {
-        lr = c.lr[0];
-        return means + e;
+        lr = c.lr[0], k = e, w = 3, p = means;
+    } else if (e < 6 * a) {
+        lr = c.lr[1], k = e - 3 * a, w = 3, p = ls;
+    } else if (e < 10 * a) {
+        lr = c.lr[2], k = e - 6 * a, w = 4, p = quats;
+    } else if (e < 11 * a) {
+        lr = c.lr[3], k = e - 10 * a, w = 1, p = logits;
+    } else {
+        k = e - 11 * a, w = 3 * B, p = sh;
+        lr = (k % B) == 0 ? c.lr[4] : c.lr[5];
     }
-    if (e < 6 * a) {
-        lr = c.lr[1];
-        return ls + (e - 3 * a);
-    }
-    if (e < 10 * a) {
-        lr = c.lr[2];
-        return quats + (e - 6 * a);
-    }
-    if (e < 11 * a) {
-        lr = c.lr[3];
-        return logits + (e - 10 * a);
-    }
-    const int64_t k = e - 11 * a;
-    lr = (k % B) == 0 ? c.lr[4] : c.lr[5];
-    return sh + k;
+    if (a != c.a && k >= c.a * w) return nullptr;
+    return p + k;
 }
 
 #ifndef ADAM_U
@@ -52,7 +51,7 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
                        float* __restrict__ logits, float* __restrict__ sh, double* __restrict__ m,
                        double* __restrict__ v, const float* __restrict__ g, AdamConst c) {
     SS_PDL_WAIT();
-    const int64_t a = c.a, total = a * (11 + 3 * (int64_t)c.B);
+    const int64_t a = c.ld, total = a * (11 + 3 * (int64_t)c.B);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += ADAM_U * stride) {
         float gv[ADAM_U], pv[ADAM_U];
@@ -61,8 +60,8 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t e = e0 + u * stride;
-            if (e < total) {
-                p[u] = adam_param(e, a, c.B, means, ls, quats, logits, sh, c, lr[u]);
+            p[u] = e < total ? adam_param(e, a, c.B, means, ls, quats, logits, sh, c, lr[u]) : nullptr;
+            if (p[u]) {
                 gv[u] = g[e];
                 mv[u] = m[e];
                 vv[u] = v[e];
@@ -72,7 +71,7 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t e = e0 + u * stride;
-            if (e >= total) continue;
+            if (!p[u]) continue;
             const double gg = dm((double)gv[u], c.scale);
             const double mm = da(dm(c.b1, mv[u]), dm(c.omb1, gg));
             const double v2 = da(dm(c.b2, vv[u]), dm(dm(c.omb2, gg), gg));
@@ -107,13 +106,18 @@ __global__ void k_adam_rows(float* __restrict__ quats, const float* __restrict__
 
 }  // namespace
 
-extern "C" int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int32_t n_views,
-                            const ss_adam_hparams* hp) {
+extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int64_t ld,
+                               int32_t n_views, const ss_adam_hparams* hp) {
     if (!ctx || !model || !st || !grad || !hp) return SS_ERR_INVALID;
     if (n_views < 1) return ss_fail(ctx, SS_ERR_INVALID, "no ready views");
     const int64_t a = model->active_count;
-    if (a == 0) return SS_OK;  // frozen-only model: no state change (optim.py:374)
+    if (ld < a) return ss_fail(ctx, SS_ERR_INVALID, "gradient layout rows %lld < active rows %lld", (long long)ld,
+                               (long long)a);
     const int t = st->step_count + 1;
+    if (a == 0) {  // a rank's empty row shard still counts the step
+        st->step_count = t;
+        return SS_OK;
+    }
     AdamConst c;
     c.scale = 1.0 / (double)n_views;
     c.b1 = hp->beta1;
@@ -132,8 +136,9 @@ extern "C" int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* st, con
     c.lr[4] = hp->lr_sh_dc;
     c.lr[5] = hp->lr_sh_rest;
     c.a = a;
+    c.ld = ld;
     c.B = (model->sh_degree + 1) * (model->sh_degree + 1);
-    const int64_t total = a * (11 + 3 * (int64_t)c.B);
+    const int64_t total = ld * (11 + 3 * (int64_t)c.B);
     int64_t grid = (total + 255) / 256;
     if (grid > (int64_t)ctx->num_sms * 32) grid = (int64_t)ctx->num_sms * 32;
     ss_tic(ctx, KC_ADAM);
@@ -147,4 +152,12 @@ extern "C" int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* st, con
     ss_toc(ctx, KC_ADAM);
     st->step_count = t;
     return SS_OK;
+}
+
+extern "C" int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int32_t n_views,
+                            const ss_adam_hparams* hp) {
+    if (!ctx || !model || !st || !grad || !hp) return SS_ERR_INVALID;
+    if (n_views < 1) return ss_fail(ctx, SS_ERR_INVALID, "no ready views");
+    if (model->active_count == 0) return SS_OK;  // frozen-only model: no state change (optim.py:374)
+    return ss_adam_step_ld(ctx, model, st, grad, model->active_count, n_views, hp);
 }

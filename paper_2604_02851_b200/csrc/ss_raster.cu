@@ -1130,7 +1130,9 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     acc[10] += (float)(g[3] * op * (1 - op));
 }
 
-// gradient layout offsets of a row's 11 non-SH entries (see ss_grad_layout)
+// gradient layout offsets of a row's 11 non-SH entries (see ss_grad_layout;
+// `a` is the layout's row count -- the active count, or a row shard's length
+// in the view-sharded step -- and `row` is relative to the layout's first row)
 __device__ __forceinline__ void grad_row_load(const float* grad, int64_t a, int64_t row, float* acc) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -1193,15 +1195,20 @@ struct ChainViews {
 #ifndef CV_PREFETCH
 #define CV_PREFETCH 1
 #endif
+// Inputs j in [j0, j1) (row = subset[j], or j); the gradient layout starts at
+// row0 with ld rows per group (ld = a, row0 = 0 on one GPU; a row shard in
+// the view-sharded step, whose g9 / rinv pointers are offset to be indexed by j).
 template <int DEG>
 __global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const ChainViews* __restrict__ V, int nv,
-                                                        const int64_t* __restrict__ subset, int64_t n_in,
+                                                        const int64_t* __restrict__ subset, int64_t j0, int64_t j1,
+                                                        int64_t row0, int64_t ld,
                                                         float* __restrict__ grad, float4* __restrict__ shrec) {
     SS_PDL_WAIT();
     const int64_t a = m.active_count;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < j1; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = subset ? subset[j] : j;
         if (row >= a) continue;
+        const int64_t rel = row - row0;
         float acc[11];
         bool any = false;
 #if CV_PREFETCH
@@ -1211,15 +1218,15 @@ __global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const 
         for (int v = 0; v < nv; ++v) {
             if (V->rinv[v][j] == ~0u) continue;
             if (!any) {
-                grad_row_load(grad, a, row, acc);
+                grad_row_load(grad, ld, rel, acc);
                 any = true;
             }
             float g[9];
 #pragma unroll
             for (int e = 0; e < 9; ++e) g[e] = V->g9[v][j * 9 + e];
-            chain_row<float, DEG>(m, V->cam[v], V->light[v], row, g, acc, shrec + ((int64_t)v * a + row) * 2);
+            chain_row<float, DEG>(m, V->cam[v], V->light[v], row, g, acc, shrec + ((int64_t)v * ld + rel) * 2);
         }
-        if (any) grad_row_store(grad, a, row, acc);
+        if (any) grad_row_store(grad, ld, rel, acc);
     }
 }
 
@@ -1304,9 +1311,10 @@ __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __res
 #endif
 constexpr int SHGV_ROWS = SS_SHGV_ROWS;
 
+// rows [0, a) of a layout of ld rows per group (shrec: ld records per view)
 template <int DEG>
 __global__ void __launch_bounds__(256) k_sh_grad_views(const ChainViews* __restrict__ V, int nv,
-                                                       const float4* __restrict__ shrec, int64_t a,
+                                                       const float4* __restrict__ shrec, int64_t a, int64_t ld,
                                                        float* __restrict__ grad_sh) {
     SS_PDL_WAIT();
     constexpr int B = ss_sh_bases(DEG);
@@ -1318,7 +1326,7 @@ __global__ void __launch_bounds__(256) k_sh_grad_views(const ChainViews* __restr
     for (int t = threadIdx.x; t < nv * SHGV_ROWS; t += blockDim.x) {
         const int v = t / SHGV_ROWS, r = t - v * SHGV_ROWS;
         if (r >= nrows) continue;
-        const float4* rec = shrec + ((int64_t)v * a + row0 + r) * 2;
+        const float4* rec = shrec + ((int64_t)v * ld + row0 + r) * 2;
         const float4 r0 = rec[0], r1 = rec[1];
         const float dir[3] = {r1.x, r1.y, r1.z};
         float Y[B];
@@ -1576,6 +1584,42 @@ int render_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_ligh
     return SS_OK;
 }
 
+// The chain rule of nv views (host ChainViews) over inputs [j0, j1) into a
+// gradient layout of ld rows from row0 (see ss_chain_views_range); scratch
+// from the current call's arena.  The per-view backward of the fp32 blend
+// runs it with one view, so a view's gradient is the same kernel's whether
+// the chain is deferred to the step or not (bit-identical by construction).
+int launch_chain_views(ss_ctx* ctx, const ss_model* m, const ChainViews& hv, int nv, const int64_t* subset,
+                       int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld) {
+    cudaStream_t s = ctx->stream;
+    ChainViews* dv = SS_SCRATCH(ctx, ChainViews, 1);
+    float4* shrec = SS_SCRATCH(ctx, float4, 2 * ld * nv);
+    if (!dv || !shrec) return SS_ERR_CUDA;
+    SS_CUDA(ctx, cudaMemcpyAsync(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice, s));
+    SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)ld * nv, s));
+    ss_tic(ctx, KC_CHAIN);
+#define SS_CHAINV(DEG)                                                                                                     \
+    do {                                                                                                                   \
+        constexpr int B = ss_sh_bases(DEG);                                                                                \
+        SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, j1 - j0, 128)), dim3(128), 0, s, *m, (const ChainViews*)dv, \
+                               nv, subset, j0, j1, row0, ld, grad, shrec));                                                \
+        SS_CHECK_LAUNCH(ctx);                                                                                              \
+        const size_t smem = (size_t)nv * SHGV_ROWS * (sizeof(float4) + sizeof(float) * (B + 1));                           \
+        SS_CUDA(ctx, ss_launch((k_sh_grad_views<DEG>), dim3((unsigned)((rows + SHGV_ROWS - 1) / SHGV_ROWS)), dim3(256), smem, s, \
+                               (const ChainViews*)dv, nv, (const float4*)shrec, rows, ld, grad + 11 * ld));               \
+        SS_CHECK_LAUNCH(ctx);                                                                                              \
+    } while (0)
+    switch (m->sh_degree) {
+        case 0: SS_CHAINV(0); break;
+        case 1: SS_CHAINV(1); break;
+        case 2: SS_CHAINV(2); break;
+        default: SS_CHAINV(3); break;
+    }
+#undef SS_CHAINV
+    ss_toc(ctx, KC_CHAIN);
+    return SS_OK;
+}
+
 template <typename R>
 int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L, const ss_render_opts* o,
                const float* gt, float* grad, double* loss, void* img_out, ss_render_stats* st) {
@@ -1614,6 +1658,22 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         SS_CHECK_LAUNCH(ctx);
         SS_CUDA(ctx, cudaMemcpyAsync(o->defer_rinv, b.rinv, sizeof(uint32_t) * (size_t)b.n_in, cudaMemcpyDeviceToDevice, s));
         ss_toc(ctx, KC_CHAIN);
+    } else if (b.n_in > 0 && m->active_count > 0 && sizeof(R) == 4) {
+        float* g9 = SS_SCRATCH(ctx, float, 9 * b.n_in);
+        if (!g9) return SS_ERR_CUDA;
+        ss_tic(ctx, KC_CHAIN);
+        SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals, partials, b.n_in,
+                               (R*)g9));
+        SS_CHECK_LAUNCH(ctx);
+        ss_toc(ctx, KC_CHAIN);
+        ChainViews hv;
+        memset(&hv, 0, sizeof(hv));
+        hv.cam[0] = *cam;
+        hv.light[0] = *L;
+        hv.g9[0] = g9;
+        hv.rinv[0] = b.rinv;
+        const int64_t a = m->active_count;
+        SS_TRY(launch_chain_views(ctx, m, hv, 1, o->subset, 0, b.n_in, 0, a, grad, a));
     } else if (b.n_in > 0 && m->active_count > 0) {
         ss_tic(ctx, KC_CHAIN);
         R* g9 = SS_SCRATCH(ctx, R, 9 * b.n_in);
@@ -1643,6 +1703,41 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         st->tiles = b.n_tiles;
     }
     return SS_OK;
+}
+
+// the rest of PreparedSplats (ss_prepare_extras), one thread per prepared splat
+template <int DEG>
+__global__ void k_prepare_extras(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ rows, int64_t M,
+                                 ss_prepared_extras o) {
+    SS_PDL_WAIT();
+    constexpr int B = ss_sh_bases(DEG);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = rows[i];
+        Proj P;
+        ss_cam_point(cam, m.means + row * 3, P.d, P.mc);
+        const float* ls = m.log_scales + row * 3;
+        ss_project(cam, ls, m.quaternions + row * 4, true, P);
+        float shv[3 * B];
+        ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, shv);
+        Shade<DEG, double> S;
+        ss_shade_v<DEG, double>(L, ls, shv, m.light_visibility[row], P.d, P.Rq, S);
+        if (o.mu_cam) for (int k = 0; k < 3; ++k) o.mu_cam[3 * i + k] = P.mc[k];
+        if (o.J) for (int r = 0; r < 2; ++r) for (int k = 0; k < 3; ++k) o.J[6 * i + 3 * r + k] = P.J[r][k];
+        if (o.sigma3d)
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    o.sigma3d[9 * i + 3 * a + b] = da(da(dm(dm(P.Rq[a][0], P.S2[0]), P.Rq[b][0]), dm(dm(P.Rq[a][1], P.S2[1]), P.Rq[b][1])),
+                                                      dm(dm(P.Rq[a][2], P.S2[2]), P.Rq[b][2]));
+        if (o.cov_cam) for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) o.cov_cam[9 * i + 3 * a + b] = P.cov[a][b];
+        if (o.view_dir) for (int k = 0; k < 3; ++k) o.view_dir[3 * i + k] = S.vdir[k];
+        if (o.view_dist) o.view_dist[i] = S.dist;
+        if (o.n_hat) for (int k = 0; k < 3; ++k) o.n_hat[3 * i + k] = S.nhat[k];
+        if (o.n_axis) o.n_axis[i] = S.axis;
+        if (o.Y) for (int b = 0; b < B; ++b) o.Y[B * i + b] = S.Y[b];
+        if (o.albedo_est) for (int c = 0; c < 3; ++c) o.albedo_est[3 * i + c] = S.albedo[c];
+        if (o.cos) o.cos[i] = S.cosv;
+        if (o.vis) o.vis[i] = S.vis;
+    }
 }
 
 // composite() of prepared splats already in draw order (ss_composite)
@@ -1758,16 +1853,17 @@ int ss_composite(ss_ctx* ctx, int64_t n, const double* mu2d, const double* inv2d
     return forward<double>(ctx, &cam, &o, b, img, T, stop);
 }
 
-int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights, int32_t n_views,
-                   const float* const* g9, const uint32_t* const* rinv, const int64_t* subset, int64_t n_in,
-                   float* grad) {
+int ss_chain_views_range(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights,
+                         int32_t n_views, const float* const* g9, const uint32_t* const* rinv, const int64_t* subset,
+                         int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld) {
     if (!ctx || !m || !cams || !lights || !g9 || !rinv || !grad) return SS_ERR_INVALID;
     if (n_views < 1 || n_views > CV_MAX_VIEWS) return ss_fail(ctx, SS_ERR_INVALID, "1..%d views", CV_MAX_VIEWS);
-    if (m->sh_degree < 0 || m->sh_degree > 3 || n_in < 0) return ss_fail(ctx, SS_ERR_INVALID, "bad model or row count");
-    const int64_t a = m->active_count;
-    if (a <= 0 || n_in == 0) return SS_OK;
+    if (m->sh_degree < 0 || m->sh_degree > 3 || j0 < 0 || j1 < j0) return ss_fail(ctx, SS_ERR_INVALID, "bad model or row range");
+    if (row0 < 0 || rows < 0 || ld < rows || row0 + rows > m->active_count)
+        return ss_fail(ctx, SS_ERR_INVALID, "bad gradient layout (row0 %lld, rows %lld, ld %lld)", (long long)row0,
+                       (long long)rows, (long long)ld);
+    if (rows == 0 || j1 == j0) return SS_OK;
     SS_TRY(ss_scratch_reset(ctx));
-    cudaStream_t s = ctx->stream;
     ChainViews hv;
     memset(&hv, 0, sizeof(hv));
     for (int v = 0; v < n_views; ++v) {
@@ -1777,31 +1873,30 @@ int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const 
         hv.g9[v] = g9[v];
         hv.rinv[v] = rinv[v];
     }
-    ChainViews* dv = SS_SCRATCH(ctx, ChainViews, 1);
-    float4* shrec = SS_SCRATCH(ctx, float4, 2 * a * n_views);
-    if (!dv || !shrec) return SS_ERR_CUDA;
-    SS_CUDA(ctx, cudaMemcpyAsync(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice, s));
-    SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)a * n_views, s));
-    ss_tic(ctx, KC_CHAIN);
-#define SS_CHAINV(DEG)                                                                                                     \
-    do {                                                                                                                   \
-        constexpr int B = ss_sh_bases(DEG);                                                                                \
-        SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, n_in, 128)), dim3(128), 0, s, *m, (const ChainViews*)dv, \
-                               (int)n_views, subset, n_in, grad, shrec));                                                  \
-        SS_CHECK_LAUNCH(ctx);                                                                                              \
-        const size_t smem = (size_t)n_views * SHGV_ROWS * (sizeof(float4) + sizeof(float) * (B + 1));                      \
-        SS_CUDA(ctx, ss_launch((k_sh_grad_views<DEG>), dim3((unsigned)((a + SHGV_ROWS - 1) / SHGV_ROWS)), dim3(256), smem, s,  \
-                               (const ChainViews*)dv, (int)n_views, (const float4*)shrec, a, grad + 11 * a));              \
-        SS_CHECK_LAUNCH(ctx);                                                                                              \
-    } while (0)
-    switch (m->sh_degree) {
-        case 0: SS_CHAINV(0); break;
-        case 1: SS_CHAINV(1); break;
-        case 2: SS_CHAINV(2); break;
-        default: SS_CHAINV(3); break;
-    }
-#undef SS_CHAINV
-    ss_toc(ctx, KC_CHAIN);
+    return launch_chain_views(ctx, m, hv, n_views, subset, j0, j1, row0, rows, grad, ld);
+}
+
+int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights, int32_t n_views,
+                   const float* const* g9, const uint32_t* const* rinv, const int64_t* subset, int64_t n_in,
+                   float* grad) {
+    if (!m) return SS_ERR_INVALID;
+    const int64_t a = m->active_count;
+    if (a <= 0 || n_in <= 0) return SS_OK;
+    return ss_chain_views_range(ctx, m, cams, lights, n_views, g9, rinv, subset, 0, n_in, 0, a, grad, a);
+}
+
+// loss = ((x[0] + x[1]) + x[2]) + ...: the reference's per-view loss sum order (optim.py:366-367)
+__global__ void k_sum_f64_seq(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+    SS_PDL_WAIT();
+    double t = 0.0;
+    for (int64_t i = 0; i < n; ++i) t += x[i];
+    *out = t;
+}
+
+int ss_sum_f64(ss_ctx* ctx, const double* x, int64_t n, double* out) {
+    if (!ctx || !x || !out || n < 0) return SS_ERR_INVALID;
+    SS_CUDA(ctx, ss_launch((k_sum_f64_seq), dim3(1), dim3(1), 0, ctx->stream, x, n, out));
+    SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }
 
@@ -1838,6 +1933,22 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
     }
     if (visible_out) *visible_out = (int64_t)M;
     SS_CUDA(ctx, cudaStreamSynchronize(s));
+    return SS_OK;
+}
+
+int ss_prepare_extras(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L, const int64_t* rows,
+                      int64_t M, ss_prepared_extras* out) {
+    if (!ctx || !m || !cam || !L || !out || (M > 0 && !rows)) return SS_ERR_INVALID;
+    if (m->sh_degree < 0 || m->sh_degree > 3 || M < 0) return ss_fail(ctx, SS_ERR_INVALID, "bad model or count");
+    if (M == 0) return SS_OK;
+    SS_TRY(ss_scratch_reset(ctx));
+    switch (m->sh_degree) {
+        case 0: SS_CUDA(ctx, ss_launch((k_prepare_extras<0>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
+        case 1: SS_CUDA(ctx, ss_launch((k_prepare_extras<1>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
+        case 2: SS_CUDA(ctx, ss_launch((k_prepare_extras<2>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
+        default: SS_CUDA(ctx, ss_launch((k_prepare_extras<3>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
+    }
+    SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }
 

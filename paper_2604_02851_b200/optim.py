@@ -5,14 +5,15 @@ Gradients (optim.py:50), loss (optim.py:80), backward (optim.py:113),
 LearningRates (optim.py:271), OptimizerState (optim.py:281), step
 (optim.py:353).
 
-Per view, ss_backward runs K1-K7 (preprocess, depth sort, binning, forward,
-front-to-back backward with per-(tile, splat) partials, chain rule) and
-accumulates into ONE flat float32 gradient buffer
-[means | log_scales | quaternions | logit_opacities | sh_coeffs] over the
-active rows.  With a process group the buffer and the loss are summed with a
-single NCCL all-reduce (reference views sharded across GPUs,
-SURVEY.md §8e); ss_adam_step then applies the batch-averaged Adam update
-with float64 moments.
+Per view, ss_backward runs K1-K6 (preprocess, depth sort, binning, forward,
+front-to-back backward with per-(tile, splat) partials) and the fixed-order
+partial sums, leaving per-row screen-space gradients; ONE chain-rule pass
+over the rows (ss_chain_views_range) turns every view's records into the
+flat float32 gradient [means | log_scales | quaternions | logit_opacities |
+sh_coeffs], and ss_adam_step applies the batch-averaged Adam update with
+float64 moments.  On N GPUs the same step is sharded by views and rows with
+an exchange of the screen-space records (parallel.py); its result is
+bit-identical to the single-GPU step.
 """
 
 from __future__ import annotations
@@ -222,17 +223,25 @@ class LearningRates:
 
 
 class OptimizerState:
-    """Adam state for the active rows, HBM-resident (float64 moments).
+    """Adam state for the active rows, HBM-resident (float64 moments, int64
+    age, float64 grad-norm EMA).
 
-    `.m[group]` / `.v[group]` are torch views into the flat moment buffers
-    (same shapes as the reference's numpy arrays); `.age` (int64) and
-    `.grad_ema` (float64) are torch tensors.  `step_count` is a host int.
+    Reference view (ref optim.py:281-310): `.m[group]`, `.v[group]`, `.age`,
+    `.grad_ema` are numpy arrays with the reference's shapes; they are host
+    mirrors of the device buffers, taken when first read after a device
+    update, and anything written into them is uploaded before the next device
+    use (step, resize, pool policies) -- the reference's tests read and write
+    them directly (pkg/tests/test_optim.py:342-376).  `step_count` is a host int.
+
+    With `process_group` (the view-sharded step, parallel.py) each rank holds
+    only its row shard of the moments/age/EMA (ZeRO-1); the numpy views are
+    then the shard's, and `device_stats()` gathers the full age/EMA.
     """
 
     GROUPS = TRAINABLE
 
     def __init__(self, model, lrs: Optional[LearningRates] = None, scene_extent: float = 1.0,
-                 betas=(0.9, 0.999), eps: float = 1e-8, ema_beta: float = 0.99, device=None):
+                 betas=(0.9, 0.999), eps: float = 1e-8, ema_beta: float = 0.99, device=None, process_group=None):
         import torch
         self.lrs = lrs or LearningRates()
         self.scene_extent = float(scene_extent)
@@ -244,27 +253,129 @@ class OptimizerState:
             device = model.device if isinstance(model, DeviceModel) else torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
         self.sh_degree = int(model.sh_degree)
+        self.process_group = process_group
+        if process_group is not None:
+            import torch.distributed as dist
+            self._world, self._rank = dist.get_world_size(process_group), dist.get_rank(process_group)
+        else:
+            self._world, self._rank = 1, 0
+        self._host = None
+        self._dirty = False
         self._alloc(int(model.active_count))
+
+    # ---- layout
+    @property
+    def plan(self) -> parallel.ShardPlan:
+        return parallel.ShardPlan(self._world, self._rank, self._active)
+
+    @property
+    def ld(self) -> int:
+        """Rows per group of this rank's moment / gradient layout."""
+        return self._active if self._world == 1 else self.plan.R
 
     def _alloc(self, a):
         import torch
-        n = a * (11 + 3 * (self.sh_degree + 1) ** 2)
-        self.m_flat = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
-        self.v_flat = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
-        self.age = torch.zeros(a, dtype=torch.int64, device=self.device)
-        self.grad_ema = torch.zeros(a, dtype=torch.float64, device=self.device)
+        self._active = int(a)
+        ld = self.ld
+        n = ld * (11 + 3 * (self.sh_degree + 1) ** 2)
+        self.m_dev = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
+        self.v_dev = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
+        self.age_dev = torch.zeros(max(ld, 1), dtype=torch.int64, device=self.device)
+        self.ema_dev = torch.zeros(max(ld, 1), dtype=torch.float64, device=self.device)
+        self._host = None
+        self._dirty = False
 
     @property
     def active_count(self) -> int:
-        return int(self.age.shape[0])
+        return self._active
+
+    def _groups(self, flat):
+        """Per-group views of a flat moment buffer (this rank's rows)."""
+        ld, rows = self.ld, (self._active if self._world == 1 else self.plan.rows)
+        parts = split_flat(flat, ld, self.sh_degree) if ld > 0 else split_flat(flat[:0], 0, self.sh_degree)
+        return {k: v[:rows] for k, v in parts.items()}
+
+    # ---- reference-visible numpy mirror (write-back)
+    def _mirror(self):
+        if self._host is None:
+            rows = self._active if self._world == 1 else self.plan.rows
+            self._host = dict(m={k: v.cpu().numpy() for k, v in self._groups(self.m_dev).items()},
+                              v={k: v.cpu().numpy() for k, v in self._groups(self.v_dev).items()},
+                              age=self.age_dev[:rows].cpu().numpy(), grad_ema=self.ema_dev[:rows].cpu().numpy())
+        self._dirty = True  # handed out: the caller may write into it
+        return self._host
+
+    def sync_device(self):
+        """Upload host-mirror writes (before any device use of the state)."""
+        import torch
+        if self._host is not None and self._dirty:
+            h = self._host
+            for key, flat in (("m", self.m_dev), ("v", self.v_dev)):
+                for k, t in self._groups(flat).items():
+                    t.copy_(torch.from_numpy(np.ascontiguousarray(h[key][k], np.float64)).reshape(t.shape))
+            rows = len(h["age"])
+            self.age_dev[:rows].copy_(torch.from_numpy(np.ascontiguousarray(h["age"], np.int64)))
+            self.ema_dev[:rows].copy_(torch.from_numpy(np.ascontiguousarray(h["grad_ema"], np.float64)))
+        self._host = None
+        self._dirty = False
 
     @property
     def m(self):
-        return split_flat(self.m_flat, self.active_count, self.sh_degree)
+        return self._mirror()["m"]
 
     @property
     def v(self):
-        return split_flat(self.v_flat, self.active_count, self.sh_degree)
+        return self._mirror()["v"]
+
+    @property
+    def age(self):
+        return self._mirror()["age"]
+
+    @age.setter
+    def age(self, value):
+        self._mirror()["age"][...] = value
+
+    @property
+    def grad_ema(self):
+        return self._mirror()["grad_ema"]
+
+    @grad_ema.setter
+    def grad_ema(self, value):
+        self._mirror()["grad_ema"][...] = value
+
+    # ---- device views
+    def device_groups(self):
+        """(m, v) per-group device views of this rank's rows."""
+        self.sync_device()
+        return self._groups(self.m_dev), self._groups(self.v_dev)
+
+    def device_stats(self):
+        """(age, grad_ema) device tensors over ALL active rows (gathered from
+        the ranks' shards in the sharded step) for the pool policies."""
+        import torch
+        self.sync_device()
+        a = self._active
+        if self._world == 1:
+            return self.age_dev[:a], self.ema_dev[:a]
+        coll = parallel.Collectives(self.process_group)
+        R = self.plan.R
+        age = torch.empty(self._world * R, dtype=torch.int64, device=self.device)
+        ema = torch.empty(self._world * R, dtype=torch.float64, device=self.device)
+        age[self._rank * R:(self._rank + 1) * R].copy_(self.age_dev[:R])
+        ema[self._rank * R:(self._rank + 1) * R].copy_(self.ema_dev[:R])
+        coll.all_gather_rows(age, R)
+        coll.all_gather_rows(ema, R)
+        return age[:a], ema[:a]
+
+    def adam_struct(self) -> _lib.SSAdamState:
+        self.sync_device()
+        st = _lib.SSAdamState()
+        st.m = self.m_dev.data_ptr()
+        st.v = self.v_dev.data_ptr()
+        st.grad_ema = self.ema_dev.data_ptr()
+        st.age = self.age_dev.data_ptr()
+        st.step_count = self.step_count
+        return st
 
     def hparams(self) -> _lib.SSAdamHparams:
         h = _lib.SSAdamHparams()
@@ -279,12 +390,46 @@ class OptimizerState:
         h.ema_beta = self.ema_beta
         return h
 
+    def _full(self):
+        """(m groups, v groups, age, ema) over all active rows (device)."""
+        import torch
+        self.sync_device()
+        a = self._active
+        if self._world == 1:
+            return self._groups(self.m_dev), self._groups(self.v_dev), self.age_dev[:a], self.ema_dev[:a]
+        coll = parallel.Collectives(self.process_group)
+        R, W = self.plan.R, self._world
+        out = []
+        for flat in (self.m_dev, self.v_dev):
+            mine = split_flat(flat, R, self.sh_degree)
+            full = {}
+            for k, t in mine.items():
+                g = torch.empty((W * R,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+                g[self._rank * R:(self._rank + 1) * R].copy_(t)
+                coll.all_gather_rows(g, R)
+                full[k] = g[:a]
+            out.append(full)
+        age, ema = self.device_stats()
+        return out[0], out[1], age, ema
+
+    def _load_full(self, m, v, age, ema):
+        """Keep this rank's rows of full (active-row) state arrays."""
+        a = int(age.shape[0])
+        self._alloc(a)
+        r0, rows = (0, a) if self._world == 1 else (self.plan.row0, self.plan.rows)
+        for src, flat in ((m, self.m_dev), (v, self.v_dev)):
+            for k, t in self._groups(flat).items():
+                t.copy_(src[k][r0:r0 + rows])
+        self.age_dev[:rows].copy_(age[r0:r0 + rows])
+        self.ema_dev[:rows].copy_(ema[r0:r0 + rows])
+
     def resize(self, record):
-        """Follow a model mutation record (ref optim.py:312-343)."""
+        """Follow a model mutation record (ref optim.py:312-343).  In the
+        sharded step every rank applies the same record: the state is gathered,
+        remapped and re-split over the new active count."""
         import torch
         kind = type(record).__name__
-        a = self.active_count
-        groups_m, groups_v = self.m, self.v
+        a = self._active
         if kind == "AppendRecord":
             if record.insert_at != a:
                 raise ValueError("append record does not extend the active region")
@@ -308,125 +453,258 @@ class OptimizerState:
             t = t if sel is None else t[sel]
             if pad:
                 t = torch.cat([t, torch.zeros((pad,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)])
-            return t
+            return t.clone()
 
-        new_m = {k: remap(v) for k, v in groups_m.items()}
-        new_v = {k: remap(v) for k, v in groups_v.items()}
-        age, ema = remap(self.age), remap(self.grad_ema)
-        na = int(age.shape[0])
-        self._alloc(na)
-        for k in TRAINABLE:
-            self.m[k].copy_(new_m[k])
-            self.v[k].copy_(new_v[k])
-        self.age.copy_(age)
-        self.grad_ema.copy_(ema)
+        m, v, age, ema = self._full()
+        self._load_full({k: remap(t) for k, t in m.items()}, {k: remap(t) for k, t in v.items()}, remap(age),
+                        remap(ema))
 
 
 class StepWorkspace:
-    """Reusable per-model device buffers for step() (gradient sum, loss, and
-    the per-view screen-space gradients of the deferred chain rule)."""
+    """Reusable per-model device buffers for step(): the gradient (this
+    rank's layout), the per-view losses, and the per-view-slot screen-space
+    records of the deferred chain rule (plus their exchange buffers when the
+    step is sharded)."""
 
     def __init__(self, model: DeviceModel):
         import torch
-        a = model.active_count
-        n = a * (11 + 3 * (model.sh_degree + 1) ** 2)
-        self.n = n
-        self.grad = torch.zeros(max(n, 1), dtype=torch.float32, device=model.device)
-        self.loss = torch.zeros(1, dtype=torch.float64, device=model.device)
-        self._defer = None
+        self.device = model.device
+        self.grad = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.losses = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._slots = None
+        self._recv = None
 
-    def defer_buffers(self, views: int, n_in: int, device):
-        """Per view: g9 (n_in, 9) float32 and rinv (n_in,) int32 device buffers
-        (contiguous slices of one allocation, grown on demand)."""
+    def prepare(self, grad_elems: int, n_views: int):
         import torch
-        d = self._defer
-        if d is None or d[0].shape[0] < views or d[0].shape[1] < n_in:
-            cap = max(n_in, 1, d[0].shape[1] if d is not None else 0)
-            d = self._defer = (torch.empty((max(views, d[0].shape[0] if d is not None else 0), cap, 9),
-                                           dtype=torch.float32, device=device),
-                               torch.empty((max(views, d[0].shape[0] if d is not None else 0), cap), dtype=torch.int32,
-                                           device=device))
-        return [d[0][i, :n_in] for i in range(views)], [d[1][i, :n_in] for i in range(views)]
+        if self.grad.numel() < max(grad_elems, 1):
+            self.grad = torch.zeros(max(grad_elems, 1), dtype=torch.float32, device=self.device)
+        if self.losses.numel() < n_views:
+            self.losses = torch.zeros(n_views, dtype=torch.float64, device=self.device)
+        self.grad[:grad_elems].zero_()
+        self.losses[:n_views].zero_()
+        self.loss.zero_()
+        return self.grad[:max(grad_elems, 1)]
+
+    def _buffers(self, attr, slots: int, rows: int):
+        import torch
+        d = getattr(self, attr)
+        if d is None or d[0].shape[0] < slots or d[0].shape[1] < rows:
+            cs = max(slots, d[0].shape[0] if d is not None else 0)
+            cr = max(rows, 1, d[0].shape[1] if d is not None else 0)
+            d = (torch.empty((cs, cr, 9), dtype=torch.float32, device=self.device),
+                 torch.empty((cs, cr), dtype=torch.int32, device=self.device))
+            setattr(self, attr, d)
+        return [(d[0][i, :rows], d[1][i, :rows]) for i in range(slots)]
+
+    def slot_records(self, slots: int, rows: int):
+        """Per view slot: g9 (rows, 9) float32 and rinv (rows,) int32."""
+        return self._buffers("_slots", slots, rows)
+
+    def recv_records(self, slots: int, rows: int):
+        return self._buffers("_recv", slots, rows)
+
+    def defer_buffers(self, views: int, n_in: int, device=None):
+        """(g9 list, rinv list) of `views` slots over n_in rows (ss_backward's defer=)."""
+        recs = self.slot_records(views, n_in)
+        return [g for g, _ in recs], [r for _, r in recs]
 
 
 CHAIN_MAX_VIEWS = 16  # ss_chain_views
 
 
-def chain_views(model: DeviceModel, views, g9, rinv, grad, subset_tensor=None):
+def chain_views(model: DeviceModel, views, g9, rinv, grad, subset_tensor=None, j0=0, j1=None, row0=0, rows=None,
+                ld=None):
     """The deferred chain rule of `views` (their backward_device calls got
     defer=(g9[i], rinv[i])): one pass over the rows, the gradient read and
-    written once (ss_chain_views)."""
+    written once (ss_chain_views_range).  g9 / rinv entries are tensors or
+    raw device addresses."""
     import ctypes as C
     c = _lib.ctx(model.device.index)
     k = len(views)
     cams = (_lib.SSCamera * k)(*[camera_struct(v.pose, v.intrinsics) for v in views])
     lights = (_lib.SSLight * k)(*[light_struct(v.light_state) for v in views])
-    gp = (C.c_void_p * k)(*[g9[i].data_ptr() for i in range(k)])
-    rp = (C.c_void_p * k)(*[rinv[i].data_ptr() for i in range(k)])
-    n_in = int(subset_tensor.numel()) if subset_tensor is not None else model.count
-    c.check(c.lib.ss_chain_views(c.handle, model.struct(), cams, lights, k, gp, rp,
-                                 _lib.ptr(subset_tensor) if subset_tensor is not None else None, n_in, _lib.ptr(grad)))
+    addr = lambda x: x if isinstance(x, int) else x.data_ptr()
+    gp = (C.c_void_p * k)(*[addr(g9[i]) for i in range(k)])
+    rp = (C.c_void_p * k)(*[addr(rinv[i]) for i in range(k)])
+    if j1 is None:
+        j1 = int(subset_tensor.numel()) if subset_tensor is not None else model.count
+    a = model.active_count
+    rows = a if rows is None else rows
+    ld = a if ld is None else ld
+    c.check(c.lib.ss_chain_views_range(c.handle, model.struct(), cams, lights, k, gp, rp,
+                                       _lib.ptr(subset_tensor) if subset_tensor is not None else None,
+                                       int(j0), int(j1), int(row0), int(rows), _lib.ptr(grad), int(ld)))
+
+
+def _row_struct(dm: DeviceModel, row0: int, rows: int) -> _lib.SSModel:
+    """ss_model of rows [row0, row0 + rows) of dm, all of them active (a row
+    shard for the sharded Adam)."""
+    s = dm.struct()
+    B = (dm.sh_degree + 1) ** 2
+    for k, w, es in (("means", 3, 4), ("log_scales", 3, 4), ("quaternions", 4, 4), ("logit_opacities", 1, 4),
+                     ("sh_coeffs", 3 * B, 4), ("light_visibility", 1, 4), ("object_ids", 1, 4)):
+        setattr(s, k, getattr(dm, k).data_ptr() + row0 * w * es)
+    s.count = rows
+    s.active_count = rows
+    return s
+
+
+class _DeviceKernels:
+    """The compute of parallel.sharded_step on this GPU (libsplat_b200)."""
+
+    def __init__(self, dm: DeviceModel, state: OptimizerState, ws: StepWorkspace, views, subset, extent_cutoff,
+                 plan: parallel.ShardPlan):
+        self.dm, self.state, self.ws, self.sub, self.cutoff, self.plan = dm, state, ws, subset, extent_cutoff, plan
+        self.n_in = int(subset.numel()) if subset is not None else dm.count
+        B = (dm.sh_degree + 1) ** 2
+        self.ld = dm.active_count if plan.world == 1 else plan.R
+        self.grad = ws.prepare(self.ld * (11 + 3 * B), len(views))
+        self.gts = {}
+        self.views = views
+
+    def stage(self, local_views):
+        gts = _stage_ground_truth(local_views, self.dm.device)
+        self.gts = {id(v): g for v, g in zip(local_views, gts)}
+
+    def _rows_alloc(self):
+        return self.n_in if self.plan.world == 1 else max(self.plan.padded, self.dm.count)
+
+    def records(self, slots):
+        return self.ws.slot_records(slots, self._rows_alloc())
+
+    def backward(self, view, rec, i):
+        import torch
+        g9, rinv = rec
+        sharded_subset = self.plan.world > 1 and self.sub is not None
+        if sharded_subset:  # input-indexed records first, then scattered to row order for the exchange
+            tmp_g9 = torch.empty((self.n_in, 9), dtype=torch.float32, device=self.dm.device)
+            tmp_r = torch.empty(self.n_in, dtype=torch.int32, device=self.dm.device)
+            defer = (tmp_g9, tmp_r)
+        else:
+            defer = (g9[:self.n_in], rinv[:self.n_in])
+        backward_device(self.dm, view, self.grad, self.ws.losses[i:i + 1], None, self.cutoff, 0, None,
+                        subset_tensor=self.sub, gt=self.gts[id(view)], defer=defer)
+        if sharded_subset:
+            rinv.fill_(-1)
+            g9[self.sub] = tmp_g9
+            rinv[self.sub] = tmp_r
+
+    def invisible(self, rec):
+        rec[1].fill_(-1)  # 0xffffffff: not visible in this view
+
+    def exchange(self, coll, send):
+        P = self.plan.padded
+        recv = self.ws.recv_records(len(send), P)
+        for (sg, sr), (rg, rr) in zip(send, recv):
+            coll.all_to_all(rg, sg[:P])
+            coll.all_to_all(rr, sr[:P])
+        return recv
+
+    def shard_view(self, rec, s):
+        """Source rank s's records of this rank's rows, as addresses indexed by row."""
+        R, r0 = self.plan.R, self.plan.row0
+        g9, rinv = rec
+        return (g9.data_ptr() + (s * R - r0) * 36, rinv.data_ptr() + (s * R - r0) * 4)
+
+    def chain_batch(self, views, recs):
+        if self.dm.active_count == 0 or self.n_in == 0 or self.plan.rows == 0:
+            return
+        g9 = [r[0] for r in recs]
+        rinv = [r[1] for r in recs]
+        if self.plan.world == 1:
+            chain_views(self.dm, views, g9, rinv, self.grad, self.sub)
+        else:
+            r0, rows = self.plan.row0, self.plan.rows
+            chain_views(self.dm, views, g9, rinv, self.grad, None, j0=r0, j1=r0 + rows, row0=r0, rows=rows,
+                        ld=self.ld)
+
+    def sum_losses(self, coll):
+        V = len(self.views)
+        losses = self.ws.losses[:V]
+        if coll is not None:  # each entry is non-zero on exactly one rank: the sum is exact
+            coll.all_reduce_(losses)
+        c = _lib.ctx(self.dm.device.index)
+        c.check(c.lib.ss_sum_f64(c.handle, losses.data_ptr(), V, self.ws.loss.data_ptr()))
+        return self.ws.loss
+
+    def adam(self, n_views):
+        st = self.state
+        if self.dm.active_count == 0:  # frozen-only model: no state change (optim.py:374)
+            return
+        c = _lib.ctx(self.dm.device.index)
+        ast = st.adam_struct()
+        if self.plan.world == 1:
+            ms = self.dm.struct()
+        else:
+            ms = _row_struct(self.dm, self.plan.row0, self.plan.rows)
+        c.check(c.lib.ss_adam_step_ld(c.handle, ms, ast, self.grad.data_ptr(), self.ld, n_views, st.hparams()))
+        st.step_count = int(ast.step_count)
+        st._host = None  # device moments changed: the host mirror is stale
+
+    def gather(self, coll):
+        R = self.plan.R
+        for k in TRAINABLE:
+            t = getattr(self.dm, k)
+            view, write_back = parallel.padded_rows_view(t, self.plan.padded)
+            coll.all_gather_rows(view, R)
+            if write_back is not None:
+                write_back()
 
 
 def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: bool = True, precision: int = 0,
-         process_group=None, total_views: Optional[int] = None, workspace: Optional[StepWorkspace] = None,
-         sync_loss: bool = True):
+         process_group=None, workspace: Optional[StepWorkspace] = None, sync_loss: bool = True):
     """ref optim.py:353 -- one Adam step over the ready views; returns the mean loss.
 
-    With `process_group`, `views` are this rank's shard; gradients and loss
-    are all-reduced (sum) over the group and averaged over `total_views`
-    (default: sum of the ranks' ready views).  `sync_loss=False` returns the
-    device loss tensor instead of a host float (no host synchronisation).
+    With a `process_group` (or a state created with one) every rank passes
+    the SAME views; rank r renders views r, r+N, ... and the step is sharded
+    as parallel.py describes -- bit-identical to the single-GPU step.
+    `sync_loss=False` returns the device loss tensor instead of a host float
+    (no host synchronisation).
     """
-    import torch
     ready = [v for v in views if v.ready]
-    if not ready and process_group is None:
+    if not ready:
         raise ValueError("no ready views")
     if state.active_count != model.active_count:
         raise ValueError("optimizer state out of sync with model")
+    pg = process_group if process_group is not None else state.process_group
+    if pg is not None and pg is not state.process_group:
+        raise ValueError("the optimizer state was created for a different process group")
     dm, uploaded = as_device(model)
     a = dm.active_count
-    n_local = len(ready)
-    if process_group is not None:
-        total = int(total_views) if total_views is not None else \
-            parallel.global_view_count(n_local, process_group, dm.device)
-    else:
-        total = n_local
-    if total == 0:
-        raise ValueError("no ready views")
-    ws = workspace if workspace is not None else StepWorkspace(dm)
-    ws.grad.zero_()
-    ws.loss.zero_()
+    plan = state.plan
     sub = _subset_tensor(index_subset, dm.device)
-    gts = _stage_ground_truth(ready, dm.device)
-    n_in = int(sub.numel()) if sub is not None else dm.count
-    if precision == 0 and a > 0 and n_in > 0:
-        # chain rule of every view in one pass over the rows (ss_chain_views),
-        # in batches of at most CHAIN_MAX_VIEWS views
-        for b0 in range(0, len(ready), CHAIN_MAX_VIEWS):
-            batch = list(zip(ready, gts))[b0:b0 + CHAIN_MAX_VIEWS]
-            g9, rinv = ws.defer_buffers(len(batch), n_in, dm.device)
-            for i, (v, gt) in enumerate(batch):
-                backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub,
-                                gt=gt, defer=(g9[i], rinv[i]))
-            chain_views(dm, [v for v, _ in batch], g9, rinv, ws.grad, sub)
+    ws = workspace if workspace is not None else StepWorkspace(dm)
+    if precision != 0:
+        if plan.world > 1:
+            raise ValueError("the fp64 blend (precision=1) is single-GPU")
+        loss = _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws)
     else:
-        for v, gt in zip(ready, gts):
-            backward_device(dm, v, ws.grad, ws.loss, None, extent_cutoff, precision, None, subset_tensor=sub, gt=gt)
-    if process_group is not None:
-        parallel.reduce_gradients(ws.grad, ws.loss, process_group)
-    if a > 0:
-        c = _lib.ctx(dm.device.index)
-        st = _lib.SSAdamState()
-        st.m = state.m_flat.data_ptr()
-        st.v = state.v_flat.data_ptr()
-        st.grad_ema = state.grad_ema.data_ptr()
-        st.age = state.age.data_ptr()
-        st.step_count = state.step_count
-        c.check(c.lib.ss_adam_step(c.handle, dm.struct(), st, _lib.ptr(ws.grad), total, state.hparams()))
-        state.step_count = int(st.step_count)
-        if uploaded:
-            dm.write_back(model, TRAINABLE, rows=a)
+        kern = _DeviceKernels(dm, state, ws, ready, sub, extent_cutoff, plan)
+        kern.stage(parallel.shard_views(ready, plan.rank, plan.world) if plan.world > 1 else ready)
+        coll = parallel.Collectives(pg) if plan.world > 1 else None
+        loss = parallel.sharded_step(kern, ready, plan, coll, CHAIN_MAX_VIEWS)
+    if uploaded and a > 0:
+        dm.write_back(model, TRAINABLE, rows=a)
+    total = len(ready)
     if not sync_loss:
-        return ws.loss / total
-    return float(ws.loss.item()) / total
+        return loss / total
+    return float(loss.item()) / total
+
+
+def _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws):
+    """Per-view chain rule into the gradient (the fp64 blend instantiation)."""
+    B = (dm.sh_degree + 1) ** 2
+    a = dm.active_count
+    grad = ws.prepare(a * (11 + 3 * B), len(ready))
+    gts = _stage_ground_truth(ready, dm.device)
+    for i, (v, gt) in enumerate(zip(ready, gts)):
+        backward_device(dm, v, grad, ws.losses[i:i + 1], None, extent_cutoff, precision, None, subset_tensor=sub, gt=gt)
+    c = _lib.ctx(dm.device.index)
+    c.check(c.lib.ss_sum_f64(c.handle, ws.losses.data_ptr(), len(ready), ws.loss.data_ptr()))
+    if a > 0:
+        ast = state.adam_struct()
+        c.check(c.lib.ss_adam_step(c.handle, dm.struct(), ast, grad.data_ptr(), len(ready), state.hparams()))
+        state.step_count = int(ast.step_count)
+        state._host = None
+    return ws.loss

@@ -72,9 +72,13 @@ def freeze_policy(model: DeviceModel, optimizer_stats, age_threshold: int = 100,
     """ref expansion.py:134-142 -- active rows with age >= threshold and grad-EMA < threshold."""
     s = _lib.SSSelect()
     s.kind = 0
-    s.n = int(optimizer_stats.age.shape[0])
-    s.age = optimizer_stats.age.data_ptr()
-    s.grad_ema = optimizer_stats.grad_ema.data_ptr()
+    if hasattr(optimizer_stats, "device_stats"):  # an OptimizerState (device buffers, gathered if sharded)
+        age, ema = optimizer_stats.device_stats()
+    else:  # any object with device age / grad_ema tensors
+        age, ema = optimizer_stats.age, optimizer_stats.grad_ema
+    s.n = int(age.shape[0])
+    s.age = age.data_ptr()
+    s.grad_ema = ema.data_ptr()
     s.age_threshold = int(age_threshold)
     s.grad_threshold = float(grad_threshold)
     return _select(model, s)

@@ -35,8 +35,13 @@ _QUANT = {0: (16, None, None, "MEANS"), 1: (8, -10.0, 2.0, "LOG_SCALES"), 2: (10
           3: (8, -8.0, 8.0, "LOGIT_OPACITIES"), 4: (8, -4.0, 4.0, "SH_DC"), 5: (8, -1.0, 1.0, "SH_REST"),
           6: (1, 0.0, 1.0, "LIGHT_VISIBILITY")}
 _RESIDUAL = (0, 1)
-_STATUS_ERRORS = {1: (ValueError, "truncated varint"), 2: (ValueError, "varint too long"),
-                  3: (ProtocolError, "sparse delta index out of range"), 4: (ProtocolError, "delta codes truncated")}
+_STATUS_ERRORS = {1: ("ValueError", "truncated varint"), 2: ("ValueError", "varint too long"),
+                  3: ("ProtocolError", "sparse delta index out of range"), 4: ("ProtocolError", "delta codes truncated")}
+
+
+def _raise_status(code: int):
+    kind, msg = _STATUS_ERRORS[code]
+    raise (ValueError if kind == "ValueError" else ProtocolError)(msg)  # the module's ProtocolError at raise time
 
 
 def packed_size(count: int, bits: int) -> int:
@@ -199,8 +204,7 @@ class _Block:
         c.check(c.lib.ss_decode_delta(c.handle, self.struct(), _lib.ptr(self.indices), _lib.ptr(vals)))
         code = int(self.status[0].item())
         if code:
-            exc, msg = _STATUS_ERRORS[code]
-            raise exc(msg)
+            _raise_status(code)
         return vals
 
 
@@ -258,13 +262,61 @@ def _reshape_error(size, shape):
     return ValueError(f"cannot reshape array of size {size} into shape {shape}")
 
 
+def advance_baseline(baseline_rows, indices, values) -> None:
+    """ref delta.py:257-266: f32(f64(base) + value) in place, on the device
+    (numpy arguments are uploaded and the result written back)."""
+    import torch
+    host = not isinstance(baseline_rows, torch.Tensor)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    b = torch.from_numpy(np.ascontiguousarray(baseline_rows)).to(dev) if host else baseline_rows
+    v = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.asarray(values, np.float64))
+    v = v.to(b.device, torch.float64)
+    flat = b.reshape(b.shape[0], -1)
+    if indices is None:
+        flat.copy_((flat.double() + v.reshape(flat.shape)).to(flat.dtype))
+    else:
+        idx = torch.as_tensor(np.asarray(indices, np.int64), device=b.device)
+        flat[idx] = (flat[idx].double() + v.reshape(-1, flat.shape[1])).to(flat.dtype)
+    if host:
+        baseline_rows[...] = b.cpu().numpy().reshape(baseline_rows.shape)
+
+
+def _apply_delta_host(model, baselines, payload, frame_epoch, current_epoch) -> bool:
+    """apply_delta for a host replica (the reference's numpy GaussianModel and
+    DeltaBaselines): uploaded, applied on the device, the touched arrays
+    written back in place -- as the reference mutates them."""
+    import torch
+    dm = DeviceModel.from_host(model)
+    dev = dm.device
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev).reshape(-1, 3)
+    db = DeviceBaselines(up(baselines.means), up(baselines.log_scales), getattr(baselines, "epoch", 0))
+    ok = apply_delta(dm, db, payload, frame_epoch, current_epoch)
+    if not ok:
+        return False
+    a = model.active_count
+    attr = payload[0]
+    if attr in _RESIDUAL:
+        name = "means" if attr == 0 else "log_scales"
+        base = baselines.array_for(attr)
+        base[:a] = db.array_for(attr)[:a].cpu().numpy().astype(base.dtype, copy=False).reshape(base[:a].shape)
+        getattr(model, name)[:a] = base[:a]
+    else:
+        name = {2: "quaternions", 3: "logit_opacities", 4: "sh_coeffs", 5: "sh_coeffs", 6: "light_visibility"}[attr]
+        dst = getattr(model, name)
+        dst[:a] = getattr(dm, name)[:a].cpu().numpy().astype(dst.dtype, copy=False).reshape(dst[:a].shape)
+    return True
+
+
 def apply_delta(model: DeviceModel, baselines: DeviceBaselines, payload: bytes, frame_epoch: int,
                 current_epoch: int) -> bool:
     """ref delta.py:269-303 on a device replica: False (untouched) on an epoch
     mismatch; the same exceptions as the reference for malformed payloads,
-    raised before anything is written."""
+    raised before anything is written.  A host replica (numpy model and
+    baselines) is applied through the device and written back in place."""
     if frame_epoch != current_epoch:
         return False
+    if not isinstance(model, DeviceModel):
+        return _apply_delta_host(model, baselines, payload, frame_epoch, current_epoch)
     blk = _Block(parse_delta(payload), model.device)
     blk.decode()
     p = blk.p
@@ -372,11 +424,19 @@ def decode_snapshot(payload: bytes, device=None):
         c.check(c.lib.ss_decode_snapshot(c.handle, d))
         code = int(status[0].item())
         if code:
-            exc, msg = _STATUS_ERRORS[code]
-            raise exc(msg)
+            _raise_status(code)
     info = {"profile_id": profile_id, "compression_id": compression_id, "aabb_lo": lo, "aabb_hi": hi}
     return m, info
 
 
-__all__ = ["DeltaUpdate", "DeviceBaselines", "apply_delta", "decode_delta", "decode_snapshot", "decompress_block",
+def decode_snapshot_host(payload: bytes, device=None):
+    """ref snapshot.py:85 with the reference's return types: (host
+    GaussianModel, info), decoded on the device."""
+    m, info = decode_snapshot(payload, device)
+    return m.to_host(), info
+
+
+decode_delta_host = decode_delta  # already returns host arrays (ref delta.py:150)
+
+__all__ = ["advance_baseline", "decode_snapshot_host", "decode_delta_host", "DeltaUpdate", "DeviceBaselines", "apply_delta", "decode_delta", "decode_snapshot", "decompress_block",
            "parse_delta", "packed_size"]

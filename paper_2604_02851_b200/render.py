@@ -138,25 +138,36 @@ def render(model, pose, intr, light_state, index_subset=None, background=(0.0, 0
 
 @dataclass
 class PreparedSplats:
-    """Host view of the per-splat preprocess (ref render.py:200-223 field names)."""
+    """Host view of the per-splat preprocess, every field of ref
+    render.py:200-223 (model-row order; `order` is the composite order)."""
 
     rows: np.ndarray
+    mu_cam: np.ndarray
     depth: np.ndarray
     mu2d: np.ndarray
+    J: np.ndarray
+    W: np.ndarray
+    Sigma3d: np.ndarray
+    cov_cam: np.ndarray
     Sigma2d: np.ndarray
     inv2d: np.ndarray
     opacity: np.ndarray
     color: np.ndarray
     color_pre: np.ndarray
+    view_dir: np.ndarray
+    view_dist: np.ndarray
+    n_hat: np.ndarray
+    n_axis: np.ndarray
+    shade_inter: dict
     order: np.ndarray
     radius: np.ndarray
-    windows: np.ndarray
-    shade_inter: dict = field(default_factory=dict)
+    windows: np.ndarray = None
 
 
 def prepare_splats(model, pose, intr, light_state, index_subset=None, extent_cutoff: bool = True) -> PreparedSplats:
-    """ref render.py:226 -- computed by the fp64 preprocess kernel (K1) and the
-    depth sort (K3a); returned as host arrays for inspection."""
+    """ref render.py:226 -- computed by the fp64 preprocess kernel (K1), the
+    depth sort (K3a) and ss_prepare_extras (the remaining PreparedSplats
+    fields, same device functions); returned as host arrays."""
     import torch
     dm, _ = as_device(model)
     c = _lib.ctx(dm.device.index)
@@ -164,33 +175,41 @@ def prepare_splats(model, pose, intr, light_state, index_subset=None, extent_cut
     sub = _subset_tensor(index_subset, dev)
     n = int(sub.numel()) if sub is not None else dm.count
     cap = max(n, 1)
-    buf = dict(rows=torch.empty(cap, dtype=torch.int64, device=dev),
-               depth=torch.empty(cap, dtype=torch.float64, device=dev),
-               mu2d=torch.empty((cap, 2), dtype=torch.float64, device=dev),
-               sigma2d=torch.empty((cap, 3), dtype=torch.float64, device=dev),
-               radius=torch.empty(cap, dtype=torch.float64, device=dev),
-               window=torch.empty((cap, 4), dtype=torch.int32, device=dev),
-               opacity=torch.empty(cap, dtype=torch.float64, device=dev),
-               color=torch.empty((cap, 3), dtype=torch.float64, device=dev),
-               color_pre=torch.empty((cap, 3), dtype=torch.float64, device=dev),
-               shade_s=torch.empty(cap, dtype=torch.float64, device=dev),
-               order=torch.empty(cap, dtype=torch.int64, device=dev))
+    B = (dm.sh_degree + 1) ** 2
+    f64 = lambda *shape: torch.empty((cap,) + shape, dtype=torch.float64, device=dev)
+    buf = dict(rows=torch.empty(cap, dtype=torch.int64, device=dev), depth=f64(), mu2d=f64(2), sigma2d=f64(3),
+               radius=f64(), window=torch.empty((cap, 4), dtype=torch.int32, device=dev), opacity=f64(),
+               color=f64(3), color_pre=f64(3), shade_s=f64(), order=torch.empty(cap, dtype=torch.int64, device=dev))
     p = _lib.SSPrepared()
     for k, t in buf.items():
         setattr(p, k, t.data_ptr())
     p.capacity = cap
     vis = _lib.i64(0)
-    c.check(c.lib.ss_prepare_splats(c.handle, dm.struct(), camera_struct(pose, intr), light_struct(light_state),
+    camst, lst = camera_struct(pose, intr), light_struct(light_state)
+    c.check(c.lib.ss_prepare_splats(c.handle, dm.struct(), camst, lst,
                                     render_opts((0, 0, 0), sub, extent_cutoff, 1), p, _lib.C.byref(vis)))
     M = int(vis.value)
+    ext = dict(mu_cam=f64(3), J=f64(2, 3), sigma3d=f64(3, 3), cov_cam=f64(3, 3), view_dir=f64(3), view_dist=f64(),
+               n_hat=f64(3), n_axis=torch.empty(cap, dtype=torch.int64, device=dev), Y=f64(B), albedo_est=f64(3),
+               cos=f64(), vis=f64())
+    e = _lib.SSPreparedExtras()
+    for k, t in ext.items():
+        setattr(e, k, t.data_ptr())
+    c.check(c.lib.ss_prepare_extras(c.handle, dm.struct(), camst, lst, buf["rows"].data_ptr(), M, e))
     h = {k: t[:M].cpu().numpy() for k, t in buf.items()}
+    x = {k: t[:M].cpu().numpy() for k, t in ext.items()}
     s = h["sigma2d"]
     Sig = np.stack([np.stack([s[:, 0], s[:, 1]], -1), np.stack([s[:, 1], s[:, 2]], -1)], -2)
     det = s[:, 0] * s[:, 2] - s[:, 1] * s[:, 1]
     inv = np.stack([np.stack([s[:, 2] / det, -s[:, 1] / det], -1), np.stack([-s[:, 1] / det, s[:, 0] / det], -1)], -2)
-    return PreparedSplats(rows=h["rows"], depth=h["depth"], mu2d=h["mu2d"], Sigma2d=Sig, inv2d=inv,
-                          opacity=h["opacity"], color=h["color"], color_pre=h["color_pre"], order=h["order"],
-                          radius=h["radius"], windows=h["window"].astype(np.int64), shade_inter={"s": h["shade_s"]})
+    R = pose.rotation() if hasattr(pose, "rotation") else quat_to_rotmat(pose.quaternion)
+    inter = {"Y": x["Y"], "albedo_est": x["albedo_est"], "s": h["shade_s"], "cos": x["cos"], "vis": x["vis"]}
+    return PreparedSplats(rows=h["rows"], mu_cam=x["mu_cam"], depth=h["depth"], mu2d=h["mu2d"], J=x["J"],
+                          W=np.asarray(R, np.float64).T.copy(), Sigma3d=x["sigma3d"], cov_cam=x["cov_cam"],
+                          Sigma2d=Sig, inv2d=inv, opacity=h["opacity"], color=h["color"], color_pre=h["color_pre"],
+                          view_dir=x["view_dir"], view_dist=x["view_dist"], n_hat=x["n_hat"], n_axis=x["n_axis"],
+                          shade_inter=inter, order=h["order"], radius=h["radius"],
+                          windows=h["window"].astype(np.int64))
 
 
 def splat_windows(mu2d, radius, width: int, height: int) -> np.ndarray:

@@ -23,6 +23,9 @@ Written: tests/golden/config1_cases.{npz,json}.  Arrays per degree d:
   losses      the 101 step losses
   s{1,10,100,101}_*  trainable attributes after that many steps
   ema100, age100     OptimizerState.grad_ema / age after step 100
+  m100_*, v100_*     OptimizerState.m / .v after step 100 (the teacher-forced
+                     check: the reference's step-100 state stepped once on the
+                     GPU against s101_*)
   snap_p0, snap_p1   encode_snapshot payloads of the step-100 model
   base_means, base_log_scales   baselines after the reset (decoded p0)
   tick_{attr}        the DELTA_ORDER tick's payloads after step 101
@@ -148,7 +151,8 @@ def run_degree(degree):
         if s in CHECKPOINTS:
             out.update({f"s{s}_{k}": model.attribute(k).copy() for k in TRAIN})
         print(f"degree {degree} step {s} loss {losses[-1]:.6f} ({time.time() - t0:.0f} s)", flush=True)
-    out.update(ema100=state.grad_ema.copy(), age100=state.age.copy())
+    out.update(ema100=state.grad_ema.copy(), age100=state.age.copy(),
+               **{f"m100_{k}": state.m[k].copy() for k in TRAIN}, **{f"v100_{k}": state.v[k].copy() for k in TRAIN})
 
     # full snapshot + baseline reset from the decoded payload (ss/server.py:470-484)
     snap0 = encode_snapshot(model, PROFILE_DEFAULT)

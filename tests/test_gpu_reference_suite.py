@@ -1,0 +1,68 @@
+"""The reference's own hot-path test suites, unmodified, against the drop-in.
+
+tests/refsuite/prepare.py stages pkg/tests/{test_render, test_optim,
+test_protocol, test_golden}.py of the reference (with its golden-packet
+script and the regenerated wire fixtures) in baseline/_ref_tests/, next to
+the reference package installed in baseline/_ref, and
+tests/refsuite/alias_conftest.py replaces the reference's render / optim /
+protocol entry points by this package's (fp64 blend instantiation, SURVEY
+§4 reuse plan).  This test runs that suite in a subprocess on the GPU and
+requires every test to pass except the exclusions listed below, each with
+its reason.
+"""
+
+import os
+import pathlib
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+
+import pytest
+
+from gpu_util import require_gpu
+
+pytestmark = pytest.mark.gpu
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+SUITE = ROOT / "baseline" / "_ref_tests"
+REF_PKG = ROOT / "baseline" / "_ref"
+
+# node id -> why it cannot pass against this drop-in
+_FD = ("the finite-difference gradcheck perturbs FLOAT64 model arrays by h = 1e-4 (pkg/tests/test_optim.py:54-79, "
+       "111-135); the drop-in's Gaussian store is float32 in HBM, so a coordinate near z = 4 moves by "
+       "f32(z + h) - f32(z - h) = 2h +- 1 ulp (2.4e-7): the finite difference itself is off by up to 2.4e-3 "
+       "relative, above the test's 1e-3 bound, while the analytic gradient is within 1e-10 of the reference's "
+       "(tests/test_gpu_raster.py)")
+EXCLUDED = {f"tests.test_optim::test_backward_matches_finite_differences[{s}]": _FD
+            for s in ("0-flat", "1-none", "2-sh1", "3-flat", "4-none", "5-sh1")}
+EXCLUDED["tests.test_optim::test_degree_three_sh_gradients"] = _FD
+
+
+def test_reference_suites_against_drop_in(tmp_path):
+    require_gpu()
+    if not (SUITE / "tests" / "conftest.py").exists() or not (REF_PKG / "splatstream").exists():
+        pytest.skip("reference suite not staged (python tests/refsuite/prepare.py; pip install --target baseline/_ref)")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(REF_PKG), str(ROOT)] + [p for p in env.get("PYTHONPATH", "").split(os.pathsep) if p])
+    env["SS_REPO_ROOT"] = str(ROOT)
+    xml = tmp_path / "ref.xml"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "--rootdir", str(SUITE),
+                        f"--junitxml={xml}", str(SUITE / "tests")], cwd=str(SUITE), env=env, capture_output=True,
+                       text=True, timeout=3000)
+    assert xml.exists(), r.stdout[-3000:] + r.stderr[-3000:]
+    failed, passed = {}, []
+    for case in ET.parse(xml).getroot().iter("testcase"):
+        node = f"{case.get('classname')}::{case.get('name')}"
+        bad = [e for e in case if e.tag in ("failure", "error")]
+        if bad:
+            failed[node] = (bad[0].get("message") or "")[:300]
+        elif not [e for e in case if e.tag == "skipped"]:
+            passed.append(node)
+    out = ROOT / "gpurun_out"
+    if out.is_dir():
+        import json
+        (out / "ref_suite.json").write_text(json.dumps({"passed": passed, "failed": failed}, indent=1))
+    unexpected = {k: v for k, v in failed.items() if k not in EXCLUDED}
+    print(f"reference suites: {len(passed)} passed, {len(failed)} failed ({len(failed) - len(unexpected)} excluded)")
+    assert not unexpected, "\n".join(f"{k}: {v}" for k, v in unexpected.items())
+    assert len(passed) >= 90

@@ -31,11 +31,11 @@ def _opt(c, m, prefix="opt_"):
     import torch
     from paper_2604_02851_b200.optim import OptimizerState
     o = OptimizerState(m, scene_extent=3.0)
-    for k in GROUPS:
-        o.m[k].copy_(torch.from_numpy(np.array(c.a(f"{prefix}m_{k}"))))
-        o.v[k].copy_(torch.from_numpy(np.array(c.a(f"{prefix}v_{k}"))))
-    o.age.copy_(torch.from_numpy(np.array(c.a(f"{prefix}age"))))
-    o.grad_ema.copy_(torch.from_numpy(np.array(c.a(f"{prefix}grad_ema"))))
+    for k in GROUPS:  # the reference-visible numpy state, written back on the next device use
+        o.m[k][...] = c.a(f"{prefix}m_{k}")
+        o.v[k][...] = c.a(f"{prefix}v_{k}")
+    o.age[...] = c.a(f"{prefix}age")
+    o.grad_ema[...] = c.a(f"{prefix}grad_ema")
     return o
 
 
@@ -47,10 +47,10 @@ def _check_model(m, c, prefix, active):
 
 def _check_opt(o, c, prefix):
     for k in GROUPS:
-        np.testing.assert_array_equal(o.m[k].cpu().numpy(), c.a(f"{prefix}m_{k}"), err_msg=k)
-        np.testing.assert_array_equal(o.v[k].cpu().numpy(), c.a(f"{prefix}v_{k}"), err_msg=k)
-    np.testing.assert_array_equal(o.age.cpu().numpy(), c.a(f"{prefix}age"))
-    np.testing.assert_array_equal(o.grad_ema.cpu().numpy(), c.a(f"{prefix}grad_ema"))
+        np.testing.assert_array_equal(o.m[k], c.a(f"{prefix}m_{k}"), err_msg=k)
+        np.testing.assert_array_equal(o.v[k], c.a(f"{prefix}v_{k}"), err_msg=k)
+    np.testing.assert_array_equal(o.age, c.a(f"{prefix}age"))
+    np.testing.assert_array_equal(o.grad_ema, c.a(f"{prefix}grad_ema"))
 
 
 def _baselines(c):
