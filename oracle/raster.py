@@ -333,18 +333,32 @@ def _alpha(prep, i, x0, x1, y0, y1):
     return np.minimum(prep["opacity"][i] * G, ALPHA_CAP), G, dx, dy
 
 
-def composite(prep, W, H, bg):
+def _clip(rect, crop):
+    """The window [x0,x1)x[y0,y1) restricted to crop (cx0, cx1, cy0, cy1): (absolute
+    x0, x1, y0, y1, and the same relative to the crop origin)."""
+    x0, x1, y0, y1 = rect
+    cx0, cx1, cy0, cy1 = crop
+    x0, x1, y0, y1 = max(x0, cx0), min(x1, cx1), max(y0, cy0), min(y1, cy1)
+    return (x0, x1, y0, y1), (x0 - cx0, x1 - cx0, y0 - cy0, y1 - cy0)
+
+
+def composite(prep, W, H, bg, crop=None):
     """Front-to-back compositing in depth order (ref render.py:317-336).
     Returns (image (H,W,3), T (H,W), pairs) where pairs counts the
-    (pixel, splat) evaluations that passed the T-gate."""
-    img = np.zeros((H, W, 3))
-    T = np.ones((H, W))
+    (pixel, splat) evaluations that passed the T-gate.  With crop =
+    (x0, x1, y0, y1) only those pixels of the (W, H) frame are composited
+    (per-pixel results identical to the full frame's: every splat whose
+    window meets the crop is walked, in the same order)."""
+    crop = (0, W, 0, H) if crop is None else tuple(int(v) for v in crop)
+    h, w_ = crop[3] - crop[2], crop[1] - crop[0]
+    img = np.zeros((h, w_, 3))
+    T = np.ones((h, w_))
     pairs = 0
     for i in prep["order"]:
-        x0, x1, y0, y1 = prep["rect"][i]
+        (x0, x1, y0, y1), (a0, a1, b0, b1) = _clip(prep["rect"][i], crop)
         if x0 >= x1 or y0 >= y1:
             continue
-        Tw = T[y0:y1, x0:x1]
+        Tw = T[b0:b1, a0:a1]
         live = Tw >= T_CUTOFF
         n_live = int(live.sum())
         if n_live == 0:
@@ -352,38 +366,42 @@ def composite(prep, W, H, bg):
         pairs += n_live
         a, _, _, _ = _alpha(prep, i, x0, x1, y0, y1)
         w = np.where(live, a * Tw, 0.0)
-        img[y0:y1, x0:x1] += w[..., None] * prep["color"][i]
-        T[y0:y1, x0:x1] = np.where(live, Tw * (1.0 - a), Tw)
+        img[b0:b1, a0:a1] += w[..., None] * prep["color"][i]
+        T[b0:b1, a0:a1] = np.where(live, Tw * (1.0 - a), Tw)
     img += T[..., None] * np.asarray(bg, np.float64)
     return img, T, pairs
 
 
-def screen_grads(prep, image, gt, W, H):
+def screen_grads(prep, image, gt, W, H, crop=None):
     """The per-splat front-to-back walk of ref optim.py:133-172.
-    Returns (g_color (M,3), g_opacity (M,), g_mu2d (M,2), g_sig (M,3) = [00,01,11])."""
+    Returns (g_color (M,3), g_opacity (M,), g_mu2d (M,2), g_sig (M,3) = [00,01,11]).
+    With crop, image / gt are the crop's pixels of the (W, H) frame and the
+    sums run over them only (complete for splats whose window lies inside the
+    crop); dL/dC keeps the full frame's normalisation 1/(H*W*3)."""
+    crop = (0, W, 0, H) if crop is None else tuple(int(v) for v in crop)
     M = prep["rows"].size
-    dLdC = np.sign(image - gt) / image.size
+    dLdC = np.sign(image - gt) / (H * W * 3)
     gc = np.zeros((M, 3))
     go = np.zeros(M)
     gm = np.zeros((M, 2))
     gs = np.zeros((M, 3))
-    T = np.ones((H, W))
-    prefix = np.zeros((H, W, 3))
+    T = np.ones(image.shape[:2])
+    prefix = np.zeros(image.shape)
     for i in prep["order"]:
-        x0, x1, y0, y1 = prep["rect"][i]
+        (x0, x1, y0, y1), (a0, a1, b0, b1) = _clip(prep["rect"][i], crop)
         if x0 >= x1 or y0 >= y1:
             continue
-        Tw = T[y0:y1, x0:x1]
+        Tw = T[b0:b1, a0:a1]
         live = Tw >= T_CUTOFF
         if not live.any():
             continue
         a, G, dx, dy = _alpha(prep, i, x0, x1, y0, y1)
         open_ = prep["opacity"][i] * G < ALPHA_CAP
         w = np.where(live, a * Tw, 0.0)
-        g = dLdC[y0:y1, x0:x1]
+        g = dLdC[b0:b1, a0:a1]
         col = prep["color"][i]
         gc[i] = (g * w[..., None]).sum(axis=(0, 1))
-        S = image[y0:y1, x0:x1] - prefix[y0:y1, x0:x1] - w[..., None] * col
+        S = image[b0:b1, a0:a1] - prefix[b0:b1, a0:a1] - w[..., None] * col
         da = (g * (col[None, None, :] * Tw[..., None] - S / (1.0 - a)[..., None])).sum(-1)
         da = np.where(live, da, 0.0)
         go[i] = (da * np.where(open_, G, 0.0)).sum()
@@ -393,8 +411,8 @@ def screen_grads(prep, image, gt, W, H):
         ay = A[1, 0] * dx + A[1, 1] * dy
         gm[i] = [(gp * ax).sum(), (gp * ay).sum()]
         gs[i] = [0.5 * (gp * ax * ax).sum(), 0.5 * (gp * ax * ay).sum(), 0.5 * (gp * ay * ay).sum()]
-        prefix[y0:y1, x0:x1] += w[..., None] * col
-        T[y0:y1, x0:x1] = np.where(live, Tw * (1.0 - a), Tw)
+        prefix[b0:b1, a0:a1] += w[..., None] * col
+        T[b0:b1, a0:a1] = np.where(live, Tw * (1.0 - a), Tw)
     return gc, go, gm, gs
 
 

@@ -21,9 +21,32 @@ struct AdamConst {
 };
 
 // parameter pointer and learning rate of flat element e (ss_grad_layout with
-// `a` = ld rows per group); NULL for an element of a padding row (>= c.a)
+// `a` = ld rows per group); with PADDED, NULL for an element of a padding
+// row (>= c.a) -- the sharded step's last shards
+template <bool PADDED>
 __device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float* means, float* ls, float* quats,
                                              float* logits, float* sh, const AdamConst& c, double& lr) {
+    if (!PADDED) {
+        if (e < 3 * a) {
+            lr = c.lr[0];
+            return means + e;
+        }
+        if (e < 6 * a) {
+            lr = c.lr[1];
+            return ls + (e - 3 * a);
+        }
+        if (e < 10 * a) {
+            lr = c.lr[2];
+            return quats + (e - 6 * a);
+        }
+        if (e < 11 * a) {
+            lr = c.lr[3];
+            return logits + (e - 10 * a);
+        }
+        const int64_t k = e - 11 * a;
+        lr = (k % B) == 0 ? c.lr[4] : c.lr[5];
+        return sh + k;
+    }
     int64_t k, w;
     float* p;
     if (e < 3 * a) {
@@ -38,8 +61,7 @@ __device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float*
         k = e - 11 * a, w = 3 * B, p = sh;
         lr = (k % B) == 0 ? c.lr[4] : c.lr[5];
     }
-    if (a != c.a && k >= c.a * w) return nullptr;
-    return p + k;
+    return k >= c.a * w ? nullptr : p + k;
 }
 
 #ifndef ADAM_U
@@ -47,6 +69,7 @@ __device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float*
 #endif
 // ADAM_U elements per thread per grid-stride step; every load (gradient,
 // moments, parameter) is issued before the fp64 update math
+template <bool PADDED>
 __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float* __restrict__ quats,
                        float* __restrict__ logits, float* __restrict__ sh, double* __restrict__ m,
                        double* __restrict__ v, const float* __restrict__ g, AdamConst c) {
@@ -60,7 +83,7 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t e = e0 + u * stride;
-            p[u] = e < total ? adam_param(e, a, c.B, means, ls, quats, logits, sh, c, lr[u]) : nullptr;
+            p[u] = e < total ? adam_param<PADDED>(e, a, c.B, means, ls, quats, logits, sh, c, lr[u]) : nullptr;
             if (p[u]) {
                 gv[u] = g[e];
                 mv[u] = m[e];
@@ -142,8 +165,12 @@ extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, 
     int64_t grid = (total + 255) / 256;
     if (grid > (int64_t)ctx->num_sms * 32) grid = (int64_t)ctx->num_sms * 32;
     ss_tic(ctx, KC_ADAM);
-    SS_CUDA(ctx, ss_launch((k_adam), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales, model->quaternions,
-                                                model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c));
+    if (ld == a)
+        SS_CUDA(ctx, ss_launch((k_adam<false>), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales,
+                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c));
+    else
+        SS_CUDA(ctx, ss_launch((k_adam<true>), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales,
+                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c));
     SS_CHECK_LAUNCH(ctx);
     int64_t rg = (a + 255) / 256;
     if (rg > (int64_t)ctx->num_sms * 32) rg = (int64_t)ctx->num_sms * 32;
