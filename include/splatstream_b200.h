@@ -216,6 +216,10 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* model, const ss_camera* cam, 
  * direction / distance, normal proxy and its axis, and the shading
  * intermediates of ref render.py:196 (Y, albedo_est, cos, vis; s is in
  * ss_prepared).  Computed by the same device functions as K1. */
+/* Diagnostics builds (-DSS_BWD_STATS) only: utilisation counters of the
+ * backward blend walk (see ss_raster.cu); SS_ERR_INVALID otherwise. */
+int ss_debug_bwd_stats(ss_ctx* ctx, unsigned long long out[8], int reset);
+
 typedef struct {
     double* mu_cam;      /* (M,3)   */
     double* J;           /* (M,2,3) */

@@ -604,6 +604,13 @@ __device__ __forceinline__ uint32_t pair_index(const uint64_t* roff, const int w
     return (uint32_t)(roff[r] + (uint64_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0)));
 }
 
+#ifdef SS_BWD_STATS
+// utilisation counters of the backward walk (diagnostics build only):
+// [0] pairs in the lists, [1] pairs walked, [2] walked pairs with an active
+// pixel, [3] active (pixel, splat) pairs, [4] lanes entering the body,
+// [5] pixel slots computed (executed row groups x QG x body lanes)
+__device__ unsigned long long g_bwd_stats[8];
+#endif
 template <typename R>
 __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restrict__ ranges,
                                                         const uint32_t* __restrict__ pvals,
@@ -659,6 +666,9 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
         }
     }
     Staged<R>* my = sm[warp];
+#ifdef SS_BWD_STATS
+    unsigned long long st[6] = {rg.y - rg.x, stop - rg.x, 0, 0, 0, 0};
+#endif
     for (uint32_t b0 = rg.x; b0 < stop; b0 += 32) {
         const uint32_t i = b0 + lane;
         if (i < stop) {
@@ -675,6 +685,18 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
             R acc[9];
 #pragma unroll
             for (int e = 0; e < 9; ++e) acc[e] = 0;
+#ifdef SS_BWD_STATS
+            {
+                const unsigned body = __ballot_sync(0xffffffffu, act != 0);
+                const unsigned wa = __reduce_or_sync(0xffffffffu, act);
+                int groups = 0;
+                for (int g = 0; g < PPT; g += QG_BWD) groups += ((wa >> g) & ((1u << QG_BWD) - 1u)) ? 1 : 0;
+                st[2] += body ? 1 : 0;
+                st[3] += __reduce_add_sync(0xffffffffu, __popc(act));
+                st[4] += __popc(body);
+                st[5] += (unsigned long long)groups * QG_BWD * __popc(body);
+            }
+#endif
             if (act) {
                 // branch-free over the lane's 8 pixels: inactive ones get
                 // G = 0, which zeroes every contribution and leaves T, R alone
@@ -740,6 +762,10 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
     }
     loss = warp_sum<double>(loss);
     if (lane == 0) tile_loss[tile] = loss;
+#ifdef SS_BWD_STATS
+    if (lane == 0)
+        for (int k = 0; k < 6; ++k) atomicAdd(&g_bwd_stats[k], st[k]);
+#endif
 }
 
 // ---------------------------------------------------------------- K5, float32 with paired rows
@@ -845,6 +871,153 @@ __global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restr
             if (Tout) Tout[p] = t;
         }
     }
+}
+
+// ---------------------------------------------------------------- K6, float32 with paired rows
+// The float32 backward walks a lane's 8 pixels as 4 row pairs (rows
+// ly0 + 4g and ly0 + 4g + 2), the pair's two independent chains in one
+// packed FFMA2 / FMUL2 / FADD2 each: per pixel the arithmetic of
+// k_blend_bwd<float> (same operations in the same order per component, so
+// T, R and every per-pixel term are bit-identical), with the 9 per-splat
+// sums kept per row-pair component and folded before the warp reduction.
+#ifndef SS_BWD2_MINB
+#define SS_BWD2_MINB 8
+#endif
+__global__ void __launch_bounds__(32 * WPB_BWD, SS_BWD2_MINB) k_blend_bwd2(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ pvals, const double2* __restrict__ mu,
+    const SplatRec<float>* __restrict__ rec_, const uint64_t* __restrict__ roffj, const uint32_t* __restrict__ tile_stop,
+    int W, int H, int tiles_x, int n_tiles, const float* __restrict__ img, const float* __restrict__ gt, double npx3,
+    float* __restrict__ partials, double* __restrict__ tile_loss, const uint32_t* __restrict__ order) {
+    SS_PDL_WAIT();
+    __shared__ Staged<float> sm[WPB_BWD][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = blockIdx.x * WPB_BWD + warp;
+    if (slot >= n_tiles) return;
+    const int tile = order ? (int)order[slot] : slot;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int X0 = tx * TILE, Y0 = ty * TILE;
+    const int lx = lane & 15, ly0 = lane >> 4;
+    const float pxc = lane_centre<float>(lx, X0), pyc = lane_centre<float>(ly0, Y0);
+    const uint2 rg = ranges[tile];
+    const uint32_t stop = rg.x + (tile_stop ? min(tile_stop[tile], rg.y - rg.x) : (rg.y - rg.x));
+
+    float2 T[PPT / 2], Rr[PPT / 2], g0[PPT / 2], g1[PPT / 2], g2[PPT / 2];
+    unsigned alive = 0;
+    double loss = 0.0;
+    const float inv = (float)(1.0 / npx3);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        const int px = X0 + lx, py = Y0 + ly0 + 2 * q;
+        float t = 1.f, r = 0.f, gg[3] = {0.f, 0.f, 0.f};
+        if (px < W && py < H) {
+            alive |= 1u << q;
+            const int64_t p = (int64_t)py * W + px;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float v = img[3 * p + c];
+                const float diff = v - gt[3 * p + c];
+                loss += fabs((double)diff);
+                const float sg = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+                gg[c] = sg * inv;  // dL/dC = sign(C - gt) / (H W 3)  (optim.py:124-125)
+                r += gg[c] * v;
+            }
+        }
+        comp(T[q >> 1], q & 1) = t;
+        comp(Rr[q >> 1], q & 1) = r;
+        comp(g0[q >> 1], q & 1) = gg[0];
+        comp(g1[q >> 1], q & 1) = gg[1];
+        comp(g2[q >> 1], q & 1) = gg[2];
+    }
+    Staged<float>* my = sm[warp];
+    const float2 cap = f2((float)ALPHA_CAP), one = f2(1.f);
+    for (uint32_t b0 = rg.x; b0 < stop; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        if (i < stop) {
+            const uint32_t j = pvals[i];
+            const SplatRec<float> rec = rec_[j];
+            stage(my[lane], mu[j], rec, X0, Y0);
+            my[lane].p = (int)pair_index(roffj, rec.win, j, tx, ty);
+        }
+        __syncwarp();
+        const int nb = (int)min(32u, stop - b0);
+        for (int k = 0; k < nb; ++k) {
+            const Staged<float> s = my[k];
+            const unsigned act = lane_mask(s, lx, ly0) & alive;
+            float2 acc[9];
+#pragma unroll
+            for (int e = 0; e < 9; ++e) acc[e] = f2(0.f);
+            if (act) {
+                PixelGeom<float, true> pg(s, pxc, pyc);
+                const unsigned wact = __reduce_or_sync(__activemask(), act);
+                const float2 cK = f2(pg.cK), Bx = f2(pg.Bx2), Ax = f2(pg.Ax2), o = f2(s.o);
+                const float2 c0 = f2(s.c0), c1 = f2(s.c1), c2 = f2(s.c2), sb = f2(s.b), sc = f2(s.c);
+                const float2 adx0 = f2(pg.adx0), bdx0 = f2(pg.bdx0);
+#pragma unroll
+                for (int g = 0; g < PPT / 2; ++g) {
+                    if (!((wact >> (2 * g)) & 3u)) continue;  // warp-uniform skip of the row pair
+                    const float2 y = add2(f2(pg.dy0), make_float2((float)(4 * g), (float)(4 * g + 2)));
+                    const float2 ex = fma2(fma2(cK, y, Bx), y, Ax);
+                    float2 G;
+                    G.x = (act >> (2 * g)) & 1u ? ss_ex2(ex.x) : 0.f;
+                    G.y = (act >> (2 * g + 1)) & 1u ? ss_ex2(ex.y) : 0.f;
+                    const float2 oG = mul2(o, G);
+                    const bool open_x = oG.x < cap.x, open_y = oG.y < cap.y;
+                    const float2 alpha = make_float2(open_x ? oG.x : cap.x, open_y ? oG.y : cap.y);
+                    const float2 w = mul2(alpha, T[g]);
+                    const float2 gcol = fma2(g2[g], c2, fma2(g1[g], c1, mul2(g0[g], c0)));
+                    acc[0] = fma2(g0[g], w, acc[0]);
+                    acc[1] = fma2(g1[g], w, acc[1]);
+                    acc[2] = fma2(g2[g], w, acc[2]);
+                    // dL/dalpha = sum_c gC_c (col_c T - S_c / (1 - alpha)), S = C - prefix - contrib
+                    const float2 rest = fma2(neg2(w), gcol, Rr[g]);
+                    const float2 oma = add2(one, neg2(alpha));
+                    const float2 rc = make_float2(ss_rcp<float>(oma.x), ss_rcp<float>(oma.y));
+                    const float2 dal = fma2(T[g], gcol, neg2(mul2(rest, rc)));
+                    Rr[g] = rest;
+                    const float2 dalm = make_float2(open_x ? dal.x : 0.f, open_y ? dal.y : 0.f);  // capped: no gradient
+                    const float2 dG = mul2(dalm, G);
+                    const float2 gp = mul2(dalm, alpha);
+                    const float2 adx = fma2(sb, y, adx0);
+                    const float2 ady = fma2(sc, y, bdx0);
+                    const float2 gpx = mul2(gp, adx), gpy = mul2(gp, ady);
+                    acc[3] = add2(acc[3], dG);
+                    acc[4] = add2(acc[4], gpx);
+                    acc[5] = add2(acc[5], gpy);
+                    acc[6] = fma2(gpx, adx, acc[6]);
+                    acc[7] = fma2(gpx, ady, acc[7]);
+                    acc[8] = fma2(gpy, ady, acc[8]);
+                    T[g] = add2(T[g], neg2(w));
+                    gate_t(alive, T[g].x, 1u << (2 * g));
+                    gate_t(alive, T[g].y, 1u << (2 * g + 1));
+                }
+            }
+            float* out = partials + (uint64_t)(uint32_t)s.p * 9;
+            if (__any_sync(0xffffffffu, act != 0)) {
+                float a8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) a8[e] = acc[e].x + acc[e].y;
+                const float y = warp_reduce8<float>(a8, lane);
+                const float z = warp_sum<float>(acc[8].x + acc[8].y);
+                if ((lane & 3) == 0) {
+                    const int e = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                    out[e] = e >= 6 ? 0.5f * y : y;
+                }
+                if (lane == 0) out[8] = 0.5f * z;
+            } else if (lane < 9) {
+                out[lane] = 0.f;
+            }
+        }
+        __syncwarp();
+    }
+    // pairs after every pixel of the tile saturated contribute nothing
+    for (uint32_t i = stop + lane; i < rg.y; i += 32) {
+        const uint32_t j = pvals[i];
+        const uint32_t p = pair_index(roffj, rec_[j].win, j, tx, ty);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) partials[(uint64_t)p * 9 + q] = 0.f;
+    }
+    loss = warp_sum<double>(loss);
+    if (lane == 0) tile_loss[tile] = loss;
 }
 
 __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, double inv_npx, double* __restrict__ out) {
@@ -1644,9 +1817,17 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     SS_CHECK_LAUNCH(ctx);
     if (o->tile_order && o->tile_hint && o->tile_hint_len == b.n_tiles)  // reused by the next forward of this camera
         SS_CUDA(ctx, cudaMemcpyAsync(o->tile_order, order, sizeof(uint32_t) * b.n_tiles, cudaMemcpyDeviceToDevice, s));
-    SS_CUDA(ctx, ss_launch((k_blend_bwd<R>), dim3((b.n_tiles + WPB_BWD - 1) / WPB_BWD), dim3(32 * WPB_BWD), 0, s, 
-        b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
-        b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order));
+#ifndef SS_BWD_PACKED
+#define SS_BWD_PACKED 0  // measured (bench step, 8 views): packed 9.69 / scalar 9.21 ms -- 17 % fewer
+#endif                   // instructions, but 114 registers drop issue-active from 77 % to 59 %
+    if (sizeof(R) == 4 && SS_BWD_PACKED)
+        SS_CUDA(ctx, ss_launch((k_blend_bwd2), dim3((b.n_tiles + WPB_BWD - 1) / WPB_BWD), dim3(32 * WPB_BWD), 0, s,
+            b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
+            b.n_tiles, (const float*)img, gt, (double)(3 * npx), (float*)partials, tloss, order));
+    else
+        SS_CUDA(ctx, ss_launch((k_blend_bwd<R>), dim3((b.n_tiles + WPB_BWD - 1) / WPB_BWD), dim3(32 * WPB_BWD), 0, s,
+            b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
+            b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order));
     SS_CHECK_LAUNCH(ctx);
     SS_CUDA(ctx, ss_launch((k_loss_reduce), dim3(1), dim3(256), 0, s, tloss, b.n_tiles, inv_npx, loss));
     SS_CHECK_LAUNCH(ctx);
@@ -1934,6 +2115,22 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
     if (visible_out) *visible_out = (int64_t)M;
     SS_CUDA(ctx, cudaStreamSynchronize(s));
     return SS_OK;
+}
+
+int ss_debug_bwd_stats(ss_ctx* ctx, unsigned long long out[8], int reset) {
+    if (!ctx || !out) return SS_ERR_INVALID;
+#ifdef SS_BWD_STATS
+    SS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    SS_CUDA(ctx, cudaMemcpyFromSymbol(out, g_bwd_stats, sizeof(unsigned long long) * 8));
+    if (reset) {
+        unsigned long long z[8] = {};
+        SS_CUDA(ctx, cudaMemcpyToSymbol(g_bwd_stats, z, sizeof(z)));
+    }
+    return SS_OK;
+#else
+    (void)reset;
+    return ss_fail(ctx, SS_ERR_INVALID, "built without SS_BWD_STATS");
+#endif
 }
 
 int ss_prepare_extras(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L, const int64_t* rows,
