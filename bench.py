@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--degree", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--atomics", action="store_true", help="with --step-only: also time the atomics mode")
     ap.add_argument("--step-only", action="store_true",
                     help="profiling: only the timed optimize steps (no encoder / pool / engine / e2e records)")
     return ap.parse_args()
@@ -370,6 +371,12 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     value = args.views * args.steps / (ms / 1e3)
 
+    # ---- the backward's throughput mode (float atomics, ss_render_opts.deterministic = 0),
+    # same workload and timing; the headline `value` is the deterministic mode
+    atomics = None
+    if not args.step_only or args.atomics:
+        atomics = atomics_bench(args, dm, state, views, ws, pg, dev, delta_tick, torch)
+
     # ---- delta encoder alone (rank 0): per-frame set, raw, device-resident
     enc = None
     extras = rank == 0 and not args.step_only
@@ -470,12 +477,43 @@ def run_ours(args):
            "config": workload_config(args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
            "gpu_launches": launches, "clocks": clock_rec,
            "kernel_ms_per_step": {k: round(v, 4) for k, v in per_step.items()},
+           "atomics_mode": atomics,
            "evaluated_pairs_per_view": evals_per_view,
            "delta_encode": enc, "pool_maintenance": pool_rec, "server_tick_zlib": zlib_rec, "engine": engine_rec, "client_render": client_rec, "fp32_peak_tflops_measured": fp32_peak,
            "precision": "fp64 preprocess/windows/depth keys, fp32 blend + chain rule, fp64 Adam moments"}
     print(json.dumps(out), flush=True)
     if pg is not None:
         dist.destroy_process_group()
+
+
+def atomics_bench(args, dm, state, views, ws, pg, dev, delta_tick, torch, steps=None):
+    """The timed loop again with the backward's throughput mode: each (tile,
+    splat) pair's sums go into the splat's record with float atomics (no
+    per-pair partials, no fixed-order partial sum).  Same step otherwise;
+    device time with CUDA events, max over ranks."""
+    import torch.distributed as dist
+    from paper_2604_02851_b200.optim import step
+    k = steps or args.steps
+    for i in range(2):
+        step(dm, state, views, workspace=ws, sync_loss=False, deterministic=False)
+    torch.cuda.synchronize()
+    if pg is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(k):
+        step(dm, state, views, workspace=ws, sync_loss=False, deterministic=False)
+        delta_tick(i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    return {"value": args.views * k / (ms / 1e3), "unit": "views/s", "ms_per_step": ms / k, "steps": k,
+            "note": "optim.step(deterministic=False): per-(tile, splat) sums added with float atomics into the "
+                    "per-row screen-space records (no partials, no fixed-order sum); the headline value is the "
+                    "deterministic mode"}
 
 
 def ctypes_peak(c):

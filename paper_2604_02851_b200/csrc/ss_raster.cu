@@ -611,7 +611,13 @@ __device__ __forceinline__ uint32_t pair_index(const uint64_t* roff, const int w
 // [5] pixel slots computed (executed row groups x QG x body lanes)
 __device__ unsigned long long g_bwd_stats[8];
 #endif
-template <typename R>
+// ATOMIC (the throughput mode, ss_render_opts.deterministic = 0): each
+// (tile, splat) pair's 9 warp-reduced sums are added straight into the
+// splat's screen-space record g9[j] with float atomics (no partials, no
+// k_sum_partials pass); the order of the additions across tiles is the
+// scheduler's, so reruns can differ in the last bits.  Otherwise one partial
+// per pair, summed in a fixed order by k_sum_partials (deterministic).
+template <typename R, bool ATOMIC = false>
 __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restrict__ ranges,
                                                         const uint32_t* __restrict__ pvals,
                                                         const double2* __restrict__ mu,
@@ -675,7 +681,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
             const uint32_t j = pvals[i];
             const SplatRec<R> rec = rec_[j];
             stage(my[lane], mu[j], rec, X0, Y0);
-            my[lane].p = (int)pair_index(roffj, rec.win, j, tx, ty);
+            my[lane].p = ATOMIC ? (int)j : (int)pair_index(roffj, rec.win, j, tx, ty);
         }
         __syncwarp();
         const int nb = (int)min(32u, stop - b0);
@@ -744,17 +750,22 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
                 const R z = warp_sum<R>(acc[8]);
                 if ((lane & 3) == 0) {
                     const int e = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                    out[e] = e >= 6 ? (R)0.5 * y : y;
+                    const R v = e >= 6 ? (R)0.5 * y : y;
+                    if (ATOMIC) atomicAdd(out + e, v);
+                    else out[e] = v;
                 }
-                if (lane == 0) out[8] = (R)0.5 * z;
-            } else if (lane < 9) {
+                if (lane == 0) {
+                    if (ATOMIC) atomicAdd(out + 8, (R)0.5 * z);
+                    else out[8] = (R)0.5 * z;
+                }
+            } else if (!ATOMIC && lane < 9) {
                 out[lane] = 0;
             }
         }
         __syncwarp();
     }
     // pairs after every pixel of the tile saturated contribute nothing
-    for (uint32_t i = stop + lane; i < rg.y; i += 32) {
+    for (uint32_t i = stop + lane; !ATOMIC && i < rg.y; i += 32) {
         const uint32_t j = pvals[i];
         const uint32_t p = pair_index(roffj, rec_[j].win, j, tx, ty);
 #pragma unroll
@@ -1800,11 +1811,16 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     Bins b;
     SS_TRY(build_bins<R>(ctx, m, cam, L, o, b, nullptr));
     const int64_t npx = (int64_t)cam->width * cam->height;
+    const bool atomic = o->deterministic == 0;
+    const bool chain = b.n_in > 0 && m->active_count > 0;
     R* img = img_out ? (R*)img_out : SS_SCRATCH(ctx, R, 3 * npx);
     uint32_t* stop = SS_SCRATCH(ctx, uint32_t, b.n_tiles);
     double* tloss = SS_SCRATCH(ctx, double, b.n_tiles);
-    R* partials = SS_SCRATCH(ctx, R, 9 * (b.pairs > 0 ? b.pairs : 1));
-    if (!img || !stop || !tloss || !partials) return SS_ERR_CUDA;
+    // per input row: the 9 screen-space sums (the deferred buffer, or scratch)
+    R* g9 = (o->defer_g9 && sizeof(R) == 4) ? (R*)o->defer_g9 : SS_SCRATCH(ctx, R, 9 * (b.n_in > 0 ? b.n_in : 1));
+    R* partials = atomic ? nullptr : SS_SCRATCH(ctx, R, 9 * (b.pairs > 0 ? b.pairs : 1));
+    if (!img || !stop || !tloss || !g9 || (!atomic && !partials)) return SS_ERR_CUDA;
+    if (atomic && b.n_in > 0) SS_CUDA(ctx, cudaMemsetAsync(g9, 0, sizeof(R) * 9 * (size_t)b.n_in, s));
     SS_TRY(forward<R>(ctx, cam, o, b, img, (R*)nullptr, stop));
     if (o->tile_hint && o->tile_hint_len == b.n_tiles)  // this call's walk lengths order the next forward
         SS_CUDA(ctx, cudaMemcpyAsync(o->tile_hint, stop, sizeof(uint32_t) * b.n_tiles, cudaMemcpyDeviceToDevice, s));
@@ -1820,49 +1836,46 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
 #ifndef SS_BWD_PACKED
 #define SS_BWD_PACKED 0  // measured (bench step, 8 views): packed 9.69 / scalar 9.21 ms -- 17 % fewer
 #endif                   // instructions, but 114 registers drop issue-active from 77 % to 59 %
-    if (sizeof(R) == 4 && SS_BWD_PACKED)
-        SS_CUDA(ctx, ss_launch((k_blend_bwd2), dim3((b.n_tiles + WPB_BWD - 1) / WPB_BWD), dim3(32 * WPB_BWD), 0, s,
-            b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
-            b.n_tiles, (const float*)img, gt, (double)(3 * npx), (float*)partials, tloss, order));
+    const dim3 grid((b.n_tiles + WPB_BWD - 1) / WPB_BWD), block(32 * WPB_BWD);
+    if (atomic)
+        SS_CUDA(ctx, ss_launch((k_blend_bwd<R, true>), grid, block, 0, s, b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec,
+                               b.roffj, stop, cam->width, cam->height, b.tiles_x, b.n_tiles, img, gt, (double)(3 * npx), g9,
+                               tloss, order));
+    else if (sizeof(R) == 4 && SS_BWD_PACKED)
+        SS_CUDA(ctx, ss_launch((k_blend_bwd2), grid, block, 0, s, b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec,
+                               b.roffj, stop, cam->width, cam->height, b.tiles_x, b.n_tiles, (const float*)img, gt,
+                               (double)(3 * npx), (float*)partials, tloss, order));
     else
-        SS_CUDA(ctx, ss_launch((k_blend_bwd<R>), dim3((b.n_tiles + WPB_BWD - 1) / WPB_BWD), dim3(32 * WPB_BWD), 0, s,
-            b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, b.roffj, stop, cam->width, cam->height, b.tiles_x,
-            b.n_tiles, img, gt, (double)(3 * npx), partials, tloss, order));
+        SS_CUDA(ctx, ss_launch((k_blend_bwd<R, false>), grid, block, 0, s, b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec,
+                               b.roffj, stop, cam->width, cam->height, b.tiles_x, b.n_tiles, img, gt, (double)(3 * npx),
+                               partials, tloss, order));
     SS_CHECK_LAUNCH(ctx);
     SS_CUDA(ctx, ss_launch((k_loss_reduce), dim3(1), dim3(256), 0, s, tloss, b.n_tiles, inv_npx, loss));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_BACKWARD);
-    if (b.n_in > 0 && m->active_count > 0 && o->defer_g9) {  // chain rule left to ss_chain_views
+    if (chain && !atomic) {  // fixed-order sum of each splat's per-tile partials
         ss_tic(ctx, KC_CHAIN);
-        SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals, partials, b.n_in,
-                               (R*)o->defer_g9));
+        SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals,
+                               partials, b.n_in, g9));
         SS_CHECK_LAUNCH(ctx);
+        ss_toc(ctx, KC_CHAIN);
+    }
+    if (chain && o->defer_g9 && sizeof(R) == 4) {  // chain rule left to ss_chain_views
         SS_CUDA(ctx, cudaMemcpyAsync(o->defer_rinv, b.rinv, sizeof(uint32_t) * (size_t)b.n_in, cudaMemcpyDeviceToDevice, s));
-        ss_toc(ctx, KC_CHAIN);
-    } else if (b.n_in > 0 && m->active_count > 0 && sizeof(R) == 4) {
-        float* g9 = SS_SCRATCH(ctx, float, 9 * b.n_in);
-        if (!g9) return SS_ERR_CUDA;
-        ss_tic(ctx, KC_CHAIN);
-        SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals, partials, b.n_in,
-                               (R*)g9));
-        SS_CHECK_LAUNCH(ctx);
-        ss_toc(ctx, KC_CHAIN);
+    } else if (chain && sizeof(R) == 4) {
         ChainViews hv;
         memset(&hv, 0, sizeof(hv));
         hv.cam[0] = *cam;
         hv.light[0] = *L;
-        hv.g9[0] = g9;
+        hv.g9[0] = (const float*)g9;
         hv.rinv[0] = b.rinv;
         const int64_t a = m->active_count;
         SS_TRY(launch_chain_views(ctx, m, hv, 1, o->subset, 0, b.n_in, 0, a, grad, a));
-    } else if (b.n_in > 0 && m->active_count > 0) {
+    } else if (chain) {
         ss_tic(ctx, KC_CHAIN);
-        R* g9 = SS_SCRATCH(ctx, R, 9 * b.n_in);
         float4* shrec = SS_SCRATCH(ctx, float4, 2 * (int64_t)m->active_count);
-        if (!g9 || !shrec) return SS_ERR_CUDA;
+        if (!shrec) return SS_ERR_CUDA;
         SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)m->active_count, s));
-        SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals, partials, b.n_in, g9));
-        SS_CHECK_LAUNCH(ctx);
 #define SS_CHAIN(DEG)                                                                                     \
     SS_CUDA(ctx, ss_launch((k_chain<R, DEG>), dim3(gridn(ctx, b.n_in, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
                                                             o->extent_cutoff, grad, shrec));                      \

@@ -172,7 +172,7 @@ def _tile_order(view, device):
 
 
 def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subset=None, extent_cutoff=True,
-                    precision=0, image_out=None, subset_tensor=None, gt=None, defer=None):
+                    precision=0, image_out=None, subset_tensor=None, gt=None, defer=None, deterministic=True):
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
     its loss into `loss_accum` (float64 CUDA scalar).  With `defer` =
     (g9, rinv) device buffers the view's screen-space gradients are left
@@ -188,7 +188,8 @@ def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subs
     st = _lib.SSRenderStats()
     c.check(c.lib.ss_backward(c.handle, model.struct(), camera_struct(view.pose, view.intrinsics),
                               light_struct(view.light_state),
-                              render_opts(view.background, sub, extent_cutoff, precision, gt_ready=ready,
+                              render_opts(view.background, sub, extent_cutoff, precision, int(bool(deterministic)),
+                                          gt_ready=ready,
                                           tile_hint=_tile_hint(view, model.device), defer=defer,
                                           tile_order=_tile_order(view, model.device)),
                               _lib.ptr(gt), _lib.ptr(grad_accum), _lib.ptr(loss_accum), _lib.ptr(image_out), st))
@@ -196,8 +197,10 @@ def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subs
     return st
 
 
-def backward(model, view: ReferenceView, index_subset=None, extent_cutoff: bool = True, precision: int = 0):
-    """ref optim.py:113 -- (loss, Gradients over active rows, rendered image)."""
+def backward(model, view: ReferenceView, index_subset=None, extent_cutoff: bool = True, precision: int = 0,
+             deterministic: bool = True):
+    """ref optim.py:113 -- (loss, Gradients over active rows, rendered image).
+    deterministic=False: the throughput mode (float atomics, see ss_render_opts)."""
     import torch
     dm, _ = as_device(model)
     a = dm.active_count
@@ -206,7 +209,7 @@ def backward(model, view: ReferenceView, index_subset=None, extent_cutoff: bool 
     L = torch.zeros(1, dtype=torch.float64, device=dm.device)
     H, W = view.intrinsics.height, view.intrinsics.width
     img = torch.empty((H, W, 3), dtype=torch.float64 if precision else torch.float32, device=dm.device)
-    backward_device(dm, view, g, L, index_subset, extent_cutoff, precision, img)
+    backward_device(dm, view, g, L, index_subset, extent_cutoff, precision, img, deterministic=deterministic)
     parts = split_flat(g[:n], a, dm.sh_degree)
     grads = Gradients(**{k: v.double().cpu().numpy() for k, v in parts.items()})
     return float(L.item()), grads, img.double().cpu().numpy()
@@ -554,8 +557,9 @@ class _DeviceKernels:
     """The compute of parallel.sharded_step on this GPU (libsplat_b200)."""
 
     def __init__(self, dm: DeviceModel, state: OptimizerState, ws: StepWorkspace, views, subset, extent_cutoff,
-                 plan: parallel.ShardPlan):
+                 plan: parallel.ShardPlan, deterministic=True):
         self.dm, self.state, self.ws, self.sub, self.cutoff, self.plan = dm, state, ws, subset, extent_cutoff, plan
+        self.deterministic = deterministic
         self.n_in = int(subset.numel()) if subset is not None else dm.count
         B = (dm.sh_degree + 1) ** 2
         self.ld = dm.active_count if plan.world == 1 else plan.R
@@ -584,7 +588,7 @@ class _DeviceKernels:
         else:
             defer = (g9[:self.n_in], rinv[:self.n_in])
         backward_device(self.dm, view, self.grad, self.ws.losses[i:i + 1], None, self.cutoff, 0, None,
-                        subset_tensor=self.sub, gt=self.gts[id(view)], defer=defer)
+                        subset_tensor=self.sub, gt=self.gts[id(view)], defer=defer, deterministic=self.deterministic)
         if sharded_subset:
             rinv.fill_(-1)
             g9[self.sub] = tmp_g9
@@ -653,14 +657,17 @@ class _DeviceKernels:
 
 
 def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: bool = True, precision: int = 0,
-         process_group=None, workspace: Optional[StepWorkspace] = None, sync_loss: bool = True):
+         process_group=None, workspace: Optional[StepWorkspace] = None, sync_loss: bool = True,
+         deterministic: bool = True):
     """ref optim.py:353 -- one Adam step over the ready views; returns the mean loss.
 
     With a `process_group` (or a state created with one) every rank passes
     the SAME views; rank r renders views r, r+N, ... and the step is sharded
     as parallel.py describes -- bit-identical to the single-GPU step.
     `sync_loss=False` returns the device loss tensor instead of a host float
-    (no host synchronisation).
+    (no host synchronisation).  `deterministic=False` selects the backward's
+    throughput mode: per-(tile, splat) sums added with float atomics instead
+    of the fixed-order partial sums (reruns may differ in the last bits).
     """
     ready = [v for v in views if v.ready]
     if not ready:
@@ -678,9 +685,9 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     if precision != 0:
         if plan.world > 1:
             raise ValueError("the fp64 blend (precision=1) is single-GPU")
-        loss = _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws)
+        loss = _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws, deterministic)
     else:
-        kern = _DeviceKernels(dm, state, ws, ready, sub, extent_cutoff, plan)
+        kern = _DeviceKernels(dm, state, ws, ready, sub, extent_cutoff, plan, deterministic)
         kern.stage(parallel.shard_views(ready, plan.rank, plan.world) if plan.world > 1 else ready)
         coll = parallel.Collectives(pg) if plan.world > 1 else None
         loss = parallel.sharded_step(kern, ready, plan, coll, CHAIN_MAX_VIEWS)
@@ -692,14 +699,15 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     return float(loss.item()) / total
 
 
-def _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws):
+def _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws, deterministic=True):
     """Per-view chain rule into the gradient (the fp64 blend instantiation)."""
     B = (dm.sh_degree + 1) ** 2
     a = dm.active_count
     grad = ws.prepare(a * (11 + 3 * B), len(ready))
     gts = _stage_ground_truth(ready, dm.device)
     for i, (v, gt) in enumerate(zip(ready, gts)):
-        backward_device(dm, v, grad, ws.losses[i:i + 1], None, extent_cutoff, precision, None, subset_tensor=sub, gt=gt)
+        backward_device(dm, v, grad, ws.losses[i:i + 1], None, extent_cutoff, precision, None, subset_tensor=sub, gt=gt,
+                        deterministic=deterministic)
     c = _lib.ctx(dm.device.index)
     c.check(c.lib.ss_sum_f64(c.handle, ws.losses.data_ptr(), len(ready), ws.loss.data_ptr()))
     if a > 0:
