@@ -93,6 +93,12 @@ typedef struct {
                                 tile_order_valid = 1 uses it instead of re-sorting (needs tile_hint) */
     int32_t tile_order_valid;
     int32_t _pad2;
+    int64_t* bins_status;    /* backward: optional device int64[2].  Set, and once the context knows a pair
+                                capacity (ss_pair_capacity; the first call sets it from its own count), the
+                                binning reads nothing back to the host: [0] counts calls whose (tile, splat)
+                                pairs exceeded the capacity (their results are void; ss_adam_step_ld with
+                                skip_if = this buffer then leaves the model alone), [1] keeps the largest
+                                pair count seen.  NULL = the pair count is read back (one host sync) */
 } ss_render_opts;
 
 /* The chain rule of a step's views in one pass over the rows (ref
@@ -153,6 +159,9 @@ typedef struct {
     double* grad_ema;        /* (a,) */
     int64_t* age;            /* (a,) */
     int32_t step_count;      /* t before this step; the call uses t+1 */
+    const int64_t* skip_if;  /* optional device int64: when non-zero at run time (a binning overflow of the
+                                step, see ss_render_opts.bins_status) the update leaves the model, moments,
+                                EMA and age untouched.  NULL = always update */
 } ss_adam_state;
 
 /* ---- context ------------------------------------------------------------ */
@@ -160,6 +169,14 @@ int ss_ctx_create(int device, ss_ctx** out);
 void ss_ctx_destroy(ss_ctx* ctx);
 const char* ss_last_error(const ss_ctx* ctx);
 int ss_set_stream(ss_ctx* ctx, void* cuda_stream);   /* cudaStream_t */
+/* Raise the pair capacity of sync-free binning to at least `cap` (grow-only)
+ * and return it; cap == 0 only reads it (0 = not yet known); cap < 0 sets it
+ * to -cap (tests: forces the overflow-and-re-run path). */
+int64_t ss_pair_capacity(ss_ctx* ctx, int64_t cap);
+/* Host synchronisations this context has issued so far (stream syncs,
+ * read-backs, scratch-arena growth): the optimizer step's fp32 path issues
+ * none once warmed up (tests/test_gpu_step.py). */
+int64_t ss_host_syncs(const ss_ctx* ctx);
 int ss_abi_version(void);
 /* Flat gradient buffer layout for `a` active rows at SH degree d:
  * [means a*3 | log_scales a*3 | quaternions a*4 | logit_opacities a | sh_coeffs a*3*B]

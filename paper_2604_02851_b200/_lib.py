@@ -44,7 +44,7 @@ class SSRenderOpts(C.Structure):
     _fields_ = [("background", f64 * 3), ("subset", vp), ("subset_count", i32), ("extent_cutoff", i32),
                 ("precision", i32), ("deterministic", i32), ("gt_ready", vp), ("tile_hint", vp),
                 ("tile_hint_len", i64), ("defer_g9", vp), ("defer_rinv", vp), ("tile_order", vp),
-                ("tile_order_valid", i32), ("_pad2", i32)]
+                ("tile_order_valid", i32), ("_pad2", i32), ("bins_status", vp)]
 
 
 class SSRenderStats(C.Structure):
@@ -58,7 +58,7 @@ class SSAdamHparams(C.Structure):
 
 
 class SSAdamState(C.Structure):
-    _fields_ = [("m", vp), ("v", vp), ("grad_ema", vp), ("age", vp), ("step_count", i32)]
+    _fields_ = [("m", vp), ("v", vp), ("grad_ema", vp), ("age", vp), ("step_count", i32), ("skip_if", vp)]
 
 
 class SSPrepared(C.Structure):
@@ -154,6 +154,8 @@ _SIGS = {
     "ss_ctx_destroy": (None, [vp]),
     "ss_last_error": (C.c_char_p, [vp]),
     "ss_set_stream": (i32, [vp, vp]),
+    "ss_pair_capacity": (i64, [vp, i64]),
+    "ss_host_syncs": (i64, [vp]),
     "ss_grad_layout": (i64, [i64, i32, C.POINTER(i64)]),
     "ss_set_timing": (i32, [vp, i32]),
     "ss_get_timing": (i32, [vp, C.POINTER(f64), C.POINTER(i64), C.POINTER(u64), i32]),

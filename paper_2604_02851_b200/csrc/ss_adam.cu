@@ -72,8 +72,10 @@ __device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float*
 template <bool PADDED>
 __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float* __restrict__ quats,
                        float* __restrict__ logits, float* __restrict__ sh, double* __restrict__ m,
-                       double* __restrict__ v, const float* __restrict__ g, AdamConst c) {
+                       double* __restrict__ v, const float* __restrict__ g, AdamConst c,
+                       const int64_t* __restrict__ skip_if) {
     SS_PDL_WAIT();
+    if (skip_if && *skip_if) return;  // the step's binning overflowed: no update
     const int64_t a = c.ld, total = a * (11 + 3 * (int64_t)c.B);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += ADAM_U * stride) {
@@ -109,8 +111,9 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
 }
 
 __global__ void k_adam_rows(float* __restrict__ quats, const float* __restrict__ g, double* __restrict__ ema,
-                            int64_t* __restrict__ age, AdamConst c) {
+                            int64_t* __restrict__ age, AdamConst c, const int64_t* __restrict__ skip_if) {
     SS_PDL_WAIT();
+    if (skip_if && *skip_if) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.a; i += (int64_t)gridDim.x * blockDim.x) {
         float* q = quats + 4 * i;
         const double w = q[0], x = q[1], y = q[2], z = q[3];
@@ -167,14 +170,14 @@ extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, 
     ss_tic(ctx, KC_ADAM);
     if (ld == a)
         SS_CUDA(ctx, ss_launch((k_adam<false>), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales,
-                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c));
+                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c, st->skip_if));
     else
         SS_CUDA(ctx, ss_launch((k_adam<true>), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales,
-                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c));
+                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c, st->skip_if));
     SS_CHECK_LAUNCH(ctx);
     int64_t rg = (a + 255) / 256;
     if (rg > (int64_t)ctx->num_sms * 32) rg = (int64_t)ctx->num_sms * 32;
-    SS_CUDA(ctx, ss_launch((k_adam_rows), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions, grad, st->grad_ema, st->age, c));
+    SS_CUDA(ctx, ss_launch((k_adam_rows), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions, grad, st->grad_ema, st->age, c, st->skip_if));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_ADAM);
     st->step_count = t;

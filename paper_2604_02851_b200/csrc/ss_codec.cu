@@ -405,7 +405,7 @@ int ss_encode_light_visibility(ss_ctx* ctx, const float* vis, int64_t n, uint8_t
     memcpy((uint8_t*)ctx->pinned + 8, &len, 8);
     SS_CUDA(ctx, cudaMemcpyAsync(out, ctx->pinned, 4, cudaMemcpyHostToDevice, s));
     SS_CUDA(ctx, cudaMemcpyAsync(out_len, (uint8_t*)ctx->pinned + 8, 8, cudaMemcpyHostToDevice, s));
-    SS_CUDA(ctx, cudaStreamSynchronize(s));  // the pinned staging buffer is reused
+    SS_CUDA(ctx, ss_stream_sync(ctx));  // the pinned staging buffer is reused
     return SS_OK;
 }
 

@@ -31,7 +31,7 @@ int ss_scratch_reset(ss_ctx* ctx) {
     if (a->call_total > a->high_water) a->high_water = a->call_total;
     if (a->blocks.size() > 1) {
         // coalesce into one block large enough for the biggest call seen
-        SS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        SS_CUDA(ctx, ss_stream_sync(ctx));
         for (auto& b : a->blocks) cudaFree(b.first);
         a->blocks.clear();
         size_t cap = ss_align(a->high_water + a->high_water / 4 + (1 << 20));
@@ -51,6 +51,7 @@ void* ss_scratch(ss_ctx* ctx, size_t bytes) {
     if (a->blocks.empty() || a->used + bytes > a->blocks.back().second) {
         size_t cap = ss_align(bytes > (64u << 20) ? bytes : (64u << 20));
         uint8_t* p = nullptr;
+        ++ctx->host_syncs;  // cudaMalloc may synchronise the device
         cudaError_t e = cudaMalloc(&p, cap);
         if (e != cudaSuccess) {
             ss_fail(ctx, SS_ERR_CUDA, "scratch cudaMalloc(%zu): %s", cap, cudaGetErrorString(e));
@@ -66,7 +67,7 @@ void* ss_scratch(ss_ctx* ctx, size_t bytes) {
 
 int ss_read_u64(ss_ctx* ctx, const void* dev, uint64_t* out, int count) {
     SS_CUDA(ctx, cudaMemcpyAsync(ctx->pinned, dev, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost, ctx->stream));
-    SS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    SS_CUDA(ctx, ss_stream_sync(ctx));
     memcpy(out, ctx->pinned, sizeof(uint64_t) * count);
     return SS_OK;
 }
@@ -88,6 +89,8 @@ int ss_ctx_create(int device, ss_ctx** out) {
     c->dev_counters = nullptr;
     c->launches = 0;
     c->stream_switch = nullptr;
+    c->pair_cap = 0;
+    c->host_syncs = 0;
     if (cudaMallocHost(&c->pinned, 4096) != cudaSuccess) {
         delete (Arena*)c->arena_state;
         delete c;
@@ -100,7 +103,7 @@ int ss_ctx_create(int device, ss_ctx** out) {
 
 void ss_ctx_destroy(ss_ctx* ctx) {
     if (!ctx) return;
-    cudaStreamSynchronize(ctx->stream);
+    ss_stream_sync(ctx);
     Arena* a = arena_of(ctx);
     for (auto& b : a->blocks) cudaFree(b.first);
     delete a;
@@ -112,6 +115,15 @@ void ss_ctx_destroy(ss_ctx* ctx) {
 }
 
 const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+int64_t ss_host_syncs(const ss_ctx* ctx) { return ctx ? ctx->host_syncs : -1; }
+
+int64_t ss_pair_capacity(ss_ctx* ctx, int64_t cap) {
+    if (!ctx) return -1;
+    if (cap > ctx->pair_cap) ctx->pair_cap = cap;
+    else if (cap < 0) ctx->pair_cap = -cap;  // tests: force a (small) capacity to exercise the overflow path
+    return ctx->pair_cap;
+}
 
 int ss_set_stream(ss_ctx* ctx, void* stream) {
     if (!ctx) return SS_ERR_INVALID;

@@ -26,6 +26,12 @@ struct ss_ctx {
     // orders a new stream after the previous one when ss_set_stream switches
     // (the scratch arena is shared by every call on the ctx)
     cudaEvent_t stream_switch;
+    // pair capacity of sync-free binning (grow-only; 0 = unknown: the next
+    // binning reads its pair count back once and sets it)
+    int64_t pair_cap;
+    // host synchronisations the library issued (stream syncs, read-backs,
+    // scratch-arena allocations): ss_host_syncs, for the sync-free tests
+    int64_t host_syncs;
 };
 
 enum ss_kernel_class {
@@ -94,6 +100,11 @@ void* ss_scratch(ss_ctx* ctx, size_t bytes);
 #define SS_SCRATCH(ctx, T, n) ((T*)ss_scratch((ctx), sizeof(T) * (size_t)(n)))
 inline size_t ss_align(size_t b) { return (b + 255) & ~size_t(255); }
 
+// every host synchronisation of the library goes through here (counted)
+inline cudaError_t ss_stream_sync(ss_ctx* ctx) {
+    ++ctx->host_syncs;
+    return cudaStreamSynchronize(ctx->stream);
+}
 // read a device scalar back to the host (synchronises the ctx stream)
 int ss_read_u64(ss_ctx* ctx, const void* dev, uint64_t* out, int count = 1);
 
@@ -132,7 +143,9 @@ int ss_scan_u32_to_u64(ss_ctx* ctx, const uint32_t* in, uint64_t* out, int64_t n
 int ss_scan_u8_to_u64(ss_ctx* ctx, const uint8_t* in, uint64_t* out, int64_t n, uint64_t* total);
 // Stable LSD radix sort of (key, value) pairs on bits [0, key_bits).
 // keys/vals are sorted in place; alt buffers are scratch of the same size.
+// With n_dev (device), the first *n_dev <= n entries are sorted (n sizes the
+// launch: no host read of the count).
 int ss_radix_sort_u32(ss_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                      int64_t n, int key_bits);
+                      int64_t n, int key_bits, const uint64_t* n_dev = nullptr);
 
 inline int ss_grid(int64_t n, int block) { return (int)((n + block - 1) / block); }

@@ -296,7 +296,7 @@ int ss_grid_rebuild(ss_ctx* ctx, const float* means, int64_t n, const ss_grid_sp
     SS_CHECK_LAUNCH(ctx);
     unsigned long long hm[6];
     SS_CUDA(ctx, cudaMemcpyAsync(hm, mm, sizeof(hm), cudaMemcpyDeviceToHost, s));
-    SS_CUDA(ctx, cudaStreamSynchronize(s));
+    SS_CUDA(ctx, ss_stream_sync(ctx));
     const double span = (double)(hm[3] - hm[0] + 1) * (double)(hm[4] - hm[1] + 1) * (double)(hm[5] - hm[2] + 1);
     if (span > 4294967295.0) return ss_fail(ctx, SS_ERR_CAPACITY, "grid spans more than 2^32 cells");
     int bits = 1;

@@ -57,6 +57,7 @@ struct Bins {
     uint32_t* pkeys;         // [pairs] tile id (sorted)
     uint32_t* pvals;         // [pairs] input index j of the splat (sorted by (tile, depth rank))
     uint2* ranges;           // [n_tiles]
+    uint64_t* n_pairs;       // [1] device: pairs emitted (<= pairs, the host-side capacity)
 };
 
 // ---------------------------------------------------------------- K1
@@ -264,7 +265,8 @@ template <typename R>
 __global__ void __launch_bounds__(256) k_emit_warp(const SplatRec<R>* __restrict__ rec, const uint32_t* __restrict__ dvals,
                                                    const uint32_t* __restrict__ rcnt, const uint64_t* __restrict__ roff,
                                                    int64_t n_in, int tiles_x, uint32_t* __restrict__ pkeys,
-                                                   uint32_t* __restrict__ pvals, uint64_t* __restrict__ roffj) {
+                                                   uint32_t* __restrict__ pvals, uint64_t* __restrict__ roffj,
+                                                   uint64_t cap) {
     SS_PDL_WAIT();
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(256) k_emit_warp(const SplatRec<R>* __restrict
             const uint32_t sj = __shfl_sync(0xffffffffu, j, src);
             const int sx = __shfl_sync(0xffffffffu, tx0, src), sy = __shfl_sync(0xffffffffu, ty0, src);
             const int sw = __shfl_sync(0xffffffffu, w, src);
-            if (p < p1) {
+            if (p < p1 && p < cap) {  // beyond the capacity: the call overflowed (flagged, results void)
                 const uint32_t q = (uint32_t)(p - so);
                 const uint32_t qy = q / (uint32_t)sw;
                 pkeys[p] = (uint32_t)((sy + (int)qy) * tiles_x + sx + (int)(q - qy * (uint32_t)sw));
@@ -310,8 +312,9 @@ __global__ void __launch_bounds__(256) k_emit_warp(const SplatRec<R>* __restrict
     }
 }
 
-__global__ void k_ranges(const uint32_t* __restrict__ keys, int64_t n, uint2* __restrict__ ranges) {
+__global__ void k_ranges(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ n_dev, uint2* __restrict__ ranges) {
     SS_PDL_WAIT();
+    const int64_t n = (int64_t)*n_dev;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t t = keys[s];
         if (s == 0 || keys[s - 1] != t) ranges[t].x = (uint32_t)s;
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
                                                         int tiles_x, int n_tiles, const R* __restrict__ img,
                                                         const float* __restrict__ gt, double npx3,
                                                         R* __restrict__ partials, double* __restrict__ tile_loss,
-                                                        const uint32_t* __restrict__ order) {
+                                                        const uint32_t* __restrict__ order, uint64_t cap) {
     SS_PDL_WAIT();
     __shared__ Staged<R> sm[WPB_BWD][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -745,20 +748,21 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
                 }
             }
             R* out = partials + (uint64_t)(uint32_t)s.p * 9;
+            const bool fits = ATOMIC || (uint64_t)(uint32_t)s.p < cap;  // else an overflowed call (flagged)
             if (__any_sync(0xffffffffu, act != 0)) {
                 const R y = warp_reduce8<R>(acc, lane);
                 const R z = warp_sum<R>(acc[8]);
-                if ((lane & 3) == 0) {
+                if ((lane & 3) == 0 && fits) {
                     const int e = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
                     const R v = e >= 6 ? (R)0.5 * y : y;
                     if (ATOMIC) atomicAdd(out + e, v);
                     else out[e] = v;
                 }
-                if (lane == 0) {
+                if (lane == 0 && fits) {
                     if (ATOMIC) atomicAdd(out + 8, (R)0.5 * z);
                     else out[8] = (R)0.5 * z;
                 }
-            } else if (!ATOMIC && lane < 9) {
+            } else if (!ATOMIC && lane < 9 && fits) {
                 out[lane] = 0;
             }
         }
@@ -768,6 +772,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
     for (uint32_t i = stop + lane; !ATOMIC && i < rg.y; i += 32) {
         const uint32_t j = pvals[i];
         const uint32_t p = pair_index(roffj, rec_[j].win, j, tx, ty);
+        if ((uint64_t)p >= cap) continue;
 #pragma unroll
         for (int q = 0; q < 9; ++q) partials[(uint64_t)p * 9 + q] = 0;
     }
@@ -898,7 +903,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD, SS_BWD2_MINB) k_blend_bwd2(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pvals, const double2* __restrict__ mu,
     const SplatRec<float>* __restrict__ rec_, const uint64_t* __restrict__ roffj, const uint32_t* __restrict__ tile_stop,
     int W, int H, int tiles_x, int n_tiles, const float* __restrict__ img, const float* __restrict__ gt, double npx3,
-    float* __restrict__ partials, double* __restrict__ tile_loss, const uint32_t* __restrict__ order) {
+    float* __restrict__ partials, double* __restrict__ tile_loss, const uint32_t* __restrict__ order, uint64_t pair_cap) {
     SS_PDL_WAIT();
     __shared__ Staged<float> sm[WPB_BWD][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1003,18 +1008,19 @@ __global__ void __launch_bounds__(32 * WPB_BWD, SS_BWD2_MINB) k_blend_bwd2(
                 }
             }
             float* out = partials + (uint64_t)(uint32_t)s.p * 9;
+            const bool fits = (uint64_t)(uint32_t)s.p < pair_cap;
             if (__any_sync(0xffffffffu, act != 0)) {
                 float a8[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) a8[e] = acc[e].x + acc[e].y;
                 const float y = warp_reduce8<float>(a8, lane);
                 const float z = warp_sum<float>(acc[8].x + acc[8].y);
-                if ((lane & 3) == 0) {
+                if ((lane & 3) == 0 && fits) {
                     const int e = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
                     out[e] = e >= 6 ? 0.5f * y : y;
                 }
-                if (lane == 0) out[8] = 0.5f * z;
-            } else if (lane < 9) {
+                if (lane == 0 && fits) out[8] = 0.5f * z;
+            } else if (lane < 9 && fits) {
                 out[lane] = 0.f;
             }
         }
@@ -1024,6 +1030,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD, SS_BWD2_MINB) k_blend_bwd2(
     for (uint32_t i = stop + lane; i < rg.y; i += 32) {
         const uint32_t j = pvals[i];
         const uint32_t p = pair_index(roffj, rec_[j].win, j, tx, ty);
+        if ((uint64_t)p >= pair_cap) continue;
 #pragma unroll
         for (int q = 0; q < 9; ++q) partials[(uint64_t)p * 9 + q] = 0.f;
     }
@@ -1057,7 +1064,7 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, doubl
 template <typename R>
 __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
                                                       const uint32_t* __restrict__ dvals, const R* __restrict__ partials,
-                                                      int64_t n_in, R* __restrict__ g9) {
+                                                      int64_t n_in, R* __restrict__ g9, uint64_t cap) {
     SS_PDL_WAIT();
     constexpr int PW = 4096 / (9 * sizeof(R));  // pairs per staged chunk (4 KB per warp)
     __shared__ R buf[8][PW * 9];
@@ -1075,6 +1082,7 @@ __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict
             const uint64_t t = __shfl_xor_sync(0xffffffffu, end, o);
             end = t > end ? t : end;
         }
+        end = end < cap ? end : cap;  // an overflowed call (flagged): never read past the partials
         R g[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // in the blend precision (fixed order: deterministic)
         for (uint64_t c0 = P0; c0 < end; c0 += PW) {
             const uint64_t c1 = min(c0 + PW, end);
@@ -1383,11 +1391,12 @@ struct ChainViews {
 // row0 with ld rows per group (ld = a, row0 = 0 on one GPU; a row shard in
 // the view-sharded step, whose g9 / rinv pointers are offset to be indexed by j).
 template <int DEG>
-__global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const ChainViews* __restrict__ V, int nv,
+__global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const __grid_constant__ ChainViews Vp, int nv,
                                                         const int64_t* __restrict__ subset, int64_t j0, int64_t j1,
                                                         int64_t row0, int64_t ld,
                                                         float* __restrict__ grad, float4* __restrict__ shrec) {
     SS_PDL_WAIT();
+    const ChainViews* V = &Vp;  // the views ride in the kernel parameters (no host-to-device copy)
     const int64_t a = m.active_count;
     for (int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < j1; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = subset ? subset[j] : j;
@@ -1497,10 +1506,11 @@ constexpr int SHGV_ROWS = SS_SHGV_ROWS;
 
 // rows [0, a) of a layout of ld rows per group (shrec: ld records per view)
 template <int DEG>
-__global__ void __launch_bounds__(256) k_sh_grad_views(const ChainViews* __restrict__ V, int nv,
+__global__ void __launch_bounds__(256) k_sh_grad_views(const __grid_constant__ ChainViews Vp, int nv,
                                                        const float4* __restrict__ shrec, int64_t a, int64_t ld,
                                                        float* __restrict__ grad_sh) {
     SS_PDL_WAIT();
+    const ChainViews* V = &Vp;
     constexpr int B = ss_sh_bases(DEG);
     extern __shared__ float4 s_dyn[];
     float4* s_r0 = s_dyn;                                          // [nv][SHGV_ROWS]
@@ -1623,16 +1633,40 @@ int validate(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_rend
     return SS_OK;
 }
 
+// The pair count of a binning on the device: n_pairs = min(total, cap); a
+// call whose pairs exceed the capacity counts an overflow in status[0]
+// (sticky: the optimizer step's Adam leaves the model alone while it is set)
+// and every call raises status[1] to its pair count (the host's next capacity).
+__global__ void k_clamp_pairs(const uint64_t* __restrict__ total, uint64_t cap, uint64_t* __restrict__ n_pairs,
+                              int64_t* __restrict__ status) {
+    SS_PDL_WAIT();
+    const uint64_t t = *total;
+    *n_pairs = t < cap ? t : cap;
+    if (status) {
+        if (t > cap) atomicAdd((unsigned long long*)&status[0], 1ull);
+        atomicMax((unsigned long long*)&status[1], (unsigned long long)t);
+    }
+}
+
 // K1..K4: preprocess, depth sort, count/scan/emit, tile sort, ranges.
 // (tile, splat) pairs of a depth-ordered splat set: counts per rank, scan,
 // warp-cooperative emission, stable tile sort, per-tile ranges.  Needs b's
 // dkey64 (~0 = culled), dvals (input index by rank), rec and the geometry.
+//
+// Pair buffers are sized on the host.  With a status buffer and a known
+// capacity (ctx->pair_cap) nothing is read back: the kernels take the pair
+// count from the device and never touch more than the capacity (an overflow
+// is flagged in status, see k_clamp_pairs).  Otherwise (no status, or the
+// first call of a context) the count is read back once and sets the
+// capacity for the calls that follow (1.1x + 64k pairs of headroom; a later
+// overflow grows it through the caller, see optim.step).
 template <typename R>
-int bin_pairs(ss_ctx* ctx, Bins& b) {
+int bin_pairs(ss_ctx* ctx, Bins& b, int64_t* status) {
     cudaStream_t s = ctx->stream;
     const int64_t n = b.n_in;
     uint64_t* total = SS_SCRATCH(ctx, uint64_t, 1);
-    if (!total) return SS_ERR_CUDA;
+    b.n_pairs = SS_SCRATCH(ctx, uint64_t, 1);
+    if (!total || !b.n_pairs) return SS_ERR_CUDA;
     ss_tic(ctx, KC_BIN);
     if (n > 0) {
         SS_CUDA(ctx, ss_launch((k_count<R>), dim3(gridn(ctx, n)), dim3(256), 0, s, b.dkey64, b.dvals, (const SplatRec<R>*)b.rec, n, b.rcnt, b.rinv));
@@ -1640,27 +1674,41 @@ int bin_pairs(ss_ctx* ctx, Bins& b) {
     }
     SS_TRY(ss_scan_u32_to_u64(ctx, b.rcnt, b.roff, n, total));
     ss_toc(ctx, KC_BIN);
-    uint64_t P = 0;
-    SS_TRY(ss_read_u64(ctx, total, &P));
-    if (P > 0xffffffffull) return ss_fail(ctx, SS_ERR_CAPACITY, "too many tile overlaps (%llu)", (unsigned long long)P);
-    b.pairs = (int64_t)P;
-    const int64_t pa = P > 0 ? (int64_t)P : 1;
+    uint64_t cap;
+#ifdef SS_FORCE_SYNC_BINS  // A/B measurements only: read every pair count back
+    if (false) {
+#else
+    if (status && ctx->pair_cap > 0) {
+#endif
+        cap = (uint64_t)ctx->pair_cap;
+    } else {
+        SS_TRY(ss_read_u64(ctx, total, &cap));
+        if (status) {
+            const int64_t want = (int64_t)(cap + cap / 10 + 65536);
+            if (want > ctx->pair_cap) ctx->pair_cap = want;
+        }
+    }
+    if (cap > 0xffffffffull) return ss_fail(ctx, SS_ERR_CAPACITY, "too many tile overlaps (%llu)", (unsigned long long)cap);
+    b.pairs = (int64_t)cap;
+    const int64_t pa = cap > 0 ? (int64_t)cap : 1;
     b.pkeys = SS_SCRATCH(ctx, uint32_t, pa);
     b.pvals = SS_SCRATCH(ctx, uint32_t, pa);
     uint32_t* pk2 = SS_SCRATCH(ctx, uint32_t, pa);
     uint32_t* pv2 = SS_SCRATCH(ctx, uint32_t, pa);
     if (!b.pkeys || !b.pvals || !pk2 || !pv2) return SS_ERR_CUDA;
-    if (P > 0) {
+    SS_CUDA(ctx, ss_launch((k_clamp_pairs), dim3(1), dim3(1), 0, s, (const uint64_t*)total, cap, b.n_pairs, status));
+    SS_CHECK_LAUNCH(ctx);
+    if (cap > 0) {
         ss_tic(ctx, KC_BIN);
         SS_CUDA(ctx, ss_launch((k_emit_warp<R>), dim3(gridn(ctx, n)), dim3(256), 0, s, (const SplatRec<R>*)b.rec, b.dvals, b.rcnt, b.roff, n,
-                               b.tiles_x, b.pkeys, b.pvals, b.roffj));
+                               b.tiles_x, b.pkeys, b.pvals, b.roffj, cap));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_BIN);
         ss_tic(ctx, KC_TILE_SORT);
-        SS_TRY(ss_radix_sort_u32(ctx, b.pkeys, b.pvals, pk2, pv2, (int64_t)P, b.tile_bits));
+        SS_TRY(ss_radix_sort_u32(ctx, b.pkeys, b.pvals, pk2, pv2, (int64_t)cap, b.tile_bits, b.n_pairs));
         ss_toc(ctx, KC_TILE_SORT);
         ss_tic(ctx, KC_BIN);
-        SS_CUDA(ctx, ss_launch((k_ranges), dim3(gridn(ctx, (int64_t)P)), dim3(256), 0, s, b.pkeys, (int64_t)P, b.ranges));
+        SS_CUDA(ctx, ss_launch((k_ranges), dim3(gridn(ctx, (int64_t)cap)), dim3(256), 0, s, b.pkeys, (const uint64_t*)b.n_pairs, b.ranges));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_BIN);
     }
@@ -1722,7 +1770,7 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_DEPTH_SORT);
     }
-    return bin_pairs<R>(ctx, b);
+    return bin_pairs<R>(ctx, b, o->bins_status);
 }
 
 template <typename R>
@@ -1776,21 +1824,19 @@ int render_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_ligh
 int launch_chain_views(ss_ctx* ctx, const ss_model* m, const ChainViews& hv, int nv, const int64_t* subset,
                        int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld) {
     cudaStream_t s = ctx->stream;
-    ChainViews* dv = SS_SCRATCH(ctx, ChainViews, 1);
     float4* shrec = SS_SCRATCH(ctx, float4, 2 * ld * nv);
-    if (!dv || !shrec) return SS_ERR_CUDA;
-    SS_CUDA(ctx, cudaMemcpyAsync(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice, s));
+    if (!shrec) return SS_ERR_CUDA;
     SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)ld * nv, s));
     ss_tic(ctx, KC_CHAIN);
 #define SS_CHAINV(DEG)                                                                                                     \
     do {                                                                                                                   \
         constexpr int B = ss_sh_bases(DEG);                                                                                \
-        SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, j1 - j0, 128)), dim3(128), 0, s, *m, (const ChainViews*)dv, \
+        SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, j1 - j0, 128)), dim3(128), 0, s, *m, hv,                  \
                                nv, subset, j0, j1, row0, ld, grad, shrec));                                                \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
         const size_t smem = (size_t)nv * SHGV_ROWS * (sizeof(float4) + sizeof(float) * (B + 1));                           \
         SS_CUDA(ctx, ss_launch((k_sh_grad_views<DEG>), dim3((unsigned)((rows + SHGV_ROWS - 1) / SHGV_ROWS)), dim3(256), smem, s, \
-                               (const ChainViews*)dv, nv, (const float4*)shrec, rows, ld, grad + 11 * ld));               \
+                               hv, nv, (const float4*)shrec, rows, ld, grad + 11 * ld));                                  \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
     } while (0)
     switch (m->sh_degree) {
@@ -1840,15 +1886,15 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (atomic)
         SS_CUDA(ctx, ss_launch((k_blend_bwd<R, true>), grid, block, 0, s, b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec,
                                b.roffj, stop, cam->width, cam->height, b.tiles_x, b.n_tiles, img, gt, (double)(3 * npx), g9,
-                               tloss, order));
+                               tloss, order, (uint64_t)b.pairs));
     else if (sizeof(R) == 4 && SS_BWD_PACKED)
         SS_CUDA(ctx, ss_launch((k_blend_bwd2), grid, block, 0, s, b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec,
                                b.roffj, stop, cam->width, cam->height, b.tiles_x, b.n_tiles, (const float*)img, gt,
-                               (double)(3 * npx), (float*)partials, tloss, order));
+                               (double)(3 * npx), (float*)partials, tloss, order, (uint64_t)b.pairs));
     else
         SS_CUDA(ctx, ss_launch((k_blend_bwd<R, false>), grid, block, 0, s, b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec,
                                b.roffj, stop, cam->width, cam->height, b.tiles_x, b.n_tiles, img, gt, (double)(3 * npx),
-                               partials, tloss, order));
+                               partials, tloss, order, (uint64_t)b.pairs));
     SS_CHECK_LAUNCH(ctx);
     SS_CUDA(ctx, ss_launch((k_loss_reduce), dim3(1), dim3(256), 0, s, tloss, b.n_tiles, inv_npx, loss));
     SS_CHECK_LAUNCH(ctx);
@@ -1856,7 +1902,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (chain && !atomic) {  // fixed-order sum of each splat's per-tile partials
         ss_tic(ctx, KC_CHAIN);
         SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals,
-                               partials, b.n_in, g9));
+                               partials, b.n_in, g9, (uint64_t)b.pairs));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_CHAIN);
     }
@@ -2036,7 +2082,7 @@ int ss_composite(ss_ctx* ctx, int64_t n, const double* mu2d, const double* inv2d
                                (SplatRec<double>*)b.rec, b.mu, b.dkey64, b.dvals));
         SS_CHECK_LAUNCH(ctx);
     }
-    SS_TRY(bin_pairs<double>(ctx, b));
+    SS_TRY(bin_pairs<double>(ctx, b, nullptr));
     ss_camera cam;
     memset(&cam, 0, sizeof(cam));
     cam.width = width;
@@ -2126,14 +2172,14 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
         SS_CHECK_LAUNCH(ctx);
     }
     if (visible_out) *visible_out = (int64_t)M;
-    SS_CUDA(ctx, cudaStreamSynchronize(s));
+    SS_CUDA(ctx, ss_stream_sync(ctx));
     return SS_OK;
 }
 
 int ss_debug_bwd_stats(ss_ctx* ctx, unsigned long long out[8], int reset) {
     if (!ctx || !out) return SS_ERR_INVALID;
 #ifdef SS_BWD_STATS
-    SS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    SS_CUDA(ctx, ss_stream_sync(ctx));
     SS_CUDA(ctx, cudaMemcpyFromSymbol(out, g_bwd_stats, sizeof(unsigned long long) * 8));
     if (reset) {
         unsigned long long z[8] = {};
@@ -2184,7 +2230,7 @@ int ss_debug_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss
         st->pairs = b.pairs;
         st->tiles = b.n_tiles;
     }
-    SS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    SS_CUDA(ctx, ss_stream_sync(ctx));
     return SS_OK;
 }
 

@@ -34,8 +34,9 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_hist_all(const K* __restrict__ keys, int64_t n, int key_bits,
-                                                         uint32_t* __restrict__ hist) {
+                                                         uint32_t* __restrict__ hist, const uint64_t* __restrict__ n_dev) {
     SS_PDL_WAIT();
+    if (n_dev) n = min(n, (int64_t)*n_dev);  // a device-side count (<= the launch capacity n)
     __shared__ uint32_t cnt[RS_MAX_PASSES][256];
     const int passes = (key_bits + 7) / 8;
     for (int p = 0; p < passes; ++p) cnt[p][threadIdx.x] = 0;
@@ -76,8 +77,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ k
                                                          int64_t n, int shift, unsigned mask,
                                                          const uint64_t* __restrict__ digit_base,
                                                          uint32_t* __restrict__ part, unsigned* __restrict__ tile_ctr,
-                                                         K* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+                                                         K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                                                         const uint64_t* __restrict__ n_dev) {
     SS_PDL_WAIT();
+    if (n_dev) n = min(n, (int64_t)*n_dev);  // a device-side count (<= the launch capacity n)
     constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
     __shared__ K s_keys[RS_TILE];
     __shared__ uint32_t s_vals[RS_TILE];
@@ -96,6 +99,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ k
     __syncthreads();
     const unsigned tile = s_tile;
     const int64_t base = (int64_t)tile * RS_TILE;
+    // tiles are taken in ticket order, so every tile past the (device-side)
+    // count is preceded only by tiles that also leave: nobody waits on them
+    if (base >= n && tile > 0) return;
 
     // ---- warp w owns keys [w*256, (w+1)*256) of the tile (item r at r*32 + lane):
     // load them all first, then rank within the warp without block barriers
@@ -220,7 +226,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ k
 }
 
 template <typename K, int RS_ITEMS>
-int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, int key_bits) {
+int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, int key_bits,
+              const uint64_t* n_dev) {
     constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
     if (n <= 1 || key_bits <= 0) return SS_OK;
     if (n > (int64_t)CNT_MASK) return ss_fail(ctx, SS_ERR_CAPACITY, "radix sort limited to 2^30 keys");
@@ -237,7 +244,7 @@ int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_
     SS_CUDA(ctx, cudaMemsetAsync(ctr, 0, sizeof(unsigned) * RS_MAX_PASSES, s));
     int hb = (int)((n + RS_THREADS * 16 - 1) / (RS_THREADS * 16));
     if (hb > ctx->num_sms * 8) hb = ctx->num_sms * 8;
-    SS_CUDA(ctx, ss_launch((k_hist_all<K>), dim3(hb), dim3(RS_THREADS), 0, s, keys, n, key_bits, hist));
+    SS_CUDA(ctx, ss_launch((k_hist_all<K>), dim3(hb), dim3(RS_THREADS), 0, s, keys, n, key_bits, hist, n_dev));
     SS_CHECK_LAUNCH(ctx);
     SS_CUDA(ctx, ss_launch((k_base_scan), dim3(1), dim3(32 * RS_MAX_PASSES), 0, s, hist, passes, base));
     SS_CHECK_LAUNCH(ctx);
@@ -250,7 +257,7 @@ int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_
         const int bits = key_bits - shift < 8 ? key_bits - shift : 8;
         const unsigned mask = (1u << bits) - 1u;
         SS_CUDA(ctx, ss_launch((k_onesweep<K, RS_ITEMS>), dim3((unsigned)tiles), dim3(RS_THREADS), 0, s, src_k, src_v, n, shift, mask, base + p * 256,
-                                                             part + (int64_t)p * tiles * 256, ctr + p, dst_k, dst_v));
+                                                             part + (int64_t)p * tiles * 256, ctr + p, dst_k, dst_v, n_dev));
         SS_CHECK_LAUNCH(ctx);
         K* tk = src_k; src_k = dst_k; dst_k = tk;
         uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
@@ -265,7 +272,7 @@ int sort_impl(ss_ctx* ctx, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_
 }  // namespace
 
 int ss_radix_sort_u32(ss_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                      int64_t n, int key_bits) {
+                      int64_t n, int key_bits, const uint64_t* n_dev) {
     // tile size: 4096 keys for the 32-bit depth keys (fewer tiles, shorter
     // look-back chains), 3072 for the short tile-id keys of the (tile, splat)
     // pairs (measured: 2048 / 3072 / 4096 -> 1.17 / 1.11 / 1.22 ms per step)
@@ -275,6 +282,6 @@ int ss_radix_sort_u32(ss_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* key
 #ifndef RS_LONG_ITEMS
 #define RS_LONG_ITEMS 16
 #endif
-    if (key_bits > 16) return sort_impl<uint32_t, RS_LONG_ITEMS>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits);
-    return sort_impl<uint32_t, RS_SHORT_ITEMS>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits);
+    if (key_bits > 16) return sort_impl<uint32_t, RS_LONG_ITEMS>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits, n_dev);
+    return sort_impl<uint32_t, RS_SHORT_ITEMS>(ctx, keys, vals, keys_alt, vals_alt, n, key_bits, n_dev);
 }

@@ -78,7 +78,7 @@ int ss_get_timing(ss_ctx* ctx, double ms_out[SS_KC_COUNT], int64_t groups_out[SS
                   int reset) {
     if (!ctx || !ctx->timer_state) return SS_ERR_INVALID;
     Timer* t = timer_of(ctx);
-    SS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    SS_CUDA(ctx, ss_stream_sync(ctx));
     for (auto& s : t->spans) {
         float ms = 0;
         cudaEventElapsedTime(&ms, s.a, s.b);

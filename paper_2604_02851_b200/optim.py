@@ -172,7 +172,8 @@ def _tile_order(view, device):
 
 
 def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subset=None, extent_cutoff=True,
-                    precision=0, image_out=None, subset_tensor=None, gt=None, defer=None, deterministic=True):
+                    precision=0, image_out=None, subset_tensor=None, gt=None, defer=None, deterministic=True,
+                    bins_status=None):
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
     its loss into `loss_accum` (float64 CUDA scalar).  With `defer` =
     (g9, rinv) device buffers the view's screen-space gradients are left
@@ -191,7 +192,7 @@ def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subs
                               render_opts(view.background, sub, extent_cutoff, precision, int(bool(deterministic)),
                                           gt_ready=ready,
                                           tile_hint=_tile_hint(view, model.device), defer=defer,
-                                          tile_order=_tile_order(view, model.device)),
+                                          tile_order=_tile_order(view, model.device), bins_status=bins_status),
                               _lib.ptr(gt), _lib.ptr(grad_accum), _lib.ptr(loss_accum), _lib.ptr(image_out), st))
     view.__dict__["_tile_order_valid"] = True
     return st
@@ -477,6 +478,18 @@ class StepWorkspace:
         self.losses = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._slots = None
         self._recv = None
+        # sync-free binning: [0] sticky overflow count, [1] largest pair count
+        # (ss_render_opts.bins_status); each step leaves a pinned snapshot
+        # checked two steps later (or at once when the loss is read)
+        self.bins_status = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self.pending = []
+        self._snaps = [torch.zeros(2, dtype=torch.int64).pin_memory() for _ in range(8)]
+        self._snap_i = 0
+
+    def flush(self):
+        """Check every pending step (re-running any that overflowed the
+        binning capacity); after this the model holds every step's update."""
+        _settle(self, keep=0)
 
     def prepare(self, grad_elems: int, n_views: int):
         import torch
@@ -588,7 +601,8 @@ class _DeviceKernels:
         else:
             defer = (g9[:self.n_in], rinv[:self.n_in])
         backward_device(self.dm, view, self.grad, self.ws.losses[i:i + 1], None, self.cutoff, 0, None,
-                        subset_tensor=self.sub, gt=self.gts[id(view)], defer=defer, deterministic=self.deterministic)
+                        subset_tensor=self.sub, gt=self.gts[id(view)], defer=defer, deterministic=self.deterministic,
+                        bins_status=self.ws.bins_status)
         if sharded_subset:
             rinv.fill_(-1)
             g9[self.sub] = tmp_g9
@@ -628,6 +642,7 @@ class _DeviceKernels:
         losses = self.ws.losses[:V]
         if coll is not None:  # each entry is non-zero on exactly one rank: the sum is exact
             coll.all_reduce_(losses)
+            coll.all_reduce_(self.ws.bins_status[:1], "max")  # any rank's binning overflow voids the step everywhere
         c = _lib.ctx(self.dm.device.index)
         c.check(c.lib.ss_sum_f64(c.handle, losses.data_ptr(), V, self.ws.loss.data_ptr()))
         return self.ws.loss
@@ -638,6 +653,7 @@ class _DeviceKernels:
             return
         c = _lib.ctx(self.dm.device.index)
         ast = st.adam_struct()
+        ast.skip_if = self.ws.bins_status.data_ptr()  # a step whose binning overflowed leaves the model alone
         if self.plan.world == 1:
             ms = self.dm.struct()
         else:
@@ -668,6 +684,14 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     (no host synchronisation).  `deterministic=False` selects the backward's
     throughput mode: per-(tile, splat) sums added with float atomics instead
     of the fixed-order partial sums (reruns may differ in the last bits).
+
+    The fp32 path bins without reading pair counts back (sync-free; see
+    ss_render_opts.bins_status): each step leaves a snapshot of its binning
+    status, checked when its loss is read or two steps later.  A step whose
+    pairs outgrew the capacity left the model untouched (its Adam is skipped
+    on the device, and every later step until the check); the check raises
+    the capacity and re-runs those steps in order, so the trajectory is the
+    same as without the capacity limit.
     """
     ready = [v for v in views if v.ready]
     if not ready:
@@ -679,24 +703,84 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
         raise ValueError("the optimizer state was created for a different process group")
     dm, uploaded = as_device(model)
     a = dm.active_count
-    plan = state.plan
     sub = _subset_tensor(index_subset, dm.device)
-    ws = workspace if workspace is not None else StepWorkspace(dm)
+    persistent = workspace is not None
+    ws = workspace if persistent else StepWorkspace(dm)
     if precision != 0:
-        if plan.world > 1:
+        if state.plan.world > 1:
             raise ValueError("the fp64 blend (precision=1) is single-GPU")
         loss = _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws, deterministic)
     else:
-        kern = _DeviceKernels(dm, state, ws, ready, sub, extent_cutoff, plan, deterministic)
-        kern.stage(parallel.shard_views(ready, plan.rank, plan.world) if plan.world > 1 else ready)
-        coll = parallel.Collectives(pg) if plan.world > 1 else None
-        loss = parallel.sharded_step(kern, ready, plan, coll, CHAIN_MAX_VIEWS)
+        _settle(ws, keep=1)  # the step before last: checked (and re-run after an overflow)
+        args = (dm, state, ready, sub, extent_cutoff, pg, deterministic)
+        loss = _step_binned(ws, *args)
+        _note(ws, args)
+        if sync_loss or not persistent:
+            loss.item()  # the device is idle after this: the check costs no extra wait
+            _settle(ws, keep=0)
+            loss = ws.loss
     if uploaded and a > 0:
         dm.write_back(model, TRAINABLE, rows=a)
     total = len(ready)
     if not sync_loss:
         return loss / total
     return float(loss.item()) / total
+
+
+def _step_binned(ws, dm, state, ready, sub, extent_cutoff, pg, deterministic):
+    plan = state.plan
+    kern = _DeviceKernels(dm, state, ws, ready, sub, extent_cutoff, plan, deterministic)
+    kern.stage(parallel.shard_views(ready, plan.rank, plan.world) if plan.world > 1 else ready)
+    coll = parallel.Collectives(pg) if plan.world > 1 else None
+    return parallel.sharded_step(kern, ready, plan, coll, CHAIN_MAX_VIEWS)
+
+
+def _note(ws, args):
+    """Snapshot this step's binning status into pinned memory (no wait)."""
+    import torch
+    snap = ws._snaps[ws._snap_i % len(ws._snaps)]  # a ring: at most 2 steps are pending
+    ws._snap_i += 1
+    snap.copy_(ws.bins_status, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    step_count_after = args[1].step_count
+    ws.pending.append((ev, snap, args, step_count_after))
+
+
+def _settle(ws, keep):
+    """Check the pending steps but the newest `keep`; after an overflow,
+    raise the pair capacity and re-run the voided steps in order."""
+    while len(ws.pending) > keep:
+        ev, snap, args, count_after = ws.pending[0]
+        ev.synchronize()
+        if int(snap[0]) == 0:
+            ws.pending.pop(0)
+            continue
+        _recover(ws)
+        return
+
+
+def _recover(ws):
+    """The oldest pending step overflowed its pair buffers (and every later
+    pending step was skipped on the device): grow, clear, re-run them all."""
+    import torch
+    torch.cuda.synchronize()
+    redo = ws.pending
+    ws.pending = []
+    st = ws.bins_status.cpu()
+    dev = redo[0][2][0].device
+    c = _lib.ctx(dev.index)
+    need = int(st[1])
+    c.lib.ss_pair_capacity(c.handle, need + need // 4 + 65536)
+    ws.bins_status.zero_()
+    state = redo[0][2][1]
+    # every pending step left the state alone: restart from the first one's count
+    state.step_count = redo[0][3] - 1
+    for _, _, args, _ in redo:
+        _step_binned(ws, *args)
+        _note(ws, args)
+    torch.cuda.synchronize()
+    _settle(ws, keep=0)
 
 
 def _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws, deterministic=True):

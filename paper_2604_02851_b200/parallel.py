@@ -103,9 +103,10 @@ class Collectives:
         if o is not out:
             out.copy_(o)
 
-    def all_reduce_(self, t):
+    def all_reduce_(self, t, op="sum"):
         s = self._staged(t)
-        self.dist.all_reduce(s, group=self.group)
+        self.dist.all_reduce(s, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM,
+                             group=self.group)
         if s is not t:
             t.copy_(s)
 

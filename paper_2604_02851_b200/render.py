@@ -86,9 +86,11 @@ def _subset_tensor(index_subset, device):
 
 
 def render_opts(background, subset, extent_cutoff, precision, deterministic=1, gt_ready=None,
-                tile_hint=None, defer=None, tile_order=None) -> _lib.SSRenderOpts:
+                tile_hint=None, defer=None, tile_order=None, bins_status=None) -> _lib.SSRenderOpts:
     o = _lib.SSRenderOpts()
     o.gt_ready = gt_ready
+    if bins_status is not None:  # sync-free binning (see ss_render_opts.bins_status)
+        o.bins_status = bins_status.data_ptr()
     if tile_order is not None:  # (buffer, valid): the backward's walk order, reused by the next forward
         o.tile_order, o.tile_order_valid = tile_order[0].data_ptr(), int(bool(tile_order[1]))
     if defer is not None:  # (g9, rinv) device buffers: the chain rule is deferred to ss_chain_views

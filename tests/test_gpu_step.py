@@ -168,3 +168,84 @@ def test_gpu_atomics_mode_matches_deterministic(degree):
         err = np.linalg.norm(a - b) / max(np.linalg.norm(a), 1e-30)
         assert err <= 1e-5, (k, err)
         assert np.linalg.norm(a) > 0
+
+
+@pytest.mark.parametrize("sync_loss", [False, True])
+def test_gpu_sync_free_binning_overflow_recovers(sync_loss):
+    """The step bins without reading pair counts back; a step whose pairs
+    outgrow the capacity is voided on the device (Adam skipped, sticky) and
+    re-run with a larger capacity when its status is checked -- the
+    trajectory is bit-identical to a run that never overflowed."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200 import _lib, synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
+    from paper_2604_02851_b200.render import render_device
+    W, H = 256, 160
+    host = synth.random_field(20_000, 2, W, H, seed=21)
+    tgt = DeviceModel.from_host(synth.target_model(host, seed=22), 0)
+    intr = synth.intrinsics(W, H)
+    light = synth.light()
+    poses = synth.ring_poses(3, radius=0.5)
+    views = [ReferenceView(p, intr, render_device(tgt, p, intr, light), light, np.zeros(3)) for p in poses]
+    c = _lib.ctx(0)
+
+    def run(cap):
+        dm = DeviceModel.from_host(host, 0)
+        state = OptimizerState(dm, scene_extent=2.0)
+        ws = StepWorkspace(dm)
+        losses = []
+        for i in range(4):
+            if cap is not None and i in (0, 2):
+                c.lib.ss_pair_capacity(c.handle, -cap)  # force an overflow at steps 0 and 2
+            L = step(dm, state, views, workspace=ws, sync_loss=sync_loss)
+            losses.append(float(L) if sync_loss else L)
+        ws.flush()
+        torch.cuda.synchronize()
+        return dm, state, ws
+
+    ref_dm, ref_state, _ = run(None)
+    dm, state, ws = run(1000)
+    assert state.step_count == ref_state.step_count == 4
+    for k in GROUPS:
+        assert torch.equal(getattr(dm, k), getattr(ref_dm, k)), k
+    np.testing.assert_array_equal(state.age, ref_state.age)
+    for k in GROUPS:
+        np.testing.assert_array_equal(state.m[k], ref_state.m[k])
+    assert int(ws.bins_status[0]) == 0 and not ws.pending
+    assert c.lib.ss_pair_capacity(c.handle, 0) > 1000
+
+
+def test_gpu_step_issues_no_host_sync():
+    """Once warmed up, optim.step (fp32 path, persistent workspace, device
+    loss) enqueues every view's binning, blending, the chain rule and Adam
+    without one host synchronisation (ss_host_syncs counts every stream sync,
+    read-back and scratch-arena growth the library issues)."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200 import _lib, synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
+    from paper_2604_02851_b200.render import render_device
+    W, H = 320, 192
+    host = synth.random_field(30_000, 3, W, H, seed=31)
+    tgt = DeviceModel.from_host(synth.target_model(host, seed=32), 0)
+    dm = DeviceModel.from_host(host, 0)
+    intr = synth.intrinsics(W, H)
+    light = synth.light()
+    views = [ReferenceView(p, intr, render_device(tgt, p, intr, light), light, np.zeros(3))
+             for p in synth.ring_poses(4, radius=0.5)]
+    state = OptimizerState(dm, scene_extent=2.0)
+    ws = StepWorkspace(dm)
+    for _ in range(3):
+        step(dm, state, views, workspace=ws, sync_loss=False)
+    ws.flush()
+    torch.cuda.synchronize()
+    c = _lib.ctx(0)
+    before = c.lib.ss_host_syncs(c.handle)
+    for _ in range(4):
+        step(dm, state, views, workspace=ws, sync_loss=False)
+    assert c.lib.ss_host_syncs(c.handle) == before
+    ws.flush()
+    assert state.step_count == 7
