@@ -120,6 +120,7 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 // 1-bit LSB-first of (v >= 0.5): one byte per 8 elements
 template <typename T>
 __global__ void k_abs_pack1(const T* __restrict__ x, int64_t n, uint8_t* __restrict__ block) {
+    SS_PDL_WAIT();
     const int64_t nbytes = (n + 7) / 8;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nbytes; j += (int64_t)gridDim.x * blockDim.x) {
         uint8_t b = 0;
@@ -144,6 +145,7 @@ struct SnapState {
 };
 
 __global__ void k_aabb(const float* __restrict__ means, int64_t n, SnapState* st) {
+    SS_PDL_WAIT();
     uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0, 0, 0};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -173,6 +175,7 @@ __global__ void k_aabb(const float* __restrict__ means, int64_t n, SnapState* st
 }
 
 __global__ void k_snap_init(SnapState* st) {
+    SS_PDL_WAIT();
     for (int a = 0; a < 3; ++a) {
         st->lo_ord[a] = 0xffffffffu;
         st->hi_ord[a] = 0u;
@@ -192,18 +195,20 @@ __device__ __forceinline__ void aabb_of(const SnapState* st, int64_t n, double l
     }
 }
 
-__global__ void k_snap_rows(ss_model m, SnapLayout L, const SnapState* st, uint8_t* __restrict__ blk,
-                            float* __restrict__ base_means, float* __restrict__ base_ls) {
+__device__ __forceinline__ void snap_rows(const ss_model& m, const SnapLayout& L, const SnapState* st,
+                                          uint8_t* __restrict__ blk, float* __restrict__ base_means,
+                                          float* __restrict__ base_ls, uint32_t* __restrict__ id_lens, int bid, int nblk) {
     double lo[3], hi[3];
     aabb_of(st, L.n, lo, hi);
     const QSpec qls = qspec(A_LS);  // the power-of-two spans go through quantize_p2
     const int B = L.B;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t stride = (int64_t)nblk * blockDim.x;
     // loop bound rounded up to whole warps so the visibility ballot is convergent
     const int64_t nw = (L.n + 31) & ~int64_t(31);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += stride) {
+    for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < nw; i += stride) {
         const bool ok = i < L.n;
         if (ok) {
+            id_lens[i] = varint_len((uint64_t)(int64_t)m.object_ids[i]);
             for (int a = 0; a < 3; ++a) {
                 uint32_t c = quantize((double)m.means[i * 3 + a], lo[a], hi[a], 16);
                 put_code(blk + L.off_means + (i * 3 + a) * 2, c, 16);
@@ -217,9 +222,7 @@ __global__ void k_snap_rows(ss_model m, SnapLayout L, const SnapState* st, uint8
                 w |= (uint64_t)quantize_p2(m.quaternions[i * 4 + j], -1.f, 1.f, 1023.0 / 2.0) << (10 * j);
             for (int b = 0; b < 5; ++b) blk[L.off_quat + i * 5 + b] = (uint8_t)(w >> (8 * b));
             blk[L.off_opac + i] = (uint8_t)quantize_p2(m.logit_opacities[i], -8.f, 8.f, 255.0 / 16.0);
-            const float* sh = m.sh_coeffs + i * 3 * B;
-            for (int c = 0; c < 3; ++c)  // the SH rest bytes: k_snap_rest, element-parallel
-                blk[L.off_dc + i * 3 + c] = (uint8_t)quantize_p2(sh[c * B], -4.f, 4.f, 255.0 / 8.0);
+            // SH DC and rest: k_snap_sh, element-parallel over the coefficient rows
         }
         unsigned bal = __ballot_sync(0xffffffffu, ok && m.light_visibility[ok ? i : 0] >= 0.5f);
         if ((threadIdx.x & 31) == 0) {
@@ -231,37 +234,71 @@ __global__ void k_snap_rows(ss_model m, SnapLayout L, const SnapState* st, uint8
     }
 }
 
-// SH rest section, one thread per output byte (coalesced reads of the
-// coefficient rows, coalesced byte stores): 3 (B - 1) codes per row
+// SH sections, read once in coefficient order (coalesced float4 loads when a
+// channel's B coefficients are a multiple of 4): DC (u8 over [-4, 4]) into
+// the DC section, the rest (u8 over [-1, 1]) into the rest section
 template <int B>
-__global__ void k_snap_rest(const float* __restrict__ sh, int64_t n, uint8_t* __restrict__ dst) {
-    constexpr uint32_t per = 3u * (uint32_t)(B - 1);  // compile-time divisors: multiply + shift
+__device__ __forceinline__ void snap_sh(const float* __restrict__ sh, int64_t n, uint8_t* __restrict__ dc,
+                                        uint8_t* __restrict__ rest, int bid, int nblk) {
+    constexpr uint32_t per = 3u * (uint32_t)B;  // compile-time divisors: multiply + shift
+    constexpr int V = (B % 4 == 0) ? 4 : 1;     // coefficients per thread step
     // rows in blocks of 2^20 keep the index arithmetic in 32 bits
     for (int64_t r0 = 0; r0 < n; r0 += 1 << 20) {
         const uint32_t rows = (uint32_t)min((int64_t)1 << 20, n - r0);
-        const uint32_t total = rows * per;
-        const float* src = sh + r0 * 3 * B;
-        uint8_t* out = dst + r0 * per;
-        for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-            const uint32_t i = e / per, r = e - i * per, c = r / (uint32_t)(B - 1), b = r - c * (uint32_t)(B - 1) + 1;
-            out[e] = (uint8_t)quantize_p2(__ldg(&src[((uint64_t)i * 3 + c) * B + b]), -1.f, 1.f, 255.0 / 2.0);
+        const uint32_t total = rows * per / V;
+        const float* src = sh + r0 * per;
+        uint8_t* dcr = dc + r0 * 3;
+        uint8_t* rr = rest + r0 * (per - 3);
+        for (uint32_t e = bid * blockDim.x + threadIdx.x; e < total; e += nblk * blockDim.x) {
+            const uint32_t f = e * V, i = f / per, r = f - i * per, c = r / (uint32_t)B, b = r - c * (uint32_t)B;
+            float v[V];
+            if constexpr (V == 4) {
+                const float4 q = __ldcs(reinterpret_cast<const float4*>(src) + e);
+                v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+            } else {
+                v[0] = __ldcs(&src[e]);
+            }
+            uint8_t* o = rr + i * (per - 3) + c * (B - 1) + b - 1;  // rest byte of coefficient b (b >= 1)
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                if (b + k == 0)
+                    dcr[i * 3 + c] = (uint8_t)quantize_p2(v[k], -4.f, 4.f, 255.0 / 8.0);
+                else
+                    o[k] = (uint8_t)quantize_p2(v[k], -1.f, 1.f, 255.0 / 2.0);
+            }
         }
     }
 }
 
+// The row sections (+ object-id varint lengths) and the SH sections in ONE
+// launch: blocks alternate 2 : 3 between the fp64-heavy row work and the
+// streaming SH work, so both run side by side on every SM.
+template <int B>
+__global__ void __launch_bounds__(256) k_snap_body(ss_model m, SnapLayout L, const SnapState* st,
+                                                   uint8_t* __restrict__ blk, float* __restrict__ base_means,
+                                                   float* __restrict__ base_ls, uint32_t* __restrict__ id_lens) {
+    SS_PDL_WAIT();
+    const int b = blockIdx.x, g = gridDim.x / 5;
+    if (b % 5 < 2) snap_rows(m, L, st, blk, base_means, base_ls, id_lens, (b / 5) * 2 + b % 5, 2 * g);
+    else snap_sh<B>(m.sh_coeffs, L.n, blk + L.off_dc, blk + L.off_rest, (b / 5) * 3 + b % 5 - 2, 3 * g);
+}
+
 __global__ void k_snap_id_lens(const int32_t* __restrict__ ids, int64_t n, uint32_t* __restrict__ lens) {
+    SS_PDL_WAIT();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         lens[i] = varint_len((uint64_t)(int64_t)ids[i]);
 }
 
 __global__ void k_snap_id_write(const int32_t* __restrict__ ids, int64_t n, const uint64_t* __restrict__ off,
                                 uint8_t* __restrict__ dst) {
+    SS_PDL_WAIT();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         varint_put(dst + off[i], (uint64_t)(int64_t)ids[i]);
 }
 
 __global__ void k_snap_header(const SnapState* st, int64_t n, int active, int degree, int profile,
                               uint64_t fixed_len, const uint64_t* var_len, uint8_t* out, uint64_t* out_len) {
+    SS_PDL_WAIT();
     double lo[3], hi[3];
     aabb_of(st, n, lo, hi);
     put_u32(out, (uint32_t)n);
@@ -330,8 +367,8 @@ int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t*
     const int B = (m->sh_degree + 1) * (m->sh_degree + 1);
     SnapState* st = SS_SCRATCH(ctx, SnapState, 1);
     if (!st) return SS_ERR_CUDA;
-    k_snap_init<<<1, 1, 0, s>>>(st);
-    if (n) k_aabb<<<grid_for(ctx, n), 256, 0, s>>>(m->means, n, st);
+    SS_CUDA(ctx, ss_launch((k_snap_init), dim3(1), dim3(1), 0, s, st));
+    if (n) SS_CUDA(ctx, ss_launch((k_aabb), dim3(grid_for(ctx, n)), dim3(256), 0, s, (const float*)m->means, n, st));
     SS_CHECK_LAUNCH(ctx);
     uint8_t* blk = out + 40;
     if (profile == 1) {
@@ -345,7 +382,7 @@ int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t*
         }
         if (base_means && n) SS_CUDA(ctx, cudaMemcpyAsync(base_means, m->means, 12ull * n, cudaMemcpyDeviceToDevice, s));
         if (base_ls && n) SS_CUDA(ctx, cudaMemcpyAsync(base_ls, m->log_scales, 12ull * n, cudaMemcpyDeviceToDevice, s));
-        k_snap_header<<<1, 1, 0, s>>>(st, n, m->active_count, m->sh_degree, 1, o, nullptr, out, out_len);
+        SS_CUDA(ctx, ss_launch((k_snap_header), dim3(1), dim3(1), 0, s, (const SnapState*)st, n, m->active_count, m->sh_degree, 1, (uint64_t)o, (const uint64_t*)nullptr, out, out_len));
         SS_CHECK_LAUNCH(ctx);
         return SS_OK;
     }
@@ -365,24 +402,23 @@ int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t*
     uint64_t* vtot = SS_SCRATCH(ctx, uint64_t, 1);
     if (!lens || !offs || !vtot) return SS_ERR_CUDA;
     if (n) {
-        k_snap_rows<<<grid_for(ctx, n), 256, 0, s>>>(*m, L, st, blk, base_means, base_ls);
-        SS_CHECK_LAUNCH(ctx);
-        if (B > 1) {
-            const int g = grid_for(ctx, n * 3 * (B - 1));
-            if (B == 4) k_snap_rest<4><<<g, 256, 0, s>>>(m->sh_coeffs, n, blk + L.off_rest);
-            else if (B == 9) k_snap_rest<9><<<g, 256, 0, s>>>(m->sh_coeffs, n, blk + L.off_rest);
-            else k_snap_rest<16><<<g, 256, 0, s>>>(m->sh_coeffs, n, blk + L.off_rest);
-            SS_CHECK_LAUNCH(ctx);
-        }
-        k_snap_id_lens<<<grid_for(ctx, n), 256, 0, s>>>(m->object_ids, n, lens);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_snap_body<16>, 256, 0);
+        int64_t g = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 4);
+        g = (g / 5) * 5;  // whole 2 : 3 groups
+        if (g < 5) g = 5;
+        if (B == 1) SS_CUDA(ctx, ss_launch((k_snap_body<1>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
+        else if (B == 4) SS_CUDA(ctx, ss_launch((k_snap_body<4>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
+        else if (B == 9) SS_CUDA(ctx, ss_launch((k_snap_body<9>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
+        else SS_CUDA(ctx, ss_launch((k_snap_body<16>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
         SS_CHECK_LAUNCH(ctx);
     }
     SS_TRY(ss_scan_u32_to_u64(ctx, lens, offs, n, vtot));
     if (n) {
-        k_snap_id_write<<<grid_for(ctx, n), 256, 0, s>>>(m->object_ids, n, offs, blk + L.off_ids);
+        SS_CUDA(ctx, ss_launch((k_snap_id_write), dim3(grid_for(ctx, n)), dim3(256), 0, s, (const int32_t*)m->object_ids, n, (const uint64_t*)offs, blk + L.off_ids));
         SS_CHECK_LAUNCH(ctx);
     }
-    k_snap_header<<<1, 1, 0, s>>>(st, n, m->active_count, m->sh_degree, 0, L.off_ids, vtot, out, out_len);
+    SS_CUDA(ctx, ss_launch((k_snap_header), dim3(1), dim3(1), 0, s, (const SnapState*)st, n, m->active_count, m->sh_degree, 0, (uint64_t)L.off_ids, (const uint64_t*)vtot, out, out_len));
     SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }

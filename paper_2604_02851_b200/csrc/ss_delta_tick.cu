@@ -14,6 +14,8 @@
 //   residual emits  wait for their job's flag, then dense quantize, or sparse
 //                   varint gaps + codes; advanced baseline f32(f64(base) + deq)
 //
+// (TK_ORDER 1 runs the residual emits before the absolute jobs instead, so
+// an emit re-reads its chunk's cur / base while they are still in L2.)
 // A block's role is its ticket from an atomic counter taken when it starts
 // (not blockIdx.x, whose dispatch order CUDA does not guarantee): every scan
 // block an emit block waits for holds a smaller ticket, so it has already
@@ -852,22 +854,31 @@ __device__ __forceinline__ void scan_chunk(const Job& J, int64_t c) {
 // one launch: [residual scans][absolute jobs][residual emits]; the emit
 // blocks are dispatched after every scan block and wait on their job's plan
 // flag (the absolute jobs in between cover the plan tail)
-__global__ void __launch_bounds__(TK_THREADS, TK_EMIT_MINB) k_tick_fused(Batch B, int64_t scan_chunks,
+#ifndef TK_ORDER
+#define TK_ORDER 1  // 1: [scans][emits][absolute]; 0: [scans][absolute][emits]
+#endif
+__global__ void __launch_bounds__(TK_THREADS, TK_EMIT_MINB) k_tick_fused(Batch B, int64_t res_chunks, int64_t abs_chunks,
                                                                           unsigned* __restrict__ ticket) {
     SS_PDL_WAIT();
     __shared__ unsigned s_ticket;
     if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1u);
     __syncthreads();
     const int64_t b = s_ticket;
-    if (b < scan_chunks) {
-        const Job& J = B.j[find_job(B, b)];
-        scan_chunk(J, b - J.chunk0);
+    // global chunk ids: residual jobs [0, res_chunks), absolute [res_chunks, res_chunks + abs_chunks)
+    int64_t scan = -1, emit = -1;
+    if (b < res_chunks) scan = b;
+    else if (TK_ORDER == 1 && b < 2 * res_chunks) emit = b - res_chunks;
+    else if (TK_ORDER == 1) scan = b - res_chunks;  // absolute chunk res_chunks + (b - 2 res_chunks)
+    else if (b < res_chunks + abs_chunks) scan = b;
+    else emit = b - res_chunks - abs_chunks;
+    if (scan >= 0) {
+        const Job& J = B.j[find_job(B, scan)];
+        scan_chunk(J, scan - J.chunk0);
         return;
     }
-    const int64_t chunk = b - scan_chunks;
-    const Job& J = B.j[find_job(B, chunk)];
+    const Job& J = B.j[find_job(B, emit)];
     wait_planned(J);
-    emit_chunk(J, chunk - J.chunk0);
+    emit_chunk(J, emit - J.chunk0);
 }
 
 }  // namespace
@@ -974,7 +985,7 @@ extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int3
         if (!ticket) return SS_ERR_CUDA;
         SS_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(unsigned), ctx->stream));
         SS_CUDA(ctx, ss_launch((k_tick_fused), dim3((unsigned)(2 * res_chunks + abs_chunks)), dim3(TK_THREADS), 0, ctx->stream, B,
-                               res_chunks + abs_chunks, ticket));
+                               res_chunks, abs_chunks, ticket));
         SS_CHECK_LAUNCH(ctx);
     }
     // jobs with zero rows and no chunk still need their header
