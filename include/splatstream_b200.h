@@ -357,6 +357,12 @@ typedef struct {
 } ss_ortho_camera;
 int ss_update_light_visibility(ss_ctx* ctx, ss_model* model, const double* depth_map,
                                const ss_ortho_camera* cam, double bias);
+/* As ss_update_light_visibility, and *changed (device int32, set by the
+ * caller to 0) becomes 1 if any row's bit flipped -- the server's "send the
+ * LightVisibility packet" test (ref server.py:406-409) without copying the
+ * vector to the host. */
+int ss_update_light_visibility_changed(ss_ctx* ctx, ss_model* model, const double* depth_map,
+                                       const ss_ortho_camera* light_cam, double bias, int32_t* changed);
 
 /* ObjectRegistry.apply_transform(): ref model.py:557-572.  Rewrites the rows
  * with object_ids == object_id from their local poses (device f64 arrays

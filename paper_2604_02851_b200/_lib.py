@@ -180,6 +180,7 @@ _SIGS = {
     "ss_crc32": (i32, [vp, vp, vp, u64, vp]),
     "ss_crc32_combine": (C.c_uint32, [C.c_uint32, C.c_uint32, u64]),
     "ss_update_light_visibility": (i32, [vp, C.POINTER(SSModel), vp, C.POINTER(SSOrthoCamera), f64]),
+    "ss_update_light_visibility_changed": (i32, [vp, C.POINTER(SSModel), vp, C.POINTER(SSOrthoCamera), f64, vp]),
     "ss_apply_object_transform": (i32, [vp, C.POINTER(SSModel), i32, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
     "ss_refresh_object_locals": (i32, [vp, C.POINTER(SSModel), i32, i32, vp, vp, C.POINTER(f64),
                                        C.POINTER(f64)]),

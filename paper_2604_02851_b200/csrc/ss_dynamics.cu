@@ -10,8 +10,14 @@
 namespace {
 
 __global__ void k_light_vis(const float* __restrict__ means, int64_t n, const double* __restrict__ depth,
-                            ss_ortho_camera cam, double bias, float* __restrict__ vis) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+                            ss_ortho_camera cam, double bias, float* __restrict__ vis, int32_t* __restrict__ changed) {
+    // rounded up to whole warps so the change ballot is convergent
+    const int64_t nw = (n + 31) & ~int64_t(31);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i >= n) {
+            if (changed) __ballot_sync(0xffffffffu, false);
+            continue;
+        }
         double d[3];
         for (int k = 0; k < 3; ++k) d[k] = ds((double)means[3 * i + k], cam.position[k]);
         double pc[3];
@@ -23,6 +29,10 @@ __global__ void k_light_vis(const float* __restrict__ means, int64_t n, const do
         const bool inside = fu >= 0.0 && fu < (double)cam.width && fv >= 0.0 && fv < (double)cam.height && pc[2] >= 0.0;
         float out = 1.0f;
         if (inside) out = pc[2] <= da(depth[(int64_t)fv * cam.width + (int64_t)fu], bias) ? 1.0f : 0.0f;
+        if (changed) {  // ref server.py:406-409: the packet goes out only when a bit flips
+            const unsigned diff = __ballot_sync(0xffffffffu, vis[i] != out);
+            if (diff && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
+        }
         vis[i] = out;
     }
 }
@@ -96,13 +106,18 @@ inline int gridn(ss_ctx* ctx, int64_t n) {
 
 extern "C" {
 
-int ss_update_light_visibility(ss_ctx* ctx, ss_model* m, const double* depth, const ss_ortho_camera* cam, double bias) {
+int ss_update_light_visibility_changed(ss_ctx* ctx, ss_model* m, const double* depth, const ss_ortho_camera* cam,
+                                       double bias, int32_t* changed) {
     if (!ctx || !m || !depth || !cam) return SS_ERR_INVALID;
     if (m->count == 0) return SS_OK;
     k_light_vis<<<gridn(ctx, m->count), 256, 0, ctx->stream>>>(m->means, m->count, depth, *cam, bias,
-                                                              m->light_visibility);
+                                                              m->light_visibility, changed);
     SS_CHECK_LAUNCH(ctx);
     return SS_OK;
+}
+
+int ss_update_light_visibility(ss_ctx* ctx, ss_model* m, const double* depth, const ss_ortho_camera* cam, double bias) {
+    return ss_update_light_visibility_changed(ctx, m, depth, cam, bias, nullptr);
 }
 
 int ss_apply_object_transform(ss_ctx* ctx, ss_model* m, int32_t oid, const double* lm, const double* lr,

@@ -288,8 +288,10 @@ def tile_bins(model, pose, intr, index_subset=None, extent_cutoff=True):
     return r[r >= 0], ranges.cpu().numpy(), ranks.cpu().numpy()[:P]
 
 
-def update_light_visibility(model, depth_map, light_cam, bias: float = 0.02) -> None:
-    """ref render.py:350 -- writes model.light_visibility (replaced for host models)."""
+def update_light_visibility(model, depth_map, light_cam, bias: float = 0.02, changed=None) -> None:
+    """ref render.py:350 -- writes model.light_visibility (replaced for host models).
+    `changed`: optional device int32 tensor (zeroed by the caller) set to 1 when
+    any bit flipped -- the server's packet test (ref server.py:406-409) on the device."""
     import torch
     dm, uploaded = as_device(model)
     if dm.count == 0:
@@ -304,6 +306,7 @@ def update_light_visibility(model, depth_map, light_cam, bias: float = 0.02) -> 
     depth = depth_map if isinstance(depth_map, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(depth_map, np.float64))
     depth = depth.to(dm.device, torch.float64).contiguous()
-    c.check(c.lib.ss_update_light_visibility(c.handle, dm.struct(), _lib.ptr(depth), cam, float(bias)))
+    c.check(c.lib.ss_update_light_visibility_changed(c.handle, dm.struct(), _lib.ptr(depth), cam, float(bias),
+                                                     _lib.ptr(changed)))
     if uploaded:
         model.light_visibility = dm.light_visibility.cpu().numpy().astype(np.float32)

@@ -42,3 +42,32 @@ def test_gpu_dynamics(c):
         out = dm.to_host()
         np.testing.assert_allclose(out.means, c.a("out_means"), rtol=2e-7, atol=1e-7)
         np.testing.assert_allclose(out.quaternions, c.a("out_quats"), rtol=0, atol=2e-7)
+
+
+def test_gpu_light_visibility_change_flag():
+    """ref server.py:406-409 on the device: the flag is set exactly when a
+    visibility bit flips (against the values before the update)."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200.geometry import OrthoCamera, Pose
+    from paper_2604_02851_b200.model import DeviceModel, GaussianModel
+    from paper_2604_02851_b200.render import update_light_visibility
+    c = [x for x in DYN if x["kind"] == "lightvis" and x["n"] == 1000][0]
+    n = c["n"]
+    m = GaussianModel(c.a("means").copy(), np.zeros((n, 3), np.float32), np.tile(np.float32([1, 0, 0, 0]), (n, 1)),
+                      np.zeros(n, np.float32), np.zeros((n, 3, 1), np.float32), np.zeros(n, np.float32),
+                      np.zeros(n, np.int32), n, 0)
+    dm = DeviceModel.from_host(m)
+    cam = OrthoCamera(Pose(c.a("cam_pos"), c.a("cam_quat")), c["half_width"], c["half_height"], c["width"],
+                      c["height"], 20.0)
+    depth = torch.from_numpy(np.array(c.a("depth"))).cuda()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    update_light_visibility(dm, depth, cam, c["bias"], changed=flag)  # from all-zero: bits flip
+    assert int(flag.item()) == 1
+    np.testing.assert_array_equal(dm.light_visibility.cpu().numpy(), c.a("vis"))
+    flag.zero_()
+    update_light_visibility(dm, depth, cam, c["bias"], changed=flag)  # same light: no change
+    assert int(flag.item()) == 0
+    dm.light_visibility[n // 2] = 1.0 - dm.light_visibility[n // 2]  # one row differs from what the map gives
+    update_light_visibility(dm, depth, cam, c["bias"], changed=flag)
+    assert int(flag.item()) == 1
