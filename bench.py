@@ -384,6 +384,12 @@ def run_ours(args):
         enc = encoder_bench(c, _lib, args, torch)
         enc["snapshot"] = snapshot_bench(dm, torch)
 
+    # ---- BASELINE configs 2 and 4 (rank 0, after the timed runs)
+    config2 = config4 = None
+    if extras:
+        config2 = config2_bench(args, dev, torch)
+        config4 = {f"sh{d}": config4_bench(args, dev, torch, degree=d) for d in (1, 3)}
+
     # ---- pool maintenance of this model, rank 0
     pool_rec = zlib_rec = engine_rec = None
     if extras:
@@ -470,6 +476,8 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(model_h, tgt_h, poses, intr, light)
+        if not args.step_only:
+            cpu["encoders"] = cpu_encoder_baseline(args)
 
     out = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -477,13 +485,173 @@ def run_ours(args):
            "config": workload_config(args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
            "gpu_launches": launches, "clocks": clock_rec,
            "kernel_ms_per_step": {k: round(v, 4) for k, v in per_step.items()},
-           "atomics_mode": atomics,
+           "atomics_mode": atomics, "config2": config2, "config4": config4,
            "evaluated_pairs_per_view": evals_per_view,
            "delta_encode": enc, "pool_maintenance": pool_rec, "server_tick_zlib": zlib_rec, "engine": engine_rec, "client_render": client_rec, "fp32_peak_tflops_measured": fp32_peak,
            "precision": "fp64 preprocess/windows/depth keys, fp32 blend + chain rule, fp64 Adam moments"}
     print(json.dumps(out), flush=True)
     if pg is not None:
         dist.destroy_process_group()
+
+
+def config2_bench(args, dev, torch, n=500_000, n_views=4, ticks=30):
+    """BASELINE config 2: 500k Gaussians, SH degree 3, 4 views of
+    1920x1080 per step, single GPU, each server tick = one optimizer step +
+    the deltas due per DEFAULT_DELTA_PERIODS (ref server.py:57-64; raw,
+    compression_id 0), the baselines reset from the decoded snapshot first.
+    30 ticks cover every period.  Device time with CUDA events."""
+    from paper_2604_02851_b200 import _lib, synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
+    from paper_2604_02851_b200.protocol import DeltaTicker, PayloadBuffer, encode_snapshot_device
+    from paper_2604_02851_b200.render import render_device
+    host = synth.random_field(n, 3, args.width, args.height, seed=5)
+    dm = DeviceModel.from_host(host, dev.index)
+    tgt = DeviceModel.from_host(synth.target_model(host, seed=6), dev.index)
+    poses = synth.ring_poses(n_views)
+    intr = synth.intrinsics(args.width, args.height)
+    light = synth.light()
+    bg = np.array([0.05, 0.05, 0.08])
+    views = [ReferenceView(p, intr, render_device(tgt, p, intr, light, background=bg), light, bg) for p in poses]
+    del tgt
+    lo, hi = host.means.min(0), host.means.max(0)
+    state = OptimizerState(dm, scene_extent=float(np.linalg.norm(hi - lo) / 2))
+    ws = StepWorkspace(dm)
+    bm = torch.empty((dm.count, 3), dtype=torch.float32, device=dev)
+    bl = torch.empty((dm.count, 3), dtype=torch.float32, device=dev)
+    encode_snapshot_device(dm, 0, None, bm, bl)
+    a = dm.active_count
+    ticker = DeltaTicker(dm, {0: bm[:a], 1: bl[:a]}, {k: PayloadBuffer(1 << 20, dev) for k in range(7)})
+
+    def tick(i):
+        step(dm, state, views, workspace=ws, sync_loss=False)
+        due = [attr for attr in DELTA_ORDER if i % DELTA_PERIODS[attr] == 0]
+        ticker(due)
+        return a * len(due)
+
+    for i in range(3):
+        tick(i)
+    ws.flush()
+    torch.cuda.synchronize()
+    c = _lib.ctx(dev.index)
+    _lib.set_timing(c, True)
+    _lib.get_timing(c, reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rows = sum(tick(i) for i in range(ticks))
+    e1.record()
+    torch.cuda.synchronize()
+    kt, _ = _lib.get_timing(c, reset=True)
+    _lib.set_timing(c, False)
+    ws.flush()
+    ms = e0.elapsed_time(e1)
+    enc_ms = kt["encoders"][0]
+    return {"workload": f"config2: {n} Gaussians SH3, {n_views} views {args.width}x{args.height} per step, 1 GPU, "
+                        "one step + the due deltas per tick (DEFAULT_DELTA_PERIODS, raw)",
+            "views_per_s": n_views * ticks / (ms / 1e3), "tick_ms": ms / ticks, "ticks": ticks,
+            "delta_rows_per_tick": rows / ticks, "encoder_ms_per_tick": enc_ms / ticks,
+            "encoder_gaussians_per_s": rows / (enc_ms / 1e3) if enc_ms > 0 else None,
+            "note": "device time (CUDA events) over the ticks; encoder = the batched delta launch's own time"}
+
+
+def config4_bench(args, dev, torch, n=2_000_000, degree=1, ticks=60):
+    """BASELINE config 4: a 60 Hz dynamic tick over a 2M-row
+    model (SH degree 1 as config_dynamics, and a degree-3 variant), 20 % of
+    the rows on 3 rigid objects moving at t = tick/60 (rotation + bounce /
+    oscillation), the light yawing at 60 deg/s, optimizer off.  Per tick, all
+    on the device: the rigid transforms (ref model.py:389-404), the light
+    camera's 1024x1024 ortho depth of the engine scene (ref engine.py:200-219),
+    light visibility with the device change flag (ref render.py:350-368,
+    server.py:406-409) and, when it flipped, the LightVisibility packet, then
+    every due delta (ref server.py:488-493; raw, compression_id 0).  The
+    moved rows exceed the gate and go out as sparse means residuals
+    (SURVEY §8d).  Reported: the device time per tick against the 16.7 ms
+    budget, the wall clock per tick including the host read of the change
+    flag and of the tick's payloads (pinned), and rows encoded per second."""
+    import math as _m
+    from paper_2604_02851_b200 import engine, synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.objects import ObjectRegistry
+    from paper_2604_02851_b200.protocol import DeltaTicker, PayloadBuffer, encode_light_visibility_device
+    from paper_2604_02851_b200.render import update_light_visibility
+    from paper_2604_02851_b200.scene import scene_from_dict
+    host = synth.random_field(n, degree, args.width, args.height, seed=9, object_fraction=0.2)
+    dm = DeviceModel.from_host(host, dev.index)
+    reg = ObjectRegistry(dev.index)
+    for oid in (1, 2, 3):
+        reg.set_transform(oid, np.array([1.0, 0.0, 0.0, 0.0]), np.zeros(3))
+    reg.refresh_locals(dm)
+    scene = scene_from_dict(ENGINE_SCENE)
+    lo, hi = host.means.min(0) - 0.25, host.means.max(0) + 0.25
+    a = dm.active_count
+    base_m, base_l = dm.means.clone(), dm.log_scales.clone()
+    ticker = DeltaTicker(dm, {0: base_m[:a], 1: base_l[:a]}, {k: PayloadBuffer(1 << 20, dev) for k in range(7)})
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    vis_out = PayloadBuffer(4 + (n + 7) // 8, dev)
+    pinned = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+
+    def transforms(t):
+        out = {}
+        for k, oid in enumerate((1, 2, 3)):
+            ang = (0.5 + 0.3 * k) * t
+            ax = np.array([0.0, 1.0, 0.2 * k])
+            ax = ax / np.linalg.norm(ax)
+            q = np.concatenate([[_m.cos(ang / 2)], _m.sin(ang / 2) * ax])
+            tr = np.array([0.3 * _m.sin(2.0 * t + k), abs(_m.sin(3.0 * t + k)) * 0.2, 0.1 * _m.cos(t + k)])
+            out[oid] = (q, tr)
+        return out
+
+    def tick(i, read):
+        t = i / 60.0
+        for oid, (q, tr) in transforms(t).items():
+            reg.apply_transform(dm, oid, q, tr, return_rows=False)
+        yaw = _m.radians(60.0) * t
+        d = np.array([0.3 * _m.cos(yaw) - 0.2 * _m.sin(yaw), -1.0, 0.3 * _m.sin(yaw) + 0.2 * _m.cos(yaw)])
+        lcam = engine.build_light_camera(lo, hi, d / np.linalg.norm(d), 1024)
+        depth = engine.render_ortho_depth(scene, lcam, as_tensor=True)
+        flag.zero_()
+        update_light_visibility(dm, depth, lcam, changed=flag)
+        encode_light_visibility_device(dm.light_visibility, vis_out)
+        due = [attr for attr in DELTA_ORDER if i % DELTA_PERIODS[attr] == 0 and not (attr == 5 and degree == 0)]
+        ticker(due)
+        nbytes = 0
+        if read:  # the server's host side: the change flag, then the frames' bytes
+            sent_vis = bool(flag.item())
+            lens = [int(ticker.outs[k].length.item()) for k in due]
+            off = 0
+            for k, ln in zip(due, lens):
+                pinned[off:off + ln].copy_(ticker.outs[k].data[:ln], non_blocking=True)
+                off += ln
+            if sent_vis:
+                ln = int(vis_out.length.item())
+                pinned[off:off + ln].copy_(vis_out.data[:ln], non_blocking=True)
+                off += ln
+            torch.cuda.current_stream().synchronize()
+            nbytes = off
+        return a * len(due), nbytes
+
+    for i in range(3):
+        tick(i, True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rows = sum(tick(3 + i, False)[0] for i in range(ticks))
+    e1.record()
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1) / ticks
+    wall, nb = [], 0
+    for i in range(ticks):
+        w0 = time.perf_counter()
+        _, b = tick(3 + ticks + i, True)
+        wall.append((time.perf_counter() - w0) * 1e3)
+        nb += b
+    return {"workload": f"config4: {n} rows SH{degree}, 20 % on 3 rigid objects, light yaw 60 deg/s, 1024^2 light "
+                        "depth, 60 Hz tick (transforms + light visibility + packet + due deltas, raw), optimizer off",
+            "tick_ms_device": dev_ms, "tick_ms_wall_p50": float(np.median(wall)), "tick_ms_wall_max": float(max(wall)),
+            "budget_ms": 1000.0 / 60.0, "within_budget": float(np.median(wall)) <= 1000.0 / 60.0,
+            "rows_encoded_per_s": rows / (dev_ms * ticks / 1e3), "bytes_per_tick": nb / ticks,
+            "note": "device time per tick (CUDA events, no host reads) and wall clock per tick with the host "
+                    "reading the change flag and the payload bytes into pinned memory"}
 
 
 def atomics_bench(args, dm, state, views, ws, pg, dev, delta_tick, torch, steps=None):
@@ -929,6 +1097,35 @@ def roofline(dom, per_step, kt, counters, args, local_views, fp32_peak):
                 "hbm_peak_gbs": hbm, "ncu": _committed(dom).get("ncu")}
     return {"bound": "hbm", "kernel": dom, "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
             "traffic": None, "ms_per_launch": ms_launch}
+
+
+def cpu_encoder_baseline(args):
+    """The oracle port of the encoders on one host core, full size (SURVEY
+    §8d): the per-frame delta set of bench.py's encoder workload (2M rows
+    SH1: dense means / log-scale residuals, opacity, DC; raw) and the
+    profile-0 snapshot of the 1M-row SH3 model (raw)."""
+    from oracle import codec as oc
+    from paper_2604_02851_b200 import synth
+    m = synth.random_field(2 * args.n, 1, args.width, args.height, seed=3)
+    a = m.active_count
+    base_m, base_l = m.means - np.float32(2e-3), m.log_scales - np.float32(2e-3)
+    t0 = time.perf_counter()
+    oc.delta_payload(0, m.means[:a], base_m[:a], None, 0)
+    oc.delta_payload(1, m.log_scales[:a], base_l[:a], None, 0)
+    oc.delta_payload(3, m.logit_opacities[:a], None, None, 0)
+    oc.delta_payload(4, m.sh_coeffs[:a, :, 0], None, None, 0)
+    t_delta = time.perf_counter() - t0
+    del m
+    s = synth.random_field(args.n, 3, args.width, args.height, seed=0)
+    t0 = time.perf_counter()
+    oc.snapshot_payload(s.means, s.log_scales, s.quaternions, s.logit_opacities, s.sh_coeffs, s.light_visibility,
+                        s.object_ids, s.active_count, s.sh_degree, 0, 0)
+    t_snap = time.perf_counter() - t0
+    return {"delta_per_frame_set": {"value": a / t_delta, "unit": "Gaussians/s", "seconds": t_delta, "rows": a,
+                                    "cores": 1, "kind": "port"},
+            "snapshot": {"value": args.n / t_snap, "unit": "Gaussians/s", "seconds": t_snap, "rows": args.n,
+                         "cores": 1, "kind": "port"},
+            "note": "oracle numpy port of encode_delta / encode_snapshot (raw), one host core, full size"}
 
 
 def cpu_baseline(model, tgt, poses, intr, light_state):

@@ -144,6 +144,12 @@ struct SnapState {
     uint32_t lo_ord[3], hi_ord[3];
 };
 
+__global__ void k_vis_header(int64_t n, uint8_t* __restrict__ out, uint64_t* __restrict__ out_len) {
+    SS_PDL_WAIT();
+    for (int b = 0; b < 4; ++b) out[b] = (uint8_t)((n >> (8 * b)) & 0xff);
+    *out_len = 4 + (uint64_t)(n + 7) / 8;
+}
+
 __global__ void k_aabb(const float* __restrict__ means, int64_t n, SnapState* st) {
     SS_PDL_WAIT();
     uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0, 0, 0};
@@ -430,18 +436,12 @@ int ss_encode_light_visibility(ss_ctx* ctx, const float* vis, int64_t n, uint8_t
     SS_TRY(ss_scratch_reset(ctx));
     cudaStream_t s = ctx->stream;
     if (n) {
-        k_abs_pack1<float><<<grid_for(ctx, (n + 7) / 8), 256, 0, s>>>(vis, n, out + 4);
+        SS_CUDA(ctx, ss_launch((k_abs_pack1<float>), dim3(grid_for(ctx, (n + 7) / 8)), dim3(256), 0, s, vis, n, out + 4));
         SS_CHECK_LAUNCH(ctx);
     }
-    // '<I' count header and the length, written from the host-known size
-    uint8_t head[4] = {(uint8_t)(n & 0xff), (uint8_t)((n >> 8) & 0xff), (uint8_t)((n >> 16) & 0xff),
-                       (uint8_t)((n >> 24) & 0xff)};
-    uint64_t len = 4 + (uint64_t)(n + 7) / 8;
-    memcpy(ctx->pinned, head, 4);
-    memcpy((uint8_t*)ctx->pinned + 8, &len, 8);
-    SS_CUDA(ctx, cudaMemcpyAsync(out, ctx->pinned, 4, cudaMemcpyHostToDevice, s));
-    SS_CUDA(ctx, cudaMemcpyAsync(out_len, (uint8_t*)ctx->pinned + 8, 8, cudaMemcpyHostToDevice, s));
-    SS_CUDA(ctx, ss_stream_sync(ctx));  // the pinned staging buffer is reused
+    // '<I' count header and the length (a kernel: no host staging, no sync)
+    SS_CUDA(ctx, ss_launch((k_vis_header), dim3(1), dim3(1), 0, s, n, out, out_len));
+    SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }
 

@@ -89,9 +89,10 @@ class ObjectRegistry:
                                                             int(rt.numel()), _lib.ptr(self.local_means),
                                                             _lib.ptr(self.local_rotations), qa, ta))
 
-    def apply_transform(self, model: DeviceModel, object_id: int, quat, translation) -> np.ndarray:
+    def apply_transform(self, model: DeviceModel, object_id: int, quat, translation, return_rows: bool = True):
         """Set a new transform and rewrite the object's world rows; returns the
-        moved rows (ref model.py:389-404)."""
+        moved rows (ref model.py:389-404), or None with return_rows=False (no
+        host read-back: a 60 Hz tick's path)."""
         import torch
         object_id = int(object_id)
         if object_id not in self.transforms:
@@ -99,6 +100,13 @@ class ObjectRegistry:
         self.set_transform(object_id, quat, translation)
         self._ensure(model)
         q, t = self.transforms[object_id]
+        if not return_rows:
+            c = _lib.ctx(model.device.index)
+            c.bind_stream()
+            c.check(c.lib.ss_apply_object_transform(c.handle, model.struct(), object_id, _lib.ptr(self.local_means),
+                                                    _lib.ptr(self.local_rotations), (_lib.f64 * 4)(*q),
+                                                    (_lib.f64 * 3)(*t)))
+            return None
         rows = torch.nonzero(model.object_ids == object_id).reshape(-1)
         if rows.numel():
             c = _lib.ctx(model.device.index)

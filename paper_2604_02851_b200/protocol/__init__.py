@@ -553,19 +553,28 @@ def encode_snapshot(model, profile: QuantizationProfile = PROFILE_DEFAULT, retur
     return payload
 
 
-def encode_light_visibility(visibility) -> bytes:
-    """ref protocol/packets.py:73-76."""
+def encode_light_visibility_device(visibility, out: PayloadBuffer = None) -> PayloadBuffer:
+    """ref protocol/packets.py:73-76 into a device PayloadBuffer (no host sync)."""
     import torch
     if isinstance(visibility, torch.Tensor) and visibility.is_cuda:
-        v = visibility.float().contiguous()
+        v = visibility if visibility.dtype == torch.float32 and visibility.is_contiguous() else \
+            visibility.float().contiguous()
     else:
         v = torch.from_numpy(np.ascontiguousarray(np.asarray(visibility), np.float32)).cuda()
     c = _lib.ctx(v.device.index)
     n = v.numel()
-    out = PayloadBuffer(4 + (n + 7) // 8, v.device)
+    if out is None:
+        out = PayloadBuffer(4 + (n + 7) // 8, v.device)
+    out.ensure(4 + (n + 7) // 8)
+    c.bind_stream()
     c.check(c.lib.ss_encode_light_visibility(c.handle, _lib.ptr(v), n, _lib.ptr(out.data), out.data.numel(),
                                              _lib.ptr(out.length)))
-    return out.to_bytes()
+    return out
+
+
+def encode_light_visibility(visibility) -> bytes:
+    """ref protocol/packets.py:73-76."""
+    return encode_light_visibility_device(visibility).to_bytes()
 
 
 # client-side ingestion on the GPU (SURVEY §8f rank 1)
