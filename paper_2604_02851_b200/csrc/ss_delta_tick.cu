@@ -871,12 +871,15 @@ __global__ void __launch_bounds__(TK_THREADS, TK_EMIT_MINB) k_tick_fused(Batch B
     else if (TK_ORDER == 1) scan = b - res_chunks;  // absolute chunk res_chunks + (b - 2 res_chunks)
     else if (b < res_chunks + abs_chunks) scan = b;
     else emit = b - res_chunks - abs_chunks;
+    SS_ASSERT(b < 2 * res_chunks + abs_chunks);
     if (scan >= 0) {
         const Job& J = B.j[find_job(B, scan)];
+        SS_ASSERT(scan - J.chunk0 >= 0 && scan - J.chunk0 < J.nchunks);
         scan_chunk(J, scan - J.chunk0);
         return;
     }
     const Job& J = B.j[find_job(B, emit)];
+    SS_ASSERT(J.residual && emit - J.chunk0 >= 0 && emit - J.chunk0 < J.nchunks);
     wait_planned(J);
     emit_chunk(J, emit - J.chunk0);
 }

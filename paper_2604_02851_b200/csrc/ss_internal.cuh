@@ -78,6 +78,20 @@ inline cudaError_t ss_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// Device-side invariants of the checked build (-DSS_CHECKS): a violated
+// index bound traps the kernel (the launch then fails loudly).  compute-
+// sanitizer is closed on the GPU pool, so this build is the bounds checker.
+#ifdef SS_CHECKS
+#define SS_ASSERT(cond)          \
+    do {                         \
+        if (!(cond)) __trap();   \
+    } while (0)
+#else
+#define SS_ASSERT(cond) \
+    do {                \
+    } while (0)
+#endif
+
 #define SS_CHECK_LAUNCH(ctx)           \
     do {                               \
         ++(ctx)->launches;             \

@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(256) k_emit_warp(const SplatRec<R>* __restrict
             if (p < p1 && p < cap) {  // beyond the capacity: the call overflowed (flagged, results void)
                 const uint32_t q = (uint32_t)(p - so);
                 const uint32_t qy = q / (uint32_t)sw;
+                SS_ASSERT(sj < (uint64_t)n_in && (int)(q - qy * (uint32_t)sw) < sw);
                 pkeys[p] = (uint32_t)((sy + (int)qy) * tiles_x + sx + (int)(q - qy * (uint32_t)sw));
                 pvals[p] = sj;
             }
@@ -317,6 +318,7 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, const uint64_t* __re
     const int64_t n = (int64_t)*n_dev;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t t = keys[s];
+        SS_ASSERT(s == 0 || keys[s - 1] <= t);  // sorted by tile
         if (s == 0 || keys[s - 1] != t) ranges[t].x = (uint32_t)s;
         if (s == n - 1 || keys[s + 1] != t) ranges[t].y = (uint32_t)(s + 1);
     }
@@ -682,6 +684,7 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
         const uint32_t i = b0 + lane;
         if (i < stop) {
             const uint32_t j = pvals[i];
+            SS_ASSERT(i < rg.y && (uint64_t)i < cap);
             const SplatRec<R> rec = rec_[j];
             stage(my[lane], mu[j], rec, X0, Y0);
             my[lane].p = ATOMIC ? (int)j : (int)pair_index(roffj, rec.win, j, tx, ty);
@@ -1106,6 +1109,7 @@ __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict
             __syncwarp();
         }
         if (valid) {
+            SS_ASSERT(dvals[r] < (uint64_t)n_in);
             R* o = g9 + (int64_t)dvals[r] * 9;
 #pragma unroll
             for (int e = 0; e < 9; ++e) o[e] = g[e];

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ k
         const K key = s_keys[i];
         const unsigned d = (unsigned)(key >> shift) & mask;
         const uint64_t o = s_goff[d] + (uint64_t)(i - s_start[d]);
+        SS_ASSERT(o < (uint64_t)n);
         keys_out[o] = key;
         vals_out[o] = s_vals[i];
     }
