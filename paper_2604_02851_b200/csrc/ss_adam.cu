@@ -134,6 +134,7 @@ __global__ void k_adam_rows(float* __restrict__ quats, const float* __restrict__
 
 extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int64_t ld,
                                int32_t n_views, const ss_adam_hparams* hp) {
+    SS_NVTX("ss_adam_step");
     if (!ctx || !model || !st || !grad || !hp) return SS_ERR_INVALID;
     if (n_views < 1) return ss_fail(ctx, SS_ERR_INVALID, "no ready views");
     const int64_t a = model->active_count;

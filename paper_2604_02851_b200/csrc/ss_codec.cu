@@ -363,6 +363,7 @@ uint64_t ss_snapshot_bound(int64_t n, int32_t degree, int32_t profile) {
 
 int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t* out, uint64_t out_cap,
                        uint64_t* out_len, float* base_means, float* base_ls) {
+    SS_NVTX("ss_encode_snapshot");
     if (!ctx || !m) return SS_ERR_INVALID;
     if (profile != 0 && profile != 1) return ss_fail(ctx, SS_ERR_PROTOCOL, "unknown profile id %d", profile);
     if (m->sh_degree < 0 || m->sh_degree > 3) return ss_fail(ctx, SS_ERR_INVALID, "sh_degree %d", m->sh_degree);

@@ -887,6 +887,7 @@ __global__ void __launch_bounds__(TK_THREADS, TK_EMIT_MINB) k_tick_fused(Batch B
 }  // namespace
 
 extern "C" int ss_encode_delta_batch(ss_ctx* ctx, const ss_delta_job* jobs, int32_t njobs) {
+    SS_NVTX("ss_encode_delta_batch");
     if (!ctx || !jobs) return SS_ERR_INVALID;
     if (njobs < 1 || njobs > TK_MAX_JOBS) return ss_fail(ctx, SS_ERR_INVALID, "1..%d jobs per batch", TK_MAX_JOBS);
     SS_TRY(ss_scratch_reset(ctx));

@@ -7,6 +7,15 @@
 #include <string.h>
 
 #include "../../include/splatstream_b200.h"
+#include <nvtx3/nvToolsExt.h>
+
+// An NVTX range over a public entry point (visible in Nsight Systems / ncu
+// range filters): SS_NVTX("ss_backward");
+struct SsNvtxRange {
+    explicit SsNvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~SsNvtxRange() { nvtxRangePop(); }
+};
+#define SS_NVTX(name) SsNvtxRange _ss_nvtx_range(name)
 
 struct ss_ctx {
     int device;

@@ -2033,6 +2033,7 @@ extern "C" {
 
 int ss_render(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L, const ss_render_opts* o,
               void* img, void* T, ss_render_stats* st) {
+    SS_NVTX("ss_render");
     if (!ctx) return SS_ERR_INVALID;
     SS_TRY(validate(ctx, m, cam, o));
     if (!img) return ss_fail(ctx, SS_ERR_INVALID, "image_out is required");
@@ -2042,6 +2043,7 @@ int ss_render(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_lig
 
 int ss_backward(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_light* L, const ss_render_opts* o,
                 const float* gt, float* grad, double* loss, void* img, ss_render_stats* st) {
+    SS_NVTX("ss_backward");
     if (!ctx) return SS_ERR_INVALID;
     SS_TRY(validate(ctx, m, cam, o));
     if (!gt || !grad || !loss) return ss_fail(ctx, SS_ERR_INVALID, "gt, grad_accum and loss_accum are required");
@@ -2100,6 +2102,7 @@ int ss_composite(ss_ctx* ctx, int64_t n, const double* mu2d, const double* inv2d
 int ss_chain_views_range(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights,
                          int32_t n_views, const float* const* g9, const uint32_t* const* rinv, const int64_t* subset,
                          int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld) {
+    SS_NVTX("ss_chain_views");
     if (!ctx || !m || !cams || !lights || !g9 || !rinv || !grad) return SS_ERR_INVALID;
     if (n_views < 1 || n_views > CV_MAX_VIEWS) return ss_fail(ctx, SS_ERR_INVALID, "1..%d views", CV_MAX_VIEWS);
     if (m->sh_degree < 0 || m->sh_degree > 3 || j0 < 0 || j1 < j0) return ss_fail(ctx, SS_ERR_INVALID, "bad model or row range");
