@@ -49,6 +49,11 @@ typedef struct {
     int32_t count;
     int32_t active_count;
     int32_t sh_degree;       /* 0..3 */
+    int32_t param_dtype;     /* 0: the float columns above are float32 (every entry point); 1: means,
+                                log_scales, quaternions, logit_opacities, sh_coeffs, light_visibility are
+                                float64 (the reference's float64 models) -- accepted by the fp64 blend
+                                instantiation only (render / backward / prepare_splats with precision 1,
+                                and ss_adam_step, which stores f32-rounded values as the reference does) */
 } ss_model;
 
 /* Pinhole camera: ref geometry.py:111-181 (CameraIntrinsics, Pose). */

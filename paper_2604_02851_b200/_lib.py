@@ -27,7 +27,7 @@ i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 class SSModel(C.Structure):
     _fields_ = [("means", vp), ("log_scales", vp), ("quaternions", vp), ("logit_opacities", vp),
                 ("sh_coeffs", vp), ("light_visibility", vp), ("object_ids", vp),
-                ("count", i32), ("active_count", i32), ("sh_degree", i32)]
+                ("count", i32), ("active_count", i32), ("sh_degree", i32), ("param_dtype", i32)]
 
 
 class SSCamera(C.Structure):

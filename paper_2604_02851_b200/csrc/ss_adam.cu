@@ -23,9 +23,9 @@ struct AdamConst {
 // parameter pointer and learning rate of flat element e (ss_grad_layout with
 // `a` = ld rows per group); with PADDED, NULL for an element of a padding
 // row (>= c.a) -- the sharded step's last shards
-template <bool PADDED>
-__device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float* means, float* ls, float* quats,
-                                             float* logits, float* sh, const AdamConst& c, double& lr) {
+template <bool PADDED, typename PT>
+__device__ __forceinline__ PT* adam_param(int64_t e, int64_t a, int B, PT* means, PT* ls, PT* quats,
+                                          PT* logits, PT* sh, const AdamConst& c, double& lr) {
     if (!PADDED) {
         if (e < 3 * a) {
             lr = c.lr[0];
@@ -48,7 +48,7 @@ __device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float*
         return sh + k;
     }
     int64_t k, w;
-    float* p;
+    PT* p;
     if (e < 3 * a) {
         lr = c.lr[0], k = e, w = 3, p = means;
     } else if (e < 6 * a) {
@@ -69,9 +69,12 @@ __device__ __forceinline__ float* adam_param(int64_t e, int64_t a, int B, float*
 #endif
 // ADAM_U elements per thread per grid-stride step; every load (gradient,
 // moments, parameter) is issued before the fp64 update math
-template <bool PADDED>
-__global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float* __restrict__ quats,
-                       float* __restrict__ logits, float* __restrict__ sh, double* __restrict__ m,
+// PT: the parameter storage (float; double for the reference's float64
+// models, which hold float32-rounded values after every update, as the
+// reference's `.astype(np.float32)` store leaves them)
+template <bool PADDED, typename PT>
+__global__ void k_adam(PT* __restrict__ means, PT* __restrict__ ls, PT* __restrict__ quats,
+                       PT* __restrict__ logits, PT* __restrict__ sh, double* __restrict__ m,
                        double* __restrict__ v, const float* __restrict__ g, AdamConst c,
                        const int64_t* __restrict__ skip_if) {
     SS_PDL_WAIT();
@@ -79,13 +82,14 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
     const int64_t a = c.ld, total = a * (11 + 3 * (int64_t)c.B);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += ADAM_U * stride) {
-        float gv[ADAM_U], pv[ADAM_U];
+        float gv[ADAM_U];
+        PT pv[ADAM_U];
         double mv[ADAM_U], vv[ADAM_U], lr[ADAM_U];
-        float* p[ADAM_U];
+        PT* p[ADAM_U];
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t e = e0 + u * stride;
-            p[u] = e < total ? adam_param<PADDED>(e, a, c.B, means, ls, quats, logits, sh, c, lr[u]) : nullptr;
+            p[u] = e < total ? adam_param<PADDED, PT>(e, a, c.B, means, ls, quats, logits, sh, c, lr[u]) : nullptr;
             if (p[u]) {
                 gv[u] = g[e];
                 mv[u] = m[e];
@@ -105,23 +109,24 @@ __global__ void k_adam(float* __restrict__ means, float* __restrict__ ls, float*
             const double mh = dd(mm, c.bc1);
             const double vh = dd(v2, c.bc2);
             const double upd = dm(dd(mh, da(dsq(vh), c.eps)), lr[u]);
-            *p[u] = __double2float_rn(ds((double)pv[u], upd));
+            *p[u] = (PT)__double2float_rn(ds((double)pv[u], upd));
         }
     }
 }
 
-__global__ void k_adam_rows(float* __restrict__ quats, const float* __restrict__ g, double* __restrict__ ema,
+template <typename PT>
+__global__ void k_adam_rows(PT* __restrict__ quats, const float* __restrict__ g, double* __restrict__ ema,
                             int64_t* __restrict__ age, AdamConst c, const int64_t* __restrict__ skip_if) {
     SS_PDL_WAIT();
     if (skip_if && *skip_if) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.a; i += (int64_t)gridDim.x * blockDim.x) {
-        float* q = quats + 4 * i;
+        PT* q = quats + 4 * i;
         const double w = q[0], x = q[1], y = q[2], z = q[3];
         const double n = dsq(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
-        q[0] = __double2float_rn(dd(w, n));
-        q[1] = __double2float_rn(dd(x, n));
-        q[2] = __double2float_rn(dd(y, n));
-        q[3] = __double2float_rn(dd(z, n));
+        q[0] = (PT)__double2float_rn(dd(w, n));
+        q[1] = (PT)__double2float_rn(dd(x, n));
+        q[2] = (PT)__double2float_rn(dd(y, n));
+        q[3] = (PT)__double2float_rn(dd(z, n));
         const double g0 = dm((double)g[3 * i], c.scale), g1 = dm((double)g[3 * i + 1], c.scale),
                      g2 = dm((double)g[3 * i + 2], c.scale);
         const double norm = dsq(da(da(dm(g0, g0), dm(g1, g1)), dm(g2, g2)));
@@ -169,16 +174,27 @@ extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, 
     int64_t grid = (total + 255) / 256;
     if (grid > (int64_t)ctx->num_sms * 32) grid = (int64_t)ctx->num_sms * 32;
     ss_tic(ctx, KC_ADAM);
-    if (ld == a)
-        SS_CUDA(ctx, ss_launch((k_adam<false>), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales,
-                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c, st->skip_if));
-    else
-        SS_CUDA(ctx, ss_launch((k_adam<true>), dim3((int)grid), dim3(256), 0, ctx->stream, model->means, model->log_scales,
-                               model->quaternions, model->logit_opacities, model->sh_coeffs, st->m, st->v, grad, c, st->skip_if));
+#define SS_ADAM(PADDED, PT)                                                                                       \
+    SS_CUDA(ctx, ss_launch((k_adam<PADDED, PT>), dim3((int)grid), dim3(256), 0, ctx->stream, (PT*)model->means,           \
+                           (PT*)model->log_scales, (PT*)model->quaternions, (PT*)model->logit_opacities,                 \
+                           (PT*)model->sh_coeffs, st->m, st->v, grad, c, st->skip_if))
+    if (model->param_dtype == 1) {
+        if (ld == a) SS_ADAM(false, double);
+        else SS_ADAM(true, double);
+    } else {
+        if (ld == a) SS_ADAM(false, float);
+        else SS_ADAM(true, float);
+    }
+#undef SS_ADAM
     SS_CHECK_LAUNCH(ctx);
     int64_t rg = (a + 255) / 256;
     if (rg > (int64_t)ctx->num_sms * 32) rg = (int64_t)ctx->num_sms * 32;
-    SS_CUDA(ctx, ss_launch((k_adam_rows), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions, grad, st->grad_ema, st->age, c, st->skip_if));
+    if (model->param_dtype == 1)
+        SS_CUDA(ctx, ss_launch((k_adam_rows<double>), dim3((int)rg), dim3(256), 0, ctx->stream, (double*)model->quaternions,
+                               grad, st->grad_ema, st->age, c, st->skip_if));
+    else
+        SS_CUDA(ctx, ss_launch((k_adam_rows<float>), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions, grad,
+                               st->grad_ema, st->age, c, st->skip_if));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_ADAM);
     st->step_count = t;

@@ -31,7 +31,8 @@ struct Proj {
 };
 
 // world->camera with W = R_cw^T: mc_k = sum_i d_i R_cw[i][k]
-__device__ __forceinline__ void ss_cam_point(const ss_camera& cam, const float* mean, double d[3], double mc[3]) {
+template <typename PT>
+__device__ __forceinline__ void ss_cam_point(const ss_camera& cam, const PT* mean, double d[3], double mc[3]) {
     d[0] = ds((double)mean[0], cam.position[0]);
     d[1] = ds((double)mean[1], cam.position[1]);
     d[2] = ds((double)mean[2], cam.position[2]);
@@ -40,7 +41,8 @@ __device__ __forceinline__ void ss_cam_point(const ss_camera& cam, const float* 
         mc[k] = da(da(dm(d[0], cam.rot_cw[0 * 3 + k]), dm(d[1], cam.rot_cw[1 * 3 + k])), dm(d[2], cam.rot_cw[2 * 3 + k]));
 }
 
-__device__ __forceinline__ void ss_quat_rot(const float* qf, double u[4], double* qn, double R[3][3]) {
+template <typename PT>
+__device__ __forceinline__ void ss_quat_rot(const PT* qf, double u[4], double* qn, double R[3][3]) {
     double w = qf[0], x = qf[1], y = qf[2], z = qf[3];
     double n = dsq(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
     w = dd(w, n);
@@ -60,8 +62,10 @@ __device__ __forceinline__ void ss_quat_rot(const float* qf, double u[4], double
     R[2][2] = ds(1.0, dm(2.0, da(dm(x, x), dm(y, y))));
 }
 
-// Full fp64 projection of one Gaussian whose camera-space point is known.
-__device__ __forceinline__ void ss_project(const ss_camera& cam, const float* ls, const float* q, bool cutoff, Proj& P) {
+// Full fp64 projection of one Gaussian whose camera-space point is known
+// (PT: the parameter storage type -- float, or double for float64 models).
+template <typename PT>
+__device__ __forceinline__ void ss_project(const ss_camera& cam, const PT* ls, const PT* q, bool cutoff, Proj& P) {
     const double x = P.mc[0], y = P.mc[1], z = P.mc[2];
     const double fx = cam.fx, fy = cam.fy;
     const double zz = dm(z, z);
@@ -204,16 +208,16 @@ struct Shade {
     T pre[3];     // colour before the [0,1] clamp
 };
 
-template <int DEG, typename T>
-__device__ __forceinline__ void ss_shade_v(const ss_light& L, const float* ls, const float* shv, float visf,
+template <int DEG, typename T, typename PT = float>
+__device__ __forceinline__ void ss_shade_v(const ss_light& L, const PT* ls, const PT* shv, PT visf,
                                            const T d[3], const T Rq[3][3], Shade<DEG, T>& S);
 
 // one row's SH coefficients (3 x B floats) into registers, 16-byte loads
 // when the row stride allows it (degrees 1 and 3)
-template <int DEG>
-__device__ __forceinline__ void ss_load_sh(const float* sh, float out[3 * ss_sh_bases(DEG)]) {
+template <int DEG, typename PT = float>
+__device__ __forceinline__ void ss_load_sh(const PT* sh, PT out[3 * ss_sh_bases(DEG)]) {
     constexpr int N = 3 * ss_sh_bases(DEG);
-    if constexpr (N % 4 == 0) {
+    if constexpr (N % 4 == 0 && sizeof(PT) == 4) {
         const float4* p = reinterpret_cast<const float4*>(sh);
 #pragma unroll
         for (int i = 0; i < N / 4; ++i) {
@@ -232,8 +236,8 @@ __device__ __forceinline__ void ss_load_sh(const float* sh, float out[3 * ss_sh_
 // ref render.py:175-197 and the normal proxy of render.py:139-151, in compute
 // type T (fp64 for the parity path, fp32 for the throughput path; preprocess
 // and chain rule call the same code, so they agree on the clamp mask)
-template <int DEG, typename T>
-__device__ __forceinline__ void ss_shade_v(const ss_light& L, const float* ls, const float* shv, float visf,
+template <int DEG, typename T, typename PT>
+__device__ __forceinline__ void ss_shade_v(const ss_light& L, const PT* ls, const PT* shv, PT visf,
                                            const T d[3], const T Rq[3][3], Shade<DEG, T>& S) {
     constexpr int B = ss_sh_bases(DEG);
     S.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
@@ -252,7 +256,7 @@ __device__ __forceinline__ void ss_shade_v(const ss_light& L, const float* ls, c
     const int BL = L.ambient_bands < B ? L.ambient_bands : B;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const float* shc = shv + c * B;
+        const PT* shc = shv + c * B;
         S.albedo[c] = (T)SS_SH_C0 * (T)shc[0] + (T)0.5;
         const T direct = S.albedo[c] * (T)L.intensity[c] * (S.cosv * S.vis);
         T base = 0;

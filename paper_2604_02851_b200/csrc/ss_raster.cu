@@ -66,17 +66,29 @@ struct DebugOut {
     const uint64_t* vpos;    // visible position of input j
 };
 
+// the parameter columns of a model stored as PT (float; double for the
+// fp64 instantiation's float64 models, ss_model.param_dtype = 1)
+template <typename PT>
+struct ParamView {
+    const PT *means, *ls, *quats, *logit, *sh, *vis;
+    __device__ __forceinline__ explicit ParamView(const ss_model& m)
+        : means((const PT*)m.means), ls((const PT*)m.log_scales), quats((const PT*)m.quaternions),
+          logit((const PT*)m.logit_opacities), sh((const PT*)m.sh_coeffs), vis((const PT*)m.light_visibility) {}
+};
+
+template <typename PT>
 __global__ void k_visible_flags(ss_model m, ss_camera cam, const int64_t* subset, int64_t n_in, uint8_t* flag) {
     SS_PDL_WAIT();
+    const ParamView<PT> pv(m);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
         int64_t row = subset ? subset[j] : j;
         double d[3], mc[3];
-        ss_cam_point(cam, m.means + row * 3, d, mc);
+        ss_cam_point(cam, pv.means + row * 3, d, mc);
         flag[j] = mc[2] >= cam.near_plane;
     }
 }
 
-template <int DEG, typename R>
+template <int DEG, typename R, typename PT>
 #ifndef SS_PRE_MINB
 #define SS_PRE_MINB 3  // with the up-front parameter loads (measured 3 / 4 / 5: 0.84 / 0.89 / 0.98 ms per step)
 #endif
@@ -90,23 +102,24 @@ __global__ void __launch_bounds__(128, SS_PRE_MINB) k_preprocess(ss_model m, ss_
     SS_PDL_WAIT();
     unsigned long long kmin = ~0ull, kmax = 0;
     constexpr int B = ss_sh_bases(DEG);
+    const ParamView<PT> pv(m);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_in; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = subset ? subset[j] : j;
 #if SS_PRE_PREFETCH
         // every parameter load of the row first (the stores below would otherwise hold them back)
-        float lsv[3], qv[4], shv[3 * B];
+        PT lsv[3], qv[4], shv[3 * B];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) lsv[k] = m.log_scales[row * 3 + k];
+        for (int k = 0; k < 3; ++k) lsv[k] = pv.ls[row * 3 + k];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) qv[k] = m.quaternions[row * 4 + k];
-        ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, shv);
-        const float logit = m.logit_opacities[row], visv = m.light_visibility[row];
+        for (int k = 0; k < 4; ++k) qv[k] = pv.quats[row * 4 + k];
+        ss_load_sh<DEG, PT>(pv.sh + row * 3 * B, shv);
+        const PT logit = pv.logit[row], visv = pv.vis[row];
 #else
-        const float* lsv = m.log_scales + row * 3;
-        const float* qv = m.quaternions + row * 4;
+        const PT* lsv = pv.ls + row * 3;
+        const PT* qv = pv.quats + row * 4;
 #endif
         Proj P;
-        ss_cam_point(cam, m.means + row * 3, P.d, P.mc);
+        ss_cam_point(cam, pv.means + row * 3, P.d, P.mc);
         dvals[j] = (uint32_t)j;
         if (!(P.mc[2] >= cam.near_plane)) {
             dkeys[j] = ~0ull;
@@ -119,9 +132,9 @@ __global__ void __launch_bounds__(128, SS_PRE_MINB) k_preprocess(ss_model m, ss_
         Shade<DEG, R> S;
         {
 #if !SS_PRE_PREFETCH
-            float shv[3 * B];
-            ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, shv);
-            const float visv = m.light_visibility[row];
+            PT shv[3 * B];
+            ss_load_sh<DEG, PT>(pv.sh + row * 3 * B, shv);
+            const PT visv = pv.vis[row];
 #endif
             const R dR[3] = {(R)P.d[0], (R)P.d[1], (R)P.d[2]};
             R RqR[3][3];
@@ -129,16 +142,16 @@ __global__ void __launch_bounds__(128, SS_PRE_MINB) k_preprocess(ss_model m, ss_
             for (int i = 0; i < 3; ++i)
 #pragma unroll
                 for (int k = 0; k < 3; ++k) RqR[i][k] = (R)P.Rq[i][k];
-            ss_shade_v<DEG, R>(L, lsv, shv, visv, dR, RqR, S);
+            ss_shade_v<DEG, R, PT>(L, lsv, shv, visv, dR, RqR, S);
         }
         SplatRec<R> g;
         g.a = (R)(P.s11 / P.det);
         g.b = (R)(-P.s01 / P.det);
         g.c = (R)(P.s00 / P.det);
 #if !SS_PRE_PREFETCH
-        const float logit = m.logit_opacities[row];
+        const PT logit = pv.logit[row];
 #endif
-        g.o = sizeof(R) == 4 ? (R)(1.0f / (1.0f + expf(-logit))) : (R)(1.0 / (1.0 + exp(-(double)logit)));
+        g.o = sizeof(R) == 4 ? (R)(1.0f / (1.0f + expf(-(float)logit))) : (R)(1.0 / (1.0 + exp(-(double)logit)));
         for (int c = 0; c < 3; ++c) g.col[c] = (R)fmin(fmax((double)S.pre[c], 0.0), 1.0);
         ss_window(P, cam.width, cam.height, g.win);
         rec[j] = g;
@@ -1126,10 +1139,11 @@ template <> __device__ __forceinline__ double t_exp<double>(double x) { return e
 // parameter gradients of this view into acc (means 3, log scales 3,
 // quaternion 4, opacity 1) with the same fp32 additions the gradient buffer
 // would see, and writes the row's SH record for k_sh_grad.
-template <typename T, int DEG>
+template <typename T, int DEG, typename PT = float>
 __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& cam, const ss_light& L, int64_t row,
                                           const T* g, float* acc, float4* __restrict__ shrec_row) {
     constexpr int B = ss_sh_bases(DEG);
+    const ParamView<PT> pv(m);
     T Rc[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -1140,10 +1154,10 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     // ---- appearance first (the SH registers die early)
     T d[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) d[i] = (T)((double)m.means[row * 3 + i] - cam.position[i]);
+    for (int i = 0; i < 3; ++i) d[i] = (T)((double)pv.means[row * 3 + i] - cam.position[i]);
     const T dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     const T vdir[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
-    const float* lsp = m.log_scales + row * 3;
+    const PT* lsp = pv.ls + row * 3;
     int axis;
     {
         const double l0 = lsp[0], l1 = lsp[1], l2 = lsp[2];
@@ -1153,7 +1167,7 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     T u[4];
     T qn;
     {
-        const float* qp = m.quaternions + row * 4;
+        const PT* qp = pv.quats + row * 4;
         const T q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
         qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
         u[0] = q0 / qn; u[1] = q1 / qn; u[2] = q2 / qn; u[3] = q3 / qn;
@@ -1167,9 +1181,9 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     T gv[3] = {0, 0, 0};
     Shade<DEG, T> S;
     {
-        float sh[3 * B];
-        ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, sh);
-        ss_shade_v<DEG, T>(L, lsp, sh, m.light_visibility[row], d, Rq, S);
+        PT sh[3 * B];
+        ss_load_sh<DEG, PT>(pv.sh + row * 3 * B, sh);
+        ss_shade_v<DEG, T, PT>(L, lsp, sh, pv.vis[row], d, Rq, S);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
             gc[c] = (S.pre[c] > (T)0 && S.pre[c] < (T)1) ? g[c] : (T)0;  // clamp mask (optim.py:176-177)
@@ -1315,7 +1329,7 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
         h[c] = t;
     }
     const T udh = u[0] * h[0] + u[1] * h[1] + u[2] * h[2] + u[3] * h[3];
-    const T op = (T)1 / ((T)1 + t_exp<T>(-(T)m.logit_opacities[row]));
+    const T op = (T)1 / ((T)1 + t_exp<T>(-(T)pv.logit[row]));
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         acc[i] += (float)gmean[i];
@@ -1353,7 +1367,7 @@ __device__ __forceinline__ void grad_row_store(float* grad, int64_t a, int64_t r
 // Chain rule in the blend precision T (fp32 for the throughput path, fp64
 // for the parity path); the normal-proxy axis pick repeats the preprocess's
 // fp64 comparison so both passes agree on it.
-template <typename T, int DEG>
+template <typename T, int DEG, typename PT = float>
 __global__ void __launch_bounds__(128, 4) k_chain(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ subset,
                         const uint32_t* __restrict__ rinv, const T* __restrict__ g9, int64_t n_in, int cutoff,
                         float* __restrict__ grad, float4* __restrict__ shrec) {
@@ -1370,7 +1384,7 @@ __global__ void __launch_bounds__(128, 4) k_chain(ss_model m, ss_camera cam, ss_
         for (int e = 0; e < 9; ++e) g[e] = g9[j * 9 + e];
         float acc[11];
         grad_row_load(grad, a, row, acc);
-        chain_row<T, DEG>(m, cam, L, row, g, acc, shrec + row * 2);
+        chain_row<T, DEG, PT>(m, cam, L, row, g, acc, shrec + row * 2);
         grad_row_store(grad, a, row, acc);
     }
 }
@@ -1634,6 +1648,8 @@ int validate(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_rend
     if (o->precision != 0 && o->precision != 1) return ss_fail(ctx, SS_ERR_INVALID, "precision must be 0 or 1");
     if (m->count < 0 || m->active_count < 0 || m->active_count > m->count)
         return ss_fail(ctx, SS_ERR_INVALID, "bad row counts");
+    if (m->param_dtype != 0 && (m->param_dtype != 1 || o->precision != 1))
+        return ss_fail(ctx, SS_ERR_INVALID, "float64 parameters need the fp64 blend (precision 1)");
     return SS_OK;
 }
 
@@ -1754,15 +1770,29 @@ int build_bins(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         SS_CUDA(ctx, ss_launch((k_init_minmax), dim3(1), dim3(1), 0, s, kminmax));
         SS_CHECK_LAUNCH(ctx);
 #define SS_PRE(DEG)                                                                                      \
-    SS_CUDA(ctx, ss_launch((k_preprocess<DEG, R>), dim3(gridn(ctx, n, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
+    SS_CUDA(ctx, ss_launch((k_preprocess<DEG, R, PT>), dim3(gridn(ctx, n, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, n, o->extent_cutoff, b.dkey64, \
                                                          b.dvals, (SplatRec<R>*)b.rec, b.mu, dbg ? *dbg : none,  \
                                                          kminmax))
-        switch (m->sh_degree) {
-            case 0: SS_PRE(0); break;
-            case 1: SS_PRE(1); break;
-            case 2: SS_PRE(2); break;
-            default: SS_PRE(3); break;
+#define SS_PRE_ALL()              \
+    switch (m->sh_degree) {       \
+        case 0: SS_PRE(0); break; \
+        case 1: SS_PRE(1); break; \
+        case 2: SS_PRE(2); break; \
+        default: SS_PRE(3); break; \
+    }
+        bool f64p = false;  // float64 parameter columns: the fp64 instantiation only
+        if constexpr (sizeof(R) == 8) {
+            f64p = m->param_dtype == 1;
+            if (f64p) {
+                using PT = double;
+                SS_PRE_ALL();
+            }
         }
+        if (!f64p) {
+            using PT = float;
+            SS_PRE_ALL();
+        }
+#undef SS_PRE_ALL
 #undef SS_PRE
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_PREPROCESS);
@@ -1927,16 +1957,30 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
         if (!shrec) return SS_ERR_CUDA;
         SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)m->active_count, s));
 #define SS_CHAIN(DEG)                                                                                     \
-    SS_CUDA(ctx, ss_launch((k_chain<R, DEG>), dim3(gridn(ctx, b.n_in, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
+    SS_CUDA(ctx, ss_launch((k_chain<R, DEG, PT>), dim3(gridn(ctx, b.n_in, 128)), dim3(128), 0, s, *m, *cam, *L, o->subset, b.rinv, g9, b.n_in,        \
                                                             o->extent_cutoff, grad, shrec));                      \
     SS_CUDA(ctx, ss_launch((k_sh_grad<DEG>), dim3((unsigned)(((int64_t)m->active_count + SHG_ROWS - 1) / SHG_ROWS)), dim3(256), 0, s,              \
         *L, shrec, m->active_count, grad + 11 * (int64_t)m->active_count))
-        switch (m->sh_degree) {
-            case 0: SS_CHAIN(0); break;
-            case 1: SS_CHAIN(1); break;
-            case 2: SS_CHAIN(2); break;
-            default: SS_CHAIN(3); break;
+#define SS_CHAIN_ALL()              \
+    switch (m->sh_degree) {         \
+        case 0: SS_CHAIN(0); break; \
+        case 1: SS_CHAIN(1); break; \
+        case 2: SS_CHAIN(2); break; \
+        default: SS_CHAIN(3); break; \
+    }
+        bool f64p = false;
+        if constexpr (sizeof(R) == 8) {
+            f64p = m->param_dtype == 1;
+            if (f64p) {
+                using PT = double;
+                SS_CHAIN_ALL();
+            }
         }
+        if (!f64p) {
+            using PT = float;
+            SS_CHAIN_ALL();
+        }
+#undef SS_CHAIN_ALL
 #undef SS_CHAIN
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_CHAIN);
@@ -1950,21 +1994,22 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
 }
 
 // the rest of PreparedSplats (ss_prepare_extras), one thread per prepared splat
-template <int DEG>
+template <int DEG, typename PT>
 __global__ void k_prepare_extras(ss_model m, ss_camera cam, ss_light L, const int64_t* __restrict__ rows, int64_t M,
                                  ss_prepared_extras o) {
     SS_PDL_WAIT();
     constexpr int B = ss_sh_bases(DEG);
+    const ParamView<PT> pv(m);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = rows[i];
         Proj P;
-        ss_cam_point(cam, m.means + row * 3, P.d, P.mc);
-        const float* ls = m.log_scales + row * 3;
-        ss_project(cam, ls, m.quaternions + row * 4, true, P);
-        float shv[3 * B];
-        ss_load_sh<DEG>(m.sh_coeffs + row * 3 * B, shv);
+        ss_cam_point(cam, pv.means + row * 3, P.d, P.mc);
+        const PT* ls = pv.ls + row * 3;
+        ss_project(cam, ls, pv.quats + row * 4, true, P);
+        PT shv[3 * B];
+        ss_load_sh<DEG, PT>(pv.sh + row * 3 * B, shv);
         Shade<DEG, double> S;
-        ss_shade_v<DEG, double>(L, ls, shv, m.light_visibility[row], P.d, P.Rq, S);
+        ss_shade_v<DEG, double, PT>(L, ls, shv, pv.vis[row], P.d, P.Rq, S);
         if (o.mu_cam) for (int k = 0; k < 3; ++k) o.mu_cam[3 * i + k] = P.mc[k];
         if (o.J) for (int r = 0; r < 2; ++r) for (int k = 0; k < 3; ++k) o.J[6 * i + 3 * r + k] = P.J[r][k];
         if (o.sigma3d)
@@ -2109,6 +2154,7 @@ int ss_chain_views_range(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, 
     if (row0 < 0 || rows < 0 || ld < rows || row0 + rows > m->active_count)
         return ss_fail(ctx, SS_ERR_INVALID, "bad gradient layout (row0 %lld, rows %lld, ld %lld)", (long long)row0,
                        (long long)rows, (long long)ld);
+    if (m->param_dtype != 0) return ss_fail(ctx, SS_ERR_INVALID, "the deferred chain rule takes float32 parameters");
     if (rows == 0 || j1 == j0) return SS_OK;
     SS_TRY(ss_scratch_reset(ctx));
     ChainViews hv;
@@ -2161,7 +2207,10 @@ int ss_prepare_splats(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
     uint64_t* vtot = SS_SCRATCH(ctx, uint64_t, 1);
     if (!flag || !vpos || !vtot) return SS_ERR_CUDA;
     if (n > 0) {
-        SS_CUDA(ctx, ss_launch((k_visible_flags), dim3(gridn(ctx, n)), dim3(256), 0, s, *m, *cam, o->subset, n, flag));
+        if (m->param_dtype == 1)
+            SS_CUDA(ctx, ss_launch((k_visible_flags<double>), dim3(gridn(ctx, n)), dim3(256), 0, s, *m, *cam, o->subset, n, flag));
+        else
+            SS_CUDA(ctx, ss_launch((k_visible_flags<float>), dim3(gridn(ctx, n)), dim3(256), 0, s, *m, *cam, o->subset, n, flag));
         SS_CHECK_LAUNCH(ctx);
     }
     SS_TRY(ss_scan_u8_to_u64(ctx, flag, vpos, n, vtot));
@@ -2205,12 +2254,24 @@ int ss_prepare_extras(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, cons
     if (m->sh_degree < 0 || m->sh_degree > 3 || M < 0) return ss_fail(ctx, SS_ERR_INVALID, "bad model or count");
     if (M == 0) return SS_OK;
     SS_TRY(ss_scratch_reset(ctx));
-    switch (m->sh_degree) {
-        case 0: SS_CUDA(ctx, ss_launch((k_prepare_extras<0>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
-        case 1: SS_CUDA(ctx, ss_launch((k_prepare_extras<1>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
-        case 2: SS_CUDA(ctx, ss_launch((k_prepare_extras<2>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
-        default: SS_CUDA(ctx, ss_launch((k_prepare_extras<3>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, *m, *cam, *L, rows, M, *out)); break;
+#define SS_EXTRAS(DEG, PT) SS_CUDA(ctx, ss_launch((k_prepare_extras<DEG, PT>), dim3(gridn(ctx, M)), dim3(256), 0, ctx->stream, \
+                                                   *m, *cam, *L, rows, M, *out))
+    if (m->param_dtype == 1) {
+        switch (m->sh_degree) {
+            case 0: SS_EXTRAS(0, double); break;
+            case 1: SS_EXTRAS(1, double); break;
+            case 2: SS_EXTRAS(2, double); break;
+            default: SS_EXTRAS(3, double); break;
+        }
+    } else {
+        switch (m->sh_degree) {
+            case 0: SS_EXTRAS(0, float); break;
+            case 1: SS_EXTRAS(1, float); break;
+            case 2: SS_EXTRAS(2, float); break;
+            default: SS_EXTRAS(3, float); break;
+        }
     }
+#undef SS_EXTRAS
     SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }

@@ -88,17 +88,23 @@ class DeviceModel:
         return getattr(self, name)
 
     @staticmethod
-    def from_host(model, device=None) -> "DeviceModel":
+    def from_host(model, device=None, keep_f64: bool = False) -> "DeviceModel":
+        """Upload a host model: float32 columns, or -- with keep_f64 and a
+        model whose means are float64 (the reference's unit tests build such
+        models) -- float64 columns for the fp64 blend instantiation, so a
+        finite-difference perturbation of 1e-4 reaches the kernels intact."""
         import torch
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        f64 = keep_f64 and np.asarray(model.means).dtype == np.float64
+        ft = np.float64 if f64 else np.float32
 
         def up(a, dt):
             return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=dt)).to(dev, non_blocking=False)
 
-        return DeviceModel(up(model.means, np.float32).reshape(-1, 3), up(model.log_scales, np.float32).reshape(-1, 3),
-                           up(model.quaternions, np.float32).reshape(-1, 4),
-                           up(model.logit_opacities, np.float32).reshape(-1),
-                           up(model.sh_coeffs, np.float32), up(model.light_visibility, np.float32).reshape(-1),
+        return DeviceModel(up(model.means, ft).reshape(-1, 3), up(model.log_scales, ft).reshape(-1, 3),
+                           up(model.quaternions, ft).reshape(-1, 4),
+                           up(model.logit_opacities, ft).reshape(-1),
+                           up(model.sh_coeffs, ft), up(model.light_visibility, ft).reshape(-1),
                            up(model.object_ids, np.int32).reshape(-1), model.active_count, model.sh_degree)
 
     def to_host(self) -> GaussianModel:
@@ -122,14 +128,21 @@ class DeviceModel:
         s.count = self.count
         s.active_count = self.active_count
         s.sh_degree = self.sh_degree
+        s.param_dtype = 1 if self.means.dtype == torch_float64() else 0
         return s
 
     def clone(self) -> "DeviceModel":
         return DeviceModel(*(getattr(self, k).clone() for k in ATTRIBUTE_NAMES), self.active_count, self.sh_degree)
 
 
-def as_device(model, device=None):
-    """(DeviceModel, uploaded?) for either kind of model."""
+def torch_float64():
+    import torch
+    return torch.float64
+
+
+def as_device(model, device=None, keep_f64: bool = False):
+    """(DeviceModel, uploaded?) for either kind of model (keep_f64: see
+    DeviceModel.from_host; only the fp64 blend entry points pass it)."""
     if isinstance(model, DeviceModel):
         return model, False
-    return DeviceModel.from_host(model, device), True
+    return DeviceModel.from_host(model, device, keep_f64), True

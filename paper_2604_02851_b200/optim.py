@@ -203,7 +203,7 @@ def backward(model, view: ReferenceView, index_subset=None, extent_cutoff: bool 
     """ref optim.py:113 -- (loss, Gradients over active rows, rendered image).
     deterministic=False: the throughput mode (float atomics, see ss_render_opts)."""
     import torch
-    dm, _ = as_device(model)
+    dm, _ = as_device(model, keep_f64=precision == 1)
     a = dm.active_count
     n = a * (11 + 3 * (dm.sh_degree + 1) ** 2)
     g = torch.zeros(max(n, 1), dtype=torch.float32, device=dm.device)
@@ -701,7 +701,7 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     pg = process_group if process_group is not None else state.process_group
     if pg is not None and pg is not state.process_group:
         raise ValueError("the optimizer state was created for a different process group")
-    dm, uploaded = as_device(model)
+    dm, uploaded = as_device(model, keep_f64=precision == 1)
     a = dm.active_count
     sub = _subset_tensor(index_subset, dm.device)
     persistent = workspace is not None

@@ -130,7 +130,7 @@ def render_device(model: DeviceModel, pose, intr, light_state, index_subset=None
 def render(model, pose, intr, light_state, index_subset=None, background=(0.0, 0.0, 0.0),
            return_transmittance: bool = False, extent_cutoff: bool = True, precision: int = 0):
     """ref render.py:339 -- returns a float64 numpy image [, T]."""
-    dm, _ = as_device(model)
+    dm, _ = as_device(model, keep_f64=precision == 1)
     r = render_device(dm, pose, intr, light_state, index_subset, background, return_transmittance, extent_cutoff,
                       precision)
     if return_transmittance:
@@ -171,7 +171,7 @@ def prepare_splats(model, pose, intr, light_state, index_subset=None, extent_cut
     depth sort (K3a) and ss_prepare_extras (the remaining PreparedSplats
     fields, same device functions); returned as host arrays."""
     import torch
-    dm, _ = as_device(model)
+    dm, _ = as_device(model, keep_f64=True)
     c = _lib.ctx(dm.device.index)
     dev = dm.device
     sub = _subset_tensor(index_subset, dev)
