@@ -12,6 +12,10 @@ Appendix B: the reference tests hold fp64-level tolerances):
   splatstream.protocol  encode_delta, encode_snapshot, decode_snapshot, decode_delta,
                         apply_delta, advance_baseline
 
+The reference's StreamServer / StreamClient (test_server.py, test_client.py)
+import those names, so their whole tick loop -- optimizer step, snapshot,
+delta emission, client ingestion -- runs on the drop-in.
+
 Everything else (geometry, model, scene, engine, the numpy helpers
 shade_gaussian / sh_basis / normal_proxies / _drotmat_dquat_batch, framing,
 packets) stays the reference's -- those are not on the hot path (SURVEY
@@ -46,16 +50,28 @@ def _fp64(fn):
     return wrapped
 
 
+def _decode_snapshot(payload):
+    """The drop-in's device decode, returned as the caller's own host model
+    type (the reference's GaussianModel, whose mutation methods the client
+    uses on its replica)."""
+    import splatstream.model as _M
+    m, info = _i2.decode_snapshot_host(payload)
+    return _M.GaussianModel(means=m.means, log_scales=m.log_scales, quaternions=m.quaternions,
+                            logit_opacities=m.logit_opacities, sh_coeffs=m.sh_coeffs,
+                            light_visibility=m.light_visibility, object_ids=m.object_ids,
+                            active_count=m.active_count, sh_degree=m.sh_degree), info
+
+
 _PATCH = {
     _R: dict(render=_fp64(_r2.render), prepare_splats=_r2.prepare_splats, composite=_r2.composite,
              update_light_visibility=_r2.update_light_visibility),
     _O: dict(backward=_fp64(_o2.backward), step=_fp64(_o2.step), OptimizerState=_o2.OptimizerState),
     _P: dict(encode_delta=_p2.encode_delta, encode_snapshot=_p2.encode_snapshot,
-             decode_snapshot=_i2.decode_snapshot_host, decode_delta=_i2.decode_delta_host,
+             decode_snapshot=_decode_snapshot, decode_delta=_i2.decode_delta_host,
              apply_delta=_i2.apply_delta),
     _PD: dict(encode_delta=_p2.encode_delta, decode_delta=_i2.decode_delta_host, apply_delta=_i2.apply_delta,
               advance_baseline=_i2.advance_baseline),
-    _PS: dict(encode_snapshot=_p2.encode_snapshot, decode_snapshot=_i2.decode_snapshot_host),
+    _PS: dict(encode_snapshot=_p2.encode_snapshot, decode_snapshot=_decode_snapshot),
 }
 for _mod, _names in _PATCH.items():
     for _k, _v in _names.items():

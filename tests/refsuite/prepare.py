@@ -21,7 +21,7 @@ import sys
 ROOT = pathlib.Path(__file__).resolve().parents[2]
 REF = pathlib.Path("/root/reference/pkg")
 OUT = ROOT / "baseline" / "_ref_tests"
-SUITES = ("test_render.py", "test_optim.py", "test_protocol.py", "test_golden.py")
+SUITES = ("test_render.py", "test_optim.py", "test_protocol.py", "test_golden.py", "test_server.py", "test_client.py")
 
 
 def prepare(ref: pathlib.Path = REF) -> bool:
