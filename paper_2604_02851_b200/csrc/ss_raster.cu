@@ -1514,15 +1514,20 @@ __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __res
     }
 }
 
-// SH gradients of all the step's views (ss_chain_views): per (row, channel,
-// basis) entry, the views' contributions in view order, the entry read and
-// written once.  Same per-entry arithmetic as k_sh_grad.
+// SH gradients of all the step's views (ss_chain_views): g_sh[row, c, b] +=
+// gc_{v,c} * K_{v,row,c,b} for the views in view order, with
+//   K = [b < BL] ambient[c][b] + [b >= 1] Y_b(view dir) + [b == 0] C0 I_c cos vis
+// (ambient light; without it K = Y_b + [b == 0] C0 I_c cos vis) -- ref
+// optim.py:221-233: the ambient product, the view-dependent basis and the
+// direct-light term through albedo_est = C0 dc + 0.5.  Phase 1 builds K and
+// gc per (view, row, channel) in shared memory (one thread per item, the
+// branches resolved once); phase 2 gives each (row, channel, basis) entry one
+// FMA per view, the entry read and written once.
 #ifndef SS_SHGV_ROWS
-#define SS_SHGV_ROWS 32
+#define SS_SHGV_ROWS 16
 #endif
 constexpr int SHGV_ROWS = SS_SHGV_ROWS;
 
-// rows [0, a) of a layout of ld rows per group (shrec: ld records per view)
 template <int DEG>
 __global__ void __launch_bounds__(256) k_sh_grad_views(const __grid_constant__ ChainViews Vp, int nv,
                                                        const float4* __restrict__ shrec, int64_t a, int64_t ld,
@@ -1530,45 +1535,45 @@ __global__ void __launch_bounds__(256) k_sh_grad_views(const __grid_constant__ C
     SS_PDL_WAIT();
     const ChainViews* V = &Vp;
     constexpr int B = ss_sh_bases(DEG);
-    extern __shared__ float4 s_dyn[];
-    float4* s_r0 = s_dyn;                                          // [nv][SHGV_ROWS]
-    float* s_y = reinterpret_cast<float*>(s_dyn + nv * SHGV_ROWS);  // [nv][SHGV_ROWS][B + 1]
+    extern __shared__ float s_dynf[];
+    constexpr int KS = B + 1;                          // padded: one item per bank offset
+    float* s_k = s_dynf;                               // [nv][SHGV_ROWS][3][KS]
+    float* s_g = s_dynf + nv * SHGV_ROWS * 3 * KS;     // [nv][SHGV_ROWS][3]
     const int64_t row0 = (int64_t)blockIdx.x * SHGV_ROWS;
     const int nrows = (int)min((int64_t)SHGV_ROWS, a - row0);
-    for (int t = threadIdx.x; t < nv * SHGV_ROWS; t += blockDim.x) {
-        const int v = t / SHGV_ROWS, r = t - v * SHGV_ROWS;
+    for (int t = threadIdx.x; t < nv * SHGV_ROWS * 3; t += blockDim.x) {
+        const int c = t % 3, vr = t / 3, v = vr / SHGV_ROWS, r = vr - v * SHGV_ROWS;
+        float* k = s_k + (size_t)t * KS;
         if (r >= nrows) continue;
         const float4* rec = shrec + ((int64_t)v * ld + row0 + r) * 2;
         const float4 r0 = rec[0], r1 = rec[1];
+        const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
+        s_g[t] = gcc;
         const float dir[3] = {r1.x, r1.y, r1.z};
         float Y[B];
         ss_sh_eval<DEG, float>(dir, Y);
+        const ss_light& L = V->light[v];
+        const int BL = L.ambient_bands < B ? L.ambient_bands : B;
 #pragma unroll
-        for (int k = 0; k < B; ++k) s_y[(v * SHGV_ROWS + r) * (B + 1) + k] = Y[k];
-        s_r0[v * SHGV_ROWS + r] = r0;
+        for (int b = 0; b < B; ++b) {
+            float kv;
+            if (L.ambient_bands == 0) kv = Y[b];
+            else kv = (b < BL ? (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? Y[b] : 0.f);
+            if (b == 0) kv += (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
+            k[b] = kv;
+        }
     }
     __syncthreads();
     const int n = nrows * 3 * B;
     float* out = grad_sh + row0 * 3 * B;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int r = e / (3 * B), rem = e - r * 3 * B, c = rem / B, b = rem - c * B;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {  // e = (r * 3 + c) * B + b, coalesced over the rows
+        const int rc = e / B, b = e - rc * B;
         float acc = out[e];
         bool touched = false;
         for (int v = 0; v < nv; ++v) {
-            const float4 r0 = s_r0[v * SHGV_ROWS + r];
-            const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
+            const float gcc = s_g[v * SHGV_ROWS * 3 + rc];
             if (gcc == 0.f) continue;  // clamped colour or row not visible in this view
-            const ss_light& L = V->light[v];
-            const int BL = L.ambient_bands < B ? L.ambient_bands : B;
-            const float yb = s_y[(v * SHGV_ROWS + r) * (B + 1) + b];
-            float val;
-            if (L.ambient_bands == 0) {
-                val = gcc * yb;
-            } else {
-                val = (b < BL ? gcc * (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? gcc * yb : 0.f);
-            }
-            if (b == 0) val += gcc * (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
-            acc += val;
+            acc = fmaf(gcc, s_k[(v * SHGV_ROWS * 3 + rc) * KS + b], acc);
             touched = true;
         }
         if (touched) out[e] = acc;
@@ -1868,7 +1873,9 @@ int launch_chain_views(ss_ctx* ctx, const ss_model* m, const ChainViews& hv, int
         SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, j1 - j0, 128)), dim3(128), 0, s, *m, hv,                  \
                                nv, subset, j0, j1, row0, ld, grad, shrec));                                                \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
-        const size_t smem = (size_t)nv * SHGV_ROWS * (sizeof(float4) + sizeof(float) * (B + 1));                           \
+        const size_t smem = (size_t)nv * SHGV_ROWS * 3 * (B + 2) * sizeof(float);  /* K (B + 1 padded) + gc */          \
+        if (smem > 48 * 1024)                                                                                              \
+            SS_CUDA(ctx, cudaFuncSetAttribute(k_sh_grad_views<DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
         SS_CUDA(ctx, ss_launch((k_sh_grad_views<DEG>), dim3((unsigned)((rows + SHGV_ROWS - 1) / SHGV_ROWS)), dim3(256), smem, s, \
                                hv, nv, (const float4*)shrec, rows, ld, grad + 11 * ld));                                  \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
