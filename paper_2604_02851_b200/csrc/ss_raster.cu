@@ -815,7 +815,10 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a
 __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
 __device__ __forceinline__ float& comp(float2& v, int h) { return h ? v.y : v.x; }
 
-__global__ void __launch_bounds__(32 * WPB, 8) k_blend_fwd2(const uint2* __restrict__ ranges,
+#ifndef SS_FWD2_MINB
+#define SS_FWD2_MINB 8
+#endif
+__global__ void __launch_bounds__(32 * WPB, SS_FWD2_MINB) k_blend_fwd2(const uint2* __restrict__ ranges,
                                                          const uint32_t* __restrict__ pvals,
                                                          const double2* __restrict__ mu,
                                                          const SplatRec<float>* __restrict__ rec, int W, int H,
