@@ -1063,7 +1063,7 @@ def measured_peaks():
 
 
 def _committed(key):
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_traffic.json")
     try:
         with open(p) as f:
             return json.load(f).get(key, {})
