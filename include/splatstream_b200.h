@@ -286,6 +286,15 @@ int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* state, const float
  * an empty shard. */
 int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* state, const float* grad_sum, int64_t ld,
                     int32_t n_views, const ss_adam_hparams* hp);
+/* ss_adam_step_ld whose every updated parameter (and renormalised
+ * quaternion) is also stored into n_peers (<= 15) other replicas of the same
+ * rows: peer_rows[5 q + g] is peer q's base address of group g (means,
+ * log_scales, quaternions, logit_opacities, sh_coeffs) at the first row of
+ * `model` -- device memory of other GPUs mapped into this process (CUDA IPC;
+ * NVLink / NVSwitch peer stores).  The view-sharded step's parameter
+ * all-gather, fused into the update.  Float32 parameters only. */
+int ss_adam_step_peers(ss_ctx* ctx, ss_model* model, ss_adam_state* state, const float* grad_sum, int64_t ld,
+                       int32_t n_views, const ss_adam_hparams* hp, int32_t n_peers, float* const* peer_rows);
 
 /* ---- encoders (ref protocol/) -------------------------------------------- */
 /* encode_delta(): ref protocol/delta.py:72 with compression_id 0 (raw).

@@ -204,6 +204,8 @@ _SIGS = {
                                 C.POINTER(SSPreparedExtras)]),
     "ss_adam_step_ld": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSAdamState), vp, i64, i32,
                               C.POINTER(SSAdamHparams)]),
+    "ss_adam_step_peers": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSAdamState), vp, i64, i32,
+                                 C.POINTER(SSAdamHparams), i32, C.POINTER(vp)]),
     "ss_engine_render": (i32, [vp, C.POINTER(SSScene), C.POINTER(SSEngineCamera), C.POINTER(SSEngineOut)]),
     "ss_grid_rebuild": (i32, [vp, vp, i64, C.POINTER(SSGridSpec), vp, vp, vp, vp, C.POINTER(i64)]),
     "ss_zigzag_varints": (i32, [vp, vp, i64, vp, u64, C.POINTER(u64)]),

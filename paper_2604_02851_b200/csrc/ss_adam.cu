@@ -25,44 +25,34 @@ struct AdamConst {
 // row (>= c.a) -- the sharded step's last shards
 template <bool PADDED, typename PT>
 __device__ __forceinline__ PT* adam_param(int64_t e, int64_t a, int B, PT* means, PT* ls, PT* quats,
-                                          PT* logits, PT* sh, const AdamConst& c, double& lr) {
-    if (!PADDED) {
-        if (e < 3 * a) {
-            lr = c.lr[0];
-            return means + e;
-        }
-        if (e < 6 * a) {
-            lr = c.lr[1];
-            return ls + (e - 3 * a);
-        }
-        if (e < 10 * a) {
-            lr = c.lr[2];
-            return quats + (e - 6 * a);
-        }
-        if (e < 11 * a) {
-            lr = c.lr[3];
-            return logits + (e - 10 * a);
-        }
-        const int64_t k = e - 11 * a;
-        lr = (k % B) == 0 ? c.lr[4] : c.lr[5];
-        return sh + k;
-    }
+                                          PT* logits, PT* sh, const AdamConst& c, double& lr, int& grp,
+                                          int64_t& off) {
     int64_t k, w;
     PT* p;
     if (e < 3 * a) {
-        lr = c.lr[0], k = e, w = 3, p = means;
+        lr = c.lr[0], k = e, w = 3, p = means, grp = 0;
     } else if (e < 6 * a) {
-        lr = c.lr[1], k = e - 3 * a, w = 3, p = ls;
+        lr = c.lr[1], k = e - 3 * a, w = 3, p = ls, grp = 1;
     } else if (e < 10 * a) {
-        lr = c.lr[2], k = e - 6 * a, w = 4, p = quats;
+        lr = c.lr[2], k = e - 6 * a, w = 4, p = quats, grp = 2;
     } else if (e < 11 * a) {
-        lr = c.lr[3], k = e - 10 * a, w = 1, p = logits;
+        lr = c.lr[3], k = e - 10 * a, w = 1, p = logits, grp = 3;
     } else {
-        k = e - 11 * a, w = 3 * B, p = sh;
+        k = e - 11 * a, w = 3 * B, p = sh, grp = 4;
         lr = (k % B) == 0 ? c.lr[4] : c.lr[5];
     }
-    return k >= c.a * w ? nullptr : p + k;
+    off = k;
+    if (PADDED && k >= c.a * w) return nullptr;
+    return p + k;
 }
+
+// The updated rows' copies in the peers' replicas (the view-sharded step's
+// parameter all-gather, fused: every update is stored to the local row and
+// straight into each peer's replica over NVLink).
+struct PeerRows {
+    float* g[SS_MAX_PEERS][5];  // per peer: means, log_scales, quaternions, logit_opacities, sh (at the shard's row)
+    int n;
+};
 
 #ifndef ADAM_U
 #define ADAM_U 1  // measured: 1 / 2 / 4 elements -> 0.60 / 0.63 / 0.66 ms per step
@@ -72,11 +62,11 @@ __device__ __forceinline__ PT* adam_param(int64_t e, int64_t a, int B, PT* means
 // PT: the parameter storage (float; double for the reference's float64
 // models, which hold float32-rounded values after every update, as the
 // reference's `.astype(np.float32)` store leaves them)
-template <bool PADDED, typename PT>
+template <bool PADDED, typename PT, bool PEERS = false>
 __global__ void k_adam(PT* __restrict__ means, PT* __restrict__ ls, PT* __restrict__ quats,
                        PT* __restrict__ logits, PT* __restrict__ sh, double* __restrict__ m,
                        double* __restrict__ v, const float* __restrict__ g, AdamConst c,
-                       const int64_t* __restrict__ skip_if) {
+                       const int64_t* __restrict__ skip_if, const __grid_constant__ PeerRows peers) {
     SS_PDL_WAIT();
     if (skip_if && *skip_if) return;  // the step's binning overflowed: no update
     const int64_t a = c.ld, total = a * (11 + 3 * (int64_t)c.B);
@@ -86,10 +76,13 @@ __global__ void k_adam(PT* __restrict__ means, PT* __restrict__ ls, PT* __restri
         PT pv[ADAM_U];
         double mv[ADAM_U], vv[ADAM_U], lr[ADAM_U];
         PT* p[ADAM_U];
+        int grp[ADAM_U];
+        int64_t off[ADAM_U];
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t e = e0 + u * stride;
-            p[u] = e < total ? adam_param<PADDED, PT>(e, a, c.B, means, ls, quats, logits, sh, c, lr[u]) : nullptr;
+            p[u] = e < total ? adam_param<PADDED, PT>(e, a, c.B, means, ls, quats, logits, sh, c, lr[u], grp[u], off[u])
+                             : nullptr;
             if (p[u]) {
                 gv[u] = g[e];
                 mv[u] = m[e];
@@ -109,24 +102,36 @@ __global__ void k_adam(PT* __restrict__ means, PT* __restrict__ ls, PT* __restri
             const double mh = dd(mm, c.bc1);
             const double vh = dd(v2, c.bc2);
             const double upd = dm(dd(mh, da(dsq(vh), c.eps)), lr[u]);
-            *p[u] = (PT)__double2float_rn(ds((double)pv[u], upd));
+            const float nv = __double2float_rn(ds((double)pv[u], upd));
+            *p[u] = (PT)nv;
+            if constexpr (PEERS) {
+#pragma unroll 1
+                for (int q = 0; q < peers.n; ++q) peers.g[q][grp[u]][off[u]] = nv;
+            }
         }
     }
 }
 
-template <typename PT>
+template <typename PT, bool PEERS = false>
 __global__ void k_adam_rows(PT* __restrict__ quats, const float* __restrict__ g, double* __restrict__ ema,
-                            int64_t* __restrict__ age, AdamConst c, const int64_t* __restrict__ skip_if) {
+                            int64_t* __restrict__ age, AdamConst c, const int64_t* __restrict__ skip_if,
+                            const __grid_constant__ PeerRows peers) {
     SS_PDL_WAIT();
     if (skip_if && *skip_if) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.a; i += (int64_t)gridDim.x * blockDim.x) {
         PT* q = quats + 4 * i;
         const double w = q[0], x = q[1], y = q[2], z = q[3];
         const double n = dsq(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
-        q[0] = (PT)__double2float_rn(dd(w, n));
-        q[1] = (PT)__double2float_rn(dd(x, n));
-        q[2] = (PT)__double2float_rn(dd(y, n));
-        q[3] = (PT)__double2float_rn(dd(z, n));
+        const float qn[4] = {__double2float_rn(dd(w, n)), __double2float_rn(dd(x, n)), __double2float_rn(dd(y, n)),
+                             __double2float_rn(dd(z, n))};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = (PT)qn[k];
+        if constexpr (PEERS) {
+#pragma unroll 1
+            for (int p = 0; p < peers.n; ++p)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) peers.g[p][2][4 * i + k] = qn[k];
+        }
         const double g0 = dm((double)g[3 * i], c.scale), g1 = dm((double)g[3 * i + 1], c.scale),
                      g2 = dm((double)g[3 * i + 2], c.scale);
         const double norm = dsq(da(da(dm(g0, g0), dm(g1, g1)), dm(g2, g2)));
@@ -137,9 +142,18 @@ __global__ void k_adam_rows(PT* __restrict__ quats, const float* __restrict__ g,
 
 }  // namespace
 
-extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int64_t ld,
-                               int32_t n_views, const ss_adam_hparams* hp) {
+extern "C" int ss_adam_step_peers(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int64_t ld,
+                                  int32_t n_views, const ss_adam_hparams* hp, int32_t n_peers, float* const* peer_rows) {
     SS_NVTX("ss_adam_step");
+    if (n_peers < 0 || n_peers > SS_MAX_PEERS || (n_peers && !peer_rows))
+        return ss_fail(ctx, SS_ERR_INVALID, "0..%d peers", SS_MAX_PEERS);
+    PeerRows peers;
+    memset(&peers, 0, sizeof(peers));
+    peers.n = n_peers;
+    for (int q = 0; q < n_peers; ++q)
+        for (int k = 0; k < 5; ++k) peers.g[q][k] = peer_rows[5 * q + k];
+    if (n_peers && model && model->param_dtype != 0)
+        return ss_fail(ctx, SS_ERR_INVALID, "peer replicas take float32 parameters");
     if (!ctx || !model || !st || !grad || !hp) return SS_ERR_INVALID;
     if (n_views < 1) return ss_fail(ctx, SS_ERR_INVALID, "no ready views");
     const int64_t a = model->active_count;
@@ -174,27 +188,33 @@ extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, 
     int64_t grid = (total + 255) / 256;
     if (grid > (int64_t)ctx->num_sms * 32) grid = (int64_t)ctx->num_sms * 32;
     ss_tic(ctx, KC_ADAM);
-#define SS_ADAM(PADDED, PT)                                                                                       \
-    SS_CUDA(ctx, ss_launch((k_adam<PADDED, PT>), dim3((int)grid), dim3(256), 0, ctx->stream, (PT*)model->means,           \
+#define SS_ADAM(PADDED, PT, PEERS)                                                                                \
+    SS_CUDA(ctx, ss_launch((k_adam<PADDED, PT, PEERS>), dim3((int)grid), dim3(256), 0, ctx->stream, (PT*)model->means,    \
                            (PT*)model->log_scales, (PT*)model->quaternions, (PT*)model->logit_opacities,                 \
-                           (PT*)model->sh_coeffs, st->m, st->v, grad, c, st->skip_if))
+                           (PT*)model->sh_coeffs, st->m, st->v, grad, c, st->skip_if, peers))
     if (model->param_dtype == 1) {
-        if (ld == a) SS_ADAM(false, double);
-        else SS_ADAM(true, double);
+        if (ld == a) SS_ADAM(false, double, false);
+        else SS_ADAM(true, double, false);
+    } else if (n_peers) {
+        if (ld == a) SS_ADAM(false, float, true);
+        else SS_ADAM(true, float, true);
     } else {
-        if (ld == a) SS_ADAM(false, float);
-        else SS_ADAM(true, float);
+        if (ld == a) SS_ADAM(false, float, false);
+        else SS_ADAM(true, float, false);
     }
 #undef SS_ADAM
     SS_CHECK_LAUNCH(ctx);
     int64_t rg = (a + 255) / 256;
     if (rg > (int64_t)ctx->num_sms * 32) rg = (int64_t)ctx->num_sms * 32;
     if (model->param_dtype == 1)
-        SS_CUDA(ctx, ss_launch((k_adam_rows<double>), dim3((int)rg), dim3(256), 0, ctx->stream, (double*)model->quaternions,
-                               grad, st->grad_ema, st->age, c, st->skip_if));
+        SS_CUDA(ctx, ss_launch((k_adam_rows<double, false>), dim3((int)rg), dim3(256), 0, ctx->stream,
+                               (double*)model->quaternions, grad, st->grad_ema, st->age, c, st->skip_if, peers));
+    else if (n_peers)
+        SS_CUDA(ctx, ss_launch((k_adam_rows<float, true>), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions,
+                               grad, st->grad_ema, st->age, c, st->skip_if, peers));
     else
-        SS_CUDA(ctx, ss_launch((k_adam_rows<float>), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions, grad,
-                               st->grad_ema, st->age, c, st->skip_if));
+        SS_CUDA(ctx, ss_launch((k_adam_rows<float, false>), dim3((int)rg), dim3(256), 0, ctx->stream, model->quaternions,
+                               grad, st->grad_ema, st->age, c, st->skip_if, peers));
     SS_CHECK_LAUNCH(ctx);
     ss_toc(ctx, KC_ADAM);
     st->step_count = t;
@@ -207,4 +227,9 @@ extern "C" int ss_adam_step(ss_ctx* ctx, ss_model* model, ss_adam_state* st, con
     if (n_views < 1) return ss_fail(ctx, SS_ERR_INVALID, "no ready views");
     if (model->active_count == 0) return SS_OK;  // frozen-only model: no state change (optim.py:374)
     return ss_adam_step_ld(ctx, model, st, grad, model->active_count, n_views, hp);
+}
+
+extern "C" int ss_adam_step_ld(ss_ctx* ctx, ss_model* model, ss_adam_state* st, const float* grad, int64_t ld,
+                               int32_t n_views, const ss_adam_hparams* hp) {
+    return ss_adam_step_peers(ctx, model, st, grad, ld, n_views, hp, 0, nullptr);
 }

@@ -123,6 +123,9 @@ void* ss_scratch(ss_ctx* ctx, size_t bytes);
 #define SS_SCRATCH(ctx, T, n) ((T*)ss_scratch((ctx), sizeof(T) * (size_t)(n)))
 inline size_t ss_align(size_t b) { return (b + 255) & ~size_t(255); }
 
+// peer replicas a fused parameter update can store into (ss_adam_step_peers)
+#define SS_MAX_PEERS 15
+
 // every host synchronisation of the library goes through here (counted)
 inline cudaError_t ss_stream_sync(ss_ctx* ctx) {
     ++ctx->host_syncs;

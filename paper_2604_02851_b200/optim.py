@@ -570,9 +570,11 @@ class _DeviceKernels:
     """The compute of parallel.sharded_step on this GPU (libsplat_b200)."""
 
     def __init__(self, dm: DeviceModel, state: OptimizerState, ws: StepWorkspace, views, subset, extent_cutoff,
-                 plan: parallel.ShardPlan, deterministic=True):
+                 plan: parallel.ShardPlan, deterministic=True, p2p=False):
         self.dm, self.state, self.ws, self.sub, self.cutoff, self.plan = dm, state, ws, subset, extent_cutoff, plan
         self.deterministic = deterministic
+        self.p2p = p2p and plan.world > 1
+        self.window = None
         self.n_in = int(subset.numel()) if subset is not None else dm.count
         B = (dm.sh_degree + 1) ** 2
         self.ld = dm.active_count if plan.world == 1 else plan.R
@@ -611,7 +613,24 @@ class _DeviceKernels:
     def invisible(self, rec):
         rec[1].fill_(-1)  # 0xffffffff: not visible in this view
 
+    def _peer_window(self, coll):
+        """Every rank's slot record buffers and parameter columns, mapped
+        into this process (parallel.PeerWindow; re-shared when reallocated)."""
+        d = self.ws._slots
+        tensors = {"g9": d[0], "rinv": d[1]}
+        tensors.update({k: getattr(self.dm, k) for k in TRAINABLE})
+        win = getattr(self.ws, "_window", None)
+        if win is None or win.key != parallel.PeerWindow.key_of(tensors):
+            win = self.ws._window = parallel.PeerWindow(coll.group, tensors)
+        return win
+
     def exchange(self, coll, send):
+        if self.p2p:
+            # zero-copy: the chain rule reads each rank's records from that
+            # rank's HBM; first every rank's records must be complete
+            self.window = self._peer_window(coll)
+            coll.barrier()
+            return list(range(len(send)))
         P = self.plan.padded
         recv = self.ws.recv_records(len(send), P)
         for (sg, sr), (rg, rr) in zip(send, recv):
@@ -621,6 +640,9 @@ class _DeviceKernels:
 
     def shard_view(self, rec, s):
         """Source rank s's records of this rank's rows, as addresses indexed by row."""
+        if self.p2p:  # rec = the view slot: rank s's own (row-indexed) buffer, mapped here
+            peer = self.window.peers[s]
+            return (peer["g9"][rec].data_ptr(), peer["rinv"][rec].data_ptr())
         R, r0 = self.plan.R, self.plan.row0
         g9, rinv = rec
         return (g9.data_ptr() + (s * R - r0) * 36, rinv.data_ptr() + (s * R - r0) * 4)
@@ -658,11 +680,29 @@ class _DeviceKernels:
             ms = self.dm.struct()
         else:
             ms = _row_struct(self.dm, self.plan.row0, self.plan.rows)
-        c.check(c.lib.ss_adam_step_ld(c.handle, ms, ast, self.grad.data_ptr(), self.ld, n_views, st.hparams()))
+        if self.p2p and self.plan.rows > 0:
+            # the parameter all-gather fused into the update: every row is
+            # also stored into each other rank's replica (peer memory)
+            import ctypes as C
+            B = (self.dm.sh_degree + 1) ** 2
+            widths = dict(means=3, log_scales=3, quaternions=4, logit_opacities=1, sh_coeffs=3 * B)
+            rows = []
+            for r, peer in enumerate(self.window.peers):
+                if r == self.plan.rank:
+                    continue
+                rows += [peer[k].data_ptr() + self.plan.row0 * widths[k] * 4 for k in TRAINABLE]
+            ptrs = (C.c_void_p * len(rows))(*rows)
+            c.check(c.lib.ss_adam_step_peers(c.handle, ms, ast, self.grad.data_ptr(), self.ld, n_views, st.hparams(),
+                                             self.plan.world - 1, ptrs))
+        else:
+            c.check(c.lib.ss_adam_step_ld(c.handle, ms, ast, self.grad.data_ptr(), self.ld, n_views, st.hparams()))
         st.step_count = int(ast.step_count)
         st._host = None  # device moments changed: the host mirror is stale
 
     def gather(self, coll):
+        if self.p2p:  # Adam already stored every row into every replica: order it before any next use
+            coll.barrier()
+            return
         R = self.plan.R
         for k in TRAINABLE:
             t = getattr(self.dm, k)
@@ -674,7 +714,7 @@ class _DeviceKernels:
 
 def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: bool = True, precision: int = 0,
          process_group=None, workspace: Optional[StepWorkspace] = None, sync_loss: bool = True,
-         deterministic: bool = True):
+         deterministic: bool = True, exchange: Optional[str] = None):
     """ref optim.py:353 -- one Adam step over the ready views; returns the mean loss.
 
     With a `process_group` (or a state created with one) every rank passes
@@ -684,6 +724,10 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     (no host synchronisation).  `deterministic=False` selects the backward's
     throughput mode: per-(tile, splat) sums added with float atomics instead
     of the fixed-order partial sums (reruns may differ in the last bits).
+    `exchange` (sharded steps): "p2p" -- the chain rule reads the other
+    ranks' records from their memory and Adam stores the updated rows into
+    every replica (CUDA IPC peer memory; the default on NCCL groups) -- or
+    "collectives" (an all-to-all and an all-gather; the default otherwise).
 
     The fp32 path bins without reading pair counts back (sync-free; see
     ss_render_opts.bins_status): each step leaves a snapshot of its binning
@@ -712,7 +756,11 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
         loss = _step_immediate(dm, state, ready, sub, extent_cutoff, precision, ws, deterministic)
     else:
         _settle(ws, keep=1)  # the step before last: checked (and re-run after an overflow)
-        args = (dm, state, ready, sub, extent_cutoff, pg, deterministic)
+        if exchange is None:
+            exchange = "p2p" if (pg is not None and _backend(pg) == "nccl") else "collectives"
+        if exchange not in ("p2p", "collectives"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        args = (dm, state, ready, sub, extent_cutoff, pg, deterministic, exchange == "p2p")
         loss = _step_binned(ws, *args)
         _note(ws, args)
         if sync_loss or not persistent:
@@ -727,9 +775,14 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     return float(loss.item()) / total
 
 
-def _step_binned(ws, dm, state, ready, sub, extent_cutoff, pg, deterministic):
+def _backend(pg):
+    import torch.distributed as dist
+    return dist.get_backend(pg)
+
+
+def _step_binned(ws, dm, state, ready, sub, extent_cutoff, pg, deterministic, p2p=False):
     plan = state.plan
-    kern = _DeviceKernels(dm, state, ws, ready, sub, extent_cutoff, plan, deterministic)
+    kern = _DeviceKernels(dm, state, ws, ready, sub, extent_cutoff, plan, deterministic, p2p)
     kern.stage(parallel.shard_views(ready, plan.rank, plan.world) if plan.world > 1 else ready)
     coll = parallel.Collectives(pg) if plan.world > 1 else None
     return parallel.sharded_step(kern, ready, plan, coll, CHAIN_MAX_VIEWS)

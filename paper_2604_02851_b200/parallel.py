@@ -27,6 +27,15 @@ So the rows are split into N equal shards (ShardPlan) and the step runs
      optimizer state and of its HBM traffic per rank);
   5. an in-place all-gather of the updated parameter rows (one per group).
 
+With exchange="p2p" (the default on NCCL groups) steps 2 and 5 are fused
+into the kernels over peer memory (PeerWindow: every rank's record buffers
+and parameter columns mapped into every rank by CUDA IPC): the chain rule
+reads the other ranks' records of its rows straight from their HBM over
+NVLink (no all-to-all copy), and Adam stores each updated row into every
+replica as it computes it (ss_adam_step_peers); two one-element all-reduces
+order the phases (records complete before any rank reads them; every
+replica's rows written before any rank's next step reads them).
+
 The per-view losses travel in a V-entry float64 vector (one all-reduce of
 entries that are non-zero on exactly one rank, so exact) and are summed in
 view order like the reference's `loss_sum`.
@@ -103,6 +112,16 @@ class Collectives:
         if o is not out:
             out.copy_(o)
 
+    def barrier(self):
+        """A device-ordered barrier: a one-element all-reduce on the stream
+        (work queued after it starts only once every rank reached it)."""
+        import torch
+        t = getattr(self, "_tick", None)
+        if t is None:
+            dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+            t = self._tick = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.all_reduce_(t)
+
     def all_reduce_(self, t, op="sum"):
         s = self._staged(t)
         self.dist.all_reduce(s, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM,
@@ -121,6 +140,34 @@ class Collectives:
                 out.copy_(o)
         else:  # NCCL gathers in place when the input is the rank's own slice of the output
             self.dist.all_gather_into_tensor(out, out[self.rank * R:(self.rank + 1) * R], group=self.group)
+
+
+class PeerWindow:
+    """Other ranks' device tensors mapped into this process (CUDA IPC; on an
+    NVSwitch box the mapped addresses are the peers' HBM over NVLink): each
+    rank shares `tensors` (name -> CUDA tensor) once, every rank gets every
+    rank's tensors.  `key` identifies the shared buffers (re-share when a
+    buffer is reallocated; every rank reallocates at the same step)."""
+
+    def __init__(self, group, tensors: dict):
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        mine = {k: reduce_tensor(t) for k, t in tensors.items()}
+        objs = [None] * self.world
+        dist.all_gather_object(objs, mine, group=group)
+        self.peers = []
+        for r, o in enumerate(objs):
+            if r == self.rank:
+                self.peers.append(dict(tensors))
+            else:
+                self.peers.append({k: fn(*args) for k, (fn, args) in o.items()})
+        self.key = self.key_of(tensors)
+
+    @staticmethod
+    def key_of(tensors: dict):
+        return tuple((k, int(t.data_ptr()), tuple(t.shape)) for k, t in sorted(tensors.items()))
 
 
 def padded_rows_view(t, rows: int):

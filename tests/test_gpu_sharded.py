@@ -37,7 +37,7 @@ def _scene(n_views):
     return host, tgt, synth.ring_poses(n_views, radius=0.8), synth.intrinsics(W, H), synth.light()
 
 
-def _run(pg, n_views, subset, steps=3):
+def _run(pg, n_views, subset, steps=3, exchange=None):
     import torch
     from paper_2604_02851_b200.model import DeviceModel
     from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
@@ -48,20 +48,20 @@ def _run(pg, n_views, subset, steps=3):
     views = [ReferenceView(p, intr, render_device(tgt, p, intr, light), light, np.zeros(3)) for p in poses]
     state = OptimizerState(dm, scene_extent=2.0, process_group=pg)
     ws = StepWorkspace(dm)
-    losses = [step(dm, state, views, index_subset=subset, workspace=ws) for _ in range(steps)]
+    losses = [step(dm, state, views, index_subset=subset, workspace=ws, exchange=exchange) for _ in range(steps)]
     torch.cuda.synchronize()
     return (dm.to_host(), {k: v.copy() for k, v in state.m.items()}, {k: v.copy() for k, v in state.v.items()},
             state.age.copy(), state.grad_ema.copy(), losses, state.step_count)
 
 
-def _worker(rank, world, port, n_views, use_subset, out):
+def _worker(rank, world, port, n_views, use_subset, exchange, out):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     subset = _subset() if use_subset else None
-    m, mm, vv, age, ema, losses, t = _run(dist.group.WORLD, n_views, subset)
+    m, mm, vv, age, ema, losses, t = _run(dist.group.WORLD, n_views, subset, exchange=exchange)
     out.put((rank, {k: getattr(m, k) for k in GROUPS}, mm, vv, age, ema, losses, t))
     dist.barrier()
     dist.destroy_process_group()
@@ -72,15 +72,20 @@ def _subset():
     return np.sort(rng.choice(30_000, 21_000, replace=False))
 
 
-@pytest.mark.parametrize("n_views,use_subset", [(4, False), (3, True)])
-def test_gpu_sharded_step_bit_identical(n_views, use_subset):
+@pytest.mark.parametrize("n_views,use_subset,exchange", [(4, False, "collectives"), (3, True, "collectives"),
+                                                         (4, False, "p2p"), (3, True, "p2p")])
+def test_gpu_sharded_step_bit_identical(n_views, use_subset, exchange):
+    """exchange="collectives": an all-to-all of the records and an all-gather of
+    the parameter rows; "p2p": the chain rule reads the peers' records from
+    their memory and Adam stores every updated row into the peers' replicas
+    (CUDA IPC -- here two processes on one device)."""
     require_gpu()
     import torch.multiprocessing as mp
     ref = _run(None, n_views, _subset() if use_subset else None)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_views, use_subset, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_views, use_subset, exchange, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=600) for _ in range(2)), key=lambda x: x[0])
