@@ -257,7 +257,15 @@ def workload_config(args):
                          "tick (raw)"),
             "gaussians": args.n, "views_per_step": args.views, "resolution": f"{args.width}x{args.height}",
             "sh_degree": args.degree, "l2": "no flush: per-step working set (244 MB model, 944 MB Adam moments, "
-                                            "~190 MB partials, 199 MB GT) exceeds the 126 MB L2"}
+                                            "~190 MB partials, 199 MB GT) exceeds the 126 MB L2",
+            "view_lanes": _view_lanes(),
+            "kernel_timing": "kernel_ms_per_step / roofline / gpu_launches from a second pass of the same steps "
+                             "with the view lanes on one stream (each kernel timed alone)"}
+
+
+def _view_lanes():
+    from paper_2604_02851_b200 import optim
+    return optim.VIEW_LANES
 
 
 # ---------------------------------------------------------------- our arm
@@ -266,6 +274,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2604_02851_b200 import _lib
+    from paper_2604_02851_b200 import optim as optim_mod
     from paper_2604_02851_b200.model import DeviceModel
     from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
     from paper_2604_02851_b200.protocol import DeltaTicker, PayloadBuffer, encode_snapshot_device
@@ -342,8 +351,6 @@ def run_ours(args):
     torch.cuda.synchronize()
     if pg is not None:
         dist.barrier()
-    _lib.set_timing(c, True)
-    _lib.get_timing(c, reset=True)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -361,9 +368,21 @@ def run_ours(args):
         dist.barrier()
     w1 = time.time()
     ms = t0.elapsed_time(t1)
+    clock_rec = clocks.stop(w0, w1)
+    # per-class device time, launch count and the dominant kernel's launch
+    # time: the same steps again (library CUDA events around every launch
+    # group), the view lanes serialised on one stream so each kernel is
+    # timed alone rather than stretched by a concurrent lane
+    lanes = optim_mod.VIEW_LANES
+    optim_mod.VIEW_LANES = 1
+    _lib.set_timing(c, True)
+    _lib.get_timing(c, reset=True)
+    for i in range(args.steps):
+        one_step(args.warmup + args.steps + i)
+    torch.cuda.synchronize()
     kt, counters = _lib.get_timing(c, reset=True)
     _lib.set_timing(c, False)
-    clock_rec = clocks.stop(w0, w1)
+    optim_mod.VIEW_LANES = lanes
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if pg is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)

@@ -287,21 +287,79 @@ def ctx(device=None) -> Context:
     return c
 
 
+def lane_ctx(device: int, lane: int) -> Context:
+    """Context of view lane `lane` on `device` (lane 0 is ctx(device)); each
+    lane owns its own scratch arena, so lanes bound to different streams run
+    concurrently.  Binds the current torch stream."""
+    if lane == 0:
+        return ctx(device)
+    cache = getattr(_ctx, "lanes", None)
+    if cache is None:
+        cache = _ctx.lanes = {}
+    key = (int(device), int(lane))
+    c = cache.get(key)
+    if c is None:
+        c = cache[key] = Context(int(device))
+        main = ctx(device)
+        cap = c.lib.ss_pair_capacity(main.handle, 0)
+        if cap > 0:
+            c.lib.ss_pair_capacity(c.handle, cap)
+        if getattr(main, "timing", False):
+            c.check(c.lib.ss_set_timing(c.handle, 1))
+            c.timing = True
+    c.bind_stream()
+    return c
+
+
+def device_contexts(device: int):
+    """Every context of `device` in this thread (the main one first)."""
+    out = [ctx(device)]
+    for (d, _), c in sorted(getattr(_ctx, "lanes", {}).items()):
+        if d == int(device):
+            out.append(c)
+    return out
+
+
+def pair_capacity(device: int, cap: int = 0) -> int:
+    """ss_pair_capacity on every context of the device; returns the main one's."""
+    cs = device_contexts(device)
+    for c in cs[1:]:
+        c.lib.ss_pair_capacity(c.handle, cap)
+    return cs[0].lib.ss_pair_capacity(cs[0].handle, cap)
+
+
+def host_syncs(device: int) -> int:
+    """ss_host_syncs summed over the device's contexts."""
+    return sum(c.lib.ss_host_syncs(c.handle) for c in device_contexts(device))
+
+
 KERNEL_CLASSES = ("preprocess", "depth_sort", "binning", "tile_sort", "blend_forward", "blend_backward",
                   "chain_rule", "adam", "encoders")
 
 
 def set_timing(c: "Context", on: bool):
-    c.check(c.lib.ss_set_timing(c.handle, 1 if on else 0))
+    """Per-kernel-class timing on c and on every view lane of its device."""
+    for x in device_contexts(c.device):
+        x.check(x.lib.ss_set_timing(x.handle, 1 if on else 0))
+        x.timing = bool(on)
 
 
 def get_timing(c: "Context", reset=True):
-    """{class: (ms, launch groups)}, counters (evaluated pairs, kernel launches)."""
-    ms = (f64 * 9)()
-    groups = (i64 * 9)()
-    cnt = (u64 * 4)()
-    c.check(c.lib.ss_get_timing(c.handle, ms, groups, cnt, 1 if reset else 0))
-    return {k: (ms[i], groups[i]) for i, k in enumerate(KERNEL_CLASSES)}, list(cnt)
+    """{class: (ms, launch groups)}, counters (evaluated pairs, kernel launches),
+    summed over c's device's contexts (view lanes overlap in time: the sum
+    is device time per class, not wall time)."""
+    tot = {k: [0.0, 0] for k in KERNEL_CLASSES}
+    cnt_tot = [0, 0, 0, 0]
+    for x in device_contexts(c.device):
+        ms = (f64 * 9)()
+        groups = (i64 * 9)()
+        cnt = (u64 * 4)()
+        x.check(x.lib.ss_get_timing(x.handle, ms, groups, cnt, 1 if reset else 0))
+        for i, k in enumerate(KERNEL_CLASSES):
+            tot[k][0] += ms[i]
+            tot[k][1] += groups[i]
+        cnt_tot = [a + b for a, b in zip(cnt_tot, cnt)]
+    return {k: (v[0], v[1]) for k, v in tot.items()}, cnt_tot
 
 
 def ptr(t) -> vp:

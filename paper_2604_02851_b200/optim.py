@@ -18,6 +18,7 @@ bit-identical to the single-GPU step.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -173,12 +174,13 @@ def _tile_order(view, device):
 
 def backward_device(model: DeviceModel, view, grad_accum, loss_accum, index_subset=None, extent_cutoff=True,
                     precision=0, image_out=None, subset_tensor=None, gt=None, defer=None, deterministic=True,
-                    bins_status=None):
+                    bins_status=None, ctx=None):
     """Accumulate one view's gradients into `grad_accum` (flat float32) and
     its loss into `loss_accum` (float64 CUDA scalar).  With `defer` =
     (g9, rinv) device buffers the view's screen-space gradients are left
-    there for one `chain_views` call over all the step's views."""
-    c = _lib.ctx(model.device.index)
+    there for one `chain_views` call over all the step's views.  `ctx`: the
+    library context to run on (a view lane's, see _DeviceKernels)."""
+    c = ctx if ctx is not None else _lib.ctx(model.device.index)
     ready = None
     if gt is None:
         gt = _gt_tensor(view, model.device)
@@ -527,6 +529,9 @@ class StepWorkspace:
 
 
 CHAIN_MAX_VIEWS = 16  # ss_chain_views
+# concurrent view lanes of a step (streams; see _DeviceKernels._lane)
+VIEW_LANES = max(1, int(os.environ.get("SS_VIEW_LANES", "2")))
+_LANE_STREAMS = {}
 
 
 def chain_views(model: DeviceModel, views, g9, rinv, grad, subset_tensor=None, j0=0, j1=None, row0=0, rows=None,
@@ -581,6 +586,8 @@ class _DeviceKernels:
         self.grad = ws.prepare(self.ld * (11 + 3 * B), len(views))
         self.gts = {}
         self.views = views
+        self.lanes = None
+        self._n_local = 0
 
     def stage(self, local_views):
         gts = _stage_ground_truth(local_views, self.dm.device)
@@ -592,7 +599,44 @@ class _DeviceKernels:
     def records(self, slots):
         return self.ws.slot_records(slots, self._rows_alloc())
 
+    def _lane(self, t):
+        """(stream, context) of the t-th local view: views alternate over
+        VIEW_LANES streams, each with its own library context (scratch
+        arena), so one view's latency-bound preprocess / sorts / binning
+        overlap the previous view's blend kernels.  Lane 0 is the caller's
+        stream; the others fork from it at the first view (join())."""
+        import torch
+        L = VIEW_LANES
+        dev = self.dm.device
+        if self.lanes is None:
+            cur = torch.cuda.current_stream(dev)
+            self.lanes = [(cur, None)]
+            pool = _LANE_STREAMS.setdefault(dev.index, [])
+            while len(pool) < L - 1:
+                pool.append(torch.cuda.Stream(dev))
+            for k in range(1, L):
+                pool[k - 1].wait_stream(cur)
+                self.lanes.append((pool[k - 1], None))
+        return t % L, self.lanes[t % L][0]
+
+    def join(self):
+        """The caller's stream waits for every view lane."""
+        import torch
+        if self.lanes is None:
+            return
+        cur = self.lanes[0][0]
+        for s, _ in self.lanes[1:]:
+            cur.wait_stream(s)
+        self.lanes = None
+
     def backward(self, view, rec, i):
+        import torch
+        k, stream = self._lane(self._n_local)
+        self._n_local += 1
+        with torch.cuda.stream(stream):
+            self._backward(view, rec, i, _lib.lane_ctx(self.dm.device.index, k))
+
+    def _backward(self, view, rec, i, ctx):
         import torch
         g9, rinv = rec
         sharded_subset = self.plan.world > 1 and self.sub is not None
@@ -604,7 +648,7 @@ class _DeviceKernels:
             defer = (g9[:self.n_in], rinv[:self.n_in])
         backward_device(self.dm, view, self.grad, self.ws.losses[i:i + 1], None, self.cutoff, 0, None,
                         subset_tensor=self.sub, gt=self.gts[id(view)], defer=defer, deterministic=self.deterministic,
-                        bins_status=self.ws.bins_status)
+                        bins_status=self.ws.bins_status, ctx=ctx)
         if sharded_subset:
             rinv.fill_(-1)
             g9[self.sub] = tmp_g9
@@ -822,9 +866,8 @@ def _recover(ws):
     ws.pending = []
     st = ws.bins_status.cpu()
     dev = redo[0][2][0].device
-    c = _lib.ctx(dev.index)
     need = int(st[1])
-    c.lib.ss_pair_capacity(c.handle, need + need // 4 + 65536)
+    _lib.pair_capacity(dev.index, need + need // 4 + 65536)
     ws.bins_status.zero_()
     state = redo[0][2][1]
     # every pending step left the state alone: restart from the first one's count

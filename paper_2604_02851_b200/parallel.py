@@ -204,6 +204,9 @@ def sharded_step(kern, views, plan: ShardPlan, coll=None, batch: int = 16):
         for k in range(slots):
             if k not in used:  # a rank with fewer views than the busiest: nothing visible
                 kern.invisible(send[k])
+        join = getattr(kern, "join", None)
+        if join is not None:  # the backward passes may run on several streams
+            join()
         if N > 1:
             recv = kern.exchange(coll, send)
             recs = [kern.shard_view(recv[view_slot(t, N)[1]], view_slot(t, N)[0]) for t in range(len(idx))]

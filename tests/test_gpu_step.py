@@ -198,7 +198,7 @@ def test_gpu_sync_free_binning_overflow_recovers(sync_loss):
         losses = []
         for i in range(4):
             if cap is not None and i in (0, 2):
-                c.lib.ss_pair_capacity(c.handle, -cap)  # force an overflow at steps 0 and 2
+                _lib.pair_capacity(0, -cap)  # force an overflow at steps 0 and 2
             L = step(dm, state, views, workspace=ws, sync_loss=sync_loss)
             losses.append(float(L) if sync_loss else L)
         ws.flush()
@@ -214,7 +214,7 @@ def test_gpu_sync_free_binning_overflow_recovers(sync_loss):
     for k in GROUPS:
         np.testing.assert_array_equal(state.m[k], ref_state.m[k])
     assert int(ws.bins_status[0]) == 0 and not ws.pending
-    assert c.lib.ss_pair_capacity(c.handle, 0) > 1000
+    assert _lib.pair_capacity(0, 0) > 1000
 
 
 def test_gpu_step_issues_no_host_sync():
@@ -243,9 +243,9 @@ def test_gpu_step_issues_no_host_sync():
     ws.flush()
     torch.cuda.synchronize()
     c = _lib.ctx(0)
-    before = c.lib.ss_host_syncs(c.handle)
+    before = _lib.host_syncs(0)
     for _ in range(4):
         step(dm, state, views, workspace=ws, sync_loss=False)
-    assert c.lib.ss_host_syncs(c.handle) == before
+    assert _lib.host_syncs(0) == before
     ws.flush()
     assert state.step_count == 7
