@@ -577,6 +577,12 @@ __global__ void __launch_bounds__(32 * WPB) k_blend_fwd(const uint2* __restrict_
 }
 
 // ---------------------------------------------------------------- K6 backward
+// the colour clamp's gradient mask from the forward's clamped colour:
+// col = clamp(color_pre, 0, 1) lies strictly inside (0, 1) exactly when
+// color_pre does (ref optim.py:176-177)
+template <typename R>
+__device__ __forceinline__ bool clamp_open(R col) { return col > (R)0 && col < (R)1; }
+
 // Transposed butterfly: reduces v[0..7] over the warp with 7+2 shuffles;
 // lane l with (l & 3) == 0 ends with the sum of value index
 // 4*bit4(l) + 2*bit3(l) + bit2(l).
@@ -770,9 +776,13 @@ __global__ void __launch_bounds__(32 * WPB_BWD) k_blend_bwd(const uint2* __restr
                 const R z = warp_sum<R>(acc[8]);
                 if ((lane & 3) == 0 && fits) {
                     const int e = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                    const R v = e >= 6 ? (R)0.5 * y : y;
-                    if (ATOMIC) atomicAdd(out + e, v);
-                    else out[e] = v;
+                    R v = e >= 6 ? (R)0.5 * y : y;
+                    if (ATOMIC) {  // no partial-sum pass: the clamp mask here
+                        if (e < 3 && !clamp_open(e == 0 ? s.c0 : (e == 1 ? s.c1 : s.c2))) v = (R)0;
+                        atomicAdd(out + e, v);
+                    } else {
+                        out[e] = v;
+                    }
                 }
                 if (lane == 0 && fits) {
                     if (ATOMIC) atomicAdd(out + 8, (R)0.5 * z);
@@ -1083,6 +1093,7 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, doubl
 template <typename R>
 __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
                                                       const uint32_t* __restrict__ dvals, const R* __restrict__ partials,
+                                                      const SplatRec<R>* __restrict__ rec,
                                                       int64_t n_in, R* __restrict__ g9, uint64_t cap) {
     SS_PDL_WAIT();
     constexpr int PW = 4096 / (9 * sizeof(R));  // pairs per staged chunk (4 KB per warp)
@@ -1125,8 +1136,13 @@ __global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict
             __syncwarp();
         }
         if (valid) {
-            SS_ASSERT(dvals[r] < (uint64_t)n_in);
-            R* o = g9 + (int64_t)dvals[r] * 9;
+            const uint32_t j = dvals[r];
+            SS_ASSERT(j < (uint64_t)n_in);
+            R* o = g9 + (int64_t)j * 9;
+            if (cnt) {  // dL/dcolour through the clamp: zero where the forward clamped (optim.py:176-177)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) g[c] = clamp_open(rec[j].col[c]) ? g[c] : (R)0;
+            }
 #pragma unroll
             for (int e = 0; e < 9; ++e) o[e] = g[e];
         }
@@ -1180,25 +1196,39 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     Rq[0][0] = 1 - 2 * (qy * qy + qz * qz); Rq[0][1] = 2 * (qx * qy - w * qz); Rq[0][2] = 2 * (qx * qz + w * qy);
     Rq[1][0] = 2 * (qx * qy + w * qz); Rq[1][1] = 1 - 2 * (qx * qx + qz * qz); Rq[1][2] = 2 * (qy * qz - w * qx);
     Rq[2][0] = 2 * (qx * qz - w * qy); Rq[2][1] = 2 * (qy * qz + w * qx); Rq[2][2] = 1 - 2 * (qx * qx + qy * qy);
+    // dL/dcolour arrives masked by the forward's clamp (the partial sums zero
+    // the channels whose pre-clamp colour was outside (0, 1): optim.py:176-177
+    // with the preprocess's own color_pre, as the reference reads
+    // prepared.color_pre), so the shading is not re-evaluated here; only its
+    // terms the gradient needs: the normal proxy's cosine, visibility, albedo
+    // (ss_shade_v's expressions) and, for the view-direction path, the SH dot.
     T gc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) gc[c] = g[c];
     T gv[3] = {0, 0, 0};
-    Shade<DEG, T> S;
+    T albedo[3];
+    T cosv, vis, sgn_s;
     {
-        PT sh[3 * B];
-        ss_load_sh<DEG, PT>(pv.sh + row * 3 * B, sh);
-        ss_shade_v<DEG, T, PT>(L, lsp, sh, pv.vis[row], d, Rq, S);
+        T nhat[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-            gc[c] = (S.pre[c] > (T)0 && S.pre[c] < (T)1) ? g[c] : (T)0;  // clamp mask (optim.py:176-177)
+        for (int i = 0; i < 3; ++i) nhat[i] = axis == 0 ? Rq[i][0] : (axis == 1 ? Rq[i][1] : Rq[i][2]);
+        sgn_s = nhat[0] * (T)-L.direction[0] + nhat[1] * (T)-L.direction[1] + nhat[2] * (T)-L.direction[2];
+        cosv = fabs(sgn_s);
+        vis = (T)pv.vis[row];
+        const PT* shr = pv.sh + row * 3 * B;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) albedo[c] = (T)SS_SH_C0 * (T)shr[c * B] + (T)0.5;
         if constexpr (DEG > 0) {
-            T coef[B];
+            if (gc[0] != (T)0 || gc[1] != (T)0 || gc[2] != (T)0) {
+                PT sh[3 * B];
+                ss_load_sh<DEG, PT>(shr, sh);
+                T coef[B];
 #pragma unroll
-            for (int k = 0; k < B; ++k) coef[k] = sh[k] * gc[0] + sh[B + k] * gc[1] + sh[2 * B + k] * gc[2];
-            ss_sh_grad_dot<DEG, T>(vdir, coef, gv);
+                for (int k = 0; k < B; ++k) coef[k] = sh[k] * gc[0] + sh[B + k] * gc[1] + sh[2 * B + k] * gc[2];
+                ss_sh_grad_dot<DEG, T>(vdir, coef, gv);
+            }
         }
     }
-    const T* albedo = S.albedo;
-    const T cosv = S.cosv, vis = S.vis, sgn_s = S.s;
     // SH coefficient gradients: written by k_sh_grad from this compact record
     shrec_row[0] = make_float4((float)gc[0], (float)gc[1], (float)gc[2], (float)(cosv * vis));
     shrec_row[1] = make_float4((float)vdir[0], (float)vdir[1], (float)vdir[2], 1.0f);
@@ -1411,8 +1441,63 @@ struct ChainViews {
 // Inputs j in [j0, j1) (row = subset[j], or j); the gradient layout starts at
 // row0 with ld rows per group (ld = a, row0 = 0 on one GPU; a row shard in
 // the view-sharded step, whose g9 / rinv pointers are offset to be indexed by j).
+// SH coefficient gradients of one row from its per-view records (gc, cos vis,
+// view dir): g_sh[c, b] += gc_{v,c} K_{v,c,b} in view order with
+//   K = [b < BL] ambient[c][b] + [b >= 1] Y_b(view dir) + [b == 0] C0 I_c cos vis
+// (ambient light; without it K = Y_b + [b == 0] C0 I_c cos vis) -- ref
+// optim.py:221-233: the ambient product, the view-dependent basis and the
+// direct-light term through albedo_est = C0 dc + 0.5.  `rec` is the row's
+// record of view v at rec[v * stride]; io holds the row's 3B entries.
 template <int DEG>
-__global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const __grid_constant__ ChainViews Vp, int nv,
+__device__ __forceinline__ void sh_grad_row(const ChainViews* V, int nv, const float4* rec, int stride, float* io) {
+    constexpr int B = ss_sh_bases(DEG);
+    float acc[3 * B];
+    bool loaded = false;
+    for (int v = 0; v < nv; ++v) {
+        const float4 r0 = rec[(size_t)v * stride];
+        if (r0.x == 0.f && r0.y == 0.f && r0.z == 0.f) continue;  // clamped colour or not visible
+        if (!loaded) {
+#pragma unroll
+            for (int e = 0; e < 3 * B; ++e) acc[e] = io[e];
+            loaded = true;
+        }
+        const float4 r1 = rec[(size_t)v * stride + 1];
+        const float dir[3] = {r1.x, r1.y, r1.z};
+        float Y[B];
+        ss_sh_eval<DEG, float>(dir, Y);
+        const ss_light& L = V->light[v];
+        const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
+            if (gcc == 0.f) continue;
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                float kv;
+                if (L.ambient_bands == 0) kv = Y[b];
+                else kv = (b < BL ? (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? Y[b] : 0.f);
+                if (b == 0) kv += (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
+                acc[c * B + b] = fmaf(gcc, kv, acc[c * B + b]);
+            }
+        }
+    }
+    if (loaded) {
+#pragma unroll
+        for (int e = 0; e < 3 * B; ++e) io[e] = acc[e];
+    }
+}
+
+constexpr int CVB = 128;  // rows (threads) per block of k_chain_views / k_sh_grad_rows
+__host__ __device__ constexpr int cv_sh_stride(int B) { return (3 * B + 1) | 1; }  // odd: conflict-free rows
+
+// Inputs j in [j0, j1) (row = subset[j], or j); the gradient layout starts at
+// row0 with ld rows per group (ld = a, row0 = 0 on one GPU; a row shard in
+// the view-sharded step, whose g9 / rinv pointers are offset to be indexed
+// by j).  Per row every view in order, the 11 non-SH gradient entries read
+// and written once; each (view, row) leaves its compact SH record in shrec
+// for k_sh_grad_rows.
+template <int DEG>
+__global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const __grid_constant__ ChainViews Vp, int nv,
                                                         const int64_t* __restrict__ subset, int64_t j0, int64_t j1,
                                                         int64_t row0, int64_t ld,
                                                         float* __restrict__ grad, float4* __restrict__ shrec) {
@@ -1430,7 +1515,10 @@ __global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const 
         for (int v = 1; v < nv; ++v) asm volatile("prefetch.global.L1 [%0];" ::"l"(V->g9[v] + j * 9));
 #endif
         for (int v = 0; v < nv; ++v) {
-            if (V->rinv[v][j] == ~0u) continue;
+            if (V->rinv[v][j] == ~0u) {  // not visible: a zero record
+                shrec[((int64_t)v * ld + rel) * 2] = make_float4(0.f, 0.f, 0.f, 0.f);
+                continue;
+            }
             if (!any) {
                 grad_row_load(grad, ld, rel, acc);
                 any = true;
@@ -1441,6 +1529,31 @@ __global__ void __launch_bounds__(128, CV_MINB) k_chain_views(ss_model m, const 
             chain_row<float, DEG>(m, V->cam[v], V->light[v], row, g, acc, shrec + ((int64_t)v * ld + rel) * 2);
         }
         if (any) grad_row_store(grad, ld, rel, acc);
+    }
+}
+
+// The SH gradients of rows [0, rows) of the layout from the step's records
+// (sh_grad_row), one thread per row; a block's SH rows are contiguous, so
+// they are staged through shared memory (coalesced reads and writes, the
+// row's 3B entries in registers across the views).
+template <int DEG>
+__global__ void __launch_bounds__(CVB) k_sh_grad_rows(const __grid_constant__ ChainViews Vp, int nv,
+                                                      const float4* __restrict__ shrec, int64_t rows, int64_t ld,
+                                                      float* __restrict__ grad_sh) {
+    SS_PDL_WAIT();
+    constexpr int B = ss_sh_bases(DEG);
+    constexpr int S = cv_sh_stride(B);
+    __shared__ float s_sh[CVB * S];
+    const int t = threadIdx.x;
+    for (int64_t rb = (int64_t)blockIdx.x * CVB; rb < rows; rb += (int64_t)gridDim.x * CVB) {
+        const int nr = (int)min((int64_t)CVB, rows - rb);
+        float* gb = grad_sh + rb * 3 * B;
+        for (int e = t; e < nr * 3 * B; e += CVB) s_sh[(e / (3 * B)) * S + e % (3 * B)] = gb[e];
+        __syncthreads();
+        if (t < nr) sh_grad_row<DEG>(&Vp, nv, shrec + (rb + t) * 2, (int)(2 * ld), s_sh + t * S);
+        __syncthreads();
+        for (int e = t; e < nr * 3 * B; e += CVB) gb[e] = s_sh[(e / (3 * B)) * S + e % (3 * B)];
+        __syncthreads();
     }
 }
 
@@ -1514,72 +1627,6 @@ __global__ void __launch_bounds__(256) k_sh_grad(ss_light L, const float4* __res
         }
         if (b == 0) v += gcc * (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
         out[e] += v;
-    }
-}
-
-// SH gradients of all the step's views (ss_chain_views): g_sh[row, c, b] +=
-// gc_{v,c} * K_{v,row,c,b} for the views in view order, with
-//   K = [b < BL] ambient[c][b] + [b >= 1] Y_b(view dir) + [b == 0] C0 I_c cos vis
-// (ambient light; without it K = Y_b + [b == 0] C0 I_c cos vis) -- ref
-// optim.py:221-233: the ambient product, the view-dependent basis and the
-// direct-light term through albedo_est = C0 dc + 0.5.  Phase 1 builds K and
-// gc per (view, row, channel) in shared memory (one thread per item, the
-// branches resolved once); phase 2 gives each (row, channel, basis) entry one
-// FMA per view, the entry read and written once.
-#ifndef SS_SHGV_ROWS
-#define SS_SHGV_ROWS 16
-#endif
-constexpr int SHGV_ROWS = SS_SHGV_ROWS;
-
-template <int DEG>
-__global__ void __launch_bounds__(256) k_sh_grad_views(const __grid_constant__ ChainViews Vp, int nv,
-                                                       const float4* __restrict__ shrec, int64_t a, int64_t ld,
-                                                       float* __restrict__ grad_sh) {
-    SS_PDL_WAIT();
-    const ChainViews* V = &Vp;
-    constexpr int B = ss_sh_bases(DEG);
-    extern __shared__ float s_dynf[];
-    constexpr int KS = B + 1;                          // padded: one item per bank offset
-    float* s_k = s_dynf;                               // [nv][SHGV_ROWS][3][KS]
-    float* s_g = s_dynf + nv * SHGV_ROWS * 3 * KS;     // [nv][SHGV_ROWS][3]
-    const int64_t row0 = (int64_t)blockIdx.x * SHGV_ROWS;
-    const int nrows = (int)min((int64_t)SHGV_ROWS, a - row0);
-    for (int t = threadIdx.x; t < nv * SHGV_ROWS * 3; t += blockDim.x) {
-        const int c = t % 3, vr = t / 3, v = vr / SHGV_ROWS, r = vr - v * SHGV_ROWS;
-        float* k = s_k + (size_t)t * KS;
-        if (r >= nrows) continue;
-        const float4* rec = shrec + ((int64_t)v * ld + row0 + r) * 2;
-        const float4 r0 = rec[0], r1 = rec[1];
-        const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
-        s_g[t] = gcc;
-        const float dir[3] = {r1.x, r1.y, r1.z};
-        float Y[B];
-        ss_sh_eval<DEG, float>(dir, Y);
-        const ss_light& L = V->light[v];
-        const int BL = L.ambient_bands < B ? L.ambient_bands : B;
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-            float kv;
-            if (L.ambient_bands == 0) kv = Y[b];
-            else kv = (b < BL ? (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? Y[b] : 0.f);
-            if (b == 0) kv += (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
-            k[b] = kv;
-        }
-    }
-    __syncthreads();
-    const int n = nrows * 3 * B;
-    float* out = grad_sh + row0 * 3 * B;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {  // e = (r * 3 + c) * B + b, coalesced over the rows
-        const int rc = e / B, b = e - rc * B;
-        float acc = out[e];
-        bool touched = false;
-        for (int v = 0; v < nv; ++v) {
-            const float gcc = s_g[v * SHGV_ROWS * 3 + rc];
-            if (gcc == 0.f) continue;  // clamped colour or row not visible in this view
-            acc = fmaf(gcc, s_k[(v * SHGV_ROWS * 3 + rc) * KS + b], acc);
-            touched = true;
-        }
-        if (touched) out[e] = acc;
     }
 }
 
@@ -1868,19 +1915,18 @@ int launch_chain_views(ss_ctx* ctx, const ss_model* m, const ChainViews& hv, int
     cudaStream_t s = ctx->stream;
     float4* shrec = SS_SCRATCH(ctx, float4, 2 * ld * nv);
     if (!shrec) return SS_ERR_CUDA;
-    SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)ld * nv, s));
+    // without a subset k_chain_views writes every (view, row) record of rows
+    // [0, rows) (a zero one where the row is not visible); a subset leaves
+    // the other rows' records to this clear
+    if (subset) SS_CUDA(ctx, cudaMemsetAsync(shrec, 0, sizeof(float4) * 2 * (size_t)ld * nv, s));
     ss_tic(ctx, KC_CHAIN);
 #define SS_CHAINV(DEG)                                                                                                     \
     do {                                                                                                                   \
-        constexpr int B = ss_sh_bases(DEG);                                                                                \
-        SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, j1 - j0, 128)), dim3(128), 0, s, *m, hv,                  \
+        SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, j1 - j0, CVB)), dim3(CVB), 0, s, *m, hv,              \
                                nv, subset, j0, j1, row0, ld, grad, shrec));                                                \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
-        const size_t smem = (size_t)nv * SHGV_ROWS * 3 * (B + 2) * sizeof(float);  /* K (B + 1 padded) + gc */          \
-        if (smem > 48 * 1024)                                                                                              \
-            SS_CUDA(ctx, cudaFuncSetAttribute(k_sh_grad_views<DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        SS_CUDA(ctx, ss_launch((k_sh_grad_views<DEG>), dim3((unsigned)((rows + SHGV_ROWS - 1) / SHGV_ROWS)), dim3(256), smem, s, \
-                               hv, nv, (const float4*)shrec, rows, ld, grad + 11 * ld));                                  \
+        SS_CUDA(ctx, ss_launch((k_sh_grad_rows<DEG>), dim3(gridn(ctx, rows, CVB)), dim3(CVB), 0, s, hv, nv,               \
+                               (const float4*)shrec, rows, ld, grad + 11 * ld));                                          \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
     } while (0)
     switch (m->sh_degree) {
@@ -1946,7 +1992,7 @@ int backward_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_li
     if (chain && !atomic) {  // fixed-order sum of each splat's per-tile partials
         ss_tic(ctx, KC_CHAIN);
         SS_CUDA(ctx, ss_launch((k_sum_partials<R>), dim3(gridn(ctx, b.n_in)), dim3(256), 0, s, b.roff, b.rcnt, b.dvals,
-                               partials, b.n_in, g9, (uint64_t)b.pairs));
+                               partials, (const SplatRec<R>*)b.rec, b.n_in, g9, (uint64_t)b.pairs));
         SS_CHECK_LAUNCH(ctx);
         ss_toc(ctx, KC_CHAIN);
     }

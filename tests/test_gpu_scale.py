@@ -116,6 +116,10 @@ def test_gpu_config3_scale_crops_through_bench_path():
                 rows = prep["rows"][inside]
                 assert rows.size > 50, (crop, rows.size)
                 assert (rinv[rows] != -1).all()
+                # the records carry dL/dcolour through the clamp (zero where the
+                # forward clamped the colour: optim.py:176-177)
+                pre = prep["color_pre"]
+                gc = np.where((pre > 0) & (pre < 1), gc, 0.0)
                 ref = np.concatenate([gc, go[:, None], gm, gs], 1)[inside]
                 got = g9[rows]
                 for name, sl in (("colour", slice(0, 3)), ("opacity", slice(3, 4)), ("mean2d", slice(4, 6)),
