@@ -103,7 +103,10 @@ def _stage_ground_truth(views, device):
     """Device ground truth per view.  Host images (pinned CPU tensors or
     numpy) are all uploaded up front on a side stream, each view's kernels
     waiting only for its own copy, so H2D overlaps the previous views'
-    backward passes."""
+    backward passes.  Two persistent buffer sets alternate between calls:
+    a step's uploads wait only for the step before the previous one (the
+    last reader of their set), so they run during the previous step instead
+    of stalling the start of this one."""
     import torch
     if all(isinstance(v.image, torch.Tensor) and v.image.is_cuda for v in views):
         return [_gt_tensor(v, device) for v in views]
@@ -111,11 +114,19 @@ def _stage_ground_truth(views, device):
     cs = _COPY_STREAMS.get(device.index)
     if cs is None:
         cs = _COPY_STREAMS[device.index] = torch.cuda.Stream(device)
-    # the copies wait for everything queued before this step, so one
-    # persistent device buffer per view slot is safe to refill every step (no
-    # allocator churn: fresh blocks would mean synchronising cudaMallocs)
-    cs.wait_stream(cur)
-    pool = _GT_POOL.setdefault(device.index, [])
+    st = _GT_POOL.setdefault(device.index, {"sets": ([], []), "k": 0, "prev": None})
+    k = st["k"]
+    st["k"] = k + 1
+    pool = st["sets"][k % 2]
+    # everything queued so far (through the previous step); the set used two
+    # calls ago was last read before the event recorded at the previous call
+    now = torch.cuda.Event()
+    now.record(cur)
+    if st["prev"] is not None:
+        cs.wait_event(st["prev"])
+    else:
+        cs.wait_stream(cur)
+    st["prev"] = now
     out = []
     with torch.cuda.stream(cs):
         for i, v in enumerate(views):
@@ -126,6 +137,8 @@ def _stage_ground_truth(views, device):
             if i >= len(pool):
                 pool.append(None)
             if pool[i] is None or tuple(pool[i].shape) != shape:
+                if pool[i] is not None:  # a reshaped slot: the old buffer may still be read
+                    cs.wait_stream(cur)
                 pool[i] = torch.empty(shape, dtype=torch.float32, device=device)
             t = pool[i]
             t.copy_(img, non_blocking=True)

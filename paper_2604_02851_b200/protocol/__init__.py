@@ -311,6 +311,11 @@ class DeltaTicker:
             jobs = self._build(key)  # may grow (reallocate) output buffers:
             full = self._key(attributes)  # key the jobs by the pointers they hold
             self._jobs[full] = jobs
+        import torch
+        done = getattr(self, "_read_done", None)
+        if done is not None:  # the last read_async's copies of the output buffers (side stream)
+            torch.cuda.current_stream(self.model.device).wait_event(done)
+            self._read_done = None
         c = self._ctx
         c.bind_stream()
         c.check(c.lib.ss_encode_delta_batch(c.handle, jobs, len(key)))
@@ -319,8 +324,10 @@ class DeltaTicker:
     def read_async(self, attributes, frame_epoch=None):
         """Start reading the last call's payloads for `attributes` back without
         a host sync: lengths and each payload's bound-sized buffer are copied
-        into pinned memory on the current stream; `.result()` waits for that
-        copy only (the GPU keeps running whatever was queued after it).
+        into pinned memory on a side stream (after the encode; the next
+        encode waits for the copies), so the work queued after this call --
+        the next optimizer step -- runs while the payloads cross PCIe;
+        `.result()` waits for that copy only.
 
         With `frame_epoch`, `.result()` returns TENSOR_DELTA frames instead
         (ref framing.py:51-53): each payload lands in pinned memory between
@@ -352,20 +359,32 @@ class DeltaTicker:
                 dcrc = self._dcrc = torch.empty(8, dtype=torch.int32, device=m.device)
             c = self._ctx
             c.bind_stream()
-        off = 0
-        for i, (a, b) in enumerate(zip(key, bounds)):
-            out = self.outs[a]
-            if frames:
+        cur = torch.cuda.current_stream(m.device)
+        last = getattr(self, "_read_last", None)
+        if last is not None:  # the previous copies out of dcrc / the payload buffers are done
+            cur.wait_event(last)
+        if frames:
+            for i, (a, b) in enumerate(zip(key, bounds)):
+                out = self.outs[a]
                 c.check(c.lib.ss_crc32(c.handle, out.data.data_ptr(), out.length.data_ptr(), b - pad,
                                        dcrc[i:].data_ptr()))
-            # payload bytes between the frame's header and CRC slots
-            host[off + (FRAME_HEAD if frames else 0):off + b - (FRAME_TAIL if frames else 0)].copy_(
-                out.data[:b - pad], non_blocking=True)
-            lens[i:i + 1].copy_(out.length, non_blocking=True)
-            off += b
-        if frames:
-            crcs[:len(key)].copy_(dcrc[:len(key)], non_blocking=True)
-        ev.record(torch.cuda.current_stream(m.device))
+        cs = getattr(self, "_copy_stream", None)
+        if cs is None:
+            cs = self._copy_stream = torch.cuda.Stream(m.device)
+        cs.wait_stream(cur)
+        off = 0
+        with torch.cuda.stream(cs):
+            for i, (a, b) in enumerate(zip(key, bounds)):
+                out = self.outs[a]
+                # payload bytes between the frame's header and CRC slots
+                host[off + (FRAME_HEAD if frames else 0):off + b - (FRAME_TAIL if frames else 0)].copy_(
+                    out.data[:b - pad], non_blocking=True)
+                lens[i:i + 1].copy_(out.length, non_blocking=True)
+                off += b
+            if frames:
+                crcs[:len(key)].copy_(dcrc[:len(key)], non_blocking=True)
+        ev.record(cs)
+        self._read_done = self._read_last = ev
         return _PendingPayloads(host, lens, ev, bounds, crcs if frames else None, frame_epoch)
 
     def _dims(self, attr):

@@ -18,7 +18,7 @@ bg = np.array([0.05, 0.05, 0.08])
 gts = [render_device(td, p, intr, light, background=bg) for p in poses]
 dv = [ReferenceView(p, intr, g, light, bg) for p, g in zip(poses, gts)]
 hv = [ReferenceView(p, intr, g.cpu().pin_memory(), light, bg) for p, g in zip(poses, gts)]
-state = OptimizerState(dm, scene_extent=10.0, device=torch.device("cuda", 0))
+state = OptimizerState(dm, scene_extent=10.0)
 ws = StepWorkspace(dm)
 
 
