@@ -20,6 +20,14 @@ struct AdamConst {
     int B;
 };
 
+// k % B == 0 for the SH bases counts B in {1, 4, 9, 16} without a 64-bit
+// division (a masked test, or k / 9 as a 64-bit multiply-high)
+__device__ __forceinline__ bool sh_is_dc(int64_t k, int B) {
+    const uint64_t u = (uint64_t)k;
+    if (B == 9) return u - 9 * (__umul64hi(u, 0xE38E38E38E38E38Full) >> 3) == 0;
+    return (u & (uint64_t)(B - 1)) == 0;  // B = 1, 4, 16
+}
+
 // parameter pointer and learning rate of flat element e (ss_grad_layout with
 // `a` = ld rows per group); with PADDED, NULL for an element of a padding
 // row (>= c.a) -- the sharded step's last shards
@@ -39,7 +47,7 @@ __device__ __forceinline__ PT* adam_param(int64_t e, int64_t a, int B, PT* means
         lr = c.lr[3], k = e - 10 * a, w = 1, p = logits, grp = 3;
     } else {
         k = e - 11 * a, w = 3 * B, p = sh, grp = 4;
-        lr = (k % B) == 0 ? c.lr[4] : c.lr[5];
+        lr = sh_is_dc(k, B) ? c.lr[4] : c.lr[5];
     }
     off = k;
     if (PADDED && k >= c.a * w) return nullptr;
