@@ -738,11 +738,11 @@ def encoder_bench(c, _lib, args, torch, reps=20):
     # L2 so the re-arm's dirty lines are written back outside the timed
     # region (in the server loop the optimizer step sits between two ticks)
     # and every tick starts with the inputs in DRAM
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dm.device)
+    flush, clean = l2_flush_buffers(dm.device, torch)
     for e0, e1 in ev:
         bm.copy_(ref_m)
         bl.copy_(ref_l)
-        flush.add_(1.0)
+        l2_flush(flush, clean)
         e0.record()
         tick(per_frame)
         e1.record()
@@ -760,7 +760,7 @@ def encoder_bench(c, _lib, args, torch, reps=20):
     out = {"value": a / (ms * 1e-3), "unit": "Gaussians/s", "rows": a, "sh_degree": 1, "ms_per_tick": ms,
            "kernel_ms_per_tick": dev_ms, "payload_bytes_per_tick": payload,
            "set": "means+log_scales (dense residual, baseline advanced) + opacity + DC, raw, one batched call",
-           "l2": "flushed between ticks (256 MB read-modify-write after the baseline re-arm)",
+           "l2": "flushed between ticks (after the baseline re-arm: 256 MB written, then 256 MB read; bench.l2_flush)",
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "traffic": committed_traffic("delta_encode"), "traffic_unit": "bytes/tick (ncu, profiles/)",
                         "algorithmic_bytes_per_tick": bytes_per_row * a, "bytes_per_row": bytes_per_row,
@@ -768,6 +768,21 @@ def encoder_bench(c, _lib, args, torch, reps=20):
     out["client_apply"] = ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch)
     del dm
     return out
+
+
+def l2_flush_buffers(device, torch):
+    return (torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device),
+            torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device))
+
+
+def l2_flush(flush, clean):
+    """L2 flush before a timed encoder call: write 256 MB (every line of the
+    126 MB L2 replaced, earlier dirty data written back), then read another
+    256 MB, so the timed call starts with its inputs in DRAM and no dirty
+    lines of the flush itself left to write back inside its region (ncu's
+    own cache control flushes and invalidates the same way)."""
+    flush.add_(1.0)
+    clean.sum()
 
 
 def snapshot_bench(dm, torch, reps=10):
@@ -781,10 +796,10 @@ def snapshot_bench(dm, torch, reps=10):
     bl = torch.empty_like(dm.log_scales)
     for _ in range(2):
         encode_snapshot_device(dm, 0, out, bm, bl)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dm.device)
+    flush, clean = l2_flush_buffers(dm.device, torch)
     ts = []
     for _ in range(reps):
-        flush.add_(1.0)
+        l2_flush(flush, clean)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         encode_snapshot_device(dm, 0, out, bm, bl)
@@ -801,7 +816,7 @@ def snapshot_bench(dm, torch, reps=10):
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                          "algorithmic_bytes": alg},
             "note": "device time per encode (profile 0, raw) incl. the decoded means/log-scales for the baseline "
-                    "reset; L2 flushed before each"}
+                    "reset; L2 flushed before each (256 MB written, then 256 MB read; bench.l2_flush)"}
 
 
 def ingest_bench(dm, tick, per_frame, ref_m, ref_l, bm, bl, torch, reps=10):

@@ -142,6 +142,9 @@ inline int grid_for(ss_ctx* ctx, int64_t n, int block = 256) {
 // ---------------------------------------------------------------- snapshot
 struct SnapState {
     uint32_t lo_ord[3], hi_ord[3];
+    uint32_t long_ids;  // any object-id varint longer than one byte (then the offsets need a scan)
+    uint32_t done;      // body blocks finished (the last one writes the header in the one-byte case)
+    uint32_t ticket;    // k_snap_ids tiles, in start order
 };
 
 __global__ void k_vis_header(int64_t n, uint8_t* __restrict__ out, uint64_t* __restrict__ out_len) {
@@ -150,8 +153,12 @@ __global__ void k_vis_header(int64_t n, uint8_t* __restrict__ out, uint64_t* __r
     *out_len = 4 + (uint64_t)(n + 7) / 8;
 }
 
-__global__ void k_aabb(const float* __restrict__ means, int64_t n, SnapState* st) {
+__global__ void k_aabb(const float* __restrict__ means, int64_t n, SnapState* st, uint64_t* __restrict__ clear,
+                       int64_t n_clear) {
     SS_PDL_WAIT();
+    // (also clears k_snap_ids' tile states, which the scratch arena leaves stale)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_clear; i += (int64_t)gridDim.x * blockDim.x)
+        clear[i] = 0;
     uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0, 0, 0};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -186,6 +193,9 @@ __global__ void k_snap_init(SnapState* st) {
         st->lo_ord[a] = 0xffffffffu;
         st->hi_ord[a] = 0u;
     }
+    st->long_ids = 0;
+    st->done = 0;
+    st->ticket = 0;
 }
 
 struct SnapLayout {
@@ -201,9 +211,36 @@ __device__ __forceinline__ void aabb_of(const SnapState* st, int64_t n, double l
     }
 }
 
+struct SnapHeader {
+    int64_t n;
+    int active, degree, profile;
+    uint64_t fixed_len;
+    uint8_t* out;
+    uint64_t* out_len;
+};
+
+__device__ void snap_header(const SnapState* st, const SnapHeader& h, uint64_t var_len) {
+    double lo[3], hi[3];
+    aabb_of(st, h.n, lo, hi);
+    uint8_t* out = h.out;
+    put_u32(out, (uint32_t)h.n);
+    put_u32(out + 4, (uint32_t)h.active);
+    out[8] = (uint8_t)h.degree;
+    out[9] = (uint8_t)h.profile;
+    out[10] = 0;  // compression id: raw
+    out[11] = 0;
+    for (int a = 0; a < 3; ++a) {
+        put_f32(out + 12 + 4 * a, (float)lo[a]);
+        put_f32(out + 24 + 4 * a, (float)hi[a]);
+    }
+    const uint64_t blen = h.fixed_len + var_len;
+    put_u32(out + 36, (uint32_t)blen);
+    *h.out_len = 40 + blen;
+}
+
 __device__ __forceinline__ void snap_rows(const ss_model& m, const SnapLayout& L, const SnapState* st,
                                           uint8_t* __restrict__ blk, float* __restrict__ base_means,
-                                          float* __restrict__ base_ls, uint32_t* __restrict__ id_lens, int bid, int nblk) {
+                                          float* __restrict__ base_ls, int bid, int nblk) {
     double lo[3], hi[3];
     aabb_of(st, L.n, lo, hi);
     const QSpec qls = qspec(A_LS);  // the power-of-two spans go through quantize_p2
@@ -213,8 +250,14 @@ __device__ __forceinline__ void snap_rows(const ss_model& m, const SnapLayout& L
     const int64_t nw = (L.n + 31) & ~int64_t(31);
     for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < nw; i += stride) {
         const bool ok = i < L.n;
+        uint32_t idl = 1;
         if (ok) {
-            id_lens[i] = varint_len((uint64_t)(int64_t)m.object_ids[i]);
+            // object ids: one-byte varints (ids 0..127, the common case) go
+            // straight to their slot i; any longer one flags the batch and
+            // k_snap_ids rewrites the whole section at scanned offsets
+            const uint64_t id = (uint64_t)(int64_t)m.object_ids[i];
+            idl = varint_len(id);
+            blk[L.off_ids + i] = (uint8_t)id;
             for (int a = 0; a < 3; ++a) {
                 uint32_t c = quantize((double)m.means[i * 3 + a], lo[a], hi[a], 16);
                 put_code(blk + L.off_means + (i * 3 + a) * 2, c, 16);
@@ -230,6 +273,8 @@ __device__ __forceinline__ void snap_rows(const ss_model& m, const SnapLayout& L
             blk[L.off_opac + i] = (uint8_t)quantize_p2(m.logit_opacities[i], -8.f, 8.f, 255.0 / 16.0);
             // SH DC and rest: k_snap_sh, element-parallel over the coefficient rows
         }
+        if (__ballot_sync(0xffffffffu, idl != 1) && (threadIdx.x & 31) == 0)
+            atomicOr(const_cast<uint32_t*>(&st->long_ids), 1u);  // the only field of st written here
         unsigned bal = __ballot_sync(0xffffffffu, ok && m.light_visibility[ok ? i : 0] >= 0.5f);
         if ((threadIdx.x & 31) == 0) {
             const int64_t i0 = i;  // warp base (i is lane 0's row)
@@ -282,24 +327,91 @@ __device__ __forceinline__ void snap_sh(const float* __restrict__ sh, int64_t n,
 template <int B>
 __global__ void __launch_bounds__(256) k_snap_body(ss_model m, SnapLayout L, const SnapState* st,
                                                    uint8_t* __restrict__ blk, float* __restrict__ base_means,
-                                                   float* __restrict__ base_ls, uint32_t* __restrict__ id_lens) {
+                                                   float* __restrict__ base_ls, SnapHeader hdr) {
     SS_PDL_WAIT();
     const int b = blockIdx.x, g = gridDim.x / 5;
-    if (b % 5 < 2) snap_rows(m, L, st, blk, base_means, base_ls, id_lens, (b / 5) * 2 + b % 5, 2 * g);
+    if (b % 5 < 2) snap_rows(m, L, st, blk, base_means, base_ls, (b / 5) * 2 + b % 5, 2 * g);
     else snap_sh<B>(m.sh_coeffs, L.n, blk + L.off_dc, blk + L.off_rest, (b / 5) * 3 + b % 5 - 2, 3 * g);
+    // the last block to finish: with every object id one byte the payload is
+    // complete -- write the header (else k_snap_ids does, after the offsets)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        SnapState* sw = const_cast<SnapState*>(st);
+        __threadfence();
+        if (atomicAdd(&sw->done, 1u) == gridDim.x - 1) {
+            __threadfence();
+            if (*(volatile uint32_t*)&sw->long_ids == 0) snap_header(st, hdr, (uint64_t)L.n);
+        }
+    }
 }
 
-__global__ void k_snap_id_lens(const int32_t* __restrict__ ids, int64_t n, uint32_t* __restrict__ lens) {
-    SS_PDL_WAIT();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        lens[i] = varint_len((uint64_t)(int64_t)ids[i]);
-}
+// Object-id varints when some id is longer than one byte (SnapState::long_ids;
+// otherwise a no-op): one pass, tiles in start order (atomic ticket), each
+// tile's byte count published and its offset found by decoupled look-back
+// over the earlier tiles (ss_sort.cu's scheme); the last tile writes the header.
+constexpr int SID_THREADS = 256, SID_ITEMS = 8, SID_TILE = SID_THREADS * SID_ITEMS;
+constexpr uint64_t SID_AGG = 1ull << 62, SID_INC = 2ull << 62, SID_VAL = (1ull << 62) - 1;
 
-__global__ void k_snap_id_write(const int32_t* __restrict__ ids, int64_t n, const uint64_t* __restrict__ off,
-                                uint8_t* __restrict__ dst) {
+__global__ void __launch_bounds__(SID_THREADS) k_snap_ids(const int32_t* __restrict__ ids, int64_t n, SnapState* st,
+                                                          uint64_t* __restrict__ tile_state, uint8_t* __restrict__ dst,
+                                                          SnapHeader hdr) {
     SS_PDL_WAIT();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        varint_put(dst + off[i], (uint64_t)(int64_t)ids[i]);
+    if (*(volatile uint32_t*)&st->long_ids == 0) return;
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_base, s_tot;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&st->ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t i0 = tile * SID_TILE + (int64_t)threadIdx.x * SID_ITEMS;
+    uint32_t len[SID_ITEMS];
+    uint64_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < SID_ITEMS; ++k) {
+        len[k] = i0 + k < n ? varint_len((uint64_t)(int64_t)ids[i0 + k]) : 0;
+        mine += len[k];
+    }
+    // block exclusive scan of the per-thread byte counts
+    __shared__ uint64_t s_w[SID_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t run = 0;
+        for (int w = 0; w < SID_THREADS / 32; ++w) {
+            const uint64_t t = s_w[w];
+            s_w[w] = run;
+            run += t;
+        }
+        s_tot = run;
+        // publish the aggregate, then look back for the exclusive prefix
+        volatile uint64_t* ts = tile_state;
+        ts[tile] = (tile == 0 ? SID_INC : SID_AGG) | run;
+        uint64_t base = 0;
+        for (int64_t p = tile - 1; p >= 0;) {
+            const uint64_t v = ts[p];
+            if (v & SID_INC) { base += v & SID_VAL; break; }
+            if (v & SID_AGG) { base += v & SID_VAL; --p; }
+        }
+        if (tile > 0) {
+            __threadfence();
+            ts[tile] = SID_INC | (base + run);
+        }
+        s_base = base;
+    }
+    __syncthreads();
+    uint64_t off = s_base + s_w[warp] + incl - mine;
+#pragma unroll
+    for (int k = 0; k < SID_ITEMS; ++k) {
+        if (i0 + k < n) varint_put(dst + off, (uint64_t)(int64_t)ids[i0 + k]);
+        off += len[k];
+    }
+    if (tile == (n + SID_TILE - 1) / SID_TILE - 1 && threadIdx.x == 0) snap_header(st, hdr, s_base + s_tot);
 }
 
 __global__ void k_snap_header(const SnapState* st, int64_t n, int active, int degree, int profile,
@@ -373,9 +485,12 @@ int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t*
     cudaStream_t s = ctx->stream;
     const int B = (m->sh_degree + 1) * (m->sh_degree + 1);
     SnapState* st = SS_SCRATCH(ctx, SnapState, 1);
-    if (!st) return SS_ERR_CUDA;
+    const int64_t id_tiles = (n + SID_TILE - 1) / SID_TILE;
+    uint64_t* tile_state = SS_SCRATCH(ctx, uint64_t, id_tiles > 0 ? id_tiles : 1);
+    if (!st || !tile_state) return SS_ERR_CUDA;
     SS_CUDA(ctx, ss_launch((k_snap_init), dim3(1), dim3(1), 0, s, st));
-    if (n) SS_CUDA(ctx, ss_launch((k_aabb), dim3(grid_for(ctx, n)), dim3(256), 0, s, (const float*)m->means, n, st));
+    if (n) SS_CUDA(ctx, ss_launch((k_aabb), dim3(grid_for(ctx, n)), dim3(256), 0, s, (const float*)m->means, n, st,
+                                  tile_state, id_tiles));
     SS_CHECK_LAUNCH(ctx);
     uint8_t* blk = out + 40;
     if (profile == 1) {
@@ -404,28 +519,32 @@ int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t*
     L.off_rest = 18ull * n;
     L.off_vis = L.off_rest + 3ull * (B - 1) * n;
     L.off_ids = L.off_vis + (uint64_t)(n + 7) / 8;
-    uint32_t* lens = SS_SCRATCH(ctx, uint32_t, n);
-    uint64_t* offs = SS_SCRATCH(ctx, uint64_t, n);
-    uint64_t* vtot = SS_SCRATCH(ctx, uint64_t, 1);
-    if (!lens || !offs || !vtot) return SS_ERR_CUDA;
     if (n) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_snap_body<16>, 256, 0);
         int64_t g = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 4);
         g = (g / 5) * 5;  // whole 2 : 3 groups
         if (g < 5) g = 5;
-        if (B == 1) SS_CUDA(ctx, ss_launch((k_snap_body<1>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
-        else if (B == 4) SS_CUDA(ctx, ss_launch((k_snap_body<4>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
-        else if (B == 9) SS_CUDA(ctx, ss_launch((k_snap_body<9>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
-        else SS_CUDA(ctx, ss_launch((k_snap_body<16>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, lens));
+        SnapHeader hdr;
+        hdr.n = n;
+        hdr.active = m->active_count;
+        hdr.degree = m->sh_degree;
+        hdr.profile = 0;
+        hdr.fixed_len = L.off_ids;
+        hdr.out = out;
+        hdr.out_len = out_len;
+        if (B == 1) SS_CUDA(ctx, ss_launch((k_snap_body<1>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
+        else if (B == 4) SS_CUDA(ctx, ss_launch((k_snap_body<4>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
+        else if (B == 9) SS_CUDA(ctx, ss_launch((k_snap_body<9>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
+        else SS_CUDA(ctx, ss_launch((k_snap_body<16>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
         SS_CHECK_LAUNCH(ctx);
-    }
-    SS_TRY(ss_scan_u32_to_u64(ctx, lens, offs, n, vtot));
-    if (n) {
-        SS_CUDA(ctx, ss_launch((k_snap_id_write), dim3(grid_for(ctx, n)), dim3(256), 0, s, (const int32_t*)m->object_ids, n, (const uint64_t*)offs, blk + L.off_ids));
+        // object ids longer than one byte (device-side test; else a no-op)
+        SS_CUDA(ctx, ss_launch((k_snap_ids), dim3((unsigned)id_tiles), dim3(SID_THREADS), 0, s, (const int32_t*)m->object_ids,
+                               n, st, tile_state, blk + L.off_ids, hdr));
         SS_CHECK_LAUNCH(ctx);
+        return SS_OK;
     }
-    SS_CUDA(ctx, ss_launch((k_snap_header), dim3(1), dim3(1), 0, s, (const SnapState*)st, n, m->active_count, m->sh_degree, 0, (uint64_t)L.off_ids, (const uint64_t*)vtot, out, out_len));
+    SS_CUDA(ctx, ss_launch((k_snap_header), dim3(1), dim3(1), 0, s, (const SnapState*)st, n, m->active_count, m->sh_degree, 0, (uint64_t)L.off_ids, (const uint64_t*)nullptr, out, out_len));
     SS_CHECK_LAUNCH(ctx);
     return SS_OK;
 }

@@ -243,3 +243,30 @@ def test_gpu_ticker_read_async_matches_read():
     p2 = t.read_async(attrs)
     assert p1.result() == sync
     assert p2.result() == t.read(attrs)
+
+
+@pytest.mark.parametrize("ids", ["one_byte", "multi_byte", "negative", "one_long"])
+def test_gpu_snapshot_object_id_varints(ids):
+    """The snapshot's object-id section: one-byte varints are written in
+    place, any longer id switches the batch to the scanned offsets (a
+    device-side flag) -- every case byte-exact vs the oracle."""
+    require_gpu()
+    from oracle import codec as oc
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.protocol import QuantizationProfile, encode_snapshot
+    n = 70_001
+    m = synth.random_field(n, 2, 320, 192, seed=3)
+    rng = np.random.default_rng(4)
+    if ids == "one_byte":
+        m.object_ids = rng.integers(0, 128, n).astype(np.int32)
+    elif ids == "multi_byte":
+        m.object_ids = rng.integers(0, 1 << 20, n).astype(np.int32)
+    elif ids == "negative":
+        m.object_ids = rng.integers(-3, 3, n).astype(np.int32)
+    else:
+        m.object_ids = np.zeros(n, np.int32)
+        m.object_ids[n - 5] = 300  # one two-byte id at the very end
+    got = encode_snapshot(m, QuantizationProfile(0, 0))
+    ref = oc.snapshot_payload(m.means, m.log_scales, m.quaternions, m.logit_opacities, m.sh_coeffs,
+                              m.light_visibility, m.object_ids, m.active_count, m.sh_degree, 0, 0)
+    assert got == ref
