@@ -249,3 +249,40 @@ def test_gpu_step_issues_no_host_sync():
     assert _lib.host_syncs(0) == before
     ws.flush()
     assert state.step_count == 7
+
+
+@pytest.mark.parametrize("lanes", [1, 3])
+def test_gpu_view_lanes_bit_identical(lanes, monkeypatch):
+    """optim.step deals the views over VIEW_LANES streams (each with its own
+    library context); every view's kernels are the same whichever lane runs
+    them, so the trajectory is bit-identical to the default (2 lanes)."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200 import optim, synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
+    from paper_2604_02851_b200.render import render_device
+    W, H = 256, 160
+    host = synth.random_field(20_000, 3, W, H, seed=41)
+    tgt = DeviceModel.from_host(synth.target_model(host, seed=42), 0)
+    intr = synth.intrinsics(W, H)
+    light = synth.light()
+    views = [ReferenceView(p, intr, render_device(tgt, p, intr, light), light, np.zeros(3))
+             for p in synth.ring_poses(5, radius=0.5)]
+
+    def run():
+        dm = DeviceModel.from_host(host, 0)
+        state = OptimizerState(dm, scene_extent=2.0)
+        ws = StepWorkspace(dm)
+        losses = [step(dm, state, views, workspace=ws) for _ in range(3)]
+        torch.cuda.synchronize()
+        return dm, state, losses
+
+    ref_dm, ref_state, ref_l = run()
+    monkeypatch.setattr(optim, "VIEW_LANES", lanes)
+    dm, state, losses = run()
+    assert losses == ref_l
+    for k in GROUPS:
+        assert torch.equal(getattr(dm, k), getattr(ref_dm, k)), k
+    for k in GROUPS:
+        np.testing.assert_array_equal(state.m[k], ref_state.m[k])
