@@ -828,6 +828,7 @@ __device__ __forceinline__ float& comp(float2& v, int h) { return h ? v.y : v.x;
 #ifndef SS_FWD2_MINB
 #define SS_FWD2_MINB 8
 #endif
+template <bool COUNT>  // COUNT: accumulate the evaluated (pixel, splat) pairs (timing runs only)
 __global__ void __launch_bounds__(32 * WPB, SS_FWD2_MINB) k_blend_fwd2(const uint2* __restrict__ ranges,
                                                          const uint32_t* __restrict__ pvals,
                                                          const double2* __restrict__ mu,
@@ -872,7 +873,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_FWD2_MINB) k_blend_fwd2(const uin
             const unsigned act = lane_mask(s, lx, ly0) & alive;
             if (!act) continue;
             last = (int)(b0 - rg.x) + k;
-            evals += __popc(act);
+            if (COUNT) evals += __popc(act);
             PixelGeom<float, true> pg(s, pxc, pyc);
             const unsigned wact = __reduce_or_sync(__activemask(), act);
             const float2 cK = f2(pg.cK), Bx = f2(pg.Bx2), Ax = f2(pg.Ax2), o = f2(s.o);
@@ -900,7 +901,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_FWD2_MINB) k_blend_fwd2(const uin
     }
     last = __reduce_max_sync(0xffffffffu, last + 1);
     if (lane == 0 && tile_stop) tile_stop[tile] = (uint32_t)last;
-    if (eval_count) {
+    if (COUNT) {
         evals = __reduce_add_sync(0xffffffffu, evals);
         if (lane == 0 && evals) atomicAdd(eval_count, (unsigned long long)evals);
     }
@@ -1876,11 +1877,13 @@ int forward(ss_ctx* ctx, const ss_camera* cam, const ss_render_opts* o, const Bi
                                order));
         SS_CHECK_LAUNCH(ctx);
     }
-    if constexpr (sizeof(R) == 4)
-        SS_CUDA(ctx, ss_launch((k_blend_fwd2), dim3((b.n_tiles + WPB - 1) / WPB), dim3(32 * WPB), 0, ctx->stream, 
+    if constexpr (sizeof(R) == 4) {
+        const bool count = ss_timing_on(ctx);
+        SS_CUDA(ctx, ss_launch(count ? k_blend_fwd2<true> : k_blend_fwd2<false>, dim3((b.n_tiles + WPB - 1) / WPB), dim3(32 * WPB), 0, ctx->stream,
             b.ranges, b.pvals, b.mu, (const SplatRec<float>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
             o->background[0], o->background[1], o->background[2], img, T, tile_stop,
-            ss_timing_on(ctx) ? ctx->dev_counters : nullptr, order));
+            count ? ctx->dev_counters : nullptr, order));
+    }
     else
         SS_CUDA(ctx, ss_launch((k_blend_fwd<R>), dim3((b.n_tiles + WPB - 1) / WPB), dim3(32 * WPB), 0, ctx->stream, 
             b.ranges, b.pvals, b.mu, (const SplatRec<R>*)b.rec, cam->width, cam->height, b.tiles_x, b.n_tiles,
