@@ -543,7 +543,7 @@ class StepWorkspace:
 
 CHAIN_MAX_VIEWS = 16  # ss_chain_views
 # concurrent view lanes of a step (streams; see _DeviceKernels._lane)
-VIEW_LANES = max(1, int(os.environ.get("SS_VIEW_LANES", "2")))
+VIEW_LANES = max(1, int(os.environ.get("SS_VIEW_LANES", "4")))
 _LANE_STREAMS = {}
 
 
