@@ -925,23 +925,22 @@ def client_render_bench(args, rank, world, pg, dev, torch, n=2_000_000, views=64
     import torch.distributed as dist
     from paper_2604_02851_b200 import synth
     from paper_2604_02851_b200.model import DeviceModel
-    from paper_2604_02851_b200.render import render_device
+    from paper_2604_02851_b200.render import render_device_many
     m = DeviceModel.from_host(synth.random_field(n, 3, args.width, args.height, seed=7), dev.index)
     intr = synth.intrinsics(args.width, args.height)
     light = synth.light()
     allp = synth.ring_poses(views, radius=0.6)
     mine = allp[rank::world]
-    out = torch.empty((args.height, args.width, 3), dtype=torch.float32, device=dev)
-    for p in mine[:2]:
-        render_device(m, p, intr, light, out=out)
+    lanes = 4
+    outs = [torch.empty((args.height, args.width, 3), dtype=torch.float32, device=dev) for _ in range(lanes)]
+    render_device_many(m, mine[:lanes], intr, light, outs=outs, lanes=lanes)
     torch.cuda.synchronize()
     if pg is not None:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        for p in mine:
-            render_device(m, p, intr, light, out=out)
+        render_device_many(m, mine, intr, light, outs=outs, lanes=lanes)
     e1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -951,8 +950,9 @@ def client_render_bench(args, rank, world, pg, dev, torch, n=2_000_000, views=64
     del m
     return {"value": views * reps / (ms / 1e3), "unit": "frames/s", "viewpoints": views, "gaussians": n,
             "sh_degree": 3, "resolution": [args.width, args.height], "ms_per_frame_per_gpu": ms / (reps * len(mine)),
-            "note": "render_device (preprocess, depth sort, binning, tile sort, forward) per viewpoint; sharded "
-                    "round-robin over the ranks, no collective; device time, max over ranks"}
+            "note": "render_device_many (per viewpoint: preprocess, depth sort, binning, tile sort, forward; 4 "
+                    "lanes of streams); viewpoints sharded round-robin over the ranks, no collective; device time, "
+                    "max over ranks"}
 
 
 def engine_bench(poses, intr, torch, reps=5):

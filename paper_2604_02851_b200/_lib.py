@@ -311,6 +311,20 @@ def lane_ctx(device: int, lane: int) -> Context:
     return c
 
 
+_LANE_STREAMS = {}
+
+
+def lane_stream(device: int, lane: int):
+    """The torch stream of view lane `lane` >= 1 on `device` (created once;
+    lane 0 is the caller's current stream)."""
+    import torch
+    key = (int(device), int(lane))
+    s = _LANE_STREAMS.get(key)
+    if s is None:
+        s = _LANE_STREAMS[key] = torch.cuda.Stream(torch.device("cuda", int(device)))
+    return s
+
+
 def device_contexts(device: int):
     """Every context of `device` in this thread (the main one first)."""
     out = [ctx(device)]

@@ -544,7 +544,6 @@ class StepWorkspace:
 CHAIN_MAX_VIEWS = 16  # ss_chain_views
 # concurrent view lanes of a step (streams; see _DeviceKernels._lane)
 VIEW_LANES = max(1, int(os.environ.get("SS_VIEW_LANES", "4")))
-_LANE_STREAMS = {}
 
 
 def chain_views(model: DeviceModel, views, g9, rinv, grad, subset_tensor=None, j0=0, j1=None, row0=0, rows=None,
@@ -624,12 +623,10 @@ class _DeviceKernels:
         if self.lanes is None:
             cur = torch.cuda.current_stream(dev)
             self.lanes = [(cur, None)]
-            pool = _LANE_STREAMS.setdefault(dev.index, [])
-            while len(pool) < L - 1:
-                pool.append(torch.cuda.Stream(dev))
             for k in range(1, L):
-                pool[k - 1].wait_stream(cur)
-                self.lanes.append((pool[k - 1], None))
+                ls = _lib.lane_stream(dev.index, k)
+                ls.wait_stream(cur)
+                self.lanes.append((ls, None))
         return t % L, self.lanes[t % L][0]
 
     def join(self):

@@ -127,6 +127,40 @@ def render_device(model: DeviceModel, pose, intr, light_state, index_subset=None
     return (img, T) if return_transmittance else img
 
 
+def render_device_many(model: DeviceModel, poses, intr, light_state, outs=None, lanes: int = 4,
+                       background=(0.0, 0.0, 0.0), extent_cutoff=True):
+    """render_device() of several viewpoints (the client-viewpoint serving
+    path), dealt over `lanes` streams with one library
+    context each so one viewpoint's latency-bound binning overlaps another's
+    blend; the caller's stream waits for all of them.  `outs`: optional
+    (H, W, 3) float32 output buffers, used round-robin (a buffer is reused
+    only after the lane that last wrote it, i.e. len(outs) >= lanes keeps
+    the lanes independent).  Returns the images in pose order."""
+    import torch
+    dev = model.device
+    cur = torch.cuda.current_stream(dev)
+    L = max(1, int(lanes))
+    streams = [cur] + [_lib.lane_stream(dev.index, k) for k in range(1, L)]
+    for s in streams[1:]:
+        s.wait_stream(cur)
+    H, W = intr.height, intr.width
+    m = model.struct()
+    L_ = light_struct(light_state)
+    o = render_opts(background, None, extent_cutoff, 0)
+    imgs = []
+    for i, pose in enumerate(poses):
+        k = i % L
+        with torch.cuda.stream(streams[k]):
+            c = _lib.lane_ctx(dev.index, k)
+            img = outs[i % len(outs)] if outs else torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+            st = _lib.SSRenderStats()
+            c.check(c.lib.ss_render(c.handle, m, camera_struct(pose, intr), L_, o, _lib.ptr(img), None, st))
+            imgs.append(img)
+    for s in streams[1:]:
+        cur.wait_stream(s)
+    return imgs
+
+
 def render(model, pose, intr, light_state, index_subset=None, background=(0.0, 0.0, 0.0),
            return_transmittance: bool = False, extent_cutoff: bool = True, precision: int = 0):
     """ref render.py:339 -- returns a float64 numpy image [, T]."""

@@ -202,3 +202,26 @@ def test_gpu_composite_of_reference_prepared_splats(c):
     img, T = composite(prep, intr, np.array([0.1, 0.2, 0.3]))
     np.testing.assert_allclose(img, c.a("img"), rtol=0, atol=1e-9)
     np.testing.assert_allclose(T, c.a("T"), rtol=0, atol=1e-9)
+
+
+def test_gpu_render_device_many_matches_single():
+    """render_device_many (viewpoints over 3 lanes of streams, one library
+    context each, 2 output buffers) == render_device per viewpoint, bit for bit."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.render import render_device, render_device_many
+    W, H = 320, 192
+    m = DeviceModel.from_host(synth.random_field(40_000, 3, W, H, seed=8), 0)
+    intr, light = synth.intrinsics(W, H), synth.light()
+    poses = synth.ring_poses(7, radius=0.6)
+    ref = [render_device(m, p, intr, light).clone() for p in poses]
+    got = [g.clone() for g in render_device_many(m, poses, intr, light, lanes=3)]
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
+    outs = [torch.empty((H, W, 3), dtype=torch.float32, device=m.device) for _ in range(3)]
+    last = render_device_many(m, poses[:3], intr, light, outs=outs, lanes=3)
+    torch.cuda.synchronize()
+    for a, b in zip(ref[:3], last):
+        assert torch.equal(a, b)
