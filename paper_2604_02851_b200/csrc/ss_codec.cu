@@ -143,7 +143,6 @@ inline int grid_for(ss_ctx* ctx, int64_t n, int block = 256) {
 struct SnapState {
     uint32_t lo_ord[3], hi_ord[3];
     uint32_t long_ids;  // any object-id varint longer than one byte (then the offsets need a scan)
-    uint32_t done;      // body blocks finished (the last one writes the header in the one-byte case)
     uint32_t ticket;    // k_snap_ids tiles, in start order
 };
 
@@ -194,7 +193,6 @@ __global__ void k_snap_init(SnapState* st) {
         st->hi_ord[a] = 0u;
     }
     st->long_ids = 0;
-    st->done = 0;
     st->ticket = 0;
 }
 
@@ -324,31 +322,24 @@ __device__ __forceinline__ void snap_sh(const float* __restrict__ sh, int64_t n,
 // The row sections (+ object-id varint lengths) and the SH sections in ONE
 // launch: blocks alternate 2 : 3 between the fp64-heavy row work and the
 // streaming SH work, so both run side by side on every SM.
+#ifndef SNAP_MINB
+#define SNAP_MINB 6  // measured (1M rows SH3, clean L2): 4 / 5 / 6 / 7 / 8 -> 107.5 / 99.3 / 96.8 / 97.3 / 97.3 us
+#endif
 template <int B>
-__global__ void __launch_bounds__(256) k_snap_body(ss_model m, SnapLayout L, const SnapState* st,
+__global__ void __launch_bounds__(256, SNAP_MINB) k_snap_body(ss_model m, SnapLayout L, const SnapState* st,
                                                    uint8_t* __restrict__ blk, float* __restrict__ base_means,
-                                                   float* __restrict__ base_ls, SnapHeader hdr) {
+                                                   float* __restrict__ base_ls) {
     SS_PDL_WAIT();
     const int b = blockIdx.x, g = gridDim.x / 5;
     if (b % 5 < 2) snap_rows(m, L, st, blk, base_means, base_ls, (b / 5) * 2 + b % 5, 2 * g);
     else snap_sh<B>(m.sh_coeffs, L.n, blk + L.off_dc, blk + L.off_rest, (b / 5) * 3 + b % 5 - 2, 3 * g);
-    // the last block to finish: with every object id one byte the payload is
-    // complete -- write the header (else k_snap_ids does, after the offsets)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        SnapState* sw = const_cast<SnapState*>(st);
-        __threadfence();
-        if (atomicAdd(&sw->done, 1u) == gridDim.x - 1) {
-            __threadfence();
-            if (*(volatile uint32_t*)&sw->long_ids == 0) snap_header(st, hdr, (uint64_t)L.n);
-        }
-    }
 }
 
 // Object-id varints when some id is longer than one byte (SnapState::long_ids;
-// otherwise a no-op): one pass, tiles in start order (atomic ticket), each
-// tile's byte count published and its offset found by decoupled look-back
-// over the earlier tiles (ss_sort.cu's scheme); the last tile writes the header.
+// otherwise block 0 only writes the header): one pass, tiles in start order
+// (atomic ticket), each tile's byte count published and its offset found by
+// decoupled look-back over the earlier tiles (ss_sort.cu's scheme); the last
+// tile writes the header.
 constexpr int SID_THREADS = 256, SID_ITEMS = 8, SID_TILE = SID_THREADS * SID_ITEMS;
 constexpr uint64_t SID_AGG = 1ull << 62, SID_INC = 2ull << 62, SID_VAL = (1ull << 62) - 1;
 
@@ -356,7 +347,10 @@ __global__ void __launch_bounds__(SID_THREADS) k_snap_ids(const int32_t* __restr
                                                           uint64_t* __restrict__ tile_state, uint8_t* __restrict__ dst,
                                                           SnapHeader hdr) {
     SS_PDL_WAIT();
-    if (*(volatile uint32_t*)&st->long_ids == 0) return;
+    if (*(volatile uint32_t*)&st->long_ids == 0) {  // every id one byte: written in place by the body
+        if (blockIdx.x == 0 && threadIdx.x == 0) snap_header(st, hdr, (uint64_t)n);
+        return;
+    }
     __shared__ uint32_t s_tile;
     __shared__ uint64_t s_base, s_tot;
     if (threadIdx.x == 0) s_tile = atomicAdd(&st->ticket, 1u);
@@ -533,10 +527,10 @@ int ss_encode_snapshot(ss_ctx* ctx, const ss_model* m, int32_t profile, uint8_t*
         hdr.fixed_len = L.off_ids;
         hdr.out = out;
         hdr.out_len = out_len;
-        if (B == 1) SS_CUDA(ctx, ss_launch((k_snap_body<1>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
-        else if (B == 4) SS_CUDA(ctx, ss_launch((k_snap_body<4>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
-        else if (B == 9) SS_CUDA(ctx, ss_launch((k_snap_body<9>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
-        else SS_CUDA(ctx, ss_launch((k_snap_body<16>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls, hdr));
+        if (B == 1) SS_CUDA(ctx, ss_launch((k_snap_body<1>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls));
+        else if (B == 4) SS_CUDA(ctx, ss_launch((k_snap_body<4>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls));
+        else if (B == 9) SS_CUDA(ctx, ss_launch((k_snap_body<9>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls));
+        else SS_CUDA(ctx, ss_launch((k_snap_body<16>), dim3((unsigned)g), dim3(256), 0, s, *m, L, (const SnapState*)st, blk, base_means, base_ls));
         SS_CHECK_LAUNCH(ctx);
         // object ids longer than one byte (device-side test; else a no-op)
         SS_CUDA(ctx, ss_launch((k_snap_ids), dim3((unsigned)id_tiles), dim3(SID_THREADS), 0, s, (const int32_t*)m->object_ids,

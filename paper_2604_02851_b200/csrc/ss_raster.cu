@@ -1537,8 +1537,11 @@ __global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const 
 // (sh_grad_row), one thread per row; a block's SH rows are contiguous, so
 // they are staged through shared memory (coalesced reads and writes, the
 // row's 3B entries in registers across the views).
+#ifndef SHR_MINB
+#define SHR_MINB 1
+#endif
 template <int DEG>
-__global__ void __launch_bounds__(CVB) k_sh_grad_rows(const __grid_constant__ ChainViews Vp, int nv,
+__global__ void __launch_bounds__(CVB, SHR_MINB) k_sh_grad_rows(const __grid_constant__ ChainViews Vp, int nv,
                                                       const float4* __restrict__ shrec, int64_t rows, int64_t ld,
                                                       float* __restrict__ grad_sh) {
     SS_PDL_WAIT();
