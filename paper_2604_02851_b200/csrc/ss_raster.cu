@@ -1538,7 +1538,7 @@ __global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const 
 // they are staged through shared memory (coalesced reads and writes, the
 // row's 3B entries in registers across the views).
 #ifndef SHR_MINB
-#define SHR_MINB 1
+#define SHR_MINB 6  // measured (chain class per step): 1 / 4 / 5 / 6 / 8 -> 1.972 / 1.972 / 1.973 / 1.934 / 2.193 ms
 #endif
 template <int DEG>
 __global__ void __launch_bounds__(CVB, SHR_MINB) k_sh_grad_rows(const __grid_constant__ ChainViews Vp, int nv,
