@@ -1091,8 +1091,11 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n, doubl
 #ifndef SP_PREFETCH
 #define SP_PREFETCH 1
 #endif
+#ifndef SP_MINB
+#define SP_MINB 4  // measured: 3 / 4 / 5 / 6 -> chain class 2.05 / 1.93 / 1.96 / 2.41 ms per step
+#endif
 template <typename R>
-__global__ void __launch_bounds__(256) k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
+__global__ void __launch_bounds__(256, SP_MINB) k_sum_partials(const uint64_t* __restrict__ roff, const uint32_t* __restrict__ rcnt,
                                                       const uint32_t* __restrict__ dvals, const R* __restrict__ partials,
                                                       const SplatRec<R>* __restrict__ rec,
                                                       int64_t n_in, R* __restrict__ g9, uint64_t cap) {

@@ -24,6 +24,12 @@ constexpr int RS_MAX_PASSES = 8;
 #define RS_LB 8
 #endif
 constexpr int LB = RS_LB;  // look-back window (tiles per step)
+#ifndef RS_MINB12
+#define RS_MINB12 3  // blocks per SM asked of the 12-item (tile sort) and 16-item (depth sort) passes (measured)
+#endif
+#ifndef RS_MINB16
+#define RS_MINB16 2
+#endif
 constexpr uint32_t FLAG_AGG = 1u << 30, FLAG_INC = 2u << 30, CNT_MASK = (1u << 30) - 1;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -73,7 +79,7 @@ __global__ void k_base_scan(const uint32_t* __restrict__ hist, int passes, uint6
 }
 
 template <typename K, int RS_ITEMS>
-__global__ void __launch_bounds__(RS_THREADS) k_onesweep(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
+__global__ void __launch_bounds__(RS_THREADS, RS_ITEMS <= 12 ? RS_MINB12 : RS_MINB16) k_onesweep(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
                                                          int64_t n, int shift, unsigned mask,
                                                          const uint64_t* __restrict__ digit_base,
                                                          uint32_t* __restrict__ part, unsigned* __restrict__ tile_ctr,
