@@ -349,7 +349,7 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, const uint64_t* __re
 #endif
 constexpr int WPB = SS_WPB;   // tiles (warps) per block of the forward kernels
 #ifndef SS_WPB_BWD
-#define SS_WPB_BWD 2
+#define SS_WPB_BWD 1  // measured (bench backward class per step): 1 / 2 / 4 -> 9.36 / 9.40 / 9.68 ms
 #endif
 constexpr int WPB_BWD = SS_WPB_BWD;  // ... of the backward (fewer tiles per block: less waiting on a block's slowest tile)
 constexpr int PPT = 8;   // pixels per lane
