@@ -811,7 +811,8 @@ def step(model, state: OptimizerState, views, index_subset=None, extent_cutoff: 
     else:
         _settle(ws, keep=1)  # the step before last: checked (and re-run after an overflow)
         if exchange is None:
-            exchange = "p2p" if (pg is not None and _backend(pg) == "nccl") else "collectives"
+            exchange = ("p2p" if (pg is not None and _backend(pg) == "nccl" and parallel.peer_access_ok(pg))
+                        else "collectives")
         if exchange not in ("p2p", "collectives"):
             raise ValueError(f"unknown exchange {exchange!r}")
         args = (dm, state, ready, sub, extent_cutoff, pg, deterministic, exchange == "p2p")

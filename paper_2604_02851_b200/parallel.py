@@ -142,6 +142,27 @@ class Collectives:
             self.dist.all_gather_into_tensor(out, out[self.rank * R:(self.rank + 1) * R], group=self.group)
 
 
+_PEER_OK = {}
+
+
+def peer_access_ok(group) -> bool:
+    """Whether every rank's GPU can map every other rank's memory (CUDA
+    peer access; the same device counts): the default exchange is "p2p"
+    only then.  Decided once per group, identically on every rank."""
+    import torch
+    import torch.distributed as dist
+    key = id(group)
+    if key not in _PEER_OK:
+        me = torch.cuda.current_device()
+        devs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(devs, me, group=group)
+        ok = all(d == me or torch.cuda.can_device_access_peer(me, d) for d in devs)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", me))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        _PEER_OK[key] = bool(int(flag.item()))
+    return _PEER_OK[key]
+
+
 class PeerWindow:
     """Other ranks' device tensors mapped into this process (CUDA IPC; on an
     NVSwitch box the mapped addresses are the peers' HBM over NVLink): each
