@@ -130,6 +130,16 @@ int ss_chain_views_range(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, 
                          int32_t n_views, const float* const* g9, const uint32_t* const* rinv, const int64_t* subset,
                          int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld);
 
+/* ss_chain_views_range with init = 1: the gradient layout's rows
+ * [0, rows) need not be cleared beforehand -- every entry is written (zero
+ * where no view contributes), saving the clear and the first read.  Needs
+ * the whole row range and no subset (j0 = row0, j1 >= row0 + rows); init = 0
+ * is ss_chain_views_range. */
+int ss_chain_views_range_init(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights,
+                              int32_t n_views, const float* const* g9, const uint32_t* const* rinv,
+                              const int64_t* subset, int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad,
+                              int64_t ld, int32_t init);
+
 /* *out = ((x[0] + x[1]) + x[2]) + ... (device doubles): the per-view loss sum
  * in the reference's order (optim.py:366-367). */
 int ss_sum_f64(ss_ctx* ctx, const double* x, int64_t n, double* out);

@@ -198,6 +198,8 @@ _SIGS = {
     "ss_chain_views": (i32, [vp, C.POINTER(SSModel), vp, vp, i32, C.POINTER(vp), C.POINTER(vp), vp, i64, vp]),
     "ss_chain_views_range": (i32, [vp, C.POINTER(SSModel), vp, vp, i32, C.POINTER(vp), C.POINTER(vp), vp, i64, i64,
                                    i64, i64, vp, i64]),
+    "ss_chain_views_range_init": (i32, [vp, C.POINTER(SSModel), vp, vp, i32, C.POINTER(vp), C.POINTER(vp), vp, i64,
+                                        i64, i64, i64, vp, i64, i32]),
     "ss_sum_f64": (i32, [vp, vp, i64, vp]),
     "ss_debug_bwd_stats": (i32, [vp, C.POINTER(u64), i32]),
     "ss_prepare_extras": (i32, [vp, C.POINTER(SSModel), C.POINTER(SSCamera), C.POINTER(SSLight), vp, i64,

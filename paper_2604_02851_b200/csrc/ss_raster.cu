@@ -1504,7 +1504,7 @@ template <int DEG>
 __global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const __grid_constant__ ChainViews Vp, int nv,
                                                         const int64_t* __restrict__ subset, int64_t j0, int64_t j1,
                                                         int64_t row0, int64_t ld,
-                                                        float* __restrict__ grad, float4* __restrict__ shrec) {
+                                                        float* __restrict__ grad, float4* __restrict__ shrec, int init) {
     SS_PDL_WAIT();
     const ChainViews* V = &Vp;  // the views ride in the kernel parameters (no host-to-device copy)
     const int64_t a = m.active_count;
@@ -1513,7 +1513,11 @@ __global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const 
         if (row >= a) continue;
         const int64_t rel = row - row0;
         float acc[11];
-        bool any = false;
+        bool any = init != 0;  // init: the layout was not cleared -- start from zero, always store
+        if (init) {
+#pragma unroll
+            for (int e = 0; e < 11; ++e) acc[e] = 0.f;
+        }
 #if CV_PREFETCH
         // the next views' screen-space gradients into L1 while this view's chain runs
         for (int v = 1; v < nv; ++v) asm volatile("prefetch.global.L1 [%0];" ::"l"(V->g9[v] + j * 9));
@@ -1546,7 +1550,7 @@ __global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const 
 template <int DEG>
 __global__ void __launch_bounds__(CVB, SHR_MINB) k_sh_grad_rows(const __grid_constant__ ChainViews Vp, int nv,
                                                       const float4* __restrict__ shrec, int64_t rows, int64_t ld,
-                                                      float* __restrict__ grad_sh) {
+                                                      float* __restrict__ grad_sh, int init) {
     SS_PDL_WAIT();
     constexpr int B = ss_sh_bases(DEG);
     constexpr int S = cv_sh_stride(B);
@@ -1555,7 +1559,8 @@ __global__ void __launch_bounds__(CVB, SHR_MINB) k_sh_grad_rows(const __grid_con
     for (int64_t rb = (int64_t)blockIdx.x * CVB; rb < rows; rb += (int64_t)gridDim.x * CVB) {
         const int nr = (int)min((int64_t)CVB, rows - rb);
         float* gb = grad_sh + rb * 3 * B;
-        for (int e = t; e < nr * 3 * B; e += CVB) s_sh[(e / (3 * B)) * S + e % (3 * B)] = gb[e];
+        // init: the layout was not cleared -- the rows start from zero
+        for (int e = t; e < nr * 3 * B; e += CVB) s_sh[(e / (3 * B)) * S + e % (3 * B)] = init ? 0.f : gb[e];
         __syncthreads();
         if (t < nr) sh_grad_row<DEG>(&Vp, nv, shrec + (rb + t) * 2, (int)(2 * ld), s_sh + t * S);
         __syncthreads();
@@ -1920,7 +1925,7 @@ int render_t(ss_ctx* ctx, const ss_model* m, const ss_camera* cam, const ss_ligh
 // runs it with one view, so a view's gradient is the same kernel's whether
 // the chain is deferred to the step or not (bit-identical by construction).
 int launch_chain_views(ss_ctx* ctx, const ss_model* m, const ChainViews& hv, int nv, const int64_t* subset,
-                       int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld) {
+                       int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld, int init = 0) {
     cudaStream_t s = ctx->stream;
     float4* shrec = SS_SCRATCH(ctx, float4, 2 * ld * nv);
     if (!shrec) return SS_ERR_CUDA;
@@ -1932,10 +1937,10 @@ int launch_chain_views(ss_ctx* ctx, const ss_model* m, const ChainViews& hv, int
 #define SS_CHAINV(DEG)                                                                                                     \
     do {                                                                                                                   \
         SS_CUDA(ctx, ss_launch((k_chain_views<DEG>), dim3(gridn(ctx, j1 - j0, CVB)), dim3(CVB), 0, s, *m, hv,              \
-                               nv, subset, j0, j1, row0, ld, grad, shrec));                                                \
+                               nv, subset, j0, j1, row0, ld, grad, shrec, init));                                          \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
         SS_CUDA(ctx, ss_launch((k_sh_grad_rows<DEG>), dim3(gridn(ctx, rows, CVB)), dim3(CVB), 0, s, hv, nv,               \
-                               (const float4*)shrec, rows, ld, grad + 11 * ld));                                          \
+                               (const float4*)shrec, rows, ld, grad + 11 * ld, init));                                    \
         SS_CHECK_LAUNCH(ctx);                                                                                              \
     } while (0)
     switch (m->sh_degree) {
@@ -2212,8 +2217,17 @@ int ss_composite(ss_ctx* ctx, int64_t n, const double* mu2d, const double* inv2d
 int ss_chain_views_range(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights,
                          int32_t n_views, const float* const* g9, const uint32_t* const* rinv, const int64_t* subset,
                          int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad, int64_t ld) {
+    return ss_chain_views_range_init(ctx, m, cams, lights, n_views, g9, rinv, subset, j0, j1, row0, rows, grad, ld, 0);
+}
+
+int ss_chain_views_range_init(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights,
+                              int32_t n_views, const float* const* g9, const uint32_t* const* rinv,
+                              const int64_t* subset, int64_t j0, int64_t j1, int64_t row0, int64_t rows, float* grad,
+                              int64_t ld, int32_t init) {
     SS_NVTX("ss_chain_views");
     if (!ctx || !m || !cams || !lights || !g9 || !rinv || !grad) return SS_ERR_INVALID;
+    if (init && (subset || j0 != row0 || j1 < row0 + rows))
+        return ss_fail(ctx, SS_ERR_INVALID, "init needs the whole row range without a subset");
     if (n_views < 1 || n_views > CV_MAX_VIEWS) return ss_fail(ctx, SS_ERR_INVALID, "1..%d views", CV_MAX_VIEWS);
     if (m->sh_degree < 0 || m->sh_degree > 3 || j0 < 0 || j1 < j0) return ss_fail(ctx, SS_ERR_INVALID, "bad model or row range");
     if (row0 < 0 || rows < 0 || ld < rows || row0 + rows > m->active_count)
@@ -2231,7 +2245,7 @@ int ss_chain_views_range(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, 
         hv.g9[v] = g9[v];
         hv.rinv[v] = rinv[v];
     }
-    return launch_chain_views(ctx, m, hv, n_views, subset, j0, j1, row0, rows, grad, ld);
+    return launch_chain_views(ctx, m, hv, n_views, subset, j0, j1, row0, rows, grad, ld, init);
 }
 
 int ss_chain_views(ss_ctx* ctx, const ss_model* m, const ss_camera* cams, const ss_light* lights, int32_t n_views,

@@ -506,13 +506,14 @@ class StepWorkspace:
         binning capacity); after this the model holds every step's update."""
         _settle(self, keep=0)
 
-    def prepare(self, grad_elems: int, n_views: int):
+    def prepare(self, grad_elems: int, n_views: int, clear_grad: bool = True):
         import torch
         if self.grad.numel() < max(grad_elems, 1):
             self.grad = torch.zeros(max(grad_elems, 1), dtype=torch.float32, device=self.device)
         if self.losses.numel() < n_views:
             self.losses = torch.zeros(n_views, dtype=torch.float64, device=self.device)
-        self.grad[:grad_elems].zero_()
+        if clear_grad:  # (else the step's first chain-rule call writes every entry)
+            self.grad[:grad_elems].zero_()
         self.losses[:n_views].zero_()
         self.loss.zero_()
         return self.grad[:max(grad_elems, 1)]
@@ -547,7 +548,7 @@ VIEW_LANES = max(1, int(os.environ.get("SS_VIEW_LANES", "4")))
 
 
 def chain_views(model: DeviceModel, views, g9, rinv, grad, subset_tensor=None, j0=0, j1=None, row0=0, rows=None,
-                ld=None):
+                ld=None, init=False):
     """The deferred chain rule of `views` (their backward_device calls got
     defer=(g9[i], rinv[i])): one pass over the rows, the gradient read and
     written once (ss_chain_views_range).  g9 / rinv entries are tensors or
@@ -565,9 +566,11 @@ def chain_views(model: DeviceModel, views, g9, rinv, grad, subset_tensor=None, j
     a = model.active_count
     rows = a if rows is None else rows
     ld = a if ld is None else ld
-    c.check(c.lib.ss_chain_views_range(c.handle, model.struct(), cams, lights, k, gp, rp,
-                                       _lib.ptr(subset_tensor) if subset_tensor is not None else None,
-                                       int(j0), int(j1), int(row0), int(rows), _lib.ptr(grad), int(ld)))
+    # init: the gradient rows were not cleared; every entry gets written (ss_chain_views_range_init)
+    c.check(c.lib.ss_chain_views_range_init(c.handle, model.struct(), cams, lights, k, gp, rp,
+                                            _lib.ptr(subset_tensor) if subset_tensor is not None else None,
+                                            int(j0), int(j1), int(row0), int(rows), _lib.ptr(grad), int(ld),
+                                            1 if init else 0))
 
 
 def _row_struct(dm: DeviceModel, row0: int, rows: int) -> _lib.SSModel:
@@ -595,7 +598,10 @@ class _DeviceKernels:
         self.n_in = int(subset.numel()) if subset is not None else dm.count
         B = (dm.sh_degree + 1) ** 2
         self.ld = dm.active_count if plan.world == 1 else plan.R
-        self.grad = ws.prepare(self.ld * (11 + 3 * B), len(views))
+        # without a row subset the first chain-rule call initialises the
+        # gradient (no clear of the 59-float rows, no first read of them)
+        self.init_chain = subset is None
+        self.grad = ws.prepare(self.ld * (11 + 3 * B), len(views), clear_grad=not self.init_chain)
         self.gts = {}
         self.views = views
         self.lanes = None
@@ -706,12 +712,13 @@ class _DeviceKernels:
             return
         g9 = [r[0] for r in recs]
         rinv = [r[1] for r in recs]
+        init, self.init_chain = self.init_chain, False  # the first batch initialises the gradient
         if self.plan.world == 1:
-            chain_views(self.dm, views, g9, rinv, self.grad, self.sub)
+            chain_views(self.dm, views, g9, rinv, self.grad, self.sub, init=init)
         else:
             r0, rows = self.plan.row0, self.plan.rows
             chain_views(self.dm, views, g9, rinv, self.grad, None, j0=r0, j1=r0 + rows, row0=r0, rows=rows,
-                        ld=self.ld)
+                        ld=self.ld, init=init)
 
     def sum_losses(self, coll):
         V = len(self.views)
