@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(SID_THREADS) k_snap_ids(const int32_t* __restr
     if (threadIdx.x == 0) s_tile = atomicAdd(&st->ticket, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
+    SS_ASSERT(tile < (n + SID_TILE - 1) / SID_TILE);
     const int64_t i0 = tile * SID_TILE + (int64_t)threadIdx.x * SID_ITEMS;
     uint32_t len[SID_ITEMS];
     uint64_t mine = 0;
