@@ -495,6 +495,7 @@ def run_ours(args):
     launches = int(counters[1])
     dom = max(per_step, key=per_step.get)
     roof = roofline(dom, per_step, kt, counters, args, len(mine), fp32_peak)
+    roof["hbm_alternative"] = step_hbm_roofline(args, dm, int(ws.bins_status[1].item()), ms_per_step, len(mine))
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -1114,6 +1115,27 @@ def committed_traffic(key):
     capture (profiles/r01_traffic.json); None when absent."""
     e = _committed(key)
     return e.get("bytes_per_launch", e.get("bytes_per_tick"))
+
+
+def step_hbm_roofline(args, dm, pairs_per_view, ms_per_step, local_views):
+    """SURVEY §8d optimize roofline (i), the HBM view of the whole step:
+    per view N (2P + 64) + pairs x 24 + H W (12 GT + 12 image + 4 T) + a P
+    bytes, plus Adam's 7 a P per step (P = 4 (11 + 3B) bytes per row), over
+    the measured step time.  Reported beside the FP32 roofline of the
+    dominant kernel (SURVEY: take the larger fraction -- the FP32 one)."""
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6551.4)
+    B = (dm.sh_degree + 1) ** 2
+    P = 4 * (11 + 3 * B)
+    n, a = dm.count, dm.active_count
+    px = args.width * args.height
+    per_view = n * (2 * P + 64) + pairs_per_view * 24 + px * 28 + a * P
+    per_step = local_views * per_view + 7 * a * P
+    gbs = per_step / (ms_per_step * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+            "bytes_per_step": per_step, "pairs_per_view": pairs_per_view,
+            "note": "whole-step algorithmic bytes (SURVEY §8d (i)) over the step time; pairs = the largest "
+                    "per-view (tile, splat) count of the run"}
 
 
 def roofline(dom, per_step, kt, counters, args, local_views, fp32_peak):
