@@ -133,13 +133,16 @@ def render_device_many(model: DeviceModel, poses, intr, light_state, outs=None, 
     path), dealt over `lanes` streams with one library
     context each so one viewpoint's latency-bound binning overlaps another's
     blend; the caller's stream waits for all of them.  `outs`: optional
-    (H, W, 3) float32 output buffers, used round-robin (a buffer is reused
-    only after the lane that last wrote it, i.e. len(outs) >= lanes keeps
-    the lanes independent).  Returns the images in pose order."""
+    (H, W, 3) float32 output buffers, used round-robin; with fewer buffers
+    than lanes the lane count drops to the buffer count (two lanes never
+    write one buffer).  Returns the images in pose order (with `outs`, a
+    buffer holds the last image written to it)."""
     import torch
     dev = model.device
     cur = torch.cuda.current_stream(dev)
     L = max(1, int(lanes))
+    if outs:
+        L = min(L, len(outs))
     streams = [cur] + [_lib.lane_stream(dev.index, k) for k in range(1, L)]
     for s in streams[1:]:
         s.wait_stream(cur)
