@@ -133,10 +133,10 @@ def render_device_many(model: DeviceModel, poses, intr, light_state, outs=None, 
     path), dealt over `lanes` streams with one library
     context each so one viewpoint's latency-bound binning overlaps another's
     blend; the caller's stream waits for all of them.  `outs`: optional
-    (H, W, 3) float32 output buffers, used round-robin; with fewer buffers
-    than lanes the lane count drops to the buffer count (two lanes never
-    write one buffer).  Returns the images in pose order (with `outs`, a
-    buffer holds the last image written to it)."""
+    (H, W, 3) float32 output buffers, one per lane (lane k writes outs[k];
+    with fewer buffers than lanes the lane count drops to the buffer count).
+    Returns the images in pose order (with `outs`, a buffer holds the last
+    image its lane wrote)."""
     import torch
     dev = model.device
     cur = torch.cuda.current_stream(dev)
@@ -155,7 +155,8 @@ def render_device_many(model: DeviceModel, poses, intr, light_state, outs=None, 
         k = i % L
         with torch.cuda.stream(streams[k]):
             c = _lib.lane_ctx(dev.index, k)
-            img = outs[i % len(outs)] if outs else torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+            # lane k always writes outs[k]: its images are ordered on its stream
+            img = outs[k] if outs else torch.empty((H, W, 3), dtype=torch.float32, device=dev)
             st = _lib.SSRenderStats()
             c.check(c.lib.ss_render(c.handle, m, camera_struct(pose, intr), L_, o, _lib.ptr(img), None, st))
             imgs.append(img)
