@@ -162,6 +162,9 @@ def render_device_many(model: DeviceModel, poses, intr, light_state, outs=None, 
             imgs.append(img)
     for s in streams[1:]:
         cur.wait_stream(s)
+    if not outs:  # allocated on lane streams, handed to the caller's stream
+        for img in imgs:
+            img.record_stream(cur)
     return imgs
 
 
