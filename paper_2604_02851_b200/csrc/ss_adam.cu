@@ -8,25 +8,9 @@
 // reference's float64 arithmetic.
 #include <math.h>
 
-#include "ss_internal.cuh"
+#include "ss_adam.cuh"
 
 namespace {
-
-struct AdamConst {
-    double scale, b1, b2, omb1, omb2, bc1, bc2, eps, ema_beta, omema;
-    double lr[6];  // means, log_scales, quaternions, logit_opacities, sh_dc, sh_rest
-    int64_t a;     // rows updated
-    int64_t ld;    // rows per group in the gradient / moment layout (>= a; padding rows are skipped)
-    int B;
-};
-
-// k % B == 0 for the SH bases counts B in {1, 4, 9, 16} without a 64-bit
-// division (a masked test, or k / 9 as a 64-bit multiply-high)
-__device__ __forceinline__ bool sh_is_dc(int64_t k, int B) {
-    const uint64_t u = (uint64_t)k;
-    if (B == 9) return u - 9 * (__umul64hi(u, 0xE38E38E38E38E38Full) >> 3) == 0;
-    return (u & (uint64_t)(B - 1)) == 0;  // B = 1, 4, 16
-}
 
 // parameter pointer and learning rate of flat element e (ss_grad_layout with
 // `a` = ld rows per group); with PADDED, NULL for an element of a padding
@@ -102,15 +86,9 @@ __global__ void k_adam(PT* __restrict__ means, PT* __restrict__ ls, PT* __restri
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t e = e0 + u * stride;
             if (!p[u]) continue;
-            const double gg = dm((double)gv[u], c.scale);
-            const double mm = da(dm(c.b1, mv[u]), dm(c.omb1, gg));
-            const double v2 = da(dm(c.b2, vv[u]), dm(dm(c.omb2, gg), gg));
-            m[e] = mm;
-            v[e] = v2;
-            const double mh = dd(mm, c.bc1);
-            const double vh = dd(v2, c.bc2);
-            const double upd = dm(dd(mh, da(dsq(vh), c.eps)), lr[u]);
-            const float nv = __double2float_rn(ds((double)pv[u], upd));
+            const float nv = adam_elem(gv[u], mv[u], vv[u], (double)pv[u], lr[u], c);
+            m[e] = mv[u];
+            v[e] = vv[u];
             *p[u] = (PT)nv;
             if constexpr (PEERS) {
 #pragma unroll 1
@@ -128,10 +106,8 @@ __global__ void k_adam_rows(PT* __restrict__ quats, const float* __restrict__ g,
     if (skip_if && *skip_if) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.a; i += (int64_t)gridDim.x * blockDim.x) {
         PT* q = quats + 4 * i;
-        const double w = q[0], x = q[1], y = q[2], z = q[3];
-        const double n = dsq(da(da(da(dm(w, w), dm(x, x)), dm(y, y)), dm(z, z)));
-        const float qn[4] = {__double2float_rn(dd(w, n)), __double2float_rn(dd(x, n)), __double2float_rn(dd(y, n)),
-                             __double2float_rn(dd(z, n))};
+        float qn[4];
+        adam_quat_renorm(q[0], q[1], q[2], q[3], qn);
 #pragma unroll
         for (int k = 0; k < 4; ++k) q[k] = (PT)qn[k];
         if constexpr (PEERS) {
@@ -140,11 +116,11 @@ __global__ void k_adam_rows(PT* __restrict__ quats, const float* __restrict__ g,
 #pragma unroll
                 for (int k = 0; k < 4; ++k) peers.g[p][2][4 * i + k] = qn[k];
         }
-        const double g0 = dm((double)g[3 * i], c.scale), g1 = dm((double)g[3 * i + 1], c.scale),
-                     g2 = dm((double)g[3 * i + 2], c.scale);
-        const double norm = dsq(da(da(dm(g0, g0), dm(g1, g1)), dm(g2, g2)));
-        ema[i] = age[i] == 0 ? norm : da(dm(c.ema_beta, ema[i]), dm(c.omema, norm));
-        age[i] += 1;
+        double e = ema[i];
+        int64_t ag = age[i];
+        adam_ema_age(g[3 * i], g[3 * i + 1], g[3 * i + 2], e, ag, c);
+        ema[i] = e;
+        age[i] = ag;
     }
 }
 
@@ -172,26 +148,7 @@ extern "C" int ss_adam_step_peers(ss_ctx* ctx, ss_model* model, ss_adam_state* s
         st->step_count = t;
         return SS_OK;
     }
-    AdamConst c;
-    c.scale = 1.0 / (double)n_views;
-    c.b1 = hp->beta1;
-    c.b2 = hp->beta2;
-    c.omb1 = 1.0 - hp->beta1;
-    c.omb2 = 1.0 - hp->beta2;
-    c.bc1 = 1.0 - pow(hp->beta1, (double)t);  // host libm pow, as Python's float **
-    c.bc2 = 1.0 - pow(hp->beta2, (double)t);
-    c.eps = hp->eps;
-    c.ema_beta = hp->ema_beta;
-    c.omema = 1.0 - hp->ema_beta;
-    c.lr[0] = hp->lr_means;
-    c.lr[1] = hp->lr_log_scales;
-    c.lr[2] = hp->lr_quaternions;
-    c.lr[3] = hp->lr_logit_opacities;
-    c.lr[4] = hp->lr_sh_dc;
-    c.lr[5] = hp->lr_sh_rest;
-    c.a = a;
-    c.ld = ld;
-    c.B = (model->sh_degree + 1) * (model->sh_degree + 1);
+    const AdamConst c = adam_const(hp, t, n_views, a, ld, model->sh_degree);
     const int64_t total = ld * (11 + 3 * (int64_t)c.B);
     int64_t grid = (total + 255) / 256;
     if (grid > (int64_t)ctx->num_sms * 32) grid = (int64_t)ctx->num_sms * 32;
