@@ -1465,13 +1465,49 @@ struct ChainViews {
 // optim.py:221-233: the ambient product, the view-dependent basis and the
 // direct-light term through albedo_est = C0 dc + 0.5.  `rec` is the row's
 // record of view v at rec[v * stride]; io holds the row's 3B entries.
+// per view, the SH-gradient constants in float (ss_light's doubles converted
+// once per block instead of once per row): amb[v][c][b] = [b < BL]
+// ambient[c][b] (zero without ambient light), dc[v][c] = C0 I_c, has_amb[v]
+struct ShConst {
+    float amb[CV_MAX_VIEWS][3][16];
+    float dc[CV_MAX_VIEWS][3];
+    int has_amb[CV_MAX_VIEWS];
+};
+
 template <int DEG>
-__device__ __forceinline__ void sh_grad_row(const ChainViews* V, int nv, const float4* rec, int stride, float* io) {
+__device__ __forceinline__ void sh_const_load(const ChainViews* V, int nv, ShConst& K) {
     constexpr int B = ss_sh_bases(DEG);
+    for (int i = threadIdx.x; i < nv * 3 * B; i += blockDim.x) {
+        const int v = i / (3 * B), r = i - v * 3 * B, c = r / B, b = r - c * B;
+        const ss_light& L = V->light[v];
+        const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+        K.amb[v][c][b] = b < BL ? (float)L.ambient[c * L.ambient_bands + b] : 0.f;
+        if (b == 0) K.dc[v][c] = (float)(SS_SH_C0 * L.intensity[c]);
+        if (r == 0) K.has_amb[v] = L.ambient_bands != 0;
+    }
+}
+
+// SH coefficient gradients of one row from its per-view records (gc, cos vis,
+// view dir): g_sh[c, b] += gc_{v,c} K_{v,c,b} in view order with
+//   K = [b < BL] ambient[c][b] + [b >= 1] Y_b(view dir) + [b == 0] C0 I_c cos vis
+// (ambient light; without it K = Y_b + [b == 0] C0 I_c cos vis) -- ref
+// optim.py:221-233: the ambient product, the view-dependent basis and the
+// direct-light term through albedo_est = C0 dc + 0.5.  `rec` is the row's
+// record of view v at rec[v * stride]; io holds the row's 3B entries.  The
+// views' first record halves are loaded up front (their loads overlap).
+template <int DEG>
+__device__ __forceinline__ void sh_grad_row(const ShConst& K, int nv, const float4* rec, int stride, float* io) {
+    constexpr int B = ss_sh_bases(DEG);
+    float4 r0s[CV_MAX_VIEWS];
+#pragma unroll
+    for (int v = 0; v < CV_MAX_VIEWS; ++v)
+        if (v < nv) r0s[v] = rec[(size_t)v * stride];
     float acc[3 * B];
     bool loaded = false;
-    for (int v = 0; v < nv; ++v) {
-        const float4 r0 = rec[(size_t)v * stride];
+#pragma unroll
+    for (int v = 0; v < CV_MAX_VIEWS; ++v) {
+        if (v >= nv) break;
+        const float4 r0 = r0s[v];
         if (r0.x == 0.f && r0.y == 0.f && r0.z == 0.f) continue;  // clamped colour or not visible
         if (!loaded) {
 #pragma unroll
@@ -1482,8 +1518,7 @@ __device__ __forceinline__ void sh_grad_row(const ChainViews* V, int nv, const f
         const float dir[3] = {r1.x, r1.y, r1.z};
         float Y[B];
         ss_sh_eval<DEG, float>(dir, Y);
-        const ss_light& L = V->light[v];
-        const int BL = L.ambient_bands < B ? L.ambient_bands : B;
+        const bool amb = K.has_amb[v];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const float gcc = c == 0 ? r0.x : (c == 1 ? r0.y : r0.z);
@@ -1491,9 +1526,9 @@ __device__ __forceinline__ void sh_grad_row(const ChainViews* V, int nv, const f
 #pragma unroll
             for (int b = 0; b < B; ++b) {
                 float kv;
-                if (L.ambient_bands == 0) kv = Y[b];
-                else kv = (b < BL ? (float)L.ambient[c * L.ambient_bands + b] : 0.f) + (b >= 1 ? Y[b] : 0.f);
-                if (b == 0) kv += (float)(SS_SH_C0 * L.intensity[c]) * r0.w;
+                if (!amb) kv = Y[b];
+                else kv = K.amb[v][c][b] + (b >= 1 ? Y[b] : 0.f);
+                if (b == 0) kv += K.dc[v][c] * r0.w;
                 acc[c * B + b] = fmaf(gcc, kv, acc[c * B + b]);
             }
         }
@@ -1558,7 +1593,7 @@ __global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const 
 // they are staged through shared memory (coalesced reads and writes, the
 // row's 3B entries in registers across the views).
 #ifndef SHR_MINB
-#define SHR_MINB 6  // measured (chain class per step): 1 / 4 / 5 / 6 / 8 -> 1.972 / 1.972 / 1.973 / 1.934 / 2.193 ms
+#define SHR_MINB 3  // measured (chain class per step, views' first records loaded up front): 2 / 3 / 4 / 5 / 6 -> 1.770 / 1.773 / 1.836 / 2.390 / 2.696 ms
 #endif
 template <int DEG>
 __global__ void __launch_bounds__(CVB, SHR_MINB) k_sh_grad_rows(const __grid_constant__ ChainViews Vp, int nv,
@@ -1568,6 +1603,8 @@ __global__ void __launch_bounds__(CVB, SHR_MINB) k_sh_grad_rows(const __grid_con
     constexpr int B = ss_sh_bases(DEG);
     constexpr int S = cv_sh_stride(B);
     __shared__ float s_sh[CVB * S];
+    __shared__ ShConst K;
+    sh_const_load<DEG>(&Vp, nv, K);
     const int t = threadIdx.x;
     for (int64_t rb = (int64_t)blockIdx.x * CVB; rb < rows; rb += (int64_t)gridDim.x * CVB) {
         const int nr = (int)min((int64_t)CVB, rows - rb);
@@ -1575,7 +1612,7 @@ __global__ void __launch_bounds__(CVB, SHR_MINB) k_sh_grad_rows(const __grid_con
         // init: the layout was not cleared -- the rows start from zero
         for (int e = t; e < nr * 3 * B; e += CVB) s_sh[(e / (3 * B)) * S + e % (3 * B)] = init ? 0.f : gb[e];
         __syncthreads();
-        if (t < nr) sh_grad_row<DEG>(&Vp, nv, shrec + (rb + t) * 2, (int)(2 * ld), s_sh + t * S);
+        if (t < nr) sh_grad_row<DEG>(K, nv, shrec + (rb + t) * 2, (int)(2 * ld), s_sh + t * S);
         __syncthreads();
         for (int e = t; e < nr * 3 * B; e += CVB) gb[e] = s_sh[(e / (3 * B)) * S + e % (3 * B)];
         __syncthreads();
