@@ -1570,8 +1570,13 @@ __global__ void __launch_bounds__(CVB, CV_MINB) k_chain_views(ss_model m, const 
         // the next views' screen-space gradients into L1 while this view's chain runs
         for (int v = 1; v < nv; ++v) asm volatile("prefetch.global.L1 [%0];" ::"l"(V->g9[v] + j * 9));
 #endif
+        // the row's visibility in every view first (independent loads, one mask)
+        unsigned vis = 0;
+#pragma unroll
+        for (int v = 0; v < CV_MAX_VIEWS; ++v)
+            if (v < nv && V->rinv[v][j] != ~0u) vis |= 1u << v;
         for (int v = 0; v < nv; ++v) {
-            if (V->rinv[v][j] == ~0u) {  // not visible: a zero record
+            if (!((vis >> v) & 1u)) {  // not visible: a zero record
                 shrec[((int64_t)v * ld + rel) * 2] = make_float4(0.f, 0.f, 0.f, 0.f);
                 continue;
             }
