@@ -312,11 +312,21 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the multi-rank orchestration on a one-GPU box only:
+    # SS_BENCH_BACKEND=gloo SS_BENCH_SAME_DEVICE=1 puts every rank on cuda:0
+    # with host-staged collectives (no rank's kernels wait on another's);
+    # its numbers measure nothing
+    backend = os.environ.get("SS_BENCH_BACKEND", "nccl")
+    if os.environ.get("SS_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist.group.WORLD
 
     model_h, tgt_h, poses, intr, light = build_workload(args)
