@@ -225,3 +225,33 @@ def test_gpu_render_device_many_matches_single():
     torch.cuda.synchronize()
     for a, b in zip(ref[:3], last):
         assert torch.equal(a, b)
+
+
+def test_gpu_evaluated_pairs_counter_matches_oracle():
+    """the roofline's work count -- (pixel, splat) evaluations
+    that pass the T-gate, counted by the forward kernel in timing runs --
+    against the oracle's own count on a config-1-sized view (10k Gaussians,
+    256x256).  fp32 vs fp64 may flip the T-gate of a handful of pixels."""
+    require_gpu()
+    from oracle import raster as orr
+    from paper_2604_02851_b200 import _lib, synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.render import render_device
+    W = H = 256
+    host = synth.random_field(10_000, 3, W, H, seed=5)
+    dm = DeviceModel.from_host(host, 0)
+    intr, light = synth.intrinsics(W, H), synth.light()
+    pose = synth.ring_poses(4, radius=0.5)[1]
+    c = _lib.ctx(0)
+    render_device(dm, pose, intr, light)  # warm (no counting)
+    _lib.set_timing(c, True)
+    _lib.get_timing(c, reset=True)
+    render_device(dm, pose, intr, light)
+    _, counters = _lib.get_timing(c, reset=True)
+    _lib.set_timing(c, False)
+    cam = orr.camera(pose, intr)
+    olight = dict(direction=light.direction, intensity=light.intensity, ambient=light.ambient_sh)
+    prep = orr.prepare(host, cam, olight, None, True)
+    _, _, pairs = orr.composite(prep, W, H, np.zeros(3))
+    assert pairs > 100_000
+    assert abs(int(counters[0]) - pairs) <= max(10, 1e-5 * pairs), (int(counters[0]), pairs)
