@@ -1122,6 +1122,14 @@ __global__ void __launch_bounds__(256, SP_MINB) k_sum_partials(const uint64_t* _
         const int64_t r = r0 + lane;
         const bool valid = r < n_in;
         const uint64_t off = valid ? roff[r] : 0, cnt = valid ? rcnt[r] : 0;
+        // the output row and its clamp mask first: their (random) loads
+        // overlap the partial sums instead of following them
+        const uint32_t j = valid ? dvals[r] : 0u;
+        bool open[3] = {false, false, false};
+        if (valid && cnt) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) open[c] = clamp_open(rec[j].col[c]);
+        }
         const uint64_t P0 = __shfl_sync(0xffffffffu, off, 0);
         uint64_t end = valid ? off + cnt : 0;
 #pragma unroll
@@ -1153,12 +1161,11 @@ __global__ void __launch_bounds__(256, SP_MINB) k_sum_partials(const uint64_t* _
             __syncwarp();
         }
         if (valid) {
-            const uint32_t j = dvals[r];
             SS_ASSERT(j < (uint64_t)n_in);
             R* o = g9 + (int64_t)j * 9;
             if (cnt) {  // dL/dcolour through the clamp: zero where the forward clamped (optim.py:176-177)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) g[c] = clamp_open(rec[j].col[c]) ? g[c] : (R)0;
+                for (int c = 0; c < 3; ++c) g[c] = open[c] ? g[c] : (R)0;
             }
 #pragma unroll
             for (int e = 0; e < 9; ++e) o[e] = g[e];
