@@ -1,5 +1,6 @@
 """The view-sharded optimize step through the product path (optim.step with a
-process group), world size 2, against the single-GPU step: bit-identical.
+process group), world size 2 and 3 (3 ranks over 2 views: a rank without a view), against
+the single-GPU step: bit-identical.
 
 Both ranks run on cuda:0 in separate processes with a gloo group; the
 collectives are staged through host memory (parallel.Collectives), so the
@@ -72,9 +73,10 @@ def _subset():
     return np.sort(rng.choice(30_000, 21_000, replace=False))
 
 
-@pytest.mark.parametrize("n_views,use_subset,exchange", [(4, False, "collectives"), (3, True, "collectives"),
-                                                         (4, False, "p2p"), (3, True, "p2p")])
-def test_gpu_sharded_step_bit_identical(n_views, use_subset, exchange):
+@pytest.mark.parametrize("n_views,use_subset,exchange,world", [(4, False, "collectives", 2), (3, True, "collectives", 2),
+                                                               (4, False, "p2p", 2), (3, True, "p2p", 2),
+                                                               (2, False, "p2p", 3), (5, True, "p2p", 3)])
+def test_gpu_sharded_step_bit_identical(n_views, use_subset, exchange, world):
     """exchange="collectives": an all-to-all of the records and an all-gather of
     the parameter rows; "p2p": the chain rule reads the peers' records from
     their memory and Adam stores every updated row into the peers' replicas
@@ -85,10 +87,11 @@ def test_gpu_sharded_step_bit_identical(n_views, use_subset, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_views, use_subset, exchange, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_views, use_subset, exchange, q))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted((q.get(timeout=600) for _ in range(2)), key=lambda x: x[0])
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda x: x[0])
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
