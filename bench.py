@@ -1073,7 +1073,7 @@ def live_tick_bench(dm, state, poses, intr, light_state, torch, ticks=6):
         marks.append(time.perf_counter())
         for p, g in zip(poses, gts):
             engine.render_ground_truth_device(scene, p, intr, out=g)
-        subset = pool.precull(dm, grid, poses, intr) if grid.cells is not None else None
+        subset = pool.precull(dm, grid, poses, intr, as_tensor=True) if grid.cells is not None else None
         step(dm, state, views, index_subset=subset, workspace=ws, sync_loss=False)
         grid.rebuild(dm)
         pool.freeze_policy(dm, state, age_threshold=120, grad_threshold=3e-4)

@@ -53,12 +53,14 @@ def _ctx(model):
     return c
 
 
-def _select(model: DeviceModel, s: _lib.SSSelect) -> np.ndarray:
+def _select(model: DeviceModel, s: _lib.SSSelect, as_tensor: bool = False):
     import torch
     out = torch.empty(max(int(s.n), 1), dtype=torch.int64, device=model.device)
     cnt = _lib.i64(0)
     c = _ctx(model)
     c.check(c.lib.ss_select_rows(c.handle, s, out.data_ptr(), C_byref(cnt)))
+    if as_tensor:  # the rows stay on the device (ascending)
+        return out[:cnt.value]
     return out[:cnt.value].cpu().numpy()
 
 
@@ -294,12 +296,16 @@ class GridIndex:
         self.initialized_cells.add(tuple(int(v) for v in cell))
 
 
-def precull(model: DeviceModel, grid: GridIndex, poses: Sequence, intr, depth_buffers=None) -> np.ndarray:
+def precull(model: DeviceModel, grid: GridIndex, poses: Sequence, intr, depth_buffers=None, as_tensor: bool = False):
     """ref expansion.py:145-181 on the device: rows (as of the grid's last
     rebuild) whose cell passes the conservative frustum test in any camera,
-    with the engine-depth occlusion test when depth buffers are given."""
+    with the engine-depth occlusion test when depth buffers are given.
+    as_tensor=True keeps the rows on the device (a CUDA int64 tensor, the
+    optimizer step's index_subset without a round trip through the host)."""
     import torch
     if grid.cells is None or grid.cells.shape[0] == 0:
+        if as_tensor:
+            return torch.zeros(0, dtype=torch.int64, device=model.device)
         return np.zeros(0, dtype=np.int64)
     cams = (_lib.SSPoolCamera * max(len(poses), 1))()
     keep_alive = []
@@ -331,8 +337,9 @@ def precull(model: DeviceModel, grid: GridIndex, poses: Sequence, intr, depth_bu
     s.margin = grid.cell_diagonal / 2.0
     s.n_cameras = len(poses)
     s.cameras = cams
-    out = _select(model, s)
-    torch.cuda.current_stream(model.device).synchronize()
+    out = _select(model, s, as_tensor)
+    if not as_tensor:
+        torch.cuda.current_stream(model.device).synchronize()
     return out
 
 

@@ -78,11 +78,18 @@ def light_struct(light) -> _lib.SSLight:
 
 
 def _subset_tensor(index_subset, device):
+    """The row subset as a sorted device int64 tensor (composite ties break
+    by row, render.py:283).  A CUDA tensor is sorted in place on the device;
+    host indices go up through pinned memory without a host stall (a
+    pageable upload would wait for all the work queued before it)."""
     if index_subset is None:
         return None
     import torch
-    idx = np.sort(np.asarray(index_subset, np.int64).ravel())  # composite ties break by row (render.py:283)
-    return torch.from_numpy(idx).to(device)
+    if isinstance(index_subset, torch.Tensor) and index_subset.is_cuda:
+        t = index_subset.to(device=device, dtype=torch.int64).reshape(-1)
+        return torch.sort(t).values
+    idx = np.sort(np.asarray(index_subset, np.int64).ravel())
+    return torch.from_numpy(idx).pin_memory().to(device, non_blocking=True)
 
 
 def render_opts(background, subset, extent_cutoff, precision, deterministic=1, gt_ready=None,

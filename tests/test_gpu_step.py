@@ -286,3 +286,37 @@ def test_gpu_view_lanes_bit_identical(lanes, monkeypatch):
         assert torch.equal(getattr(dm, k), getattr(ref_dm, k)), k
     for k in GROUPS:
         np.testing.assert_array_equal(state.m[k], ref_state.m[k])
+
+
+def test_gpu_step_device_subset_matches_host_subset():
+    """index_subset as a CUDA tensor (e.g. pool.precull(..., as_tensor=True),
+    unsorted here) gives the same step as the host indices."""
+    require_gpu()
+    import torch
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
+    from paper_2604_02851_b200.render import render_device
+    W, H = 256, 160
+    host = synth.random_field(20_000, 2, W, H, seed=51)
+    tgt = DeviceModel.from_host(synth.target_model(host, seed=52), 0)
+    intr, light = synth.intrinsics(W, H), synth.light()
+    views = [ReferenceView(p, intr, render_device(tgt, p, intr, light), light, np.zeros(3))
+             for p in synth.ring_poses(3, radius=0.5)]
+    rng = np.random.default_rng(3)
+    sub = np.sort(rng.choice(20_000, 14_000, replace=False))
+
+    def run(s):
+        dm = DeviceModel.from_host(host, 0)
+        state = OptimizerState(dm, scene_extent=2.0)
+        ws = StepWorkspace(dm)
+        losses = [step(dm, state, views, index_subset=s, workspace=ws) for _ in range(2)]
+        torch.cuda.synchronize()
+        return dm, losses
+
+    ref_dm, ref_l = run(sub)
+    perm = rng.permutation(sub.size)
+    dm, losses = run(torch.from_numpy(sub[perm]).cuda())
+    assert losses == ref_l
+    for k in GROUPS:
+        assert torch.equal(getattr(dm, k), getattr(ref_dm, k)), k

@@ -78,6 +78,7 @@ def test_gpu_grid_and_precull(c):
     intr = CameraIntrinsics(width=c["width"], height=c["height"], fov_y=c["fov_y"], near=c["near"], far=c["far"])
     poses = [Pose(p[:3], p[3:]) for p in c.a("poses")]
     np.testing.assert_array_equal(pool.precull(m, g, poses, intr), c.a("precull"))
+    np.testing.assert_array_equal(pool.precull(m, g, poses, intr, as_tensor=True).cpu().numpy(), c.a("precull"))
     np.testing.assert_array_equal(pool.precull(m, g, poses, intr, [c.a("depth0"), c.a("depth1")]),
                                   c.a("precull_depth"))
 
