@@ -606,6 +606,7 @@ class _DeviceKernels:
         self.views = views
         self.lanes = None
         self._n_local = 0
+        self._view_lane = {}
 
     def stage(self, local_views):
         gts = _stage_ground_truth(local_views, self.dm.device)
@@ -649,6 +650,11 @@ class _DeviceKernels:
         import torch
         k, stream = self._lane(self._n_local)
         self._n_local += 1
+        # a view object passed twice keeps its first lane: its per-camera tile
+        # hint / order buffers are then written in stream order
+        k0 = self._view_lane.setdefault(id(view), k)
+        if k0 != k:
+            k, stream = k0, self.lanes[k0][0]
         with torch.cuda.stream(stream):
             self._backward(view, rec, i, _lib.lane_ctx(self.dm.device.index, k))
 

@@ -320,3 +320,40 @@ def test_gpu_step_device_subset_matches_host_subset():
     assert losses == ref_l
     for k in GROUPS:
         assert torch.equal(getattr(dm, k), getattr(ref_dm, k)), k
+
+
+def test_gpu_step_repeated_view_object():
+    """The same ReferenceView passed twice in one step (its camera's tile
+    buffers shared by both backward passes) equals two separate, identical
+    view objects."""
+    require_gpu()
+    import copy
+    import torch
+    from paper_2604_02851_b200 import synth
+    from paper_2604_02851_b200.model import DeviceModel
+    from paper_2604_02851_b200.optim import OptimizerState, ReferenceView, StepWorkspace, step
+    from paper_2604_02851_b200.render import render_device
+    W, H = 256, 160
+    host = synth.random_field(20_000, 1, W, H, seed=61)
+    tgt = DeviceModel.from_host(synth.target_model(host, seed=62), 0)
+    intr, light = synth.intrinsics(W, H), synth.light()
+    base = [ReferenceView(p, intr, render_device(tgt, p, intr, light), light, np.zeros(3))
+            for p in synth.ring_poses(3, radius=0.5)]
+
+    def run(views):
+        dm = DeviceModel.from_host(host, 0)
+        state = OptimizerState(dm, scene_extent=2.0)
+        ws = StepWorkspace(dm)
+        losses = [step(dm, state, views, workspace=ws) for _ in range(3)]
+        torch.cuda.synchronize()
+        return dm, losses
+
+    a = [base[0], base[1], base[0], base[2], base[0]]
+    b = [copy.copy(base[0]), copy.copy(base[1]), copy.copy(base[0]), copy.copy(base[2]), copy.copy(base[0])]
+    for v in b:
+        v.__dict__.pop("_tile_hint", None), v.__dict__.pop("_tile_order", None)
+    dm_a, la = run(a)
+    dm_b, lb = run(b)
+    assert la == lb
+    for k in GROUPS:
+        assert torch.equal(getattr(dm_a, k), getattr(dm_b, k)), k
