@@ -146,3 +146,48 @@ def as_device(model, device=None, keep_f64: bool = False):
     if isinstance(model, DeviceModel):
         return model, False
     return DeviceModel.from_host(model, device, keep_f64), True
+
+
+# ---------------------------------------------------------------- GSM1 container (ref model.py:407-442)
+MODEL_MAGIC = b"GSM1"
+
+
+def save_model(path, model) -> None:
+    """ref model.py:410-416: magic, <III (sh_degree, count, active_count), then
+    every attribute as little-endian float32 (object ids too), in
+    ATTRIBUTE_NAMES order.  A DeviceModel is read back attribute by
+    attribute; the bytes equal the reference's for the same rows."""
+    import struct
+    with open(path, "wb") as f:
+        f.write(MODEL_MAGIC)
+        f.write(struct.pack("<III", model.sh_degree, model.count, model.active_count))
+        for name in ATTRIBUTE_NAMES:
+            a = getattr(model, name)
+            if not isinstance(a, np.ndarray):  # a CUDA tensor of a DeviceModel
+                a = a.cpu().numpy()
+            f.write(np.ascontiguousarray(a, dtype="<f4").tobytes())
+
+
+def load_model(path, device=None):
+    """ref model.py:419-442: the container as a host GaussianModel, or, with
+    `device`, uploaded as a DeviceModel."""
+    import struct
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:4] != MODEL_MAGIC:
+        raise ValueError("not a model container")
+    sh_degree, count, active_count = struct.unpack_from("<III", data, 4)
+    B = num_sh_bases(sh_degree)
+    shapes = {"means": (count, 3), "log_scales": (count, 3), "quaternions": (count, 4), "logit_opacities": (count,),
+              "sh_coeffs": (count, 3, B), "light_visibility": (count,), "object_ids": (count,)}
+    off = 16
+    arrays = {}
+    for name in ATTRIBUTE_NAMES:
+        n = int(np.prod(shapes[name]))
+        arr = np.frombuffer(data, dtype="<f4", count=n, offset=off).reshape(shapes[name])
+        off += 4 * n
+        arrays[name] = arr.astype(np.int32) if name == "object_ids" else arr.astype(np.float32)
+    host = GaussianModel(active_count=active_count, sh_degree=sh_degree, **arrays)
+    if device is None:
+        return host
+    return DeviceModel.from_host(host, device)
