@@ -1178,6 +1178,15 @@ template <typename T> __device__ __forceinline__ T t_exp(T x);
 template <> __device__ __forceinline__ float t_exp<float>(float x) { return expf(x); }
 template <> __device__ __forceinline__ double t_exp<double>(double x) { return exp(x); }
 
+// a / b in the chain rule: fp32 multiplies by the reciprocal ib = 1 / b (one
+// division per divisor instead of one per quotient; the fp32 chain rule is
+// tolerance-checked against the reference), fp64 divides exactly
+template <typename T>
+__device__ __forceinline__ T cdiv(T a, T b, T ib) {
+    if constexpr (sizeof(T) == 4) return a * ib;
+    else return a / b;
+}
+
 // The chain rule of one (row, view) (ref optim.py:170-268): adds the row's
 // parameter gradients of this view into acc (means 3, log scales 3,
 // quaternion 4, opacity 1) with the same fp32 additions the gradient buffer
@@ -1199,7 +1208,8 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
 #pragma unroll
     for (int i = 0; i < 3; ++i) d[i] = (T)((double)pv.means[row * 3 + i] - cam.position[i]);
     const T dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    const T vdir[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+    const T idist = (T)1 / dist;
+    const T vdir[3] = {cdiv(d[0], dist, idist), cdiv(d[1], dist, idist), cdiv(d[2], dist, idist)};
     const PT* lsp = pv.ls + row * 3;
     int axis;
     {
@@ -1208,12 +1218,13 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
         axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
     }
     T u[4];
-    T qn;
+    T qn, iqn;
     {
         const PT* qp = pv.quats + row * 4;
         const T q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
         qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-        u[0] = q0 / qn; u[1] = q1 / qn; u[2] = q2 / qn; u[3] = q3 / qn;
+        iqn = (T)1 / qn;
+        u[0] = cdiv(q0, qn, iqn); u[1] = cdiv(q1, qn, iqn); u[2] = cdiv(q2, qn, iqn); u[3] = cdiv(q3, qn, iqn);
     }
     const T w = u[0], qx = u[1], qy = u[2], qz = u[3];
     T Rq[3][3];
@@ -1336,7 +1347,7 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     if constexpr (DEG > 0) {  // view-direction path (optim.py:235-240)
         const T vg = vdir[0] * gv[0] + vdir[1] * gv[1] + vdir[2] * gv[2];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) gmean[i] += (gv[i] - vdir[i] * vg) / dist;
+        for (int i = 0; i < 3; ++i) gmean[i] += cdiv(gv[i] - vdir[i] * vg, dist, idist);
     }
     // ---- scales and rotation (optim.py:204-218)
     T gls[3];
@@ -1393,7 +1404,7 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
         acc[3 + i] += (float)gls[i];
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc[6 + k] += (float)((h[k] - u[k] * udh) / qn);
+    for (int k = 0; k < 4; ++k) acc[6 + k] += (float)cdiv(h[k] - u[k] * udh, qn, iqn);
     acc[10] += (float)(g[3] * op * (1 - op));
 }
 
