@@ -1174,13 +1174,34 @@ __global__ void __launch_bounds__(256, SP_MINB) k_sum_partials(const uint64_t* _
 }
 
 // (b) the chain rule in row order
+#ifndef CHAIN_FAST_NORM
+#define CHAIN_FAST_NORM 1  // fp32 chain rule: norms and their inverses from one rsqrt
+#endif
+#ifndef CHAIN_FAST_EXP
+#define CHAIN_FAST_EXP 1  // fp32 chain rule: the hardware exp2-based __expf (tolerance-checked)
+#endif
 template <typename T> __device__ __forceinline__ T t_exp(T x);
-template <> __device__ __forceinline__ float t_exp<float>(float x) { return expf(x); }
+template <> __device__ __forceinline__ float t_exp<float>(float x) { return CHAIN_FAST_EXP ? __expf(x) : expf(x); }
 template <> __device__ __forceinline__ double t_exp<double>(double x) { return exp(x); }
 
 // a / b in the chain rule: fp32 multiplies by the reciprocal ib = 1 / b (one
 // division per divisor instead of one per quotient; the fp32 chain rule is
 // tolerance-checked against the reference), fp64 divides exactly
+// |v| and 1 / |v| from v.v: fp32 from one rsqrt (x * rsqrt(x) for the norm),
+// fp64 the IEEE sqrt and its reciprocal
+template <typename T>
+__device__ __forceinline__ void norm_and_inverse(T x, T& n, T& inv) {
+    if constexpr (sizeof(T) == 4) {
+        if (CHAIN_FAST_NORM) {
+            inv = rsqrtf(x);
+            n = x * inv;
+            return;
+        }
+    }
+    n = sqrt(x);
+    inv = (T)1 / n;
+}
+
 template <typename T>
 __device__ __forceinline__ T cdiv(T a, T b, T ib) {
     if constexpr (sizeof(T) == 4) return a * ib;
@@ -1207,8 +1228,8 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     T d[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) d[i] = (T)((double)pv.means[row * 3 + i] - cam.position[i]);
-    const T dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    const T idist = (T)1 / dist;
+    T dist, idist;
+    norm_and_inverse(d[0] * d[0] + d[1] * d[1] + d[2] * d[2], dist, idist);
     const T vdir[3] = {cdiv(d[0], dist, idist), cdiv(d[1], dist, idist), cdiv(d[2], dist, idist)};
     const PT* lsp = pv.ls + row * 3;
     int axis;
@@ -1222,8 +1243,7 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     {
         const PT* qp = pv.quats + row * 4;
         const T q0 = qp[0], q1 = qp[1], q2 = qp[2], q3 = qp[3];
-        qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-        iqn = (T)1 / qn;
+        norm_and_inverse(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3, qn, iqn);
         u[0] = cdiv(q0, qn, iqn); u[1] = cdiv(q1, qn, iqn); u[2] = cdiv(q2, qn, iqn); u[3] = cdiv(q3, qn, iqn);
     }
     const T w = u[0], qx = u[1], qy = u[2], qz = u[3];
