@@ -1294,7 +1294,8 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
     for (int k = 0; k < 3; ++k) mc[k] = d[0] * Rc[0][k] + d[1] * Rc[1][k] + d[2] * Rc[2][k];
     const T x = mc[0], y = mc[1], z = mc[2];
     const T iz = (T)1 / z, z2 = z * z;
-    const T J00 = fx * iz, J02 = -fx * x / z2, J11 = fy * iz, J12 = -fy * y / z2;
+    const T iz2 = (T)1 / z2;  // (fp32: the quotients below multiply by it; fp64 divides)
+    const T J00 = fx * iz, J02 = cdiv(-fx * x, z2, iz2), J11 = fy * iz, J12 = cdiv(-fy * y, z2, iz2);
     T S2[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) S2[k] = t_exp<T>((T)2 * (T)lsp[k]);
@@ -1356,11 +1357,13 @@ __device__ __forceinline__ void chain_row(const ss_model& m, const ss_camera& ca
         for (int k = 0; k < 3; ++k) G3[i][k] = tm[i][0] * Rc[k][0] + tm[i][1] * Rc[k][1] + tm[i][2] * Rc[k][2];
     const T gm0 = g[4], gm1 = g[5];
     const T z3 = z2 * z;
+    const T iz3 = (T)1 / z3;
+    const T fxz2 = cdiv(-fx, z2, iz2), fyz2 = cdiv(-fy, z2, iz2);
     T gmc[3];
-    gmc[0] = J00 * gm0 + gJ0[2] * (-fx / z2);
-    gmc[1] = J11 * gm1 + gJ1[2] * (-fy / z2);
-    gmc[2] = J02 * gm0 + J12 * gm1 + gJ0[0] * (-fx / z2) + gJ1[1] * (-fy / z2) + gJ0[2] * (2 * fx * x / z3) +
-             gJ1[2] * (2 * fy * y / z3);
+    gmc[0] = J00 * gm0 + gJ0[2] * fxz2;
+    gmc[1] = J11 * gm1 + gJ1[2] * fyz2;
+    gmc[2] = J02 * gm0 + J12 * gm1 + gJ0[0] * fxz2 + gJ1[1] * fyz2 + gJ0[2] * cdiv(2 * fx * x, z3, iz3) +
+             gJ1[2] * cdiv(2 * fy * y, z3, iz3);
     T gmean[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) gmean[i] = Rc[i][0] * gmc[0] + Rc[i][1] * gmc[1] + Rc[i][2] * gmc[2];
