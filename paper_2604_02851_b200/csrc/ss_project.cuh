@@ -240,10 +240,19 @@ template <int DEG, typename T, typename PT>
 __device__ __forceinline__ void ss_shade_v(const ss_light& L, const PT* ls, const PT* shv, PT visf,
                                            const T d[3], const T Rq[3][3], Shade<DEG, T>& S) {
     constexpr int B = ss_sh_bases(DEG);
-    S.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    S.vdir[0] = d[0] / S.dist;
-    S.vdir[1] = d[1] / S.dist;
-    S.vdir[2] = d[2] / S.dist;
+    if constexpr (sizeof(T) == 4) {  // fp32 colour: one rsqrt for the view distance and direction
+        const T x = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+        const T inv = rsqrtf(x);
+        S.dist = x * inv;
+        S.vdir[0] = d[0] * inv;
+        S.vdir[1] = d[1] * inv;
+        S.vdir[2] = d[2] * inv;
+    } else {
+        S.dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        S.vdir[0] = d[0] / S.dist;
+        S.vdir[1] = d[1] / S.dist;
+        S.vdir[2] = d[2] / S.dist;
+    }
     const double l0 = ls[0], l1 = ls[1], l2 = ls[2];  // axis pick in fp64 for every T
     const double mn = fmin(l0, fmin(l1, l2)) + SS_AXIS_MARGIN;
     S.axis = (l0 <= mn) ? 0 : ((l1 <= mn) ? 1 : 2);
